@@ -1,0 +1,467 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 SPD-solve path (BASELINE.json north_star).
+
+Headline (N=1): CG iterations/s on the GP squared-exponential matrix
+n=32768, b=128 (BASELINE.json configs[1]), FP64, one B200.
+
+* ``value``   — iterations/s with A, rhs resident in HBM: one device-resident
+  ``hs_cg_solve`` with max_iters=K (eps=1e-300, recompute every 50 as the
+  reference default), timed with CUDA events on the library's stream
+  (torch's current stream is handed to the context). A = 4.31 GB >> L2.
+* ``e2e``     — the same metric through the reference-facing host-buffer
+  entry ``hs_solve_cg_host`` (== ``hsolve::solve_cg``): every call uploads
+  the packed matrix from pinned host memory, solves 50 iterations, and
+  downloads x. One e2e step = one such call.
+* ``roofline`` — the dominant kernel (symv_slab_kernel<128>): algorithmic
+  bytes per launch (packed tiles, T*b^2*8) / its mean launch time measured
+  with CUDA events around every SYMV launch of the timed solve; peak =
+  MEASURED_PEAKS.json hbm_gbs.
+* ``cpu_baseline`` — the compiled reference (oracle/_ref, kind "reference")
+  or the C restatement (kind "port") on this host's cores, bounded sample.
+* ``secondary`` — tiled Cholesky n=32768, b=512 (configs[2]) GFLOP/s
+  (n^3/3 / factor time) against cuBLAS DGEMM measured live in this run.
+
+``--impl reference`` times the reference CPU implementation (rank 0 only).
+Multi-GPU (torchrun, N>1): row-sharded CG over NCCL, strong scaling on the
+same n (override with --n).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+REASON_BITS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+    0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+    0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+    0x100: "display_clock_setting",
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return json.load(open(p))
+    return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                s, m = float(parts[0]), float(parts[1])
+                mask = int(parts[2], 16) if parts[2].startswith("0x") else int(parts[2])
+            except ValueError:
+                continue
+            sm.append(s)
+            mx.append(m)
+            for bit, name in REASON_BITS.items():
+                if mask & bit and name != "gpu_idle":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm
+
+
+def cpu_reference_cg(n: int, b: int, iters: int, warm: int) -> dict:
+    """Reference CG on the host cores: oracle/_ref when built, else the port."""
+    from oracle import Oracle, Reference
+    threads = len(os.sched_getaffinity(0))
+    if Reference.available():
+        ref, kind = Reference(), "reference"
+    else:
+        ref, kind = Oracle(), "port"
+    t0 = time.time()
+    a = ref.generate_spd(n, b, seed=42)
+    rhs = ref.generate_rhs(n, b, seed=42)
+    gen_s = time.time() - t0
+    if warm > 0:
+        (ref.solve_cg(n, b, a, rhs, eps=1e-300, max_iters=warm, workers=threads, trace=False)
+         if kind == "reference" else
+         ref.solve_cg(n, b, a, rhs, eps=1e-300, max_iters=warm, threads=threads, trace=False))
+    t0 = time.time()
+    if kind == "reference":
+        r = ref.solve_cg(n, b, a, rhs, eps=1e-300, max_iters=iters, workers=threads, trace=False)
+        wall = r["wall_ms"] / 1e3
+    else:
+        r = ref.solve_cg(n, b, a, rhs, eps=1e-300, max_iters=iters, threads=threads, trace=False)
+        wall = time.time() - t0  # includes the exit residual matvec
+    del a
+    return {"value": r["iterations"] / wall, "unit": "iters/s", "cores": threads,
+            "kind": kind,
+            "sample": f"{r['iterations']} CG iterations (after {warm} warm-up) at n={n}, "
+                      f"b={b}, fraction=0, workers_a={threads}; matrix generation "
+                      f"{gen_s:.1f} s untimed"}
+
+
+def cpu_reference_cholesky(n: int, b: int) -> dict:
+    from oracle import Oracle, Reference
+    threads = len(os.sched_getaffinity(0))
+    if Reference.available():
+        ref, kind = Reference(), "reference"
+    else:
+        ref, kind = Oracle(), "port"
+    a = ref.generate_spd(n, b, seed=42)
+    t0 = time.time()
+    if kind == "reference":
+        r = ref.factorize(n, b, a, workers=threads)
+        sec = r["factor_ms"] / 1e3
+    else:
+        ref.factorize(n, b, a, threads=threads)
+        sec = time.time() - t0
+    return {"value": n ** 3 / 3 / sec / 1e9, "unit": "GFLOP/s", "cores": threads,
+            "kind": kind, "sample": f"factorize n={n}, b={b}, workers_a={threads}"}
+
+
+def run_reference_arm(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    iters = max(1, min(args.steps, args.ref_iters))
+    warm = min(args.warmup, 3)
+    cb = cpu_reference_cg(args.n, args.b, iters, warm)
+    line = {
+        "impl": "reference", "metric": "cg_iters_per_s", "value": cb["value"],
+        "unit": "iters/s", "n_gpus": args.gpus, "steps": iters, "warmup": warm,
+        "ms_per_step": 1e3 / cb["value"], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "CG on GP squared-exponential SPD matrix (configs[1])",
+                   "n": args.n, "b": args.b, "seed": 42, "recompute_interval": 50,
+                   "device": "host CPU (reference hsolve, homogeneous executor A)"},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": cb["value"], "unit": "iters/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def dgemm_peak(torch) -> float:
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn_like(a)
+    c = torch.empty_like(a)
+    for _ in range(2):
+        torch.matmul(a, b, out=c)
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(3):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        torch.matmul(a, b, out=c)
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e))
+    del a, b, c
+    torch.cuda.empty_cache()
+    return 2 * n ** 3 / (best * 1e-3) / 1e12
+
+
+def cholesky_secondary(hs, H, rt, torch, args, peak_tf: float) -> dict:
+    n, b = args.chol_n, args.chol_b
+    m = hs.generate_spd_device(rt, n, b, seed=42)
+    work = hs.DeviceMatrix(rt, n, b)
+    nbytes = m.packed_len * 8
+    times = []
+    launches0 = rt.kernel_launches()
+    for rep in range(1 + args.chol_reps):
+        work.copy_from(m)  # fresh input each repetition (device copy, untimed)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        H.potrf_device(rt, work)
+        e.record()
+        e.synchronize()
+        if rep > 0:
+            times.append(s.elapsed_time(e))
+    launches = (rt.kernel_launches() - launches0) // (1 + args.chol_reps)
+    ms = statistics.median(times)
+    gflops = n ** 3 / 3 / (ms * 1e-3) / 1e9
+    # solve (substitutions) once, for the record
+    rhs = torch.from_numpy(hs.generate_rhs(n, b, 42).values).cuda()
+    x = torch.empty_like(rhs)
+    torch.cuda.synchronize()
+    t0 = time.time()
+    x.copy_(rhs)
+    H.trsv_device(rt, work, x.data_ptr(), upper=False)
+    H.trsv_device(rt, work, x.data_ptr(), upper=True)
+    torch.cuda.synchronize()
+    solve_ms = (time.time() - t0) * 1e3
+    res = H.true_residual_device(rt, m, x.data_ptr(), rhs.data_ptr())
+    rel = res / float(torch.linalg.vector_norm(rhs[:n]))
+    out = {"metric": "cholesky_gflops", "value": gflops, "unit": "GFLOP/s",
+           "ms_per_factor": ms, "solve_ms": solve_ms, "relative_residual": rel,
+           "config": {"workload": "tiled Cholesky + substitutions (configs[2])", "n": n,
+                      "b": b, "flops": "n^3/3"},
+           "gpu_launches_per_factor": int(launches),
+           "roofline": {"bound": "tensor", "achieved": gflops / 1e3, "peak": peak_tf,
+                        "unit": "TFLOP/s", "frac": gflops / 1e3 / peak_tf,
+                        "peak_source": "cuBLAS DGEMM 8192^3 measured live in this run "
+                                       "(MEASURED_PEAKS.json has no FP64 entry)"}}
+    work.free()
+    m.free()
+    return out
+
+
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    import paper_2605_13209_b200 as hs
+    from paper_2605_13209_b200 import hsolve as H
+
+    stream = torch.cuda.current_stream().cuda_stream
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(hs.Runtime.nccl_unique_id()),
+                                       dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        rt = hs.Runtime.distributed(local, rank, world, bytes(idt.cpu().tolist()),
+                                    stream=stream)
+    else:
+        rt = hs.Runtime(device=local, stream=stream)
+
+    n, b = args.n, args.b
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
+
+    # --- inputs resident in HBM (each rank assembles its own block rows) ---
+    t0 = time.time()
+    m = hs.generate_spd_device(rt, n, b, seed=42)
+    torch.cuda.synchronize()
+    gen_s = time.time() - t0
+    rhs_np = hs.generate_rhs(n, b, 42).values
+    d_rhs = torch.from_numpy(rhs_np).cuda()
+    d_x = torch.zeros_like(d_rhs)
+    N = (n + b - 1) // b
+    T = N * (N + 1) // 2
+    packed_bytes = T * b * b * 8
+    local_bytes = (m.row_hi * (m.row_hi + 1) // 2 - m.row_lo * (m.row_lo + 1) // 2) * b * b * 8
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up: W iterations
+    cfgw = hs.SolverConfig(block_size=b, eps=1e-300, max_iters=max(args.warmup, 1))
+    hs.solve_cg_device(rt, m, d_rhs.data_ptr(), d_x.data_ptr(), cfgw)
+
+    # timed: exactly K iterations in one solve
+    cfg = hs.SolverConfig(block_size=b, eps=1e-300, max_iters=args.steps,
+                          recompute_interval=50)
+    rt.prof_enable(True)
+    rt.prof_reset()
+    launches0 = rt.kernel_launches()
+    with ClockSampler(local) as clocks:
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        st = hs.solve_cg_device(rt, m, d_rhs.data_ptr(), d_x.data_ptr(), cfg)
+        ev1.record()
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = rt.kernel_launches() - launches0
+    n_symv, symv_ms = rt.prof_symv()
+    rt.prof_enable(False)
+    assert st.iterations == args.steps, (st.iterations, args.steps)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        s2 = torch.tensor([symv_ms / max(n_symv, 1)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(s2, op=dist.ReduceOp.MAX)
+        symv_avg = float(s2.item())
+    else:
+        symv_avg = symv_ms / max(n_symv, 1)
+    value = args.steps / (ms * 1e-3)
+
+    # dominant kernel roofline (per rank: local tiles per launch)
+    achieved = local_bytes / (symv_avg * 1e-3) / 1e9
+    traffic = None
+    prof_json = os.path.join(ROOT, "profiles", "r01_symv_ncu.json")
+    if os.path.exists(prof_json):
+        try:
+            pj = json.load(open(prof_json))
+            if pj.get("n") == n and pj.get("b") == b:
+                traffic = pj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": traffic,
+                "kernel": f"symv_slab_kernel<{b}>", "launches": n_symv,
+                "algorithmic_bytes_per_launch": local_bytes, "peak_source": hbm_src}
+
+    line = {
+        "metric": "cg_iters_per_s", "value": value, "unit": "iters/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic GP squared-exponential matrix (generate_spd seed 42, median "
+                "length-scale rule) assembled on the device",
+        "config": {"workload": "CG on GP SE matrix, n=%d, b=%d (BASELINE.json configs[1])"
+                               % (n, b), "n": n, "b": b, "seed": 42,
+                   "recompute_interval": 50, "eps": "1e-300 (fixed iteration count)",
+                   "parallelism": f"row-sharded x{world}" if world > 1 else "single GPU",
+                   "l2": f"inputs larger than L2 (packed A = {packed_bytes / 1e9:.2f} GB)",
+                   "matrix_assembly_s": round(gen_s, 3)},
+        "gpu_launches": int(launches),
+        "roofline": roofline,
+    }
+
+    # ---- e2e through the host-buffer C-ABI entry (rank 0 / single GPU) ----
+    if world == 1 and not args.no_e2e:
+        host = torch.empty(packed_bytes // 8, dtype=torch.float64, pin_memory=True)
+        m.download(host.numpy())
+        rhs_pin = torch.from_numpy(rhs_np.copy()).pin_memory()
+        x_pin = torch.zeros_like(rhs_pin).pin_memory()
+        import ctypes as C
+        cfge = hs.SolverConfig(block_size=b, eps=1e-300, max_iters=args.e2e_iters)
+        p = H._cg_params(cfge)
+        from paper_2605_13209_b200._lib import CgStats
+        ste = CgStats()
+        # one untimed call (allocator / plan warm-up), then timed calls
+        H._check(rt._L.hs_solve_cg_host(rt.ctx, n, b, C.c_void_p(host.data_ptr()),
+                                        C.c_void_p(rhs_pin.data_ptr()), C.byref(p),
+                                        C.c_void_p(x_pin.data_ptr()), C.byref(ste), None))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        its = 0
+        for _ in range(args.e2e_reps):
+            H._check(rt._L.hs_solve_cg_host(rt.ctx, n, b, C.c_void_p(host.data_ptr()),
+                                            C.c_void_p(rhs_pin.data_ptr()), C.byref(p),
+                                            C.c_void_p(x_pin.data_ptr()), C.byref(ste),
+                                            None))
+            its += ste.iterations
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        line["e2e"] = {"value": its / e2e_s, "unit": "iters/s",
+                       "h2d_bytes_per_step": packed_bytes + rhs_np.nbytes,
+                       "d2h_bytes_per_step": rhs_np.nbytes,
+                       "step": f"one hs_solve_cg_host call ({args.e2e_iters} iterations) "
+                               "from pinned host buffers; host wall clock",
+                       "transfer_ms_per_step": ste.transfer_ms}
+        del host
+    else:
+        line["e2e"] = None
+
+    clk = clocks.summary()
+    line["clocks"] = clk
+
+    if rank == 0 and world == 1 and not args.no_secondary:
+        m.free()
+        del d_rhs, d_x
+        torch.cuda.empty_cache()
+        peak_tf = dgemm_peak(torch)
+        try:
+            line["secondary"] = cholesky_secondary(hs, H, rt, torch, args, peak_tf)
+        except Exception as e:  # keep the headline line even if this fails
+            line["secondary"] = {"error": repr(e)}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_reference_cg(n, b, args.cpu_iters, 1)
+            if not args.no_secondary:
+                line["secondary"]["cpu_baseline"] = cpu_reference_cholesky(
+                    args.cpu_chol_n, args.chol_b)
+        except Exception as e:
+            line["cpu_baseline"] = {"error": repr(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    rt.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--b", type=int, default=128)
+    ap.add_argument("--chol-n", type=int, default=32768)
+    ap.add_argument("--chol-b", type=int, default=512)
+    ap.add_argument("--chol-reps", type=int, default=2)
+    ap.add_argument("--cpu-chol-n", type=int, default=4096)
+    ap.add_argument("--cpu-iters", type=int, default=20)
+    ap.add_argument("--ref-iters", type=int, default=50)
+    ap.add_argument("--e2e-iters", type=int, default=50)
+    ap.add_argument("--e2e-reps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warning: --warmup < 3 violates the timing rules; using 3")
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

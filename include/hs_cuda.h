@@ -1,0 +1,216 @@
+/*
+ * hs_cuda.h — C ABI of libhsolve_cuda.so, the B200-native (sm_100a) SPD-solve
+ * path: GP squared-exponential assembly, blocked CG, tiled right-looking
+ * Cholesky with triangular solves.
+ *
+ * This is the drop-in boundary for the reference `hsolve` solver API (paths
+ * relative to /root/reference/proj). The reference has no FFI; its boundary
+ * is the C++ header API called by bench.cpp:108-126 and the tests. Every
+ * entry point below names the reference interface it replaces. The C++ shim
+ * in include/hsolve/ (libhsolve_b200.so) re-exposes the reference signatures
+ * verbatim on top of this ABI; Python reaches it through ctypes
+ * (paper_2605_13209_b200/_lib.py).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no exceptions cross the ABI.
+ *  - Every call returns an hs_status: 0 = ok, else 1 + hsolve::ErrorKind
+ *    (errors.hpp:10-21) or HS_ERR_CUDA for device/runtime failures.
+ *    hs_last_error() gives the message, hs_last_error_payload() the payload
+ *    (not_spd: block row + pivot, errors.hpp:45-63; numerical: iteration).
+ *  - "host" pointers are ordinary (pageable or pinned) host memory; "d_"
+ *    pointers are device memory on the context's GPU.
+ *  - Layouts are the reference's: packed lower-triangular b x b tiles,
+ *    tile (i, j) at (i(i+1)/2 + j) * b * b, row-major inside a tile
+ *    (blocked_matrix.hpp:10-61); vectors are N*b doubles with a zero tail
+ *    (blocked_matrix.hpp:63-89). N = ceil(n / b).
+ *  - Calls are blocking with respect to the host (the reference's barrier()
+ *    semantics, executor.hpp:160-162) unless documented otherwise; work is
+ *    ordered on the context's stream.
+ */
+#ifndef HS_CUDA_H
+#define HS_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int hs_status;
+
+enum {
+  HS_OK = 0,
+  HS_ERR_CONFIG = 1,         /* ErrorKind::config         */
+  HS_ERR_NOT_SPD = 2,        /* ErrorKind::not_spd        */
+  HS_ERR_SINGULAR_BLOCK = 3, /* ErrorKind::singular_block */
+  HS_ERR_NUMERICAL = 4,      /* ErrorKind::numerical      */
+  HS_ERR_NOT_CONVERGED = 5,  /* status only; never returned by a solve */
+  HS_ERR_CUDA = 100          /* device / runtime failure (no reference kind) */
+};
+
+typedef struct hs_ctx hs_ctx;       /* one GPU + stream (+ NCCL comm) */
+typedef struct hs_matrix hs_matrix; /* device-resident packed tiles   */
+
+/* ---- errors ------------------------------------------------------------ */
+const char* hs_last_error(void);
+void hs_last_error_payload(int64_t* a, int64_t* b);
+const char* hs_error_kind_name(hs_status s); /* transfer_ledger.cpp:28-42 */
+
+/* ---- context (replaces hsolve::Runtime, executor.hpp:128-221) ---------- */
+/* stream: a cudaStream_t to order work on (NULL = the library creates one). */
+hs_status hs_ctx_create(int device, void* stream, hs_ctx** out);
+/* Multi-GPU: one process per GPU; nccl_id = 128 bytes from
+ * hs_nccl_unique_id() on rank 0, distributed by the caller. */
+hs_status hs_nccl_unique_id(void* id128);
+hs_status hs_ctx_create_nccl(int device, void* stream, int rank, int world,
+                             const void* id128, hs_ctx** out);
+void hs_ctx_destroy(hs_ctx* ctx);
+int hs_ctx_rank(const hs_ctx* ctx);
+int hs_ctx_world(const hs_ctx* ctx);
+void* hs_ctx_stream(const hs_ctx* ctx);
+/* Number of kernels this library launched on the context so far. */
+uint64_t hs_ctx_kernel_launches(const hs_ctx* ctx);
+
+/* ---- host-side generators (genmat.cpp:16-112, 156-162; exact) ---------- */
+uint64_t hs_rng_at(uint64_t key, uint64_t counter);
+double hs_rng_uniform_pm1(uint64_t key, uint64_t counter);
+hs_status hs_generate_inputs(size_t n, size_t dim, uint64_t seed,
+                             double* out /* n*dim */);
+double hs_median_pairwise_distance(const double* points, size_t n, size_t dim);
+hs_status hs_generate_rhs(size_t n, size_t b, uint64_t seed,
+                          double* out /* N*b */);
+
+/* ---- work split (partition.cpp:11-74; host-only, no GPU needed) -------- */
+/* split_row = floor(f*N + 0.5)  (partition.hpp:20-22) */
+hs_status hs_partition_for_fraction(double fraction, size_t block_rows,
+                                    size_t* split_row);
+/* beta_j (partition.hpp:24-30) */
+hs_status hs_cholesky_border(double fraction, size_t column, size_t block_rows,
+                             size_t* beta);
+/* Multi-GPU row partition for CG: contiguous block-row ranges balanced by
+ * packed-tile count; bounds has world+1 entries (bounds[0]=0,
+ * bounds[world]=N). Generalises partition_for_fraction to G devices. */
+hs_status hs_partition_rows(size_t block_rows, int world, size_t* bounds);
+
+/* ---- device matrices (BlockedSPDMatrix storage, blocked_matrix.hpp) ---- */
+/* Allocates the tiles this rank owns (all tiles when world == 1), zeroed,
+ * with identity padding (blocked_matrix.cpp:17-24, 57-74). */
+hs_status hs_matrix_create(hs_ctx* ctx, size_t n, size_t b, hs_matrix** out);
+void hs_matrix_destroy(hs_matrix* m);
+hs_status hs_matrix_info(const hs_matrix* m, size_t* n, size_t* b,
+                         size_t* row_lo, size_t* row_hi);
+/* Full packed array on the host (N(N+1)/2*b*b doubles); a sharded matrix
+ * uploads/downloads only its own block rows of it. */
+hs_status hs_matrix_upload(hs_matrix* m, const double* host_packed);
+hs_status hs_matrix_download(const hs_matrix* m, double* host_packed);
+/* dst <- src (same shape and context), device to device. */
+hs_status hs_matrix_copy(hs_matrix* dst, const hs_matrix* src);
+/* Raw device pointer to the local packed tiles (for tests / interop). */
+double* hs_matrix_device_data(hs_matrix* m);
+
+/* ---- (1) GP squared-exponential assembly (genmat.cpp:114-154) ---------- */
+/* Device tile generation from host points (n*dim). Element (p,q):
+ * p,q >= n -> identity padding; p == q -> sigma_f2 + sigma_n2;
+ * else sigma_f2 * exp(-||x_p - x_q||^2 * inv2l2). */
+hs_status hs_assemble_se(hs_matrix* m, const double* points, size_t dim,
+                         double sigma_f2, double inv2l2, double sigma_n2);
+/* generate_spd (genmat.hpp:41-42) without the host matrix: points and the
+ * median length-scale rule on the host, tiles on the device. */
+hs_status hs_generate_spd(hs_matrix* m, double sigma_f2, double length_scale,
+                          double sigma_n2, size_t dim, uint64_t seed);
+
+/* ---- (2) conjugate gradient (cg_solver.hpp:48-49) ---------------------- */
+typedef struct {
+  double eps;                  /* SolverConfig::eps (solver_config.hpp:13) */
+  uint64_t max_iters;          /* SolverConfig::max_iters                   */
+  uint64_t recompute_interval; /* SolverConfig::recompute_interval          */
+  int record_trace;            /* SolverConfig::record_trace                */
+} hs_cg_params;
+
+typedef struct { /* CgStats (cg_solver.hpp:19-29) */
+  uint64_t iterations;
+  uint64_t recomputations;
+  int converged;
+  double u0;
+  double true_residual; /* ||rhs - A x||_2 at exit */
+  double wall_ms;       /* whole call                          */
+  double compute_ms;    /* wall minus host<->device transfers  */
+  double transfer_ms;   /* H2D/D2H inside the call             */
+  int64_t error_iteration;
+} hs_cg_stats;
+
+/* Device-resident solve: d_rhs, d_x are N*b device vectors (the rank's full
+ * vectors). trace: 3*max_iters host doubles (u, alpha, beta) or NULL. */
+hs_status hs_cg_solve(hs_ctx* ctx, const hs_matrix* a, const double* d_rhs,
+                      const hs_cg_params* p, double* d_x, hs_cg_stats* stats,
+                      double* trace);
+/* Drop-in for solve_cg with HOST buffers: uploads the packed matrix and rhs,
+ * solves, downloads x (all inside the call, timed as transfer_ms). */
+hs_status hs_solve_cg_host(hs_ctx* ctx, size_t n, size_t b,
+                           const double* a_packed, const double* rhs,
+                           const hs_cg_params* p, double* x,
+                           hs_cg_stats* stats, double* trace);
+
+/* t = A x (symv_range over all rows, block_kernels.hpp:34-38). */
+hs_status hs_symv(hs_ctx* ctx, const hs_matrix* a, const double* d_x,
+                  double* d_y);
+/* ||rhs - A x||_2 (the solvers' exit diagnostic). */
+hs_status hs_true_residual(hs_ctx* ctx, const hs_matrix* a, const double* d_x,
+                           const double* d_rhs, double* out);
+
+/* ---- (3) Cholesky (cholesky_solver.hpp:44-58) -------------------------- */
+typedef struct {
+  double factor_ms;
+  double solve_ms;
+  double wall_ms;
+  double compute_ms;
+  double transfer_ms;
+  double true_residual;
+} hs_chol_stats;
+
+/* In-place factorization: the lower tiles of a hold L (diag-tile upper
+ * halves stale). HS_ERR_NOT_SPD with payload (column, pivot);
+ * HS_ERR_NUMERICAL on a non-finite factor (cholesky_solver.cpp:222-238). */
+hs_status hs_potrf(hs_ctx* ctx, hs_matrix* a, hs_chol_stats* stats);
+/* In-place L y = v (forward_substitute) and L^T x = y (back_substitute) on a
+ * device vector; HS_ERR_SINGULAR_BLOCK on a zero / NaN diagonal. */
+hs_status hs_trsv_lower(hs_ctx* ctx, const hs_matrix* l, double* d_v);
+hs_status hs_trsv_upper(hs_ctx* ctx, const hs_matrix* l, double* d_v);
+/* factorize + substitutions, device resident (a is destroyed, holds L).
+ * true_residual needs the original matrix: pass it as a_orig or NULL. */
+hs_status hs_solve_spd(hs_ctx* ctx, hs_matrix* a, const double* d_rhs,
+                       double* d_x, const hs_matrix* a_orig,
+                       hs_chol_stats* stats);
+/* Drop-ins with HOST buffers (factorize / solve_spd / substitutions). */
+hs_status hs_factorize_host(hs_ctx* ctx, size_t n, size_t b, double* a_packed,
+                            hs_chol_stats* stats);
+hs_status hs_solve_spd_host(hs_ctx* ctx, size_t n, size_t b, double* a_packed,
+                            const double* rhs, double* x,
+                            hs_chol_stats* stats);
+hs_status hs_forward_substitute_host(hs_ctx* ctx, size_t n, size_t b,
+                                     const double* l_packed, const double* rhs,
+                                     double* y);
+hs_status hs_back_substitute_host(hs_ctx* ctx, size_t n, size_t b,
+                                  const double* l_packed, const double* y,
+                                  double* x);
+
+/* ---- single-tile kernels (block_kernels.hpp:17-31), for parity tests --- */
+/* Batched over `count` independent b x b tiles in device memory. */
+hs_status hs_potf_tiles(hs_ctx* ctx, double* d_tiles, size_t b, size_t count,
+                        int64_t* first_bad_pivot);
+hs_status hs_gemm_update_tiles(hs_ctx* ctx, double* d_c, const double* d_p,
+                               const double* d_q, size_t b, size_t count,
+                               int lower_only);
+
+/* ---- profiling hooks (bench.py roofline) ------------------------------- */
+/* When enabled, the CG driver brackets every SYMV launch with CUDA events
+ * on the context stream; hs_prof_symv returns (launches, total ms). */
+void hs_prof_enable(hs_ctx* ctx, int on);
+void hs_prof_symv(hs_ctx* ctx, uint64_t* launches, double* total_ms);
+void hs_prof_reset(hs_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HS_CUDA_H */

@@ -1,0 +1,92 @@
+"""Build the in-tree native libraries (sm_100a only).
+
+* ``libhsolve_cuda.so`` — CUDA kernels + the C ABI (include/hs_cuda.h),
+  nvcc ``-gencode arch=compute_100a,code=sm_100a``.
+* ``libhsolve_b200.so`` — the C++ host shim re-exposing the reference
+  ``hsolve`` API (include/hsolve/*.hpp) on top of the C ABI.
+
+Both land next to this file so they travel with the repo snapshot to the GPU
+box. Rebuilds only when a source is newer than the library.
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+HOST = os.path.join(PKG, "host")
+INC = os.path.join(ROOT, "include")
+CUDA_LIB = os.path.join(PKG, "libhsolve_cuda.so")
+HOST_LIB = os.path.join(PKG, "libhsolve_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
+    "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills",
+]
+
+
+def _stale(target: str, sources: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def _run(cmd: list[str]) -> None:
+    print("+", " ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+
+
+def build_cuda(force: bool = False, verbose_ptxas: bool = False) -> str:
+    cus = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    deps = cus + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(
+        os.path.join(CSRC, "*.cuh")) + [os.path.join(INC, "hs_cuda.h")]
+    if not force and not _stale(CUDA_LIB, deps):
+        return CUDA_LIB
+    objdir = os.path.join(ROOT, "build", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    objs = []
+    procs = []
+    for cu in cus:
+        obj = os.path.join(objdir, os.path.basename(cu) + ".o")
+        objs.append(obj)
+        cmd = [NVCC, *NVCC_FLAGS, "-I", INC, "-I", CSRC, "-c", cu, "-o", obj]
+        if verbose_ptxas:
+            cmd += ["-Xptxas", "-v"]
+        print("+", " ".join(cmd), flush=True)
+        procs.append(subprocess.Popen(cmd))
+    bad = [p for p in procs if p.wait() != 0]
+    if bad:
+        raise RuntimeError("nvcc failed")
+    _run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+          "-Xcompiler", "-fPIC", *objs, "-o", CUDA_LIB, "-ldl"])
+    return CUDA_LIB
+
+
+def build_host(force: bool = False) -> str:
+    srcs = sorted(glob.glob(os.path.join(HOST, "*.cpp")))
+    if not srcs:
+        return ""
+    deps = srcs + glob.glob(os.path.join(INC, "hsolve", "*.hpp")) + [
+        os.path.join(INC, "hs_cuda.h"), CUDA_LIB]
+    if not force and not _stale(HOST_LIB, deps):
+        return HOST_LIB
+    cxx = os.environ.get("CXX", "g++")
+    _run([cxx, "-std=c++20", "-O2", "-fPIC", "-shared", "-I", INC, *srcs,
+          "-o", HOST_LIB, "-L", PKG, "-lhsolve_cuda", "-Wl,-rpath,$ORIGIN"])
+    return HOST_LIB
+
+
+def build(force: bool = False) -> None:
+    build_cuda(force)
+    build_host(force)
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv)

@@ -1,0 +1,1090 @@
+// Blocked conjugate gradient on B200 (reference cg_solver.cpp:223-368).
+//
+// Hot kernel: packed-symmetric SYMV that streams every stored tile of A
+// exactly once per matvec. Persistent CTAs (one per SM) own contiguous
+// ranges of 32-KB "slabs" (row strips of the row-major tiles) in packed
+// order. A producer warp moves slabs + the two s-vector segments they need
+// into a 5-stage shared-memory ring with the TMA bulk-copy engine
+// (cp.async.bulk + mbarrier complete_tx); 8 consumer warps read each element
+// once from shared memory and use it twice: for the row sum (A_ij s_j -> t_i)
+// and for the transposed column sum (A_ij^T s_i -> t_j). Row sums are
+// accumulated per CTA per block row, column sums per CTA per tile, into
+// fixed segment slots; a finalize kernel adds the slots in a fixed order,
+// so results are deterministic (no atomics on values). Diagonal tiles read
+// only their lower triangle (block_kernels.cpp:76-85 semantics).
+//
+// Roofline: HBM-bound. Algorithmic bytes per matvec = packed tile bytes
+// (T * b^2 * 8); the partial slots add ~2/b of that (0.8 % at b = 128).
+#include <math.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <vector>
+
+#include "hs_internal.h"
+
+namespace hs {
+
+void comm_allgather(hs_ctx* c, const double* send, double* recv, size_t count);
+void comm_reduce_scatter(hs_ctx* c, const double* send, double* recv,
+                         size_t count);
+
+// ---------------------------------------------------------------------------
+// Fast SYMV for b in {64, 128, 256, 512}
+
+template <int B>
+struct SymvCfg {
+  static constexpr int SLAB_BYTES = 32768;
+  static constexpr int RS = 4096 / B;    // tile rows per slab
+  static constexpr int SPT = B / RS;     // slabs per tile
+  static constexpr int TPR = B / 8;      // consumer threads per tile row
+  static constexpr int RPP = 256 / TPR;  // row lanes (rows per pass)
+  static constexpr int W = TPR < 32 ? TPR : 32;  // lanes of a row in a warp
+  static constexpr int H = TPR / W;      // warps sharing a row
+  static constexpr int NSTAGE = B == 512 ? 4 : 5;
+  static constexpr int STAGE_BYTES = SLAB_BYTES + B * 8 + RS * 8;
+  static constexpr int COLRED_BYTES = RPP * B * 8;
+  static constexpr int YROW_BYTES = H * B * 8;
+  static constexpr int SMEM = NSTAGE * STAGE_BYTES + 2 * COLRED_BYTES +
+                              2 * YROW_BYTES + 2 * NSTAGE * 8;
+  static_assert(RS == 2 * RPP, "two rows per consumer thread per slab");
+  static_assert(STAGE_BYTES % 16 == 0, "bulk copy alignment");
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+};
+
+struct SymvArgs {
+  const double* a;        // local tiles
+  const double* s;        // input vector (padded layout)
+  const int64_t* row_off; // [N] element offset of block row i in s / out
+  int64_t tile_lo;        // global index of the first local tile
+  const int64_t* cta_slab;
+  const int64_t* cta_rseg;
+  const int64_t* cta_cseg;
+  double* rowpart;
+  double* colpart;
+  const int32_t* done;    // CG early-exit flag (nullable)
+};
+
+template <int B>
+__global__ void __launch_bounds__(288, 1) symv_slab_kernel(SymvArgs args) {
+  using Cfg = SymvCfg<B>;
+  constexpr int RS = Cfg::RS, SPT = Cfg::SPT, TPR = Cfg::TPR, RPP = Cfg::RPP;
+  constexpr int W = Cfg::W, NS = Cfg::NSTAGE;
+  if (args.done && *args.done) return;
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* stages = smem;
+  double* colred = reinterpret_cast<double*>(smem + NS * Cfg::STAGE_BYTES);
+  double* yrow = colred + 2 * RPP * B;  // [2][H][B]
+  uint64_t* full = reinterpret_cast<uint64_t*>(yrow + 2 * Cfg::H * B);
+  uint64_t* empty = full + NS;
+
+  const int tid = threadIdx.x;
+  const int64_t g0 = args.cta_slab[blockIdx.x];
+  const int64_t g1 = args.cta_slab[blockIdx.x + 1];
+  if (g0 >= g1) return;
+
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    fence_mbar_init();
+  }
+  for (int k = tid; k < 2 * Cfg::H * B; k += blockDim.x) yrow[k] = 0.0;
+  __syncthreads();
+
+  const int64_t t_first = g0 / SPT;
+  const int64_t i_first = tile_row(t_first);
+
+  if (tid >= 256) {
+    // ---------------- producer warp ----------------
+    if (tid == 256) {
+      int64_t t = t_first, i = i_first, j = t_first - tri(i_first, 0);
+      int q = (int)(g0 - t_first * SPT);
+      for (int64_t g = g0; g < g1; ++g) {
+        const int64_t k = g - g0;
+        const int st = (int)(k % NS);
+        if (k >= NS) mbar_wait(&empty[st], (uint32_t)(((k / NS) - 1) & 1));
+        unsigned char* buf = stages + st * Cfg::STAGE_BYTES;
+        mbar_arrive_expect_tx(&full[st], Cfg::STAGE_BYTES);
+        const double* src =
+            args.a + ((t - args.tile_lo) * B + (int64_t)q * RS) * B;
+        bulk_g2s(buf, src, Cfg::SLAB_BYTES, &full[st]);
+        bulk_g2s(buf + Cfg::SLAB_BYTES, args.s + args.row_off[j], B * 8,
+                 &full[st]);
+        bulk_g2s(buf + Cfg::SLAB_BYTES + B * 8,
+                 args.s + args.row_off[i] + q * RS, RS * 8, &full[st]);
+        if (++q == SPT) {
+          q = 0;
+          ++t;
+          if (++j > i) {
+            ++i;
+            j = 0;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  const int lane = tid & 31;
+  const int cl = tid % TPR;  // column lane: columns 2cl + 2TPR*m (+1)
+  const int rl = tid / TPR;  // row lane: slab rows 2rl, 2rl+1
+  const int h = cl / W;      // row-sharing warp index (B = 512)
+  const int64_t rseg0 = args.cta_rseg[blockIdx.x];
+  const int64_t cseg0 = args.cta_cseg[blockIdx.x];
+
+  double cacc[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) cacc[m] = 0.0;
+
+  int64_t t = t_first, i = i_first, j = t_first - tri(i_first, 0);
+  int q = (int)(g0 - t_first * SPT);
+  int tpar = 0, rpar = 0;  // parity of tiles / block rows flushed
+
+  for (int64_t g = g0; g < g1; ++g) {
+    const int64_t k = g - g0;
+    const int st = (int)(k % NS);
+    mbar_wait(&full[st], (uint32_t)((k / NS) & 1));
+    const unsigned char* buf = stages + st * Cfg::STAGE_BYTES;
+    const double2* A2 = reinterpret_cast<const double2*>(buf);
+    const double2* sj2 =
+        reinterpret_cast<const double2*>(buf + Cfg::SLAB_BYTES);
+    const double* si =
+        reinterpret_cast<const double*>(buf + Cfg::SLAB_BYTES + B * 8);
+
+    double2 a[2][4], sj[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) sj[m] = sj2[cl + TPR * m];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        a[r][m] = A2[(2 * rl + r) * (B / 2) + cl + TPR * m];
+    const double si0 = si[2 * rl], si1 = si[2 * rl + 1];
+
+    double rs[2] = {0.0, 0.0};
+    if (i != j) {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          rs[r] = fma(a[r][m].x, sj[m].x, rs[r]);
+          rs[r] = fma(a[r][m].y, sj[m].y, rs[r]);
+        }
+        cacc[2 * m] = fma(a[0][m].x, si0, cacc[2 * m]);
+        cacc[2 * m] = fma(a[1][m].x, si1, cacc[2 * m]);
+        cacc[2 * m + 1] = fma(a[0][m].y, si0, cacc[2 * m + 1]);
+        cacc[2 * m + 1] = fma(a[1][m].y, si1, cacc[2 * m + 1]);
+      }
+    } else {
+      // diagonal tile: lower triangle only (c <= r for rows, c < r for cols)
+      const int rbase = q * RS + 2 * rl;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int c0 = 2 * cl + 2 * TPR * m;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int rr = rbase + r;
+          const double ax = c0 <= rr ? a[r][m].x : 0.0;
+          const double ay = c0 + 1 <= rr ? a[r][m].y : 0.0;
+          rs[r] = fma(ax, sj[m].x, rs[r]);
+          rs[r] = fma(ay, sj[m].y, rs[r]);
+          const double sir = r ? si1 : si0;
+          cacc[2 * m] = fma(c0 < rr ? a[r][m].x : 0.0, sir, cacc[2 * m]);
+          cacc[2 * m + 1] =
+              fma(c0 + 1 < rr ? a[r][m].y : 0.0, sir, cacc[2 * m + 1]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+
+    // row sums: reduce the 2 rows over the W lanes of this warp (transposed
+    // first step), then the owning lane accumulates into yrow[rpar][h][row].
+    {
+      const bool hi = (cl & (W / 2)) != 0;
+      const double send = hi ? rs[0] : rs[1];
+      double v = (hi ? rs[1] : rs[0]) + __shfl_xor_sync(0xffffffffu, send, W / 2);
+#pragma unroll
+      for (int off = W / 4; off >= 1; off >>= 1)
+        v += __shfl_xor_sync(0xffffffffu, v, off);
+      if ((cl & (W / 2 - 1)) == 0) {
+        const int row = q * RS + 2 * rl + (hi ? 1 : 0);
+        yrow[(rpar * Cfg::H + h) * B + row] += v;
+      }
+    }
+
+    const bool tile_end = (q == SPT - 1) || (g + 1 == g1);
+    if (tile_end) {
+      double* cr = colred + tpar * RPP * B;
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        reinterpret_cast<double2*>(cr + rl * B)[cl + TPR * m] =
+            make_double2(cacc[2 * m], cacc[2 * m + 1]);
+      named_bar_sync(1, 256);
+      const int64_t cseg = cseg0 + (t - t_first);
+      for (int c = tid; c < B; c += 256) {
+        double acc = 0.0;
+#pragma unroll 4
+        for (int r = 0; r < RPP; ++r) acc += cr[r * B + c];
+        args.colpart[cseg * B + c] = acc;
+      }
+      const bool row_end = (j == i && q == SPT - 1) || (g + 1 == g1);
+      if (row_end) {
+        const int64_t rseg = rseg0 + (i - i_first);
+        double* yr = yrow + rpar * Cfg::H * B;
+        for (int c = tid; c < B; c += 256) {
+          double acc = yr[c];
+          yr[c] = 0.0;
+#pragma unroll
+          for (int hh = 1; hh < Cfg::H; ++hh) {
+            acc += yr[hh * B + c];
+            yr[hh * B + c] = 0.0;
+          }
+          args.rowpart[rseg * B + c] = acc;
+        }
+        rpar ^= 1;
+      }
+      tpar ^= 1;
+#pragma unroll
+      for (int m = 0; m < 8; ++m) cacc[m] = 0.0;
+    }
+    if (++q == SPT) {
+      q = 0;
+      ++t;
+      if (++j > i) {
+        ++i;
+        j = 0;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Finalize: out[row_off[j] + c] = sum of row segments of block row j + sum of
+// column segments of tiles (i, j), i >= j, in a fixed order. Optionally
+// fused with the per-row dot s_j . out_j and the CG alpha step.
+
+struct Scal;  // fwd
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  // deterministic fixed-shape tree over the CTA (blockDim multiple of 32)
+  for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < nw; ++k) s += red[k];
+  return s;  // valid in thread 0
+}
+
+// Reduce `count` per-CTA partials in fixed order into a double-double.
+__device__ Dd dd_reduce_parts(const double* parts, int count, Dd* red) {
+  Dd acc{0.0, 0.0};
+  for (int k = threadIdx.x; k < count; k += blockDim.x)
+    acc = dd_add(acc, parts[k]);
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w >= 1; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] = dd_add(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  return red[0];
+}
+
+enum ScalarStep : int { STEP_NONE = 0, STEP_INIT = 1, STEP_ALPHA = 2, STEP_BETA = 3 };
+
+struct StepArgs {
+  CgScalars* sc;
+  double* trace;       // device trace buffer (3 per iteration) or null
+  double eps;
+  Dd* dd_slots;        // [world] per-rank partials (multi-GPU) or null
+  int world;
+};
+
+// Single-thread scalar step on the combined dot value (cg_solver.cpp lines
+// 5, 8-10 and the start-up checks :243-249).
+__device__ void scalar_step(int step, double val, const StepArgs& sa) {
+  CgScalars* sc = sa.sc;
+  if (step == STEP_INIT) {
+    sc->u0 = val;
+    sc->u = val;
+    sc->iter = 0;
+    sc->recomputations = 0;
+    sc->status = HS_OK;
+    sc->err_iter = -1;
+    sc->alpha = sc->beta = 0.0;
+    if (!isfinite(val)) {
+      sc->status = HS_ERR_NUMERICAL;
+      sc->err_iter = 0;
+      sc->done = 1;
+      return;
+    }
+    sc->limit = sa.eps * sa.eps * val;
+    sc->done = (val <= sc->limit) ? 1 : 0;
+  } else if (step == STEP_ALPHA) {
+    const double alpha = sc->u / val;
+    sc->alpha = alpha;
+    if (!isfinite(alpha)) {
+      sc->status = HS_ERR_NUMERICAL;
+      sc->err_iter = sc->iter + 1;
+      sc->done = 1;
+    }
+  } else if (step == STEP_BETA) {
+    const double u = val;
+    if (!(u >= 0.0) || !isfinite(u)) {
+      sc->status = HS_ERR_NUMERICAL;
+      sc->err_iter = sc->iter + 1;
+      sc->done = 1;
+      return;
+    }
+    const double beta = u / sc->u;
+    sc->beta = beta;
+    sc->u = u;
+    const int64_t it = ++sc->iter;
+    if (sa.trace) {
+      sa.trace[3 * (it - 1) + 0] = u;
+      sa.trace[3 * (it - 1) + 1] = sc->alpha;
+      sa.trace[3 * (it - 1) + 2] = beta;
+    }
+    if (u <= sc->limit) sc->done = 1;
+  }
+}
+
+// Last-CTA epilogue shared by the dot-producing kernels: combine per-CTA
+// partials (fixed order); single rank -> apply the scalar step directly,
+// multi rank -> publish this rank's (hi, lo) for the all-gather.
+__device__ void dot_epilogue(double part, double* dpart, int step,
+                             const StepArgs& sa) {
+  __shared__ double red_d[32];
+  __shared__ Dd red_dd[256];
+  __shared__ bool last;
+  const double p = block_sum(part, red_d);
+  if (threadIdx.x == 0) {
+    dpart[blockIdx.x] = p;
+    __threadfence();
+    const unsigned prev = atomicAdd(&sa.sc->ticket, 1u);
+    last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const Dd tot = dd_reduce_parts(dpart, gridDim.x, red_dd);
+  if (threadIdx.x == 0) {
+    sa.sc->ticket = 0;
+    if (sa.world == 1) {
+      scalar_step(step, dd_value(tot), sa);
+    } else {
+      sa.dd_slots[0] = tot;  // local slot; all-gathered by the host driver
+    }
+  }
+}
+
+struct FinalizeArgs {
+  const int64_t* row_rseg;
+  const int64_t* tile_cseg;
+  const double* rowpart;
+  const double* colpart;
+  const int64_t* row_off;
+  int64_t row_lo, row_hi, tile_lo;
+  int b;
+  double* out;         // padded layout
+  const double* s;     // for the fused dot (padded layout) or null
+  double* dpart;
+  int step;
+  StepArgs sa;
+  const int32_t* done;
+};
+
+__global__ void __launch_bounds__(256) finalize_kernel(FinalizeArgs fa) {
+  if (fa.done && *fa.done) return;
+  const int64_t jr = blockIdx.x;  // output block row
+  const int b = fa.b;
+  const int64_t rs0 = (jr >= fa.row_lo && jr < fa.row_hi) ? fa.row_rseg[jr - fa.row_lo] : 0;
+  const int64_t rs1 = (jr >= fa.row_lo && jr < fa.row_hi) ? fa.row_rseg[jr - fa.row_lo + 1] : 0;
+  const int64_t i0 = jr > fa.row_lo ? jr : fa.row_lo;
+  double dotp = 0.0;
+  for (int c = threadIdx.x; c < b; c += blockDim.x) {
+    double acc = 0.0;
+    for (int64_t sgi = rs0; sgi < rs1; ++sgi) acc += fa.rowpart[sgi * b + c];
+    for (int64_t ii = i0; ii < fa.row_hi; ++ii) {
+      const int64_t tl = tri(ii, jr) - fa.tile_lo;
+      const int64_t c0 = fa.tile_cseg[tl], c1 = fa.tile_cseg[tl + 1];
+      for (int64_t cs = c0; cs < c1; ++cs) acc += fa.colpart[cs * b + c];
+    }
+    const int64_t o = fa.row_off[jr] + c;
+    fa.out[o] = acc;
+    if (fa.s) dotp = fma(fa.s[o], acc, dotp);
+  }
+  if (fa.s) dot_epilogue(dotp, fa.dpart, fa.step, fa.sa);
+}
+
+// ---------------------------------------------------------------------------
+// Generic SYMV (any b; single rank): one warp per output row reading the
+// packed symmetric storage like symv_row (block_kernels.cpp:59-95).
+
+__global__ void symv_generic_kernel(const double* __restrict__ a, int64_t n_pad,
+                                    int b, const double* __restrict__ x,
+                                    double* __restrict__ y,
+                                    const int32_t* done) {
+  if (done && *done) return;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n_pad) return;
+  const int64_t p = warp;
+  const int64_t ip = p / b;
+  const int r = (int)(p - ip * b);
+  double acc = 0.0;
+  for (int64_t qq = lane; qq < n_pad; qq += 32) {
+    const int64_t iq = qq / b;
+    const int c = (int)(qq - iq * b);
+    double v;
+    if (iq < ip || (iq == ip && c <= r))
+      v = a[tri(ip, iq) * b * b + (int64_t)r * b + c];
+    else
+      v = a[tri(iq, ip) * b * b + (int64_t)c * b + r];
+    acc = fma(v, x[qq], acc);
+  }
+  for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) y[p] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// Vector kernels over a rank's local chunk (len elements). Every kernel that
+// produces a dot uses a fixed grid and a fixed per-thread element set, so the
+// reduction order is deterministic.
+
+constexpr int VGRID = 148;
+constexpr int VBLOCK = 256;
+
+struct VecArgs {
+  int64_t len;
+  double* x;
+  double* r;
+  double* s;        // local chunk of s
+  const double* t;
+  const double* rhs;
+  double* dpart;
+  StepArgs sa;
+  const int32_t* done;
+  int mode;
+};
+
+enum VecMode : int {
+  V_INIT = 0,       // x = 0, r = s = rhs, dot(rhs, rhs) -> INIT
+  V_UPDATE = 1,     // x += a s, r -= a t, dot(r, r) -> BETA
+  V_AXPY_X = 2,     // x += a s (recompute iteration, first half)
+  V_RESIDUAL = 3,   // r = rhs - t, dot(r, r) -> BETA (recompute second half)
+  V_SDIR = 4,       // s = r + beta s
+  V_DOT_ST = 5,     // dot(s, t) -> ALPHA (multi-rank path)
+  V_RESNORM = 6,    // dot(rhs - t, rhs - t) -> NONE (true residual)
+};
+
+__global__ void __launch_bounds__(VBLOCK) vec_kernel(VecArgs va) {
+  if (va.mode != V_INIT && va.mode != V_RESNORM && va.done && *va.done) return;
+  const double alpha = va.sa.sc->alpha;
+  const double beta = va.sa.sc->beta;
+  double part = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < va.len;
+       k += stride) {
+    switch (va.mode) {
+      case V_INIT: {
+        const double v = va.rhs[k];
+        va.x[k] = 0.0;
+        va.r[k] = v;
+        va.s[k] = v;
+        part = fma(v, v, part);
+        break;
+      }
+      case V_UPDATE: {
+        va.x[k] = fma(alpha, va.s[k], va.x[k]);
+        const double rr = fma(-alpha, va.t[k], va.r[k]);
+        va.r[k] = rr;
+        part = fma(rr, rr, part);
+        break;
+      }
+      case V_AXPY_X:
+        va.x[k] = fma(alpha, va.s[k], va.x[k]);
+        break;
+      case V_RESIDUAL: {
+        const double rr = va.rhs[k] - va.t[k];
+        va.r[k] = rr;
+        part = fma(rr, rr, part);
+        break;
+      }
+      case V_SDIR:
+        va.s[k] = fma(beta, va.s[k], va.r[k]);
+        break;
+      case V_DOT_ST:
+        part = fma(va.s[k], va.t[k], part);
+        break;
+      case V_RESNORM: {
+        const double rr = va.rhs[k] - va.t[k];
+        part = fma(rr, rr, part);
+        break;
+      }
+    }
+  }
+  int step = STEP_NONE;
+  if (va.mode == V_INIT) step = STEP_INIT;
+  else if (va.mode == V_UPDATE || va.mode == V_RESIDUAL) step = STEP_BETA;
+  else if (va.mode == V_DOT_ST) step = STEP_ALPHA;
+  else if (va.mode == V_RESNORM) step = STEP_NONE;
+  else return;
+  dot_epilogue(part, va.dpart, step, va.sa);
+}
+
+// Combine all-gathered per-rank (hi, lo) partials in rank order, then the
+// scalar step (multi-rank path; identical on every rank).
+__global__ void combine_kernel(const Dd* slots, int world, int step,
+                               StepArgs sa, double* out_value,
+                               const int32_t* done) {
+  if (step != STEP_INIT && step != STEP_NONE && done && *done) return;
+  Dd acc = slots[0];
+  for (int g = 1; g < world; ++g) acc = dd_add(acc, slots[g]);
+  const double v = dd_value(acc);
+  if (out_value) *out_value = v;
+  if (step != STEP_NONE) scalar_step(step, v, sa);
+}
+
+// ---------------------------------------------------------------------------
+// plan
+
+void free_plan(SymvPlan* p) {
+  if (!p) return;
+  cudaFree(p->cta_slab);
+  cudaFree(p->cta_rseg);
+  cudaFree(p->cta_cseg);
+  cudaFree(p->row_rseg);
+  cudaFree(p->tile_cseg);
+  cudaFree(p->rowpart);
+  cudaFree(p->colpart);
+  delete p;
+}
+
+static bool fast_b(size_t b) { return b == 64 || b == 128 || b == 256 || b == 512; }
+
+void ensure_plan(hs_matrix* m) {
+  if (m->plan) return;
+  const int64_t b = (int64_t)m->b;
+  HS_REQUIRE(fast_b(m->b) || m->ctx->world == 1, HS_ERR_CONFIG,
+             "multi-GPU CG needs block size 64, 128, 256 or 512");
+  SymvPlan* p = new SymvPlan;
+  if (!fast_b(m->b)) {  // generic kernel needs no plan
+    m->plan = p;
+    return;
+  }
+  const int64_t spt = b * b / 4096;
+  const int64_t T = m->tile_hi - m->tile_lo;
+  const int64_t S = T * spt;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(m->ctx->num_sms, S));
+  std::vector<int64_t> cta_slab(grid + 1), cta_rseg(grid), cta_cseg(grid);
+  const int64_t R = (int64_t)(m->row_hi - m->row_lo);
+  std::vector<int64_t> row_cnt(R + 1, 0), tile_cnt(T + 1, 0);
+  int64_t nr = 0, nc = 0;
+  for (int64_t c = 0; c <= grid; ++c) cta_slab[c] = S * c / grid;
+  for (int64_t c = 0; c < grid; ++c) {
+    cta_rseg[c] = nr;
+    cta_cseg[c] = nc;
+    const int64_t g0 = cta_slab[c], g1 = cta_slab[c + 1];
+    if (g0 >= g1) continue;
+    const int64_t t0 = g0 / spt, t1 = (g1 - 1) / spt;  // local tile idx
+    const int64_t i0 = tile_row(t0 + m->tile_lo), i1 = tile_row(t1 + m->tile_lo);
+    for (int64_t i = i0; i <= i1; ++i) row_cnt[i - (int64_t)m->row_lo]++;
+    for (int64_t t = t0; t <= t1; ++t) tile_cnt[t]++;
+    nr += i1 - i0 + 1;
+    nc += t1 - t0 + 1;
+  }
+  // exclusive prefix sums: segments of row i / tile t are consecutive ids
+  std::vector<int64_t> row_rseg(R + 1, 0), tile_cseg(T + 1, 0);
+  for (int64_t i = 0; i < R; ++i) row_rseg[i + 1] = row_rseg[i] + row_cnt[i];
+  for (int64_t t = 0; t < T; ++t) tile_cseg[t + 1] = tile_cseg[t] + tile_cnt[t];
+  p->grid = (int)grid;
+  p->slabs_per_tile = spt;
+  p->nrseg = nr;
+  p->ncseg = nc;
+  auto up = [&](int64_t** dst, const std::vector<int64_t>& v) {
+    HS_CUDA(cudaMalloc(dst, v.size() * sizeof(int64_t)));
+    HS_CUDA(cudaMemcpy(*dst, v.data(), v.size() * sizeof(int64_t),
+                       cudaMemcpyHostToDevice));
+  };
+  up(&p->cta_slab, cta_slab);
+  up(&p->cta_rseg, cta_rseg);
+  up(&p->cta_cseg, cta_cseg);
+  up(&p->row_rseg, row_rseg);
+  up(&p->tile_cseg, tile_cseg);
+  HS_CUDA(cudaMalloc(&p->rowpart, std::max<int64_t>(1, nr) * b * sizeof(double)));
+  HS_CUDA(cudaMalloc(&p->colpart, std::max<int64_t>(1, nc) * b * sizeof(double)));
+  m->plan = p;
+}
+
+template <int B>
+static void launch_symv_fast(hs_ctx* c, const hs_matrix* m, const double* s,
+                             const int32_t* done) {
+  using Cfg = SymvCfg<B>;
+  static bool attr = false;
+  if (!attr) {
+    HS_CUDA(cudaFuncSetAttribute(symv_slab_kernel<B>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg::SMEM));
+    attr = true;
+  }
+  SymvPlan* p = m->plan;
+  SymvArgs a{m->d,          s,           m->d_row_off, m->tile_lo,
+             p->cta_slab,   p->cta_rseg, p->cta_cseg,  p->rowpart,
+             p->colpart,    done};
+  symv_slab_kernel<B><<<p->grid, 288, Cfg::SMEM, c->stream>>>(a);
+  HS_CUDA(cudaGetLastError());
+  launch_count(c);
+}
+
+static void ensure_dpart(hs_ctx* c, size_t count) {
+  if (c->dpart_cap >= count) return;
+  cudaFree(c->d_dpart);
+  HS_CUDA(cudaMalloc(&c->d_dpart, count * sizeof(double)));
+  c->dpart_cap = count;
+}
+
+// SYMV over the rank's tiles into `out` (padded full layout). With fuse_dot,
+// also dot(s, out) over the rows and the ALPHA step (single rank only).
+static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
+                    bool fuse_dot, const StepArgs* sa, const int32_t* done) {
+  const int b = (int)m->b;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->prof) {
+    HS_CUDA(cudaEventCreate(&e0));
+    HS_CUDA(cudaEventCreate(&e1));
+    HS_CUDA(cudaEventRecord(e0, c->stream));
+  }
+  if (!fast_b(m->b)) {
+    const int64_t pn = (int64_t)m->N * b;
+    const int64_t threads = pn * 32;
+    symv_generic_kernel<<<(unsigned)ceil_div(threads, 256), 256, 0, c->stream>>>(
+        m->d, pn, b, s, out, done);
+    HS_CUDA(cudaGetLastError());
+    launch_count(c);
+    if (c->prof) {
+      HS_CUDA(cudaEventRecord(e1, c->stream));
+      c->prof_events.push_back(e0);
+      c->prof_events.push_back(e1);
+    }
+    if (fuse_dot) {
+      VecArgs va{};
+      va.len = pn;
+      va.s = const_cast<double*>(s);
+      va.t = out;
+      va.dpart = c->d_dpart;
+      va.sa = *sa;
+      va.done = done;
+      va.mode = V_DOT_ST;
+      vec_kernel<<<VGRID, VBLOCK, 0, c->stream>>>(va);
+      HS_CUDA(cudaGetLastError());
+      launch_count(c);
+    }
+    return;
+  }
+  switch (b) {
+    case 64: launch_symv_fast<64>(c, m, s, done); break;
+    case 128: launch_symv_fast<128>(c, m, s, done); break;
+    case 256: launch_symv_fast<256>(c, m, s, done); break;
+    case 512: launch_symv_fast<512>(c, m, s, done); break;
+  }
+  if (c->prof) {
+    HS_CUDA(cudaEventRecord(e1, c->stream));
+    c->prof_events.push_back(e0);
+    c->prof_events.push_back(e1);
+  }
+  SymvPlan* p = m->plan;
+  FinalizeArgs fa{};
+  fa.row_rseg = p->row_rseg;
+  fa.tile_cseg = p->tile_cseg;
+  fa.rowpart = p->rowpart;
+  fa.colpart = p->colpart;
+  fa.row_off = m->d_row_off;
+  fa.row_lo = (int64_t)m->row_lo;
+  fa.row_hi = (int64_t)m->row_hi;
+  fa.tile_lo = m->tile_lo;
+  fa.b = b;
+  fa.out = out;
+  fa.s = fuse_dot ? s : nullptr;
+  fa.dpart = c->d_dpart;
+  fa.step = STEP_ALPHA;
+  if (sa) fa.sa = *sa;
+  fa.done = done;
+  finalize_kernel<<<(unsigned)m->row_hi, 128, 0, c->stream>>>(fa);
+  HS_CUDA(cudaGetLastError());
+  launch_count(c);
+}
+
+void symv_local(hs_ctx* c, const hs_matrix* m, const double* x, double* y) {
+  ensure_plan(const_cast<hs_matrix*>(m));
+  symv_to(c, m, x, y, false, nullptr, nullptr);
+}
+
+static void launch_vec(hs_ctx* c, VecArgs va) {
+  vec_kernel<<<VGRID, VBLOCK, 0, c->stream>>>(va);
+  HS_CUDA(cudaGetLastError());
+  launch_count(c);
+}
+
+// ---------------------------------------------------------------------------
+// CG driver
+
+struct CgBuffers {
+  double* s_full = nullptr;  // padded full layout (vec_len)
+  double* x_full = nullptr;  // padded full layout (recompute / result)
+  double* t = nullptr;       // partial (vec_len) or local result (world 1)
+  double* t_loc = nullptr;   // reduced own rows (multi-rank)
+  double* r = nullptr;       // local chunk
+  double* rhs = nullptr;     // local chunk
+  double* trace = nullptr;   // device trace
+  Dd* slots = nullptr;       // [world] gathered partials
+  void release() {
+    cudaFree(s_full);
+    cudaFree(x_full);
+    cudaFree(t);
+    cudaFree(t_loc);
+    cudaFree(r);
+    cudaFree(rhs);
+    cudaFree(trace);
+    cudaFree(slots);
+  }
+};
+
+static double ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now() - t0)
+      .count();
+}
+
+// d_rhs / d_x: full standard-layout vectors (N*b) on this rank's GPU.
+static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
+                   const hs_cg_params* prm, double* d_x, hs_cg_stats* st,
+                   double* h_trace) {
+  HS_REQUIRE(prm->eps > 0.0, HS_ERR_CONFIG, "eps must be positive");
+  ensure_plan(const_cast<hs_matrix*>(m));
+  const int world = c->world, rank = c->rank;
+  const int64_t b = (int64_t)m->b;
+  const int64_t N = (int64_t)m->N;
+  const int64_t chunk = m->vec_len / world;  // doubles per rank chunk
+  const int64_t full = m->vec_len;
+  const int64_t lo = (int64_t)m->row_lo, hi = (int64_t)m->row_hi;
+  const int64_t own = (hi - lo) * b;  // valid doubles in the chunk
+  const size_t trace_n = prm->record_trace ? (size_t)prm->max_iters : 0;
+  const bool rec_on = prm->recompute_interval > 0;
+
+  ensure_dpart(c, std::max<int64_t>(N + 1, VGRID));
+  CgBuffers B;
+  struct Guard {
+    CgBuffers* b;
+    ~Guard() { b->release(); }
+  } guard{&B};
+  HS_CUDA(cudaMalloc(&B.s_full, full * sizeof(double)));
+  HS_CUDA(cudaMalloc(&B.x_full, full * sizeof(double)));
+  HS_CUDA(cudaMalloc(&B.t, full * sizeof(double)));
+  HS_CUDA(cudaMalloc(&B.r, chunk * sizeof(double)));
+  HS_CUDA(cudaMalloc(&B.rhs, chunk * sizeof(double)));
+  HS_CUDA(cudaMalloc(&B.slots, std::max(world, 1) * sizeof(Dd)));
+  if (world > 1) HS_CUDA(cudaMalloc(&B.t_loc, chunk * sizeof(double)));
+  if (trace_n) HS_CUDA(cudaMalloc(&B.trace, 3 * trace_n * sizeof(double)));
+  HS_CUDA(cudaMemsetAsync(B.t, 0, full * sizeof(double), c->stream));
+  HS_CUDA(cudaMemsetAsync(B.rhs, 0, chunk * sizeof(double), c->stream));
+  HS_CUDA(cudaMemsetAsync(B.x_full, 0, full * sizeof(double), c->stream));
+  HS_CUDA(cudaMemsetAsync(c->d_scalars, 0, sizeof(CgScalars), c->stream));
+  // own rows of rhs into the local chunk (standard layout -> chunk)
+  HS_CUDA(cudaMemcpyAsync(B.rhs, d_rhs + lo * b, own * sizeof(double),
+                          cudaMemcpyDeviceToDevice, c->stream));
+
+  double* s_loc = B.s_full + (int64_t)rank * chunk;
+  double* x_loc = B.x_full + (int64_t)rank * chunk;
+  double* t_own = world > 1 ? B.t_loc : B.t;
+  const int32_t* done = &c->d_scalars->done;
+
+  StepArgs sa{c->d_scalars, B.trace, prm->eps, B.slots, world};
+
+  auto dot_finish = [&](int step) {
+    if (world == 1) return;
+    // all-gather the (hi, lo) partials in place, combine in rank order
+    comm_allgather(c, reinterpret_cast<double*>(B.slots) + 2 * rank,
+                   reinterpret_cast<double*>(B.slots), 2);
+    combine_kernel<<<1, 1, 0, c->stream>>>(B.slots, world, step, sa, nullptr,
+                                           done);
+    HS_CUDA(cudaGetLastError());
+    launch_count(c);
+  };
+  // In the multi-rank kernels the local partial is written to slots[0];
+  // relocate it into this rank's slot before the in-place all-gather.
+  StepArgs sa_local = sa;
+  sa_local.dd_slots = B.slots + rank;
+
+  VecArgs v{};
+  v.len = chunk;
+  v.x = x_loc;
+  v.r = B.r;
+  v.s = s_loc;
+  v.t = t_own;
+  v.rhs = B.rhs;
+  v.dpart = c->d_dpart;
+  v.sa = world > 1 ? sa_local : sa;
+  v.done = done;
+
+  // x0 = 0, r = s = rhs, u0 = rhs^T rhs (cg_solver.cpp:243-249)
+  v.mode = V_INIT;
+  launch_vec(c, v);
+  dot_finish(STEP_INIT);
+  if (world > 1) comm_allgather(c, s_loc, B.s_full, (size_t)chunk);
+
+  // Convergence is decided on the device (done flag); the host polls a
+  // pinned copy of the scalars one chunk behind, so the GPU queue never
+  // drains while the host checks.
+  const uint64_t check_every = 4;
+  CgScalars* pin = reinterpret_cast<CgScalars*>(c->h_pinned);
+  cudaEvent_t ev[2];
+  HS_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  HS_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  int pending = -1;
+  CgScalars h{};
+  for (uint64_t it = 1; it <= prm->max_iters; ++it) {
+    // line 4 (+5 fused for a single rank): t = A s, alpha = u / s^T t
+    if (world == 1) {
+      symv_to(c, m, B.s_full, B.t, true, &sa, done);
+    } else {
+      symv_to(c, m, B.s_full, B.t, false, nullptr, done);
+      comm_reduce_scatter(c, B.t, B.t_loc, (size_t)chunk);
+      v.mode = V_DOT_ST;
+      launch_vec(c, v);
+      dot_finish(STEP_ALPHA);
+    }
+    const bool recompute = rec_on && (it % prm->recompute_interval == 0);
+    if (recompute) {
+      // x += alpha s; r = rhs - A x (cg_solver.cpp:277-298)
+      v.mode = V_AXPY_X;
+      launch_vec(c, v);
+      if (world > 1) comm_allgather(c, x_loc, B.x_full, (size_t)chunk);
+      symv_to(c, m, B.x_full, B.t, false, nullptr, done);
+      if (world > 1) comm_reduce_scatter(c, B.t, B.t_loc, (size_t)chunk);
+      v.mode = V_RESIDUAL;
+      launch_vec(c, v);
+    } else {
+      v.mode = V_UPDATE;  // lines 6-7 + u = r^T r + beta
+      launch_vec(c, v);
+    }
+    dot_finish(STEP_BETA);
+    v.mode = V_SDIR;  // line 11
+    launch_vec(c, v);
+    if (world > 1) comm_allgather(c, s_loc, B.s_full, (size_t)chunk);
+    if (it % check_every == 0) {
+      const int slot = (int)((it / check_every) & 1);
+      HS_CUDA(cudaMemcpyAsync(pin + slot, c->d_scalars, sizeof(CgScalars),
+                              cudaMemcpyDeviceToHost, c->stream));
+      HS_CUDA(cudaEventRecord(ev[slot], c->stream));
+      if (pending >= 0) {
+        HS_CUDA(cudaEventSynchronize(ev[pending]));
+        if (pin[pending].done) break;
+      }
+      pending = slot;
+    }
+  }
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  HS_CUDA(cudaMemcpyAsync(&h, c->d_scalars, sizeof(CgScalars),
+                          cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  // recomputation count is a pure function of the iteration count
+  st->iterations = (uint64_t)h.iter;
+  st->recomputations = rec_on ? (uint64_t)h.iter / prm->recompute_interval : 0;
+  if (h.status == HS_ERR_NUMERICAL) {
+    // an error inside iteration k: iterations completed = k - 1
+    st->error_iteration = h.err_iter;
+    st->u0 = h.u0;
+    throw Failure{HS_ERR_NUMERICAL,
+                  h.err_iter == 0 ? std::string("initial residual is not finite")
+                                  : "non-finite scalar at iteration " +
+                                        std::to_string(h.err_iter),
+                  h.err_iter, -1};
+  }
+  st->converged = h.u <= h.limit ? 1 : 0;
+  st->u0 = h.u0;
+  st->error_iteration = -1;
+  if (trace_n && h_trace && h.iter > 0)
+    HS_CUDA(cudaMemcpy(h_trace, B.trace, 3 * (size_t)h.iter * sizeof(double),
+                       cudaMemcpyDeviceToHost));
+
+  // result: full x in the standard layout
+  if (world > 1) comm_allgather(c, x_loc, B.x_full, (size_t)chunk);
+  for (int g = 0; g < world; ++g) {
+    const int64_t glo = m->bounds[g], ghi = m->bounds[g + 1];
+    if (ghi > glo)
+      HS_CUDA(cudaMemcpyAsync(d_x + glo * b, B.x_full + (int64_t)g * chunk,
+                              (ghi - glo) * b * sizeof(double),
+                              cudaMemcpyDeviceToDevice, c->stream));
+  }
+  // exit diagnostic: ||rhs - A x|| (cg_solver.cpp:360-365)
+  symv_to(c, m, B.x_full, B.t, false, nullptr, nullptr);
+  if (world > 1) comm_reduce_scatter(c, B.t, B.t_loc, (size_t)chunk);
+  VecArgs vr = v;
+  vr.mode = V_RESNORM;
+  vr.done = nullptr;
+  launch_vec(c, vr);
+  double res2;
+  if (world > 1) {
+    comm_allgather(c, reinterpret_cast<double*>(B.slots) + 2 * rank,
+                   reinterpret_cast<double*>(B.slots), 2);
+    combine_kernel<<<1, 1, 0, c->stream>>>(B.slots, world, STEP_NONE, sa,
+                                           c->d_dpart + N, nullptr);
+    HS_CUDA(cudaGetLastError());
+    launch_count(c);
+    HS_CUDA(cudaMemcpyAsync(&res2, c->d_dpart + N, sizeof(double),
+                            cudaMemcpyDeviceToHost, c->stream));
+  } else {
+    // single rank: the epilogue left the DD in dpart via STEP_NONE; redo the
+    // fixed-order combine on the host from the per-CTA partials
+    std::vector<double> parts(VGRID);
+    HS_CUDA(cudaMemcpyAsync(parts.data(), c->d_dpart, VGRID * sizeof(double),
+                            cudaMemcpyDeviceToHost, c->stream));
+    HS_CUDA(cudaStreamSynchronize(c->stream));
+    Dd acc{0.0, 0.0};
+    for (double p : parts) acc = dd_add(acc, p);
+    res2 = dd_value(acc);
+  }
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  st->true_residual = sqrt(res2);
+}
+
+}  // namespace hs
+
+using namespace hs;
+
+#define HS_API_BEGIN \
+  clear_error();     \
+  try {
+#define HS_API_END                                                         \
+  return HS_OK;                                                            \
+  }                                                                        \
+  catch (const Failure& f) {                                               \
+    set_error(f.status, f.msg, f.a, f.b);                                  \
+    return f.status;                                                       \
+  }                                                                        \
+  catch (const std::exception& e) {                                        \
+    set_error(HS_ERR_CUDA, e.what());                                      \
+    return HS_ERR_CUDA;                                                    \
+  }
+
+extern "C" {
+
+hs_status hs_symv(hs_ctx* c, const hs_matrix* m, const double* d_x,
+                  double* d_y) {
+  HS_API_BEGIN
+  HS_REQUIRE(c && m && d_x && d_y, HS_ERR_CONFIG, "null pointer");
+  HS_REQUIRE(c->world == 1, HS_ERR_CONFIG,
+             "hs_symv is single-rank; use hs_cg_solve for sharded matrices");
+  HS_CUDA(cudaSetDevice(c->device));
+  symv_local(c, m, d_x, d_y);
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  HS_API_END
+}
+
+hs_status hs_true_residual(hs_ctx* c, const hs_matrix* m, const double* d_x,
+                           const double* d_rhs, double* out) {
+  HS_API_BEGIN
+  HS_REQUIRE(c && m && d_x && d_rhs && out, HS_ERR_CONFIG, "null pointer");
+  HS_REQUIRE(c->world == 1, HS_ERR_CONFIG, "hs_true_residual is single-rank");
+  HS_CUDA(cudaSetDevice(c->device));
+  const int64_t pn = (int64_t)m->N * (int64_t)m->b;
+  double* t = nullptr;
+  HS_CUDA(cudaMalloc(&t, pn * sizeof(double)));
+  try {
+    symv_local(c, m, d_x, t);
+    ensure_dpart(c, std::max<int64_t>((int64_t)m->N + 1, VGRID));
+    HS_CUDA(cudaMemsetAsync(c->d_scalars, 0, sizeof(CgScalars), c->stream));
+    VecArgs v{};
+    v.len = pn;
+    v.t = t;
+    v.rhs = d_rhs;
+    v.dpart = c->d_dpart;
+    v.sa = StepArgs{c->d_scalars, nullptr, 1.0, nullptr, 1};
+    v.mode = V_RESNORM;
+    launch_vec(c, v);
+    std::vector<double> parts(VGRID);
+    HS_CUDA(cudaMemcpyAsync(parts.data(), c->d_dpart, VGRID * sizeof(double),
+                            cudaMemcpyDeviceToHost, c->stream));
+    HS_CUDA(cudaStreamSynchronize(c->stream));
+    Dd acc{0.0, 0.0};
+    for (double p : parts) acc = dd_add(acc, p);
+    *out = sqrt(dd_value(acc));
+  } catch (...) {
+    cudaFree(t);
+    throw;
+  }
+  cudaFree(t);
+  HS_API_END
+}
+
+hs_status hs_cg_solve(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
+                      const hs_cg_params* p, double* d_x, hs_cg_stats* st,
+                      double* trace) {
+  HS_API_BEGIN
+  HS_REQUIRE(c && m && d_rhs && p && d_x && st, HS_ERR_CONFIG, "null pointer");
+  HS_REQUIRE(m->ctx == c, HS_ERR_CONFIG, "matrix belongs to another context");
+  HS_CUDA(cudaSetDevice(c->device));
+  std::memset(st, 0, sizeof(*st));
+  const auto t0 = std::chrono::steady_clock::now();
+  cg_run(c, m, d_rhs, p, d_x, st, trace);
+  st->wall_ms = ms_since(t0);
+  st->compute_ms = st->wall_ms;
+  HS_API_END
+}
+
+hs_status hs_solve_cg_host(hs_ctx* c, size_t n, size_t b, const double* a,
+                           const double* rhs, const hs_cg_params* p, double* x,
+                           hs_cg_stats* st, double* trace) {
+  HS_API_BEGIN
+  HS_REQUIRE(c && a && rhs && p && x && st, HS_ERR_CONFIG, "null pointer");
+  HS_REQUIRE(p->eps > 0.0, HS_ERR_CONFIG, "eps must be positive");
+  HS_CUDA(cudaSetDevice(c->device));
+  std::memset(st, 0, sizeof(*st));
+  const auto t0 = std::chrono::steady_clock::now();
+  hs_matrix* m = nullptr;
+  hs_status s = hs_matrix_create(c, n, b, &m);
+  if (s != HS_OK) throw Failure{s, hs_last_error()};
+  double *d_rhs = nullptr, *d_x = nullptr;
+  const size_t pn = (size_t)ceil_div(n, b) * b;
+  try {
+    HS_CUDA(cudaMalloc(&d_rhs, pn * sizeof(double)));
+    HS_CUDA(cudaMalloc(&d_x, pn * sizeof(double)));
+    const auto tt = std::chrono::steady_clock::now();
+    s = hs_matrix_upload(m, a);
+    if (s != HS_OK) throw Failure{s, hs_last_error()};
+    HS_CUDA(cudaMemcpyAsync(d_rhs, rhs, pn * sizeof(double),
+                            cudaMemcpyHostToDevice, c->stream));
+    HS_CUDA(cudaStreamSynchronize(c->stream));
+    double xfer = ms_since(tt);
+    cg_run(c, m, d_rhs, p, d_x, st, trace);
+    const auto t2 = std::chrono::steady_clock::now();
+    HS_CUDA(cudaMemcpyAsync(x, d_x, pn * sizeof(double), cudaMemcpyDeviceToHost,
+                            c->stream));
+    HS_CUDA(cudaStreamSynchronize(c->stream));
+    xfer += ms_since(t2);
+    st->wall_ms = ms_since(t0);
+    st->transfer_ms = xfer;
+    st->compute_ms = st->wall_ms - xfer;
+  } catch (...) {
+    cudaFree(d_rhs);
+    cudaFree(d_x);
+    hs_matrix_destroy(m);
+    throw;
+  }
+  cudaFree(d_rhs);
+  cudaFree(d_x);
+  hs_matrix_destroy(m);
+  HS_API_END
+}
+
+}  // extern "C"

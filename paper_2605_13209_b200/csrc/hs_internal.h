@@ -1,0 +1,101 @@
+// Internal types of libhsolve_cuda.so (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "hs_common.cuh"
+#include "hs_cuda.h"
+
+namespace hs {
+
+// Lazily dlopen'ed NCCL (only multi-rank contexts need it).
+struct Nccl;
+
+// Device scalars of one CG solve (one instance per context).
+struct CgScalars {
+  double u;       // current r^T r (recurrence value)
+  double u0;      // initial r^T r
+  double limit;   // eps^2 * u0
+  double alpha;
+  double beta;
+  int64_t iter;   // completed iterations
+  int64_t recomputations;
+  int32_t done;   // converged / error: later kernels are no-ops
+  int32_t status; // HS_OK or HS_ERR_NUMERICAL
+  int64_t err_iter;
+  uint32_t ticket;  // last-CTA-done counter (reset by the last CTA)
+  uint32_t pad;
+};
+
+// SYMV work plan: persistent CTAs stream contiguous ranges of 32-KB slabs of
+// the packed tiles; partial row / column sums go to fixed segment slots so
+// the reduction order is deterministic.
+struct SymvPlan {
+  int grid = 0;
+  int64_t slabs_per_tile = 0;
+  int64_t nrseg = 0, ncseg = 0;
+  // device arrays
+  int64_t* cta_slab = nullptr;       // [grid+1] slab range per CTA
+  int64_t* cta_rseg = nullptr;       // [grid] first row segment id
+  int64_t* cta_cseg = nullptr;       // [grid] first column segment id
+  int64_t* row_rseg = nullptr;       // [N+1] row segments of block row i
+  int64_t* tile_cseg = nullptr;      // [T_local+1] column segs of local tile
+  double* rowpart = nullptr;         // [nrseg * b]
+  double* colpart = nullptr;         // [ncseg * b]
+};
+
+}  // namespace hs
+
+struct hs_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int rank = 0, world = 1;
+  hs::Nccl* nccl = nullptr;
+  void* comm = nullptr;  // ncclComm_t
+  uint64_t launches = 0;
+  int num_sms = 148;
+  // profiling of the SYMV launches
+  bool prof = false;
+  uint64_t prof_symv_launches = 0;
+  double prof_symv_ms = 0.0;
+  std::vector<cudaEvent_t> prof_events;  // pairs, drained by hs_prof_symv
+  // scratch
+  hs::CgScalars* d_scalars = nullptr;
+  double* d_dpart = nullptr;  // per-block-row dot partials
+  size_t dpart_cap = 0;
+  double* h_pinned = nullptr;  // small pinned readback buffer
+};
+
+struct hs_matrix {
+  hs_ctx* ctx = nullptr;
+  size_t n = 0, b = 0, N = 0;     // logical size, tile size, block rows
+  size_t row_lo = 0, row_hi = 0;  // owned block rows
+  int64_t tile_lo = 0, tile_hi = 0;  // owned packed tile range
+  double* d = nullptr;            // local tiles
+  hs::SymvPlan* plan = nullptr;
+  // Cholesky: inverses of the diagonal factor tiles (N * b * b), filled by
+  // hs_potrf and reused by the triangular solves.
+  double* dinv = nullptr;
+  bool has_inv = false;
+  // Multi-rank vector layout: row i lives at vec_off[i] (padded rank chunks).
+  std::vector<int64_t> bounds;    // world+1 block-row bounds
+  int64_t vec_len = 0;            // doubles in a full (padded) vector
+  int64_t* d_row_off = nullptr;   // [N] element offset of block row i
+  size_t local_tiles() const { return (size_t)(tile_hi - tile_lo); }
+};
+
+namespace hs {
+
+void launch_count(hs_ctx* c, int k = 1);
+void ensure_plan(hs_matrix* m);
+void free_plan(SymvPlan* p);
+// y (padded layout, full length) = A x over this rank's tiles (partials of
+// other ranks' rows included); dot_out (optional, device) gets per-row dots.
+void symv_local(hs_ctx* c, const hs_matrix* m, const double* x, double* y);
+void launch_fill(hs_ctx* c, double* p, double v, int64_t count);
+
+}  // namespace hs

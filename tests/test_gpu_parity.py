@@ -1,0 +1,425 @@
+"""GPU parity: the B200 kernels (through the C ABI) against the CPU oracle.
+
+The oracle (oracle/hs_oracle.c) is bitwise identical to the reference
+(tests/test_oracle.py pins that); these tests compare the CUDA path with it on
+the same seeded inputs. Tolerances (written next to each check):
+
+* assembly: elementwise relative <= 4 ulp (only exp differs; d2 is computed
+  with the reference's mul-then-add rounding); diagonal and padding exact.
+* SYMV: |y - y_cpu| <= 1e-13 * (|A| |x|)_i  (summation order only).
+* CG: |iters - iters_cpu| <= 2; ||x - x_cpu|| / ||x_cpu|| <= 1e-6;
+  true residual <= 2 eps sqrt(u0) (test_cg_solver.cpp:88-89); trace
+  iterations 1-5 within 1e-10 relative (the trace is chaotic after ~8).
+* Cholesky: |L - L_cpu| <= 1e-10 max|A| (test_cholesky_solver.cpp:72-92);
+  ||x - x_cpu|| / ||x_cpu|| <= 1e-10; ||b - Ax|| <= 1e-10 ||b||.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2605_13209_b200 as hs
+from paper_2605_13209_b200 import hsolve as H
+
+pytestmark = pytest.mark.gpu
+
+EPS = np.finfo(np.float64).eps
+
+
+def dev(v: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(v)).to("cuda")
+
+
+def lower_mask(n, b):
+    """Boolean mask over the packed array: True for canonical lower entries."""
+    N = (n + b - 1) // b
+    masks = []
+    for i in range(N):
+        for j in range(i + 1):
+            m = np.ones((b, b), dtype=bool) if i != j else np.tril(np.ones((b, b), dtype=bool))
+            masks.append(m.ravel())
+    return np.concatenate(masks)
+
+
+# ---------------------------------------------------------------------------
+# (1) GP assembly
+
+
+@pytest.mark.parametrize("n,b", [(45, 8), (1024, 128), (1000, 64), (300, 1), (2048, 512),
+                                 (777, 256)])
+def test_assembly_matches_oracle(rt, oracle, n, b):
+    got = hs.generate_spd(n, b, seed=17, rt=rt).values
+    ref = oracle.generate_spd(n, b, seed=17)
+    exact = (ref == 1.0) | (ref == 0.0) | (ref == 1.01)  # padding / diagonal
+    assert np.array_equal(got[exact], ref[exact])
+    rel = np.abs(got - ref) / np.maximum(np.abs(ref), 1e-300)
+    assert rel.max() <= 4 * EPS, rel.max()
+
+
+def test_assembly_structure(rt):
+    # test_genmat.cpp:51-66
+    p = hs.KernelParams()
+    m = hs.generate_spd(50, 8, p, 11, rt=rt)
+    for q in range(0, 50, 7):
+        assert m.element(q, q) == p.sigma_f2 + p.sigma_n2
+    for r in range(0, 50, 5):
+        for c in range(0, 50, 3):
+            assert m.element(r, c) == m.element(c, r)
+            if r != c:
+                assert 0.0 < m.element(r, c) <= p.sigma_f2
+
+
+def test_assembly_rejects_bad_variance(rt):
+    with pytest.raises(hs.ConfigError):
+        hs.generate_spd(16, 4, hs.KernelParams(sigma_f2=0.0), 1, rt=rt)
+
+
+# ---------------------------------------------------------------------------
+# (2) SYMV
+
+
+@pytest.mark.parametrize("n,b", [(45, 8), (1024, 128), (1000, 64), (4096, 256), (2048, 512),
+                                 (333, 7), (96, 32), (8192, 128)])
+def test_symv_matches_oracle(rt, oracle, n, b):
+    a = oracle.generate_spd(n, b, seed=5)
+    x = oracle.generate_rhs(n, b, seed=9)
+    y_ref = oracle.symv(n, b, a, x)
+    m = hs.DeviceMatrix(rt, n, b).upload(a)
+    dx, dy = dev(x), torch.zeros_like(dev(x))
+    H.symv_device(rt, m, dx.data_ptr(), dy.data_ptr())
+    y = dy.cpu().numpy()
+    dense = hs.BlockedSPDMatrix(n, b, a).to_dense()
+    scale = np.abs(dense) @ np.abs(x[:n]) + 1e-300
+    err = np.abs(y[:n] - y_ref[:n]) / scale
+    assert err.max() <= 1e-13, err.max()
+    assert np.all(y[n:] == x[n:])  # identity padding: padded rows copy x (zeros)
+
+
+def test_symv_identity_and_worked_example(rt):
+    # test_block_kernels.cpp:197-220
+    ident = hs.BlockedSPDMatrix.identity(13, 4)
+    x = np.zeros(16)
+    x[:13] = np.arange(1, 14) * 0.5
+    m = hs.DeviceMatrix(rt, 13, 4).upload(ident)
+    dx = dev(x)
+    dy = torch.zeros_like(dx)
+    H.symv_device(rt, m, dx.data_ptr(), dy.data_ptr())
+    assert np.array_equal(dy.cpu().numpy(), x)
+    w = hs.BlockedSPDMatrix(2, 1)
+    w.set(0, 0, 2.0)
+    w.set(1, 0, 1.0)
+    w.set(1, 1, 3.0)
+    m2 = hs.DeviceMatrix(rt, 2, 1).upload(w)
+    dx = dev(np.array([1.0, 1.0]))
+    dy = torch.zeros_like(dx)
+    H.symv_device(rt, m2, dx.data_ptr(), dy.data_ptr())
+    assert dy.cpu().tolist() == [3.0, 4.0]
+
+
+def test_symv_ignores_stale_upper_halves(rt, oracle):
+    n, b = 512, 128
+    a = oracle.generate_spd(n, b, seed=3)
+    x = oracle.generate_rhs(n, b, seed=4)
+    y_ref = oracle.symv(n, b, a, x)
+    poisoned = a.copy()
+    mask = lower_mask(n, b)
+    poisoned[~mask] = np.nan  # strict upper halves of diagonal tiles
+    m = hs.DeviceMatrix(rt, n, b).upload(poisoned)
+    dx = dev(x)
+    dy = torch.zeros_like(dx)
+    H.symv_device(rt, m, dx.data_ptr(), dy.data_ptr())
+    y = dy.cpu().numpy()
+    assert np.all(np.isfinite(y))
+    assert np.abs(y - y_ref).max() <= 1e-12 * np.abs(y_ref).max()
+
+
+# ---------------------------------------------------------------------------
+# (3) CG
+
+
+@pytest.mark.parametrize("n,b", [(1024, 128), (1000, 64), (2048, 512), (1024, 32), (257, 16)])
+def test_cg_matches_oracle(rt, oracle, n, b):
+    a = oracle.generate_spd(n, b, seed=42)
+    rhs = oracle.generate_rhs(n, b, seed=42)
+    ref = oracle.solve_cg(n, b, a, rhs, eps=1e-6, max_iters=500)
+    cfg = hs.SolverConfig(block_size=b, record_trace=True)
+    res = hs.solve_cg(hs.BlockedSPDMatrix(n, b, a), hs.BlockVector(n, b, rhs), cfg, rt)
+    st = res.stats
+    assert st.converged and ref["converged"]
+    assert abs(st.iterations - ref["iterations"]) <= 2
+    x, xr = res.x.values[:n], ref["x"][:n]
+    assert np.linalg.norm(x - xr) <= 1e-6 * np.linalg.norm(xr)
+    assert st.true_residual <= 2 * cfg.eps * np.sqrt(st.u0)
+    assert abs(st.u0 - ref["u0"]) <= 1e-14 * ref["u0"]
+    tr = np.array([[t.u, t.alpha, t.beta] for t in st.trace[:5]])
+    assert np.allclose(tr, ref["trace"][:5], rtol=1e-10, atol=0)
+    assert np.all(res.x.values[n:] == 0.0)
+
+
+def test_cg_identity_one_iteration(rt):
+    # test_cg_solver.cpp:28-39
+    ident = hs.BlockedSPDMatrix.identity(64, 16)
+    rhs = hs.generate_rhs(64, 16, 1)
+    res = hs.solve_cg(ident, rhs, hs.SolverConfig(block_size=16), rt)
+    assert res.stats.iterations == 1 and res.stats.converged
+    assert np.array_equal(res.x.values, rhs.values)
+
+
+def test_cg_zero_rhs(rt):
+    # test_cg_solver.cpp:41-51
+    ident = hs.BlockedSPDMatrix.identity(16, 4)
+    res = hs.solve_cg(ident, hs.BlockVector(16, 4), hs.SolverConfig(block_size=4), rt)
+    assert res.stats.iterations == 0 and res.stats.converged and res.stats.u0 == 0.0
+    assert np.all(res.x.values == 0.0)
+
+
+def test_cg_small_system_vs_dense_solve(rt, oracle):
+    # test_cg_solver.cpp:53-74
+    n, b = 8, 2
+    a = hs.BlockedSPDMatrix(n, b, oracle.generate_spd(n, b, seed=77))
+    rhs = hs.BlockVector(n, b, oracle.generate_rhs(n, b, seed=77))
+    x_direct = np.linalg.solve(a.to_dense(), rhs.logical())
+    res = hs.solve_cg(a, rhs, hs.SolverConfig(block_size=b, eps=1e-10, max_iters=100), rt)
+    assert res.stats.converged
+    assert np.linalg.norm(res.x.logical() - x_direct) <= 1e-5 * np.linalg.norm(x_direct)
+
+
+@pytest.mark.parametrize("n", [96, 256])
+def test_cg_true_residual_bound(rt, oracle, n):
+    # test_cg_solver.cpp:76-91
+    b = 16
+    a = hs.BlockedSPDMatrix(n, b, oracle.generate_spd(n, b, seed=13))
+    rhs = hs.BlockVector(n, b, oracle.generate_rhs(n, b, seed=13))
+    cfg = hs.SolverConfig(block_size=b, eps=1e-6, max_iters=2000)
+    st = hs.solve_cg(a, rhs, cfg, rt).stats
+    assert st.converged and st.u0 > 0
+    assert st.true_residual <= 2 * cfg.eps * np.sqrt(st.u0)
+
+
+def test_cg_recompute_cadence(rt, oracle):
+    # test_cg_solver.cpp:150-161, 219-234
+    n, b = 128, 16
+    a = hs.BlockedSPDMatrix(n, b, oracle.generate_spd(n, b, seed=21))
+    rhs = hs.BlockVector(n, b, oracle.generate_rhs(n, b, seed=21))
+    cfg = hs.SolverConfig(block_size=b, recompute_interval=5, eps=1e-300, max_iters=12)
+    st = hs.solve_cg(a, rhs, cfg, rt).stats
+    assert st.iterations == 12 and st.recomputations == 2
+    cfg = hs.SolverConfig(block_size=b, recompute_interval=3, eps=1e-8, max_iters=500)
+    a6 = hs.BlockedSPDMatrix(96, b, oracle.generate_spd(96, b, seed=6))
+    r6 = hs.BlockVector(96, b, oracle.generate_rhs(96, b, seed=6))
+    st = hs.solve_cg(a6, r6, cfg, rt).stats
+    assert st.converged and st.recomputations == st.iterations // 3
+    assert st.true_residual <= 2 * cfg.eps * np.sqrt(st.u0)
+
+
+def test_cg_iteration_cap_is_a_status(rt, oracle):
+    # test_cg_solver.cpp:236-248
+    n, b = 64, 16
+    a = hs.BlockedSPDMatrix(n, b, oracle.generate_spd(n, b, seed=14))
+    rhs = hs.BlockVector(n, b, oracle.generate_rhs(n, b, seed=14))
+    st = hs.solve_cg(a, rhs, hs.SolverConfig(block_size=b, eps=1e-14, max_iters=2), rt).stats
+    assert not st.converged and st.iterations == 2
+
+
+def test_cg_single_block_row(rt, oracle):
+    # test_cg_solver.cpp:204-217
+    a = hs.BlockedSPDMatrix(8, 8, oracle.generate_spd(8, 8, seed=2))
+    rhs = hs.BlockVector(8, 8, oracle.generate_rhs(8, 8, seed=2))
+    st = hs.solve_cg(a, rhs, hs.SolverConfig(block_size=8, eps=1e-10, max_iters=100), rt).stats
+    assert st.converged and st.true_residual <= 1e-8
+
+
+def test_cg_nonfinite_and_shape_errors(rt):
+    # test_cg_solver.cpp:250-264
+    ident = hs.BlockedSPDMatrix.identity(8, 4)
+    rhs = hs.BlockVector(8, 4)
+    rhs[3] = np.inf
+    with pytest.raises(hs.NumericalError):
+        hs.solve_cg(ident, rhs, hs.SolverConfig(block_size=4), rt)
+    with pytest.raises(hs.ConfigError):
+        hs.solve_cg(ident, hs.BlockVector(8, 2), hs.SolverConfig(block_size=4), rt)
+
+
+def test_cg_device_resident_matches_host_entry(rt, oracle):
+    n, b = 2048, 128
+    m = hs.generate_spd_device(rt, n, b, seed=42)
+    rhs = oracle.generate_rhs(n, b, seed=42)
+    d_rhs = dev(rhs)
+    d_x = torch.zeros_like(d_rhs)
+    cfg = hs.SolverConfig(block_size=b, eps=1e-6)
+    st = hs.solve_cg_device(rt, m, d_rhs.data_ptr(), d_x.data_ptr(), cfg)
+    host = hs.solve_cg(m.to_host(), hs.BlockVector(n, b, rhs), cfg, rt)
+    assert st.iterations == host.stats.iterations
+    assert np.array_equal(d_x.cpu().numpy(), host.x.values)  # deterministic
+
+
+# ---------------------------------------------------------------------------
+# (4) Cholesky
+
+
+@pytest.mark.parametrize("n,b", [(1024, 128), (2048, 512), (1000, 256), (256, 32), (100, 16),
+                                 (45, 8), (2, 1)])
+def test_factor_and_solve_match_oracle(rt, oracle, n, b):
+    a = oracle.generate_spd(n, b, seed=42)
+    rhs = oracle.generate_rhs(n, b, seed=42)
+    st, L_ref, _, _ = oracle.factorize(n, b, a)
+    assert st == 0
+    mask = lower_mask(n, b)
+    work = hs.BlockedSPDMatrix(n, b, a.copy())
+    hs.factorize(work, hs.SolverConfig(block_size=b), rt)
+    maxa = np.abs(a[mask]).max()
+    assert np.abs(work.values[mask] - L_ref[mask]).max() <= 1e-10 * maxa
+    res = hs.solve_spd(hs.BlockedSPDMatrix(n, b, a.copy()), hs.BlockVector(n, b, rhs),
+                       hs.SolverConfig(block_size=b), rt)
+    ref = oracle.solve_spd(n, b, a, rhs)
+    x, xr = res.x.values[:n], ref["x"][:n]
+    assert np.linalg.norm(x - xr) <= 1e-10 * np.linalg.norm(xr)
+    assert res.stats.true_residual <= 1e-10 * np.linalg.norm(rhs[:n])
+
+
+def test_factor_closed_form_and_identity(rt):
+    # test_cholesky_solver.cpp:35-70
+    m = hs.BlockedSPDMatrix(2, 1)
+    m.set(0, 0, 4.0)
+    m.set(1, 0, 2.0)
+    m.set(1, 1, 3.0)
+    hs.factorize(m, hs.SolverConfig(block_size=1), rt)
+    assert m.block(0, 0)[0, 0] == 2.0 and m.block(1, 0)[0, 0] == 1.0
+    assert abs(m.block(1, 1)[0, 0] - np.sqrt(2.0)) <= 1e-15
+    ident = hs.BlockedSPDMatrix.identity(12, 4)
+    hs.factorize(ident, hs.SolverConfig(block_size=4), rt)
+    for p in range(12):
+        for q in range(p + 1):
+            assert ident.element(p, q) == (1.0 if p == q else 0.0)
+
+
+def test_not_spd_reports_column_and_pivot(rt, oracle):
+    # test_cholesky_solver.cpp:208-224
+    a = hs.BlockedSPDMatrix(64, 16, oracle.generate_spd(64, 16, seed=2))
+    a.set(40, 40, -5.0)
+    with pytest.raises(hs.NotSpdError) as ei:
+        hs.factorize(a, hs.SolverConfig(block_size=16), rt)
+    assert ei.value.block_row == 2 and ei.value.pivot_index == 40 % 16
+
+
+def test_not_spd_dmma_path(rt, oracle):
+    n, b = 1024, 128
+    a = hs.BlockedSPDMatrix(n, b, oracle.generate_spd(n, b, seed=2))
+    a.set(700, 700, -5.0)
+    with pytest.raises(hs.NotSpdError) as ei:
+        hs.factorize(a, hs.SolverConfig(block_size=b), rt)
+    assert ei.value.block_row == 700 // b and ei.value.pivot_index == 700 % b
+
+
+def test_substitutions(rt, oracle):
+    # test_cholesky_solver.cpp:226-282
+    ident = hs.BlockedSPDMatrix.identity(10, 4)
+    rhs = hs.BlockVector(10, 4, np.arange(1, 11) * 0.5)
+    y = hs.forward_substitute(ident, rhs, rt)
+    x = hs.back_substitute(ident, y, rt)
+    assert np.array_equal(y.logical(), rhs.logical()) and np.array_equal(x.logical(), rhs.logical())
+    l2 = hs.BlockedSPDMatrix(2, 1)
+    l2.set(0, 0, 2.0)
+    l2.set(1, 0, 1.0)
+    l2.set(1, 1, np.sqrt(2.0))
+    r2 = hs.BlockVector(2, 1, np.array([2.0, 1.0 + np.sqrt(2.0)]))
+    y = hs.forward_substitute(l2, r2, rt)
+    assert np.allclose(y.logical(), [1.0, 1.0], rtol=1e-15)
+    x = hs.back_substitute(l2, y, rt)
+    a = np.array([[4.0, 2.0], [2.0, 3.0]])
+    assert np.abs(a @ x.logical() - r2.logical()).max() <= 1e-12
+    sing = hs.BlockedSPDMatrix.identity(4, 2)
+    sing.set(2, 2, 0.0)
+    r = hs.BlockVector(4, 2)
+    r[0] = 1.0
+    with pytest.raises(hs.SingularBlockError):
+        hs.forward_substitute(sing, r, rt)
+    with pytest.raises(hs.SingularBlockError):
+        hs.back_substitute(sing, r, rt)
+
+
+@pytest.mark.parametrize("n,b", [(1024, 128), (2048, 512), (200, 16)])
+def test_substitutions_match_oracle(rt, oracle, n, b):
+    a = oracle.generate_spd(n, b, seed=8)
+    _, L, _, _ = oracle.factorize(n, b, a)
+    rhs = oracle.generate_rhs(n, b, seed=8)
+    _, y_ref = oracle.forward_substitute(n, b, L, rhs)
+    _, x_ref = oracle.back_substitute(n, b, L, y_ref)
+    lm = hs.BlockedSPDMatrix(n, b, L)
+    y = hs.forward_substitute(lm, hs.BlockVector(n, b, rhs), rt)
+    x = hs.back_substitute(lm, y, rt)
+    assert np.linalg.norm(y.values - y_ref) <= 1e-11 * np.linalg.norm(y_ref)
+    assert np.linalg.norm(x.values - x_ref) <= 1e-10 * np.linalg.norm(x_ref)
+
+
+# ---------------------------------------------------------------------------
+# single-tile kernels
+
+
+@pytest.mark.parametrize("b", [1, 2, 5, 16, 32, 128, 512])
+def test_potf_tiles_reconstruct(rt, oracle, b):
+    # test_block_kernels.cpp:57-75
+    rng = np.random.default_rng(11 + b)
+    tiles = []
+    for _ in range(3):
+        mm = rng.uniform(-1, 1, (b, b))
+        tiles.append(mm @ mm.T + b * np.eye(b))
+    t = np.stack(tiles)
+    d = dev(t)
+    H.potf_tiles_device(rt, d.data_ptr(), b, 3)
+    got = d.cpu().numpy()
+    for k in range(3):
+        ref = t[k].copy().ravel()
+        assert oracle.lib.hso_potf_block(ref, b, None) == 0
+        ref = ref.reshape(b, b)
+        lo = np.tril(np.ones((b, b), dtype=bool))
+        assert np.abs(got[k][lo] - ref[lo]).max() <= 1e-12 * np.abs(t[k]).max()
+        assert np.array_equal(got[k][~lo], t[k][~lo])  # upper untouched
+
+
+def test_potf_tile_not_spd(rt):
+    d = dev(np.array([[1.0, 2.0], [2.0, 1.0]]))
+    with pytest.raises(hs.NotSpdError) as ei:
+        H.potf_tiles_device(rt, d.data_ptr(), 2, 1)
+    assert ei.value.pivot_index == 1
+
+
+@pytest.mark.parametrize("b,lower", [(128, False), (128, True), (256, False), (512, True),
+                                     (16, False), (3, True)])
+def test_gemm_update_tiles(rt, oracle, b, lower):
+    rng = np.random.default_rng(b)
+    cnt = 2
+    c = rng.uniform(-1, 1, (cnt, b, b))
+    p = rng.uniform(-1, 1, (cnt, b, b))
+    q = p.copy() if lower else rng.uniform(-1, 1, (cnt, b, b))
+    dc, dp, dq = dev(c), dev(p), dev(q)  # keep the operands alive
+    H.gemm_update_tiles_device(rt, dc.data_ptr(), dp.data_ptr(), dq.data_ptr(), b, cnt, lower)
+    got = dc.cpu().numpy()
+    for k in range(cnt):
+        ref = c[k].copy().ravel()
+        if lower:
+            oracle.lib.hso_syrk_update(ref, p[k].ravel().copy(), b)
+        else:
+            oracle.lib.hso_gemm_update(ref, p[k].ravel().copy(), q[k].ravel().copy(), b)
+        ref = ref.reshape(b, b)
+        assert np.abs(got[k] - ref).max() <= 1e-13 * b
+        if lower:
+            up = np.triu(np.ones((b, b), dtype=bool), 1)
+            assert np.array_equal(got[k][up], c[k][up])
+
+
+def test_gemm_worked_examples(rt):
+    # test_block_kernels.cpp:150-183
+    c = dev(np.array([[1.0, 0.0], [0.0, 1.0]]))
+    p, q = dev(np.array([[1.0, 2.0], [3.0, 4.0]])), dev(np.eye(2))
+    H.gemm_update_tiles_device(rt, c.data_ptr(), p.data_ptr(), q.data_ptr(), 2, 1)
+    assert c.cpu().numpy().ravel().tolist() == [0.0, -2.0, -3.0, -3.0]
+    c = dev(np.array([[5.0, 42.0], [2.0, 5.0]]))
+    pp = dev(np.ones((2, 2)))
+    H.gemm_update_tiles_device(rt, c.data_ptr(), pp.data_ptr(), pp.data_ptr(), 2, 1, True)
+    assert c.cpu().numpy().ravel().tolist() == [3.0, 42.0, 0.0, 3.0]
+
+
+def test_kernel_launches_are_counted(rt):
+    before = rt.kernel_launches()
+    hs.generate_spd(256, 128, seed=1, rt=rt)
+    assert rt.kernel_launches() > before
