@@ -60,9 +60,10 @@ struct SymvArgs {
   int64_t tile_lo;        // global index of the first local tile
   const int64_t* cta_slab;
   const int64_t* cta_rseg;
-  const int64_t* cta_cseg;
-  double* rowpart;
-  double* colpart;
+  double* rowpart;        // [nrseg][B]  (CTA, block row) segments
+  double* colmain;        // [T_local][B] column partial of each tile
+  double* colextra;       // [grid][B]   a CTA's first tile when it starts
+                          //             mid-tile (split tiles)
   const int32_t* done;    // CG early-exit flag (nullable)
 };
 
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(288, 1) symv_slab_kernel(SymvArgs args) {
   const int rl = tid / TPR;  // row lane: slab rows 2rl, 2rl+1
   const int h = cl / W;      // row-sharing warp index (B = 512)
   const int64_t rseg0 = args.cta_rseg[blockIdx.x];
-  const int64_t cseg0 = args.cta_cseg[blockIdx.x];
+  const bool split_start = (g0 % SPT) != 0;
 
   double cacc[8];
 #pragma unroll
@@ -226,12 +227,14 @@ __global__ void __launch_bounds__(288, 1) symv_slab_kernel(SymvArgs args) {
         reinterpret_cast<double2*>(cr + rl * B)[cl + TPR * m] =
             make_double2(cacc[2 * m], cacc[2 * m + 1]);
       named_bar_sync(1, 256);
-      const int64_t cseg = cseg0 + (t - t_first);
+      double* dst = (split_start && t == t_first)
+                        ? args.colextra + (int64_t)blockIdx.x * B
+                        : args.colmain + (t - args.tile_lo) * B;
       for (int c = tid; c < B; c += 256) {
         double acc = 0.0;
 #pragma unroll 4
         for (int r = 0; r < RPP; ++r) acc += cr[r * B + c];
-        args.colpart[cseg * B + c] = acc;
+        dst[c] = acc;
       }
       const bool row_end = (j == i && q == SPT - 1) || (g + 1 == g1);
       if (row_end) {
@@ -360,22 +363,22 @@ __device__ void scalar_step(int step, double val, const StepArgs& sa) {
 // Last-CTA epilogue shared by the dot-producing kernels: combine per-CTA
 // partials (fixed order); single rank -> apply the scalar step directly,
 // multi rank -> publish this rank's (hi, lo) for the all-gather.
-__device__ void dot_epilogue(double part, double* dpart, int step,
-                             const StepArgs& sa) {
+__device__ void dot_epilogue(double part, double* dpart, int slot, int count,
+                             int step, const StepArgs& sa) {
   __shared__ double red_d[32];
   __shared__ Dd red_dd[256];
   __shared__ bool last;
   const double p = block_sum(part, red_d);
   if (threadIdx.x == 0) {
-    dpart[blockIdx.x] = p;
+    dpart[slot] = p;
     __threadfence();
     const unsigned prev = atomicAdd(&sa.sc->ticket, 1u);
-    last = (prev == gridDim.x - 1);
+    last = (prev == (unsigned)count - 1);
   }
   __syncthreads();
   if (!last) return;
   __threadfence();
-  const Dd tot = dd_reduce_parts(dpart, gridDim.x, red_dd);
+  const Dd tot = dd_reduce_parts(dpart, count, red_dd);
   if (threadIdx.x == 0) {
     sa.sc->ticket = 0;
     if (sa.world == 1) {
@@ -386,11 +389,26 @@ __device__ void dot_epilogue(double part, double* dpart, int step,
   }
 }
 
+// Two-stage fixed-order reduction of the SYMV partial slots.
+//  stage 1: unit u = (output block row j, tiles i in [i0, i1) of column j,
+//           <= 16 tiles): sum of the tiles' column partials -> upart[u]
+//  stage 2: the last unit CTA of row j (per-row ticket) adds, in order, its
+//           row's unit partials, row segments and split-tile extras -> t_j,
+//           then (optionally) the dot s_j . t_j and, via a global ticket, the
+//           double-double total and the CG alpha step.
 struct FinalizeArgs {
-  const int64_t* row_rseg;
-  const int64_t* tile_cseg;
+  const int32_t* unit_row;
+  const int32_t* unit_i0;
+  const int32_t* unit_i1;
+  const int32_t* row_unit;   // [rows+1] unit range of each output row
+  const int64_t* row_rseg;   // [own rows+1] row segments
+  const int32_t* row_extra;  // [rows+1] range into extra_cta
+  const int32_t* extra_cta;  // CTAs whose first (split) tile is in row j
   const double* rowpart;
-  const double* colpart;
+  const double* colmain;
+  const double* colextra;
+  double* upart;
+  uint32_t* row_ticket;
   const int64_t* row_off;
   int64_t row_lo, row_hi, tile_lo;
   int b;
@@ -402,27 +420,45 @@ struct FinalizeArgs {
   const int32_t* done;
 };
 
-__global__ void __launch_bounds__(256) finalize_kernel(FinalizeArgs fa) {
+__global__ void __launch_bounds__(128) finalize_kernel(FinalizeArgs fa) {
   if (fa.done && *fa.done) return;
-  const int64_t jr = blockIdx.x;  // output block row
+  const int u = blockIdx.x;
+  const int64_t jr = fa.unit_row[u];
+  const int i0 = fa.unit_i0[u], i1 = fa.unit_i1[u];
   const int b = fa.b;
-  const int64_t rs0 = (jr >= fa.row_lo && jr < fa.row_hi) ? fa.row_rseg[jr - fa.row_lo] : 0;
-  const int64_t rs1 = (jr >= fa.row_lo && jr < fa.row_hi) ? fa.row_rseg[jr - fa.row_lo + 1] : 0;
-  const int64_t i0 = jr > fa.row_lo ? jr : fa.row_lo;
+  for (int c = threadIdx.x; c < b; c += blockDim.x) {
+    double acc = 0.0;
+#pragma unroll 8
+    for (int i = i0; i < i1; ++i)
+      acc += fa.colmain[(tri(i, jr) - fa.tile_lo) * b + c];
+    fa.upart[(int64_t)u * b + c] = acc;
+  }
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  const int ub = fa.row_unit[jr], ue = fa.row_unit[jr + 1];
+  if (threadIdx.x == 0) {
+    last = atomicAdd(&fa.row_ticket[jr], 1u) == (unsigned)(ue - ub - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const bool own = jr >= fa.row_lo && jr < fa.row_hi;
+  const int64_t rs0 = own ? fa.row_rseg[jr - fa.row_lo] : 0;
+  const int64_t rs1 = own ? fa.row_rseg[jr - fa.row_lo + 1] : 0;
+  const int e0 = fa.row_extra[jr], e1 = fa.row_extra[jr + 1];
   double dotp = 0.0;
   for (int c = threadIdx.x; c < b; c += blockDim.x) {
     double acc = 0.0;
-    for (int64_t sgi = rs0; sgi < rs1; ++sgi) acc += fa.rowpart[sgi * b + c];
-    for (int64_t ii = i0; ii < fa.row_hi; ++ii) {
-      const int64_t tl = tri(ii, jr) - fa.tile_lo;
-      const int64_t c0 = fa.tile_cseg[tl], c1 = fa.tile_cseg[tl + 1];
-      for (int64_t cs = c0; cs < c1; ++cs) acc += fa.colpart[cs * b + c];
-    }
+    for (int uu = ub; uu < ue; ++uu) acc += fa.upart[(int64_t)uu * b + c];
+    for (int64_t sg = rs0; sg < rs1; ++sg) acc += fa.rowpart[sg * b + c];
+    for (int e = e0; e < e1; ++e) acc += fa.colextra[(int64_t)fa.extra_cta[e] * b + c];
     const int64_t o = fa.row_off[jr] + c;
     fa.out[o] = acc;
     if (fa.s) dotp = fma(fa.s[o], acc, dotp);
   }
-  if (fa.s) dot_epilogue(dotp, fa.dpart, fa.step, fa.sa);
+  if (threadIdx.x == 0) fa.row_ticket[jr] = 0;
+  if (fa.s) dot_epilogue(dotp, fa.dpart, (int)jr, (int)fa.row_hi, fa.step, fa.sa);
 }
 
 // ---------------------------------------------------------------------------
@@ -538,7 +574,7 @@ __global__ void __launch_bounds__(VBLOCK) vec_kernel(VecArgs va) {
   else if (va.mode == V_DOT_ST) step = STEP_ALPHA;
   else if (va.mode == V_RESNORM) step = STEP_NONE;
   else return;
-  dot_epilogue(part, va.dpart, step, va.sa);
+  dot_epilogue(part, va.dpart, blockIdx.x, gridDim.x, step, va.sa);
 }
 
 // Combine all-gathered per-rank (hi, lo) partials in rank order, then the
@@ -559,18 +595,25 @@ __global__ void combine_kernel(const Dd* slots, int world, int step,
 
 void free_plan(SymvPlan* p) {
   if (!p) return;
-  cudaFree(p->cta_slab);
-  cudaFree(p->cta_rseg);
-  cudaFree(p->cta_cseg);
-  cudaFree(p->row_rseg);
-  cudaFree(p->tile_cseg);
-  cudaFree(p->rowpart);
-  cudaFree(p->colpart);
+  for (void* q : {(void*)p->cta_slab, (void*)p->cta_rseg, (void*)p->row_rseg,
+                  (void*)p->unit_row, (void*)p->unit_i0, (void*)p->unit_i1,
+                  (void*)p->row_unit, (void*)p->row_extra, (void*)p->extra_cta,
+                  (void*)p->row_ticket, (void*)p->rowpart, (void*)p->colmain,
+                  (void*)p->colextra, (void*)p->upart})
+    cudaFree(q);
   delete p;
 }
 
 static bool fast_b(size_t b) { return b == 64 || b == 128 || b == 256 || b == 512; }
 
+template <typename T>
+static void upload_vec(T** dst, const std::vector<T>& v) {
+  HS_CUDA(cudaMalloc(dst, std::max<size_t>(v.size(), 1) * sizeof(T)));
+  if (!v.empty())
+    HS_CUDA(cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+// Static work plan of the SYMV + finalize pair for one matrix (host side).
 void ensure_plan(hs_matrix* m) {
   if (m->plan) return;
   const int64_t b = (int64_t)m->b;
@@ -584,44 +627,59 @@ void ensure_plan(hs_matrix* m) {
   const int64_t spt = b * b / 4096;
   const int64_t T = m->tile_hi - m->tile_lo;
   const int64_t S = T * spt;
+  const int64_t lo = (int64_t)m->row_lo, hi = (int64_t)m->row_hi;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(m->ctx->num_sms, S));
-  std::vector<int64_t> cta_slab(grid + 1), cta_rseg(grid), cta_cseg(grid);
-  const int64_t R = (int64_t)(m->row_hi - m->row_lo);
-  std::vector<int64_t> row_cnt(R + 1, 0), tile_cnt(T + 1, 0);
-  int64_t nr = 0, nc = 0;
+  std::vector<int64_t> cta_slab(grid + 1), cta_rseg(grid);
+  std::vector<int64_t> row_cnt(hi - lo + 1, 0);
+  std::vector<std::vector<int32_t>> extras(hi);
+  int64_t nr = 0;
   for (int64_t c = 0; c <= grid; ++c) cta_slab[c] = S * c / grid;
   for (int64_t c = 0; c < grid; ++c) {
     cta_rseg[c] = nr;
-    cta_cseg[c] = nc;
     const int64_t g0 = cta_slab[c], g1 = cta_slab[c + 1];
     if (g0 >= g1) continue;
-    const int64_t t0 = g0 / spt, t1 = (g1 - 1) / spt;  // local tile idx
-    const int64_t i0 = tile_row(t0 + m->tile_lo), i1 = tile_row(t1 + m->tile_lo);
-    for (int64_t i = i0; i <= i1; ++i) row_cnt[i - (int64_t)m->row_lo]++;
-    for (int64_t t = t0; t <= t1; ++t) tile_cnt[t]++;
+    const int64_t t0 = g0 / spt + m->tile_lo, t1 = (g1 - 1) / spt + m->tile_lo;
+    const int64_t i0 = tile_row(t0), i1 = tile_row(t1);
+    for (int64_t i = i0; i <= i1; ++i) row_cnt[i - lo]++;
     nr += i1 - i0 + 1;
-    nc += t1 - t0 + 1;
+    if (g0 % spt != 0) extras[t0 - tri(i0, 0)].push_back((int32_t)c);
   }
-  // exclusive prefix sums: segments of row i / tile t are consecutive ids
-  std::vector<int64_t> row_rseg(R + 1, 0), tile_cseg(T + 1, 0);
-  for (int64_t i = 0; i < R; ++i) row_rseg[i + 1] = row_rseg[i] + row_cnt[i];
-  for (int64_t t = 0; t < T; ++t) tile_cseg[t + 1] = tile_cseg[t] + tile_cnt[t];
+  std::vector<int64_t> row_rseg(hi - lo + 1, 0);
+  for (int64_t i = 0; i < hi - lo; ++i) row_rseg[i + 1] = row_rseg[i] + row_cnt[i];
+  std::vector<int32_t> row_extra(hi + 1, 0), extra_cta;
+  for (int64_t j = 0; j < hi; ++j) {
+    for (int32_t c : extras[j]) extra_cta.push_back(c);
+    row_extra[j + 1] = (int32_t)extra_cta.size();
+  }
+  // finalize units: column j's local tiles i in [max(j, lo), hi), 16 per unit
+  constexpr int64_t kUnit = 16;
+  std::vector<int32_t> unit_row, unit_i0, unit_i1, row_unit(hi + 1, 0);
+  for (int64_t j = 0; j < hi; ++j) {
+    for (int64_t i = std::max(j, lo); i < hi; i += kUnit) {
+      unit_row.push_back((int32_t)j);
+      unit_i0.push_back((int32_t)i);
+      unit_i1.push_back((int32_t)std::min(hi, i + kUnit));
+    }
+    row_unit[j + 1] = (int32_t)unit_row.size();
+  }
   p->grid = (int)grid;
+  p->units = (int)unit_row.size();
   p->slabs_per_tile = spt;
   p->nrseg = nr;
-  p->ncseg = nc;
-  auto up = [&](int64_t** dst, const std::vector<int64_t>& v) {
-    HS_CUDA(cudaMalloc(dst, v.size() * sizeof(int64_t)));
-    HS_CUDA(cudaMemcpy(*dst, v.data(), v.size() * sizeof(int64_t),
-                       cudaMemcpyHostToDevice));
-  };
-  up(&p->cta_slab, cta_slab);
-  up(&p->cta_rseg, cta_rseg);
-  up(&p->cta_cseg, cta_cseg);
-  up(&p->row_rseg, row_rseg);
-  up(&p->tile_cseg, tile_cseg);
+  upload_vec(&p->cta_slab, cta_slab);
+  upload_vec(&p->cta_rseg, cta_rseg);
+  upload_vec(&p->row_rseg, row_rseg);
+  upload_vec(&p->unit_row, unit_row);
+  upload_vec(&p->unit_i0, unit_i0);
+  upload_vec(&p->unit_i1, unit_i1);
+  upload_vec(&p->row_unit, row_unit);
+  upload_vec(&p->row_extra, row_extra);
+  upload_vec(&p->extra_cta, extra_cta);
+  upload_vec(&p->row_ticket, std::vector<uint32_t>(hi, 0u));
   HS_CUDA(cudaMalloc(&p->rowpart, std::max<int64_t>(1, nr) * b * sizeof(double)));
-  HS_CUDA(cudaMalloc(&p->colpart, std::max<int64_t>(1, nc) * b * sizeof(double)));
+  HS_CUDA(cudaMalloc(&p->colmain, std::max<int64_t>(1, T) * b * sizeof(double)));
+  HS_CUDA(cudaMalloc(&p->colextra, grid * b * sizeof(double)));
+  HS_CUDA(cudaMalloc(&p->upart, std::max<int>(1, p->units) * b * sizeof(double)));
   m->plan = p;
 }
 
@@ -637,9 +695,8 @@ static void launch_symv_fast(hs_ctx* c, const hs_matrix* m, const double* s,
     attr = true;
   }
   SymvPlan* p = m->plan;
-  SymvArgs a{m->d,          s,           m->d_row_off, m->tile_lo,
-             p->cta_slab,   p->cta_rseg, p->cta_cseg,  p->rowpart,
-             p->colpart,    done};
+  SymvArgs a{m->d,        s,           m->d_row_off, m->tile_lo, p->cta_slab,
+             p->cta_rseg, p->rowpart, p->colmain,   p->colextra, done};
   symv_slab_kernel<B><<<p->grid, 288, Cfg::SMEM, c->stream>>>(a);
   HS_CUDA(cudaGetLastError());
   launch_count(c);
@@ -703,10 +760,18 @@ static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
   }
   SymvPlan* p = m->plan;
   FinalizeArgs fa{};
+  fa.unit_row = p->unit_row;
+  fa.unit_i0 = p->unit_i0;
+  fa.unit_i1 = p->unit_i1;
+  fa.row_unit = p->row_unit;
   fa.row_rseg = p->row_rseg;
-  fa.tile_cseg = p->tile_cseg;
+  fa.row_extra = p->row_extra;
+  fa.extra_cta = p->extra_cta;
   fa.rowpart = p->rowpart;
-  fa.colpart = p->colpart;
+  fa.colmain = p->colmain;
+  fa.colextra = p->colextra;
+  fa.upart = p->upart;
+  fa.row_ticket = p->row_ticket;
   fa.row_off = m->d_row_off;
   fa.row_lo = (int64_t)m->row_lo;
   fa.row_hi = (int64_t)m->row_hi;
@@ -718,7 +783,7 @@ static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
   fa.step = STEP_ALPHA;
   if (sa) fa.sa = *sa;
   fa.done = done;
-  finalize_kernel<<<(unsigned)m->row_hi, 128, 0, c->stream>>>(fa);
+  finalize_kernel<<<(unsigned)p->units, 128, 0, c->stream>>>(fa);
   HS_CUDA(cudaGetLastError());
   launch_count(c);
 }

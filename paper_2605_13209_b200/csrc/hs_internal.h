@@ -35,16 +35,24 @@ struct CgScalars {
 // the reduction order is deterministic.
 struct SymvPlan {
   int grid = 0;
+  int units = 0;
   int64_t slabs_per_tile = 0;
-  int64_t nrseg = 0, ncseg = 0;
+  int64_t nrseg = 0;
   // device arrays
-  int64_t* cta_slab = nullptr;       // [grid+1] slab range per CTA
-  int64_t* cta_rseg = nullptr;       // [grid] first row segment id
-  int64_t* cta_cseg = nullptr;       // [grid] first column segment id
-  int64_t* row_rseg = nullptr;       // [N+1] row segments of block row i
-  int64_t* tile_cseg = nullptr;      // [T_local+1] column segs of local tile
-  double* rowpart = nullptr;         // [nrseg * b]
-  double* colpart = nullptr;         // [ncseg * b]
+  int64_t* cta_slab = nullptr;   // [grid+1] slab range per CTA
+  int64_t* cta_rseg = nullptr;   // [grid] first row segment id
+  int64_t* row_rseg = nullptr;   // [own rows+1] row segments of block row i
+  int32_t* unit_row = nullptr;   // [units] finalize stage-1 work units
+  int32_t* unit_i0 = nullptr;
+  int32_t* unit_i1 = nullptr;
+  int32_t* row_unit = nullptr;   // [row_hi+1]
+  int32_t* row_extra = nullptr;  // [row_hi+1]
+  int32_t* extra_cta = nullptr;  // [grid]
+  uint32_t* row_ticket = nullptr;  // [row_hi]
+  double* rowpart = nullptr;     // [nrseg * b]
+  double* colmain = nullptr;     // [T_local * b]
+  double* colextra = nullptr;    // [grid * b]
+  double* upart = nullptr;       // [units * b]
 };
 
 }  // namespace hs

@@ -1,0 +1,32 @@
+"""The C++ shim (include/hsolve/*.hpp, libhsolve_b200.so) builds against
+unchanged reference-style caller code and passes reference assertions."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PKG = os.path.join(ROOT, "paper_2605_13209_b200")
+
+
+def _build(tmp_path):
+    exe = str(tmp_path / "test_hsolve_api")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "test_hsolve_api.cpp"), "-o", exe,
+                    "-L", PKG, "-lhsolve_b200", "-lhsolve_cuda", f"-Wl,-rpath,{PKG}"],
+                   check=True)
+    return exe
+
+
+def test_cpp_shim_compiles(tmp_path):
+    if not os.path.exists(os.path.join(PKG, "libhsolve_b200.so")):
+        pytest.skip("shim not built")
+    assert os.path.exists(_build(tmp_path))
+
+
+@pytest.mark.gpu
+def test_cpp_shim_runs_reference_assertions(tmp_path):
+    exe = _build(tmp_path)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(out.stdout)
+    assert out.returncode == 0 and "ALL PASSED" in out.stdout, out.stdout + out.stderr
