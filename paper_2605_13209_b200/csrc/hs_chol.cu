@@ -172,11 +172,12 @@ __global__ void __launch_bounds__(256)
 // W[r0:r0+32, c] = -Winv t. Zero / NaN diagonal -> singular_block.
 
 __global__ void __launch_bounds__(256)
-    trtri_tile_kernel(const double* lbase, int64_t lstride, double* wbase,
-                      int b, CholFlag* flag, int64_t column0) {
+    trtri_tile_kernel(const double* A, int64_t tile_lo, double* wbase, int b,
+                      CholFlag* flag, int64_t j0) {
   if (flag && flag->status) return;
-  const double* L = lbase + (int64_t)blockIdx.x * lstride;
-  double* Wt = wbase + (int64_t)blockIdx.x * b * b;
+  const int64_t jt = j0 + blockIdx.x;  // diagonal tile (jt, jt)
+  const double* L = A + (tri(jt, jt) - tile_lo) * b * b;
+  double* Wt = wbase + jt * b * b;
   extern __shared__ double tsm[];
   double* Wi = tsm;               // 32 x 33 inverse of the diagonal block
   double* Lr = tsm + PNB * PLD;   // 32 x b block row of L (cols < r0)
@@ -217,7 +218,7 @@ __global__ void __launch_bounds__(256)
     }
     __syncthreads();
     if (bad >= 0) {
-      if (tid == 0 && flag) raise_flag(flag, HS_ERR_SINGULAR_BLOCK, column0 + blockIdx.x, bad);
+      if (tid == 0 && flag) raise_flag(flag, HS_ERR_SINGULAR_BLOCK, jt, bad);
       return;
     }
     for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
@@ -251,98 +252,185 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------
-// Tile GEMM items. Every mode computes C (+)= -/+ A B^T on b x b tiles whose
-// rows are the M / N index and whose columns are the shared K index.
+// Sub-block GEMM. Every item computes one cb x cb output sub-block
+//   C  =  A_op B_op^T          (op SET)   or
+//   C -=  A_op B_op^T          (op SUB, lower-only on diagonal sub-blocks)
+// where A_op / B_op are cb x K row strips of packed tiles (k contiguous) or
+// of the inverse blocks. cb = 128 on the DMMA path (b % 128 == 0); on the
+// SIMT path cb = b. f = b / cb sub-blocks per tile side.
 
 enum GemmMode : int {
-  G_UPDATE_ALL = 0,  // column j: A_ik -= X_i X_k^T, j < k <= i
-  G_UPDATE_COL = 1,  // column j: only k == j + 1        (lookahead part)
+  G_UPDATE_ALL = 0,  // column j: A_ik -= A_ij A_kj^T, j < k <= i   [K4/K5]
+  G_UPDATE_COL = 1,  // column j: only k == j + 1  (lookahead part)
   G_UPDATE_REST = 2, // column j: only k >= j + 2
-  G_TRSM = 3,        // column j: X_i = A_ij W_j^T  (out of place)
-  G_BATCH = 4,       // C_t -= P_t Q_t^T  (parity tests), lower_only option
+  G_PANEL_UPD = 3,   // column j, step c: A_ij[:,c] -= A_ij[:,<c] L_jj[c,<c]^T
+  G_PANEL_TRSM = 4,  // column j, step c: A_ij[:,c]  = A_ij[:,c] W_jc^T   [K3]
+  G_DIAG_TRSM = 5,   // column j, step s: D[r,s] = D[r,s] W_js^T, r > s
+  G_DIAG_UPD = 6,    // column j, step s: D[r,c] -= D[r,s] D[c,s]^T, s<c<=r
+  G_TRSM_X = 7,      // SIMT path: X_i = A_ij W_j^T into the panel buffer
+  G_BATCH = 8,       // tests: C_t -= P_t Q_t^T (lower_only option)
 };
 
 struct GemmArgs {
   int mode;
-  int64_t j;         // column
-  int64_t N;         // block rows
-  int b;
-  int tpd;           // CTA tiles per tile dimension (b / 128)
-  double* A;         // packed tiles (local)
+  int64_t j;        // column
+  int step;         // c or s
+  int64_t N;        // block rows
+  int b, cb, f;
+  double* A;        // packed tiles (local)
   int64_t tile_lo;
-  double* X;         // panel workspace: tile i at (i - j - 1) * b*b
-  const double* W;   // inverse of L_jj (b*b)
-  double* C;         // batch outputs
-  const double* P;   // batch A operands
-  const double* Q;   // batch B operands
+  const double* X;  // SIMT path panel buffer (tile i at (i - j - 1) b^2), or null
+  double* Xout;
+  const double* W;  // inverse blocks, block J at J * cb^2 (ld cb)
+  double* C;        // batch outputs
+  const double* P;  // batch operands
+  const double* Q;
   int lower_only;
   const CholFlag* flag;
 };
 
 struct GemmItem {
-  const double* a;  // operand tiles (b x b row-major)
-  const double* bt;
-  double* c;        // output tile
-  int64_t a_tile, b_tile;  // tile coordinates for the TMA maps
-  int op;           // 0: c -= acc, 1: c = acc
-  bool lower;       // write only col <= row (diagonal tiles)
-  int kmax;         // K range [0, kmax)
+  const double* a;  // A_op: row 0, k 0 (ld = lda)
+  const double* bp; // B_op
+  int lda, ldb;
+  int64_t a_tile, b_tile;  // TMA coordinates: tile index, row, k offset
+  int a_r0, a_k0, b_r0, b_k0;
+  double* c;        // output sub-block (ld = b)
+  int K;
+  int op;           // 0 SUB, 1 SET
+  bool lower;
   bool skip;
 };
 
-__device__ __forceinline__ GemmItem decode_item(const GemmArgs& g, int64_t item,
-                                                int mb, int nb) {
+__device__ __forceinline__ GemmItem decode_item(const GemmArgs& g, int64_t item) {
   GemmItem it{};
-  const int64_t bb = (int64_t)g.b * g.b;
-  it.kmax = g.b;
-  if (g.mode == G_TRSM) {
-    const int64_t i = g.j + 1 + item;
-    it.a = g.A + (tri(i, g.j) - g.tile_lo) * bb;
-    it.bt = g.W;
-    it.c = g.X + (i - g.j - 1) * bb;
-    it.a_tile = tri(i, g.j) - g.tile_lo;
-    it.b_tile = 0;
-    it.op = 1;
-    it.lower = false;
-    it.kmax = min(g.b, (nb + 1) * 128);  // W lower: W^T rows > col are zero
-    return it;
-  }
-  if (g.mode == G_BATCH) {
-    it.a = g.P + item * bb;
-    it.bt = g.Q + item * bb;
-    it.c = g.C + item * bb;
-    it.a_tile = item;
-    it.b_tile = item;
-    it.op = 0;
-    it.lower = g.lower_only != 0;
-    it.skip = it.lower && nb > mb;
-    return it;
-  }
-  int64_t i, k;
-  if (g.mode == G_UPDATE_COL) {
-    i = g.j + 1 + item;
-    k = g.j + 1;
-  } else {
-    const int64_t base = g.mode == G_UPDATE_REST ? g.j + 2 : g.j + 1;
-    const int64_t ii = tile_row(item);
-    i = base + ii;
-    k = base + (item - tri(ii, 0));
-  }
-  it.a = g.X + (i - g.j - 1) * bb;
-  it.bt = g.X + (k - g.j - 1) * bb;
-  it.c = g.A + (tri(i, k) - g.tile_lo) * bb;
-  it.a_tile = i - g.j - 1;
-  it.b_tile = k - g.j - 1;
+  const int b = g.b, cb = g.cb, f = g.f;
+  const int64_t bb = (int64_t)b * b;
+  auto tile = [&](int64_t i, int64_t k) { return tri(i, k) - g.tile_lo; };
+  auto sub = [&](int64_t t, int r, int c) { return g.A + t * bb + (int64_t)r * cb * b + (int64_t)c * cb; };
+  it.lda = it.ldb = b;
   it.op = 0;
-  it.lower = (i == k);
-  it.skip = it.lower && nb > mb;
-  return it;
+  switch (g.mode) {
+    case G_UPDATE_ALL:
+    case G_UPDATE_COL:
+    case G_UPDATE_REST: {
+      const int64_t u = item / (f * f);
+      const int sb = (int)(item % (f * f));
+      const int mb = sb / f, nb = sb % f;
+      int64_t i, k;
+      if (g.mode == G_UPDATE_COL) {
+        i = g.j + 1 + u;
+        k = g.j + 1;
+      } else {
+        const int64_t base = g.mode == G_UPDATE_REST ? g.j + 2 : g.j + 1;
+        const int64_t ii = tile_row(u);
+        i = base + ii;
+        k = base + (u - tri(ii, 0));
+      }
+      it.lower = (i == k) && mb == nb;
+      it.skip = (i == k) && nb > mb;
+      it.K = b;
+      if (g.X) {  // SIMT path: panel in the buffer
+        it.a = g.X + (i - g.j - 1) * bb + (int64_t)mb * cb * b;
+        it.bp = g.X + (k - g.j - 1) * bb + (int64_t)nb * cb * b;
+        it.a_tile = i - g.j - 1;
+        it.b_tile = k - g.j - 1;
+      } else {
+        it.a = g.A + tile(i, g.j) * bb + (int64_t)mb * cb * b;
+        it.bp = g.A + tile(k, g.j) * bb + (int64_t)nb * cb * b;
+        it.a_tile = tile(i, g.j);
+        it.b_tile = tile(k, g.j);
+      }
+      it.a_r0 = mb * cb;
+      it.b_r0 = nb * cb;
+      it.c = sub(tile(i, k), mb, nb);
+      return it;
+    }
+    case G_PANEL_UPD:
+    case G_PANEL_TRSM: {
+      const int64_t i = g.j + 1 + item / f;
+      const int mb = (int)(item % f);
+      const int c = g.step;
+      it.a_tile = tile(i, g.j);
+      it.a_r0 = mb * cb;
+      it.c = sub(it.a_tile, mb, c);
+      if (g.mode == G_PANEL_UPD) {
+        it.a_k0 = 0;
+        it.K = c * cb;
+        it.b_tile = tile(g.j, g.j);
+        it.b_r0 = c * cb;
+        it.bp = g.A + it.b_tile * bb + (int64_t)c * cb * b;
+      } else {
+        it.a_k0 = c * cb;
+        it.K = cb;
+        it.b_tile = g.j * f + c;
+        it.bp = g.W + it.b_tile * cb * cb;
+        it.ldb = cb;
+        it.op = 1;
+      }
+      it.a = g.A + it.a_tile * bb + (int64_t)it.a_r0 * b + it.a_k0;
+      return it;
+    }
+    case G_DIAG_TRSM: {
+      const int s = g.step, r = s + 1 + (int)item;
+      it.a_tile = tile(g.j, g.j);
+      it.a_r0 = r * cb;
+      it.a_k0 = s * cb;
+      it.a = g.A + it.a_tile * bb + (int64_t)it.a_r0 * b + it.a_k0;
+      it.K = cb;
+      it.b_tile = g.j * f + s;
+      it.bp = g.W + it.b_tile * cb * cb;
+      it.ldb = cb;
+      it.c = sub(it.a_tile, r, s);
+      it.op = 1;
+      return it;
+    }
+    case G_DIAG_UPD: {
+      const int s = g.step;
+      const int ii = (int)tile_row(item), cc = (int)(item - tri(ii, 0));
+      const int r = s + 1 + ii, c = s + 1 + cc;
+      it.a_tile = it.b_tile = tile(g.j, g.j);
+      it.a_r0 = r * cb;
+      it.b_r0 = c * cb;
+      it.a_k0 = it.b_k0 = s * cb;
+      it.a = g.A + it.a_tile * bb + (int64_t)it.a_r0 * b + it.a_k0;
+      it.bp = g.A + it.b_tile * bb + (int64_t)it.b_r0 * b + it.b_k0;
+      it.K = cb;
+      it.c = sub(it.a_tile, r, c);
+      it.lower = (r == c);
+      return it;
+    }
+    case G_TRSM_X: {  // SIMT path only (f == 1)
+      const int64_t i = g.j + 1 + item;
+      it.a = g.A + tile(i, g.j) * bb;
+      it.bp = g.W + g.j * bb;
+      it.K = b;
+      it.c = g.Xout + (i - g.j - 1) * bb;
+      it.op = 1;
+      return it;
+    }
+    default: {  // G_BATCH
+      const int64_t t = item / (f * f);
+      const int sb = (int)(item % (f * f));
+      const int mb = sb / f, nb = sb % f;
+      it.a = g.P + t * bb + (int64_t)mb * cb * b;
+      it.bp = g.Q + t * bb + (int64_t)nb * cb * b;
+      it.a_tile = it.b_tile = t;
+      it.a_r0 = mb * cb;
+      it.b_r0 = nb * cb;
+      it.K = b;
+      it.c = g.C + t * bb + (int64_t)mb * cb * b + (int64_t)nb * cb;
+      it.lower = g.lower_only && mb == nb;
+      it.skip = g.lower_only && nb > mb;
+      return it;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
-// DMMA tile GEMM (b % 128 == 0), TMA-fed.
+// DMMA sub-block GEMM (cb = 128), TMA-fed.
 
-constexpr int GBM = 128, GBN = 128, GKS = 32, GSTAGES = 3;
+constexpr int GBM = 128, GKS = 32, GSTAGES = 3;
 constexpr int G_OPERAND_BYTES = GBM * GKS * 8;        // 32 KB
 constexpr int G_STAGE_BYTES = 2 * G_OPERAND_BYTES;    // A + B
 constexpr int G_SMEM = GSTAGES * G_STAGE_BYTES + 1024 + 64;
@@ -374,13 +462,9 @@ __global__ void __launch_bounds__(288, 1)
     gemm_dmma_kernel(const __grid_constant__ CUtensorMap mapA,
                      const __grid_constant__ CUtensorMap mapB, GemmArgs g) {
   if (g.flag && g.flag->status) return;
-  const int per = g.tpd * g.tpd;
-  const int64_t item = blockIdx.x / per;
-  const int sub = (int)(blockIdx.x % per);
-  const int mb = sub / g.tpd, nb = sub % g.tpd;
-  const GemmItem it = decode_item(g, item, mb, nb);
+  const GemmItem it = decode_item(g, blockIdx.x);
   if (it.skip) return;
-  const int nks = it.kmax / GKS;
+  const int nks = it.K / GKS;
 
   extern __shared__ __align__(1024) unsigned char gsm_raw[];
   unsigned char* gsm = reinterpret_cast<unsigned char*>(
@@ -399,19 +483,18 @@ __global__ void __launch_bounds__(288, 1)
 
   if (warp == 8) {
     if (lane == 0) {
-      const int arow = mb * GBM, brow = nb * GBN;
       for (int ks = 0; ks < nks; ++ks) {
         const int st = ks % GSTAGES;
         if (ks >= GSTAGES) mbar_wait(&empty[st], ((ks / GSTAGES) - 1) & 1);
         unsigned char* sa = gsm + st * G_STAGE_BYTES;
         unsigned char* sb = sa + G_OPERAND_BYTES;
         mbar_arrive_expect_tx(&full[st], G_STAGE_BYTES);
-        const int k0 = ks * GKS;
-        tma_load_3d(sa, &mapA, k0, arow, (int)it.a_tile, &full[st]);
-        tma_load_3d(sa + G_OPERAND_BYTES / 2, &mapA, k0 + 16, arow,
+        const int ka = it.a_k0 + ks * GKS, kb = it.b_k0 + ks * GKS;
+        tma_load_3d(sa, &mapA, ka, it.a_r0, (int)it.a_tile, &full[st]);
+        tma_load_3d(sa + G_OPERAND_BYTES / 2, &mapA, ka + 16, it.a_r0,
                     (int)it.a_tile, &full[st]);
-        tma_load_3d(sb, &mapB, k0, brow, (int)it.b_tile, &full[st]);
-        tma_load_3d(sb + G_OPERAND_BYTES / 2, &mapB, k0 + 16, brow,
+        tma_load_3d(sb, &mapB, kb, it.b_r0, (int)it.b_tile, &full[st]);
+        tma_load_3d(sb + G_OPERAND_BYTES / 2, &mapB, kb + 16, it.b_r0,
                     (int)it.b_tile, &full[st]);
       }
     }
@@ -452,15 +535,40 @@ __global__ void __launch_bounds__(288, 1)
     if (lane == 0) mbar_arrive(&empty[st]);
   }
 
-  // epilogue: C rows (mb*128 + wm*32 + x*8 + fr), cols (nb*128 + wn*64 +
-  // y*8 + 2*fk + {0,1})
+  // epilogue: sub-block rows (wm*32 + x*8 + fr), cols (wn*64 + y*8 + 2*fk)
   const int b = g.b;
+  if (it.op == 0 && !it.lower) {
+    // C -= acc through the TMA engine: stage -acc row-major in the (now free)
+    // stage buffers, then one bulk reduce-add per 1-KB row. The L2 performs
+    // the read-modify-write; no register-held HBM round trips.
+    named_bar_sync(1, 256);  // every MMA warp is done with the stage buffers
+    constexpr int RS = GBM * 8 + 16;  // padded smem row stride (bytes)
+    unsigned char* tile = gsm;
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int row = wm * 32 + x * 8 + fr;
+#pragma unroll
+      for (int y = 0; y < 8; ++y) {
+        const int col = wn * 64 + y * 8 + 2 * fk;
+        *reinterpret_cast<double2*>(tile + row * RS + col * 8) =
+            make_double2(-acc[x][y][0], -acc[x][y][1]);
+      }
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(1, 256);
+    if (tid < GBM) {
+      bulk_reduce_add_f64(it.c + (int64_t)tid * b, tile + tid * RS, GBM * 8);
+      bulk_commit_group();
+      bulk_wait_group_read0();
+    }
+    return;
+  }
 #pragma unroll
   for (int x = 0; x < 4; ++x) {
-    const int row = mb * GBM + wm * 32 + x * 8 + fr;
+    const int row = wm * 32 + x * 8 + fr;
 #pragma unroll
     for (int y = 0; y < 8; ++y) {
-      const int col = nb * GBN + wn * 64 + y * 8 + 2 * fk;
+      const int col = wn * 64 + y * 8 + 2 * fk;
       double2* p = reinterpret_cast<double2*>(it.c + (int64_t)row * b + col);
       if (it.op == 1) {
         *p = make_double2(acc[x][y][0], acc[x][y][1]);
@@ -477,21 +585,22 @@ __global__ void __launch_bounds__(288, 1)
 }
 
 // ---------------------------------------------------------------------------
-// SIMT FP64 tile GEMM (any b): 64 x 64 CTA tile, 4 x 4 per thread, K chunks
-// of 16 staged in shared memory.
+// SIMT FP64 sub-block GEMM (any cb): 64 x 64 CTA tiles over each item's
+// cb x cb output, 4 x 4 per thread, K chunks of 16 staged in shared memory.
+// Used only where cb % 128 != 0 (small / odd tile sizes), never in place
+// across CTAs (G_TRSM_X writes the panel buffer).
 
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
   if (g.flag && g.flag->status) return;
-  const int b = g.b;
-  const int tpd = (b + 63) / 64;
+  const int cb = g.cb;
+  const int tpd = (cb + 63) / 64;
   const int per = tpd * tpd;
   const int64_t item = blockIdx.x / per;
   const int sub = (int)(blockIdx.x % per);
-  const int mb = sub / tpd, nb = sub % tpd;
-  GemmItem it = decode_item(g, item, mb, nb);
-  // recompute skip / kmax at 64 granularity
-  if (it.lower && nb > mb) return;
-  if (g.mode == G_TRSM) it.kmax = min(b, (nb + 1) * 64);
+  const int sm = sub / tpd, sn = sub % tpd;
+  const GemmItem it = decode_item(g, item);
+  if (it.skip) return;
+  if (it.lower && sn > sm) return;
   __shared__ double As[16][65], Bs[16][65];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   double acc[4][4];
@@ -499,13 +608,13 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
   for (int x = 0; x < 4; ++x)
 #pragma unroll
     for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
-  const int m0 = mb * 64, n0 = nb * 64;
-  for (int k0 = 0; k0 < it.kmax; k0 += 16) {
+  const int m0 = sm * 64, n0 = sn * 64;
+  for (int k0 = 0; k0 < it.K; k0 += 16) {
     for (int idx = threadIdx.x; idx < 64 * 16; idx += 256) {
       const int r = idx / 16, k = idx % 16;
       const int gr = m0 + r, gn = n0 + r, gk = k0 + k;
-      As[k][r] = (gr < b && gk < it.kmax) ? it.a[(int64_t)gr * b + gk] : 0.0;
-      Bs[k][r] = (gn < b && gk < it.kmax) ? it.bt[(int64_t)gn * b + gk] : 0.0;
+      As[k][r] = (gr < cb && gk < it.K) ? it.a[(int64_t)gr * it.lda + gk] : 0.0;
+      Bs[k][r] = (gn < cb && gk < it.K) ? it.bp[(int64_t)gn * it.ldb + gk] : 0.0;
     }
     __syncthreads();
 #pragma unroll
@@ -522,12 +631,13 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
     }
     __syncthreads();
   }
+  const int b = g.b;
 #pragma unroll
   for (int x = 0; x < 4; ++x)
 #pragma unroll
     for (int y = 0; y < 4; ++y) {
       const int row = m0 + ty * 4 + x, col = n0 + tx * 4 + y;
-      if (row >= b || col >= b) continue;
+      if (row >= cb || col >= cb) continue;
       if (it.lower && col > row) continue;
       double* p = it.c + (int64_t)row * b + col;
       if (it.op == 1) *p = acc[x][y];
@@ -536,9 +646,182 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
 }
 
 // ---------------------------------------------------------------------------
+// diag128: POTRF + in-place TRTRI of one 128 x 128 diagonal sub-block held
+// entirely in shared memory (512 threads), blocked in 32-wide panels so the
+// CTA synchronises only a few times per panel:
+//   factor, per panel p: warp 0 factors the 32x32 diagonal block; one thread
+//     per row solves the panel rows below (x L^T = a, 32 registers); 4x4
+//     register tiles apply the rank-32 update to the trailing triangle.
+//   invert, panels right to left (LAPACK trtri order): one lane per column
+//     inverts the 32x32 diagonal block; T = W_trail L_panel (scratch);
+//     W_panel = -T W_pp.
+// mode 0: factor + invert (the factorization's diagonal step; L is written
+// back in place); mode 1: invert only (triangular solves on an uploaded
+// factor; zero / NaN diagonal -> singular_block). W = L^-1 (zeros above the
+// diagonal) goes to W + J*128^2.
+
+constexpr int DCB = 128, DLD = 129, DPB = 32;
+constexpr size_t kDiagSmemBytes = (size_t)(DCB * DLD + (DCB - DPB) * (DPB + 1)) * 8;
+
+__global__ void __launch_bounds__(512)
+    diag128_kernel(double* A, int64_t tile_lo, int b, int f, double* W,
+                   int64_t J0, int mode, CholFlag* flag) {
+  if (flag->status) return;
+  const int64_t J = J0 + blockIdx.x;
+  const int64_t j = J / f;
+  const int sblk = (int)(J % f);
+  double* D = A + (tri(j, j) - tile_lo) * (int64_t)b * b + (int64_t)sblk * DCB * b +
+              sblk * DCB;
+  extern __shared__ double S[];       // [128][129]
+  double* Tm = S + DCB * DLD;         // [96][33] scratch
+  __shared__ int bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < DCB * DCB; idx += blockDim.x) {
+    const int r = idx >> 7, c = idx & 127;
+    S[r * DLD + c] = c <= r ? D[(int64_t)r * b + c] : 0.0;
+  }
+  if (tid == 0) bad = DCB;
+  __syncthreads();
+
+  if (mode == 0) {
+    for (int p = 0; p < DCB / DPB; ++p) {
+      const int o = p * DPB;
+      if (warp == 0) {
+        for (int k = 0; k < DPB; ++k) {
+          double d = S[(o + k) * DLD + o + k];
+          if (!(d > 0.0)) {
+            if (lane == 0) bad = o + k;
+            break;
+          }
+          d = sqrt(d);
+          __syncwarp();
+          if (lane == k) S[(o + k) * DLD + o + k] = d;
+          if (lane > k) S[(o + lane) * DLD + o + k] /= d;
+          __syncwarp();
+          if (lane > k) {
+            const double lr = S[(o + lane) * DLD + o + k];
+            for (int c = k + 1; c <= lane; ++c)
+              S[(o + lane) * DLD + o + c] =
+                  fma(-lr, S[(o + c) * DLD + o + k], S[(o + lane) * DLD + o + c]);
+          }
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      if (bad < DCB) {
+        if (tid == 0) raise_flag(flag, HS_ERR_NOT_SPD, j, (int64_t)sblk * DCB + bad);
+        return;
+      }
+      const int q0 = o + DPB, m = DCB - q0;
+      // panel rows below: x L_pp^T = a
+      for (int r = tid; r < m; r += blockDim.x) {
+        double* row = S + (q0 + r) * DLD + o;
+        double x[DPB];
+#pragma unroll
+        for (int c = 0; c < DPB; ++c) x[c] = row[c];
+#pragma unroll
+        for (int c = 0; c < DPB; ++c) {
+          double acc = x[c];
+#pragma unroll
+          for (int k = 0; k < c; ++k) acc = fma(-x[k], S[(o + c) * DLD + o + k], acc);
+          x[c] = acc / S[(o + c) * DLD + o + c];
+        }
+#pragma unroll
+        for (int c = 0; c < DPB; ++c) row[c] = x[c];
+      }
+      __syncthreads();
+      // trailing rank-32 update of the lower triangle, 4x4 register tiles
+      const int mt = m / 4, ntile = mt * (mt + 1) / 2;
+      for (int u = tid; u < ntile; u += blockDim.x) {
+        const int ti = (int)tile_row(u), tj = u - (int)tri(ti, 0);
+        const int r0 = q0 + ti * 4, c0 = q0 + tj * 4;
+        double acc[4][4] = {};
+#pragma unroll 8
+        for (int k = 0; k < DPB; ++k) {
+          double a4[4], b4[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            a4[x] = S[(r0 + x) * DLD + o + k];
+            b4[x] = S[(c0 + x) * DLD + o + k];
+          }
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) acc[x][y] = fma(a4[x], b4[y], acc[x][y]);
+        }
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y)
+            if (c0 + y <= r0 + x) S[(r0 + x) * DLD + c0 + y] -= acc[x][y];
+      }
+      __syncthreads();
+    }
+    for (int idx = tid; idx < DCB * DCB; idx += blockDim.x) {
+      const int r = idx >> 7, c = idx & 127;
+      if (c <= r) D[(int64_t)r * b + c] = S[r * DLD + c];
+    }
+  } else {
+    for (int r = tid; r < DCB; r += blockDim.x) {
+      const double d = S[r * DLD + r];
+      if (d == 0.0 || isnan(d)) atomicMin(&bad, r);
+    }
+    __syncthreads();
+    if (bad < DCB) {
+      if (tid == 0) raise_flag(flag, HS_ERR_SINGULAR_BLOCK, j, (int64_t)sblk * DCB + bad);
+      return;
+    }
+  }
+
+  // blocked in-place inverse, panels right to left
+  for (int p = DCB / DPB - 1; p >= 0; --p) {
+    const int o = p * DPB, q0 = o + DPB, m = DCB - q0;
+    // (1) T = W_trail L_panel  (W_trail already inverted in place, lower)
+    for (int idx = tid; idx < m * DPB; idx += blockDim.x) {
+      const int r = idx / DPB, c = idx % DPB;
+      double acc = 0.0;
+      for (int k = 0; k <= r; ++k)
+        acc = fma(S[(q0 + r) * DLD + q0 + k], S[(q0 + k) * DLD + o + c], acc);
+      Tm[r * (DPB + 1) + c] = acc;
+    }
+    // (2) lane c inverts column c of the 32x32 diagonal block (registers)
+    if (warp == 0) {
+      double w[DPB];
+#pragma unroll
+      for (int r = 0; r < DPB; ++r) {
+        double acc = (r == lane) ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < r; ++k)
+          if (k >= lane) acc = fma(-S[(o + r) * DLD + o + k], w[k], acc);
+        w[r] = r >= lane ? acc / S[(o + r) * DLD + o + r] : 0.0;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < DPB; ++r)
+        if (r >= lane) S[(o + r) * DLD + o + lane] = w[r];
+    }
+    __syncthreads();
+    // (3) W_panel = -T W_pp  (W_pp lower: k >= c)
+    for (int idx = tid; idx < m * DPB; idx += blockDim.x) {
+      const int r = idx / DPB, c = idx % DPB;
+      double acc = 0.0;
+      for (int k = c; k < DPB; ++k)
+        acc = fma(Tm[r * (DPB + 1) + k], S[(o + k) * DLD + o + c], acc);
+      S[(q0 + r) * DLD + o + c] = -acc;
+    }
+    __syncthreads();
+  }
+  double* Wj = W + J * DCB * DCB;
+  for (int idx = tid; idx < DCB * DCB; idx += blockDim.x) {
+    const int r = idx >> 7, c = idx & 127;
+    Wj[idx] = c <= r ? S[r * DLD + c] : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // small kernels
 
-// A_ij <- X_i for i in (j, N)
+// A_ij <- X_i for i in (j, N)  (SIMT path)
 __global__ void copy_panel_kernel(double* A, int64_t tile_lo, const double* X,
                                   int64_t j, int b, const CholFlag* flag) {
   if (flag->status) return;
@@ -546,99 +829,100 @@ __global__ void copy_panel_kernel(double* A, int64_t tile_lo, const double* X,
   const int64_t bb = (int64_t)b * b;
   const double* src = X + (i - j - 1) * bb;
   double* dst = A + (tri(i, j) - tile_lo) * bb;
-  if ((bb & 1) == 0) {
-    const double2* s2 = reinterpret_cast<const double2*>(src);
-    double2* d2 = reinterpret_cast<double2*>(dst);
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < bb / 2;
-         k += (int64_t)gridDim.x * blockDim.x)
-      d2[k] = s2[k];
-  } else {
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < bb;
-         k += (int64_t)gridDim.x * blockDim.x)
-      dst[k] = src[k];
-  }
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < bb;
+       k += (int64_t)gridDim.x * blockDim.x)
+    dst[k] = src[k];
 }
 
-// NaN/Inf scan of the lower triangles (cholesky_solver.cpp:222-238)
+// NaN/Inf scan of the lower triangles (cholesky_solver.cpp:222-238): one
+// warp per tile row, lanes over columns, no divisions in the inner loop.
 __global__ void check_finite_kernel(const double* A, int64_t tile_lo,
                                     int64_t ntiles, int b, CholFlag* flag) {
   const int64_t bb = (int64_t)b * b;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  bool badv = false;
+  int64_t bad_t = 0;
+  for (int64_t w = warp; w < ntiles * b; w += nwarps) {
+    const int64_t t = w / b;
+    const int r = (int)(w - t * b);
     const int64_t gt = tile_lo + t;
-    const int64_t i = tile_row(gt), j = gt - tri(i, 0);
-    const double* blk = A + t * bb;
-    for (int idx = threadIdx.x; idx < bb; idx += blockDim.x) {
-      const int r = idx / b, c = idx % b;
-      if (i == j && c > r) continue;
-      if (!isfinite(blk[idx])) raise_flag(flag, HS_ERR_NUMERICAL, i, j);
-    }
+    const int64_t i = tile_row(gt);
+    const bool diag = (gt - tri(i, 0)) == i;
+    const int cols = diag ? r + 1 : b;
+    const double* row = A + t * bb + (int64_t)r * b;
+    for (int c = lane; c < cols; c += 32)
+      if (!isfinite(row[c])) {
+        badv = true;
+        bad_t = gt;
+      }
+  }
+  if (badv) {
+    const int64_t i = tile_row(bad_t);
+    raise_flag(flag, HS_ERR_NUMERICAL, i, bad_t - tri(i, 0));
   }
 }
 
-// ---- triangular solves with the stored inverses ---------------------------
-// forward row i: s = v_i - sum_{j<i} L_ij v_j ; v_i = W_i s
-// back row i:    s = v_i - sum_{j>i} L_ji^T v_j ; v_i = W_i^T s
-// Stage 1: CTA (tile jj, 32-row/col chunk) writes a partial; stage 2 sums
-// partials in fixed order and applies the inverse.
+// ---- triangular solves on cb-blocks with the stored inverses --------------
+// Sub-row I covers vector entries [I cb, (I+1) cb); sub-block (I, J) lives in
+// tile (I / f, J / f) at rows (I % f) cb, cols (J % f) cb.
+// forward: s = v_I - sum_{J<I} L_IJ v_J ; v_I = W_I s
+// back:    s = v_I - sum_{J>I} L_JI^T v_J ; v_I = W_I^T s
+
+__device__ __forceinline__ const double* subblock(const double* A, int64_t tile_lo,
+                                                  int b, int cb, int f, int64_t I,
+                                                  int64_t J) {
+  const int64_t ti = I / f, tj = J / f;
+  return A + (tri(ti, tj) - tile_lo) * (int64_t)b * b + (int64_t)(I % f) * cb * b +
+         (int64_t)(J % f) * cb;
+}
 
 __global__ void trsv_partial_kernel(const double* A, int64_t tile_lo,
-                                    const double* v, int b, int64_t i,
-                                    int upper, double* part,
-                                    const CholFlag* flag) {
-  if (flag && flag->status) return;
-  const int64_t jj = blockIdx.y;  // j index among the contributing tiles
-  const int chunk = blockIdx.x;   // 32 outputs
-  const int64_t bb = (int64_t)b * b;
+                                    const double* v, int b, int cb, int f,
+                                    int64_t I, int upper, double* part) {
+  const int64_t jj = blockIdx.y;
+  const int chunk = blockIdx.x;  // 32 outputs
   __shared__ double vs[1024];
   __shared__ double red[8][33];
-  int64_t tile, vj;
-  if (!upper) {
-    tile = tri(i, jj);
-    vj = jj;
-  } else {
-    tile = tri(i + 1 + jj, i);
-    vj = i + 1 + jj;
-  }
-  const double* T = A + (tile - tile_lo) * bb;
-  for (int k = threadIdx.x; k < b; k += blockDim.x) vs[k] = v[vj * b + k];
+  const int64_t J = upper ? I + 1 + jj : jj;
+  const double* T = upper ? subblock(A, tile_lo, b, cb, f, J, I)
+                          : subblock(A, tile_lo, b, cb, f, I, J);
+  for (int k = threadIdx.x; k < cb; k += blockDim.x) vs[k] = v[J * cb + k];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int o0 = chunk * 32;
   if (!upper) {
-    // outputs r in [o0, o0+32): sum_c T[r][c] vs[c]; warp w takes rows
     for (int rr = warp; rr < 32; rr += 8) {
       const int r = o0 + rr;
       double acc = 0.0;
-      if (r < b)
-        for (int c = lane; c < b; c += 32) acc = fma(T[(int64_t)r * b + c], vs[c], acc);
+      if (r < cb)
+        for (int c = lane; c < cb; c += 32) acc = fma(T[(int64_t)r * b + c], vs[c], acc);
       for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-      if (lane == 0 && r < b) part[jj * b + r] = acc;
+      if (lane == 0 && r < cb) part[jj * cb + r] = acc;
     }
   } else {
-    // outputs c in [o0, o0+32): sum_r T[r][c] vs[r]; lane = column
     const int c = o0 + lane;
     double acc = 0.0;
-    if (c < b)
-      for (int r = warp; r < b; r += 8) acc = fma(T[(int64_t)r * b + c], vs[r], acc);
+    if (c < cb)
+      for (int r = warp; r < cb; r += 8) acc = fma(T[(int64_t)r * b + c], vs[r], acc);
     red[warp][lane] = acc;
     __syncthreads();
-    if (warp == 0 && c < b) {
-      double s = 0.0;
-      for (int w = 0; w < 8; ++w) s += red[w][lane];
-      part[jj * b + c] = s;
+    if (warp == 0 && c < cb) {
+      double s2 = 0.0;
+      for (int w = 0; w < 8; ++w) s2 += red[w][lane];
+      part[jj * cb + c] = s2;
     }
   }
 }
 
 __global__ void trsv_apply_kernel(const double* W, const double* rhs, double* v,
-                                  int b, int64_t i, int upper,
-                                  const double* part, int64_t nparts,
-                                  const CholFlag* flag) {
-  if (flag && flag->status) return;
+                                  int cb, int64_t I, int upper,
+                                  const double* part, int64_t nparts) {
   __shared__ double s[1024];
-  for (int k = threadIdx.x; k < b; k += blockDim.x) {
-    double acc = rhs[i * b + k];
-    for (int64_t p = 0; p < nparts; ++p) acc -= part[p * b + k];
+  for (int k = threadIdx.x; k < cb; k += blockDim.x) {
+    double acc = rhs[I * cb + k];
+    for (int64_t p = 0; p < nparts; ++p) acc -= part[p * cb + k];
     s[k] = acc;
   }
   __syncthreads();
@@ -648,25 +932,24 @@ __global__ void trsv_apply_kernel(const double* W, const double* rhs, double* v,
   if (!upper) {
     for (int rr = warp; rr < 32; rr += nw) {
       const int r = o0 + rr;
-      if (r >= b) break;
+      if (r >= cb) break;
       double acc = 0.0;
-      for (int c = lane; c <= r; c += 32) acc = fma(W[(int64_t)r * b + c], s[c], acc);
+      for (int c = lane; c <= r; c += 32) acc = fma(W[(int64_t)r * cb + c], s[c], acc);
       for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-      if (lane == 0) v[i * b + r] = acc;
+      if (lane == 0) v[I * cb + r] = acc;
     }
   } else {
-    // (W^T s)[c] = sum_{r >= c} W[r][c] s[r]
     __shared__ double red[32][33];
     const int c = o0 + lane;
     double acc = 0.0;
-    if (c < b)
-      for (int r = c + warp; r < b; r += nw) acc = fma(W[(int64_t)r * b + c], s[r], acc);
+    if (c < cb)
+      for (int r = c + warp; r < cb; r += nw) acc = fma(W[(int64_t)r * cb + c], s[r], acc);
     red[warp][lane] = acc;
     __syncthreads();
-    if (warp == 0 && c < b) {
+    if (warp == 0 && c < cb) {
       double t = 0.0;
       for (int w = 0; w < nw; ++w) t += red[w][lane];
-      v[i * b + c] = t;
+      v[I * cb + c] = t;
     }
   }
 }
@@ -695,12 +978,12 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 3-D map over `ntiles` contiguous b x b tiles: box 16 (k) x 128 (rows) x 1.
-static CUtensorMap tile_map(const double* base, int b, int64_t ntiles) {
+// 3-D map over `ntiles` contiguous side x side tiles: box 16 (k) x 128 x 1.
+static CUtensorMap tile_map(const double* base, int side, int64_t ntiles) {
   CUtensorMap m;
-  cuuint64_t dims[3] = {(cuuint64_t)b, (cuuint64_t)b,
+  cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)side,
                         (cuuint64_t)std::max<int64_t>(ntiles, 1)};
-  cuuint64_t strides[2] = {(cuuint64_t)b * 8, (cuuint64_t)b * b * 8};
+  cuuint64_t strides[2] = {(cuuint64_t)side * 8, (cuuint64_t)side * side * 8};
   cuuint32_t box[3] = {16, 128, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
@@ -714,12 +997,13 @@ static CUtensorMap tile_map(const double* base, int b, int64_t ntiles) {
 }
 
 static bool dmma_ok(int b) { return b % 128 == 0; }
+static int compute_block(int b) { return dmma_ok(b) ? 128 : b; }
 
 static void launch_gemm(hs_ctx* c, cudaStream_t s, const GemmArgs& g,
                         int64_t items, const CUtensorMap* ma,
                         const CUtensorMap* mb) {
   if (items <= 0) return;
-  if (dmma_ok(g.b) && ma && mb) {
+  if (g.cb == 128 && ma && mb) {
     static bool attr = false;
     if (!attr) {
       HS_CUDA(cudaFuncSetAttribute(gemm_dmma_kernel,
@@ -727,12 +1011,10 @@ static void launch_gemm(hs_ctx* c, cudaStream_t s, const GemmArgs& g,
                                    G_SMEM));
       attr = true;
     }
-    const int64_t grid = items * g.tpd * g.tpd;
-    gemm_dmma_kernel<<<(unsigned)grid, 288, G_SMEM, s>>>(*ma, *mb, g);
+    gemm_dmma_kernel<<<(unsigned)items, 288, G_SMEM, s>>>(*ma, *mb, g);
   } else {
-    const int tpd = (g.b + 63) / 64;
-    const int64_t grid = items * tpd * tpd;
-    gemm_simt_kernel<<<(unsigned)grid, 256, 0, s>>>(g);
+    const int tpd = (g.cb + 63) / 64;
+    gemm_simt_kernel<<<(unsigned)(items * tpd * tpd), 256, 0, s>>>(g);
   }
   HS_CUDA(cudaGetLastError());
   launch_count(c);
@@ -740,10 +1022,24 @@ static void launch_gemm(hs_ctx* c, cudaStream_t s, const GemmArgs& g,
 
 static size_t potrf_smem(int b) { return (size_t)(PNB * PLD + b * PLD) * 8; }
 static size_t trtri_smem(int b) { return (size_t)(PNB * PLD + PNB * b) * 8; }
+static const size_t kDiagSmem = kDiagSmemBytes;
+
+static void set_simt_tile_attrs(int b);
 
 static void set_tile_kernel_attrs(int b) {
+  if (dmma_ok(b)) {
+    HS_CUDA(cudaFuncSetAttribute(diag128_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kDiagSmem));
+    return;
+  }
+  set_simt_tile_attrs(b);
+}
+
+static void set_simt_tile_attrs(int b) {
   HS_REQUIRE(potrf_smem(b) <= 227 * 1024 && trtri_smem(b) <= 227 * 1024,
-             HS_ERR_CONFIG, "block size too large for the tile kernels (max 768)");
+             HS_ERR_CONFIG,
+             "block size not a multiple of 128 must be <= 640 for the tile kernels");
   HS_CUDA(cudaFuncSetAttribute(potrf_tile_kernel,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)potrf_smem(b)));
@@ -774,15 +1070,42 @@ static double ms_since(std::chrono::steady_clock::time_point t0) {
       .count();
 }
 
+static void throw_flag(const CholFlag& h) {
+  if (h.status == HS_ERR_NOT_SPD)
+    throw Failure{HS_ERR_NOT_SPD,
+                  "matrix is not positive definite (block row " +
+                      std::to_string(h.col) + ", pivot " + std::to_string(h.pivot) + ")",
+                  h.col, h.pivot};
+  if (h.status == HS_ERR_NUMERICAL)
+    throw Failure{HS_ERR_NUMERICAL,
+                  "factor has a non-finite value in block (" + std::to_string(h.col) +
+                      ", " + std::to_string(h.pivot) + ")",
+                  h.col, h.pivot};
+  if (h.status == HS_ERR_SINGULAR_BLOCK)
+    throw Failure{HS_ERR_SINGULAR_BLOCK,
+                  "triangular block has zero or NaN diagonal at index " +
+                      std::to_string(h.pivot),
+                  h.col, h.pivot};
+  if (h.status != HS_OK) throw Failure{h.status, "factorization failed", h.col, h.pivot};
+}
+
+static void alloc_inverses(hs_matrix* m) {
+  const int cb = compute_block((int)m->b);
+  const int64_t nblk = (int64_t)m->N * ((int64_t)m->b / cb);
+  if (!m->dinv) HS_CUDA(cudaMalloc(&m->dinv, nblk * cb * cb * sizeof(double)));
+}
+
 // In-place factorization of a single-rank matrix.
 static void potrf_run(hs_ctx* c, hs_matrix* m) {
   HS_REQUIRE(c->world == 1, HS_ERR_CONFIG,
              "multi-GPU Cholesky is not available in this build");
   const int b = (int)m->b;
+  const int cb = compute_block(b), f = b / cb;
+  const bool fast = dmma_ok(b);
   const int64_t N = (int64_t)m->N;
   const int64_t bb = (int64_t)b * b;
   set_tile_kernel_attrs(b);
-  if (!m->dinv) HS_CUDA(cudaMalloc(&m->dinv, N * bb * sizeof(double)));
+  alloc_inverses(m);
   m->has_inv = false;
   CholFlag* flag = nullptr;
   double* X[2] = {nullptr, nullptr};
@@ -797,8 +1120,10 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
     }
   } guard{flag, X};
   const int64_t panel = std::max<int64_t>(N - 1, 1);
-  HS_CUDA(cudaMalloc(&X[0], panel * bb * sizeof(double)));
-  HS_CUDA(cudaMalloc(&X[1], panel * bb * sizeof(double)));
+  if (!fast) {
+    HS_CUDA(cudaMalloc(&X[0], panel * bb * sizeof(double)));
+    HS_CUDA(cudaMalloc(&X[1], panel * bb * sizeof(double)));
+  }
   HS_CUDA(cudaMemsetAsync(flag, 0, sizeof(CholFlag), c->stream));
 
   ColStreams cs;
@@ -811,45 +1136,72 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
   HS_CUDA(cudaStreamWaitEvent(cs.p, start));
   HS_CUDA(cudaStreamWaitEvent(cs.u, start));
 
-  const bool fast = dmma_ok(b);
-  CUtensorMap mapA{}, mapX[2]{};
+  CUtensorMap mapA{}, mapW{};
   if (fast) {
     mapA = tile_map(m->d, b, (int64_t)m->local_tiles());
-    mapX[0] = tile_map(X[0], b, panel);
-    mapX[1] = tile_map(X[1], b, panel);
+    mapW = tile_map(m->dinv, cb, N * f);
   }
 
   GemmArgs g{};
   g.N = N;
   g.b = b;
-  g.tpd = b / 128;
+  g.cb = cb;
+  g.f = f;
   g.A = m->d;
   g.tile_lo = m->tile_lo;
+  g.W = m->dinv;
   g.flag = flag;
 
-  // P-stream work for column j: potrf, trtri, trsm into X[j&1], copy back.
+  // P-stream work for column j: diagonal tile, then the panel below it.
   auto panel_work = [&](int64_t j) {
+    const int64_t t = N - 1 - j;
+    if (fast) {
+      for (int s = 0; s < f; ++s) {
+        diag128_kernel<<<1, 512, kDiagSmem, cs.p>>>(m->d, m->tile_lo, b, f, m->dinv,
+                                                    j * f + s, 0, flag);
+        HS_CUDA(cudaGetLastError());
+        launch_count(c);
+        if (s + 1 < f) {
+          GemmArgs gd = g;
+          gd.j = j;
+          gd.step = s;
+          gd.mode = G_DIAG_TRSM;
+          launch_gemm(c, cs.p, gd, f - 1 - s, &mapA, &mapW);
+          gd.mode = G_DIAG_UPD;
+          const int64_t tt = f - 1 - s;
+          launch_gemm(c, cs.p, gd, tt * (tt + 1) / 2, &mapA, &mapA);
+        }
+      }
+      for (int cc = 0; cc < f && t > 0; ++cc) {
+        GemmArgs gp = g;
+        gp.j = j;
+        gp.step = cc;
+        if (cc > 0) {
+          gp.mode = G_PANEL_UPD;
+          launch_gemm(c, cs.p, gp, t * f, &mapA, &mapA);
+        }
+        gp.mode = G_PANEL_TRSM;
+        launch_gemm(c, cs.p, gp, t * f, &mapA, &mapW);
+      }
+      return;
+    }
+    // SIMT path (b % 128 != 0): single-CTA tile kernels, panel via buffer
     double* djj = m->d + (tri(j, j) - m->tile_lo) * bb;
-    double* wj = m->dinv + j * bb;
     potrf_tile_kernel<<<1, 256, potrf_smem(b), cs.p>>>(djj, 0, b, flag, j);
     HS_CUDA(cudaGetLastError());
-    trtri_tile_kernel<<<1, 256, trtri_smem(b), cs.p>>>(djj, 0, wj, b, flag, j);
+    trtri_tile_kernel<<<1, 256, trtri_smem(b), cs.p>>>(m->d, m->tile_lo, m->dinv, b,
+                                                       flag, j);
     HS_CUDA(cudaGetLastError());
     launch_count(c, 2);
-    const int64_t t = N - 1 - j;
     if (t > 0) {
       GemmArgs gt = g;
-      gt.mode = G_TRSM;
+      gt.mode = G_TRSM_X;
       gt.j = j;
-      gt.X = X[j & 1];
-      gt.W = wj;
-      CUtensorMap mw;
-      if (fast) mw = tile_map(wj, b, 1);
-      launch_gemm(c, cs.p, gt, t, fast ? &mapA : nullptr, fast ? &mw : nullptr);
+      gt.Xout = X[j & 1];
+      launch_gemm(c, cs.p, gt, t, nullptr, nullptr);
       dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(64, ceil_div(bb, 512))),
                 (unsigned)t);
-      copy_panel_kernel<<<grid, 256, 0, cs.p>>>(m->d, m->tile_lo, X[j & 1], j, b,
-                                                flag);
+      copy_panel_kernel<<<grid, 256, 0, cs.p>>>(m->d, m->tile_lo, X[j & 1], j, b, flag);
       HS_CUDA(cudaGetLastError());
       launch_count(c);
     }
@@ -864,21 +1216,19 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
     HS_CUDA(cudaStreamWaitEvent(cs.u, pdone));
     GemmArgs gu = g;
     gu.j = j;
-    gu.X = X[j & 1];
-    const CUtensorMap* mx = fast ? &mapX[j & 1] : nullptr;
+    gu.X = fast ? nullptr : X[j & 1];
+    const CUtensorMap* mx = fast ? &mapA : nullptr;
     // lookahead: tile column j+1 first
     gu.mode = G_UPDATE_COL;
-    launch_gemm(c, cs.u, gu, t, mx, mx);
+    launch_gemm(c, cs.u, gu, t * f * f, mx, mx);
     cudaEvent_t ucol = cs.make();
     HS_CUDA(cudaEventRecord(ucol, cs.u));
     HS_CUDA(cudaStreamWaitEvent(cs.p, ucol));
-    // the rest of column j's update overlaps column j+1's panel work; the
-    // panel writes X[(j+1)&1], the update reads X[j&1]
+    // the rest of column j's update overlaps column j+1's panel work (the
+    // panel touches only tile column j+1; the update reads column j)
     gu.mode = G_UPDATE_REST;
     const int64_t tr = t - 1;
-    launch_gemm(c, cs.u, gu, tr * (tr + 1) / 2, mx, mx);
-    // X[(j+1)&1] is about to be overwritten: the update of column j-1 (which
-    // read it) is ordered before this point on cs.u, and P waited on ucol.
+    launch_gemm(c, cs.u, gu, tr * (tr + 1) / 2 * f * f, mx, mx);
     panel_work(j + 1);
   }
   cudaEvent_t pend = cs.make(), uend = cs.make();
@@ -886,57 +1236,42 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
   HS_CUDA(cudaEventRecord(uend, cs.u));
   HS_CUDA(cudaStreamWaitEvent(c->stream, pend));
   HS_CUDA(cudaStreamWaitEvent(c->stream, uend));
-  // check_finite (only when no earlier failure)
-  check_finite_kernel<<<(unsigned)std::min<int64_t>(m->local_tiles(), 4 * 148), 256,
-                        0, c->stream>>>(m->d, m->tile_lo, (int64_t)m->local_tiles(),
-                                        b, flag);
+  check_finite_kernel<<<4 * 148, 256, 0, c->stream>>>(
+      m->d, m->tile_lo, (int64_t)m->local_tiles(), b, flag);
   HS_CUDA(cudaGetLastError());
   launch_count(c);
   CholFlag h{};
   HS_CUDA(cudaMemcpyAsync(&h, flag, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
-  if (h.status == HS_ERR_NOT_SPD)
-    throw Failure{HS_ERR_NOT_SPD,
-                  "matrix is not positive definite (block row " +
-                      std::to_string(h.col) + ", pivot " + std::to_string(h.pivot) + ")",
-                  h.col, h.pivot};
-  if (h.status == HS_ERR_NUMERICAL)
-    throw Failure{HS_ERR_NUMERICAL,
-                  "factor has a non-finite value in block (" + std::to_string(h.col) +
-                      ", " + std::to_string(h.pivot) + ")",
-                  h.col, h.pivot};
-  if (h.status != HS_OK)
-    throw Failure{h.status, "factorization failed", h.col, h.pivot};
+  throw_flag(h);
   m->has_inv = true;
 }
 
-// inverses of all diagonal tiles of an (uploaded) factor; singular check
+// inverses of all diagonal cb-blocks of an (uploaded) factor; singular check
 static void ensure_inverses(hs_ctx* c, hs_matrix* m) {
   if (m->has_inv) return;
   const int b = (int)m->b;
+  const int cb = compute_block(b), f = b / cb;
   const int64_t N = (int64_t)m->N;
-  const int64_t bb = (int64_t)b * b;
   set_tile_kernel_attrs(b);
-  if (!m->dinv) HS_CUDA(cudaMalloc(&m->dinv, N * bb * sizeof(double)));
+  alloc_inverses(m);
   CholFlag* flag = nullptr;
   HS_CUDA(cudaMalloc(&flag, sizeof(CholFlag)));
   HS_CUDA(cudaMemsetAsync(flag, 0, sizeof(CholFlag), c->stream));
-  // diagonal tile j sits at tri(j, j); launch one CTA per tile row j
-  for (int64_t j = 0; j < N; ++j) {
-    trtri_tile_kernel<<<1, 256, trtri_smem(b), c->stream>>>(
-        m->d + (tri(j, j) - m->tile_lo) * bb, 0, m->dinv + j * bb, b, flag, j);
-    HS_CUDA(cudaGetLastError());
+  if (dmma_ok(b)) {
+    diag128_kernel<<<(unsigned)(N * f), 512, kDiagSmem, c->stream>>>(
+        m->d, m->tile_lo, b, f, m->dinv, 0, 1, flag);
+  } else {
+    trtri_tile_kernel<<<(unsigned)N, 256, trtri_smem(b), c->stream>>>(
+        m->d, m->tile_lo, m->dinv, b, flag, 0);
   }
-  launch_count(c, (int)N);
+  HS_CUDA(cudaGetLastError());
+  launch_count(c);
   CholFlag h{};
   HS_CUDA(cudaMemcpyAsync(&h, flag, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
   cudaFree(flag);
-  if (h.status == HS_ERR_SINGULAR_BLOCK)
-    throw Failure{HS_ERR_SINGULAR_BLOCK,
-                  "triangular block has zero or NaN diagonal at index " +
-                      std::to_string(h.pivot),
-                  h.col, h.pivot};
+  throw_flag(h);
   m->has_inv = true;
 }
 
@@ -944,29 +1279,28 @@ static void trsv_run(hs_ctx* c, hs_matrix* m, double* v, bool upper) {
   HS_REQUIRE(c->world == 1, HS_ERR_CONFIG, "triangular solves are single-rank");
   ensure_inverses(c, m);
   const int b = (int)m->b;
-  HS_REQUIRE(b <= 1024, HS_ERR_CONFIG, "block size > 1024 unsupported in trsv");
-  const int64_t N = (int64_t)m->N;
-  const int64_t bb = (int64_t)b * b;
-  // rhs snapshot: the apply step reads row i of it and writes row i of v,
-  // so CTAs of one row never read values another CTA already overwrote
+  const int cb = compute_block(b), f = b / cb;
+  HS_REQUIRE(cb <= 1024, HS_ERR_CONFIG, "block size unsupported in trsv");
+  const int64_t NB = (int64_t)m->N * f;  // cb-sized sub-rows
+  // rhs snapshot: the apply step reads sub-row I of it and writes v, so no
+  // CTA reads a value another CTA of the same step already overwrote
   double *part = nullptr, *rhs = nullptr;
-  HS_CUDA(cudaMalloc(&part, std::max<int64_t>(N, 1) * b * sizeof(double)));
-  HS_CUDA(cudaMalloc(&rhs, N * b * sizeof(double)));
-  HS_CUDA(cudaMemcpyAsync(rhs, v, N * b * sizeof(double),
-                          cudaMemcpyDeviceToDevice, c->stream));
-  const int chunks = (b + 31) / 32;
-  for (int64_t s = 0; s < N; ++s) {
-    const int64_t i = upper ? N - 1 - s : s;
-    const int64_t np = upper ? N - 1 - i : i;
+  HS_CUDA(cudaMalloc(&part, std::max<int64_t>(NB, 1) * cb * sizeof(double)));
+  HS_CUDA(cudaMalloc(&rhs, NB * cb * sizeof(double)));
+  HS_CUDA(cudaMemcpyAsync(rhs, v, NB * cb * sizeof(double), cudaMemcpyDeviceToDevice,
+                          c->stream));
+  const int chunks = (cb + 31) / 32;
+  for (int64_t s = 0; s < NB; ++s) {
+    const int64_t I = upper ? NB - 1 - s : s;
+    const int64_t np = upper ? NB - 1 - I : I;
     if (np > 0) {
       trsv_partial_kernel<<<dim3(chunks, (unsigned)np), 256, 0, c->stream>>>(
-          m->d, m->tile_lo, v, b, i, upper ? 1 : 0, part, nullptr);
+          m->d, m->tile_lo, v, b, cb, f, I, upper ? 1 : 0, part);
       HS_CUDA(cudaGetLastError());
       launch_count(c);
     }
-    trsv_apply_kernel<<<chunks, 256, 0, c->stream>>>(m->dinv + i * bb, rhs, v,
-                                                     b, i, upper ? 1 : 0, part,
-                                                     np, nullptr);
+    trsv_apply_kernel<<<chunks, 256, 0, c->stream>>>(m->dinv + I * cb * cb, rhs, v, cb,
+                                                     I, upper ? 1 : 0, part, np);
     HS_CUDA(cudaGetLastError());
     launch_count(c);
   }
@@ -1198,7 +1532,7 @@ hs_status hs_potf_tiles(hs_ctx* c, double* d_tiles, size_t b, size_t count,
   HS_API_BEGIN
   HS_REQUIRE(c && d_tiles && b > 0, HS_ERR_CONFIG, "bad arguments");
   HS_CUDA(cudaSetDevice(c->device));
-  set_tile_kernel_attrs((int)b);
+  set_simt_tile_attrs((int)b);
   CholFlag* flag = nullptr;
   HS_CUDA(cudaMalloc(&flag, sizeof(CholFlag)));
   HS_CUDA(cudaMemsetAsync(flag, 0, sizeof(CholFlag), c->stream));
@@ -1228,17 +1562,19 @@ hs_status hs_gemm_update_tiles(hs_ctx* c, double* d_c, const double* d_p,
   GemmArgs g{};
   g.mode = G_BATCH;
   g.b = (int)b;
-  g.tpd = (int)b / 128;
+  g.cb = compute_block((int)b);
+  g.f = (int)b / g.cb;
   g.C = d_c;
   g.P = d_p;
   g.Q = d_q;
   g.lower_only = lower_only;
+  const int64_t items = (int64_t)count * g.f * g.f;
   if (dmma_ok((int)b)) {
     CUtensorMap mp = tile_map(d_p, (int)b, (int64_t)count);
     CUtensorMap mq = tile_map(d_q, (int)b, (int64_t)count);
-    launch_gemm(c, c->stream, g, (int64_t)count, &mp, &mq);
+    launch_gemm(c, c->stream, g, items, &mp, &mq);
   } else {
-    launch_gemm(c, c->stream, g, (int64_t)count, nullptr, nullptr);
+    launch_gemm(c, c->stream, g, items, nullptr, nullptr);
   }
   HS_CUDA(cudaStreamSynchronize(c->stream));
   HS_API_END

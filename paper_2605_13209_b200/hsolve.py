@@ -280,6 +280,8 @@ class Runtime:
             _check(self._L.hs_ctx_create(device, C.c_void_p(stream or 0), C.byref(h)))
             self.ctx = h
         self.device = device
+        import weakref
+        self._matrices = weakref.WeakSet()  # freed before the context closes
 
     @classmethod
     def distributed(cls, device: int, rank: int, world: int, nccl_id: bytes,
@@ -314,6 +316,8 @@ class Runtime:
 
     def close(self) -> None:
         if getattr(self, "ctx", None):
+            for m in list(getattr(self, "_matrices", ())):
+                m.free()
             self._L.hs_ctx_destroy(self.ctx)
             self.ctx = None
 
@@ -359,6 +363,7 @@ class DeviceMatrix:
         h = C.c_void_p()
         _check(rt._L.hs_matrix_create(rt.ctx, n, b, C.byref(h)))
         self.h = h
+        rt._matrices.add(self)
         lo, hi = C.c_size_t(), C.c_size_t()
         _check(rt._L.hs_matrix_info(h, None, None, C.byref(lo), C.byref(hi)))
         self.row_lo, self.row_hi = lo.value, hi.value
@@ -397,7 +402,8 @@ class DeviceMatrix:
 
     def free(self) -> None:
         if getattr(self, "h", None):
-            self.rt._L.hs_matrix_destroy(self.h)
+            if self.rt.ctx is not None:  # the context owns the device memory
+                self.rt._L.hs_matrix_destroy(self.h)
             self.h = None
 
     def __del__(self):

@@ -256,8 +256,8 @@ def test_cg_device_resident_matches_host_entry(rt, oracle):
 # (4) Cholesky
 
 
-@pytest.mark.parametrize("n,b", [(1024, 128), (2048, 512), (1000, 256), (256, 32), (100, 16),
-                                 (45, 8), (2, 1)])
+@pytest.mark.parametrize("n,b", [(1024, 128), (2048, 512), (1000, 256), (1200, 384), (256, 32),
+                                 (100, 16), (45, 8), (2, 1), (700, 96)])
 def test_factor_and_solve_match_oracle(rt, oracle, n, b):
     a = oracle.generate_spd(n, b, seed=42)
     rhs = oracle.generate_rhs(n, b, seed=42)
@@ -337,7 +337,16 @@ def test_substitutions(rt, oracle):
         hs.back_substitute(sing, r, rt)
 
 
-@pytest.mark.parametrize("n,b", [(1024, 128), (2048, 512), (200, 16)])
+def test_singular_factor_dmma_path(rt):
+    sing = hs.BlockedSPDMatrix.identity(300, 128)
+    sing.set(130, 130, 0.0)
+    r = hs.BlockVector(300, 128)
+    r[0] = 1.0
+    with pytest.raises(hs.SingularBlockError):
+        hs.forward_substitute(sing, r, rt)
+
+
+@pytest.mark.parametrize("n,b", [(1024, 128), (2048, 512), (200, 16), (1500, 256)])
 def test_substitutions_match_oracle(rt, oracle, n, b):
     a = oracle.generate_spd(n, b, seed=8)
     _, L, _, _ = oracle.factorize(n, b, a)
