@@ -305,6 +305,7 @@ def run_ours(args) -> None:
             dist.barrier()
         torch.cuda.synchronize()
 
+    clocks = ClockSampler(local).__enter__()  # sample warm-up + timed region
     # warm-up: W iterations
     cfgw = hs.SolverConfig(block_size=b, eps=1e-300, max_iters=max(args.warmup, 1))
     hs.solve_cg_device(rt, m, d_rhs.data_ptr(), d_x.data_ptr(), cfgw)
@@ -312,20 +313,20 @@ def run_ours(args) -> None:
     # timed: exactly K iterations in one solve
     cfg = hs.SolverConfig(block_size=b, eps=1e-300, max_iters=args.steps,
                           recompute_interval=50)
-    rt.prof_enable(True)
+    rt.prof_enable(args.prof_every)
     rt.prof_reset()
     launches0 = rt.kernel_launches()
-    with ClockSampler(local) as clocks:
-        barrier()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        st = hs.solve_cg_device(rt, m, d_rhs.data_ptr(), d_x.data_ptr(), cfg)
-        ev1.record()
-        barrier()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    st = hs.solve_cg_device(rt, m, d_rhs.data_ptr(), d_x.data_ptr(), cfg)
+    ev1.record()
+    barrier()
+    clocks.__exit__(None, None, None)
     ms = ev0.elapsed_time(ev1)
     launches = rt.kernel_launches() - launches0
     n_symv, symv_ms = rt.prof_symv()
-    rt.prof_enable(False)
+    rt.prof_enable(0)
     assert st.iterations == args.steps, (st.iterations, args.steps)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -437,8 +438,8 @@ def run_ours(args) -> None:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=32768)
     ap.add_argument("--b", type=int, default=128)
@@ -448,6 +449,8 @@ def main():
     ap.add_argument("--cpu-chol-n", type=int, default=4096)
     ap.add_argument("--cpu-iters", type=int, default=20)
     ap.add_argument("--ref-iters", type=int, default=50)
+    ap.add_argument("--prof-every", type=int, default=8,
+                    help="bracket every k-th SYMV launch of the timed solve with events")
     ap.add_argument("--e2e-iters", type=int, default=50)
     ap.add_argument("--e2e-reps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")

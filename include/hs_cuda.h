@@ -204,9 +204,10 @@ hs_status hs_gemm_update_tiles(hs_ctx* ctx, double* d_c, const double* d_p,
                                int lower_only);
 
 /* ---- profiling hooks (bench.py roofline) ------------------------------- */
-/* When enabled, the CG driver brackets every SYMV launch with CUDA events
- * on the context stream; hs_prof_symv returns (launches, total ms). */
-void hs_prof_enable(hs_ctx* ctx, int on);
+/* every > 0: the CG driver brackets every `every`-th SYMV launch with CUDA
+ * events on the context stream (0 disables); hs_prof_symv returns
+ * (bracketed launches, their total ms). */
+void hs_prof_enable(hs_ctx* ctx, int every);
 void hs_prof_symv(hs_ctx* ctx, uint64_t* launches, double* total_ms);
 void hs_prof_reset(hs_ctx* ctx);
 

@@ -43,7 +43,10 @@ struct SymvCfg {
   static constexpr int W = TPR < 32 ? TPR : 32;  // lanes of a row in a warp
   static constexpr int H = TPR / W;      // warps sharing a row
   static constexpr int NSTAGE = B == 512 ? 4 : 5;
-  static constexpr int STAGE_BYTES = SLAB_BYTES + B * 8 + RS * 8;
+  // slab | seg_j (B) | seg_i (RS) | r_j (B) | r_i (RS); the r segments are
+  // filled only when the s update is fused (s = r + beta s_old on the fly)
+  static constexpr int SEG_BYTES = (B + RS) * 8;
+  static constexpr int STAGE_BYTES = SLAB_BYTES + 2 * SEG_BYTES;
   static constexpr int COLRED_BYTES = RPP * B * 8;
   static constexpr int YROW_BYTES = H * B * 8;
   static constexpr int SMEM = NSTAGE * STAGE_BYTES + 2 * COLRED_BYTES +
@@ -65,6 +68,13 @@ struct SymvArgs {
   double* colextra;       // [grid][B]   a CTA's first tile when it starts
                           //             mid-tile (split tiles)
   const int32_t* done;    // CG early-exit flag (nullable)
+  // fused CG direction update (single rank): the input `s` is s_old and the
+  // kernel multiplies with s = r + beta s_old, which it also stores to s_out
+  // (each entry once, by the slab of its diagonal tile)
+  const double* r;
+  double* s_out;
+  const double* beta;
+  int fuse;
 };
 
 template <int B>
@@ -72,6 +82,8 @@ __global__ void __launch_bounds__(288, 1) symv_slab_kernel(SymvArgs args) {
   using Cfg = SymvCfg<B>;
   constexpr int RS = Cfg::RS, SPT = Cfg::SPT, TPR = Cfg::TPR, RPP = Cfg::RPP;
   constexpr int W = Cfg::W, NS = Cfg::NSTAGE;
+  pdl_wait();
+  pdl_trigger();
   if (args.done && *args.done) return;
 
   extern __shared__ __align__(128) unsigned char smem[];
@@ -109,14 +121,20 @@ __global__ void __launch_bounds__(288, 1) symv_slab_kernel(SymvArgs args) {
         const int st = (int)(k % NS);
         if (k >= NS) mbar_wait(&empty[st], (uint32_t)(((k / NS) - 1) & 1));
         unsigned char* buf = stages + st * Cfg::STAGE_BYTES;
-        mbar_arrive_expect_tx(&full[st], Cfg::STAGE_BYTES);
+        mbar_arrive_expect_tx(&full[st], Cfg::SLAB_BYTES + Cfg::SEG_BYTES *
+                                                               (args.fuse ? 2 : 1));
         const double* src =
             args.a + ((t - args.tile_lo) * B + (int64_t)q * RS) * B;
+        const int64_t oj = args.row_off[j], oi = args.row_off[i] + q * RS;
         bulk_g2s(buf, src, Cfg::SLAB_BYTES, &full[st]);
-        bulk_g2s(buf + Cfg::SLAB_BYTES, args.s + args.row_off[j], B * 8,
-                 &full[st]);
-        bulk_g2s(buf + Cfg::SLAB_BYTES + B * 8,
-                 args.s + args.row_off[i] + q * RS, RS * 8, &full[st]);
+        bulk_g2s(buf + Cfg::SLAB_BYTES, args.s + oj, B * 8, &full[st]);
+        bulk_g2s(buf + Cfg::SLAB_BYTES + B * 8, args.s + oi, RS * 8, &full[st]);
+        if (args.fuse) {
+          bulk_g2s(buf + Cfg::SLAB_BYTES + Cfg::SEG_BYTES, args.r + oj, B * 8,
+                   &full[st]);
+          bulk_g2s(buf + Cfg::SLAB_BYTES + Cfg::SEG_BYTES + B * 8, args.r + oi,
+                   RS * 8, &full[st]);
+        }
         if (++q == SPT) {
           q = 0;
           ++t;
@@ -137,6 +155,8 @@ __global__ void __launch_bounds__(288, 1) symv_slab_kernel(SymvArgs args) {
   const int h = cl / W;      // row-sharing warp index (B = 512)
   const int64_t rseg0 = args.cta_rseg[blockIdx.x];
   const bool split_start = (g0 % SPT) != 0;
+  const bool fuse = args.fuse != 0;
+  const double beta = fuse ? *args.beta : 0.0;
 
   double cacc[8];
 #pragma unroll
@@ -165,7 +185,22 @@ __global__ void __launch_bounds__(288, 1) symv_slab_kernel(SymvArgs args) {
 #pragma unroll
       for (int m = 0; m < 4; ++m)
         a[r][m] = A2[(2 * rl + r) * (B / 2) + cl + TPR * m];
-    const double si0 = si[2 * rl], si1 = si[2 * rl + 1];
+    double si0 = si[2 * rl], si1 = si[2 * rl + 1];
+    if (fuse) {  // s = r + beta s_old  (cg_solver.cpp line 11, xpay_range)
+      const double2* rj2 = reinterpret_cast<const double2*>(
+          buf + Cfg::SLAB_BYTES + Cfg::SEG_BYTES);
+      const double* ri = reinterpret_cast<const double*>(
+          buf + Cfg::SLAB_BYTES + Cfg::SEG_BYTES + B * 8);
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const double2 rv = rj2[cl + TPR * m];
+        sj[m] = make_double2(fma(beta, sj[m].x, rv.x), fma(beta, sj[m].y, rv.y));
+      }
+      si0 = fma(beta, si0, ri[2 * rl]);
+      si1 = fma(beta, si1, ri[2 * rl + 1]);
+      if (i == j && tid < RS)  // the diagonal tile's slab owns these rows
+        args.s_out[args.row_off[i] + q * RS + tid] = fma(beta, si[tid], ri[tid]);
+    }
 
     double rs[2] = {0.0, 0.0};
     if (i != j) {
@@ -421,6 +456,8 @@ struct FinalizeArgs {
 };
 
 __global__ void __launch_bounds__(128) finalize_kernel(FinalizeArgs fa) {
+  pdl_wait();
+  pdl_trigger();
   if (fa.done && *fa.done) return;
   const int u = blockIdx.x;
   const int64_t jr = fa.unit_row[u];
@@ -469,6 +506,8 @@ __global__ void symv_generic_kernel(const double* __restrict__ a, int64_t n_pad,
                                     int b, const double* __restrict__ x,
                                     double* __restrict__ y,
                                     const int32_t* done) {
+  pdl_wait();
+  pdl_trigger();
   if (done && *done) return;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -523,6 +562,8 @@ enum VecMode : int {
 };
 
 __global__ void __launch_bounds__(VBLOCK) vec_kernel(VecArgs va) {
+  pdl_wait();
+  pdl_trigger();
   if (va.mode != V_INIT && va.mode != V_RESNORM && va.done && *va.done) return;
   const double alpha = va.sa.sc->alpha;
   const double beta = va.sa.sc->beta;
@@ -683,9 +724,15 @@ void ensure_plan(hs_matrix* m) {
   m->plan = p;
 }
 
+struct SymvFuse {  // fused direction update s_out = r + beta * s
+  const double* r;
+  double* s_out;
+  const double* beta;
+};
+
 template <int B>
 static void launch_symv_fast(hs_ctx* c, const hs_matrix* m, const double* s,
-                             const int32_t* done) {
+                             const int32_t* done, const SymvFuse* fz) {
   using Cfg = SymvCfg<B>;
   static bool attr = false;
   if (!attr) {
@@ -696,8 +743,10 @@ static void launch_symv_fast(hs_ctx* c, const hs_matrix* m, const double* s,
   }
   SymvPlan* p = m->plan;
   SymvArgs a{m->d,        s,           m->d_row_off, m->tile_lo, p->cta_slab,
-             p->cta_rseg, p->rowpart, p->colmain,   p->colextra, done};
-  symv_slab_kernel<B><<<p->grid, 288, Cfg::SMEM, c->stream>>>(a);
+             p->cta_rseg, p->rowpart, p->colmain,   p->colextra, done,
+             fz ? fz->r : nullptr, fz ? fz->s_out : nullptr,
+             fz ? fz->beta : nullptr, fz ? 1 : 0};
+  HS_CUDA(launch_pdl(symv_slab_kernel<B>, dim3(p->grid), dim3(288), Cfg::SMEM, c->stream, a));
   HS_CUDA(cudaGetLastError());
   launch_count(c);
 }
@@ -711,11 +760,15 @@ static void ensure_dpart(hs_ctx* c, size_t count) {
 
 // SYMV over the rank's tiles into `out` (padded full layout). With fuse_dot,
 // also dot(s, out) over the rows and the ALPHA step (single rank only).
+// With fz, `s` is s_old and the kernel multiplies with s = r + beta s_old
+// (written to fz->s_out); the fused dot then uses fz->s_out.
 static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
-                    bool fuse_dot, const StepArgs* sa, const int32_t* done) {
+                    bool fuse_dot, const StepArgs* sa, const int32_t* done,
+                    const SymvFuse* fz = nullptr) {
   const int b = (int)m->b;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (c->prof) {
+  const bool prof = c->prof && (c->prof_counter++ % c->prof_every == 0);
+  if (prof) {
     HS_CUDA(cudaEventCreate(&e0));
     HS_CUDA(cudaEventCreate(&e1));
     HS_CUDA(cudaEventRecord(e0, c->stream));
@@ -723,11 +776,11 @@ static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
   if (!fast_b(m->b)) {
     const int64_t pn = (int64_t)m->N * b;
     const int64_t threads = pn * 32;
-    symv_generic_kernel<<<(unsigned)ceil_div(threads, 256), 256, 0, c->stream>>>(
-        m->d, pn, b, s, out, done);
+    HS_CUDA(launch_pdl(symv_generic_kernel, dim3((unsigned)ceil_div(threads, 256)), dim3(256),
+                       0, c->stream, (const double*)m->d, pn, b, s, out, done));
     HS_CUDA(cudaGetLastError());
     launch_count(c);
-    if (c->prof) {
+    if (prof) {
       HS_CUDA(cudaEventRecord(e1, c->stream));
       c->prof_events.push_back(e0);
       c->prof_events.push_back(e1);
@@ -741,19 +794,18 @@ static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
       va.sa = *sa;
       va.done = done;
       va.mode = V_DOT_ST;
-      vec_kernel<<<VGRID, VBLOCK, 0, c->stream>>>(va);
-      HS_CUDA(cudaGetLastError());
+      HS_CUDA(launch_pdl(vec_kernel, dim3(VGRID), dim3(VBLOCK), 0, c->stream, va));
       launch_count(c);
     }
     return;
   }
   switch (b) {
-    case 64: launch_symv_fast<64>(c, m, s, done); break;
-    case 128: launch_symv_fast<128>(c, m, s, done); break;
-    case 256: launch_symv_fast<256>(c, m, s, done); break;
-    case 512: launch_symv_fast<512>(c, m, s, done); break;
+    case 64: launch_symv_fast<64>(c, m, s, done, fz); break;
+    case 128: launch_symv_fast<128>(c, m, s, done, fz); break;
+    case 256: launch_symv_fast<256>(c, m, s, done, fz); break;
+    case 512: launch_symv_fast<512>(c, m, s, done, fz); break;
   }
-  if (c->prof) {
+  if (prof) {
     HS_CUDA(cudaEventRecord(e1, c->stream));
     c->prof_events.push_back(e0);
     c->prof_events.push_back(e1);
@@ -778,12 +830,12 @@ static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
   fa.tile_lo = m->tile_lo;
   fa.b = b;
   fa.out = out;
-  fa.s = fuse_dot ? s : nullptr;
+  fa.s = fuse_dot ? (fz ? fz->s_out : s) : nullptr;
   fa.dpart = c->d_dpart;
   fa.step = STEP_ALPHA;
   if (sa) fa.sa = *sa;
   fa.done = done;
-  finalize_kernel<<<(unsigned)p->units, 128, 0, c->stream>>>(fa);
+  HS_CUDA(launch_pdl(finalize_kernel, dim3((unsigned)p->units), dim3(128), 0, c->stream, fa));
   HS_CUDA(cudaGetLastError());
   launch_count(c);
 }
@@ -794,7 +846,7 @@ void symv_local(hs_ctx* c, const hs_matrix* m, const double* x, double* y) {
 }
 
 static void launch_vec(hs_ctx* c, VecArgs va) {
-  vec_kernel<<<VGRID, VBLOCK, 0, c->stream>>>(va);
+  HS_CUDA(launch_pdl(vec_kernel, dim3(VGRID), dim3(VBLOCK), 0, c->stream, va));
   HS_CUDA(cudaGetLastError());
   launch_count(c);
 }
@@ -804,6 +856,7 @@ static void launch_vec(hs_ctx* c, VecArgs va) {
 
 struct CgBuffers {
   double* s_full = nullptr;  // padded full layout (vec_len)
+  double* s_alt = nullptr;   // second direction buffer (fused s update)
   double* x_full = nullptr;  // padded full layout (recompute / result)
   double* t = nullptr;       // partial (vec_len) or local result (world 1)
   double* t_loc = nullptr;   // reduced own rows (multi-rank)
@@ -813,6 +866,7 @@ struct CgBuffers {
   Dd* slots = nullptr;       // [world] gathered partials
   void release() {
     cudaFree(s_full);
+    cudaFree(s_alt);
     cudaFree(x_full);
     cudaFree(t);
     cudaFree(t_loc);
@@ -851,7 +905,11 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
     CgBuffers* b;
     ~Guard() { b->release(); }
   } guard{&B};
+  // single rank + fast SYMV: the direction update rides inside the SYMV
+  // (double-buffered s); otherwise a separate vector kernel does it
+  const bool fuse_sdir = world == 1 && fast_b(m->b);
   HS_CUDA(cudaMalloc(&B.s_full, full * sizeof(double)));
+  if (fuse_sdir) HS_CUDA(cudaMalloc(&B.s_alt, full * sizeof(double)));
   HS_CUDA(cudaMalloc(&B.x_full, full * sizeof(double)));
   HS_CUDA(cudaMalloc(&B.t, full * sizeof(double)));
   HS_CUDA(cudaMalloc(&B.r, chunk * sizeof(double)));
@@ -916,10 +974,19 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   HS_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
   int pending = -1;
   CgScalars h{};
+  double* sbuf[2] = {B.s_full, B.s_alt};
   for (uint64_t it = 1; it <= prm->max_iters; ++it) {
     // line 4 (+5 fused for a single rank): t = A s, alpha = u / s^T t
     if (world == 1) {
-      symv_to(c, m, B.s_full, B.t, true, &sa, done);
+      if (fuse_sdir) {
+        // s_it = r + beta s_{it-1} (line 11 of the previous iteration, with
+        // beta_0 = 0 so s_1 = r_0 = rhs), formed inside the SYMV
+        SymvFuse fz{B.r, sbuf[it & 1], &c->d_scalars->beta};
+        symv_to(c, m, sbuf[(it - 1) & 1], B.t, true, &sa, done, &fz);
+        v.s = sbuf[it & 1];
+      } else {
+        symv_to(c, m, B.s_full, B.t, true, &sa, done);
+      }
     } else {
       symv_to(c, m, B.s_full, B.t, false, nullptr, done);
       comm_reduce_scatter(c, B.t, B.t_loc, (size_t)chunk);
@@ -942,8 +1009,10 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
       launch_vec(c, v);
     }
     dot_finish(STEP_BETA);
-    v.mode = V_SDIR;  // line 11
-    launch_vec(c, v);
+    if (!fuse_sdir) {
+      v.mode = V_SDIR;  // line 11
+      launch_vec(c, v);
+    }
     if (world > 1) comm_allgather(c, s_loc, B.s_full, (size_t)chunk);
     if (it % check_every == 0) {
       const int slot = (int)((it / check_every) & 1);
@@ -1116,16 +1185,14 @@ hs_status hs_solve_cg_host(hs_ctx* c, size_t n, size_t b, const double* a,
   HS_CUDA(cudaSetDevice(c->device));
   std::memset(st, 0, sizeof(*st));
   const auto t0 = std::chrono::steady_clock::now();
-  hs_matrix* m = nullptr;
-  hs_status s = hs_matrix_create(c, n, b, &m);
-  if (s != HS_OK) throw Failure{s, hs_last_error()};
+  hs_matrix* m = cached_matrix(c, 0, n, b);
   double *d_rhs = nullptr, *d_x = nullptr;
   const size_t pn = (size_t)ceil_div(n, b) * b;
   try {
     HS_CUDA(cudaMalloc(&d_rhs, pn * sizeof(double)));
     HS_CUDA(cudaMalloc(&d_x, pn * sizeof(double)));
     const auto tt = std::chrono::steady_clock::now();
-    s = hs_matrix_upload(m, a);
+    hs_status s = hs_matrix_upload(m, a);
     if (s != HS_OK) throw Failure{s, hs_last_error()};
     HS_CUDA(cudaMemcpyAsync(d_rhs, rhs, pn * sizeof(double),
                             cudaMemcpyHostToDevice, c->stream));
@@ -1143,12 +1210,10 @@ hs_status hs_solve_cg_host(hs_ctx* c, size_t n, size_t b, const double* a,
   } catch (...) {
     cudaFree(d_rhs);
     cudaFree(d_x);
-    hs_matrix_destroy(m);
     throw;
   }
   cudaFree(d_rhs);
   cudaFree(d_x);
-  hs_matrix_destroy(m);
   HS_API_END
 }
 

@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
 
 // ---------------------------------------------------------------------------
 // diag128: POTRF + in-place TRTRI of one 128 x 128 diagonal sub-block held
-// entirely in shared memory (512 threads), blocked in 32-wide panels so the
+// entirely in shared memory (256 threads), blocked in 32-wide panels so the
 // CTA synchronises only a few times per panel:
 //   factor, per panel p: warp 0 factors the 32x32 diagonal block; one thread
 //     per row solves the panel rows below (x L^T = a, 32 registers); 4x4
@@ -663,7 +663,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
 constexpr int DCB = 128, DLD = 129, DPB = 32;
 constexpr size_t kDiagSmemBytes = (size_t)(DCB * DLD + (DCB - DPB) * (DPB + 1)) * 8;
 
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(256)
     diag128_kernel(double* A, int64_t tile_lo, int b, int f, double* W,
                    int64_t J0, int mode, CholFlag* flag) {
   if (flag->status) return;
@@ -674,8 +674,10 @@ __global__ void __launch_bounds__(512)
               sblk * DCB;
   extern __shared__ double S[];       // [128][129]
   double* Tm = S + DCB * DLD;         // [96][33] scratch
+  __shared__ double Rv[DPB];          // reciprocal diagonal of the panel
   __shared__ int bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll 8
   for (int idx = tid; idx < DCB * DCB; idx += blockDim.x) {
     const int r = idx >> 7, c = idx & 127;
     S[r * DLD + c] = c <= r ? D[(int64_t)r * b + c] : 0.0;
@@ -687,24 +689,33 @@ __global__ void __launch_bounds__(512)
     for (int p = 0; p < DCB / DPB; ++p) {
       const int o = p * DPB;
       if (warp == 0) {
+        // lane r holds row r of the 32x32 diagonal block in registers;
+        // column k of L is broadcast with shuffles (no smem round trips)
+        double a[DPB];
+#pragma unroll
+        for (int c = 0; c < DPB; ++c) a[c] = S[(o + lane) * DLD + o + c];
+        int failed = -1;
+#pragma unroll
         for (int k = 0; k < DPB; ++k) {
-          double d = S[(o + k) * DLD + o + k];
-          if (!(d > 0.0)) {
-            if (lane == 0) bad = o + k;
-            break;
+          const double akk = __shfl_sync(0xffffffffu, a[k], k);
+          if (failed < 0 && !(akk > 0.0)) failed = k;
+          const double d = sqrt(akk);
+          const double rinv = 1.0 / d;
+          if (lane == k) a[k] = d;
+          if (lane > k) a[k] *= rinv;
+#pragma unroll
+          for (int c = k + 1; c < DPB; ++c) {
+            const double lck = __shfl_sync(0xffffffffu, a[k], c);
+            if (lane >= c) a[c] = fma(-a[k], lck, a[c]);
           }
-          d = sqrt(d);
-          __syncwarp();
-          if (lane == k) S[(o + k) * DLD + o + k] = d;
-          if (lane > k) S[(o + lane) * DLD + o + k] /= d;
-          __syncwarp();
-          if (lane > k) {
-            const double lr = S[(o + lane) * DLD + o + k];
-            for (int c = k + 1; c <= lane; ++c)
-              S[(o + lane) * DLD + o + c] =
-                  fma(-lr, S[(o + c) * DLD + o + k], S[(o + lane) * DLD + o + c]);
-          }
-          __syncwarp();
+        }
+        if (failed >= 0) {
+          if (lane == 0) bad = o + failed;
+        } else {
+#pragma unroll
+          for (int c = 0; c < DPB; ++c)
+            if (c <= lane) S[(o + lane) * DLD + o + c] = a[c];
+          Rv[lane] = 1.0 / a[lane];  // reciprocal diagonal for the solves
         }
       }
       __syncthreads();
@@ -724,7 +735,7 @@ __global__ void __launch_bounds__(512)
           double acc = x[c];
 #pragma unroll
           for (int k = 0; k < c; ++k) acc = fma(-x[k], S[(o + c) * DLD + o + k], acc);
-          x[c] = acc / S[(o + c) * DLD + o + c];
+          x[c] = acc * Rv[c];
         }
 #pragma unroll
         for (int c = 0; c < DPB; ++c) row[c] = x[c];
@@ -786,6 +797,8 @@ __global__ void __launch_bounds__(512)
     }
     // (2) lane c inverts column c of the 32x32 diagonal block (registers)
     if (warp == 0) {
+      Rv[lane] = 1.0 / S[(o + lane) * DLD + o + lane];
+      __syncwarp();
       double w[DPB];
 #pragma unroll
       for (int r = 0; r < DPB; ++r) {
@@ -793,7 +806,7 @@ __global__ void __launch_bounds__(512)
 #pragma unroll
         for (int k = 0; k < r; ++k)
           if (k >= lane) acc = fma(-S[(o + r) * DLD + o + k], w[k], acc);
-        w[r] = r >= lane ? acc / S[(o + r) * DLD + o + r] : 0.0;
+        w[r] = r >= lane ? acc * Rv[r] : 0.0;
       }
       __syncwarp();
 #pragma unroll
@@ -1157,7 +1170,7 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
     const int64_t t = N - 1 - j;
     if (fast) {
       for (int s = 0; s < f; ++s) {
-        diag128_kernel<<<1, 512, kDiagSmem, cs.p>>>(m->d, m->tile_lo, b, f, m->dinv,
+        diag128_kernel<<<1, 256, kDiagSmem, cs.p>>>(m->d, m->tile_lo, b, f, m->dinv,
                                                     j * f + s, 0, flag);
         HS_CUDA(cudaGetLastError());
         launch_count(c);
@@ -1259,7 +1272,7 @@ static void ensure_inverses(hs_ctx* c, hs_matrix* m) {
   HS_CUDA(cudaMalloc(&flag, sizeof(CholFlag)));
   HS_CUDA(cudaMemsetAsync(flag, 0, sizeof(CholFlag), c->stream));
   if (dmma_ok(b)) {
-    diag128_kernel<<<(unsigned)(N * f), 512, kDiagSmem, c->stream>>>(
+    diag128_kernel<<<(unsigned)(N * f), 256, kDiagSmem, c->stream>>>(
         m->d, m->tile_lo, b, f, m->dinv, 0, 1, flag);
   } else {
     trtri_tile_kernel<<<(unsigned)N, 256, trtri_smem(b), c->stream>>>(
@@ -1392,13 +1405,8 @@ hs_status hs_factorize_host(hs_ctx* c, size_t n, size_t b, double* a_packed,
   HS_API_BEGIN
   HS_REQUIRE(c && a_packed, HS_ERR_CONFIG, "null pointer");
   HS_CUDA(cudaSetDevice(c->device));
-  hs_matrix* m = nullptr;
-  hs_status s = hs_matrix_create(c, n, b, &m);
-  if (s != HS_OK) throw Failure{s, hs_last_error()};
-  struct G {
-    hs_matrix* m;
-    ~G() { hs_matrix_destroy(m); }
-  } guard{m};
+  hs_matrix* m = cached_matrix(c, 0, n, b);
+  hs_status s = HS_OK;
   const auto t0 = std::chrono::steady_clock::now();
   s = hs_matrix_upload(m, a_packed);
   if (s != HS_OK) throw Failure{s, hs_last_error()};
@@ -1424,25 +1432,17 @@ hs_status hs_solve_spd_host(hs_ctx* c, size_t n, size_t b, double* a_packed,
   HS_API_BEGIN
   HS_REQUIRE(c && a_packed && rhs && x, HS_ERR_CONFIG, "null pointer");
   HS_CUDA(cudaSetDevice(c->device));
-  hs_matrix *m = nullptr, *orig = nullptr;
-  hs_status s = hs_matrix_create(c, n, b, &m);
-  if (s != HS_OK) throw Failure{s, hs_last_error()};
-  s = hs_matrix_create(c, n, b, &orig);
-  if (s != HS_OK) {
-    hs_matrix_destroy(m);
-    throw Failure{s, hs_last_error()};
-  }
+  hs_matrix* m = cached_matrix(c, 0, n, b);
+  hs_matrix* orig = cached_matrix(c, 1, n, b);
+  hs_status s = HS_OK;
   double *d_rhs = nullptr, *d_x = nullptr;
   struct G {
-    hs_matrix *a, *b;
     double **r, **x;
     ~G() {
-      hs_matrix_destroy(a);
-      hs_matrix_destroy(b);
       cudaFree(*r);
       cudaFree(*x);
     }
-  } guard{m, orig, &d_rhs, &d_x};
+  } guard{&d_rhs, &d_x};
   const size_t pn = (size_t)ceil_div(n, b) * b;
   HS_CUDA(cudaMalloc(&d_rhs, pn * sizeof(double)));
   HS_CUDA(cudaMalloc(&d_x, pn * sizeof(double)));

@@ -188,6 +188,7 @@ static std::vector<int64_t> row_bounds(int64_t N, int world) {
 // array). d2 uses explicit round-to-nearest mul/add (no FMA contraction) to
 // keep the reference's rounding; exp is CUDA's double exp (<= 1 ulp).
 
+template <int DIM>  // DIM > 0: compile-time dimension; 0: runtime `dim`
 __global__ void __launch_bounds__(256)
     assemble_se_kernel(double* __restrict__ tiles, int64_t tile_base, int64_t n,
                        int b, const double* __restrict__ pts, int dim,
@@ -197,27 +198,43 @@ __global__ void __launch_bounds__(256)
   const int64_t i = tile_row(t);
   const int64_t j = t - tri(i, 0);
   const int r0 = blockIdx.y * rows_per_cta;
+  const int r1 = min(b, r0 + rows_per_cta);
   double* blk = tiles + (int64_t)blockIdx.x * b * b;
-  const int total = rows_per_cta * b;
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int r = r0 + idx / b;
-    const int c = idx - (idx / b) * b;
-    if (r >= b) break;
-    const int64_t p = i * b + r, q = j * b + c;
-    double v;
-    if (p >= n || q >= n) {
-      v = (p == q) ? 1.0 : 0.0;
-    } else if (p == q) {
-      v = __dadd_rn(sf2, sn2);
-    } else {
-      double d2 = 0.0;
-      for (int k = 0; k < dim; ++k) {
-        const double d = __dsub_rn(__ldg(pts + p * dim + k), __ldg(pts + q * dim + k));
-        d2 = __dadd_rn(d2, __dmul_rn(d, d));
-      }
-      v = __dmul_rn(sf2, exp(__dmul_rn(-d2, inv2l2)));
+  const double diag = __dadd_rn(sf2, sn2);
+  // each thread owns column c: its point stays in registers; the row point
+  // is warp-uniform (broadcast load); stores are coalesced along the row
+  for (int c = threadIdx.x; c < b; c += blockDim.x) {
+    const int64_t q = j * b + c;
+    double xq[DIM > 0 ? DIM : 1];
+    if (DIM > 0 && q < n) {
+#pragma unroll
+      for (int k = 0; k < (DIM > 0 ? DIM : 1); ++k) xq[k] = __ldg(pts + q * DIM + k);
     }
-    __stcs(blk + (int64_t)r * b + c, v);
+    for (int r = r0; r < r1; ++r) {
+      const int64_t p = i * b + r;
+      double v;
+      if (p >= n || q >= n) {
+        v = (p == q) ? 1.0 : 0.0;
+      } else if (p == q) {
+        v = diag;
+      } else {
+        double d2 = 0.0;
+        if (DIM > 0) {
+#pragma unroll
+          for (int k = 0; k < (DIM > 0 ? DIM : 1); ++k) {
+            const double d = __dsub_rn(__ldg(pts + p * DIM + k), xq[k]);
+            d2 = __dadd_rn(d2, __dmul_rn(d, d));
+          }
+        } else {
+          for (int k = 0; k < dim; ++k) {
+            const double d = __dsub_rn(__ldg(pts + p * dim + k), __ldg(pts + q * dim + k));
+            d2 = __dadd_rn(d2, __dmul_rn(d, d));
+          }
+        }
+        v = __dmul_rn(sf2, exp(__dmul_rn(-d2, inv2l2)));
+      }
+      __stcs(blk + (int64_t)r * b + c, v);
+    }
   }
 }
 
@@ -264,16 +281,37 @@ static void assemble(hs_matrix* m, const double* h_pts, size_t dim, double sf2,
   HS_CUDA(cudaMemcpyAsync(d_pts, h_pts, bytes, cudaMemcpyHostToDevice,
                           c->stream));
   const int b = (int)m->b;
+  // ~8K elements per CTA: 256 threads x 32 rows for b = 256
   const int rows_per_cta = std::max(1, std::min(b, 8192 / b));
   dim3 grid((unsigned)m->local_tiles(), (unsigned)ceil_div(b, rows_per_cta));
-  assemble_se_kernel<<<grid, 256, 0, c->stream>>>(
-      m->d, m->tile_lo, (int64_t)m->n, b, d_pts, (int)dim, sf2, inv2l2, sn2,
-      rows_per_cta);
+  const int threads = std::min(256, std::max(32, (b + 31) / 32 * 32));
+  if (dim == 2)
+    assemble_se_kernel<2><<<grid, threads, 0, c->stream>>>(
+        m->d, m->tile_lo, (int64_t)m->n, b, d_pts, (int)dim, sf2, inv2l2, sn2,
+        rows_per_cta);
+  else
+    assemble_se_kernel<0><<<grid, threads, 0, c->stream>>>(
+        m->d, m->tile_lo, (int64_t)m->n, b, d_pts, (int)dim, sf2, inv2l2, sn2,
+        rows_per_cta);
   HS_CUDA(cudaGetLastError());
   launch_count(c);
   HS_CUDA(cudaFreeAsync(d_pts, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
   m->has_inv = false;
+}
+
+hs_matrix* cached_matrix(hs_ctx* c, int slot, size_t n, size_t b) {
+  hs_matrix*& m = c->cache[slot];
+  if (m && (m->n != n || m->b != b)) {
+    hs_matrix_destroy(m);
+    m = nullptr;
+  }
+  if (!m) {
+    const hs_status s = hs_matrix_create(c, n, b, &m);
+    if (s != HS_OK) throw Failure{s, hs_last_error()};
+  }
+  m->has_inv = false;
+  return m;
 }
 
 }  // namespace hs
@@ -388,6 +426,10 @@ void hs_ctx_destroy(hs_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  for (hs_matrix*& m : c->cache) {
+    hs_matrix_destroy(m);
+    m = nullptr;
+  }
   if (c->comm) c->nccl->CommDestroy((ncclComm_t)c->comm);
   for (cudaEvent_t e : c->prof_events) cudaEventDestroy(e);
   cudaFree(c->d_scalars);
@@ -606,8 +648,11 @@ hs_status hs_generate_spd(hs_matrix* m, double sf2, double length_scale,
   HS_API_END
 }
 
-void hs_prof_enable(hs_ctx* c, int on) {
-  if (c) c->prof = on != 0;
+void hs_prof_enable(hs_ctx* c, int every) {
+  if (!c) return;
+  c->prof = every > 0;
+  c->prof_every = every > 0 ? every : 1;
+  c->prof_counter = 0;
 }
 
 void hs_prof_symv(hs_ctx* c, uint64_t* launches, double* total_ms) {

@@ -68,6 +68,8 @@ struct hs_ctx {
   int num_sms = 148;
   // profiling of the SYMV launches
   bool prof = false;
+  int prof_every = 1;        // bracket every k-th SYMV launch with events
+  uint64_t prof_counter = 0;
   uint64_t prof_symv_launches = 0;
   double prof_symv_ms = 0.0;
   std::vector<cudaEvent_t> prof_events;  // pairs, drained by hs_prof_symv
@@ -76,6 +78,9 @@ struct hs_ctx {
   double* d_dpart = nullptr;  // per-block-row dot partials
   size_t dpart_cap = 0;
   double* h_pinned = nullptr;  // small pinned readback buffer
+  // device matrices reused by the host-buffer entry points (slot 0: the
+  // solve matrix, slot 1: the unfactored copy kept for the residual)
+  hs_matrix* cache[2] = {nullptr, nullptr};
 };
 
 struct hs_matrix {
@@ -105,5 +110,8 @@ void free_plan(SymvPlan* p);
 // other ranks' rows included); dot_out (optional, device) gets per-row dots.
 void symv_local(hs_ctx* c, const hs_matrix* m, const double* x, double* y);
 void launch_fill(hs_ctx* c, double* p, double v, int64_t count);
+// Scratch matrix of the context for host-buffer calls (created on first use
+// or when the shape changes; contents are overwritten by the caller).
+hs_matrix* cached_matrix(hs_ctx* c, int slot, size_t n, size_t b);
 
 }  // namespace hs

@@ -328,8 +328,9 @@ class Runtime:
             pass
 
     # profiling hooks used by bench.py
-    def prof_enable(self, on: bool = True) -> None:
-        self._L.hs_prof_enable(self.ctx, 1 if on else 0)
+    def prof_enable(self, every: int = 1) -> None:
+        """Bracket every `every`-th SYMV launch with CUDA events (0: off)."""
+        self._L.hs_prof_enable(self.ctx, int(every))
 
     def prof_symv(self) -> tuple[int, float]:
         n, ms = C.c_uint64(0), C.c_double(0.0)
