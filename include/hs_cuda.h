@@ -97,6 +97,12 @@ hs_status hs_partition_rows(size_t block_rows, int world, size_t* bounds);
 /* Allocates the tiles this rank owns (all tiles when world == 1), zeroed,
  * with identity padding (blocked_matrix.cpp:17-24, 57-74). */
 hs_status hs_matrix_create(hs_ctx* ctx, size_t n, size_t b, hs_matrix** out);
+/* 2D block-cyclic variant for the distributed Cholesky (hs_potrf on a
+ * multi-rank context): tile (i, j) lives on rank (i mod P) * Q + (j mod Q)
+ * of a P x Q grid (1x1, 1x2, 2x2, 2x4 for 1/2/4/8 ranks). Same upload /
+ * download / assembly semantics (each rank moves only its own tiles). */
+hs_status hs_matrix_create_cyclic(hs_ctx* ctx, size_t n, size_t b,
+                                  hs_matrix** out);
 void hs_matrix_destroy(hs_matrix* m);
 hs_status hs_matrix_info(const hs_matrix* m, size_t* n, size_t* b,
                          size_t* row_lo, size_t* row_hi);
@@ -210,6 +216,14 @@ hs_status hs_gemm_update_tiles(hs_ctx* ctx, double* d_c, const double* d_p,
 void hs_prof_enable(hs_ctx* ctx, int every);
 void hs_prof_symv(hs_ctx* ctx, uint64_t* launches, double* total_ms);
 void hs_prof_reset(hs_ctx* ctx);
+
+/* ---- diagnostics ------------------------------------------------------ */
+/* Read-only HBM bandwidth over `bytes` of device memory, the roofline of the
+ * CG SYMV: mode 0 = the SYMV's TMA bulk-copy ring (32-KB slabs, 5 stages,
+ * one CTA per SM), mode 1 = plain 128-bit loads, all SMs. Best of `reps`
+ * (CUDA events); returns GB/s. */
+hs_status hs_probe_hbm_read(hs_ctx* ctx, size_t bytes, int mode, int reps,
+                            double* gbs);
 
 #ifdef __cplusplus
 }

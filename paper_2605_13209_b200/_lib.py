@@ -29,14 +29,14 @@ EXPORTED = [
     "hs_rng_at", "hs_rng_uniform_pm1", "hs_generate_inputs",
     "hs_median_pairwise_distance", "hs_generate_rhs",
     "hs_partition_for_fraction", "hs_cholesky_border", "hs_partition_rows",
-    "hs_matrix_create", "hs_matrix_destroy", "hs_matrix_info", "hs_matrix_upload",
+    "hs_matrix_create", "hs_matrix_create_cyclic", "hs_matrix_destroy", "hs_matrix_info", "hs_matrix_upload",
     "hs_matrix_download", "hs_matrix_copy", "hs_matrix_device_data",
     "hs_assemble_se", "hs_generate_spd",
     "hs_cg_solve", "hs_solve_cg_host", "hs_symv", "hs_true_residual",
     "hs_potrf", "hs_trsv_lower", "hs_trsv_upper", "hs_solve_spd",
     "hs_factorize_host", "hs_solve_spd_host", "hs_forward_substitute_host",
     "hs_back_substitute_host", "hs_potf_tiles", "hs_gemm_update_tiles",
-    "hs_prof_enable", "hs_prof_symv", "hs_prof_reset",
+    "hs_prof_enable", "hs_prof_symv", "hs_prof_reset", "hs_probe_hbm_read",
 ]
 
 
@@ -97,6 +97,7 @@ def lib():
         "hs_cholesky_border": (C.c_int, [C.c_double, sz, sz, C.POINTER(sz)]),
         "hs_partition_rows": (C.c_int, [sz, C.c_int, dp]),
         "hs_matrix_create": (C.c_int, [vp, sz, sz, pp]),
+        "hs_matrix_create_cyclic": (C.c_int, [vp, sz, sz, pp]),
         "hs_matrix_destroy": (None, [vp]),
         "hs_matrix_info": (C.c_int, [vp, C.POINTER(sz), C.POINTER(sz), C.POINTER(sz),
                                      C.POINTER(sz)]),
@@ -125,6 +126,7 @@ def lib():
         "hs_prof_enable": (None, [vp, C.c_int]),
         "hs_prof_symv": (None, [vp, C.POINTER(u64), C.POINTER(C.c_double)]),
         "hs_prof_reset": (None, [vp]),
+        "hs_probe_hbm_read": (C.c_int, [vp, sz, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

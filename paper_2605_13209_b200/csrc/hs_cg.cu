@@ -16,6 +16,7 @@
 // Roofline: HBM-bound. Algorithmic bytes per matvec = packed tile bytes
 // (T * b^2 * 8); the partial slots add ~2/b of that (0.8 % at b = 128).
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <chrono>
@@ -33,25 +34,33 @@ void comm_reduce_scatter(hs_ctx* c, const double* send, double* recv,
 // ---------------------------------------------------------------------------
 // Fast SYMV for b in {64, 128, 256, 512}
 
-template <int B>
+template <int B, int NCW_ = 8>
 struct SymvCfg {
+  static constexpr int NCW = NCW_;               // consumer warps
+  static constexpr int CT = NCW * 32;            // consumer threads
+  static constexpr int THREADS = CT + 32;        // + one producer warp
   static constexpr int SLAB_BYTES = 32768;
   static constexpr int RS = 4096 / B;    // tile rows per slab
   static constexpr int SPT = B / RS;     // slabs per tile
   static constexpr int TPR = B / 8;      // consumer threads per tile row
-  static constexpr int RPP = 256 / TPR;  // row lanes (rows per pass)
+  static constexpr int RPP = CT / TPR;   // row lanes
+  static constexpr int RT = RS / RPP;    // rows per consumer thread per slab
   static constexpr int W = TPR < 32 ? TPR : 32;  // lanes of a row in a warp
   static constexpr int H = TPR / W;      // warps sharing a row
+  // column partials are pre-reduced inside a warp, so one smem row per warp
+  // (TPR <= 32) or per row lane (TPR = 64)
+  static constexpr int G = TPR <= 32 ? NCW : RPP;
+  // 8 consumer warps (16 measured slower: more smem traffic per slab)
   static constexpr int NSTAGE = B == 512 ? 4 : 5;
   // slab | seg_j (B) | seg_i (RS) | r_j (B) | r_i (RS); the r segments are
   // filled only when the s update is fused (s = r + beta s_old on the fly)
   static constexpr int SEG_BYTES = (B + RS) * 8;
   static constexpr int STAGE_BYTES = SLAB_BYTES + 2 * SEG_BYTES;
-  static constexpr int COLRED_BYTES = RPP * B * 8;
+  static constexpr int COLRED_BYTES = G * B * 8;
   static constexpr int YROW_BYTES = H * B * 8;
   static constexpr int SMEM = NSTAGE * STAGE_BYTES + 2 * COLRED_BYTES +
                               2 * YROW_BYTES + 2 * NSTAGE * 8;
-  static_assert(RS == 2 * RPP, "two rows per consumer thread per slab");
+  static_assert(RT >= 1 && RT <= 2 && RS == RT * RPP, "row mapping");
   static_assert(STAGE_BYTES % 16 == 0, "bulk copy alignment");
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
@@ -77,11 +86,12 @@ struct SymvArgs {
   int fuse;
 };
 
-template <int B>
-__global__ void __launch_bounds__(288, 1) symv_slab_kernel(SymvArgs args) {
-  using Cfg = SymvCfg<B>;
-  constexpr int RS = Cfg::RS, SPT = Cfg::SPT, TPR = Cfg::TPR, RPP = Cfg::RPP;
-  constexpr int W = Cfg::W, NS = Cfg::NSTAGE;
+template <int B, int NCW>
+__global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
+    symv_slab_kernel(SymvArgs args) {
+  using Cfg = SymvCfg<B, NCW>;
+  constexpr int RS = Cfg::RS, SPT = Cfg::SPT, TPR = Cfg::TPR, RT = Cfg::RT;
+  constexpr int W = Cfg::W, NS = Cfg::NSTAGE, CT = Cfg::CT, G = Cfg::G;
   pdl_wait();
   pdl_trigger();
   if (args.done && *args.done) return;
@@ -89,7 +99,7 @@ __global__ void __launch_bounds__(288, 1) symv_slab_kernel(SymvArgs args) {
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* stages = smem;
   double* colred = reinterpret_cast<double*>(smem + NS * Cfg::STAGE_BYTES);
-  double* yrow = colred + 2 * RPP * B;  // [2][H][B]
+  double* yrow = colred + 2 * G * B;  // [2][H][B]
   uint64_t* full = reinterpret_cast<uint64_t*>(yrow + 2 * Cfg::H * B);
   uint64_t* empty = full + NS;
 
@@ -101,7 +111,7 @@ __global__ void __launch_bounds__(288, 1) symv_slab_kernel(SymvArgs args) {
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 8);
+      mbar_init(&empty[s], Cfg::NCW);
     }
     fence_mbar_init();
   }
@@ -111,9 +121,9 @@ __global__ void __launch_bounds__(288, 1) symv_slab_kernel(SymvArgs args) {
   const int64_t t_first = g0 / SPT;
   const int64_t i_first = tile_row(t_first);
 
-  if (tid >= 256) {
+  if (tid >= CT) {
     // ---------------- producer warp ----------------
-    if (tid == 256) {
+    if (tid == CT) {
       int64_t t = t_first, i = i_first, j = t_first - tri(i_first, 0);
       int q = (int)(g0 - t_first * SPT);
       for (int64_t g = g0; g < g1; ++g) {
@@ -121,19 +131,26 @@ __global__ void __launch_bounds__(288, 1) symv_slab_kernel(SymvArgs args) {
         const int st = (int)(k % NS);
         if (k >= NS) mbar_wait(&empty[st], (uint32_t)(((k / NS) - 1) & 1));
         unsigned char* buf = stages + st * Cfg::STAGE_BYTES;
-        mbar_arrive_expect_tx(&full[st], Cfg::SLAB_BYTES + Cfg::SEG_BYTES *
-                                                               (args.fuse ? 2 : 1));
+        // the s_j (and r_j) segment is constant over a tile: consumers keep
+        // it in registers, so it is only staged with a tile's first slab
+        const bool seg_j = (q == 0) || (g == g0);
+        const int nvec = args.fuse ? 2 : 1;
+        mbar_arrive_expect_tx(&full[st],
+                              Cfg::SLAB_BYTES + nvec * (RS * 8 + (seg_j ? B * 8 : 0)));
         const double* src =
             args.a + ((t - args.tile_lo) * B + (int64_t)q * RS) * B;
-        const int64_t oj = args.row_off[j], oi = args.row_off[i] + q * RS;
+        const int64_t oi = args.row_off[i] + q * RS;
         bulk_g2s(buf, src, Cfg::SLAB_BYTES, &full[st]);
-        bulk_g2s(buf + Cfg::SLAB_BYTES, args.s + oj, B * 8, &full[st]);
         bulk_g2s(buf + Cfg::SLAB_BYTES + B * 8, args.s + oi, RS * 8, &full[st]);
-        if (args.fuse) {
-          bulk_g2s(buf + Cfg::SLAB_BYTES + Cfg::SEG_BYTES, args.r + oj, B * 8,
-                   &full[st]);
+        if (args.fuse)
           bulk_g2s(buf + Cfg::SLAB_BYTES + Cfg::SEG_BYTES + B * 8, args.r + oi,
                    RS * 8, &full[st]);
+        if (seg_j) {
+          const int64_t oj = args.row_off[j];
+          bulk_g2s(buf + Cfg::SLAB_BYTES, args.s + oj, B * 8, &full[st]);
+          if (args.fuse)
+            bulk_g2s(buf + Cfg::SLAB_BYTES + Cfg::SEG_BYTES, args.r + oj, B * 8,
+                     &full[st]);
         }
         if (++q == SPT) {
           q = 0;
@@ -149,10 +166,11 @@ __global__ void __launch_bounds__(288, 1) symv_slab_kernel(SymvArgs args) {
   }
 
   // ---------------- consumer warps ----------------
-  const int lane = tid & 31;
+  const int lane = tid & 31, warp = tid >> 5;
   const int cl = tid % TPR;  // column lane: columns 2cl + 2TPR*m (+1)
-  const int rl = tid / TPR;  // row lane: slab rows 2rl, 2rl+1
+  const int rl = tid / TPR;  // row lane: slab rows RT*rl + r
   const int h = cl / W;      // row-sharing warp index (B = 512)
+  const int grp = TPR <= 32 ? warp : rl;  // colred row after the warp reduce
   const int64_t rseg0 = args.cta_rseg[blockIdx.x];
   const bool split_start = (g0 % SPT) != 0;
   const bool fuse = args.fuse != 0;
@@ -161,6 +179,7 @@ __global__ void __launch_bounds__(288, 1) symv_slab_kernel(SymvArgs args) {
   double cacc[8];
 #pragma unroll
   for (int m = 0; m < 8; ++m) cacc[m] = 0.0;
+  double2 sj[4];  // this thread's 8 columns of s_j, kept for the whole tile
 
   int64_t t = t_first, i = i_first, j = t_first - tri(i_first, 0);
   int q = (int)(g0 - t_first * SPT);
@@ -172,110 +191,128 @@ __global__ void __launch_bounds__(288, 1) symv_slab_kernel(SymvArgs args) {
     mbar_wait(&full[st], (uint32_t)((k / NS) & 1));
     const unsigned char* buf = stages + st * Cfg::STAGE_BYTES;
     const double2* A2 = reinterpret_cast<const double2*>(buf);
-    const double2* sj2 =
-        reinterpret_cast<const double2*>(buf + Cfg::SLAB_BYTES);
     const double* si =
         reinterpret_cast<const double*>(buf + Cfg::SLAB_BYTES + B * 8);
 
-    double2 a[2][4], sj[4];
+    double2 a[RT][4];
+    double sir[RT];
 #pragma unroll
-    for (int m = 0; m < 4; ++m) sj[m] = sj2[cl + TPR * m];
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
+    for (int r = 0; r < RT; ++r)
 #pragma unroll
       for (int m = 0; m < 4; ++m)
-        a[r][m] = A2[(2 * rl + r) * (B / 2) + cl + TPR * m];
-    double si0 = si[2 * rl], si1 = si[2 * rl + 1];
+        a[r][m] = A2[(RT * rl + r) * (B / 2) + cl + TPR * m];
+    if (q == 0 || g == g0) {  // tile start: load (and update) s_j once
+      const double2* sj2 =
+          reinterpret_cast<const double2*>(buf + Cfg::SLAB_BYTES);
+#pragma unroll
+      for (int m = 0; m < 4; ++m) sj[m] = sj2[cl + TPR * m];
+      if (fuse) {
+        const double2* rj2 = reinterpret_cast<const double2*>(
+            buf + Cfg::SLAB_BYTES + Cfg::SEG_BYTES);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const double2 rv = rj2[cl + TPR * m];
+          sj[m] = make_double2(fma(beta, sj[m].x, rv.x), fma(beta, sj[m].y, rv.y));
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RT; ++r) sir[r] = si[RT * rl + r];
     if (fuse) {  // s = r + beta s_old  (cg_solver.cpp line 11, xpay_range)
-      const double2* rj2 = reinterpret_cast<const double2*>(
-          buf + Cfg::SLAB_BYTES + Cfg::SEG_BYTES);
       const double* ri = reinterpret_cast<const double*>(
           buf + Cfg::SLAB_BYTES + Cfg::SEG_BYTES + B * 8);
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const double2 rv = rj2[cl + TPR * m];
-        sj[m] = make_double2(fma(beta, sj[m].x, rv.x), fma(beta, sj[m].y, rv.y));
-      }
-      si0 = fma(beta, si0, ri[2 * rl]);
-      si1 = fma(beta, si1, ri[2 * rl + 1]);
+      for (int r = 0; r < RT; ++r) sir[r] = fma(beta, sir[r], ri[RT * rl + r]);
       if (i == j && tid < RS)  // the diagonal tile's slab owns these rows
         args.s_out[args.row_off[i] + q * RS + tid] = fma(beta, si[tid], ri[tid]);
     }
 
-    double rs[2] = {0.0, 0.0};
+    double rs[RT];
+#pragma unroll
+    for (int r = 0; r < RT; ++r) rs[r] = 0.0;
+    // (the stage is released after the FMAs below: an earlier release
+    // measured slower)
     if (i != j) {
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
+      for (int r = 0; r < RT; ++r) {
+        double p0 = 0.0, p1 = 0.0;  // two chains for ILP
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          rs[r] = fma(a[r][m].x, sj[m].x, rs[r]);
-          rs[r] = fma(a[r][m].y, sj[m].y, rs[r]);
+        for (int m = 0; m < 4; ++m) {
+          p0 = fma(a[r][m].x, sj[m].x, p0);
+          p1 = fma(a[r][m].y, sj[m].y, p1);
+          cacc[2 * m] = fma(a[r][m].x, sir[r], cacc[2 * m]);
+          cacc[2 * m + 1] = fma(a[r][m].y, sir[r], cacc[2 * m + 1]);
         }
-        cacc[2 * m] = fma(a[0][m].x, si0, cacc[2 * m]);
-        cacc[2 * m] = fma(a[1][m].x, si1, cacc[2 * m]);
-        cacc[2 * m + 1] = fma(a[0][m].y, si0, cacc[2 * m + 1]);
-        cacc[2 * m + 1] = fma(a[1][m].y, si1, cacc[2 * m + 1]);
+        rs[r] = p0 + p1;
       }
     } else {
       // diagonal tile: lower triangle only (c <= r for rows, c < r for cols)
-      const int rbase = q * RS + 2 * rl;
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int c0 = 2 * cl + 2 * TPR * m;
+      for (int r = 0; r < RT; ++r) {
+        const int rr = q * RS + RT * rl + r;
+        double p0 = 0.0, p1 = 0.0;
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const int rr = rbase + r;
-          const double ax = c0 <= rr ? a[r][m].x : 0.0;
-          const double ay = c0 + 1 <= rr ? a[r][m].y : 0.0;
-          rs[r] = fma(ax, sj[m].x, rs[r]);
-          rs[r] = fma(ay, sj[m].y, rs[r]);
-          const double sir = r ? si1 : si0;
-          cacc[2 * m] = fma(c0 < rr ? a[r][m].x : 0.0, sir, cacc[2 * m]);
-          cacc[2 * m + 1] =
-              fma(c0 + 1 < rr ? a[r][m].y : 0.0, sir, cacc[2 * m + 1]);
+        for (int m = 0; m < 4; ++m) {
+          const int c0 = 2 * cl + 2 * TPR * m;
+          p0 = fma(c0 <= rr ? a[r][m].x : 0.0, sj[m].x, p0);
+          p1 = fma(c0 + 1 <= rr ? a[r][m].y : 0.0, sj[m].y, p1);
+          cacc[2 * m] = fma(c0 < rr ? a[r][m].x : 0.0, sir[r], cacc[2 * m]);
+          cacc[2 * m + 1] = fma(c0 + 1 < rr ? a[r][m].y : 0.0, sir[r], cacc[2 * m + 1]);
         }
+        rs[r] = p0 + p1;
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
 
-    // row sums: reduce the 2 rows over the W lanes of this warp (transposed
-    // first step), then the owning lane accumulates into yrow[rpar][h][row].
-    {
+    // row sums over the W lanes of a row in this warp; the owning lane adds
+    // into yrow[rpar][h][row]
+    if (RT == 2) {
       const bool hi = (cl & (W / 2)) != 0;
-      const double send = hi ? rs[0] : rs[1];
-      double v = (hi ? rs[1] : rs[0]) + __shfl_xor_sync(0xffffffffu, send, W / 2);
+      const double send = hi ? rs[0] : rs[RT - 1];
+      double v = (hi ? rs[RT - 1] : rs[0]) + __shfl_xor_sync(0xffffffffu, send, W / 2);
 #pragma unroll
       for (int off = W / 4; off >= 1; off >>= 1)
         v += __shfl_xor_sync(0xffffffffu, v, off);
-      if ((cl & (W / 2 - 1)) == 0) {
-        const int row = q * RS + 2 * rl + (hi ? 1 : 0);
-        yrow[(rpar * Cfg::H + h) * B + row] += v;
-      }
+      if ((cl & (W / 2 - 1)) == 0)
+        yrow[(rpar * Cfg::H + h) * B + q * RS + RT * rl + (hi ? 1 : 0)] += v;
+    } else {
+      double v = rs[0];
+#pragma unroll
+      for (int off = W / 2; off >= 1; off >>= 1)
+        v += __shfl_xor_sync(0xffffffffu, v, off);
+      if ((cl & (W - 1)) == 0) yrow[(rpar * Cfg::H + h) * B + q * RS + rl] += v;
     }
 
     const bool tile_end = (q == SPT - 1) || (g + 1 == g1);
     if (tile_end) {
-      double* cr = colred + tpar * RPP * B;
+      // pre-reduce the row lanes that share columns inside the warp
 #pragma unroll
-      for (int m = 0; m < 4; ++m)
-        reinterpret_cast<double2*>(cr + rl * B)[cl + TPR * m] =
-            make_double2(cacc[2 * m], cacc[2 * m + 1]);
-      named_bar_sync(1, 256);
+      for (int off = TPR; off < 32; off <<= 1)
+#pragma unroll
+        for (int m = 0; m < 8; ++m) cacc[m] += __shfl_xor_sync(0xffffffffu, cacc[m], off);
+      double* cr = colred + tpar * G * B;
+      if (TPR >= 32 || lane < TPR) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          reinterpret_cast<double2*>(cr + grp * B)[cl + TPR * m] =
+              make_double2(cacc[2 * m], cacc[2 * m + 1]);
+      }
+      named_bar_sync(1, CT);
       double* dst = (split_start && t == t_first)
                         ? args.colextra + (int64_t)blockIdx.x * B
                         : args.colmain + (t - args.tile_lo) * B;
-      for (int c = tid; c < B; c += 256) {
+      for (int c = tid; c < B; c += CT) {
         double acc = 0.0;
 #pragma unroll 4
-        for (int r = 0; r < RPP; ++r) acc += cr[r * B + c];
+        for (int r = 0; r < G; ++r) acc += cr[r * B + c];
         dst[c] = acc;
       }
       const bool row_end = (j == i && q == SPT - 1) || (g + 1 == g1);
       if (row_end) {
         const int64_t rseg = rseg0 + (i - i_first);
         double* yr = yrow + rpar * Cfg::H * B;
-        for (int c = tid; c < B; c += 256) {
+        for (int c = tid; c < B; c += CT) {
           double acc = yr[c];
           yr[c] = 0.0;
 #pragma unroll
@@ -401,7 +438,7 @@ __device__ void scalar_step(int step, double val, const StepArgs& sa) {
 __device__ void dot_epilogue(double part, double* dpart, int slot, int count,
                              int step, const StepArgs& sa) {
   __shared__ double red_d[32];
-  __shared__ Dd red_dd[256];
+  __shared__ Dd red_dd[1024];  // up to 1024 threads (finalize)
   __shared__ bool last;
   const double p = block_sum(part, red_d);
   if (threadIdx.x == 0) {
@@ -455,46 +492,45 @@ struct FinalizeArgs {
   const int32_t* done;
 };
 
-__global__ void __launch_bounds__(128) finalize_kernel(FinalizeArgs fa) {
+// One CTA of FIN_THREADS per output block row j: the FIN_THREADS / b threads
+// of each column split the row's tile slots (i = i0 + p, i0 + p + P, ...),
+// then add in a fixed order (smem), plus row segments and split-tile extras;
+// fused dot s_j . t_j and, via a global ticket, the alpha step.
+constexpr int FIN_THREADS = 1024;
+
+__global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(FinalizeArgs fa) {
   pdl_wait();
   pdl_trigger();
   if (fa.done && *fa.done) return;
-  const int u = blockIdx.x;
-  const int64_t jr = fa.unit_row[u];
-  const int i0 = fa.unit_i0[u], i1 = fa.unit_i1[u];
+  const int64_t jr = blockIdx.x;  // output block row
   const int b = fa.b;
-  for (int c = threadIdx.x; c < b; c += blockDim.x) {
-    double acc = 0.0;
+  const int P = blockDim.x / b;   // threads per column
+  const int c = threadIdx.x % b, p = threadIdx.x / b;
+  __shared__ double red[FIN_THREADS];
+  double acc = 0.0;
+  if (p < P) {
+    const int64_t i0 = (jr > fa.row_lo ? jr : fa.row_lo) + p;
+    const double* base = fa.colmain - fa.tile_lo * b + c;
 #pragma unroll 8
-    for (int i = i0; i < i1; ++i)
-      acc += fa.colmain[(tri(i, jr) - fa.tile_lo) * b + c];
-    fa.upart[(int64_t)u * b + c] = acc;
+    for (int64_t i = i0; i < fa.row_hi; i += P) acc += __ldg(base + tri(i, jr) * b);
   }
-  __shared__ bool last;
-  __threadfence();
+  red[threadIdx.x] = acc;
   __syncthreads();
-  const int ub = fa.row_unit[jr], ue = fa.row_unit[jr + 1];
-  if (threadIdx.x == 0) {
-    last = atomicAdd(&fa.row_ticket[jr], 1u) == (unsigned)(ue - ub - 1);
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  const bool own = jr >= fa.row_lo && jr < fa.row_hi;
-  const int64_t rs0 = own ? fa.row_rseg[jr - fa.row_lo] : 0;
-  const int64_t rs1 = own ? fa.row_rseg[jr - fa.row_lo + 1] : 0;
-  const int e0 = fa.row_extra[jr], e1 = fa.row_extra[jr + 1];
   double dotp = 0.0;
-  for (int c = threadIdx.x; c < b; c += blockDim.x) {
-    double acc = 0.0;
-    for (int uu = ub; uu < ue; ++uu) acc += fa.upart[(int64_t)uu * b + c];
-    for (int64_t sg = rs0; sg < rs1; ++sg) acc += fa.rowpart[sg * b + c];
-    for (int e = e0; e < e1; ++e) acc += fa.colextra[(int64_t)fa.extra_cta[e] * b + c];
+  if (p == 0) {
+    double t = 0.0;
+    for (int pp = 0; pp < P; ++pp) t += red[pp * b + c];
+    const bool own = jr >= fa.row_lo && jr < fa.row_hi;
+    if (own) {
+      const int64_t rs0 = fa.row_rseg[jr - fa.row_lo], rs1 = fa.row_rseg[jr - fa.row_lo + 1];
+      for (int64_t sg = rs0; sg < rs1; ++sg) t += fa.rowpart[sg * b + c];
+    }
+    const int e0 = fa.row_extra[jr], e1 = fa.row_extra[jr + 1];
+    for (int e = e0; e < e1; ++e) t += fa.colextra[(int64_t)fa.extra_cta[e] * b + c];
     const int64_t o = fa.row_off[jr] + c;
-    fa.out[o] = acc;
-    if (fa.s) dotp = fma(fa.s[o], acc, dotp);
+    fa.out[o] = t;
+    if (fa.s) dotp = fa.s[o] * t;
   }
-  if (threadIdx.x == 0) fa.row_ticket[jr] = 0;
   if (fa.s) dot_epilogue(dotp, fa.dpart, (int)jr, (int)fa.row_hi, fa.step, fa.sa);
 }
 
@@ -658,6 +694,8 @@ static void upload_vec(T** dst, const std::vector<T>& v) {
 void ensure_plan(hs_matrix* m) {
   if (m->plan) return;
   const int64_t b = (int64_t)m->b;
+  HS_REQUIRE(m->layout == 0 || m->ctx->world == 1, HS_ERR_CONFIG,
+             "CG needs a row-sharded matrix (hs_matrix_create), not a cyclic one");
   HS_REQUIRE(fast_b(m->b) || m->ctx->world == 1, HS_ERR_CONFIG,
              "multi-GPU CG needs block size 64, 128, 256 or 512");
   SymvPlan* p = new SymvPlan;
@@ -730,13 +768,13 @@ struct SymvFuse {  // fused direction update s_out = r + beta * s
   const double* beta;
 };
 
-template <int B>
+template <int B, int NCW>
 static void launch_symv_fast(hs_ctx* c, const hs_matrix* m, const double* s,
                              const int32_t* done, const SymvFuse* fz) {
-  using Cfg = SymvCfg<B>;
+  using Cfg = SymvCfg<B, NCW>;
   static bool attr = false;
   if (!attr) {
-    HS_CUDA(cudaFuncSetAttribute(symv_slab_kernel<B>,
+    HS_CUDA(cudaFuncSetAttribute(symv_slab_kernel<B, NCW>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Cfg::SMEM));
     attr = true;
@@ -746,7 +784,8 @@ static void launch_symv_fast(hs_ctx* c, const hs_matrix* m, const double* s,
              p->cta_rseg, p->rowpart, p->colmain,   p->colextra, done,
              fz ? fz->r : nullptr, fz ? fz->s_out : nullptr,
              fz ? fz->beta : nullptr, fz ? 1 : 0};
-  HS_CUDA(launch_pdl(symv_slab_kernel<B>, dim3(p->grid), dim3(288), Cfg::SMEM, c->stream, a));
+  HS_CUDA(launch_pdl(symv_slab_kernel<B, NCW>, dim3(p->grid), dim3(Cfg::THREADS),
+                     Cfg::SMEM, c->stream, a));
   HS_CUDA(cudaGetLastError());
   launch_count(c);
 }
@@ -800,10 +839,10 @@ static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
     return;
   }
   switch (b) {
-    case 64: launch_symv_fast<64>(c, m, s, done, fz); break;
-    case 128: launch_symv_fast<128>(c, m, s, done, fz); break;
-    case 256: launch_symv_fast<256>(c, m, s, done, fz); break;
-    case 512: launch_symv_fast<512>(c, m, s, done, fz); break;
+    case 64: launch_symv_fast<64, 8>(c, m, s, done, fz); break;
+    case 128: launch_symv_fast<128, 8>(c, m, s, done, fz); break;
+    case 256: launch_symv_fast<256, 8>(c, m, s, done, fz); break;
+    case 512: launch_symv_fast<512, 8>(c, m, s, done, fz); break;
   }
   if (prof) {
     HS_CUDA(cudaEventRecord(e1, c->stream));
@@ -835,7 +874,8 @@ static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
   fa.step = STEP_ALPHA;
   if (sa) fa.sa = *sa;
   fa.done = done;
-  HS_CUDA(launch_pdl(finalize_kernel, dim3((unsigned)p->units), dim3(128), 0, c->stream, fa));
+  HS_CUDA(launch_pdl(finalize_kernel, dim3((unsigned)m->row_hi), dim3(FIN_THREADS / b * b), 0,
+                     c->stream, fa));
   HS_CUDA(cudaGetLastError());
   launch_count(c);
 }

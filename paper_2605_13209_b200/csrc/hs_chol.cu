@@ -269,6 +269,10 @@ enum GemmMode : int {
   G_DIAG_UPD = 6,    // column j, step s: D[r,c] -= D[r,s] D[c,s]^T, s<c<=r
   G_TRSM_X = 7,      // SIMT path: X_i = A_ij W_j^T into the panel buffer
   G_BATCH = 8,       // tests: C_t -= P_t Q_t^T (lower_only option)
+  // distributed (2D block-cyclic) variants, items from host-built lists
+  G_DIST_UPDATE = 9,      // owned (i, k): A_ik -= PB_i PB_k^T
+  G_DIST_PANEL_UPD = 10,  // owned panel rows i: A_ij[:,c] -= A_ij[:,<c] Ld[c,<c]^T
+  G_DIST_PANEL_TRSM = 11, // owned panel rows i: A_ij[:,c] = A_ij[:,c] Wb_c^T
 };
 
 struct GemmArgs {
@@ -287,6 +291,8 @@ struct GemmArgs {
   const double* Q;
   int lower_only;
   const CholFlag* flag;
+  const int64_t* lpos;    // cyclic layout: global tile -> local slot
+  const int32_t* list;    // dist modes: (i, k) pairs or panel rows i
 };
 
 struct GemmItem {
@@ -306,7 +312,9 @@ __device__ __forceinline__ GemmItem decode_item(const GemmArgs& g, int64_t item)
   GemmItem it{};
   const int b = g.b, cb = g.cb, f = g.f;
   const int64_t bb = (int64_t)b * b;
-  auto tile = [&](int64_t i, int64_t k) { return tri(i, k) - g.tile_lo; };
+  auto tile = [&](int64_t i, int64_t k) {
+    return g.lpos ? g.lpos[tri(i, k)] : tri(i, k) - g.tile_lo;
+  };
   auto sub = [&](int64_t t, int r, int c) { return g.A + t * bb + (int64_t)r * cb * b + (int64_t)c * cb; };
   it.lda = it.ldb = b;
   it.op = 0;
@@ -407,6 +415,48 @@ __device__ __forceinline__ GemmItem decode_item(const GemmArgs& g, int64_t item)
       it.K = b;
       it.c = g.Xout + (i - g.j - 1) * bb;
       it.op = 1;
+      return it;
+    }
+    case G_DIST_UPDATE: {
+      const int64_t u = item / (f * f);
+      const int sb = (int)(item % (f * f));
+      const int mb = sb / f, nb = sb % f;
+      const int64_t i = g.list[2 * u], k = g.list[2 * u + 1];
+      it.lower = (i == k) && mb == nb;
+      it.skip = (i == k) && nb > mb;
+      it.K = b;
+      it.a_tile = i - g.j - 1;  // panel buffer tiles
+      it.b_tile = k - g.j - 1;
+      it.a = g.X + it.a_tile * bb + (int64_t)mb * cb * b;
+      it.bp = g.X + it.b_tile * bb + (int64_t)nb * cb * b;
+      it.a_r0 = mb * cb;
+      it.b_r0 = nb * cb;
+      it.c = sub(tile(i, k), mb, nb);
+      return it;
+    }
+    case G_DIST_PANEL_UPD:
+    case G_DIST_PANEL_TRSM: {
+      const int64_t i = g.list[item / f];
+      const int mb = (int)(item % f);
+      const int c = g.step;
+      it.a_tile = tile(i, g.j);
+      it.a_r0 = mb * cb;
+      it.c = sub(it.a_tile, mb, c);
+      if (g.mode == G_DIST_PANEL_UPD) {
+        it.a_k0 = 0;
+        it.K = c * cb;
+        it.b_tile = 0;  // the broadcast L_jj
+        it.b_r0 = c * cb;
+        it.bp = g.X + (int64_t)c * cb * b;
+      } else {
+        it.a_k0 = c * cb;
+        it.K = cb;
+        it.b_tile = c;  // the broadcast inverse blocks of L_jj
+        it.bp = g.W + (int64_t)c * cb * cb;
+        it.ldb = cb;
+        it.op = 1;
+      }
+      it.a = g.A + it.a_tile * bb + (int64_t)it.a_r0 * b + it.a_k0;
       return it;
     }
     default: {  // G_BATCH
@@ -664,14 +714,14 @@ constexpr int DCB = 128, DLD = 129, DPB = 32;
 constexpr size_t kDiagSmemBytes = (size_t)(DCB * DLD + (DCB - DPB) * (DPB + 1)) * 8;
 
 __global__ void __launch_bounds__(256)
-    diag128_kernel(double* A, int64_t tile_lo, int b, int f, double* W,
-                   int64_t J0, int mode, CholFlag* flag) {
+    diag128_kernel(double* A, int64_t tile_lo, const int64_t* lpos, int b, int f,
+                   double* W, int64_t J0, int mode, CholFlag* flag) {
   if (flag->status) return;
   const int64_t J = J0 + blockIdx.x;
   const int64_t j = J / f;
   const int sblk = (int)(J % f);
-  double* D = A + (tri(j, j) - tile_lo) * (int64_t)b * b + (int64_t)sblk * DCB * b +
-              sblk * DCB;
+  const int64_t slot = lpos ? lpos[tri(j, j)] : tri(j, j) - tile_lo;
+  double* D = A + slot * (int64_t)b * b + (int64_t)sblk * DCB * b + sblk * DCB;
   extern __shared__ double S[];       // [128][129]
   double* Tm = S + DCB * DLD;         // [96][33] scratch
   __shared__ double Rv[DPB];          // reciprocal diagonal of the panel
@@ -684,41 +734,59 @@ __global__ void __launch_bounds__(256)
   }
   if (tid == 0) bad = DCB;
   __syncthreads();
+#ifdef HS_DIAG_TIMING
+  __shared__ long long ts_clk[40];
+  __shared__ const char* ts_name[40];
+  int ts_n = 0;
+  const long long ts0 = clock64();
+#define HS_PHASE(name)                         \
+  if (tid == 0 && ts_n < 40) {                 \
+    ts_clk[ts_n] = clock64();                  \
+    ts_name[ts_n++] = name;                    \
+  }
+#else
+#define HS_PHASE(name)
+#endif
+  HS_PHASE("load");
 
   if (mode == 0) {
     for (int p = 0; p < DCB / DPB; ++p) {
       const int o = p * DPB;
       if (warp == 0) {
-        // lane r holds row r of the 32x32 diagonal block in registers;
-        // column k of L is broadcast with shuffles (no smem round trips)
-        double a[DPB];
-#pragma unroll
-        for (int c = 0; c < DPB; ++c) a[c] = S[(o + lane) * DLD + o + c];
+        // right-looking 32x32 factor in smem, lane r owns row r; fixed-bound
+        // predicated inner loop (no register arrays -> no local memory)
+        double* Dp = S + o * DLD + o;
         int failed = -1;
-#pragma unroll
         for (int k = 0; k < DPB; ++k) {
-          const double akk = __shfl_sync(0xffffffffu, a[k], k);
-          if (failed < 0 && !(akk > 0.0)) failed = k;
-          const double d = sqrt(akk);
-          const double rinv = 1.0 / d;
-          if (lane == k) a[k] = d;
-          if (lane > k) a[k] *= rinv;
-#pragma unroll
-          for (int c = k + 1; c < DPB; ++c) {
-            const double lck = __shfl_sync(0xffffffffu, a[k], c);
-            if (lane >= c) a[c] = fma(-a[k], lck, a[c]);
+          const double akk = Dp[k * DLD + k];
+          if (!(akk > 0.0)) {
+            failed = k;
+            break;
           }
+          const double rinv = rsqrt(akk);
+          const double lrk = lane > k ? Dp[lane * DLD + k] * rinv : 0.0;
+          __syncwarp();
+          if (lane == k) Dp[k * DLD + k] = akk * rinv;
+          if (lane > k) Dp[lane * DLD + k] = lrk;
+          __syncwarp();
+// column k of L comes from the owning lanes by shuffle; only this lane's
+          // own row is touched in smem, so loads / stores pipeline
+          double* myrow = Dp + lane * DLD;
+#pragma unroll
+          for (int c = 1; c < DPB; ++c) {
+            const double lck = __shfl_sync(0xffffffffu, lrk, c);
+            if (c > k && c <= lane) myrow[c] = fma(-lrk, lck, myrow[c]);
+          }
+          __syncwarp();
         }
         if (failed >= 0) {
           if (lane == 0) bad = o + failed;
         } else {
-#pragma unroll
-          for (int c = 0; c < DPB; ++c)
-            if (c <= lane) S[(o + lane) * DLD + o + c] = a[c];
-          Rv[lane] = 1.0 / a[lane];  // reciprocal diagonal for the solves
+          Rv[lane] = 1.0 / Dp[lane * DLD + lane];  // reciprocal diagonal
         }
       }
       __syncthreads();
+      HS_PHASE("warpfactor");
       if (bad < DCB) {
         if (tid == 0) raise_flag(flag, HS_ERR_NOT_SPD, j, (int64_t)sblk * DCB + bad);
         return;
@@ -741,6 +809,7 @@ __global__ void __launch_bounds__(256)
         for (int c = 0; c < DPB; ++c) row[c] = x[c];
       }
       __syncthreads();
+      HS_PHASE("paneltrsm");
       // trailing rank-32 update of the lower triangle, 4x4 register tiles
       const int mt = m / 4, ntile = mt * (mt + 1) / 2;
       for (int u = tid; u < ntile; u += blockDim.x) {
@@ -767,6 +836,7 @@ __global__ void __launch_bounds__(256)
             if (c0 + y <= r0 + x) S[(r0 + x) * DLD + c0 + y] -= acc[x][y];
       }
       __syncthreads();
+      HS_PHASE("update");
     }
     for (int idx = tid; idx < DCB * DCB; idx += blockDim.x) {
       const int r = idx >> 7, c = idx & 127;
@@ -787,14 +857,31 @@ __global__ void __launch_bounds__(256)
   // blocked in-place inverse, panels right to left
   for (int p = DCB / DPB - 1; p >= 0; --p) {
     const int o = p * DPB, q0 = o + DPB, m = DCB - q0;
-    // (1) T = W_trail L_panel  (W_trail already inverted in place, lower)
-    for (int idx = tid; idx < m * DPB; idx += blockDim.x) {
-      const int r = idx / DPB, c = idx % DPB;
-      double acc = 0.0;
-      for (int k = 0; k <= r; ++k)
-        acc = fma(S[(q0 + r) * DLD + q0 + k], S[(q0 + k) * DLD + o + c], acc);
-      Tm[r * (DPB + 1) + c] = acc;
+    // (1) T = W_trail L_panel  (W_trail already inverted in place, lower;
+    //     the strict upper part of S is zero, so k runs over full tiles)
+    //     4x4 register tiles: 16 independent FMA chains per thread
+    for (int u = tid; u < (m / 4) * (DPB / 4); u += blockDim.x) {
+      const int r0 = (u / (DPB / 4)) * 4, c0 = (u % (DPB / 4)) * 4;
+      double acc[4][4] = {};
+      const int kend = r0 + 4;
+#pragma unroll 4
+      for (int k = 0; k < kend; ++k) {
+        double w4[4], l4[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) w4[x] = S[(q0 + r0 + x) * DLD + q0 + k];
+#pragma unroll
+        for (int y = 0; y < 4; ++y) l4[y] = S[(q0 + k) * DLD + o + c0 + y];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[x][y] = fma(w4[x], l4[y], acc[x][y]);
+      }
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) Tm[(r0 + x) * (DPB + 1) + c0 + y] = acc[x][y];
     }
+    HS_PHASE("inv_T");
     // (2) lane c inverts column c of the 32x32 diagonal block (registers)
     if (warp == 0) {
       Rv[lane] = 1.0 / S[(o + lane) * DLD + o + lane];
@@ -814,22 +901,49 @@ __global__ void __launch_bounds__(256)
         if (r >= lane) S[(o + r) * DLD + o + lane] = w[r];
     }
     __syncthreads();
-    // (3) W_panel = -T W_pp  (W_pp lower: k >= c)
-    for (int idx = tid; idx < m * DPB; idx += blockDim.x) {
-      const int r = idx / DPB, c = idx % DPB;
-      double acc = 0.0;
-      for (int k = c; k < DPB; ++k)
-        acc = fma(Tm[r * (DPB + 1) + k], S[(o + k) * DLD + o + c], acc);
-      S[(q0 + r) * DLD + o + c] = -acc;
+    HS_PHASE("inv_diag");
+    // (3) W_panel = -T W_pp  (W_pp lower; its upper part in S is zero)
+    for (int u = tid; u < (m / 4) * (DPB / 4); u += blockDim.x) {
+      const int r0 = (u / (DPB / 4)) * 4, c0 = (u % (DPB / 4)) * 4;
+      double acc[4][4] = {};
+#pragma unroll 8
+      for (int k = c0; k < DPB; ++k) {
+        double t4[4], w4[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) t4[x] = Tm[(r0 + x) * (DPB + 1) + k];
+#pragma unroll
+        for (int y = 0; y < 4; ++y) w4[y] = S[(o + k) * DLD + o + c0 + y];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[x][y] = fma(t4[x], w4[y], acc[x][y]);
+      }
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) S[(q0 + r0 + x) * DLD + o + c0 + y] = -acc[x][y];
     }
     __syncthreads();
+    HS_PHASE("inv_panel");
   }
   double* Wj = W + J * DCB * DCB;
   for (int idx = tid; idx < DCB * DCB; idx += blockDim.x) {
     const int r = idx >> 7, c = idx & 127;
     Wj[idx] = c <= r ? S[r * DLD + c] : 0.0;
   }
+  HS_PHASE("store");
+#ifdef HS_DIAG_TIMING
+  if (tid == 0 && blockIdx.x == 0 && J0 == 0) {
+    long long prev = ts0;
+    for (int k = 0; k < ts_n; ++k) {
+      printf("diag128 %-12s %8lld\n", ts_name[k], ts_clk[k] - prev);
+      prev = ts_clk[k];
+    }
+    printf("diag128 TOTAL %lld cycles\n", prev - ts0);
+  }
+#endif
 }
+#undef HS_PHASE
 
 // ---------------------------------------------------------------------------
 // small kernels
@@ -850,7 +964,8 @@ __global__ void copy_panel_kernel(double* A, int64_t tile_lo, const double* X,
 // NaN/Inf scan of the lower triangles (cholesky_solver.cpp:222-238): one
 // warp per tile row, lanes over columns, no divisions in the inner loop.
 __global__ void check_finite_kernel(const double* A, int64_t tile_lo,
-                                    int64_t ntiles, int b, CholFlag* flag) {
+                                    const int64_t* owned, int64_t ntiles, int b,
+                                    CholFlag* flag) {
   const int64_t bb = (int64_t)b * b;
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -860,7 +975,7 @@ __global__ void check_finite_kernel(const double* A, int64_t tile_lo,
   for (int64_t w = warp; w < ntiles * b; w += nwarps) {
     const int64_t t = w / b;
     const int r = (int)(w - t * b);
-    const int64_t gt = tile_lo + t;
+    const int64_t gt = owned ? owned[t] : tile_lo + t;
     const int64_t i = tile_row(gt);
     const bool diag = (gt - tri(i, 0)) == i;
     const int cols = diag ? r + 1 : b;
@@ -877,92 +992,142 @@ __global__ void check_finite_kernel(const double* A, int64_t tile_lo,
   }
 }
 
-// ---- triangular solves on cb-blocks with the stored inverses --------------
-// Sub-row I covers vector entries [I cb, (I+1) cb); sub-block (I, J) lives in
-// tile (I / f, J / f) at rows (I % f) cb, cols (J % f) cb.
-// forward: s = v_I - sum_{J<I} L_IJ v_J ; v_I = W_I s
-// back:    s = v_I - sum_{J>I} L_JI^T v_J ; v_I = W_I^T s
+// ---- triangular solves with the stored inverses ----------------------------
+// Right-looking at tile granularity, 2 launches per tile row (PDL-chained):
+//   forward  (L y = v):   y_i = solve(L_ii, v_i)   [trsv_diag_kernel, 1 CTA]
+//                         v_k -= L_ki y_i, k > i   [trsv_update_kernel]
+//   backward (L^T x = v): x_i = solve(L_ii^T, v_i)
+//                         v_k -= L_ik^T x_i, k < i
+// The diagonal tile solve walks its f = b / cb sub-blocks with the stored
+// cb x cb inverses W (cb = 128 on the DMMA path, b otherwise).
 
-__device__ __forceinline__ const double* subblock(const double* A, int64_t tile_lo,
-                                                  int b, int cb, int f, int64_t I,
-                                                  int64_t J) {
-  const int64_t ti = I / f, tj = J / f;
-  return A + (tri(ti, tj) - tile_lo) * (int64_t)b * b + (int64_t)(I % f) * cb * b +
-         (int64_t)(J % f) * cb;
+// v_i <- L_ii^-1 v_i (forward) or L_ii^-T v_i (backward), one CTA.
+constexpr int TRSV_DIAG_THREADS = 1024;
+
+__global__ void __launch_bounds__(TRSV_DIAG_THREADS)
+    trsv_diag_kernel(const double* A, int64_t tile_lo, const double* W, double* v,
+                     int b, int cb, int f, int64_t i, int upper) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ double sh[];  // vin[b] | sol[b]
+  double* vin = sh;
+  double* sol = sh + b;
+  const double* D = A + (tri(i, i) - tile_lo) * (int64_t)b * b;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  for (int k = tid; k < b; k += blockDim.x) vin[k] = v[i * b + k];
+  __syncthreads();
+  for (int step = 0; step < f; ++step) {
+    const int sb = upper ? f - 1 - step : step;  // sub-block being solved
+    const int o = sb * cb;
+    // residual of sub-block sb: vin_sb - sum over solved sub-blocks
+    //   forward:  L[sb][s'] sol_s' for s' < sb  (rows o.., cols < o)
+    //   backward: L[s'][sb]^T sol_s' for s' > sb (rows > o+cb, cols o..)
+    if (!upper) {
+      for (int r = warp; r < cb; r += nw) {
+        // 4 independent partial sums keep several loads in flight
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        const double* row = D + (int64_t)(o + r) * b;
+        int c = lane;
+        for (; c + 96 < o; c += 128) {
+          a0 = fma(row[c], sol[c], a0);
+          a1 = fma(row[c + 32], sol[c + 32], a1);
+          a2 = fma(row[c + 64], sol[c + 64], a2);
+          a3 = fma(row[c + 96], sol[c + 96], a3);
+        }
+        for (; c < o; c += 32) a0 = fma(row[c], sol[c], a0);
+        double acc = (a0 + a1) + (a2 + a3);
+        for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (lane == 0) vin[o + r] -= acc;
+      }
+    } else {
+      const int c = o + (tid % cb);  // column of L = row of L^T
+      const int stride = blockDim.x / cb;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int r = o + cb + tid / cb;
+      for (; r + 3 * stride < b; r += 4 * stride) {
+        a0 = fma(D[(int64_t)r * b + c], sol[r], a0);
+        a1 = fma(D[(int64_t)(r + stride) * b + c], sol[r + stride], a1);
+        a2 = fma(D[(int64_t)(r + 2 * stride) * b + c], sol[r + 2 * stride], a2);
+        a3 = fma(D[(int64_t)(r + 3 * stride) * b + c], sol[r + 3 * stride], a3);
+      }
+      for (; r < b; r += stride) a0 = fma(D[(int64_t)r * b + c], sol[r], a0);
+      const double acc = (a0 + a1) + (a2 + a3);
+      // reduce the blockDim / cb partials of each column
+      __shared__ double red[TRSV_DIAG_THREADS];
+      red[tid] = acc;
+      __syncthreads();
+      if (tid < cb) {
+        double t = 0.0;
+        for (int p = 0; p < (int)blockDim.x / cb; ++p) t += red[p * cb + tid];
+        vin[o + tid] -= t;
+      }
+    }
+    __syncthreads();
+    // sol_sb = W_sb vin_sb (forward) or W_sb^T vin_sb (backward)
+    const double* Wb = W + (i * f + sb) * (int64_t)cb * cb;
+    if (!upper) {
+      for (int r = warp; r < cb; r += nw) {
+        double acc = 0.0;
+        for (int c = lane; c <= r; c += 32) acc = fma(Wb[(int64_t)r * cb + c], vin[o + c], acc);
+        for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (lane == 0) sol[o + r] = acc;
+      }
+    } else {
+      __shared__ double red2[TRSV_DIAG_THREADS];
+      const int c = tid % cb;
+      double acc = 0.0;
+      for (int r = c + tid / cb; r < cb; r += blockDim.x / cb)
+        acc = fma(Wb[(int64_t)r * cb + c], vin[o + r], acc);
+      red2[tid] = acc;
+      __syncthreads();
+      if (tid < cb) {
+        double t = 0.0;
+        for (int p = 0; p < (int)blockDim.x / cb; ++p) t += red2[p * cb + tid];
+        sol[o + tid] = t;
+      }
+    }
+    __syncthreads();
+  }
+  for (int k = tid; k < b; k += blockDim.x) v[i * b + k] = sol[k];
 }
 
-__global__ void trsv_partial_kernel(const double* A, int64_t tile_lo,
-                                    const double* v, int b, int cb, int f,
-                                    int64_t I, int upper, double* part) {
-  const int64_t jj = blockIdx.y;
-  const int chunk = blockIdx.x;  // 32 outputs
-  __shared__ double vs[1024];
+// forward: v_k[rows] -= L_ki[rows, :] y_i for k = i+1 .. N-1 (blockIdx.y),
+//          32-row chunks (blockIdx.x)
+// backward: v_k[cols] -= L_ik[:, cols]^T x_i for k = 0 .. i-1, 32-col chunks
+__global__ void __launch_bounds__(256)
+    trsv_update_kernel(const double* A, int64_t tile_lo, double* v, int b,
+                       int64_t i, int upper) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t k = upper ? (int64_t)blockIdx.y : i + 1 + blockIdx.y;
+  const int o0 = blockIdx.x * 32;
+  extern __shared__ double yi[];  // [b]
   __shared__ double red[8][33];
-  const int64_t J = upper ? I + 1 + jj : jj;
-  const double* T = upper ? subblock(A, tile_lo, b, cb, f, J, I)
-                          : subblock(A, tile_lo, b, cb, f, I, J);
-  for (int k = threadIdx.x; k < cb; k += blockDim.x) vs[k] = v[J * cb + k];
+  for (int c = threadIdx.x; c < b; c += blockDim.x) yi[c] = v[i * b + c];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int o0 = chunk * 32;
   if (!upper) {
+    const double* T = A + (tri(k, i) - tile_lo) * (int64_t)b * b;
     for (int rr = warp; rr < 32; rr += 8) {
       const int r = o0 + rr;
+      if (r >= b) break;
       double acc = 0.0;
-      if (r < cb)
-        for (int c = lane; c < cb; c += 32) acc = fma(T[(int64_t)r * b + c], vs[c], acc);
+      for (int c = lane; c < b; c += 32) acc = fma(T[(int64_t)r * b + c], yi[c], acc);
       for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-      if (lane == 0 && r < cb) part[jj * cb + r] = acc;
+      if (lane == 0) v[k * b + r] -= acc;
     }
   } else {
+    const double* T = A + (tri(i, k) - tile_lo) * (int64_t)b * b;
     const int c = o0 + lane;
     double acc = 0.0;
-    if (c < cb)
-      for (int r = warp; r < cb; r += 8) acc = fma(T[(int64_t)r * b + c], vs[r], acc);
+    if (c < b)
+      for (int r = warp; r < b; r += 8) acc = fma(T[(int64_t)r * b + c], yi[r], acc);
     red[warp][lane] = acc;
     __syncthreads();
-    if (warp == 0 && c < cb) {
-      double s2 = 0.0;
-      for (int w = 0; w < 8; ++w) s2 += red[w][lane];
-      part[jj * cb + c] = s2;
-    }
-  }
-}
-
-__global__ void trsv_apply_kernel(const double* W, const double* rhs, double* v,
-                                  int cb, int64_t I, int upper,
-                                  const double* part, int64_t nparts) {
-  __shared__ double s[1024];
-  for (int k = threadIdx.x; k < cb; k += blockDim.x) {
-    double acc = rhs[I * cb + k];
-    for (int64_t p = 0; p < nparts; ++p) acc -= part[p * cb + k];
-    s[k] = acc;
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nw = blockDim.x >> 5;
-  const int o0 = blockIdx.x * 32;
-  if (!upper) {
-    for (int rr = warp; rr < 32; rr += nw) {
-      const int r = o0 + rr;
-      if (r >= cb) break;
-      double acc = 0.0;
-      for (int c = lane; c <= r; c += 32) acc = fma(W[(int64_t)r * cb + c], s[c], acc);
-      for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-      if (lane == 0) v[I * cb + r] = acc;
-    }
-  } else {
-    __shared__ double red[32][33];
-    const int c = o0 + lane;
-    double acc = 0.0;
-    if (c < cb)
-      for (int r = c + warp; r < cb; r += nw) acc = fma(W[(int64_t)r * cb + c], s[r], acc);
-    red[warp][lane] = acc;
-    __syncthreads();
-    if (warp == 0 && c < cb) {
+    if (warp == 0 && c < b) {
       double t = 0.0;
-      for (int w = 0; w < nw; ++w) t += red[w][lane];
-      v[I * cb + c] = t;
+      for (int w = 0; w < 8; ++w) t += red[w][lane];
+      v[k * b + c] -= t;
     }
   }
 }
@@ -1109,9 +1274,15 @@ static void alloc_inverses(hs_matrix* m) {
 }
 
 // In-place factorization of a single-rank matrix.
+static void potrf_run_dist(hs_ctx* c, hs_matrix* m);
+
 static void potrf_run(hs_ctx* c, hs_matrix* m) {
+  if (c->comm && m->layout == 1) {  // NCCL context: 2D block-cyclic path
+    potrf_run_dist(c, m);
+    return;
+  }
   HS_REQUIRE(c->world == 1, HS_ERR_CONFIG,
-             "multi-GPU Cholesky is not available in this build");
+             "multi-GPU Cholesky needs a cyclic matrix (hs_matrix_create_cyclic)");
   const int b = (int)m->b;
   const int cb = compute_block(b), f = b / cb;
   const bool fast = dmma_ok(b);
@@ -1170,8 +1341,8 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
     const int64_t t = N - 1 - j;
     if (fast) {
       for (int s = 0; s < f; ++s) {
-        diag128_kernel<<<1, 256, kDiagSmem, cs.p>>>(m->d, m->tile_lo, b, f, m->dinv,
-                                                    j * f + s, 0, flag);
+        diag128_kernel<<<1, 256, kDiagSmem, cs.p>>>(m->d, m->tile_lo, nullptr, b, f,
+                                                    m->dinv, j * f + s, 0, flag);
         HS_CUDA(cudaGetLastError());
         launch_count(c);
         if (s + 1 < f) {
@@ -1250,12 +1421,234 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
   HS_CUDA(cudaStreamWaitEvent(c->stream, pend));
   HS_CUDA(cudaStreamWaitEvent(c->stream, uend));
   check_finite_kernel<<<4 * 148, 256, 0, c->stream>>>(
-      m->d, m->tile_lo, (int64_t)m->local_tiles(), b, flag);
+      m->d, m->tile_lo, nullptr, (int64_t)m->local_tiles(), b, flag);
   HS_CUDA(cudaGetLastError());
   launch_count(c);
   CholFlag h{};
   HS_CUDA(cudaMemcpyAsync(&h, flag, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
+  throw_flag(h);
+  m->has_inv = true;
+}
+
+
+// ---------------------------------------------------------------------------
+// Distributed factorization: 2D block-cyclic tiles over a P x Q grid
+// (hs_matrix_create_cyclic), one process per GPU, NCCL over NVLink.
+// Per column j:
+//   owner(j,j): POTRF/TRTRI of the diagonal tile (diag128 + DMMA GEMMs)
+//   broadcast L_jj and its 128^2 inverse blocks to every rank
+//   owners of panel tiles (i, j): in-place blocked TRSM (DMMA)
+//   broadcast every panel tile from its owner into the panel buffer PB
+//   every rank: A_ik -= PB_i PB_k^T on its own trailing tiles
+// with the same one-column lookahead as the single-GPU path (P stream:
+// diagonal, TRSM and all NCCL calls, in the same order on every rank; U
+// stream: updates, the column j+1 tiles first).
+
+void comm_bcast_on(hs_ctx* c, const double* send, double* recv, size_t count,
+                   int root, cudaStream_t s);
+void comm_group(hs_ctx* c, bool start);
+void comm_allreduce_max_i64(hs_ctx* c, int64_t* buf, size_t count, cudaStream_t s);
+
+static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
+  const int b = (int)m->b;
+  HS_REQUIRE(dmma_ok(b), HS_ERR_CONFIG,
+             "distributed Cholesky needs a block size that is a multiple of 128");
+  HS_REQUIRE(m->layout == 1, HS_ERR_CONFIG,
+             "distributed Cholesky needs a cyclic matrix (hs_matrix_create_cyclic)");
+  const int cb = 128, f = b / cb;
+  const int64_t N = (int64_t)m->N;
+  const int64_t bb = (int64_t)b * b;
+  const int P = m->P, Q = m->Q, me = c->rank;
+  set_tile_kernel_attrs(b);
+  alloc_inverses(m);
+  m->has_inv = false;
+
+  // host work lists: per column, the owned panel rows and owned trailing
+  // pairs (COL part k == j+1 first, then REST), concatenated
+  std::vector<int32_t> rows, pairs;
+  std::vector<int64_t> row_off(N + 1, 0), col_off(N + 1, 0), rest_off(N + 1, 0);
+  for (int64_t j = 0; j < N; ++j) {
+    row_off[j] = (int64_t)rows.size();
+    for (int64_t i = j + 1; i < N; ++i)
+      if (cyclic_owner(i, j, P, Q) == me) rows.push_back((int32_t)i);
+    col_off[j] = (int64_t)pairs.size() / 2;
+    for (int64_t i = j + 1; i < N; ++i)
+      if (cyclic_owner(i, j + 1, P, Q) == me) {
+        pairs.push_back((int32_t)i);
+        pairs.push_back((int32_t)(j + 1));
+      }
+    rest_off[j] = (int64_t)pairs.size() / 2;
+    for (int64_t i = j + 2; i < N; ++i)
+      for (int64_t k = j + 2; k <= i; ++k)
+        if (cyclic_owner(i, k, P, Q) == me) {
+          pairs.push_back((int32_t)i);
+          pairs.push_back((int32_t)k);
+        }
+  }
+  row_off[N] = (int64_t)rows.size();
+  col_off[N] = rest_off[N] = (int64_t)pairs.size() / 2;
+
+  CholFlag* flag = nullptr;
+  int32_t *d_rows = nullptr, *d_pairs = nullptr;
+  double *Ld = nullptr, *Wb = nullptr, *PB[2] = {nullptr, nullptr};
+  int64_t* d_status = nullptr;
+  struct Guard {
+    std::vector<void*> p;
+    ~Guard() {
+      for (void* q : p) cudaFree(q);
+    }
+  } guard;
+  const int64_t panel = std::max<int64_t>(N - 1, 1);
+  HS_CUDA(cudaMalloc(&flag, sizeof(CholFlag)));
+  guard.p.push_back(flag);
+  HS_CUDA(cudaMalloc(&d_rows, std::max<size_t>(rows.size(), 1) * sizeof(int32_t)));
+  guard.p.push_back(d_rows);
+  HS_CUDA(cudaMalloc(&d_pairs, std::max<size_t>(pairs.size(), 2) * sizeof(int32_t)));
+  guard.p.push_back(d_pairs);
+  HS_CUDA(cudaMalloc(&Ld, bb * sizeof(double)));
+  guard.p.push_back(Ld);
+  HS_CUDA(cudaMalloc(&Wb, (int64_t)f * cb * cb * sizeof(double)));
+  guard.p.push_back(Wb);
+  for (int k = 0; k < 2; ++k) {
+    HS_CUDA(cudaMalloc(&PB[k], panel * bb * sizeof(double)));
+    guard.p.push_back(PB[k]);
+  }
+  HS_CUDA(cudaMalloc(&d_status, 3 * sizeof(int64_t)));
+  guard.p.push_back(d_status);
+  if (!rows.empty())
+    HS_CUDA(cudaMemcpy(d_rows, rows.data(), rows.size() * sizeof(int32_t),
+                       cudaMemcpyHostToDevice));
+  if (!pairs.empty())
+    HS_CUDA(cudaMemcpy(d_pairs, pairs.data(), pairs.size() * sizeof(int32_t),
+                       cudaMemcpyHostToDevice));
+  HS_CUDA(cudaMemsetAsync(flag, 0, sizeof(CholFlag), c->stream));
+
+  ColStreams cs;
+  int lo_pri, hi_pri;
+  HS_CUDA(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
+  HS_CUDA(cudaStreamCreateWithPriority(&cs.p, cudaStreamNonBlocking, hi_pri));
+  HS_CUDA(cudaStreamCreateWithPriority(&cs.u, cudaStreamNonBlocking, lo_pri));
+  cudaEvent_t start = cs.make();
+  HS_CUDA(cudaEventRecord(start, c->stream));
+  HS_CUDA(cudaStreamWaitEvent(cs.p, start));
+  HS_CUDA(cudaStreamWaitEvent(cs.u, start));
+
+  const CUtensorMap mapA = tile_map(m->d, b, std::max<int64_t>((int64_t)m->local_tiles(), 1));
+  const CUtensorMap mapW = tile_map(m->dinv, cb, N * f);
+  const CUtensorMap mapLd = tile_map(Ld, b, 1);
+  const CUtensorMap mapWb = tile_map(Wb, cb, f);
+  const CUtensorMap mapPB[2] = {tile_map(PB[0], b, panel), tile_map(PB[1], b, panel)};
+
+  GemmArgs g{};
+  g.N = N;
+  g.b = b;
+  g.cb = cb;
+  g.f = f;
+  g.A = m->d;
+  g.tile_lo = 0;
+  g.lpos = m->d_lpos;
+  g.flag = flag;
+
+  auto panel_work = [&](int64_t j) {
+    const int dj = cyclic_owner(j, j, P, Q);
+    if (dj == me) {  // diagonal tile (local)
+      for (int s = 0; s < f; ++s) {
+        diag128_kernel<<<1, 256, kDiagSmem, cs.p>>>(m->d, 0, m->d_lpos, b, f, m->dinv,
+                                                    j * f + s, 0, flag);
+        HS_CUDA(cudaGetLastError());
+        launch_count(c);
+        if (s + 1 < f) {
+          GemmArgs gd = g;
+          gd.j = j;
+          gd.step = s;
+          gd.W = m->dinv;
+          gd.mode = G_DIAG_TRSM;
+          launch_gemm(c, cs.p, gd, f - 1 - s, &mapA, &mapW);
+          gd.mode = G_DIAG_UPD;
+          const int64_t tt = f - 1 - s;
+          launch_gemm(c, cs.p, gd, tt * (tt + 1) / 2, &mapA, &mapA);
+        }
+      }
+    }
+    // L_jj and its inverse blocks to every rank
+    const int64_t dslot = m->lpos[tri(j, j)];
+    comm_group(c, true);
+    comm_bcast_on(c, dj == me ? m->d + dslot * bb : nullptr, Ld, (size_t)bb, dj, cs.p);
+    comm_bcast_on(c, dj == me ? m->dinv + j * f * (int64_t)cb * cb : nullptr, Wb,
+                  (size_t)f * cb * cb, dj, cs.p);
+    comm_group(c, false);
+    // TRSM of the owned panel tiles (in place)
+    const int64_t nr = row_off[j + 1] - row_off[j];
+    if (nr > 0) {
+      for (int cc = 0; cc < f; ++cc) {
+        GemmArgs gp = g;
+        gp.j = j;
+        gp.step = cc;
+        gp.list = d_rows + row_off[j];
+        gp.X = Ld;
+        gp.W = Wb;
+        if (cc > 0) {
+          gp.mode = G_DIST_PANEL_UPD;
+          launch_gemm(c, cs.p, gp, nr * f, &mapA, &mapLd);
+        }
+        gp.mode = G_DIST_PANEL_TRSM;
+        launch_gemm(c, cs.p, gp, nr * f, &mapA, &mapWb);
+      }
+    }
+    // every panel tile from its owner into PB[j & 1] on every rank
+    if (j + 1 < N) {
+      comm_group(c, true);
+      for (int64_t i = j + 1; i < N; ++i) {
+        const int own = cyclic_owner(i, j, P, Q);
+        const double* send = own == me ? m->d + m->lpos[tri(i, j)] * bb : nullptr;
+        comm_bcast_on(c, send, PB[j & 1] + (i - j - 1) * bb, (size_t)bb, own, cs.p);
+      }
+      comm_group(c, false);
+    }
+  };
+
+  panel_work(0);
+  for (int64_t j = 0; j < N; ++j) {
+    cudaEvent_t pdone = cs.make();
+    HS_CUDA(cudaEventRecord(pdone, cs.p));
+    if (j + 1 >= N) break;
+    HS_CUDA(cudaStreamWaitEvent(cs.u, pdone));
+    GemmArgs gu = g;
+    gu.j = j;
+    gu.mode = G_DIST_UPDATE;
+    gu.X = PB[j & 1];
+    gu.list = d_pairs + 2 * col_off[j];
+    launch_gemm(c, cs.u, gu, (rest_off[j] - col_off[j]) * f * f, &mapPB[j & 1], &mapPB[j & 1]);
+    cudaEvent_t ucol = cs.make();
+    HS_CUDA(cudaEventRecord(ucol, cs.u));
+    HS_CUDA(cudaStreamWaitEvent(cs.p, ucol));
+    gu.list = d_pairs + 2 * rest_off[j];
+    launch_gemm(c, cs.u, gu, (col_off[j + 1] - rest_off[j]) * f * f, &mapPB[j & 1],
+                &mapPB[j & 1]);
+    panel_work(j + 1);
+  }
+  cudaEvent_t pend = cs.make(), uend = cs.make();
+  HS_CUDA(cudaEventRecord(pend, cs.p));
+  HS_CUDA(cudaEventRecord(uend, cs.u));
+  HS_CUDA(cudaStreamWaitEvent(c->stream, pend));
+  HS_CUDA(cudaStreamWaitEvent(c->stream, uend));
+  check_finite_kernel<<<4 * 148, 256, 0, c->stream>>>(
+      m->d, 0, m->d_owned, (int64_t)m->local_tiles(), b, flag);
+  HS_CUDA(cudaGetLastError());
+  launch_count(c);
+  // agree on the outcome: element-wise max of (status, column, pivot)
+  CholFlag h{};
+  HS_CUDA(cudaMemcpyAsync(&h, flag, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  int64_t st[3] = {h.status, h.status ? h.col : -1, h.status ? h.pivot : -1};
+  HS_CUDA(cudaMemcpy(d_status, st, sizeof(st), cudaMemcpyHostToDevice));
+  comm_allreduce_max_i64(c, d_status, 3, c->stream);
+  HS_CUDA(cudaMemcpyAsync(st, d_status, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  h.status = (int32_t)st[0];
+  h.col = st[1];
+  h.pivot = st[2];
   throw_flag(h);
   m->has_inv = true;
 }
@@ -1273,7 +1666,7 @@ static void ensure_inverses(hs_ctx* c, hs_matrix* m) {
   HS_CUDA(cudaMemsetAsync(flag, 0, sizeof(CholFlag), c->stream));
   if (dmma_ok(b)) {
     diag128_kernel<<<(unsigned)(N * f), 256, kDiagSmem, c->stream>>>(
-        m->d, m->tile_lo, b, f, m->dinv, 0, 1, flag);
+        m->d, m->tile_lo, m->d_lpos, b, f, m->dinv, 0, 1, flag);
   } else {
     trtri_tile_kernel<<<(unsigned)N, 256, trtri_smem(b), c->stream>>>(
         m->d, m->tile_lo, m->dinv, b, flag, 0);
@@ -1293,33 +1686,29 @@ static void trsv_run(hs_ctx* c, hs_matrix* m, double* v, bool upper) {
   ensure_inverses(c, m);
   const int b = (int)m->b;
   const int cb = compute_block(b), f = b / cb;
-  HS_REQUIRE(cb <= 1024, HS_ERR_CONFIG, "block size unsupported in trsv");
-  const int64_t NB = (int64_t)m->N * f;  // cb-sized sub-rows
-  // rhs snapshot: the apply step reads sub-row I of it and writes v, so no
-  // CTA reads a value another CTA of the same step already overwrote
-  double *part = nullptr, *rhs = nullptr;
-  HS_CUDA(cudaMalloc(&part, std::max<int64_t>(NB, 1) * cb * sizeof(double)));
-  HS_CUDA(cudaMalloc(&rhs, NB * cb * sizeof(double)));
-  HS_CUDA(cudaMemcpyAsync(rhs, v, NB * cb * sizeof(double), cudaMemcpyDeviceToDevice,
-                          c->stream));
-  const int chunks = (cb + 31) / 32;
-  for (int64_t s = 0; s < NB; ++s) {
-    const int64_t I = upper ? NB - 1 - s : s;
-    const int64_t np = upper ? NB - 1 - I : I;
-    if (np > 0) {
-      trsv_partial_kernel<<<dim3(chunks, (unsigned)np), 256, 0, c->stream>>>(
-          m->d, m->tile_lo, v, b, cb, f, I, upper ? 1 : 0, part);
-      HS_CUDA(cudaGetLastError());
+  HS_REQUIRE(b <= 2048 && cb <= TRSV_DIAG_THREADS, HS_ERR_CONFIG,
+             "block size unsupported in the triangular solves");
+  const int64_t N = (int64_t)m->N;
+  const int chunks = (b + 31) / 32;
+  const size_t dsm = 2 * (size_t)b * sizeof(double), usm = (size_t)b * sizeof(double);
+  if (dsm > 48 * 1024)
+    HS_CUDA(cudaFuncSetAttribute(trsv_diag_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+  for (int64_t s = 0; s < N; ++s) {
+    const int64_t i = upper ? N - 1 - s : s;
+    HS_CUDA(launch_pdl(trsv_diag_kernel, dim3(1), dim3(TRSV_DIAG_THREADS / cb * cb), dsm, c->stream,
+                       (const double*)m->d, m->tile_lo, (const double*)m->dinv, v, b, cb, f,
+                       i, upper ? 1 : 0));
+    launch_count(c);
+    const int64_t nk = upper ? i : N - 1 - i;
+    if (nk > 0) {
+      HS_CUDA(launch_pdl(trsv_update_kernel, dim3(chunks, (unsigned)nk), dim3(256), usm,
+                         c->stream, (const double*)m->d, m->tile_lo, v, b, i,
+                         upper ? 1 : 0));
       launch_count(c);
     }
-    trsv_apply_kernel<<<chunks, 256, 0, c->stream>>>(m->dinv + I * cb * cb, rhs, v, cb,
-                                                     I, upper ? 1 : 0, part, np);
-    HS_CUDA(cudaGetLastError());
-    launch_count(c);
   }
   HS_CUDA(cudaStreamSynchronize(c->stream));
-  cudaFree(part);
-  cudaFree(rhs);
 }
 
 }  // namespace hs

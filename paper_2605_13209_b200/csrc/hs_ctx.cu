@@ -106,6 +106,26 @@ void comm_broadcast(hs_ctx* c, double* buf, size_t count, int root) {
                                 (ncclComm_t)c->comm, c->stream),
              "ncclBroadcast");
 }
+// broadcast from root's `send` into every rank's `recv` on stream s
+void comm_bcast_on(hs_ctx* c, const double* send, double* recv, size_t count,
+                   int root, cudaStream_t s) {
+  nccl_check(c->nccl,
+             c->nccl->Broadcast(send, recv, count, ncclFloat64, root,
+                                (ncclComm_t)c->comm, s),
+             "ncclBroadcast");
+}
+void comm_group(hs_ctx* c, bool start) {
+  nccl_check(c->nccl, start ? c->nccl->GroupStart() : c->nccl->GroupEnd(),
+             "ncclGroupStart/End");
+}
+// element-wise max over ranks of `count` int64 values (in place)
+void comm_allreduce_max_i64(hs_ctx* c, int64_t* buf, size_t count,
+                            cudaStream_t s) {
+  nccl_check(c->nccl,
+             c->nccl->AllReduce(buf, buf, count, ncclInt64, ncclMax,
+                                (ncclComm_t)c->comm, s),
+             "ncclAllReduce");
+}
 
 // ---------------------------------------------------------------------------
 // host generators — genmat.cpp:16-34, 45-54, 77-112, 156-162 (exact)
@@ -190,11 +210,12 @@ static std::vector<int64_t> row_bounds(int64_t N, int world) {
 
 template <int DIM>  // DIM > 0: compile-time dimension; 0: runtime `dim`
 __global__ void __launch_bounds__(256)
-    assemble_se_kernel(double* __restrict__ tiles, int64_t tile_base, int64_t n,
+    assemble_se_kernel(double* __restrict__ tiles, int64_t tile_base,
+                       const int64_t* __restrict__ owned, int64_t n,
                        int b, const double* __restrict__ pts, int dim,
                        double sf2, double inv2l2, double sn2,
                        int rows_per_cta) {
-  const int64_t t = tile_base + blockIdx.x;
+  const int64_t t = owned ? owned[blockIdx.x] : tile_base + blockIdx.x;
   const int64_t i = tile_row(t);
   const int64_t j = t - tri(i, 0);
   const int r0 = blockIdx.y * rows_per_cta;
@@ -240,12 +261,15 @@ __global__ void __launch_bounds__(256)
 
 // identity padding of an uploaded/zeroed matrix's last block row
 // (blocked_matrix.cpp:57-74)
-__global__ void identity_pad_kernel(double* tiles, int64_t tile_base, int64_t n,
-                                    int b, int64_t N) {
+__global__ void identity_pad_kernel(double* tiles, int64_t tile_base,
+                                    const int64_t* lpos, int64_t n, int b,
+                                    int64_t N) {
   const int64_t last = N - 1;
   const int64_t t = tri(last, 0) + blockIdx.x;  // tile (last, j)
   const int64_t j = blockIdx.x;
-  double* blk = tiles + (t - tile_base) * b * b;
+  const int64_t slot = lpos ? lpos[j] : t - tile_base;
+  if (slot < 0) return;  // not on this rank
+  double* blk = tiles + slot * b * b;
   for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
     const int r = idx / b, c = idx % b;
     const int64_t p = last * b + r, q = j * b + c;
@@ -287,17 +311,73 @@ static void assemble(hs_matrix* m, const double* h_pts, size_t dim, double sf2,
   const int threads = std::min(256, std::max(32, (b + 31) / 32 * 32));
   if (dim == 2)
     assemble_se_kernel<2><<<grid, threads, 0, c->stream>>>(
-        m->d, m->tile_lo, (int64_t)m->n, b, d_pts, (int)dim, sf2, inv2l2, sn2,
-        rows_per_cta);
+        m->d, m->tile_lo, m->d_owned, (int64_t)m->n, b, d_pts, (int)dim, sf2, inv2l2,
+        sn2, rows_per_cta);
   else
     assemble_se_kernel<0><<<grid, threads, 0, c->stream>>>(
-        m->d, m->tile_lo, (int64_t)m->n, b, d_pts, (int)dim, sf2, inv2l2, sn2,
-        rows_per_cta);
+        m->d, m->tile_lo, m->d_owned, (int64_t)m->n, b, d_pts, (int)dim, sf2, inv2l2,
+        sn2, rows_per_cta);
   HS_CUDA(cudaGetLastError());
   launch_count(c);
   HS_CUDA(cudaFreeAsync(d_pts, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
   m->has_inv = false;
+}
+
+// ---- read-bandwidth probes (diagnostics) ----------------------------------
+
+__global__ void __launch_bounds__(288, 1)
+    probe_bulk_kernel(const double* __restrict__ src, int64_t slabs, double* sink) {
+  constexpr int NS = 5, SLAB = 32768;
+  extern __shared__ __align__(128) unsigned char psmem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(psmem + NS * SLAB);
+  uint64_t* empty = full + NS;
+  const int tid = threadIdx.x;
+  const int64_t g0 = slabs * blockIdx.x / gridDim.x, g1 = slabs * (blockIdx.x + 1) / gridDim.x;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid >= 256) {
+    if (tid == 256)
+      for (int64_t g = g0; g < g1; ++g) {
+        const int64_t k = g - g0;
+        const int st = (int)(k % NS);
+        if (k >= NS) mbar_wait(&empty[st], (uint32_t)(((k / NS) - 1) & 1));
+        mbar_arrive_expect_tx(&full[st], SLAB);
+        bulk_g2s(psmem + st * SLAB, src + g * (SLAB / 8), SLAB, &full[st]);
+      }
+    return;
+  }
+  double acc = 0.0;
+  for (int64_t g = g0; g < g1; ++g) {
+    const int64_t k = g - g0;
+    const int st = (int)(k % NS);
+    mbar_wait(&full[st], (uint32_t)((k / NS) & 1));
+    const double2* p = reinterpret_cast<const double2*>(psmem + st * SLAB);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {  // consumers read the slab like the SYMV
+      const double2 v = p[tid + 256 * m];
+      acc += v.x + v.y;
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[st]);
+  }
+  if (acc == 123.456) *sink = acc;
+}
+
+__global__ void probe_ldg_kernel(const double2* __restrict__ src, int64_t n2, double* sink) {
+  double acc = 0.0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n2;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = __ldcs(src + k);
+    acc += v.x + v.y;
+  }
+  if (acc == 123.456) *sink = acc;
 }
 
 hs_matrix* cached_matrix(hs_ctx* c, int slot, size_t n, size_t b) {
@@ -545,7 +625,7 @@ hs_status hs_matrix_create(hs_ctx* c, size_t n, size_t b, hs_matrix** out) {
       HS_CUDA(cudaMemsetAsync(m->d, 0, bytes, c->stream));
       if (m->row_hi == m->N && m->N * b != n) {
         identity_pad_kernel<<<(unsigned)m->N, 256, 0, c->stream>>>(
-            m->d, m->tile_lo, (int64_t)n, (int)b, (int64_t)m->N);
+            m->d, m->tile_lo, nullptr, (int64_t)n, (int)b, (int64_t)m->N);
         HS_CUDA(cudaGetLastError());
         launch_count(c);
       }
@@ -561,11 +641,78 @@ hs_status hs_matrix_create(hs_ctx* c, size_t n, size_t b, hs_matrix** out) {
   HS_API_END
 }
 
+hs_status hs_matrix_create_cyclic(hs_ctx* c, size_t n, size_t b, hs_matrix** out) {
+  HS_API_BEGIN
+  HS_REQUIRE(c && out, HS_ERR_CONFIG, "null pointer");
+  HS_REQUIRE(n > 0 && b > 0, HS_ERR_CONFIG,
+             "matrix size and block size must be positive");
+  HS_CUDA(cudaSetDevice(c->device));
+  hs_matrix* m = new hs_matrix;
+  m->ctx = c;
+  m->n = n;
+  m->b = b;
+  m->N = (size_t)ceil_div(n, b);
+  m->layout = 1;
+  cyclic_grid(c->world, &m->P, &m->Q);
+  const int64_t N = (int64_t)m->N, T = tri(N, 0);
+  m->lpos.assign(T, -1);
+  std::vector<int64_t> last_row_slot(N, -1);
+  for (int64_t i = 0; i < N; ++i)
+    for (int64_t j = 0; j <= i; ++j)
+      if (cyclic_owner(i, j, m->P, m->Q) == c->rank) {
+        m->lpos[tri(i, j)] = (int64_t)m->owned.size();
+        if (i == N - 1) last_row_slot[j] = (int64_t)m->owned.size();
+        m->owned.push_back(tri(i, j));
+      }
+  m->row_lo = 0;
+  m->row_hi = m->N;
+  m->tile_lo = 0;
+  m->tile_hi = T;
+  m->bounds = {0, (int64_t)m->N};
+  m->vec_len = (int64_t)(m->N * b);
+  try {
+    const size_t bytes = m->local_tiles() * b * b * sizeof(double);
+    if (bytes) HS_CUDA(cudaMalloc(&m->d, bytes));
+    HS_CUDA(cudaMalloc(&m->d_owned, std::max<size_t>(1, m->owned.size()) * sizeof(int64_t)));
+    HS_CUDA(cudaMalloc(&m->d_lpos, T * sizeof(int64_t)));
+    HS_CUDA(cudaMemcpy(m->d_lpos, m->lpos.data(), T * sizeof(int64_t), cudaMemcpyHostToDevice));
+    if (!m->owned.empty())
+      HS_CUDA(cudaMemcpy(m->d_owned, m->owned.data(), m->owned.size() * sizeof(int64_t),
+                         cudaMemcpyHostToDevice));
+    if (bytes) {
+      HS_CUDA(cudaMemsetAsync(m->d, 0, bytes, c->stream));
+      if (m->N * b != n) {
+        int64_t* d_slot = nullptr;
+        HS_CUDA(cudaMalloc(&d_slot, N * sizeof(int64_t)));
+        HS_CUDA(cudaMemcpy(d_slot, last_row_slot.data(), N * sizeof(int64_t),
+                           cudaMemcpyHostToDevice));
+        identity_pad_kernel<<<(unsigned)N, 256, 0, c->stream>>>(m->d, 0, d_slot, (int64_t)n,
+                                                                (int)b, N);
+        HS_CUDA(cudaGetLastError());
+        launch_count(c);
+        HS_CUDA(cudaStreamSynchronize(c->stream));
+        cudaFree(d_slot);
+      }
+      HS_CUDA(cudaStreamSynchronize(c->stream));
+    }
+  } catch (...) {
+    cudaFree(m->d);
+    cudaFree(m->d_owned);
+    cudaFree(m->d_lpos);
+    delete m;
+    throw;
+  }
+  *out = m;
+  HS_API_END
+}
+
 void hs_matrix_destroy(hs_matrix* m) {
   if (!m) return;
   cudaSetDevice(m->ctx->device);
   cudaStreamSynchronize(m->ctx->stream);
   if (m->plan) free_plan(m->plan);
+  cudaFree(m->d_owned);
+  cudaFree(m->d_lpos);
   cudaFree(m->d);
   cudaFree(m->dinv);
   cudaFree(m->d_row_off);
@@ -583,9 +730,27 @@ hs_status hs_matrix_info(const hs_matrix* m, size_t* n, size_t* b,
   HS_API_END
 }
 
+static void cyclic_copy(hs_matrix* m, double* host, bool to_device) {
+  const size_t bb = m->b * m->b;
+  for (size_t k = 0; k < m->owned.size(); ++k) {
+    double* h = host + (size_t)m->owned[k] * bb;
+    double* d = m->d + k * bb;
+    HS_CUDA(cudaMemcpyAsync(to_device ? (void*)d : (void*)h, to_device ? (void*)h : (void*)d,
+                            bb * sizeof(double),
+                            to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
+                            m->ctx->stream));
+  }
+  HS_CUDA(cudaStreamSynchronize(m->ctx->stream));
+}
+
 hs_status hs_matrix_upload(hs_matrix* m, const double* host) {
   HS_API_BEGIN
   HS_REQUIRE(m && host, HS_ERR_CONFIG, "null pointer");
+  if (m->layout == 1) {
+    cyclic_copy(m, const_cast<double*>(host), true);
+    m->has_inv = false;
+    return HS_OK;
+  }
   const size_t bytes = m->local_tiles() * m->b * m->b * sizeof(double);
   if (bytes)
     HS_CUDA(cudaMemcpyAsync(m->d, host + (size_t)m->tile_lo * m->b * m->b,
@@ -598,6 +763,10 @@ hs_status hs_matrix_upload(hs_matrix* m, const double* host) {
 hs_status hs_matrix_download(const hs_matrix* m, double* host) {
   HS_API_BEGIN
   HS_REQUIRE(m && host, HS_ERR_CONFIG, "null pointer");
+  if (m->layout == 1) {
+    cyclic_copy(const_cast<hs_matrix*>(m), host, false);
+    return HS_OK;
+  }
   const size_t bytes = m->local_tiles() * m->b * m->b * sizeof(double);
   if (bytes)
     HS_CUDA(cudaMemcpyAsync(host + (size_t)m->tile_lo * m->b * m->b, m->d,
@@ -609,7 +778,8 @@ hs_status hs_matrix_download(const hs_matrix* m, double* host) {
 hs_status hs_matrix_copy(hs_matrix* dst, const hs_matrix* src) {
   HS_API_BEGIN
   HS_REQUIRE(dst && src, HS_ERR_CONFIG, "null pointer");
-  HS_REQUIRE(dst->ctx == src->ctx && dst->n == src->n && dst->b == src->b,
+  HS_REQUIRE(dst->ctx == src->ctx && dst->n == src->n && dst->b == src->b &&
+                 dst->layout == src->layout,
              HS_ERR_CONFIG, "matrix shapes do not match");
   const size_t bytes = src->local_tiles() * src->b * src->b * sizeof(double);
   if (bytes)
@@ -645,6 +815,47 @@ hs_status hs_generate_spd(hs_matrix* m, double sf2, double length_scale,
   const double ell =
       length_scale > 0.0 ? length_scale : median_dist(pts.data(), m->n, dim);
   assemble(m, pts.data(), dim, sf2, 1.0 / (2.0 * ell * ell), sn2);
+  HS_API_END
+}
+
+hs_status hs_probe_hbm_read(hs_ctx* c, size_t bytes, int mode, int reps,
+                            double* gbs) {
+  HS_API_BEGIN
+  HS_REQUIRE(c && gbs && bytes >= (1u << 20), HS_ERR_CONFIG, "bad probe arguments");
+  HS_CUDA(cudaSetDevice(c->device));
+  bytes &= ~size_t(32767);
+  double* buf = nullptr;
+  double* sink = nullptr;
+  HS_CUDA(cudaMalloc(&buf, bytes));
+  HS_CUDA(cudaMalloc(&sink, 8));
+  cudaEvent_t e0, e1;
+  HS_CUDA(cudaEventCreate(&e0));
+  HS_CUDA(cudaEventCreate(&e1));
+  HS_CUDA(cudaMemsetAsync(buf, 0, bytes, c->stream));
+  const int smem = 5 * 32768 + 128;
+  HS_CUDA(cudaFuncSetAttribute(probe_bulk_kernel,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  float best = 1e30f;
+  for (int r = 0; r < std::max(reps, 1) + 1; ++r) {
+    HS_CUDA(cudaEventRecord(e0, c->stream));
+    if (mode == 0)
+      probe_bulk_kernel<<<c->num_sms, 288, smem, c->stream>>>(buf, (int64_t)(bytes / 32768),
+                                                              sink);
+    else
+      probe_ldg_kernel<<<c->num_sms * 8, 512, 0, c->stream>>>(
+          reinterpret_cast<const double2*>(buf), (int64_t)(bytes / 16), sink);
+    HS_CUDA(cudaGetLastError());
+    HS_CUDA(cudaEventRecord(e1, c->stream));
+    HS_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    HS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (r > 0) best = std::min(best, ms);  // first run is a warm-up
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(buf);
+  cudaFree(sink);
+  *gbs = (double)bytes / (best * 1e-3) / 1e9;
   HS_API_END
 }
 

@@ -85,6 +85,14 @@ struct hs_ctx {
 
 struct hs_matrix {
   hs_ctx* ctx = nullptr;
+  // layout: 0 = row-sharded (CG; the full matrix when world == 1),
+  //         1 = 2D block-cyclic over a P x Q grid (distributed Cholesky)
+  int layout = 0;
+  int P = 1, Q = 1;
+  std::vector<int64_t> owned;      // cyclic: global tile ids held, ascending
+  int64_t* d_owned = nullptr;      // cyclic: device copy of `owned`
+  std::vector<int64_t> lpos;       // cyclic: global tile -> local slot or -1
+  int64_t* d_lpos = nullptr;       // cyclic: device copy of `lpos`
   size_t n = 0, b = 0, N = 0;     // logical size, tile size, block rows
   size_t row_lo = 0, row_hi = 0;  // owned block rows
   int64_t tile_lo = 0, tile_hi = 0;  // owned packed tile range
@@ -98,10 +106,26 @@ struct hs_matrix {
   std::vector<int64_t> bounds;    // world+1 block-row bounds
   int64_t vec_len = 0;            // doubles in a full (padded) vector
   int64_t* d_row_off = nullptr;   // [N] element offset of block row i
-  size_t local_tiles() const { return (size_t)(tile_hi - tile_lo); }
+  size_t local_tiles() const {
+    return layout == 1 ? owned.size() : (size_t)(tile_hi - tile_lo);
+  }
 };
 
 namespace hs {
+
+// 2D block-cyclic grid for G ranks: P x Q with P <= Q, P the largest divisor
+// of G not above sqrt(G) (1x1, 1x2, 2x2, 2x4, ...); tile (i, j) -> rank
+// (i mod P) * Q + (j mod Q).
+inline void cyclic_grid(int world, int* P, int* Q) {
+  int p = 1;
+  for (int d = 1; d * d <= world; ++d)
+    if (world % d == 0) p = d;
+  *P = p;
+  *Q = world / p;
+}
+inline int cyclic_owner(int64_t i, int64_t j, int P, int Q) {
+  return (int)(i % P) * Q + (int)(j % Q);
+}
 
 void launch_count(hs_ctx* c, int k = 1);
 void ensure_plan(hs_matrix* m);

@@ -356,13 +356,16 @@ def default_runtime() -> Runtime:
 
 
 class DeviceMatrix:
-    """Packed tiles resident in HBM (this rank's block rows for multi-GPU)."""
+    """Packed tiles resident in HBM: this rank's block rows (CG layout) or,
+    with ``cyclic=True``, its tiles of the 2D block-cyclic distribution used
+    by the multi-GPU Cholesky."""
 
-    def __init__(self, rt: Runtime, n: int, b: int):
+    def __init__(self, rt: Runtime, n: int, b: int, cyclic: bool = False):
         self.rt, self.n, self.b = rt, int(n), int(b)
         self.rows = block_rows(n, b)
         h = C.c_void_p()
-        _check(rt._L.hs_matrix_create(rt.ctx, n, b, C.byref(h)))
+        create = rt._L.hs_matrix_create_cyclic if cyclic else rt._L.hs_matrix_create
+        _check(create(rt.ctx, n, b, C.byref(h)))
         self.h = h
         rt._matrices.add(self)
         lo, hi = C.c_size_t(), C.c_size_t()
@@ -436,10 +439,11 @@ def generate_rhs(n: int, b: int, seed: int) -> BlockVector:
 
 
 def generate_spd_device(rt: Runtime, n: int, b: int, params: KernelParams | None = None,
-                        seed: int = 42) -> DeviceMatrix:
-    """GP squared-exponential matrix assembled on the GPU (never on the host)."""
+                        seed: int = 42, cyclic: bool = False) -> DeviceMatrix:
+    """GP squared-exponential matrix assembled on the GPU (never on the host);
+    each rank assembles only the tiles it owns."""
     p = params or KernelParams()
-    m = DeviceMatrix(rt, n, b)
+    m = DeviceMatrix(rt, n, b, cyclic=cyclic)
     _check(rt._L.hs_generate_spd(m.h, p.sigma_f2, p.length_scale, p.sigma_n2, p.dim,
                                  seed))
     return m

@@ -432,3 +432,34 @@ def test_kernel_launches_are_counted(rt):
     before = rt.kernel_launches()
     hs.generate_spd(256, 128, seed=1, rt=rt)
     assert rt.kernel_launches() > before
+
+
+# ---------------------------------------------------------------------------
+# distributed Cholesky path (2D block-cyclic + NCCL broadcasts), exercised on
+# one GPU through a world-size-1 NCCL communicator
+
+
+@pytest.mark.parametrize("n,b", [(1024, 128), (2048, 512), (1500, 256)])
+def test_distributed_cholesky_world1_matches_oracle(oracle, n, b):
+    rt = hs.Runtime.distributed(0, 0, 1, hs.Runtime.nccl_unique_id())
+    try:
+        a = oracle.generate_spd(n, b, seed=42)
+        st, L_ref, _, _ = oracle.factorize(n, b, a)
+        m = hs.DeviceMatrix(rt, n, b, cyclic=True).upload(a)
+        H.potrf_device(rt, m)
+        got = m.download()
+        mask = lower_mask(n, b)
+        assert np.abs(got[mask] - L_ref[mask]).max() <= 1e-10 * np.abs(a[mask]).max()
+        # device-assembled cyclic matrix factors to the same L
+        m2 = hs.generate_spd_device(rt, n, b, seed=42, cyclic=True)
+        H.potrf_device(rt, m2)
+        assert np.abs(m2.download()[mask] - L_ref[mask]).max() <= 1e-10 * np.abs(a[mask]).max()
+        bad = a.copy()
+        k = (0 * 1 // 2 + 0) * b * b + 5 * b + 5  # element (5, 5) of tile (0, 0)
+        bad[k] = -1.0
+        m3 = hs.DeviceMatrix(rt, n, b, cyclic=True).upload(bad)
+        with pytest.raises(hs.NotSpdError) as ei:
+            H.potrf_device(rt, m3)
+        assert ei.value.block_row == 0 and ei.value.pivot_index == 5
+    finally:
+        rt.close()
