@@ -212,47 +212,60 @@ def dgemm_peak(torch) -> float:
     return 2 * n ** 3 / (best * 1e-3) / 1e12
 
 
-def cholesky_secondary(hs, H, rt, torch, args, peak_tf: float) -> dict:
+def cholesky_secondary(hs, H, rt, torch, args, peak_tf: float, world: int = 1,
+                       dist=None) -> dict:
+    """Tiled Cholesky GFLOP/s: single GPU, or 2D block-cyclic over `world`
+    GPUs (each rank assembles and factors its own tiles; max over ranks)."""
     n, b = args.chol_n, args.chol_b
-    m = hs.generate_spd_device(rt, n, b, seed=42)
-    work = hs.DeviceMatrix(rt, n, b)
-    nbytes = m.packed_len * 8
+    cyclic = dist is not None
+    m = hs.generate_spd_device(rt, n, b, seed=42, cyclic=cyclic)
+    work = hs.DeviceMatrix(rt, n, b, cyclic=cyclic)
     times = []
     launches0 = rt.kernel_launches()
     for rep in range(1 + args.chol_reps):
         work.copy_from(m)  # fresh input each repetition (device copy, untimed)
         torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         H.potrf_device(rt, work)
         e.record()
         e.synchronize()
         if rep > 0:
-            times.append(s.elapsed_time(e))
+            t = s.elapsed_time(e)
+            if dist is not None:
+                tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t = float(tt.item())
+            times.append(t)
     launches = (rt.kernel_launches() - launches0) // (1 + args.chol_reps)
     ms = statistics.median(times)
     gflops = n ** 3 / 3 / (ms * 1e-3) / 1e9
-    # solve (substitutions) once, for the record
-    rhs = torch.from_numpy(hs.generate_rhs(n, b, 42).values).cuda()
-    x = torch.empty_like(rhs)
-    torch.cuda.synchronize()
-    t0 = time.time()
-    x.copy_(rhs)
-    H.trsv_device(rt, work, x.data_ptr(), upper=False)
-    H.trsv_device(rt, work, x.data_ptr(), upper=True)
-    torch.cuda.synchronize()
-    solve_ms = (time.time() - t0) * 1e3
-    res = H.true_residual_device(rt, m, x.data_ptr(), rhs.data_ptr())
-    rel = res / float(torch.linalg.vector_norm(rhs[:n]))
     out = {"metric": "cholesky_gflops", "value": gflops, "unit": "GFLOP/s",
-           "ms_per_factor": ms, "solve_ms": solve_ms, "relative_residual": rel,
-           "config": {"workload": "tiled Cholesky + substitutions (configs[2])", "n": n,
-                      "b": b, "flops": "n^3/3"},
+           "ms_per_factor": ms,
+           "config": {"workload": "tiled Cholesky + substitutions (configs[2])"
+                                  if world == 1 else
+                                  "tiled Cholesky, 2D block-cyclic (configs[4] layout)",
+                      "n": n, "b": b, "flops": "n^3/3", "gpus": world},
            "gpu_launches_per_factor": int(launches),
-           "roofline": {"bound": "tensor", "achieved": gflops / 1e3, "peak": peak_tf,
-                        "unit": "TFLOP/s", "frac": gflops / 1e3 / peak_tf,
+           "roofline": {"bound": "tensor", "achieved": gflops / 1e3 / world,
+                        "peak": peak_tf, "unit": "TFLOP/s per GPU",
+                        "frac": gflops / 1e3 / world / peak_tf,
                         "peak_source": "cuBLAS DGEMM 8192^3 measured live in this run "
                                        "(MEASURED_PEAKS.json has no FP64 entry)"}}
+    if not cyclic:  # substitutions (single GPU), for the record
+        rhs = torch.from_numpy(hs.generate_rhs(n, b, 42).values).cuda()
+        x = torch.empty_like(rhs)
+        torch.cuda.synchronize()
+        t0 = time.time()
+        x.copy_(rhs)
+        H.trsv_device(rt, work, x.data_ptr(), upper=False)
+        H.trsv_device(rt, work, x.data_ptr(), upper=True)
+        torch.cuda.synchronize()
+        out["solve_ms"] = (time.time() - t0) * 1e3
+        res = H.true_residual_device(rt, m, x.data_ptr(), rhs.data_ptr())
+        out["relative_residual"] = res / float(torch.linalg.vector_norm(rhs[:n]))
     work.free()
     m.free()
     return out
@@ -270,7 +283,12 @@ def run_ours(args) -> None:
     from paper_2605_13209_b200 import hsolve as H
 
     stream = torch.cuda.current_stream().cuda_stream
-    if world > 1:
+    use_dist = world > 1 or args.dist
+    if use_dist:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
@@ -301,7 +319,7 @@ def run_ours(args) -> None:
     local_bytes = (m.row_hi * (m.row_hi + 1) // 2 - m.row_lo * (m.row_lo + 1) // 2) * b * b * 8
 
     def barrier():
-        if world > 1:
+        if use_dist:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -328,7 +346,7 @@ def run_ours(args) -> None:
     n_symv, symv_ms = rt.prof_symv()
     rt.prof_enable(0)
     assert st.iterations == args.steps, (st.iterations, args.steps)
-    if world > 1:
+    if use_dist:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -364,7 +382,7 @@ def run_ours(args) -> None:
         "config": {"workload": "CG on GP SE matrix, n=%d, b=%d (BASELINE.json configs[1])"
                                % (n, b), "n": n, "b": b, "seed": 42,
                    "recompute_interval": 50, "eps": "1e-300 (fixed iteration count)",
-                   "parallelism": f"row-sharded x{world}" if world > 1 else "single GPU",
+                   "parallelism": (f"row-sharded x{world} (NCCL)" if use_dist else "single GPU"),
                    "l2": f"inputs larger than L2 (packed A = {packed_bytes / 1e9:.2f} GB)",
                    "matrix_assembly_s": round(gen_s, 3)},
         "gpu_launches": int(launches),
@@ -372,7 +390,7 @@ def run_ours(args) -> None:
     }
 
     # ---- e2e through the host-buffer C-ABI entry (rank 0 / single GPU) ----
-    if world == 1 and not args.no_e2e:
+    if not use_dist and not args.no_e2e:
         host = torch.empty(packed_bytes // 8, dtype=torch.float64, pin_memory=True)
         m.download(host.numpy())
         rhs_pin = torch.from_numpy(rhs_np.copy()).pin_memory()
@@ -410,15 +428,18 @@ def run_ours(args) -> None:
     clk = clocks.summary()
     line["clocks"] = clk
 
-    if rank == 0 and world == 1 and not args.no_secondary:
+    if not args.no_secondary:
         m.free()
         del d_rhs, d_x
         torch.cuda.empty_cache()
         peak_tf = dgemm_peak(torch)
         try:
-            line["secondary"] = cholesky_secondary(hs, H, rt, torch, args, peak_tf)
+            sec = cholesky_secondary(hs, H, rt, torch, args, peak_tf, world,
+                                     dist if use_dist else None)
         except Exception as e:  # keep the headline line even if this fails
-            line["secondary"] = {"error": repr(e)}
+            sec = {"error": repr(e)}
+        if rank == 0:
+            line["secondary"] = sec
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -431,7 +452,7 @@ def run_ours(args) -> None:
     if rank == 0:
         print(json.dumps(line), flush=True)
     rt.close()
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
 
 
@@ -454,6 +475,8 @@ def main():
     ap.add_argument("--e2e-iters", type=int, default=50)
     ap.add_argument("--e2e-reps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the NCCL (multi-GPU) code paths even on one GPU")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -930,6 +930,9 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   HS_REQUIRE(prm->eps > 0.0, HS_ERR_CONFIG, "eps must be positive");
   ensure_plan(const_cast<hs_matrix*>(m));
   const int world = c->world, rank = c->rank;
+  // distributed protocol whenever there is a communicator (also world == 1,
+  // which runs the NCCL path on one GPU)
+  const bool dp = c->comm != nullptr;
   const int64_t b = (int64_t)m->b;
   const int64_t N = (int64_t)m->N;
   const int64_t chunk = m->vec_len / world;  // doubles per rank chunk
@@ -947,7 +950,7 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   } guard{&B};
   // single rank + fast SYMV: the direction update rides inside the SYMV
   // (double-buffered s); otherwise a separate vector kernel does it
-  const bool fuse_sdir = world == 1 && fast_b(m->b);
+  const bool fuse_sdir = !dp && fast_b(m->b);
   HS_CUDA(cudaMalloc(&B.s_full, full * sizeof(double)));
   if (fuse_sdir) HS_CUDA(cudaMalloc(&B.s_alt, full * sizeof(double)));
   HS_CUDA(cudaMalloc(&B.x_full, full * sizeof(double)));
@@ -955,7 +958,7 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   HS_CUDA(cudaMalloc(&B.r, chunk * sizeof(double)));
   HS_CUDA(cudaMalloc(&B.rhs, chunk * sizeof(double)));
   HS_CUDA(cudaMalloc(&B.slots, std::max(world, 1) * sizeof(Dd)));
-  if (world > 1) HS_CUDA(cudaMalloc(&B.t_loc, chunk * sizeof(double)));
+  if (dp) HS_CUDA(cudaMalloc(&B.t_loc, chunk * sizeof(double)));
   if (trace_n) HS_CUDA(cudaMalloc(&B.trace, 3 * trace_n * sizeof(double)));
   HS_CUDA(cudaMemsetAsync(B.t, 0, full * sizeof(double), c->stream));
   HS_CUDA(cudaMemsetAsync(B.rhs, 0, chunk * sizeof(double), c->stream));
@@ -967,13 +970,15 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
 
   double* s_loc = B.s_full + (int64_t)rank * chunk;
   double* x_loc = B.x_full + (int64_t)rank * chunk;
-  double* t_own = world > 1 ? B.t_loc : B.t;
+  double* t_own = dp ? B.t_loc : B.t;
   const int32_t* done = &c->d_scalars->done;
 
-  StepArgs sa{c->d_scalars, B.trace, prm->eps, B.slots, world};
+  // sa.world == 1: the last CTA applies the scalar step itself; otherwise it
+  // publishes its (hi, lo) partial for the all-gather + rank-ordered combine
+  StepArgs sa{c->d_scalars, B.trace, prm->eps, B.slots, dp ? 0 : 1};
 
   auto dot_finish = [&](int step) {
-    if (world == 1) return;
+    if (!dp) return;
     // all-gather the (hi, lo) partials in place, combine in rank order
     comm_allgather(c, reinterpret_cast<double*>(B.slots) + 2 * rank,
                    reinterpret_cast<double*>(B.slots), 2);
@@ -995,14 +1000,14 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   v.t = t_own;
   v.rhs = B.rhs;
   v.dpart = c->d_dpart;
-  v.sa = world > 1 ? sa_local : sa;
+  v.sa = dp ? sa_local : sa;
   v.done = done;
 
   // x0 = 0, r = s = rhs, u0 = rhs^T rhs (cg_solver.cpp:243-249)
   v.mode = V_INIT;
   launch_vec(c, v);
   dot_finish(STEP_INIT);
-  if (world > 1) comm_allgather(c, s_loc, B.s_full, (size_t)chunk);
+  if (dp) comm_allgather(c, s_loc, B.s_full, (size_t)chunk);
 
   // Convergence is decided on the device (done flag); the host polls a
   // pinned copy of the scalars one chunk behind, so the GPU queue never
@@ -1017,7 +1022,7 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   double* sbuf[2] = {B.s_full, B.s_alt};
   for (uint64_t it = 1; it <= prm->max_iters; ++it) {
     // line 4 (+5 fused for a single rank): t = A s, alpha = u / s^T t
-    if (world == 1) {
+    if (!dp) {
       if (fuse_sdir) {
         // s_it = r + beta s_{it-1} (line 11 of the previous iteration, with
         // beta_0 = 0 so s_1 = r_0 = rhs), formed inside the SYMV
@@ -1039,9 +1044,9 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
       // x += alpha s; r = rhs - A x (cg_solver.cpp:277-298)
       v.mode = V_AXPY_X;
       launch_vec(c, v);
-      if (world > 1) comm_allgather(c, x_loc, B.x_full, (size_t)chunk);
+      if (dp) comm_allgather(c, x_loc, B.x_full, (size_t)chunk);
       symv_to(c, m, B.x_full, B.t, false, nullptr, done);
-      if (world > 1) comm_reduce_scatter(c, B.t, B.t_loc, (size_t)chunk);
+      if (dp) comm_reduce_scatter(c, B.t, B.t_loc, (size_t)chunk);
       v.mode = V_RESIDUAL;
       launch_vec(c, v);
     } else {
@@ -1053,7 +1058,7 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
       v.mode = V_SDIR;  // line 11
       launch_vec(c, v);
     }
-    if (world > 1) comm_allgather(c, s_loc, B.s_full, (size_t)chunk);
+    if (dp) comm_allgather(c, s_loc, B.s_full, (size_t)chunk);
     if (it % check_every == 0) {
       const int slot = (int)((it / check_every) & 1);
       HS_CUDA(cudaMemcpyAsync(pin + slot, c->d_scalars, sizeof(CgScalars),
@@ -1092,7 +1097,7 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
                        cudaMemcpyDeviceToHost));
 
   // result: full x in the standard layout
-  if (world > 1) comm_allgather(c, x_loc, B.x_full, (size_t)chunk);
+  if (dp) comm_allgather(c, x_loc, B.x_full, (size_t)chunk);
   for (int g = 0; g < world; ++g) {
     const int64_t glo = m->bounds[g], ghi = m->bounds[g + 1];
     if (ghi > glo)
@@ -1102,13 +1107,13 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   }
   // exit diagnostic: ||rhs - A x|| (cg_solver.cpp:360-365)
   symv_to(c, m, B.x_full, B.t, false, nullptr, nullptr);
-  if (world > 1) comm_reduce_scatter(c, B.t, B.t_loc, (size_t)chunk);
+  if (dp) comm_reduce_scatter(c, B.t, B.t_loc, (size_t)chunk);
   VecArgs vr = v;
   vr.mode = V_RESNORM;
   vr.done = nullptr;
   launch_vec(c, vr);
   double res2;
-  if (world > 1) {
+  if (dp) {
     comm_allgather(c, reinterpret_cast<double*>(B.slots) + 2 * rank,
                    reinterpret_cast<double*>(B.slots), 2);
     combine_kernel<<<1, 1, 0, c->stream>>>(B.slots, world, STEP_NONE, sa,

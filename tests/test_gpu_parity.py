@@ -463,3 +463,25 @@ def test_distributed_cholesky_world1_matches_oracle(oracle, n, b):
         assert ei.value.block_row == 0 and ei.value.pivot_index == 5
     finally:
         rt.close()
+
+
+@pytest.mark.parametrize("n,b", [(2048, 128), (1000, 64)])
+def test_distributed_cg_world1_matches_oracle(oracle, n, b):
+    """The row-sharded NCCL protocol (reduce-scatter, all-gather of s,
+    rank-ordered double-double dots) on one GPU via a world-1 communicator."""
+    rt = hs.Runtime.distributed(0, 0, 1, hs.Runtime.nccl_unique_id())
+    try:
+        a = oracle.generate_spd(n, b, seed=42)
+        rhs = oracle.generate_rhs(n, b, seed=42)
+        ref = oracle.solve_cg(n, b, a, rhs, eps=1e-6, max_iters=500)
+        m = hs.DeviceMatrix(rt, n, b).upload(a)
+        d_rhs = dev(rhs)
+        d_x = torch.zeros_like(d_rhs)
+        st = hs.solve_cg_device(rt, m, d_rhs.data_ptr(), d_x.data_ptr(),
+                                hs.SolverConfig(block_size=b, eps=1e-6))
+        x = d_x.cpu().numpy()
+        assert st.converged and abs(st.iterations - ref["iterations"]) <= 2
+        assert np.linalg.norm(x[:n] - ref["x"][:n]) <= 1e-6 * np.linalg.norm(ref["x"][:n])
+        assert st.true_residual <= 2e-6 * np.sqrt(st.u0)
+    finally:
+        rt.close()
