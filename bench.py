@@ -372,6 +372,16 @@ def run_ours(args) -> None:
                 "frac": achieved / hbm_peak, "traffic": traffic,
                 "kernel": f"symv_slab_kernel<{b}>", "launches": n_symv,
                 "algorithmic_bytes_per_launch": local_bytes, "peak_source": hbm_src}
+    # the driver's peak is a copy (read + write); the SYMV only reads, so also
+    # report the read-only roofline of this box measured now (same TMA ring)
+    try:
+        import ctypes as C
+        g = C.c_double()
+        H._check(rt._L.hs_probe_hbm_read(rt.ctx, 4 << 30, 0, 3, C.byref(g)))
+        roofline["read_only_peak_gbs"] = g.value
+        roofline["frac_of_read_only_peak"] = achieved / g.value
+    except Exception as e:  # diagnostics only
+        roofline["read_only_peak_gbs"] = repr(e)
 
     line = {
         "metric": "cg_iters_per_s", "value": value, "unit": "iters/s", "n_gpus": world,
