@@ -223,13 +223,48 @@ __global__ void __launch_bounds__(256)
   double* blk = tiles + (int64_t)blockIdx.x * b * b;
   const double diag = __dadd_rn(sf2, sn2);
   // each thread owns column c: its point stays in registers; the row point
-  // is warp-uniform (broadcast load); stores are coalesced along the row
+  // is warp-uniform (broadcast load); stores are coalesced along the row.
+  // Interior tiles (off-diagonal, no padding) take a branch-free path with
+  // four rows per iteration, so the exp constants and the address math are
+  // shared by four independent exp evaluations.
+  const bool interior = (i != j) && ((i + 1) * (int64_t)b <= n) && DIM > 0;
   for (int c = threadIdx.x; c < b; c += blockDim.x) {
     const int64_t q = j * b + c;
     double xq[DIM > 0 ? DIM : 1];
     if (DIM > 0 && q < n) {
 #pragma unroll
       for (int k = 0; k < (DIM > 0 ? DIM : 1); ++k) xq[k] = __ldg(pts + q * DIM + k);
+    }
+    if (interior) {
+      const double nl = -inv2l2;
+      const double* prow = pts + (i * b + r0) * DIM;
+      double* out = blk + (int64_t)r0 * b + c;
+      int r = r0;
+      for (; r + 4 <= r1; r += 4, prow += 4 * DIM, out += 4 * (int64_t)b) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          double d2 = 0.0;
+#pragma unroll
+          for (int k = 0; k < (DIM > 0 ? DIM : 1); ++k) {
+            const double d = __dsub_rn(__ldg(prow + u * DIM + k), xq[k]);
+            d2 = __dadd_rn(d2, __dmul_rn(d, d));
+          }
+          v[u] = __dmul_rn(sf2, exp(__dmul_rn(d2, nl)));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) __stcs(out + u * (int64_t)b, v[u]);
+      }
+      for (; r < r1; ++r, prow += DIM, out += b) {
+        double d2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < (DIM > 0 ? DIM : 1); ++k) {
+          const double d = __dsub_rn(__ldg(prow + k), xq[k]);
+          d2 = __dadd_rn(d2, __dmul_rn(d, d));
+        }
+        __stcs(out, __dmul_rn(sf2, exp(__dmul_rn(d2, nl))));
+      }
+      continue;
     }
     for (int r = r0; r < r1; ++r) {
       const int64_t p = i * b + r;
