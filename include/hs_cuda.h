@@ -46,6 +46,11 @@ enum {
   HS_ERR_SINGULAR_BLOCK = 3, /* ErrorKind::singular_block */
   HS_ERR_NUMERICAL = 4,      /* ErrorKind::numerical      */
   HS_ERR_NOT_CONVERGED = 5,  /* status only; never returned by a solve */
+  HS_ERR_RESIDENCY = 6,      /* ErrorKind::residency (never produced)  */
+  HS_ERR_FORMAT = 7,         /* ErrorKind::format                      */
+  HS_ERR_VERSION_MISMATCH = 8, /* ErrorKind::version_mismatch: payload (expected, actual) */
+  HS_ERR_TRUNCATED_FILE = 9, /* ErrorKind::truncated_file: payload (expected, actual bytes) */
+  HS_ERR_IO = 10,            /* ErrorKind::io                          */
   HS_ERR_CUDA = 100          /* device / runtime failure (no reference kind) */
 };
 
@@ -216,6 +221,54 @@ hs_status hs_gemm_update_tiles(hs_ctx* ctx, double* d_c, const double* d_p,
 void hs_prof_enable(hs_ctx* ctx, int every);
 void hs_prof_symv(hs_ctx* ctx, uint64_t* launches, double* total_ms);
 void hs_prof_reset(hs_ctx* ctx);
+
+/* ---- communication ledger (transfer_ledger.hpp:9-52) ------------------ */
+/* Every NCCL collective a multi-rank context issues is appended to the
+ * context's ledger: kind (TransferKind: 0 scalar, 1 subvector, 2 block,
+ * 3 block_row, 4 initial_matrix, 5 result), direction (Direction:
+ * 2 = bidirectional for collectives), payload bytes (the collective's output
+ * buffer on this rank: the full vector for an all-gather, as the reference
+ * logs subvector exchanges with the full logical vector,
+ * test_cg_solver.cpp:171-176) and step (CG iteration / Cholesky column, -1
+ * for setup). Single-GPU contexts issue no collectives, so their ledger stays
+ * empty like the reference's homogeneous runs (test_cg_solver.cpp:178-187). */
+typedef struct {
+  uint8_t kind;
+  uint8_t direction;
+  uint64_t bytes;
+  int64_t step;
+} hs_ledger_entry;
+size_t hs_ctx_ledger_size(const hs_ctx* ctx);
+/* Copies up to `cap` entries (oldest first); returns the number copied. */
+size_t hs_ctx_ledger_read(const hs_ctx* ctx, hs_ledger_entry* out, size_t cap);
+void hs_ctx_ledger_clear(hs_ctx* ctx);
+
+/* ---- BSPD1 matrix / vector files (matrix_io.hpp:9-19) ------------------- */
+/* Format (matrix_io.cpp): "BSPD", version byte 0x01, u64 n, u64 b (little
+ * endian), then the packed tiles in triangular order, b*b FP64 row-major per
+ * tile. Errors: HS_ERR_IO (cannot open / write), HS_ERR_FORMAT (magic,
+ * implausible header n == 0, b == 0, n > 2^32, b > 2^20),
+ * HS_ERR_VERSION_MISMATCH (payload expected, actual), HS_ERR_TRUNCATED_FILE
+ * (payload expected, actual byte counts). Host-only calls need no GPU. */
+hs_status hs_bspd1_probe(const char* path, size_t* n, size_t* b);
+hs_status hs_bspd1_read(const char* path, double* host_packed, size_t count);
+hs_status hs_bspd1_write(const char* path, size_t n, size_t b,
+                         const double* host_packed);
+/* Vector files: u64 n then n FP64 values (matrix_io.hpp:16-19). */
+hs_status hs_vector_probe(const char* path, size_t* n);
+hs_status hs_vector_read(const char* path, double* out, size_t n);
+hs_status hs_vector_write(const char* path, size_t n, const double* v);
+/* Stream a BSPD1 file straight into device tiles (no host copy of the
+ * matrix): pinned staging ring, file reads overlapped with H2D copies. Each
+ * rank reads only the tiles it owns (cyclic = 0: its block rows, a contiguous
+ * byte range; cyclic = 1: its 2D block-cyclic tiles). Files larger than host
+ * RAM load fine. */
+hs_status hs_matrix_load_bspd1(hs_ctx* ctx, const char* path, int cyclic,
+                               hs_matrix** out);
+/* Write a device matrix as BSPD1, streamed through pinned staging. Every rank
+ * writes its own tiles at their file offsets (no barrier needed); rank 0
+ * writes the header, the rank owning the last block row sets the length. */
+hs_status hs_matrix_save_bspd1(const hs_matrix* m, const char* path);
 
 /* ---- diagnostics ------------------------------------------------------ */
 /* Read-only HBM bandwidth over `bytes` of device memory, the roofline of the

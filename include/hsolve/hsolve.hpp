@@ -4,7 +4,8 @@
 // Reference headers this replaces (paths relative to /root/reference/proj):
 //   blocked_matrix.hpp, solver_config.hpp, errors.hpp, partition.hpp,
 //   transfer_ledger.hpp, executor.hpp (Runtime), genmat.hpp, cg_solver.hpp,
-//   cholesky_solver.hpp. The per-name headers next to this one include it,
+//   cholesky_solver.hpp; matrix_io.hpp and bench.hpp have their own headers
+//   next to this one. The per-name headers next to this one include it,
 //   so `#include "hsolve/cg_solver.hpp"` keeps compiling unchanged.
 //
 // Semantics kept: packed lower-triangular b x b tiles with identity padding,
@@ -85,6 +86,27 @@ struct ResidencyError : Error {
 };
 struct FormatError : Error {
   explicit FormatError(const std::string& m) : Error(ErrorKind::format, m) {}
+};
+class VersionMismatchError : public Error {
+ public:
+  VersionMismatchError(unsigned expected, unsigned actual)
+      : Error(ErrorKind::version_mismatch,
+              "unsupported file version " + std::to_string(actual) +
+                  " (expected " + std::to_string(expected) + ")") {}
+};
+class TruncatedFileError : public Error {
+ public:
+  TruncatedFileError(std::uint64_t expected_bytes, std::uint64_t actual_bytes)
+      : Error(ErrorKind::truncated_file,
+              "file truncated: expected " + std::to_string(expected_bytes) +
+                  " bytes, got " + std::to_string(actual_bytes)),
+        expected_(expected_bytes),
+        actual_(actual_bytes) {}
+  std::uint64_t expected_bytes() const { return expected_; }
+  std::uint64_t actual_bytes() const { return actual_; }
+
+ private:
+  std::uint64_t expected_, actual_;
 };
 struct IoError : Error {
   explicit IoError(const std::string& m) : Error(ErrorKind::io, m) {}
@@ -246,6 +268,9 @@ class Runtime {
 
   hs_ctx* native();  // the C-ABI context (created on first use)
   void add_transfer_ms(double ms) { transfer_seconds_ += ms * 1e-3; }
+  // Moves the context's NCCL ledger entries (one per collective) into
+  // ledger(); called by the solvers after each native call.
+  void sync_ledger();
 
  private:
   int device_ = 0;

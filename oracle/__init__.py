@@ -196,6 +196,32 @@ class Reference:
         L.ref_partition_for_fraction.argtypes = [C.c_double, _sz]
         L.ref_cholesky_border.restype = _sz
         L.ref_cholesky_border.argtypes = [C.c_double, _sz, _sz]
+        L.ref_save_matrix.argtypes = [_sz, _sz, _dp, C.c_char_p]
+        L.ref_load_matrix.argtypes = [C.c_char_p, C.POINTER(_sz), C.POINTER(_sz), C.c_void_p,
+                                      _sz, _i64p, _i64p]
+        L.ref_save_vector.argtypes = [_sz, _sz, _dp, C.c_char_p]
+
+    # matrix_io.hpp:16-19
+    def save_matrix(self, n, b, a, path):
+        st = self.lib.ref_save_matrix(n, b, np.ascontiguousarray(a), os.fsencode(path))
+        assert st == 0, st
+
+    def load_matrix(self, path):
+        """(status, n, b, values | None, expected, actual)."""
+        n, b = _sz(), _sz()
+        ea, eb = C.c_int64(-1), C.c_int64(-1)
+        st = self.lib.ref_load_matrix(os.fsencode(path), C.byref(n), C.byref(b), None, 0,
+                                      C.byref(ea), C.byref(eb))
+        if st != 0:
+            return st, 0, 0, None, ea.value, eb.value
+        out = np.empty(packed_len(n.value, b.value))
+        st = self.lib.ref_load_matrix(os.fsencode(path), C.byref(n), C.byref(b),
+                                      out.ctypes.data, out.size, C.byref(ea), C.byref(eb))
+        return st, n.value, b.value, out, -1, -1
+
+    def save_vector(self, n, b, v, path):
+        st = self.lib.ref_save_vector(n, b, np.ascontiguousarray(v), os.fsencode(path))
+        assert st == 0, st
 
     def generate_spd(self, n, b, seed=42, sigma_f2=1.0, length_scale=0.0, sigma_n2=1e-2, dim=2):
         out = np.zeros(packed_len(n, b))

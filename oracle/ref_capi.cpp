@@ -17,6 +17,7 @@
 #include "hsolve/cholesky_solver.hpp"
 #include "hsolve/errors.hpp"
 #include "hsolve/genmat.hpp"
+#include "hsolve/matrix_io.hpp"
 #include "hsolve/partition.hpp"
 
 using namespace hsolve;
@@ -271,6 +272,46 @@ std::size_t ref_partition_for_fraction(double f, std::size_t rows) {
 }
 std::size_t ref_cholesky_border(double f, std::size_t col, std::size_t rows) {
   return cholesky_border(f, col, rows);
+}
+
+// matrix_io.hpp:16-19 (BSPD1 files). load: *n, *b set on success; the
+// packed values are copied to `out` when it is non-null and `cap` matches.
+int ref_save_matrix(std::size_t n, std::size_t b, const double* v, const char* path) {
+  try {
+    save_matrix(from_packed(n, b, v), path);
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return status_of(e);
+  }
+}
+int ref_load_matrix(const char* path, std::size_t* n, std::size_t* b, double* out,
+                    std::size_t cap, std::int64_t* err_a, std::int64_t* err_b) {
+  try {
+    const BlockedSPDMatrix m = load_matrix(path);
+    *n = m.n();
+    *b = m.block_size();
+    if (out && cap == m.value_count())
+      std::memcpy(out, m.data(), cap * sizeof(double));
+    return 0;
+  } catch (const TruncatedFileError& e) {
+    g_err = e.what();
+    *err_a = (std::int64_t)e.expected_bytes();
+    *err_b = (std::int64_t)e.actual_bytes();
+    return status_of(e);
+  } catch (const Error& e) {
+    g_err = e.what();
+    return status_of(e);
+  }
+}
+int ref_save_vector(std::size_t n, std::size_t b, const double* v, const char* path) {
+  try {
+    save_vector(from_vec(n, b, v), path);
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return status_of(e);
+  }
 }
 
 }  // extern "C"

@@ -9,4 +9,6 @@ from .hsolve import (  # noqa: F401
     generate_rhs, generate_spd, generate_spd_device, median_pairwise_distance,
     partition_for_fraction, partition_rows, potrf_device, solve_cg, solve_cg_device,
     solve_spd, solve_spd_device, symv_device, trsv_device, true_residual_device,
+    FormatError, IoError, ResidencyError, TransferEntry, TruncatedFileError,
+    VersionMismatchError, load_matrix, load_vector, save_matrix, save_vector,
 )

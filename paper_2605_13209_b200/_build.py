@@ -22,6 +22,8 @@ HOST = os.path.join(PKG, "host")
 INC = os.path.join(ROOT, "include")
 CUDA_LIB = os.path.join(PKG, "libhsolve_cuda.so")
 HOST_LIB = os.path.join(PKG, "libhsolve_b200.so")
+CLI_SRC = os.path.join(ROOT, "tools", "hsolve_bench.cpp")
+CLI_BIN = os.path.join(PKG, "bin", "hsolve_bench")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [
@@ -73,8 +75,8 @@ def build_host(force: bool = False) -> str:
     srcs = sorted(glob.glob(os.path.join(HOST, "*.cpp")))
     if not srcs:
         return ""
-    deps = srcs + glob.glob(os.path.join(INC, "hsolve", "*.hpp")) + [
-        os.path.join(INC, "hs_cuda.h"), CUDA_LIB]
+    deps = srcs + glob.glob(os.path.join(HOST, "*.hpp")) + glob.glob(
+        os.path.join(INC, "hsolve", "*.hpp")) + [os.path.join(INC, "hs_cuda.h"), CUDA_LIB]
     if not force and not _stale(HOST_LIB, deps):
         return HOST_LIB
     cxx = os.environ.get("CXX", "g++")
@@ -83,9 +85,21 @@ def build_host(force: bool = False) -> str:
     return HOST_LIB
 
 
+def build_cli(force: bool = False) -> str:
+    """The reference's hsolve_bench CLI (gen / solve / sweep)."""
+    if not force and not _stale(CLI_BIN, [CLI_SRC, HOST_LIB]):
+        return CLI_BIN
+    os.makedirs(os.path.dirname(CLI_BIN), exist_ok=True)
+    cxx = os.environ.get("CXX", "g++")
+    _run([cxx, "-std=c++20", "-O2", "-I", INC, CLI_SRC, "-o", CLI_BIN, "-L", PKG,
+          "-lhsolve_b200", "-lhsolve_cuda", "-Wl,-rpath,$ORIGIN/.."])
+    return CLI_BIN
+
+
 def build(force: bool = False) -> None:
     build_cuda(force)
     build_host(force)
+    build_cli(force)
 
 
 if __name__ == "__main__":

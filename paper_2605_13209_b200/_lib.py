@@ -19,6 +19,11 @@ HS_ERR_NOT_SPD = 2
 HS_ERR_SINGULAR_BLOCK = 3
 HS_ERR_NUMERICAL = 4
 HS_ERR_NOT_CONVERGED = 5
+HS_ERR_RESIDENCY = 6
+HS_ERR_FORMAT = 7
+HS_ERR_VERSION_MISMATCH = 8
+HS_ERR_TRUNCATED_FILE = 9
+HS_ERR_IO = 10
 HS_ERR_CUDA = 100
 
 # Every symbol include/hs_cuda.h declares (checked by tests/test_abi.py).
@@ -37,6 +42,9 @@ EXPORTED = [
     "hs_factorize_host", "hs_solve_spd_host", "hs_forward_substitute_host",
     "hs_back_substitute_host", "hs_potf_tiles", "hs_gemm_update_tiles",
     "hs_prof_enable", "hs_prof_symv", "hs_prof_reset", "hs_probe_hbm_read",
+    "hs_ctx_ledger_size", "hs_ctx_ledger_read", "hs_ctx_ledger_clear",
+    "hs_bspd1_probe", "hs_bspd1_read", "hs_bspd1_write", "hs_vector_probe",
+    "hs_vector_read", "hs_vector_write", "hs_matrix_load_bspd1", "hs_matrix_save_bspd1",
 ]
 
 
@@ -57,6 +65,11 @@ class CholStats(C.Structure):
     _fields_ = [("factor_ms", C.c_double), ("solve_ms", C.c_double),
                 ("wall_ms", C.c_double), ("compute_ms", C.c_double),
                 ("transfer_ms", C.c_double), ("true_residual", C.c_double)]
+
+
+class LedgerEntry(C.Structure):  # hs_ledger_entry
+    _fields_ = [("kind", C.c_uint8), ("direction", C.c_uint8), ("bytes", C.c_uint64),
+                ("step", C.c_int64)]
 
 
 def lib_path() -> str:
@@ -127,6 +140,17 @@ def lib():
         "hs_prof_symv": (None, [vp, C.POINTER(u64), C.POINTER(C.c_double)]),
         "hs_prof_reset": (None, [vp]),
         "hs_probe_hbm_read": (C.c_int, [vp, sz, C.c_int, C.c_int, C.POINTER(C.c_double)]),
+        "hs_ctx_ledger_size": (sz, [vp]),
+        "hs_ctx_ledger_read": (sz, [vp, C.POINTER(LedgerEntry), sz]),
+        "hs_ctx_ledger_clear": (None, [vp]),
+        "hs_bspd1_probe": (C.c_int, [C.c_char_p, C.POINTER(sz), C.POINTER(sz)]),
+        "hs_bspd1_read": (C.c_int, [C.c_char_p, dp, sz]),
+        "hs_bspd1_write": (C.c_int, [C.c_char_p, sz, sz, dp]),
+        "hs_vector_probe": (C.c_int, [C.c_char_p, C.POINTER(sz)]),
+        "hs_vector_read": (C.c_int, [C.c_char_p, dp, sz]),
+        "hs_vector_write": (C.c_int, [C.c_char_p, sz, dp]),
+        "hs_matrix_load_bspd1": (C.c_int, [vp, C.c_char_p, C.c_int, pp]),
+        "hs_matrix_save_bspd1": (C.c_int, [vp, C.c_char_p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

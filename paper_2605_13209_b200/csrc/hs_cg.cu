@@ -27,9 +27,6 @@
 
 namespace hs {
 
-void comm_allgather(hs_ctx* c, const double* send, double* recv, size_t count);
-void comm_reduce_scatter(hs_ctx* c, const double* send, double* recv,
-                         size_t count);
 
 // ---------------------------------------------------------------------------
 // Fast SYMV for b in {64, 128, 256, 512}
@@ -981,7 +978,7 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
     if (!dp) return;
     // all-gather the (hi, lo) partials in place, combine in rank order
     comm_allgather(c, reinterpret_cast<double*>(B.slots) + 2 * rank,
-                   reinterpret_cast<double*>(B.slots), 2);
+                   reinterpret_cast<double*>(B.slots), 2, LK_SCALAR);
     combine_kernel<<<1, 1, 0, c->stream>>>(B.slots, world, step, sa, nullptr,
                                            done);
     HS_CUDA(cudaGetLastError());
@@ -1006,8 +1003,9 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   // x0 = 0, r = s = rhs, u0 = rhs^T rhs (cg_solver.cpp:243-249)
   v.mode = V_INIT;
   launch_vec(c, v);
+  c->step = -1;  // ledger: setup
   dot_finish(STEP_INIT);
-  if (dp) comm_allgather(c, s_loc, B.s_full, (size_t)chunk);
+  if (dp) comm_allgather(c, s_loc, B.s_full, (size_t)chunk, LK_SUBVECTOR);
 
   // Convergence is decided on the device (done flag); the host polls a
   // pinned copy of the scalars one chunk behind, so the GPU queue never
@@ -1021,6 +1019,7 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   CgScalars h{};
   double* sbuf[2] = {B.s_full, B.s_alt};
   for (uint64_t it = 1; it <= prm->max_iters; ++it) {
+    c->step = (int64_t)it;
     // line 4 (+5 fused for a single rank): t = A s, alpha = u / s^T t
     if (!dp) {
       if (fuse_sdir) {
@@ -1034,7 +1033,7 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
       }
     } else {
       symv_to(c, m, B.s_full, B.t, false, nullptr, done);
-      comm_reduce_scatter(c, B.t, B.t_loc, (size_t)chunk);
+      comm_reduce_scatter(c, B.t, B.t_loc, (size_t)chunk, LK_SUBVECTOR);
       v.mode = V_DOT_ST;
       launch_vec(c, v);
       dot_finish(STEP_ALPHA);
@@ -1044,9 +1043,9 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
       // x += alpha s; r = rhs - A x (cg_solver.cpp:277-298)
       v.mode = V_AXPY_X;
       launch_vec(c, v);
-      if (dp) comm_allgather(c, x_loc, B.x_full, (size_t)chunk);
+      if (dp) comm_allgather(c, x_loc, B.x_full, (size_t)chunk, LK_SUBVECTOR);
       symv_to(c, m, B.x_full, B.t, false, nullptr, done);
-      if (dp) comm_reduce_scatter(c, B.t, B.t_loc, (size_t)chunk);
+      if (dp) comm_reduce_scatter(c, B.t, B.t_loc, (size_t)chunk, LK_SUBVECTOR);
       v.mode = V_RESIDUAL;
       launch_vec(c, v);
     } else {
@@ -1058,7 +1057,7 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
       v.mode = V_SDIR;  // line 11
       launch_vec(c, v);
     }
-    if (dp) comm_allgather(c, s_loc, B.s_full, (size_t)chunk);
+    if (dp) comm_allgather(c, s_loc, B.s_full, (size_t)chunk, LK_SUBVECTOR);
     if (it % check_every == 0) {
       const int slot = (int)((it / check_every) & 1);
       HS_CUDA(cudaMemcpyAsync(pin + slot, c->d_scalars, sizeof(CgScalars),
@@ -1097,7 +1096,8 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
                        cudaMemcpyDeviceToHost));
 
   // result: full x in the standard layout
-  if (dp) comm_allgather(c, x_loc, B.x_full, (size_t)chunk);
+  c->step = -1;
+  if (dp) comm_allgather(c, x_loc, B.x_full, (size_t)chunk, LK_RESULT);
   for (int g = 0; g < world; ++g) {
     const int64_t glo = m->bounds[g], ghi = m->bounds[g + 1];
     if (ghi > glo)
@@ -1107,7 +1107,7 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   }
   // exit diagnostic: ||rhs - A x|| (cg_solver.cpp:360-365)
   symv_to(c, m, B.x_full, B.t, false, nullptr, nullptr);
-  if (dp) comm_reduce_scatter(c, B.t, B.t_loc, (size_t)chunk);
+  if (dp) comm_reduce_scatter(c, B.t, B.t_loc, (size_t)chunk, LK_SUBVECTOR);
   VecArgs vr = v;
   vr.mode = V_RESNORM;
   vr.done = nullptr;
@@ -1115,7 +1115,7 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   double res2;
   if (dp) {
     comm_allgather(c, reinterpret_cast<double*>(B.slots) + 2 * rank,
-                   reinterpret_cast<double*>(B.slots), 2);
+                   reinterpret_cast<double*>(B.slots), 2, LK_SCALAR);
     combine_kernel<<<1, 1, 0, c->stream>>>(B.slots, world, STEP_NONE, sa,
                                            c->d_dpart + N, nullptr);
     HS_CUDA(cudaGetLastError());

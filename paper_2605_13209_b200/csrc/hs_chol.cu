@@ -1445,10 +1445,6 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
 // diagonal, TRSM and all NCCL calls, in the same order on every rank; U
 // stream: updates, the column j+1 tiles first).
 
-void comm_bcast_on(hs_ctx* c, const double* send, double* recv, size_t count,
-                   int root, cudaStream_t s);
-void comm_group(hs_ctx* c, bool start);
-void comm_allreduce_max_i64(hs_ctx* c, int64_t* buf, size_t count, cudaStream_t s);
 
 static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
   const int b = (int)m->b;
@@ -1573,10 +1569,12 @@ static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
     }
     // L_jj and its inverse blocks to every rank
     const int64_t dslot = m->lpos[tri(j, j)];
+    c->step = j;
     comm_group(c, true);
-    comm_bcast_on(c, dj == me ? m->d + dslot * bb : nullptr, Ld, (size_t)bb, dj, cs.p);
+    comm_bcast_on(c, dj == me ? m->d + dslot * bb : nullptr, Ld, (size_t)bb, dj, cs.p,
+                  LK_BLOCK);
     comm_bcast_on(c, dj == me ? m->dinv + j * f * (int64_t)cb * cb : nullptr, Wb,
-                  (size_t)f * cb * cb, dj, cs.p);
+                  (size_t)f * cb * cb, dj, cs.p, LK_BLOCK);
     comm_group(c, false);
     // TRSM of the owned panel tiles (in place)
     const int64_t nr = row_off[j + 1] - row_off[j];
@@ -1602,7 +1600,8 @@ static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
       for (int64_t i = j + 1; i < N; ++i) {
         const int own = cyclic_owner(i, j, P, Q);
         const double* send = own == me ? m->d + m->lpos[tri(i, j)] * bb : nullptr;
-        comm_bcast_on(c, send, PB[j & 1] + (i - j - 1) * bb, (size_t)bb, own, cs.p);
+        comm_bcast_on(c, send, PB[j & 1] + (i - j - 1) * bb, (size_t)bb, own, cs.p,
+                      LK_BLOCK);
       }
       comm_group(c, false);
     }
@@ -1643,6 +1642,7 @@ static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
   HS_CUDA(cudaStreamSynchronize(c->stream));
   int64_t st[3] = {h.status, h.status ? h.col : -1, h.status ? h.pivot : -1};
   HS_CUDA(cudaMemcpy(d_status, st, sizeof(st), cudaMemcpyHostToDevice));
+  c->step = -1;
   comm_allreduce_max_i64(c, d_status, 3, c->stream);
   HS_CUDA(cudaMemcpyAsync(st, d_status, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));

@@ -86,33 +86,35 @@ void nccl_check(Nccl* n, ncclResult_t r, const char* what) {
     throw Failure{HS_ERR_CUDA, std::string(what) + ": " + n->GetErrorString(r)};
 }
 
+static void ledger_add(hs_ctx* c, LedgerKind kind, uint64_t bytes) {
+  c->ledger.push_back(hs_ledger_entry{(uint8_t)kind, 2 /* bidirectional */,
+                                      bytes, c->step});
+}
+
 void comm_allgather(hs_ctx* c, const double* send, double* recv,
-                    size_t count) {
+                    size_t count, LedgerKind kind) {
   nccl_check(c->nccl,
              c->nccl->AllGather(send, recv, count, ncclFloat64,
                                 (ncclComm_t)c->comm, c->stream),
              "ncclAllGather");
+  ledger_add(c, kind, (uint64_t)count * c->world * sizeof(double));
 }
 void comm_reduce_scatter(hs_ctx* c, const double* send, double* recv,
-                         size_t count) {
+                         size_t count, LedgerKind kind) {
   nccl_check(c->nccl,
              c->nccl->ReduceScatter(send, recv, count, ncclFloat64, ncclSum,
                                     (ncclComm_t)c->comm, c->stream),
              "ncclReduceScatter");
-}
-void comm_broadcast(hs_ctx* c, double* buf, size_t count, int root) {
-  nccl_check(c->nccl,
-             c->nccl->Broadcast(buf, buf, count, ncclFloat64, root,
-                                (ncclComm_t)c->comm, c->stream),
-             "ncclBroadcast");
+  ledger_add(c, kind, (uint64_t)count * sizeof(double));
 }
 // broadcast from root's `send` into every rank's `recv` on stream s
 void comm_bcast_on(hs_ctx* c, const double* send, double* recv, size_t count,
-                   int root, cudaStream_t s) {
+                   int root, cudaStream_t s, LedgerKind kind) {
   nccl_check(c->nccl,
              c->nccl->Broadcast(send, recv, count, ncclFloat64, root,
                                 (ncclComm_t)c->comm, s),
              "ncclBroadcast");
+  ledger_add(c, kind, (uint64_t)count * sizeof(double));
 }
 void comm_group(hs_ctx* c, bool start) {
   nccl_check(c->nccl, start ? c->nccl->GroupStart() : c->nccl->GroupEnd(),
@@ -125,6 +127,7 @@ void comm_allreduce_max_i64(hs_ctx* c, int64_t* buf, size_t count,
              c->nccl->AllReduce(buf, buf, count, ncclInt64, ncclMax,
                                 (ncclComm_t)c->comm, s),
              "ncclAllReduce");
+  ledger_add(c, LK_SCALAR, (uint64_t)count * sizeof(int64_t));
 }
 
 // ---------------------------------------------------------------------------
@@ -463,6 +466,11 @@ const char* hs_error_kind_name(hs_status s) {
     case HS_ERR_SINGULAR_BLOCK: return "singular_block";
     case HS_ERR_NUMERICAL: return "numerical_error";
     case HS_ERR_NOT_CONVERGED: return "not_converged";
+    case HS_ERR_RESIDENCY: return "residency_error";
+    case HS_ERR_FORMAT: return "format_error";
+    case HS_ERR_VERSION_MISMATCH: return "version_mismatch";
+    case HS_ERR_TRUNCATED_FILE: return "truncated_file";
+    case HS_ERR_IO: return "io_error";
     case HS_ERR_CUDA: return "cuda_error";
   }
   return "unknown";
@@ -558,6 +566,17 @@ int hs_ctx_rank(const hs_ctx* c) { return c ? c->rank : -1; }
 int hs_ctx_world(const hs_ctx* c) { return c ? c->world : 0; }
 void* hs_ctx_stream(const hs_ctx* c) { return c ? (void*)c->stream : nullptr; }
 uint64_t hs_ctx_kernel_launches(const hs_ctx* c) { return c ? c->launches : 0; }
+
+size_t hs_ctx_ledger_size(const hs_ctx* c) { return c ? c->ledger.size() : 0; }
+size_t hs_ctx_ledger_read(const hs_ctx* c, hs_ledger_entry* out, size_t cap) {
+  if (!c || !out) return 0;
+  const size_t k = std::min(cap, c->ledger.size());
+  std::copy(c->ledger.begin(), c->ledger.begin() + k, out);
+  return k;
+}
+void hs_ctx_ledger_clear(hs_ctx* c) {
+  if (c) c->ledger.clear();
+}
 
 uint64_t hs_rng_at(uint64_t key, uint64_t counter) { return rng_at(key, counter); }
 double hs_rng_uniform_pm1(uint64_t key, uint64_t counter) {

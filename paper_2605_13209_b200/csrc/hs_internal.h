@@ -81,6 +81,10 @@ struct hs_ctx {
   // device matrices reused by the host-buffer entry points (slot 0: the
   // solve matrix, slot 1: the unfactored copy kept for the residual)
   hs_matrix* cache[2] = {nullptr, nullptr};
+  // communication ledger: one entry per NCCL collective (multi-rank only);
+  // `step` is the CG iteration / Cholesky column the drivers are in
+  std::vector<hs_ledger_entry> ledger;
+  int64_t step = -1;
 };
 
 struct hs_matrix {
@@ -128,6 +132,23 @@ inline int cyclic_owner(int64_t i, int64_t j, int P, int Q) {
 }
 
 void launch_count(hs_ctx* c, int k = 1);
+
+// ledger kinds (transfer_ledger.hpp:9-16)
+enum LedgerKind : uint8_t {
+  LK_SCALAR = 0, LK_SUBVECTOR = 1, LK_BLOCK = 2, LK_BLOCK_ROW = 3,
+  LK_INITIAL_MATRIX = 4, LK_RESULT = 5
+};
+// NCCL collectives (hs_ctx.cu); each appends one ledger entry of `kind`
+// whose bytes are the collective's output buffer on this rank.
+void comm_allgather(hs_ctx* c, const double* send, double* recv, size_t count,
+                    LedgerKind kind);
+void comm_reduce_scatter(hs_ctx* c, const double* send, double* recv,
+                         size_t count, LedgerKind kind);
+void comm_bcast_on(hs_ctx* c, const double* send, double* recv, size_t count,
+                   int root, cudaStream_t s, LedgerKind kind);
+void comm_group(hs_ctx* c, bool start);
+void comm_allreduce_max_i64(hs_ctx* c, int64_t* buf, size_t count,
+                            cudaStream_t s);
 void ensure_plan(hs_matrix* m);
 void free_plan(SymvPlan* p);
 // y (padded layout, full length) = A x over this rank's tiles (partials of

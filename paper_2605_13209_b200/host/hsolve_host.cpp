@@ -9,10 +9,11 @@
 #include <mutex>
 
 #include "hs_cuda.h"
+#include "host_internal.hpp"
 
 namespace hsolve {
 
-namespace {
+namespace detail {
 
 [[noreturn]] void raise(hs_status s) {
   const std::string msg = hs_last_error();
@@ -23,6 +24,11 @@ namespace {
     case HS_ERR_NOT_SPD: throw NotSpdError(a, (std::size_t)b);
     case HS_ERR_SINGULAR_BLOCK: throw SingularBlockError((std::size_t)b);
     case HS_ERR_NUMERICAL: throw NumericalError(msg);
+    case HS_ERR_RESIDENCY: throw ResidencyError(msg);
+    case HS_ERR_FORMAT: throw FormatError(msg);
+    case HS_ERR_VERSION_MISMATCH: throw VersionMismatchError((unsigned)a, (unsigned)b);
+    case HS_ERR_TRUNCATED_FILE: throw TruncatedFileError((std::uint64_t)a, (std::uint64_t)b);
+    case HS_ERR_IO: throw IoError(msg);
     default: throw DeviceError(msg);
   }
 }
@@ -30,6 +36,12 @@ namespace {
 void check(hs_status s) {
   if (s != HS_OK) raise(s);
 }
+
+}  // namespace detail
+
+namespace {
+
+using detail::check;
 
 // Context for the reference entry points that take no Runtime
 // (forward_substitute / back_substitute, generate_spd).
@@ -243,6 +255,16 @@ hs_ctx* Runtime::native() {
   return ctx_;
 }
 
+void Runtime::sync_ledger() {
+  if (!ctx_) return;
+  std::vector<hs_ledger_entry> e(hs_ctx_ledger_size(ctx_));
+  e.resize(hs_ctx_ledger_read(ctx_, e.data(), e.size()));
+  hs_ctx_ledger_clear(ctx_);
+  for (const hs_ledger_entry& x : e)
+    ledger_.append(TransferEntry{static_cast<TransferKind>(x.kind),
+                                 static_cast<Direction>(x.direction), x.bytes, x.step});
+}
+
 // ---- assembly --------------------------------------------------------------
 
 namespace rng {
@@ -304,6 +326,7 @@ CgResult solve_cg(const BlockedSPDMatrix& a, const BlockVector& rhs,
   check(hs_solve_cg_host(rt.native(), a.n(), a.block_size(), a.data(), rhs.data(), &p,
                          res.x.data(), &st, cfg.record_trace ? trace.data() : nullptr));
   rt.add_transfer_ms(st.transfer_ms);
+  rt.sync_ledger();
   res.stats.iterations = st.iterations;
   res.stats.recomputations = st.recomputations;
   res.stats.converged = st.converged != 0;
@@ -324,6 +347,7 @@ FactorizeStats factorize(BlockedSPDMatrix& a, const SolverConfig& cfg, Runtime& 
   hs_chol_stats st{};
   check(hs_factorize_host(rt.native(), a.n(), a.block_size(), a.data(), &st));
   rt.add_transfer_ms(st.transfer_ms);
+  rt.sync_ledger();
   FactorizeStats out;
   out.plan = plan_for(cfg, a.block_rows());
   out.factor_ms = st.factor_ms;
@@ -359,6 +383,7 @@ SpdSolveResult solve_spd(BlockedSPDMatrix& a, const BlockVector& rhs,
   check(hs_solve_spd_host(rt.native(), a.n(), a.block_size(), a.data(), rhs.data(),
                           res.x.data(), &st));
   rt.add_transfer_ms(st.transfer_ms);
+  rt.sync_ledger();
   res.stats.plan = plan_for(cfg, a.block_rows());
   res.stats.factor_ms = st.factor_ms;
   res.stats.solve_ms = st.solve_ms;

@@ -24,6 +24,7 @@ skip host<->device copies for the measured hot path.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -64,6 +65,34 @@ class NumericalError(HsolveError):
     kind = "numerical_error"
 
 
+class ResidencyError(HsolveError):
+    kind = "residency_error"
+
+
+class FormatError(HsolveError):
+    kind = "format_error"
+
+
+class VersionMismatchError(HsolveError):
+    kind = "version_mismatch"
+
+    def __init__(self, msg, expected=-1, actual=-1):
+        super().__init__(msg)
+        self.expected, self.actual = expected, actual
+
+
+class TruncatedFileError(HsolveError):
+    kind = "truncated_file"
+
+    def __init__(self, msg, expected_bytes=-1, actual_bytes=-1):
+        super().__init__(msg)
+        self.expected_bytes, self.actual_bytes = expected_bytes, actual_bytes
+
+
+class IoError(HsolveError):
+    kind = "io_error"
+
+
 class DeviceError(HsolveError):
     kind = "cuda_error"
 
@@ -80,6 +109,16 @@ def _check(status: int) -> None:
         raise SingularBlockError(msg, b)
     if status == _lib.HS_ERR_NUMERICAL:
         raise NumericalError(msg)
+    if status == _lib.HS_ERR_RESIDENCY:
+        raise ResidencyError(msg)
+    if status == _lib.HS_ERR_FORMAT:
+        raise FormatError(msg)
+    if status == _lib.HS_ERR_VERSION_MISMATCH:
+        raise VersionMismatchError(msg, a, b)
+    if status == _lib.HS_ERR_TRUNCATED_FILE:
+        raise TruncatedFileError(msg, a, b)
+    if status == _lib.HS_ERR_IO:
+        raise IoError(msg)
     raise DeviceError(f"status {status}: {msg}")
 
 
@@ -340,6 +379,29 @@ class Runtime:
     def prof_reset(self) -> None:
         self._L.hs_prof_reset(self.ctx)
 
+    # communication ledger (transfer_ledger.hpp): one entry per NCCL collective
+    def ledger(self, clear: bool = False) -> list[TransferEntry]:
+        k = int(self._L.hs_ctx_ledger_size(self.ctx))
+        buf = (_lib.LedgerEntry * max(k, 1))()
+        k = int(self._L.hs_ctx_ledger_read(self.ctx, buf, k))
+        out = [TransferEntry(TRANSFER_KINDS[e.kind], DIRECTIONS[e.direction], int(e.bytes),
+                             int(e.step)) for e in buf[:k]]
+        if clear:
+            self._L.hs_ctx_ledger_clear(self.ctx)
+        return out
+
+
+TRANSFER_KINDS = ("scalar", "subvector", "block", "block_row", "initial_matrix", "result")
+DIRECTIONS = ("a_to_b", "b_to_a", "bidirectional")
+
+
+@dataclass
+class TransferEntry:  # transfer_ledger.hpp:28-33
+    kind: str
+    direction: str
+    bytes: int
+    step: int
+
 
 _DEFAULT_RT: Runtime | None = None
 
@@ -397,6 +459,25 @@ class DeviceMatrix:
 
     def data_ptr(self) -> int:
         return self.rt._L.hs_matrix_device_data(self.h) or 0
+
+    @classmethod
+    def load_bspd1(cls, rt: Runtime, path: str, cyclic: bool = False) -> "DeviceMatrix":
+        """Stream a BSPD1 file into HBM tiles (no host copy of the matrix)."""
+        h = C.c_void_p()
+        _check(rt._L.hs_matrix_load_bspd1(rt.ctx, os.fsencode(path), int(cyclic),
+                                          C.byref(h)))
+        self = cls.__new__(cls)
+        self.rt, self.h = rt, h
+        n, b, lo, hi = C.c_size_t(), C.c_size_t(), C.c_size_t(), C.c_size_t()
+        _check(rt._L.hs_matrix_info(h, C.byref(n), C.byref(b), C.byref(lo), C.byref(hi)))
+        self.n, self.b = n.value, b.value
+        self.rows = block_rows(self.n, self.b)
+        self.row_lo, self.row_hi = lo.value, hi.value
+        rt._matrices.add(self)
+        return self
+
+    def save_bspd1(self, path: str) -> None:
+        _check(self.rt._L.hs_matrix_save_bspd1(self.h, os.fsencode(path)))
 
     def assemble_se(self, points: np.ndarray, dim: int, sigma_f2: float, inv2l2: float,
                     sigma_n2: float) -> None:
@@ -686,3 +767,35 @@ def gemm_update_tiles_device(rt: Runtime, d_c: int, d_p: int, d_q: int, b: int, 
                              lower_only: bool = False) -> None:
     _check(rt._L.hs_gemm_update_tiles(rt.ctx, C.c_void_p(d_c), C.c_void_p(d_p),
                                       C.c_void_p(d_q), b, count, 1 if lower_only else 0))
+
+
+# ---------------------------------------------------------------------------
+# BSPD1 files (matrix_io.hpp:9-19), host side; DeviceMatrix.load_bspd1 /
+# save_bspd1 stream the same format straight to / from HBM.
+
+
+def save_matrix(m: BlockedSPDMatrix, path: str) -> None:
+    v = np.ascontiguousarray(m.values, dtype=np.float64)
+    _check(_lib.lib().hs_bspd1_write(os.fsencode(path), m.n, m.b, v.ctypes.data))
+
+
+def load_matrix(path: str) -> BlockedSPDMatrix:
+    L = _lib.lib()
+    n, b = C.c_size_t(), C.c_size_t()
+    _check(L.hs_bspd1_probe(os.fsencode(path), C.byref(n), C.byref(b)))
+    m = BlockedSPDMatrix(n.value, b.value)
+    _check(L.hs_bspd1_read(os.fsencode(path), m.values.ctypes.data, m.values.size))
+    return m
+
+
+def save_vector(v: BlockVector, path: str) -> None:
+    _check(_lib.lib().hs_vector_write(os.fsencode(path), v.n, v.values.ctypes.data))
+
+
+def load_vector(path: str, block_size: int) -> BlockVector:
+    L = _lib.lib()
+    n = C.c_size_t()
+    _check(L.hs_vector_probe(os.fsencode(path), C.byref(n)))
+    v = BlockVector(n.value, block_size)
+    _check(L.hs_vector_read(os.fsencode(path), v.values.ctypes.data, n.value))
+    return v

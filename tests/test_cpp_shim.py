@@ -30,3 +30,28 @@ def test_cpp_shim_runs_reference_assertions(tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     print(out.stdout)
     assert out.returncode == 0 and "ALL PASSED" in out.stdout, out.stdout + out.stderr
+
+
+def _build_io(tmp_path):
+    exe = str(tmp_path / "test_io_cli")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "test_io_cli.cpp"), "-o", exe,
+                    "-L", PKG, "-lhsolve_b200", "-lhsolve_cuda", f"-Wl,-rpath,{PKG}"],
+                   check=True)
+    return exe
+
+
+def test_cpp_matrix_io_and_cli_host_part(tmp_path):
+    """matrix_io.hpp / bench.hpp drop-in: format, error kinds, usage errors
+    (no GPU needed)."""
+    if not os.path.exists(os.path.join(PKG, "libhsolve_b200.so")):
+        pytest.skip("shim not built")
+    out = subprocess.run([_build_io(tmp_path)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "ALL PASSED" in out.stdout, out.stdout + out.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_matrix_io_and_cli_gpu_part(tmp_path):
+    out = subprocess.run([_build_io(tmp_path), "--gpu"], capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0 and "ALL PASSED" in out.stdout, out.stdout + out.stderr
