@@ -76,6 +76,13 @@ int hs_ctx_world(const hs_ctx* ctx);
 void* hs_ctx_stream(const hs_ctx* ctx);
 /* Number of kernels this library launched on the context so far. */
 uint64_t hs_ctx_kernel_launches(const hs_ctx* ctx);
+/* Engine of the Cholesky trailing update (gemm_update / syrk_update,
+ * block_kernels.cpp:39-57) for later hs_potrf / solve calls on this context:
+ * slices = 0 -> FP64 DMMA tensor cores (default, the reference's FP64
+ * arithmetic); 1..8 -> FP64 emulated on the INT8 tensor cores (Ozaki scheme,
+ * that many 7-bit slices per operand; 8 keeps the worst-case error at the
+ * FP64 GEMM rounding bound). Single-GPU path, b % 128 == 0; otherwise DMMA. */
+hs_status hs_ctx_set_cholesky_gemm(hs_ctx* ctx, int slices);
 
 /* ---- host-side generators (genmat.cpp:16-112, 156-162; exact) ---------- */
 uint64_t hs_rng_at(uint64_t key, uint64_t counter);
@@ -213,6 +220,15 @@ hs_status hs_potf_tiles(hs_ctx* ctx, double* d_tiles, size_t b, size_t count,
 hs_status hs_gemm_update_tiles(hs_ctx* ctx, double* d_c, const double* d_p,
                                const double* d_q, size_t b, size_t count,
                                int lower_only);
+
+/* C_t -= P_t Q_t^T (t < count) on the INT8 tensor cores with FP64-accurate
+ * Ozaki slicing (`slices` int8 slices per operand, 1..8; 8 gives FP64-level
+ * error bounds), b % 128 == 0; lower_only as hs_gemm_update_tiles. The
+ * emulated-FP64 building block of the Cholesky trailing update (gemm_update /
+ * syrk_update, block_kernels.cpp:39-57). */
+hs_status hs_oz_gemm_tiles(hs_ctx* ctx, double* d_c, const double* d_p,
+                           const double* d_q, size_t b, size_t count,
+                           int slices, int lower_only);
 
 /* ---- profiling hooks (bench.py roofline) ------------------------------- */
 /* every > 0: the CG driver brackets every `every`-th SYMV launch with CUDA

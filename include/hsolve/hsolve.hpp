@@ -185,6 +185,10 @@ struct SolverConfig {
   std::uint64_t seed = 42;
   bool record_trace = false;
   int device = 0;  // B200 build: GPU ordinal of the Runtime
+  // B200 build: Cholesky trailing-update engine. 0 = FP64 DMMA tensor cores
+  // (the reference's arithmetic); 1..8 = FP64 emulated on the INT8 tensor
+  // cores with that many slices (8: FP64-level error bound).
+  int emulated_fp64_slices = 0;
   void validate() const;
 };
 

@@ -31,6 +31,7 @@ EXPORTED = [
     "hs_last_error", "hs_last_error_payload", "hs_error_kind_name",
     "hs_ctx_create", "hs_nccl_unique_id", "hs_ctx_create_nccl", "hs_ctx_destroy",
     "hs_ctx_rank", "hs_ctx_world", "hs_ctx_stream", "hs_ctx_kernel_launches",
+    "hs_ctx_set_cholesky_gemm",
     "hs_rng_at", "hs_rng_uniform_pm1", "hs_generate_inputs",
     "hs_median_pairwise_distance", "hs_generate_rhs",
     "hs_partition_for_fraction", "hs_cholesky_border", "hs_partition_rows",
@@ -40,7 +41,7 @@ EXPORTED = [
     "hs_cg_solve", "hs_solve_cg_host", "hs_symv", "hs_true_residual",
     "hs_potrf", "hs_trsv_lower", "hs_trsv_upper", "hs_solve_spd",
     "hs_factorize_host", "hs_solve_spd_host", "hs_forward_substitute_host",
-    "hs_back_substitute_host", "hs_potf_tiles", "hs_gemm_update_tiles",
+    "hs_back_substitute_host", "hs_potf_tiles", "hs_gemm_update_tiles", "hs_oz_gemm_tiles",
     "hs_prof_enable", "hs_prof_symv", "hs_prof_reset", "hs_probe_hbm_read",
     "hs_ctx_ledger_size", "hs_ctx_ledger_read", "hs_ctx_ledger_clear",
     "hs_bspd1_probe", "hs_bspd1_read", "hs_bspd1_write", "hs_vector_probe",
@@ -101,6 +102,7 @@ def lib():
         "hs_ctx_world": (C.c_int, [vp]),
         "hs_ctx_stream": (vp, [vp]),
         "hs_ctx_kernel_launches": (u64, [vp]),
+        "hs_ctx_set_cholesky_gemm": (C.c_int, [vp, C.c_int]),
         "hs_rng_at": (u64, [u64, u64]),
         "hs_rng_uniform_pm1": (C.c_double, [u64, u64]),
         "hs_generate_inputs": (C.c_int, [sz, sz, u64, dp]),
@@ -136,6 +138,7 @@ def lib():
         "hs_back_substitute_host": (C.c_int, [vp, sz, sz, dp, dp, dp]),
         "hs_potf_tiles": (C.c_int, [vp, dp, sz, sz, C.POINTER(i64)]),
         "hs_gemm_update_tiles": (C.c_int, [vp, dp, dp, dp, sz, sz, C.c_int]),
+        "hs_oz_gemm_tiles": (C.c_int, [vp, dp, dp, dp, sz, sz, C.c_int, C.c_int]),
         "hs_prof_enable": (None, [vp, C.c_int]),
         "hs_prof_symv": (None, [vp, C.POINTER(u64), C.POINTER(C.c_double)]),
         "hs_prof_reset": (None, [vp]),

@@ -1174,6 +1174,19 @@ static CUtensorMap tile_map(const double* base, int side, int64_t ntiles) {
   return m;
 }
 
+CUtensorMap make_tensor_map(CUtensorMapDataType type, const void* base, int rank,
+                            const cuuint64_t* dims, const cuuint64_t* strides,
+                            const cuuint32_t* box, CUtensorMapSwizzle swizzle) {
+  CUtensorMap m;
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = encode_fn()(&m, type, (cuuint32_t)rank, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  HS_REQUIRE(r == CUDA_SUCCESS, HS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  return m;
+}
+
 static bool dmma_ok(int b) { return b % 128 == 0; }
 static int compute_block(int b) { return dmma_ok(b) ? 128 : b; }
 
@@ -1325,6 +1338,10 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
     mapA = tile_map(m->d, b, (int64_t)m->local_tiles());
     mapW = tile_map(m->dinv, cb, N * f);
   }
+  // trailing update on the INT8 tensor cores (emulated FP64) when selected
+  const bool use_oz = fast && c->chol_slices > 0 && N > 1;
+  OzPanel oz;
+  if (use_oz) oz.init(b, N, c->chol_slices);
 
   GemmArgs g{};
   g.N = N;
@@ -1367,6 +1384,7 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
         gp.mode = G_PANEL_TRSM;
         launch_gemm(c, cs.p, gp, t * f, &mapA, &mapW);
       }
+      if (use_oz && t > 0) oz.slice(c, cs.p, m->d, m->tile_lo, N, j, &flag->status);
       return;
     }
     // SIMT path (b % 128 != 0): single-CTA tile kernels, panel via buffer
@@ -1404,7 +1422,10 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
     const CUtensorMap* mx = fast ? &mapA : nullptr;
     // lookahead: tile column j+1 first
     gu.mode = G_UPDATE_COL;
-    launch_gemm(c, cs.u, gu, t * f * f, mx, mx);
+    if (use_oz)
+      oz.update(c, cs.u, m->d, m->tile_lo, N, j, true, &flag->status);
+    else
+      launch_gemm(c, cs.u, gu, t * f * f, mx, mx);
     cudaEvent_t ucol = cs.make();
     HS_CUDA(cudaEventRecord(ucol, cs.u));
     HS_CUDA(cudaStreamWaitEvent(cs.p, ucol));
@@ -1412,7 +1433,10 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
     // panel touches only tile column j+1; the update reads column j)
     gu.mode = G_UPDATE_REST;
     const int64_t tr = t - 1;
-    launch_gemm(c, cs.u, gu, tr * (tr + 1) / 2 * f * f, mx, mx);
+    if (use_oz)
+      oz.update(c, cs.u, m->d, m->tile_lo, N, j, false, &flag->status);
+    else
+      launch_gemm(c, cs.u, gu, tr * (tr + 1) / 2 * f * f, mx, mx);
     panel_work(j + 1);
   }
   cudaEvent_t pend = cs.make(), uend = cs.make();

@@ -567,6 +567,15 @@ int hs_ctx_world(const hs_ctx* c) { return c ? c->world : 0; }
 void* hs_ctx_stream(const hs_ctx* c) { return c ? (void*)c->stream : nullptr; }
 uint64_t hs_ctx_kernel_launches(const hs_ctx* c) { return c ? c->launches : 0; }
 
+hs_status hs_ctx_set_cholesky_gemm(hs_ctx* c, int slices) {
+  HS_API_BEGIN
+  HS_REQUIRE(c, HS_ERR_CONFIG, "null context");
+  HS_REQUIRE(slices >= 0 && slices <= 8, HS_ERR_CONFIG,
+             "Cholesky GEMM slices must be 0 (FP64 DMMA) or 1..8 (INT8 emulation)");
+  c->chol_slices = slices;
+  HS_API_END
+}
+
 size_t hs_ctx_ledger_size(const hs_ctx* c) { return c ? c->ledger.size() : 0; }
 size_t hs_ctx_ledger_read(const hs_ctx* c, hs_ledger_entry* out, size_t cap) {
   if (!c || !out) return 0;

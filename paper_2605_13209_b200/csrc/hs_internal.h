@@ -1,6 +1,7 @@
 // Internal types of libhsolve_cuda.so (not part of the ABI).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -85,6 +86,9 @@ struct hs_ctx {
   // `step` is the CG iteration / Cholesky column the drivers are in
   std::vector<hs_ledger_entry> ledger;
   int64_t step = -1;
+  // Cholesky trailing-update engine: 0 = FP64 DMMA (reference precision),
+  // 1..8 = emulated FP64 on the INT8 tensor cores with that many slices
+  int chol_slices = 0;
 };
 
 struct hs_matrix {
@@ -158,5 +162,27 @@ void launch_fill(hs_ctx* c, double* p, double v, int64_t count);
 // Scratch matrix of the context for host-buffer calls (created on first use
 // or when the shape changes; contents are overwritten by the caller).
 hs_matrix* cached_matrix(hs_ctx* c, int slot, size_t n, size_t b);
+// cuTensorMapEncodeTiled through the runtime's driver entry point (hs_chol.cu):
+// `rank`-D map, dims / box in elements, strides (rank-1 of them) in bytes.
+CUtensorMap make_tensor_map(CUtensorMapDataType type, const void* base, int rank,
+                            const cuuint64_t* dims, const cuuint64_t* strides,
+                            const cuuint32_t* box, CUtensorMapSwizzle swizzle);
+
+// Emulated-FP64 (Ozaki, INT8 tensor core) trailing update of the Cholesky
+// factorization (hs_oz.cu): int8 slices of the current panel, double
+// buffered by column parity so column j+1's slicing overlaps column j's
+// update.
+struct OzPanel {
+  int b = 0, s = 0;
+  int64_t rows = 0;                       // panel rows per buffer ((N-1) b)
+  int8_t* S[2] = {nullptr, nullptr};     // [slice][row][K] planes
+  int32_t* E[2] = {nullptr, nullptr};    // row exponents
+  ~OzPanel();
+  void init(int b, int64_t N, int s);
+  void slice(hs_ctx* c, cudaStream_t st, const double* A, int64_t tile_lo, int64_t N,
+             int64_t j, const int32_t* status);
+  void update(hs_ctx* c, cudaStream_t st, double* A, int64_t tile_lo, int64_t N, int64_t j,
+              bool col, const int32_t* status);
+};
 
 }  // namespace hs

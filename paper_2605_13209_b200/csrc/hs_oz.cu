@@ -1,0 +1,609 @@
+// FP64-accurate GEMM update C -= P Q^T on the sm_100a INT8 tensor cores
+// (Ozaki scheme I), for the Cholesky trailing update (reference
+// block_kernels.cpp:39-57 gemm_update / syrk_update).
+//
+// sm_100a has no FP64 tcgen05 kind; its FP64 path is warp-level DMMA at
+// ~35 TF/s. The INT8 tensor cores run 4.5 POPS dense, and an FP64 product can
+// be rebuilt exactly from INT8 products:
+//
+//   * slicing (oz_slice_kernel): each operand row r gets an exponent e_r
+//     (max_c |x_rc| * 2^-e_r in [0.5, 1)) and s signed 8-bit slices d_1..d_s
+//     with x = 2^e_r * sum_p d_p 2^(-6-7(p-1)) + O(2^(e_r - 7s - 1)):
+//     d_1 = rint(x 2^(6-e)), then repeatedly t = 128 * remainder,
+//     d = rint(t) -- every step exact in FP64, |d_p| <= 64.
+//   * products (oz_gemm_kernel): for each slice pair with p + q <= s + 1, an
+//     INT8 x INT8 -> INT32 tcgen05.mma accumulates exactly into the TMEM
+//     accumulator of group g = p + q (all pairs of a group share the weight
+//     2^(-12-7(g-2)); |group sum| <= 8 * K * 64^2 = 2^24 for K = 512). Up to
+//     four pairs (p, q..q+3) go out as one N = 256 MMA (see the stage layout).
+//   * epilogue: the group sums are folded exactly in int64 (groups 0-3 and
+//     4-7, each < 2^46), C -= 2^(e_r + e_c) (2^-33 hi + 2^-61 lo) with one
+//     FP64 rounding, then one TMA bulk reduce-add per output row.
+//
+// Dropped pairs (p + q > s + 1) and the slicing tail bound the error per
+// element by ~2^(-7s+12) * 2^(e_r+e_c) * K / 2^7 -- for s = 8 at or below the
+// worst-case FP64 GEMM rounding bound 2^-53 * K * 2^(e_r+e_c).
+//
+// Kernel shape: one CTA = 128 output rows x 64 columns, the whole K; all
+// s <= 8 group accumulators live in TMEM at once (8 x 64 = 512 columns).
+// 4 warps: warp 0 lane 0 issues TMA (per 64-wide K chunk one 3-D box per
+// operand carries all s slices), warp 1 lane 0 issues tcgen05.mma, then all
+// 4 warps drain TMEM (warp w owns TMEM lanes 32w..32w+31 = output rows).
+#include <cuda.h>
+#include <math.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "hs_internal.h"
+
+namespace hs {
+namespace oz {
+
+constexpr int M = 128;      // output rows per CTA (TMEM lanes)
+constexpr int N = 64;       // output columns per CTA
+constexpr int KS = 32;      // K (int8 elements = bytes) per stage: one MMA K step
+constexpr int MAXS = 8;     // max slices (8 groups x 64 columns = 512 TMEM cols)
+constexpr int STAGES = 3;
+// Slices are stored plane-major ([slice][operand row][K]); a stage holds, for
+// each slice, the rows' next 32 K bytes (32-B swizzle rows), slices stacked
+// along the row axis. The B slices q..q+3 then form one contiguous 256-row
+// K-major operand, so A_p x [B_q .. B_q+3]^T is a single N = 256 MMA whose
+// four 64-column results land in the accumulators of groups p+q .. p+q+3 --
+// consecutive TMEM columns. 12 MMAs per K step cover all 36 pairs (s = 8).
+constexpr int ROWB = KS;                  // bytes per swizzled smem row
+constexpr int A_SLICE = M * ROWB;         // 4 KB
+constexpr int B_SLICE = N * ROWB;         // 2 KB
+constexpr int A_STAGE = MAXS * A_SLICE;   // 32 KB
+constexpr int B_STAGE = MAXS * B_SLICE;   // 16 KB
+constexpr int STAGE = A_STAGE + B_STAGE;
+constexpr int RS = N * 8 + 16;            // epilogue staging row stride (bytes)
+constexpr int STAGING = M * RS;           // 66 KB, separate from the ring
+constexpr int SMEM = STAGES * STAGE + STAGING + 1024 + 256;
+// warp roles: 0 TMA producer, 1 MMA issuer, 2-3 idle, 4-11 epilogue (two
+// warps per TMEM lane quadrant, 32 output columns each)
+constexpr int EPI_WARP0 = 4, EPI_WARPS = 8;
+constexpr int THREADS = (EPI_WARP0 + EPI_WARPS) * 32;
+constexpr int32_t NONFINITE = -100000;   // row exponent sentinel (NaN / Inf row)
+
+enum Mode : int {
+  BATCH = 0,     // C_t -= P_t Q_t^T over `count` contiguous tile triples
+  CHOL_COL = 1,  // Cholesky column j: A_i,j+1 -= L_ij L_j+1,j^T, i > j
+  CHOL_REST = 2  // Cholesky column j: A_ik -= L_ij L_kj^T, j + 2 <= k <= i
+};
+
+struct Args {
+  int mode;
+  double* C;            // BATCH: output tiles; CHOL: packed tiles (local)
+  const int32_t* EA;    // row exponents of the A operand rows
+  const int32_t* EB;    // row exponents of the B operand rows
+  int b, s;
+  int lower_only;       // BATCH: SYRK-style lower-triangle update
+  int64_t count;        // BATCH: number of (C, P, Q) triples
+  int64_t j, tile_lo;   // CHOL: column, first local packed tile
+  const int32_t* status;  // optional: non-zero -> skip (factorization failed)
+};
+
+// ---------------------------------------------------------------------------
+// slicing: one warp per operand row; lane handles 4 consecutive elements
+// per step so every int8 slice row is written with 32-bit stores.
+
+// col >= 0: the operand rows are the panel tiles (i, col), i > col, of a
+// packed matrix (tile t of the panel = packed tile tri(col + 1 + t, col) -
+// tile_lo); col < 0: `rows` contiguous rows of X.
+__global__ void __launch_bounds__(256)
+    slice_kernel(const double* __restrict__ X, int64_t rows, int b, int s,
+                 int8_t* __restrict__ S, int32_t* __restrict__ E, int64_t plane_rows,
+                 int64_t col, int64_t tile_lo, const int32_t* status) {
+  if (status && *status) return;
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int64_t t = row / b, r = row % b;
+  const double* x = col < 0 ? X + row * (int64_t)b
+                            : X + ((tri(col + 1 + t, col) - tile_lo) * b + r) * (int64_t)b;
+  double mx = 0.0;
+  bool finite = true;
+  for (int c = lane; c < b; c += 32) {
+    const double v = x[c];
+    finite &= isfinite(v);
+    mx = fmax(mx, fabs(v));
+  }
+  for (int o = 16; o; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    finite = __all_sync(0xffffffffu, finite);
+  }
+  const int e = (mx > 0.0) ? ilogb(mx) + 1 : 0;
+  if (lane == 0) E[row] = finite ? e : NONFINITE;
+  (void)t;
+  (void)r;
+  // plane-major: slice p of this row at S + (p * plane_rows + row) * b
+  int8_t* base = S + row * (int64_t)b;
+  const int64_t pstride = plane_rows * (int64_t)b;
+  for (int c0 = lane * 4; c0 < b; c0 += 128) {
+    double rem[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) rem[u] = finite ? ldexp(x[c0 + u], 6 - e) : 0.0;
+    for (int p = 0; p < s; ++p) {
+      uint32_t w = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double d = rint(rem[u]);
+        rem[u] = (rem[u] - d) * 128.0;
+        w |= (uint32_t)(uint8_t)(int8_t)(int)d << (8 * u);
+      }
+      *reinterpret_cast<uint32_t*>(base + p * pstride + c0) = w;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 / TMA primitives
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0,
+                                            int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_"
+      "tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// K-major operand tile in shared memory, 32-byte swizzle (TMA
+// CU_TENSOR_MAP_SWIZZLE_32B): rows of 32 B, 8-row atoms of 256 B.
+__device__ __forceinline__ uint64_t sdesc_sw32(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);  // start address
+  d |= (uint64_t)1 << 16;                           // LBO (unused, swizzled K-major)
+  d |= (uint64_t)(256 >> 4) << 32;                  // SBO: next 8-row atom
+  d |= (uint64_t)1 << 46;                           // descriptor version (sm_100)
+  d |= (uint64_t)6 << 61;                           // layout: SWIZZLE_32B
+  return d;
+}
+
+// kind::i8 instruction descriptor: s8 x s8 -> s32, K-major A and B.
+__host__ __device__ constexpr uint32_t idesc_i8(int m, int n) {
+  return (2u << 4)                       // D format s32
+         | (1u << 7) | (1u << 10)        // A, B signed int8
+         | ((uint32_t)(n >> 3) << 17)    // N
+         | ((uint32_t)(m >> 4) << 24);   // M
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+// 16 consecutive TMEM columns of this thread's lane -> registers (no wait)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"
+      "%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+        "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+        "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// 2^e as a double (normal range; ldexp outside it)
+__device__ __forceinline__ double pow2(int e) {
+  return (e > -1023 && e < 1024) ? __longlong_as_double((long long)(e + 1023) << 52)
+                                 : ldexp(1.0, e);
+}
+
+// ---------------------------------------------------------------------------
+// one output sub-block: decoded item
+
+struct Item {
+  int a_row, b_row; // first operand row (global row of the slice buffers)
+  int a_off, b_off; // row offsets inside their b x b tiles
+  int64_t ea, eb;   // exponent index of the first A / B row
+  double* c;        // output (row-major, ld = b)
+  bool lower;       // mask to the lower triangle (col <= row) of the tile
+  bool skip;
+};
+
+__device__ __forceinline__ Item decode_item(const Args& g, int64_t item) {
+  const int fm = g.b / M, fn = g.b / N;
+  const int64_t u = item / (fm * fn);
+  const int sb = (int)(item % (fm * fn));
+  const int mb = sb / fn, nb = sb % fn;
+  const int64_t bb = (int64_t)g.b * g.b;
+  Item it;
+  it.a_off = mb * M;
+  it.b_off = nb * N;
+  bool diag;
+  if (g.mode == BATCH) {
+    it.a_row = (int)(u * g.b + mb * M);
+    it.b_row = (int)(u * g.b + nb * N);
+    it.c = g.C + u * bb + (int64_t)mb * M * g.b + nb * N;
+    diag = g.lower_only != 0;
+  } else {
+    // trailing tile (i, k) of column j; panel rows of tile i start at
+    // (i - j - 1) b in the slice buffer (gemm_update / syrk_update,
+    // block_kernels.cpp:39-57)
+    int64_t i, k;
+    if (g.mode == CHOL_COL) {
+      i = g.j + 1 + u;
+      k = g.j + 1;
+    } else {
+      const int64_t ii = tile_row(u);
+      i = g.j + 2 + ii;
+      k = g.j + 2 + (u - tri(ii, 0));
+    }
+    it.a_row = (int)((i - g.j - 1) * g.b + mb * M);
+    it.b_row = (int)((k - g.j - 1) * g.b + nb * N);
+    it.c = g.C + (tri(i, k) - g.tile_lo) * bb + (int64_t)mb * M * g.b + nb * N;
+    diag = i == k;
+  }
+  it.ea = it.a_row;
+  it.eb = it.b_row;
+  // sub-block rows [mb*M, +M), cols [nb*N, +N) of the tile
+  it.lower = diag && (nb * N + N - 1 > mb * M);
+  it.skip = diag && (nb * N > mb * M + M - 1);
+  return it;
+}
+
+// Persistent, warp-specialized: each CTA walks items blockIdx.x,
+// blockIdx.x + gridDim.x, ...; the smem ring runs ahead across items, and the
+// epilogue of item i (TMEM -> registers -> smem -> bulk reduce-add) overlaps
+// the loads of item i + 1 -- the accumulators are released as soon as they
+// are read, before the FP64 combine and the global update.
+template <int S>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap mapA,
+                const __grid_constant__ CUtensorMap mapB, Args g, int64_t items) {
+  if (g.status && *g.status) return;
+  const int nk = g.b / KS;
+
+  extern __shared__ __align__(1024) unsigned char raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* staging = sm + STAGES * STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + STAGING);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, EPI_WARPS);
+    fence_mbar_init();
+  }
+  if (warp == 0) {  // whole warp: allocate all 512 TMEM columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer: all S slices of the A rows and B rows per K chunk
+      const uint32_t bytes = (uint32_t)(S * (M + N) * ROWB);
+      int64_t kg = 0;
+      for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+        const Item it = decode_item(g, item);
+        if (it.skip) continue;
+        for (int kc = 0; kc < nk; ++kc, ++kg) {
+          const int st = (int)(kg % STAGES);
+          if (kg >= STAGES) mbar_wait(&empty[st], (uint32_t)((kg / STAGES) - 1) & 1);
+          unsigned char* sa = sm + st * STAGE;
+          mbar_arrive_expect_tx(&full[st], bytes);
+          tma_load_3d(sa, &mapA, kc * KS, it.a_row, 0, &full[st]);
+          tma_load_3d(sa + A_STAGE, &mapB, kc * KS, it.b_row, 0, &full[st]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---- MMA issuer: pairs (p, q), p + q < S (0-based) into group p + q;
+      // q in chunks of up to 4 per N <= 256 MMA; fully unrolled
+      int64_t kg = 0, lt = 0;
+      for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+        const Item it = decode_item(g, item);
+        if (it.skip) continue;
+        if (lt > 0) mbar_wait(tempty, (uint32_t)(lt - 1) & 1);  // accumulators drained
+        tc_fence_after();
+        for (int kc = 0; kc < nk; ++kc, ++kg) {
+          const int st = (int)(kg % STAGES);
+          mbar_wait(&full[st], (uint32_t)(kg / STAGES) & 1);
+          tc_fence_after();
+          const uint64_t da = sdesc_sw32(smem_u32(sm + st * STAGE));
+          const uint64_t db = sdesc_sw32(smem_u32(sm + st * STAGE + A_STAGE));
+#pragma unroll
+          for (int p = 0; p < S; ++p) {
+            // the p = 0 MMAs touch every group first: they overwrite at the
+            // first K chunk, everything else accumulates
+            const uint32_t acc = (kc > 0 || p > 0) ? 1u : 0u;
+#pragma unroll
+            for (int q0 = 0; q0 < S - p; q0 += 4) {
+              constexpr uint32_t unit = 0;  // (silences unused warnings)
+              (void)unit;
+              const int len = (S - p - q0) < 4 ? (S - p - q0) : 4;
+              mma_i8(tmem + (uint32_t)((p + q0) * N), da + (uint64_t)((p * A_SLICE) >> 4),
+                     db + (uint64_t)((q0 * B_SLICE) >> 4), idesc_i8(M, N * len), acc);
+            }
+          }
+          mma_commit(&empty[st]);  // frees the stage when these MMAs complete
+        }
+        mma_commit(tfull);
+        ++lt;
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ---- epilogue: warp quadrant qd = warp % 4 -> TMEM lanes 32 qd.., rows;
+    // half h = (warp - 4) / 4 -> columns 32 h .. 32 h + 31
+    const int qd = warp & 3, half = (warp - EPI_WARP0) >> 2;
+    const int row = qd * 32 + lane;
+    const uint32_t lane_addr = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(half * 32);
+    double* srow = reinterpret_cast<double*>(staging + row * RS) + half * 32;
+    constexpr int HG = S < 4 ? S : 4, LG = S > 4 ? S - 4 : 0;
+    const double whi = pow2(-12 - 7 * (HG - 1));
+    const double wlo = pow2(-12 - 7 * (4 + LG - 1));
+    int64_t lt = 0;
+    for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+      const Item it = decode_item(g, item);
+      if (it.skip) continue;
+      const int32_t ea = g.EA[it.ea + row];
+      bulk_wait_group_read0();  // the previous item's staging row is free
+      mbar_wait(tfull, (uint32_t)lt & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {  // 16-column chunks
+        long long hi[16], lo[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) hi[c] = lo[c] = 0;
+#pragma unroll
+        for (int grp = 0; grp < S; ++grp) {
+          int32_t v[16];
+          tmem_ld16(lane_addr + (uint32_t)(grp * N + ch * 16), v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            if (grp < 4) hi[c] = hi[c] * 128 + v[c];
+            else lo[c] = lo[c] * 128 + v[c];
+          }
+        }
+        if (ch == 1) {  // every accumulator column of this warp is read
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty);
+        }
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const int col = half * 32 + ch * 16 + c;
+          const int32_t eb = g.EB[it.eb + col];
+          const double val = fma((double)lo[c], wlo, (double)hi[c] * whi);
+          const double r = (ea == NONFINITE || eb == NONFINITE)
+                               ? __longlong_as_double(0x7ff8000000000000ll)
+                               : val * pow2(ea + eb);
+          srow[ch * 16 + c] = -r;
+        }
+      }
+      if (!it.lower) {
+        fence_proxy_async_smem();
+        bulk_reduce_add_f64(it.c + (int64_t)row * g.b + half * 32, srow, 32 * 8);
+        bulk_commit_group();
+      } else {
+        // diagonal sub-block of a SYRK update: lower triangle only
+        const int grow = it.a_off + row;
+        for (int c = 0; c < 32; ++c)
+          if (it.b_off + half * 32 + c <= grow)
+            it.c[(int64_t)row * g.b + half * 32 + c] += srow[c];
+      }
+      ++lt;
+    }
+    bulk_wait_group_read0();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem)
+                 : "memory");
+}
+
+template <int S>
+static void launch_gemm_s(hs_ctx* c, cudaStream_t st, const CUtensorMap& ma,
+                          const CUtensorMap& mb, const Args& g, int64_t items) {
+  static bool attr = false;
+  if (!attr) {
+    HS_CUDA(cudaFuncSetAttribute(gemm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 SMEM));
+    attr = true;
+  }
+  const int64_t grid = std::min<int64_t>(items, c->num_sms);
+  gemm_kernel<S><<<(unsigned)grid, THREADS, SMEM, st>>>(ma, mb, g, items);
+  HS_CUDA(cudaGetLastError());
+  launch_count(c);
+}
+
+static void launch_gemm(hs_ctx* c, cudaStream_t st, const CUtensorMap& ma,
+                        const CUtensorMap& mb, const Args& g, int64_t items) {
+  if (items <= 0) return;
+  switch (g.s) {
+    case 1: launch_gemm_s<1>(c, st, ma, mb, g, items); break;
+    case 2: launch_gemm_s<2>(c, st, ma, mb, g, items); break;
+    case 3: launch_gemm_s<3>(c, st, ma, mb, g, items); break;
+    case 4: launch_gemm_s<4>(c, st, ma, mb, g, items); break;
+    case 5: launch_gemm_s<5>(c, st, ma, mb, g, items); break;
+    case 6: launch_gemm_s<6>(c, st, ma, mb, g, items); break;
+    case 7: launch_gemm_s<7>(c, st, ma, mb, g, items); break;
+    default: launch_gemm_s<8>(c, st, ma, mb, g, items); break;
+  }
+}
+
+// 3-D map over the slice planes [slice][row][K]: box 32 B x box_rows x s.
+static CUtensorMap slice_map(const int8_t* base, int b, int64_t rows, int box_rows, int s) {
+  cuuint64_t dims[3] = {(cuuint64_t)b, (cuuint64_t)std::max<int64_t>(rows, 1), (cuuint64_t)MAXS};
+  cuuint64_t strides[2] = {(cuuint64_t)b, (cuuint64_t)b * std::max<int64_t>(rows, 1)};
+  cuuint32_t box[3] = {(cuuint32_t)KS, (cuuint32_t)box_rows, (cuuint32_t)s};
+  return make_tensor_map(CU_TENSOR_MAP_DATA_TYPE_UINT8, base, 3, dims, strides, box,
+                         CU_TENSOR_MAP_SWIZZLE_32B);
+}
+
+}  // namespace oz
+
+// Slice `tiles` consecutive b x b FP64 tiles (tiles * b operand rows) into
+// int8 slice planes ([slice][row][K], plane = plane_rows * b bytes), plus
+// per-row exponents.
+void oz_slice(hs_ctx* c, cudaStream_t st, const double* X, int64_t tiles, int b, int s,
+              int8_t* S, int32_t* E, int64_t plane_rows, int64_t col, int64_t tile_lo,
+              const int32_t* status) {
+  const int64_t rows = tiles * b;
+  if (rows <= 0) return;
+  oz::slice_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(X, rows, b, s, S, E,
+                                                                 plane_rows, col, tile_lo,
+                                                                 status);
+  HS_CUDA(cudaGetLastError());
+  launch_count(c);
+}
+
+// ---- Cholesky trailing update on the INT8 tensor cores ---------------------
+
+OzPanel::~OzPanel() {
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(S[k]);
+    cudaFree(E[k]);
+  }
+}
+
+void OzPanel::init(int b_, int64_t N_, int s_) {
+  b = b_;
+  s = s_;
+  rows = std::max<int64_t>(N_ - 1, 1) * b;
+  for (int k = 0; k < 2; ++k) {
+    HS_CUDA(cudaMalloc(&S[k], (size_t)rows * b * oz::MAXS));
+    HS_CUDA(cudaMalloc(&E[k], (size_t)rows * sizeof(int32_t)));
+  }
+}
+
+// Slices the panel tiles (i, j), i > j, of column j into buffer j & 1.
+void OzPanel::slice(hs_ctx* c, cudaStream_t st, const double* A, int64_t tile_lo, int64_t N,
+                    int64_t j, const int32_t* status) {
+  const int64_t t = N - 1 - j;
+  oz_slice(c, st, A, t, b, s, S[j & 1], E[j & 1], rows, j, tile_lo, status);
+}
+
+// A_ik -= L_ij L_kj^T for the tiles of column j: `col` selects k == j + 1
+// (the lookahead column), else j + 2 <= k <= i.
+void OzPanel::update(hs_ctx* c, cudaStream_t st, double* A, int64_t tile_lo, int64_t N,
+                     int64_t j, bool col, const int32_t* status) {
+  const int64_t t = N - 1 - j;
+  const int64_t tiles = col ? t : (t - 1) * t / 2;
+  if (tiles <= 0) return;
+  const int fm = b / oz::M, fn = b / oz::N;
+  const CUtensorMap ma = oz::slice_map(S[j & 1], b, rows, oz::M, s);
+  const CUtensorMap mb = oz::slice_map(S[j & 1], b, rows, oz::N, s);
+  oz::Args g{};
+  g.mode = col ? oz::CHOL_COL : oz::CHOL_REST;
+  g.C = A;
+  g.EA = g.EB = E[j & 1];
+  g.b = b;
+  g.s = s;
+  g.j = j;
+  g.tile_lo = tile_lo;
+  g.status = status;
+  oz::launch_gemm(c, st, ma, mb, g, tiles * fm * fn);
+}
+
+}  // namespace hs
+
+using namespace hs;
+
+#define HS_API_BEGIN \
+  clear_error();     \
+  try {
+#define HS_API_END                                                         \
+  return HS_OK;                                                            \
+  }                                                                        \
+  catch (const Failure& f) {                                               \
+    set_error(f.status, f.msg, f.a, f.b);                                  \
+    return f.status;                                                       \
+  }                                                                        \
+  catch (const std::exception& e) {                                        \
+    set_error(HS_ERR_CUDA, e.what());                                      \
+    return HS_ERR_CUDA;                                                    \
+  }
+
+extern "C" {
+
+hs_status hs_oz_gemm_tiles(hs_ctx* c, double* d_c, const double* d_p, const double* d_q,
+                           size_t b, size_t count, int slices, int lower_only) {
+  HS_API_BEGIN
+  HS_REQUIRE(c && d_c && d_p && d_q, HS_ERR_CONFIG, "null pointer");
+  HS_REQUIRE(b % 128 == 0 && b > 0, HS_ERR_CONFIG, "the INT8 path needs b % 128 == 0");
+  HS_REQUIRE(slices >= 1 && slices <= oz::MAXS, HS_ERR_CONFIG, "slices must be in [1, 8]");
+  HS_CUDA(cudaSetDevice(c->device));
+  if (count == 0) return HS_OK;
+  const int s = slices;
+  const size_t plane = b * b;
+  int8_t *sp = nullptr, *sq = nullptr;
+  int32_t *ep = nullptr, *eq = nullptr;
+  auto release = [&] {
+    cudaFree(sp);
+    cudaFree(sq);
+    cudaFree(ep);
+    cudaFree(eq);
+  };
+  try {
+    HS_CUDA(cudaMalloc(&sp, count * oz::MAXS * plane));
+    HS_CUDA(cudaMalloc(&sq, count * oz::MAXS * plane));
+    HS_CUDA(cudaMalloc(&ep, count * b * sizeof(int32_t)));
+    HS_CUDA(cudaMalloc(&eq, count * b * sizeof(int32_t)));
+    const int64_t rows = (int64_t)(count * b);
+    oz_slice(c, c->stream, d_p, (int64_t)count, (int)b, s, sp, ep, rows, -1, 0, nullptr);
+    oz_slice(c, c->stream, d_q, (int64_t)count, (int)b, s, sq, eq, rows, -1, 0, nullptr);
+    const CUtensorMap ma = oz::slice_map(sp, (int)b, rows, oz::M, s);
+    const CUtensorMap mb = oz::slice_map(sq, (int)b, rows, oz::N, s);
+    oz::Args g{};
+    g.mode = oz::BATCH;
+    g.C = d_c;
+    g.EA = ep;
+    g.EB = eq;
+    g.b = (int)b;
+    g.s = s;
+    g.lower_only = lower_only;
+    g.count = (int64_t)count;
+    const int64_t items = (int64_t)count * (b / oz::M) * (b / oz::N);
+    oz::launch_gemm(c, c->stream, ma, mb, g, items);
+    HS_CUDA(cudaStreamSynchronize(c->stream));
+  } catch (...) {
+    release();
+    throw;
+  }
+  release();
+  HS_API_END
+}
+
+}  // extern "C"

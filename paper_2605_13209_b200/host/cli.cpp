@@ -58,6 +58,7 @@ const std::vector<Opt>& options() {
       {"matrix", Kind::text, S | W},
       {"no-warmup", Kind::flag, S | W},
       {"device", Kind::size, G | S | W},
+      {"fp64-emulation-slices", Kind::size, S | W},
       {"fractions", Kind::text, W},
       {"sizes", Kind::text, W},
       {"block-sizes", Kind::text, W},
@@ -204,7 +205,9 @@ void usage(std::ostream& os) {
         "  sweep  [--sizes L --block-sizes L --fractions lo:hi:step|list --summary]\n"
         "solver options: --block-size --fraction --eps --max-iters --recompute-interval\n"
         "  --workers-a --workers-b --slowdown-a --slowdown-b --reps --seed --no-warmup\n"
-        "  --device; kernel options: --sigma-f2 --sigma-n2 --length-scale --dim;\n"
+        "  --device --fp64-emulation-slices S (Cholesky update on the INT8 tensor\n"
+        "  cores, 1..8; 0 = FP64 DMMA); kernel options: --sigma-f2 --sigma-n2\n"
+        "  --length-scale --dim;\n"
         "  --config FILE (key=value, [command] sections; flags override)\n";
 }
 
@@ -296,6 +299,8 @@ Common apply(const Values& v) {
   if (auto s = get("slowdown-a")) c.cfg.slowdown_a = as_real("slowdown-a", *s);
   if (auto s = get("slowdown-b")) c.cfg.slowdown_b = as_real("slowdown-b", *s);
   if (auto s = get("device")) c.cfg.device = (int)as_size("device", *s);
+  if (auto s = get("fp64-emulation-slices"))
+    c.cfg.emulated_fp64_slices = (int)as_size("fp64-emulation-slices", *s);
   if (auto s = get("reps")) c.reps = as_size("reps", *s);
   if (auto s = get("sigma-f2")) c.kernel.sigma_f2 = as_real("sigma-f2", *s);
   if (auto s = get("sigma-n2")) c.kernel.sigma_n2 = as_real("sigma-n2", *s);

@@ -166,6 +166,8 @@ void SolverConfig::validate() const {
     throw ConfigError("both executors need at least one worker");
   if (!(slowdown_a >= 1.0) || !(slowdown_b >= 1.0))
     throw ConfigError("slowdown factors must be >= 1.0");
+  if (emulated_fp64_slices < 0 || emulated_fp64_slices > 8)
+    throw ConfigError("emulated_fp64_slices must be in [0, 8]");
 }
 
 Partition partition_for_fraction(double f, std::size_t rows) {
@@ -345,6 +347,7 @@ CgResult solve_cg(const BlockedSPDMatrix& a, const BlockVector& rhs,
 FactorizeStats factorize(BlockedSPDMatrix& a, const SolverConfig& cfg, Runtime& rt) {
   cfg.validate();
   hs_chol_stats st{};
+  check(hs_ctx_set_cholesky_gemm(rt.native(), cfg.emulated_fp64_slices));
   check(hs_factorize_host(rt.native(), a.n(), a.block_size(), a.data(), &st));
   rt.add_transfer_ms(st.transfer_ms);
   rt.sync_ledger();
@@ -380,6 +383,7 @@ SpdSolveResult solve_spd(BlockedSPDMatrix& a, const BlockVector& rhs,
     throw ConfigError("matrix and right-hand side shapes do not match");
   SpdSolveResult res{BlockVector(a.n(), a.block_size()), SpdSolveStats{}};
   hs_chol_stats st{};
+  check(hs_ctx_set_cholesky_gemm(rt.native(), cfg.emulated_fp64_slices));
   check(hs_solve_spd_host(rt.native(), a.n(), a.block_size(), a.data(), rhs.data(),
                           res.x.data(), &st));
   rt.add_transfer_ms(st.transfer_ms);

@@ -353,6 +353,11 @@ class Runtime:
     def kernel_launches(self) -> int:
         return int(self._L.hs_ctx_kernel_launches(self.ctx))
 
+    def set_cholesky_gemm(self, slices: int) -> None:
+        """Cholesky trailing-update engine: 0 = FP64 DMMA (default), 1..8 =
+        FP64 emulated on the INT8 tensor cores with that many slices."""
+        _check(self._L.hs_ctx_set_cholesky_gemm(self.ctx, int(slices)))
+
     def close(self) -> None:
         if getattr(self, "ctx", None):
             for m in list(getattr(self, "_matrices", ())):
