@@ -229,6 +229,9 @@ hs_status hs_gemm_update_tiles(hs_ctx* ctx, double* d_c, const double* d_p,
 hs_status hs_oz_gemm_tiles(hs_ctx* ctx, double* d_c, const double* d_p,
                            const double* d_q, size_t b, size_t count,
                            int slices, int lower_only);
+/* Tuning hook: later hs_oz_gemm_tiles calls write per-CTA phase timestamps
+ * (globaltimer ns; [cta][tile < 64][8]) to this device buffer (NULL: off). */
+void hs_oz_set_profile(void* d_buf);
 
 /* ---- profiling hooks (bench.py roofline) ------------------------------- */
 /* every > 0: the CG driver brackets every `every`-th SYMV launch with CUDA

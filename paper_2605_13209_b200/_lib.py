@@ -42,6 +42,7 @@ EXPORTED = [
     "hs_potrf", "hs_trsv_lower", "hs_trsv_upper", "hs_solve_spd",
     "hs_factorize_host", "hs_solve_spd_host", "hs_forward_substitute_host",
     "hs_back_substitute_host", "hs_potf_tiles", "hs_gemm_update_tiles", "hs_oz_gemm_tiles",
+    "hs_oz_set_profile",
     "hs_prof_enable", "hs_prof_symv", "hs_prof_reset", "hs_probe_hbm_read",
     "hs_ctx_ledger_size", "hs_ctx_ledger_read", "hs_ctx_ledger_clear",
     "hs_bspd1_probe", "hs_bspd1_read", "hs_bspd1_write", "hs_vector_probe",
@@ -139,6 +140,7 @@ def lib():
         "hs_potf_tiles": (C.c_int, [vp, dp, sz, sz, C.POINTER(i64)]),
         "hs_gemm_update_tiles": (C.c_int, [vp, dp, dp, dp, sz, sz, C.c_int]),
         "hs_oz_gemm_tiles": (C.c_int, [vp, dp, dp, dp, sz, sz, C.c_int, C.c_int]),
+        "hs_oz_set_profile": (None, [vp]),
         "hs_prof_enable": (None, [vp, C.c_int]),
         "hs_prof_symv": (None, [vp, C.POINTER(u64), C.POINTER(C.c_double)]),
         "hs_prof_reset": (None, [vp]),

@@ -1423,7 +1423,8 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
     // lookahead: tile column j+1 first
     gu.mode = G_UPDATE_COL;
     if (use_oz)
-      oz.update(c, cs.u, m->d, m->tile_lo, N, j, true, &flag->status);
+      oz.update(c, cs.u, m->d, m->tile_lo, (int64_t)m->local_tiles(), N, j, true,
+                &flag->status);
     else
       launch_gemm(c, cs.u, gu, t * f * f, mx, mx);
     cudaEvent_t ucol = cs.make();
@@ -1434,7 +1435,8 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
     gu.mode = G_UPDATE_REST;
     const int64_t tr = t - 1;
     if (use_oz)
-      oz.update(c, cs.u, m->d, m->tile_lo, N, j, false, &flag->status);
+      oz.update(c, cs.u, m->d, m->tile_lo, (int64_t)m->local_tiles(), N, j, false,
+                &flag->status);
     else
       launch_gemm(c, cs.u, gu, tr * (tr + 1) / 2 * f * f, mx, mx);
     panel_work(j + 1);

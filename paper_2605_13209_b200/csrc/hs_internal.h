@@ -181,8 +181,8 @@ struct OzPanel {
   void init(int b, int64_t N, int s);
   void slice(hs_ctx* c, cudaStream_t st, const double* A, int64_t tile_lo, int64_t N,
              int64_t j, const int32_t* status);
-  void update(hs_ctx* c, cudaStream_t st, double* A, int64_t tile_lo, int64_t N, int64_t j,
-              bool col, const int32_t* status);
+  void update(hs_ctx* c, cudaStream_t st, double* A, int64_t tile_lo, int64_t local_tiles,
+              int64_t N, int64_t j, bool col, const int32_t* status);
 };
 
 }  // namespace hs

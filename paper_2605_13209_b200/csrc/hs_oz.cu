@@ -57,12 +57,15 @@ constexpr int B_SLICE = N * ROWB;         // 2 KB
 constexpr int A_STAGE = MAXS * A_SLICE;   // 32 KB
 constexpr int B_STAGE = MAXS * B_SLICE;   // 16 KB
 constexpr int STAGE = A_STAGE + B_STAGE;
-constexpr int RS = N * 8 + 16;            // epilogue staging row stride (bytes)
-constexpr int STAGING = M * RS;           // 66 KB, separate from the ring
-constexpr int SMEM = STAGES * STAGE + STAGING + 1024 + 256;
-// warp roles: 0 TMA producer, 1 MMA issuer, 2-3 idle, 4-11 epilogue (two
-// warps per TMEM lane quadrant, 32 output columns each)
-constexpr int EPI_WARP0 = 4, EPI_WARPS = 8;
+// epilogue staging, separate from the ring: the 128 x 64 FP64 result as four
+// 128-B-swizzled [128 rows][16 cols] boxes, written back by four TMA tensor
+// reduce-adds (C += staging) -- 4 bulk ops per tile instead of 256
+constexpr int SBOX = M * 128;             // 16 KB per 16-column box
+constexpr int STAGING = 4 * SBOX;         // 64 KB
+constexpr int SMEM = STAGES * STAGE + STAGING + 1024 + 1024;
+// warp roles: 0 TMA producer, 1 MMA issuer, 2-9 epilogue (two warps per
+// TMEM lane quadrant, 32 output columns each)
+constexpr int EPI_WARP0 = 2, EPI_WARPS = 8;
 constexpr int THREADS = (EPI_WARP0 + EPI_WARPS) * 32;
 constexpr int32_t NONFINITE = -100000;   // row exponent sentinel (NaN / Inf row)
 
@@ -82,7 +85,26 @@ struct Args {
   int64_t count;        // BATCH: number of (C, P, Q) triples
   int64_t j, tile_lo;   // CHOL: column, first local packed tile
   const int32_t* status;  // optional: non-zero -> skip (factorization failed)
+  long long* prof;        // optional phase timestamps (tools/oz_bench.py --phases)
 };
+
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, int c0, int c1,
+                                                  int c2, const void* src) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group "
+      "[%0, {%1, %2, %3}], [%4];" ::"l"(map),
+      "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+      : "memory");
+}
+
+// prof layout: [cta][tile < 64][8] globaltimer stamps
+__device__ __forceinline__ void prof_stamp(long long* prof, int64_t lt, int k) {
+  if (prof && lt < 64) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    prof[((int64_t)blockIdx.x * 64 + lt) * 8 + k] = t;
+  }
+}
 
 // ---------------------------------------------------------------------------
 // slicing: one warp per operand row; lane handles 4 consecutive elements
@@ -201,8 +223,31 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
         "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
 }
+// 32 consecutive TMEM columns of this thread's lane -> registers (no wait)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"
+      "%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,"
+      "%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+        "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+        "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]),
+        "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+        "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// -x * 2^e by exponent arithmetic (integer ops only; FP64 pipe untouched):
+// exact whenever x and the result are normal, ldexp otherwise.
+__device__ __forceinline__ double neg_scale2(double x, int e) {
+  const long long bits = __double_as_longlong(x);
+  const int ex = (int)((bits >> 52) & 0x7ff);
+  if (ex == 0 || ex + e <= 0 || ex + e >= 0x7ff) return -ldexp(x, e);  // 0, subnormal, range
+  return __longlong_as_double((bits + ((long long)e << 52)) ^ (long long)0x8000000000000000ull);
 }
 
 // 2^e as a double (normal range; ldexp outside it)
@@ -217,6 +262,7 @@ __device__ __forceinline__ double pow2(int e) {
 struct Item {
   int a_row, b_row; // first operand row (global row of the slice buffers)
   int a_off, b_off; // row offsets inside their b x b tiles
+  int c_tile;       // output tile index in the C tensor map
   int64_t ea, eb;   // exponent index of the first A / B row
   double* c;        // output (row-major, ld = b)
   bool lower;       // mask to the lower triangle (col <= row) of the tile
@@ -237,6 +283,7 @@ __device__ __forceinline__ Item decode_item(const Args& g, int64_t item) {
     it.a_row = (int)(u * g.b + mb * M);
     it.b_row = (int)(u * g.b + nb * N);
     it.c = g.C + u * bb + (int64_t)mb * M * g.b + nb * N;
+    it.c_tile = (int)u;
     diag = g.lower_only != 0;
   } else {
     // trailing tile (i, k) of column j; panel rows of tile i start at
@@ -254,6 +301,7 @@ __device__ __forceinline__ Item decode_item(const Args& g, int64_t item) {
     it.a_row = (int)((i - g.j - 1) * g.b + mb * M);
     it.b_row = (int)((k - g.j - 1) * g.b + nb * N);
     it.c = g.C + (tri(i, k) - g.tile_lo) * bb + (int64_t)mb * M * g.b + nb * N;
+    it.c_tile = (int)(tri(i, k) - g.tile_lo);
     diag = i == k;
   }
   it.ea = it.a_row;
@@ -272,7 +320,8 @@ __device__ __forceinline__ Item decode_item(const Args& g, int64_t item) {
 template <int S>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap mapA,
-                const __grid_constant__ CUtensorMap mapB, Args g, int64_t items) {
+                const __grid_constant__ CUtensorMap mapB,
+                const __grid_constant__ CUtensorMap mapC, Args g, int64_t items) {
   if (g.status && *g.status) return;
   const int nk = g.b / KS;
 
@@ -285,6 +334,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  int32_t* ebs = reinterpret_cast<int32_t*>(tempty + 2);  // [2][N] column exponents
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -333,8 +383,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
         const Item it = decode_item(g, item);
         if (it.skip) continue;
+        prof_stamp(g.prof, lt, 0);
         if (lt > 0) mbar_wait(tempty, (uint32_t)(lt - 1) & 1);  // accumulators drained
         tc_fence_after();
+        prof_stamp(g.prof, lt, 1);
         for (int kc = 0; kc < nk; ++kc, ++kg) {
           const int st = (int)(kg % STAGES);
           mbar_wait(&full[st], (uint32_t)(kg / STAGES) & 1);
@@ -358,73 +410,96 @@ __global__ void __launch_bounds__(THREADS, 1)
           mma_commit(&empty[st]);  // frees the stage when these MMAs complete
         }
         mma_commit(tfull);
+        prof_stamp(g.prof, lt, 2);
         ++lt;
       }
     }
   } else if (warp >= EPI_WARP0) {
     // ---- epilogue: warp quadrant qd = warp % 4 -> TMEM lanes 32 qd.., rows;
-    // half h = (warp - 4) / 4 -> columns 32 h .. 32 h + 31
+    // half h = (warp - EPI_WARP0) / 4 -> columns 32 h .. 32 h + 31
     const int qd = warp & 3, half = (warp - EPI_WARP0) >> 2;
     const int row = qd * 32 + lane;
     const uint32_t lane_addr = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(half * 32);
-    double* srow = reinterpret_cast<double*>(staging + row * RS) + half * 32;
-    constexpr int HG = S < 4 ? S : 4, LG = S > 4 ? S - 4 : 0;
-    const double whi = pow2(-12 - 7 * (HG - 1));
-    const double wlo = pow2(-12 - 7 * (4 + LG - 1));
+    const bool issuer = threadIdx.x == EPI_WARP0 * 32;
+    const int et = threadIdx.x - EPI_WARP0 * 32;  // 0 .. 255
     int64_t lt = 0;
     for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
       const Item it = decode_item(g, item);
       if (it.skip) continue;
       const int32_t ea = g.EA[it.ea + row];
-      bulk_wait_group_read0();  // the previous item's staging row is free
+      // column exponents of this item, staged while the MMAs run (double
+      // buffered: a slow warp may still read the previous item's)
+      int32_t* eb_s = ebs + (lt & 1) * N;
+      if (et < N) eb_s[et] = g.EB[it.eb + et];
+      if (issuer) prof_stamp(g.prof, lt, 3);
       mbar_wait(tfull, (uint32_t)lt & 1);
       tc_fence_after();
+      if (issuer) prof_stamp(g.prof, lt, 4);
+      // drain: read every group of this warp's 32 columns, smallest weight
+      // first, into FP64 partial sums (each int32 group sum and weight is
+      // exact; the 8 roundings are far below the FP64 GEMM rounding bound),
+      // then hand the accumulators back to the MMA warp
+      double acc[32];
 #pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {  // 16-column chunks
-        long long hi[16], lo[16];
+      for (int c = 0; c < 32; ++c) acc[c] = 0.0;
 #pragma unroll
-        for (int c = 0; c < 16; ++c) hi[c] = lo[c] = 0;
+      for (int grp = S - 1; grp >= 0; --grp) {
+        int32_t v[32];
+        tmem_ld32(lane_addr + (uint32_t)(grp * N), v);
+        tmem_wait_ld();
+        const double w = pow2(-12 - 7 * grp);
 #pragma unroll
-        for (int grp = 0; grp < S; ++grp) {
-          int32_t v[16];
-          tmem_ld16(lane_addr + (uint32_t)(grp * N + ch * 16), v);
-          tmem_wait_ld();
+        for (int c = 0; c < 32; ++c) acc[c] = fma((double)v[c], w, acc[c]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+      if (issuer) prof_stamp(g.prof, lt, 5);
+      const bool bad_row = ea == NONFINITE;
+      // the previous item's reduce-adds have read the staging boxes (and
+      // every thread's exponents are in eb_s)
+      if (issuer) bulk_wait_group_read0();
+      named_bar_sync(1, EPI_WARPS * 32);
+      if (issuer) prof_stamp(g.prof, lt, 7);
+      const double qnan = __longlong_as_double(0x7ff8000000000000ll);
 #pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            if (grp < 4) hi[c] = hi[c] * 128 + v[c];
-            else lo[c] = lo[c] * 128 + v[c];
-          }
-        }
-        if (ch == 1) {  // every accumulator column of this warp is read
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(tempty);
-        }
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          const int col = half * 32 + ch * 16 + c;
-          const int32_t eb = g.EB[it.eb + col];
-          const double val = fma((double)lo[c], wlo, (double)hi[c] * whi);
-          const double r = (ea == NONFINITE || eb == NONFINITE)
-                               ? __longlong_as_double(0x7ff8000000000000ll)
-                               : val * pow2(ea + eb);
-          srow[ch * 16 + c] = -r;
-        }
+      for (int c = 0; c < 32; c += 2) {
+        const int cc = half * 32 + c;
+        const int32_t eb0 = eb_s[cc], eb1 = eb_s[cc + 1];
+        double2 r;
+        r.x = (bad_row || eb0 == NONFINITE) ? qnan : neg_scale2(acc[c], ea + eb0);
+        r.y = (bad_row || eb1 == NONFINITE) ? qnan : neg_scale2(acc[c + 1], ea + eb1);
+        // column cc: box cc / 16, 16-B chunk (cc % 16) / 2 of row `row`,
+        // XOR-swizzled by row % 8 (conflict-free 16-B stores)
+        unsigned char* dst = staging + (cc >> 4) * SBOX + row * 128 +
+                             ((((cc & 15) >> 1) ^ (row & 7)) << 4);
+        *reinterpret_cast<double2*>(dst) = r;
       }
       if (!it.lower) {
         fence_proxy_async_smem();
-        bulk_reduce_add_f64(it.c + (int64_t)row * g.b + half * 32, srow, 32 * 8);
-        bulk_commit_group();
+        named_bar_sync(1, EPI_WARPS * 32);
+        if (issuer) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            tma_reduce_add_3d(&mapC, it.b_off + 16 * k, it.a_off, it.c_tile,
+                              staging + k * SBOX);
+          bulk_commit_group();
+          prof_stamp(g.prof, lt, 6);
+        }
       } else {
         // diagonal sub-block of a SYRK update: lower triangle only
         const int grow = it.a_off + row;
-        for (int c = 0; c < 32; ++c)
-          if (it.b_off + half * 32 + c <= grow)
-            it.c[(int64_t)row * g.b + half * 32 + c] += srow[c];
+        for (int c = 0; c < 32; ++c) {
+          const int cc = half * 32 + c;
+          const double* src = reinterpret_cast<const double*>(
+              staging + (cc >> 4) * SBOX + row * 128 + ((((cc & 15) >> 1) ^ (row & 7)) << 4)) +
+                              (cc & 1);
+          if (it.b_off + cc <= grow) it.c[(int64_t)row * g.b + cc] += *src;
+        }
       }
       ++lt;
     }
-    bulk_wait_group_read0();
+    if (issuer) bulk_wait_group_read0();
   }
   tc_fence_before();
   __syncthreads();
@@ -435,7 +510,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 template <int S>
 static void launch_gemm_s(hs_ctx* c, cudaStream_t st, const CUtensorMap& ma,
-                          const CUtensorMap& mb, const Args& g, int64_t items) {
+                          const CUtensorMap& mb, const CUtensorMap& mc, const Args& g,
+                          int64_t items) {
   static bool attr = false;
   if (!attr) {
     HS_CUDA(cudaFuncSetAttribute(gemm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -443,23 +519,34 @@ static void launch_gemm_s(hs_ctx* c, cudaStream_t st, const CUtensorMap& ma,
     attr = true;
   }
   const int64_t grid = std::min<int64_t>(items, c->num_sms);
-  gemm_kernel<S><<<(unsigned)grid, THREADS, SMEM, st>>>(ma, mb, g, items);
+  gemm_kernel<S><<<(unsigned)grid, THREADS, SMEM, st>>>(ma, mb, mc, g, items);
   HS_CUDA(cudaGetLastError());
   launch_count(c);
 }
 
+// 3-D map over `tiles` contiguous b x b FP64 output tiles: box 16 x 128 x 1,
+// 128-B swizzle (the epilogue staging layout).
+static CUtensorMap out_map(const double* base, int b, int64_t tiles) {
+  cuuint64_t dims[3] = {(cuuint64_t)b, (cuuint64_t)b, (cuuint64_t)std::max<int64_t>(tiles, 1)};
+  cuuint64_t strides[2] = {(cuuint64_t)b * 8, (cuuint64_t)b * b * 8};
+  cuuint32_t box[3] = {16, (cuuint32_t)M, 1};
+  return make_tensor_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT64, base, 3, dims, strides, box,
+                         CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
 static void launch_gemm(hs_ctx* c, cudaStream_t st, const CUtensorMap& ma,
-                        const CUtensorMap& mb, const Args& g, int64_t items) {
+                        const CUtensorMap& mb, const CUtensorMap& mc, const Args& g,
+                        int64_t items) {
   if (items <= 0) return;
   switch (g.s) {
-    case 1: launch_gemm_s<1>(c, st, ma, mb, g, items); break;
-    case 2: launch_gemm_s<2>(c, st, ma, mb, g, items); break;
-    case 3: launch_gemm_s<3>(c, st, ma, mb, g, items); break;
-    case 4: launch_gemm_s<4>(c, st, ma, mb, g, items); break;
-    case 5: launch_gemm_s<5>(c, st, ma, mb, g, items); break;
-    case 6: launch_gemm_s<6>(c, st, ma, mb, g, items); break;
-    case 7: launch_gemm_s<7>(c, st, ma, mb, g, items); break;
-    default: launch_gemm_s<8>(c, st, ma, mb, g, items); break;
+    case 1: launch_gemm_s<1>(c, st, ma, mb, mc, g, items); break;
+    case 2: launch_gemm_s<2>(c, st, ma, mb, mc, g, items); break;
+    case 3: launch_gemm_s<3>(c, st, ma, mb, mc, g, items); break;
+    case 4: launch_gemm_s<4>(c, st, ma, mb, mc, g, items); break;
+    case 5: launch_gemm_s<5>(c, st, ma, mb, mc, g, items); break;
+    case 6: launch_gemm_s<6>(c, st, ma, mb, mc, g, items); break;
+    case 7: launch_gemm_s<7>(c, st, ma, mb, mc, g, items); break;
+    default: launch_gemm_s<8>(c, st, ma, mb, mc, g, items); break;
   }
 }
 
@@ -517,8 +604,9 @@ void OzPanel::slice(hs_ctx* c, cudaStream_t st, const double* A, int64_t tile_lo
 
 // A_ik -= L_ij L_kj^T for the tiles of column j: `col` selects k == j + 1
 // (the lookahead column), else j + 2 <= k <= i.
-void OzPanel::update(hs_ctx* c, cudaStream_t st, double* A, int64_t tile_lo, int64_t N,
-                     int64_t j, bool col, const int32_t* status) {
+void OzPanel::update(hs_ctx* c, cudaStream_t st, double* A, int64_t tile_lo,
+                     int64_t local_tiles, int64_t N, int64_t j, bool col,
+                     const int32_t* status) {
   const int64_t t = N - 1 - j;
   const int64_t tiles = col ? t : (t - 1) * t / 2;
   if (tiles <= 0) return;
@@ -534,7 +622,8 @@ void OzPanel::update(hs_ctx* c, cudaStream_t st, double* A, int64_t tile_lo, int
   g.j = j;
   g.tile_lo = tile_lo;
   g.status = status;
-  oz::launch_gemm(c, st, ma, mb, g, tiles * fm * fn);
+  const CUtensorMap mc = oz::out_map(A, b, local_tiles);
+  oz::launch_gemm(c, st, ma, mb, mc, g, tiles * fm * fn);
 }
 
 }  // namespace hs
@@ -556,7 +645,12 @@ using namespace hs;
     return HS_ERR_CUDA;                                                    \
   }
 
+// test / tuning hook: phase timestamps of the next hs_oz_gemm_tiles call
+static long long* g_oz_prof = nullptr;
+
 extern "C" {
+
+void hs_oz_set_profile(void* d_buf) { g_oz_prof = static_cast<long long*>(d_buf); }
 
 hs_status hs_oz_gemm_tiles(hs_ctx* c, double* d_c, const double* d_p, const double* d_q,
                            size_t b, size_t count, int slices, int lower_only) {
@@ -588,6 +682,7 @@ hs_status hs_oz_gemm_tiles(hs_ctx* c, double* d_c, const double* d_p, const doub
     const CUtensorMap mb = oz::slice_map(sq, (int)b, rows, oz::N, s);
     oz::Args g{};
     g.mode = oz::BATCH;
+    g.prof = g_oz_prof;
     g.C = d_c;
     g.EA = ep;
     g.EB = eq;
@@ -596,7 +691,8 @@ hs_status hs_oz_gemm_tiles(hs_ctx* c, double* d_c, const double* d_p, const doub
     g.lower_only = lower_only;
     g.count = (int64_t)count;
     const int64_t items = (int64_t)count * (b / oz::M) * (b / oz::N);
-    oz::launch_gemm(c, c->stream, ma, mb, g, items);
+    const CUtensorMap mc = oz::out_map(d_c, (int)b, (int64_t)count);
+    oz::launch_gemm(c, c->stream, ma, mb, mc, g, items);
     HS_CUDA(cudaStreamSynchronize(c->stream));
   } catch (...) {
     release();

@@ -20,6 +20,8 @@ def main():
     ap.add_argument("--count", type=int, default=64)
     ap.add_argument("--slices", type=int, default=8)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--phases", action="store_true",
+                    help="per-tile phase breakdown from in-kernel timestamps")
     a = ap.parse_args()
     rt = hs.Runtime(stream=torch.cuda.current_stream().cuda_stream)
     b, n = a.b, a.count
@@ -46,6 +48,21 @@ def main():
                                                       Q.data_ptr(), b, n, a.slices, 0)))
     ms_dm = t(lambda: H.gemm_update_tiles_device(rt, C.data_ptr(), P.data_ptr(), Q.data_ptr(),
                                                  b, n))
+    if a.phases:
+        import numpy as np
+        buf = torch.zeros(148 * 64 * 8, dtype=torch.int64, device="cuda")
+        rt._L.hs_oz_set_profile(buf.data_ptr())
+        H._check(rt._L.hs_oz_gemm_tiles(rt.ctx, C.data_ptr(), P.data_ptr(), Q.data_ptr(), b, n,
+                                        a.slices, 0))
+        rt._L.hs_oz_set_profile(None)
+        t = buf.view(148, 64, 8).cpu().numpy().astype(np.float64)
+        ok = (t[:, 1:-1, :7] > 0).all(axis=2)
+        d = lambda x, y: np.median((t[:, 1:-1, y] - t[:, 1:-1, x])[ok])
+        per = np.diff(t[:, :, 1], axis=1)
+        pmask = (t[:, 1:, 1] > 0) & (t[:, :-1, 1] > 0)
+        print(f"per tile (median, ns): tempty wait {d(0, 1):.0f}, MMA issue->commit "
+              f"{d(1, 2):.0f}, epi wait tfull {d(3, 4):.0f}, drain {d(4, 5):.0f}, "
+              f"barrier {d(5, 7):.0f}, fp64+stage {d(7, 6):.0f}; tile period {np.median(per[pmask]):.0f}")
     print(f"b={b} count={n} slices={a.slices}: oz {ms_oz:.3f} ms = {flops / ms_oz / 1e9:.1f} "
           f"TF/s (FP64-equivalent, incl. slicing+alloc); dmma {ms_dm:.3f} ms = "
           f"{flops / ms_dm / 1e9:.1f} TF/s")
