@@ -19,7 +19,9 @@ n=32768, b=128 (BASELINE.json configs[1]), FP64, one B200.
 * ``cpu_baseline`` — the compiled reference (oracle/_ref, kind "reference")
   or the C restatement (kind "port") on this host's cores, bounded sample.
 * ``secondary`` — tiled Cholesky n=32768, b=512 (configs[2]) GFLOP/s
-  (n^3/3 / factor time) against cuBLAS DGEMM measured live in this run.
+  (n^3/3 / factor time) against cuBLAS DGEMM measured live in this run;
+  ``secondary.emulated_fp64`` — the same factorization with the trailing
+  update on the INT8 tensor cores (Ozaki slicing, FP64-level accuracy).
 
 ``--impl reference`` times the reference CPU implementation (rank 0 only).
 Multi-GPU (torchrun, N>1): row-sharded CG over NCCL, strong scaling on the
@@ -254,6 +256,57 @@ def cholesky_secondary(hs, H, rt, torch, args, peak_tf: float, world: int = 1,
                         "frac": gflops / 1e3 / world / peak_tf,
                         "peak_source": "cuBLAS DGEMM 8192^3 measured live in this run "
                                        "(MEASURED_PEAKS.json has no FP64 entry)"}}
+    if not cyclic and args.chol_slices > 0:
+        # the same factorization with the trailing update on the INT8 tensor
+        # cores (emulated FP64, Ozaki slicing); L compared with the DMMA L
+        small = n <= 65536  # both factors on the device for the comparison
+        L_dmma = torch.from_numpy(work.download()).cuda() if small else None
+        rt.set_cholesky_gemm(args.chol_slices)
+        et = []
+        for rep in range(1 + args.chol_reps):
+            work.copy_from(m)
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            H.potrf_device(rt, work)
+            e.record()
+            e.synchronize()
+            if rep > 0:
+                et.append(s.elapsed_time(e))
+        rt.set_cholesky_gemm(0)
+        ems = statistics.median(et)
+        eg = n ** 3 / 3 / (ems * 1e-3) / 1e9
+        diff = None
+        if small:
+            L_oz = torch.from_numpy(work.download()).cuda()
+            diff = float((L_oz - L_dmma).abs().max() / L_dmma.abs().max())
+            del L_oz, L_dmma
+        # solve with the emulated factor: relative residual
+        rhs_e = torch.from_numpy(hs.generate_rhs(n, b, 42).values).cuda()
+        x_e = rhs_e.clone()
+        H.trsv_device(rt, work, x_e.data_ptr(), upper=False)
+        H.trsv_device(rt, work, x_e.data_ptr(), upper=True)
+        res_e = H.true_residual_device(rt, m, x_e.data_ptr(), rhs_e.data_ptr())
+        rel_e = res_e / float(torch.linalg.vector_norm(rhs_e[:n]))
+        del rhs_e, x_e
+        # INT8 tensor work: every FP64 MAC of the trailing update becomes
+        # s(s+1)/2 INT8 MACs; nominal dense INT8 peak 4.5 POPS (no measured one)
+        pairs = args.chol_slices * (args.chol_slices + 1) // 2
+        i8 = eg * 1e9 * pairs / 1e15
+        out["emulated_fp64"] = {
+            "value": eg, "unit": "GFLOP/s", "ms_per_factor": ems,
+            "speedup_vs_dmma": ms / ems,
+            "engine": f"trailing update on the INT8 tensor cores (tcgen05 kind::i8), "
+                      f"Ozaki slicing, {args.chol_slices} slices",
+            "max_abs_L_minus_L_dmma_over_max_L": diff,
+            "relative_residual": rel_e,
+            "roofline": {"bound": "tensor", "achieved": eg / 1e3, "peak": peak_tf,
+                         "unit": "TFLOP/s (FP64-equivalent) vs DGEMM",
+                         "frac": eg / 1e3 / peak_tf,
+                         "int8_pops_achieved_approx": i8, "int8_pops_nominal": 4.5,
+                         "int8_frac_approx": i8 / 4.5}}
+        work.copy_from(m)
+        H.potrf_device(rt, work)  # DMMA factor again for the solve below
     if not cyclic:  # substitutions (single GPU), for the record
         rhs = torch.from_numpy(hs.generate_rhs(n, b, 42).values).cuda()
         x = torch.empty_like(rhs)
@@ -477,6 +530,9 @@ def main():
     ap.add_argument("--chol-n", type=int, default=32768)
     ap.add_argument("--chol-b", type=int, default=512)
     ap.add_argument("--chol-reps", type=int, default=2)
+    ap.add_argument("--chol-slices", type=int, default=8,
+                    help="also time the INT8-emulated FP64 Cholesky with this many "
+                         "slices (0: skip)")
     ap.add_argument("--cpu-chol-n", type=int, default=4096)
     ap.add_argument("--cpu-iters", type=int, default=20)
     ap.add_argument("--ref-iters", type=int, default=50)

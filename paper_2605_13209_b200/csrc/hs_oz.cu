@@ -33,6 +33,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "hs_internal.h"
@@ -518,7 +519,17 @@ static void launch_gemm_s(hs_ctx* c, cudaStream_t st, const CUtensorMap& ma,
                                  SMEM));
     attr = true;
   }
-  const int64_t grid = std::min<int64_t>(items, c->num_sms);
+  // Bounded persistence: each CTA walks ~ipc items (strided by the grid, so
+  // co-resident CTAs work on neighbouring items), then retires. A CTA that
+  // owned its SM for the whole update would lock the Cholesky's
+  // high-priority panel stream out of the GPU; retiring every few tiles lets
+  // the block scheduler slip panel CTAs in.
+  static const int ipc = [] {
+    const char* e = getenv("HS_OZ_ITEMS_PER_CTA");
+    return e ? std::max(1, atoi(e)) : 16;
+  }();
+  const int64_t grid = std::max<int64_t>(
+      std::min<int64_t>(items, c->num_sms), ceil_div(items, ipc));
   gemm_kernel<S><<<(unsigned)grid, THREADS, SMEM, st>>>(ma, mb, mc, g, items);
   HS_CUDA(cudaGetLastError());
   launch_count(c);

@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--n", type=int, default=32768)
     ap.add_argument("--b", type=int, default=128)
     ap.add_argument("--iters", type=int, default=6)
+    ap.add_argument("--slices", type=int, default=0,
+                    help="Cholesky trailing update on the INT8 tensor cores (0: DMMA)")
     a = ap.parse_args()
     rt = hs.Runtime()
     m = hs.generate_spd_device(rt, a.n, a.b, seed=42)
@@ -32,6 +34,7 @@ def main():
         st = hs.solve_cg_device(rt, m, rhs.data_ptr(), x.data_ptr(), cfg)
         print("cg iterations", st.iterations)
     else:
+        rt.set_cholesky_gemm(a.slices)
         st = hs.potrf_device(rt, m)
         print("factor ms", st.factor_ms)
     torch.cuda.synchronize()
