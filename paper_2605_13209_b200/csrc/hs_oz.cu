@@ -17,8 +17,10 @@
 //     2^(-12-7(g-2)); |group sum| <= 8 * K * 64^2 = 2^24 for K = 512). Up to
 //     four pairs (p, q..q+3) go out as one N = 256 MMA (see the stage layout).
 //   * epilogue: the group sums are folded exactly in int64 (groups 0-3 and
-//     4-7, each < 2^46), C -= 2^(e_r + e_c) (2^-33 hi + 2^-61 lo) with one
-//     FP64 rounding, then one TMA bulk reduce-add per output row.
+//     4-7, each < 2^46), converted without I2F (2^52 + 2^51 trick),
+//     C -= 2^(e_r + e_c) (2^-33 hi + 2^-61 lo) with one FP64 rounding (the
+//     power of two applied by exponent arithmetic), read-modify-write of the
+//     output block straight from registers.
 //
 // Dropped pairs (p + q > s + 1) and the slicing tail bound the error per
 // element by ~2^(-7s+12) * 2^(e_r+e_c) * K / 2^7 -- for s = 8 at or below the
@@ -26,9 +28,12 @@
 //
 // Kernel shape: one CTA = 128 output rows x 64 columns, the whole K; all
 // s <= 8 group accumulators live in TMEM at once (8 x 64 = 512 columns).
-// 4 warps: warp 0 lane 0 issues TMA (per 64-wide K chunk one 3-D box per
-// operand carries all s slices), warp 1 lane 0 issues tcgen05.mma, then all
-// 4 warps drain TMEM (warp w owns TMEM lanes 32w..32w+31 = output rows).
+// Persistent with bounded item counts (the Cholesky panel stream must be
+// able to interleave), warp-specialized: warp 0 lane 0 issues TMA (per
+// 64-wide K chunk one 3-D box per operand carries all s slices, 64-B
+// swizzle, 2-stage ring), warp 1 lane 0 issues tcgen05.mma, warps 2-9 drain
+// TMEM (two warps per 32-lane quadrant, 32 columns each) and release it
+// before the FP64 work, so the next item's MMAs overlap this epilogue.
 #include <cuda.h>
 #include <math.h>
 
@@ -43,27 +48,22 @@ namespace oz {
 
 constexpr int M = 128;      // output rows per CTA (TMEM lanes)
 constexpr int N = 64;       // output columns per CTA
-constexpr int KS = 32;      // K (int8 elements = bytes) per stage: one MMA K step
+constexpr int KS = 64;      // K (int8 elements = bytes) per stage: two MMA K steps
 constexpr int MAXS = 8;     // max slices (8 groups x 64 columns = 512 TMEM cols)
-constexpr int STAGES = 3;
+constexpr int STAGES = 2;
 // Slices are stored plane-major ([slice][operand row][K]); a stage holds, for
-// each slice, the rows' next 32 K bytes (32-B swizzle rows), slices stacked
-// along the row axis. The B slices q..q+3 then form one contiguous 256-row
+// each slice, the rows' next 64 K bytes (64-B swizzle rows: half the TMA
+// row requests of 32-B rows), slices stacked along the row axis. The B slices q..q+3 then form one contiguous 256-row
 // K-major operand, so A_p x [B_q .. B_q+3]^T is a single N = 256 MMA whose
 // four 64-column results land in the accumulators of groups p+q .. p+q+3 --
 // consecutive TMEM columns. 12 MMAs per K step cover all 36 pairs (s = 8).
 constexpr int ROWB = KS;                  // bytes per swizzled smem row
-constexpr int A_SLICE = M * ROWB;         // 4 KB
-constexpr int B_SLICE = N * ROWB;         // 2 KB
+constexpr int A_SLICE = M * ROWB;         // 8 KB
+constexpr int B_SLICE = N * ROWB;         // 4 KB
 constexpr int A_STAGE = MAXS * A_SLICE;   // 32 KB
 constexpr int B_STAGE = MAXS * B_SLICE;   // 16 KB
 constexpr int STAGE = A_STAGE + B_STAGE;
-// epilogue staging, separate from the ring: the 128 x 64 FP64 result as four
-// 128-B-swizzled [128 rows][16 cols] boxes, written back by four TMA tensor
-// reduce-adds (C += staging) -- 4 bulk ops per tile instead of 256
-constexpr int SBOX = M * 128;             // 16 KB per 16-column box
-constexpr int STAGING = 4 * SBOX;         // 64 KB
-constexpr int SMEM = STAGES * STAGE + STAGING + 1024 + 1024;
+constexpr int SMEM = STAGES * STAGE + 1024 + 1024;
 // warp roles: 0 TMA producer, 1 MMA issuer, 2-9 epilogue (two warps per
 // TMEM lane quadrant, 32 output columns each)
 constexpr int EPI_WARP0 = 2, EPI_WARPS = 8;
@@ -88,15 +88,6 @@ struct Args {
   const int32_t* status;  // optional: non-zero -> skip (factorization failed)
   long long* prof;        // optional phase timestamps (tools/oz_bench.py --phases)
 };
-
-__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, int c0, int c1,
-                                                  int c2, const void* src) {
-  asm volatile(
-      "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group "
-      "[%0, {%1, %2, %3}], [%4];" ::"l"(map),
-      "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
-      : "memory");
-}
 
 // prof layout: [cta][tile < 64][8] globaltimer stamps
 __device__ __forceinline__ void prof_stamp(long long* prof, int64_t lt, int k) {
@@ -172,14 +163,15 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// K-major operand tile in shared memory, 32-byte swizzle (TMA
-// CU_TENSOR_MAP_SWIZZLE_32B): rows of 32 B, 8-row atoms of 256 B.
-__device__ __forceinline__ uint64_t sdesc_sw32(uint32_t saddr) {
+// K-major operand tile in shared memory, 64-byte swizzle (TMA
+// CU_TENSOR_MAP_SWIZZLE_64B): rows of 64 B, 8-row atoms of 512 B; the start
+// address may sit 32 B into the row (second MMA K step).
+__device__ __forceinline__ uint64_t sdesc_sw64(uint32_t saddr) {
   uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);  // start address
   d |= (uint64_t)1 << 16;                           // LBO (unused, swizzled K-major)
-  d |= (uint64_t)(256 >> 4) << 32;                  // SBO: next 8-row atom
+  d |= (uint64_t)(512 >> 4) << 32;                  // SBO: next 8-row atom
   d |= (uint64_t)1 << 46;                           // descriptor version (sm_100)
-  d |= (uint64_t)6 << 61;                           // layout: SWIZZLE_32B
+  d |= (uint64_t)4 << 61;                           // layout: SWIZZLE_64B
   return d;
 }
 
@@ -263,7 +255,6 @@ __device__ __forceinline__ double pow2(int e) {
 struct Item {
   int a_row, b_row; // first operand row (global row of the slice buffers)
   int a_off, b_off; // row offsets inside their b x b tiles
-  int c_tile;       // output tile index in the C tensor map
   int64_t ea, eb;   // exponent index of the first A / B row
   double* c;        // output (row-major, ld = b)
   bool lower;       // mask to the lower triangle (col <= row) of the tile
@@ -284,7 +275,6 @@ __device__ __forceinline__ Item decode_item(const Args& g, int64_t item) {
     it.a_row = (int)(u * g.b + mb * M);
     it.b_row = (int)(u * g.b + nb * N);
     it.c = g.C + u * bb + (int64_t)mb * M * g.b + nb * N;
-    it.c_tile = (int)u;
     diag = g.lower_only != 0;
   } else {
     // trailing tile (i, k) of column j; panel rows of tile i start at
@@ -302,7 +292,6 @@ __device__ __forceinline__ Item decode_item(const Args& g, int64_t item) {
     it.a_row = (int)((i - g.j - 1) * g.b + mb * M);
     it.b_row = (int)((k - g.j - 1) * g.b + nb * N);
     it.c = g.C + (tri(i, k) - g.tile_lo) * bb + (int64_t)mb * M * g.b + nb * N;
-    it.c_tile = (int)(tri(i, k) - g.tile_lo);
     diag = i == k;
   }
   it.ea = it.a_row;
@@ -321,16 +310,14 @@ __device__ __forceinline__ Item decode_item(const Args& g, int64_t item) {
 template <int S>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap mapA,
-                const __grid_constant__ CUtensorMap mapB,
-                const __grid_constant__ CUtensorMap mapC, Args g, int64_t items) {
+                const __grid_constant__ CUtensorMap mapB, Args g, int64_t items) {
   if (g.status && *g.status) return;
   const int nk = g.b / KS;
 
   extern __shared__ __align__(1024) unsigned char raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
-  unsigned char* staging = sm + STAGES * STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(staging + STAGING);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * STAGE);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 1;
@@ -392,20 +379,21 @@ __global__ void __launch_bounds__(THREADS, 1)
           const int st = (int)(kg % STAGES);
           mbar_wait(&full[st], (uint32_t)(kg / STAGES) & 1);
           tc_fence_after();
-          const uint64_t da = sdesc_sw32(smem_u32(sm + st * STAGE));
-          const uint64_t db = sdesc_sw32(smem_u32(sm + st * STAGE + A_STAGE));
 #pragma unroll
-          for (int p = 0; p < S; ++p) {
-            // the p = 0 MMAs touch every group first: they overwrite at the
-            // first K chunk, everything else accumulates
-            const uint32_t acc = (kc > 0 || p > 0) ? 1u : 0u;
+          for (int ks = 0; ks < KS / 32; ++ks) {
+            const uint64_t da = sdesc_sw64(smem_u32(sm + st * STAGE) + ks * 32);
+            const uint64_t db = sdesc_sw64(smem_u32(sm + st * STAGE + A_STAGE) + ks * 32);
 #pragma unroll
-            for (int q0 = 0; q0 < S - p; q0 += 4) {
-              constexpr uint32_t unit = 0;  // (silences unused warnings)
-              (void)unit;
-              const int len = (S - p - q0) < 4 ? (S - p - q0) : 4;
-              mma_i8(tmem + (uint32_t)((p + q0) * N), da + (uint64_t)((p * A_SLICE) >> 4),
-                     db + (uint64_t)((q0 * B_SLICE) >> 4), idesc_i8(M, N * len), acc);
+            for (int p = 0; p < S; ++p) {
+              // the p = 0 MMAs touch every group first: they overwrite at
+              // the first K step, everything else accumulates
+              const uint32_t acc = (kc > 0 || ks > 0 || p > 0) ? 1u : 0u;
+#pragma unroll
+              for (int q0 = 0; q0 < S - p; q0 += 4) {
+                const int len = (S - p - q0) < 4 ? (S - p - q0) : 4;
+                mma_i8(tmem + (uint32_t)((p + q0) * N), da + (uint64_t)((p * A_SLICE) >> 4),
+                       db + (uint64_t)((q0 * B_SLICE) >> 4), idesc_i8(M, N * len), acc);
+              }
             }
           }
           mma_commit(&empty[st]);  // frees the stage when these MMAs complete
@@ -436,71 +424,77 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(tfull, (uint32_t)lt & 1);
       tc_fence_after();
       if (issuer) prof_stamp(g.prof, lt, 4);
-      // drain: read every group of this warp's 32 columns, smallest weight
-      // first, into FP64 partial sums (each int32 group sum and weight is
-      // exact; the 8 roundings are far below the FP64 GEMM rounding bound),
-      // then hand the accumulators back to the MMA warp
+      // drain: per 16-column half, fold the groups exactly in int64 (groups
+      // 0-3 -> hi, 4-7 -> lo, each < 2^46), convert both with the 2^52 + 2^51
+      // magic-number trick (no I2F: the conversion pipe was the drain's
+      // bottleneck), acc = 2^-33 hi + 2^-61 lo (one FP64 rounding); then hand
+      // the accumulators back to the MMA warp
+      constexpr int HG = S < 4 ? S : 4, LG = S > 4 ? S - 4 : 0;
+      const double whi = pow2(-12 - 7 * (HG - 1));
+      const double wlo = pow2(-12 - 7 * (4 + LG - 1));
       double acc[32];
 #pragma unroll
-      for (int c = 0; c < 32; ++c) acc[c] = 0.0;
+      for (int h = 0; h < 2; ++h) {
+        long long hi[16], lo[16];
 #pragma unroll
-      for (int grp = S - 1; grp >= 0; --grp) {
-        int32_t v[32];
-        tmem_ld32(lane_addr + (uint32_t)(grp * N), v);
-        tmem_wait_ld();
-        const double w = pow2(-12 - 7 * grp);
+        for (int c = 0; c < 16; ++c) hi[c] = lo[c] = 0;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) acc[c] = fma((double)v[c], w, acc[c]);
+        for (int grp = 0; grp < S; ++grp) {
+          int32_t v[16];
+          tmem_ld16(lane_addr + (uint32_t)(grp * N + h * 16), v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            if (grp < 4) hi[c] = (hi[c] << 7) + v[c];
+            else lo[c] = (lo[c] << 7) + v[c];
+          }
+        }
+        constexpr long long kMagic = 0x4338000000000000ll;  // 2^52 + 2^51
+        const double kMagicD = 6755399441055744.0;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const double dh = __longlong_as_double(hi[c] + kMagic) - kMagicD;
+          const double dl = __longlong_as_double(lo[c] + kMagic) - kMagicD;
+          acc[h * 16 + c] = fma(dl, wlo, dh * whi);
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty);
       if (issuer) prof_stamp(g.prof, lt, 5);
       const bool bad_row = ea == NONFINITE;
-      // the previous item's reduce-adds have read the staging boxes (and
-      // every thread's exponents are in eb_s)
-      if (issuer) bulk_wait_group_read0();
-      named_bar_sync(1, EPI_WARPS * 32);
+      named_bar_sync(1, EPI_WARPS * 32);  // every thread's exponents are in eb_s
       if (issuer) prof_stamp(g.prof, lt, 7);
       const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+      // write-back straight from registers: this CTA owns the output block,
+      // so a plain read-modify-write of the thread's 32-column row segment
+      // (16-B accesses). Measured faster than staging through shared memory
+      // (a smem transpose + coalesced RMW, or TMA tensor reduce-adds): the
+      // tensor cores' operand reads keep the smem/L1 datapath busy, and every
+      // extra smem pass of the epilogue stretches it.
+      double* crow = it.c + (int64_t)row * g.b + half * 32;
+      const int grow = it.a_off + row;
 #pragma unroll
-      for (int c = 0; c < 32; c += 2) {
-        const int cc = half * 32 + c;
-        const int32_t eb0 = eb_s[cc], eb1 = eb_s[cc + 1];
-        double2 r;
-        r.x = (bad_row || eb0 == NONFINITE) ? qnan : neg_scale2(acc[c], ea + eb0);
-        r.y = (bad_row || eb1 == NONFINITE) ? qnan : neg_scale2(acc[c + 1], ea + eb1);
-        // column cc: box cc / 16, 16-B chunk (cc % 16) / 2 of row `row`,
-        // XOR-swizzled by row % 8 (conflict-free 16-B stores)
-        unsigned char* dst = staging + (cc >> 4) * SBOX + row * 128 +
-                             ((((cc & 15) >> 1) ^ (row & 7)) << 4);
-        *reinterpret_cast<double2*>(dst) = r;
-      }
-      if (!it.lower) {
-        fence_proxy_async_smem();
-        named_bar_sync(1, EPI_WARPS * 32);
-        if (issuer) {
+      for (int h = 0; h < 2; ++h) {
+        double2 cur[8];
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            tma_reduce_add_3d(&mapC, it.b_off + 16 * k, it.a_off, it.c_tile,
-                              staging + k * SBOX);
-          bulk_commit_group();
-          prof_stamp(g.prof, lt, 6);
-        }
-      } else {
-        // diagonal sub-block of a SYRK update: lower triangle only
-        const int grow = it.a_off + row;
-        for (int c = 0; c < 32; ++c) {
-          const int cc = half * 32 + c;
-          const double* src = reinterpret_cast<const double*>(
-              staging + (cc >> 4) * SBOX + row * 128 + ((((cc & 15) >> 1) ^ (row & 7)) << 4)) +
-                              (cc & 1);
-          if (it.b_off + cc <= grow) it.c[(int64_t)row * g.b + cc] += *src;
+        for (int u = 0; u < 8; ++u) cur[u] = reinterpret_cast<const double2*>(crow)[h * 8 + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = h * 16 + 2 * u, cc = half * 32 + c;
+          const int32_t eb0 = eb_s[cc], eb1 = eb_s[cc + 1];
+          const double d0 = (bad_row || eb0 == NONFINITE) ? qnan : neg_scale2(acc[c], ea + eb0);
+          const double d1 =
+              (bad_row || eb1 == NONFINITE) ? qnan : neg_scale2(acc[c + 1], ea + eb1);
+          double2 v = cur[u];
+          if (!it.lower || it.b_off + cc <= grow) v.x += d0;
+          if (!it.lower || it.b_off + cc + 1 <= grow) v.y += d1;
+          reinterpret_cast<double2*>(crow)[h * 8 + u] = v;
         }
       }
+      if (issuer) prof_stamp(g.prof, lt, 6);
       ++lt;
     }
-    if (issuer) bulk_wait_group_read0();
   }
   tc_fence_before();
   __syncthreads();
@@ -511,7 +505,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 template <int S>
 static void launch_gemm_s(hs_ctx* c, cudaStream_t st, const CUtensorMap& ma,
-                          const CUtensorMap& mb, const CUtensorMap& mc, const Args& g,
+                          const CUtensorMap& mb, const Args& g,
                           int64_t items) {
   static bool attr = false;
   if (!attr) {
@@ -530,44 +524,34 @@ static void launch_gemm_s(hs_ctx* c, cudaStream_t st, const CUtensorMap& ma,
   }();
   const int64_t grid = std::max<int64_t>(
       std::min<int64_t>(items, c->num_sms), ceil_div(items, ipc));
-  gemm_kernel<S><<<(unsigned)grid, THREADS, SMEM, st>>>(ma, mb, mc, g, items);
+  gemm_kernel<S><<<(unsigned)grid, THREADS, SMEM, st>>>(ma, mb, g, items);
   HS_CUDA(cudaGetLastError());
   launch_count(c);
 }
 
-// 3-D map over `tiles` contiguous b x b FP64 output tiles: box 16 x 128 x 1,
-// 128-B swizzle (the epilogue staging layout).
-static CUtensorMap out_map(const double* base, int b, int64_t tiles) {
-  cuuint64_t dims[3] = {(cuuint64_t)b, (cuuint64_t)b, (cuuint64_t)std::max<int64_t>(tiles, 1)};
-  cuuint64_t strides[2] = {(cuuint64_t)b * 8, (cuuint64_t)b * b * 8};
-  cuuint32_t box[3] = {16, (cuuint32_t)M, 1};
-  return make_tensor_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT64, base, 3, dims, strides, box,
-                         CU_TENSOR_MAP_SWIZZLE_128B);
-}
-
 static void launch_gemm(hs_ctx* c, cudaStream_t st, const CUtensorMap& ma,
-                        const CUtensorMap& mb, const CUtensorMap& mc, const Args& g,
+                        const CUtensorMap& mb, const Args& g,
                         int64_t items) {
   if (items <= 0) return;
   switch (g.s) {
-    case 1: launch_gemm_s<1>(c, st, ma, mb, mc, g, items); break;
-    case 2: launch_gemm_s<2>(c, st, ma, mb, mc, g, items); break;
-    case 3: launch_gemm_s<3>(c, st, ma, mb, mc, g, items); break;
-    case 4: launch_gemm_s<4>(c, st, ma, mb, mc, g, items); break;
-    case 5: launch_gemm_s<5>(c, st, ma, mb, mc, g, items); break;
-    case 6: launch_gemm_s<6>(c, st, ma, mb, mc, g, items); break;
-    case 7: launch_gemm_s<7>(c, st, ma, mb, mc, g, items); break;
-    default: launch_gemm_s<8>(c, st, ma, mb, mc, g, items); break;
+    case 1: launch_gemm_s<1>(c, st, ma, mb, g, items); break;
+    case 2: launch_gemm_s<2>(c, st, ma, mb, g, items); break;
+    case 3: launch_gemm_s<3>(c, st, ma, mb, g, items); break;
+    case 4: launch_gemm_s<4>(c, st, ma, mb, g, items); break;
+    case 5: launch_gemm_s<5>(c, st, ma, mb, g, items); break;
+    case 6: launch_gemm_s<6>(c, st, ma, mb, g, items); break;
+    case 7: launch_gemm_s<7>(c, st, ma, mb, g, items); break;
+    default: launch_gemm_s<8>(c, st, ma, mb, g, items); break;
   }
 }
 
-// 3-D map over the slice planes [slice][row][K]: box 32 B x box_rows x s.
+// 3-D map over the slice planes [slice][row][K]: box 64 B x box_rows x s.
 static CUtensorMap slice_map(const int8_t* base, int b, int64_t rows, int box_rows, int s) {
   cuuint64_t dims[3] = {(cuuint64_t)b, (cuuint64_t)std::max<int64_t>(rows, 1), (cuuint64_t)MAXS};
   cuuint64_t strides[2] = {(cuuint64_t)b, (cuuint64_t)b * std::max<int64_t>(rows, 1)};
   cuuint32_t box[3] = {(cuuint32_t)KS, (cuuint32_t)box_rows, (cuuint32_t)s};
   return make_tensor_map(CU_TENSOR_MAP_DATA_TYPE_UINT8, base, 3, dims, strides, box,
-                         CU_TENSOR_MAP_SWIZZLE_32B);
+                         CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
 }  // namespace oz
@@ -633,8 +617,8 @@ void OzPanel::update(hs_ctx* c, cudaStream_t st, double* A, int64_t tile_lo,
   g.j = j;
   g.tile_lo = tile_lo;
   g.status = status;
-  const CUtensorMap mc = oz::out_map(A, b, local_tiles);
-  oz::launch_gemm(c, st, ma, mb, mc, g, tiles * fm * fn);
+  (void)local_tiles;
+  oz::launch_gemm(c, st, ma, mb, g, tiles * fm * fn);
 }
 
 }  // namespace hs
@@ -702,8 +686,7 @@ hs_status hs_oz_gemm_tiles(hs_ctx* c, double* d_c, const double* d_p, const doub
     g.lower_only = lower_only;
     g.count = (int64_t)count;
     const int64_t items = (int64_t)count * (b / oz::M) * (b / oz::N);
-    const CUtensorMap mc = oz::out_map(d_c, (int)b, (int64_t)count);
-    oz::launch_gemm(c, c->stream, ma, mb, mc, g, items);
+    oz::launch_gemm(c, c->stream, ma, mb, g, items);
     HS_CUDA(cudaStreamSynchronize(c->stream));
   } catch (...) {
     release();
