@@ -81,7 +81,8 @@ uint64_t hs_ctx_kernel_launches(const hs_ctx* ctx);
  * slices = 0 -> FP64 DMMA tensor cores (default, the reference's FP64
  * arithmetic); 1..8 -> FP64 emulated on the INT8 tensor cores (Ozaki scheme,
  * that many 7-bit slices per operand; 8 keeps the worst-case error at the
- * FP64 GEMM rounding bound). Single-GPU path, b % 128 == 0; otherwise DMMA. */
+ * FP64 GEMM rounding bound). Single-GPU and 2D block-cyclic multi-GPU paths,
+ * b % 128 == 0; otherwise DMMA. */
 hs_status hs_ctx_set_cholesky_gemm(hs_ctx* ctx, int slices);
 
 /* ---- host-side generators (genmat.cpp:16-112, 156-162; exact) ---------- */

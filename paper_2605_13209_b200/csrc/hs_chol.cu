@@ -1558,6 +1558,11 @@ static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
 
   const CUtensorMap mapA = tile_map(m->d, b, std::max<int64_t>((int64_t)m->local_tiles(), 1));
   const CUtensorMap mapW = tile_map(m->dinv, cb, N * f);
+  // trailing update on the INT8 tensor cores when selected (slices of the
+  // broadcast panel, double buffered like PB)
+  const bool use_oz = c->chol_slices > 0 && N > 1;
+  OzPanel oz;
+  if (use_oz) oz.init(b, N, c->chol_slices);
   const CUtensorMap mapLd = tile_map(Ld, b, 1);
   const CUtensorMap mapWb = tile_map(Wb, cb, f);
   const CUtensorMap mapPB[2] = {tile_map(PB[0], b, panel), tile_map(PB[1], b, panel)};
@@ -1630,6 +1635,7 @@ static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
                       LK_BLOCK);
       }
       comm_group(c, false);
+      if (use_oz) oz.slice_contig(c, cs.p, PB[j & 1], N, j, &flag->status);
     }
   };
 
@@ -1644,13 +1650,22 @@ static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
     gu.mode = G_DIST_UPDATE;
     gu.X = PB[j & 1];
     gu.list = d_pairs + 2 * col_off[j];
-    launch_gemm(c, cs.u, gu, (rest_off[j] - col_off[j]) * f * f, &mapPB[j & 1], &mapPB[j & 1]);
+    if (use_oz)
+      oz.update_list(c, cs.u, m->d, m->d_lpos, j, gu.list, rest_off[j] - col_off[j],
+                     &flag->status);
+    else
+      launch_gemm(c, cs.u, gu, (rest_off[j] - col_off[j]) * f * f, &mapPB[j & 1],
+                  &mapPB[j & 1]);
     cudaEvent_t ucol = cs.make();
     HS_CUDA(cudaEventRecord(ucol, cs.u));
     HS_CUDA(cudaStreamWaitEvent(cs.p, ucol));
     gu.list = d_pairs + 2 * rest_off[j];
-    launch_gemm(c, cs.u, gu, (col_off[j + 1] - rest_off[j]) * f * f, &mapPB[j & 1],
-                &mapPB[j & 1]);
+    if (use_oz)
+      oz.update_list(c, cs.u, m->d, m->d_lpos, j, gu.list, col_off[j + 1] - rest_off[j],
+                     &flag->status);
+    else
+      launch_gemm(c, cs.u, gu, (col_off[j + 1] - rest_off[j]) * f * f, &mapPB[j & 1],
+                  &mapPB[j & 1]);
     panel_work(j + 1);
   }
   cudaEvent_t pend = cs.make(), uend = cs.make();

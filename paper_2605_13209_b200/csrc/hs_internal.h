@@ -183,6 +183,10 @@ struct OzPanel {
              int64_t j, const int32_t* status);
   void update(hs_ctx* c, cudaStream_t st, double* A, int64_t tile_lo, int64_t local_tiles,
               int64_t N, int64_t j, bool col, const int32_t* status);
+  void slice_contig(hs_ctx* c, cudaStream_t st, const double* X, int64_t N, int64_t j,
+                    const int32_t* status);
+  void update_list(hs_ctx* c, cudaStream_t st, double* A, const int64_t* lpos, int64_t j,
+                   const int32_t* pairs, int64_t npairs, const int32_t* status);
 };
 
 }  // namespace hs

@@ -73,7 +73,8 @@ constexpr int32_t NONFINITE = -100000;   // row exponent sentinel (NaN / Inf row
 enum Mode : int {
   BATCH = 0,     // C_t -= P_t Q_t^T over `count` contiguous tile triples
   CHOL_COL = 1,  // Cholesky column j: A_i,j+1 -= L_ij L_j+1,j^T, i > j
-  CHOL_REST = 2  // Cholesky column j: A_ik -= L_ij L_kj^T, j + 2 <= k <= i
+  CHOL_REST = 2,  // Cholesky column j: A_ik -= L_ij L_kj^T, j + 2 <= k <= i
+  CHOL_LIST = 3   // distributed Cholesky column j: the listed owned (i, k)
 };
 
 struct Args {
@@ -85,6 +86,8 @@ struct Args {
   int lower_only;       // BATCH: SYRK-style lower-triangle update
   int64_t count;        // BATCH: number of (C, P, Q) triples
   int64_t j, tile_lo;   // CHOL: column, first local packed tile
+  const int32_t* pairs;  // CHOL_LIST: (i, k) pairs of this launch
+  const int64_t* lpos;   // CHOL_LIST: packed tile -> local slot (2D block-cyclic)
   const int32_t* status;  // optional: non-zero -> skip (factorization failed)
   long long* prof;        // optional phase timestamps (tools/oz_bench.py --phases)
 };
@@ -284,6 +287,9 @@ __device__ __forceinline__ Item decode_item(const Args& g, int64_t item) {
     if (g.mode == CHOL_COL) {
       i = g.j + 1 + u;
       k = g.j + 1;
+    } else if (g.mode == CHOL_LIST) {
+      i = g.pairs[2 * u];
+      k = g.pairs[2 * u + 1];
     } else {
       const int64_t ii = tile_row(u);
       i = g.j + 2 + ii;
@@ -291,7 +297,8 @@ __device__ __forceinline__ Item decode_item(const Args& g, int64_t item) {
     }
     it.a_row = (int)((i - g.j - 1) * g.b + mb * M);
     it.b_row = (int)((k - g.j - 1) * g.b + nb * N);
-    it.c = g.C + (tri(i, k) - g.tile_lo) * bb + (int64_t)mb * M * g.b + nb * N;
+    const int64_t slot = g.mode == CHOL_LIST ? g.lpos[tri(i, k)] : tri(i, k) - g.tile_lo;
+    it.c = g.C + slot * bb + (int64_t)mb * M * g.b + nb * N;
     diag = i == k;
   }
   it.ea = it.a_row;
@@ -619,6 +626,36 @@ void OzPanel::update(hs_ctx* c, cudaStream_t st, double* A, int64_t tile_lo,
   g.status = status;
   (void)local_tiles;
   oz::launch_gemm(c, st, ma, mb, g, tiles * fm * fn);
+}
+
+// Distributed variant: the panel of column j arrives broadcast into a
+// contiguous buffer X (tile i at (i - j - 1) b^2); slice it as is.
+void OzPanel::slice_contig(hs_ctx* c, cudaStream_t st, const double* X, int64_t N, int64_t j,
+                           const int32_t* status) {
+  const int64_t t = N - 1 - j;
+  oz_slice(c, st, X, t, b, s, S[j & 1], E[j & 1], rows, -1, 0, status);
+}
+
+// A_ik -= L_ij L_kj^T for `npairs` owned (i, k) of column j (device list),
+// output tiles at their 2D block-cyclic local slots.
+void OzPanel::update_list(hs_ctx* c, cudaStream_t st, double* A, const int64_t* lpos,
+                          int64_t j, const int32_t* pairs, int64_t npairs,
+                          const int32_t* status) {
+  if (npairs <= 0) return;
+  const int fm = b / oz::M, fn = b / oz::N;
+  const CUtensorMap ma = oz::slice_map(S[j & 1], b, rows, oz::M, s);
+  const CUtensorMap mb = oz::slice_map(S[j & 1], b, rows, oz::N, s);
+  oz::Args g{};
+  g.mode = oz::CHOL_LIST;
+  g.C = A;
+  g.EA = g.EB = E[j & 1];
+  g.b = b;
+  g.s = s;
+  g.j = j;
+  g.pairs = pairs;
+  g.lpos = lpos;
+  g.status = status;
+  oz::launch_gemm(c, st, ma, mb, g, npairs * fm * fn);
 }
 
 }  // namespace hs

@@ -167,3 +167,21 @@ def test_cholesky_emulated_solve_and_not_spd(oracle):
             rt.set_cholesky_gemm(9)
     finally:
         rt.close()
+
+
+@pytest.mark.parametrize("n,b", [(2048, 512), (1536, 128)])
+def test_distributed_cholesky_emulated_world1(oracle, n, b):
+    """The 2D block-cyclic NCCL path with the INT8-emulated update (panel
+    broadcast into the contiguous buffer, sliced there; owned-pair lists)."""
+    rt = hs.Runtime.distributed(0, 0, 1, hs.Runtime.nccl_unique_id())
+    try:
+        rt.set_cholesky_gemm(8)
+        a = oracle.generate_spd(n, b, seed=42)
+        st, L_ref, _, _ = oracle.factorize(n, b, a)
+        m = hs.DeviceMatrix(rt, n, b, cyclic=True).upload(a)
+        H.potrf_device(rt, m)
+        mask = lower_mask(n, b)
+        err = np.abs(m.download()[mask] - L_ref[mask]).max()
+        assert err <= 1e-10 * np.abs(a[mask]).max(), err
+    finally:
+        rt.close()
