@@ -241,6 +241,7 @@ def cholesky_secondary(hs, H, rt, torch, args, peak_tf: float, world: int = 1,
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
                 t = float(tt.item())
             times.append(t)
+        log(f"cholesky rep {rep}: {s.elapsed_time(e):.1f} ms")
     launches = (rt.kernel_launches() - launches0) // (1 + args.chol_reps)
     ms = statistics.median(times)
     gflops = n ** 3 / 3 / (ms * 1e-3) / 1e9
@@ -256,6 +257,32 @@ def cholesky_secondary(hs, H, rt, torch, args, peak_tf: float, world: int = 1,
                         "frac": gflops / 1e3 / world / peak_tf,
                         "peak_source": "cuBLAS DGEMM 8192^3 measured live in this run "
                                        "(MEASURED_PEAKS.json has no FP64 entry)"}}
+    if cyclic and args.chol_slices > 0:
+        # 2D block-cyclic factorization with the INT8-emulated update (time only)
+        rt.set_cholesky_gemm(args.chol_slices)
+        et = []
+        for rep in range(1 + args.chol_reps):
+            work.copy_from(m)
+            torch.cuda.synchronize()
+            dist.barrier()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            H.potrf_device(rt, work)
+            e.record()
+            e.synchronize()
+            if rep > 0:
+                tt = torch.tensor([s.elapsed_time(e)], dtype=torch.float64, device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                et.append(float(tt.item()))
+        rt.set_cholesky_gemm(0)
+        ems = statistics.median(et)
+        eg = n ** 3 / 3 / (ems * 1e-3) / 1e9
+        out["emulated_fp64"] = {
+            "value": eg, "unit": "GFLOP/s", "ms_per_factor": ems, "speedup_vs_dmma": ms / ems,
+            "engine": f"trailing update on the INT8 tensor cores, {args.chol_slices} slices",
+            "roofline": {"bound": "tensor", "achieved": eg / 1e3 / world, "peak": peak_tf,
+                         "unit": "TFLOP/s per GPU (FP64-equivalent) vs DGEMM",
+                         "frac": eg / 1e3 / world / peak_tf}}
     if not cyclic and args.chol_slices > 0:
         # the same factorization with the trailing update on the INT8 tensor
         # cores (emulated FP64, Ozaki slicing); L compared with the DMMA L

@@ -22,11 +22,14 @@ def main():
     ap.add_argument("--n", type=int, default=32768)
     ap.add_argument("--b", type=int, default=128)
     ap.add_argument("--iters", type=int, default=6)
+    ap.add_argument("--dist", action="store_true",
+                    help="world-1 NCCL context, 2D block-cyclic Cholesky path")
     ap.add_argument("--slices", type=int, default=0,
                     help="Cholesky trailing update on the INT8 tensor cores (0: DMMA)")
     a = ap.parse_args()
-    rt = hs.Runtime()
-    m = hs.generate_spd_device(rt, a.n, a.b, seed=42)
+    rt = (hs.Runtime.distributed(0, 0, 1, hs.Runtime.nccl_unique_id()) if a.dist
+          else hs.Runtime())
+    m = hs.generate_spd_device(rt, a.n, a.b, seed=42, cyclic=a.dist and a.what == "chol")
     if a.what == "cg":
         rhs = torch.from_numpy(hs.generate_rhs(a.n, a.b, 42).values).cuda()
         x = torch.zeros_like(rhs)
