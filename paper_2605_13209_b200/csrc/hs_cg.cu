@@ -769,13 +769,8 @@ template <int B, int NCW>
 static void launch_symv_fast(hs_ctx* c, const hs_matrix* m, const double* s,
                              const int32_t* done, const SymvFuse* fz) {
   using Cfg = SymvCfg<B, NCW>;
-  static bool attr = false;
-  if (!attr) {
-    HS_CUDA(cudaFuncSetAttribute(symv_slab_kernel<B, NCW>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Cfg::SMEM));
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  HS_CUDA(smem_attr_once(symv_slab_kernel<B, NCW>, Cfg::SMEM, attr));
   SymvPlan* p = m->plan;
   SymvArgs a{m->d,        s,           m->d_row_off, m->tile_lo, p->cta_slab,
              p->cta_rseg, p->rowpart, p->colmain,   p->colextra, done,

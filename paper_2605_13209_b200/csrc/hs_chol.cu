@@ -1195,13 +1195,8 @@ static void launch_gemm(hs_ctx* c, cudaStream_t s, const GemmArgs& g,
                         const CUtensorMap* mb) {
   if (items <= 0) return;
   if (g.cb == 128 && ma && mb) {
-    static bool attr = false;
-    if (!attr) {
-      HS_CUDA(cudaFuncSetAttribute(gemm_dmma_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   G_SMEM));
-      attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};
+    HS_CUDA(smem_attr_once(gemm_dmma_kernel, G_SMEM, attr));
     gemm_dmma_kernel<<<(unsigned)items, 288, G_SMEM, s>>>(*ma, *mb, g);
   } else {
     const int tpd = (g.cb + 63) / 64;

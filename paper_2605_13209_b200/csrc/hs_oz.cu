@@ -514,12 +514,8 @@ template <int S>
 static void launch_gemm_s(hs_ctx* c, cudaStream_t st, const CUtensorMap& ma,
                           const CUtensorMap& mb, const Args& g,
                           int64_t items) {
-  static bool attr = false;
-  if (!attr) {
-    HS_CUDA(cudaFuncSetAttribute(gemm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 SMEM));
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  HS_CUDA(smem_attr_once(gemm_kernel<S>, SMEM, attr));
   // Bounded persistence: each CTA walks ~ipc items (strided by the grid, so
   // co-resident CTAs work on neighbouring items), then retires. A CTA that
   // owned its SM for the whole update would lock the Cholesky's
