@@ -183,3 +183,14 @@ def test_config_file_defaults_and_override(tmp_path):
     assert code == 0, err
     _, _, rows = csv_rows(out)
     assert rows[0]["n"] == "96" and rows[0]["fraction"] == "0.25"
+
+
+@pytest.mark.gpu
+def test_solve_cholesky_with_int8_emulation(tmp_path):
+    out = str(tmp_path / "o.csv")
+    code, _, err = run("solve", "cholesky", "--size", "1024", "--block-size", "128",
+                       "--reps", "1", "--fp64-emulation-slices", "8", "--output", out)
+    assert code == 0, err
+    _, _, rows = csv_rows(out)
+    assert rows[0]["status"] == "ok" and float(rows[0]["true_residual"]) < 1e-9
+    assert run("solve", "cholesky", "--size", "64", "--fp64-emulation-slices", "9")[0] == 2
