@@ -1,0 +1,111 @@
+"""Full BASELINE.json sizes on one B200, checked through size-independent
+properties (no CPU oracle finishes at these sizes):
+
+* cfg2 CG n=32768, b=128: converges to eps = 1e-6 with the true residual
+  within the reference bound 2 eps sqrt(u0) (test_cg_solver.cpp:76-91),
+  in a comparable iteration count (45 on the CPU, 39 here), and
+  agrees with the Cholesky solution of the same system;
+* SYMV symmetry s^T (A t) = t^T (A s) and linearity A(s + t) = As + At;
+* cfg3 Cholesky n=32768, b=512: relative residual <= 1e-10 (reference
+  test_cholesky_solver.cpp:255-269), DMMA and INT8-emulated, factors
+  within 1e-11 of each other;
+* n=131072 (cfg4/5 sizes, 68.8 GB): CG converges with the reference bound;
+  the INT8-emulated Cholesky solves to 1e-10.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2605_13209_b200 as hs
+from paper_2605_13209_b200 import hsolve as H
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(v):
+    return torch.from_numpy(np.ascontiguousarray(v)).cuda()
+
+
+def cg_solve(rt, m, n, b, eps=1e-6):
+    rhs = dev(hs.generate_rhs(n, b, 42).values)
+    x = torch.zeros_like(rhs)
+    st = hs.solve_cg_device(rt, m, rhs.data_ptr(), x.data_ptr(),
+                            hs.SolverConfig(block_size=b, eps=eps))
+    return st, x, rhs
+
+
+def test_cfg2_cg_full_size(rt):
+    n, b = 32768, 128
+    m = hs.generate_spd_device(rt, n, b, seed=42)
+    st, x, rhs = cg_solve(rt, m, n, b)
+    assert st.converged
+    # the reference CPU run takes 45; the count is rounding-order sensitive
+    # (the trace is chaotic), measured 39 here (FMA SYMV)
+    assert 30 <= st.iterations <= 60, st.iterations
+    assert st.true_residual <= 2e-6 * np.sqrt(st.u0)
+    # SYMV symmetry and linearity (fixed-order, deterministic kernels)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    s = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    t = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    As, At, Ast = torch.empty_like(s), torch.empty_like(s), torch.empty_like(s)
+    H.symv_device(rt, m, s.data_ptr(), As.data_ptr())
+    H.symv_device(rt, m, t.data_ptr(), At.data_ptr())
+    st_sum = s + t
+    H.symv_device(rt, m, st_sum.data_ptr(), Ast.data_ptr())
+    scale = float(torch.linalg.vector_norm(As)) + float(torch.linalg.vector_norm(At))
+    assert float(torch.linalg.vector_norm(Ast - As - At)) <= 1e-12 * scale
+    lhs, rhs_s = float(torch.dot(s, At)), float(torch.dot(t, As))
+    assert abs(lhs - rhs_s) <= 1e-12 * (abs(lhs) + float(torch.linalg.vector_norm(s)) *
+                                         float(torch.linalg.vector_norm(At)))
+    # CG x vs the Cholesky x of the same system (<= 1e-4)
+    w = hs.DeviceMatrix(rt, n, b).copy_from(m)
+    y = torch.empty_like(rhs)
+    sp = hs.solve_spd_device(rt, w, rhs.data_ptr(), y.data_ptr(), a_orig=m)
+    assert sp.true_residual <= 1e-10 * float(torch.linalg.vector_norm(rhs))
+    rel = float(torch.linalg.vector_norm(x - y) / torch.linalg.vector_norm(y))
+    assert rel <= 1e-4, rel
+    w.free()
+    m.free()
+
+
+def test_cfg3_cholesky_full_size_dmma_and_emulated(rt):
+    n, b = 32768, 512
+    m = hs.generate_spd_device(rt, n, b, seed=42)
+    rhs = dev(hs.generate_rhs(n, b, 42).values)
+    nb = float(torch.linalg.vector_norm(rhs))
+    factors = []
+    for slices in (0, 8):
+        rt.set_cholesky_gemm(slices)
+        w = hs.DeviceMatrix(rt, n, b).copy_from(m)
+        x = torch.empty_like(rhs)
+        sp = hs.solve_spd_device(rt, w, rhs.data_ptr(), x.data_ptr(), a_orig=m)
+        assert sp.true_residual <= 1e-10 * nb, (slices, sp.true_residual / nb)
+        factors.append(torch.from_numpy(w.download()).cuda())
+        w.free()
+    rt.set_cholesky_gemm(0)
+    d = float((factors[0] - factors[1]).abs().max() / factors[0].abs().max())
+    assert d <= 1e-11, d
+    m.free()
+
+
+def test_n131072_cg_and_emulated_cholesky(rt):
+    n = 131072
+    m = hs.generate_spd_device(rt, n, 128, seed=42)
+    st, x, rhs = cg_solve(rt, m, n, 128)
+    assert st.converged and st.true_residual <= 2e-6 * np.sqrt(st.u0)
+    m.free()
+    del x, rhs
+    torch.cuda.empty_cache()
+    b = 512
+    m = hs.generate_spd_device(rt, n, b, seed=42)
+    w = hs.DeviceMatrix(rt, n, b).copy_from(m)
+    rhs = dev(hs.generate_rhs(n, b, 42).values)
+    x = torch.empty_like(rhs)
+    rt.set_cholesky_gemm(8)
+    try:
+        sp = hs.solve_spd_device(rt, w, rhs.data_ptr(), x.data_ptr(), a_orig=m)
+    finally:
+        rt.set_cholesky_gemm(0)
+    assert sp.true_residual <= 1e-10 * float(torch.linalg.vector_norm(rhs))
+    w.free()
+    m.free()
