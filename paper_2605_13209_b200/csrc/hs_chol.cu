@@ -753,35 +753,36 @@ __global__ void __launch_bounds__(256)
     for (int p = 0; p < DCB / DPB; ++p) {
       const int o = p * DPB;
       if (warp == 0) {
-        // right-looking 32x32 factor in smem, lane r owns row r; fixed-bound
-        // predicated inner loop (no register arrays -> no local memory)
+        // right-looking 32x32 factor, lane r owns row r IN REGISTERS (fully
+        // unrolled: static indices); step k broadcasts the pivot and column
+        // k by shuffle, the 31 - k row updates of a step are independent
         double* Dp = S + o * DLD + o;
-        int failed = -1;
-        for (int k = 0; k < DPB; ++k) {
-          const double akk = Dp[k * DLD + k];
-          if (!(akk > 0.0)) {
-            failed = k;
-            break;
-          }
-          const double rinv = rsqrt(akk);
-          const double lrk = lane > k ? Dp[lane * DLD + k] * rinv : 0.0;
-          __syncwarp();
-          if (lane == k) Dp[k * DLD + k] = akk * rinv;
-          if (lane > k) Dp[lane * DLD + k] = lrk;
-          __syncwarp();
-// column k of L comes from the owning lanes by shuffle; only this lane's
-          // own row is touched in smem, so loads / stores pipeline
-          double* myrow = Dp + lane * DLD;
+        double a[DPB];
 #pragma unroll
-          for (int c = 1; c < DPB; ++c) {
+        for (int c = 0; c < DPB; ++c) a[c] = c <= lane ? Dp[lane * DLD + c] : 0.0;
+        int failed = -1;
+#pragma unroll
+        for (int k = 0; k < DPB; ++k) {
+          const double akk = __shfl_sync(0xffffffffu, a[k], k);
+          // uniform (every lane holds lane k's pivot); no `break`, so the
+          // loop unrolls fully and a[] stays in registers
+          if (failed < 0 && !(akk > 0.0)) failed = k;
+          const double rinv = rsqrt(akk);
+          const double lrk = lane > k ? a[k] * rinv : 0.0;
+          if (lane == k) a[k] = akk * rinv;
+          if (lane > k) a[k] = lrk;
+#pragma unroll
+          for (int c = 1; c < DPB; ++c) {  // fixed bounds: unrolls with k
             const double lck = __shfl_sync(0xffffffffu, lrk, c);
-            if (c > k && c <= lane) myrow[c] = fma(-lrk, lck, myrow[c]);
+            if (c > k && lane >= c) a[c] = fma(-lrk, lck, a[c]);
           }
-          __syncwarp();
         }
         if (failed >= 0) {
           if (lane == 0) bad = o + failed;
         } else {
+#pragma unroll
+          for (int c = 0; c < DPB; ++c)
+            if (c <= lane) Dp[lane * DLD + c] = a[c];
           Rv[lane] = 1.0 / Dp[lane * DLD + lane];  // reciprocal diagonal
         }
       }
@@ -882,23 +883,25 @@ __global__ void __launch_bounds__(256)
         for (int y = 0; y < 4; ++y) Tm[(r0 + x) * (DPB + 1) + c0 + y] = acc[x][y];
     }
     HS_PHASE("inv_T");
-    // (2) lane c inverts column c of the 32x32 diagonal block (registers)
+    // (2) lane c inverts column c of the 32x32 diagonal block, right-looking
+    //     (w_k = (delta_kc - acc_k) / L_kk, then acc_r += L_rk w_k for r > k:
+    //     the 31 - k updates of a step are independent); w_k overwrites
+    //     L[k][c] (c <= k), which no later step reads
     if (warp == 0) {
       Rv[lane] = 1.0 / S[(o + lane) * DLD + o + lane];
       __syncwarp();
-      double w[DPB];
+      double acc[DPB];
 #pragma unroll
-      for (int r = 0; r < DPB; ++r) {
-        double acc = (r == lane) ? 1.0 : 0.0;
+      for (int r = 0; r < DPB; ++r) acc[r] = 0.0;
 #pragma unroll
-        for (int k = 0; k < r; ++k)
-          if (k >= lane) acc = fma(-S[(o + r) * DLD + o + k], w[k], acc);
-        w[r] = r >= lane ? acc * Rv[r] : 0.0;
+      for (int k = 0; k < DPB; ++k) {
+        const double wk = k >= lane ? ((k == lane ? 1.0 : 0.0) - acc[k]) * Rv[k] : 0.0;
+#pragma unroll
+        for (int r = k + 1; r < DPB; ++r)
+          acc[r] = fma(S[(o + r) * DLD + o + k], wk, acc[r]);
+        __syncwarp();
+        if (k >= lane) S[(o + k) * DLD + o + lane] = wk;
       }
-      __syncwarp();
-#pragma unroll
-      for (int r = 0; r < DPB; ++r)
-        if (r >= lane) S[(o + r) * DLD + o + lane] = w[r];
     }
     __syncthreads();
     HS_PHASE("inv_diag");
