@@ -311,9 +311,9 @@ __device__ __forceinline__ Item decode_item(const Args& g, int64_t item) {
 
 // Persistent, warp-specialized: each CTA walks items blockIdx.x,
 // blockIdx.x + gridDim.x, ...; the smem ring runs ahead across items, and the
-// epilogue of item i (TMEM -> registers -> smem -> bulk reduce-add) overlaps
-// the loads of item i + 1 -- the accumulators are released as soon as they
-// are read, before the FP64 combine and the global update.
+// epilogue of item i (TMEM -> registers -> FP64 read-modify-write of C)
+// overlaps the loads and MMAs of item i + 1 -- the accumulators are released
+// as soon as they are read, before the FP64 work and the global update.
 template <int S>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap mapA,
