@@ -753,36 +753,35 @@ __global__ void __launch_bounds__(256)
     for (int p = 0; p < DCB / DPB; ++p) {
       const int o = p * DPB;
       if (warp == 0) {
-        // right-looking 32x32 factor, lane r owns row r IN REGISTERS (fully
-        // unrolled: static indices); step k broadcasts the pivot and column
-        // k by shuffle, the 31 - k row updates of a step are independent
+        // right-looking 32x32 factor in smem, lane r owns row r; fixed-bound
+        // predicated inner loop (no register arrays -> no local memory)
         double* Dp = S + o * DLD + o;
-        double a[DPB];
-#pragma unroll
-        for (int c = 0; c < DPB; ++c) a[c] = c <= lane ? Dp[lane * DLD + c] : 0.0;
         int failed = -1;
-#pragma unroll
         for (int k = 0; k < DPB; ++k) {
-          const double akk = __shfl_sync(0xffffffffu, a[k], k);
-          // uniform (every lane holds lane k's pivot); no `break`, so the
-          // loop unrolls fully and a[] stays in registers
-          if (failed < 0 && !(akk > 0.0)) failed = k;
-          const double rinv = rsqrt(akk);
-          const double lrk = lane > k ? a[k] * rinv : 0.0;
-          if (lane == k) a[k] = akk * rinv;
-          if (lane > k) a[k] = lrk;
-#pragma unroll
-          for (int c = 1; c < DPB; ++c) {  // fixed bounds: unrolls with k
-            const double lck = __shfl_sync(0xffffffffu, lrk, c);
-            if (c > k && lane >= c) a[c] = fma(-lrk, lck, a[c]);
+          const double akk = Dp[k * DLD + k];
+          if (!(akk > 0.0)) {
+            failed = k;
+            break;
           }
+          const double rinv = rsqrt(akk);
+          const double lrk = lane > k ? Dp[lane * DLD + k] * rinv : 0.0;
+          __syncwarp();
+          if (lane == k) Dp[k * DLD + k] = akk * rinv;
+          if (lane > k) Dp[lane * DLD + k] = lrk;
+          __syncwarp();
+// column k of L comes from the owning lanes by shuffle; only this lane's
+          // own row is touched in smem, so loads / stores pipeline
+          double* myrow = Dp + lane * DLD;
+#pragma unroll
+          for (int c = 1; c < DPB; ++c) {
+            const double lck = __shfl_sync(0xffffffffu, lrk, c);
+            if (c > k && c <= lane) myrow[c] = fma(-lrk, lck, myrow[c]);
+          }
+          __syncwarp();
         }
         if (failed >= 0) {
           if (lane == 0) bad = o + failed;
         } else {
-#pragma unroll
-          for (int c = 0; c < DPB; ++c)
-            if (c <= lane) Dp[lane * DLD + c] = a[c];
           Rv[lane] = 1.0 / Dp[lane * DLD + lane];  // reciprocal diagonal
         }
       }
@@ -883,25 +882,23 @@ __global__ void __launch_bounds__(256)
         for (int y = 0; y < 4; ++y) Tm[(r0 + x) * (DPB + 1) + c0 + y] = acc[x][y];
     }
     HS_PHASE("inv_T");
-    // (2) lane c inverts column c of the 32x32 diagonal block, right-looking
-    //     (w_k = (delta_kc - acc_k) / L_kk, then acc_r += L_rk w_k for r > k:
-    //     the 31 - k updates of a step are independent); w_k overwrites
-    //     L[k][c] (c <= k), which no later step reads
+    // (2) lane c inverts column c of the 32x32 diagonal block (registers)
     if (warp == 0) {
       Rv[lane] = 1.0 / S[(o + lane) * DLD + o + lane];
       __syncwarp();
-      double acc[DPB];
+      double w[DPB];
 #pragma unroll
-      for (int r = 0; r < DPB; ++r) acc[r] = 0.0;
+      for (int r = 0; r < DPB; ++r) {
+        double acc = (r == lane) ? 1.0 : 0.0;
 #pragma unroll
-      for (int k = 0; k < DPB; ++k) {
-        const double wk = k >= lane ? ((k == lane ? 1.0 : 0.0) - acc[k]) * Rv[k] : 0.0;
-#pragma unroll
-        for (int r = k + 1; r < DPB; ++r)
-          acc[r] = fma(S[(o + r) * DLD + o + k], wk, acc[r]);
-        __syncwarp();
-        if (k >= lane) S[(o + k) * DLD + o + lane] = wk;
+        for (int k = 0; k < r; ++k)
+          if (k >= lane) acc = fma(-S[(o + r) * DLD + o + k], w[k], acc);
+        w[r] = r >= lane ? acc * Rv[r] : 0.0;
       }
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < DPB; ++r)
+        if (r >= lane) S[(o + r) * DLD + o + lane] = w[r];
     }
     __syncthreads();
     HS_PHASE("inv_diag");
@@ -1238,12 +1235,13 @@ static void set_simt_tile_attrs(int b) {
 }
 
 struct ColStreams {
-  cudaStream_t p = nullptr, u = nullptr;
+  cudaStream_t p = nullptr, u = nullptr, u2 = nullptr;
   std::vector<cudaEvent_t> ev;
   ~ColStreams() {
     for (auto e : ev) cudaEventDestroy(e);
     if (p) cudaStreamDestroy(p);
     if (u) cudaStreamDestroy(u);
+    if (u2) cudaStreamDestroy(u2);
   }
   cudaEvent_t make() {
     cudaEvent_t e;
@@ -1339,7 +1337,7 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
   // trailing update on the INT8 tensor cores (emulated FP64) when selected
   const bool use_oz = fast && c->chol_slices > 0 && N > 1;
   OzPanel oz;
-  if (use_oz) oz.init(b, N, c->chol_slices);
+  if (use_oz) oz.init(b, N, c->chol_slices, /*pairs=*/true);
 
   GemmArgs g{};
   g.N = N;
@@ -1382,7 +1380,9 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
         gp.mode = G_PANEL_TRSM;
         launch_gemm(c, cs.p, gp, t * f, &mapA, &mapW);
       }
-      if (use_oz && t > 0) oz.slice(c, cs.p, m->d, m->tile_lo, N, j, &flag->status);
+      // single-column slices feed the even column's lookahead update
+      if (use_oz && t > 0 && j % 2 == 0)
+        oz.slice(c, cs.p, m->d, m->tile_lo, N, j, &flag->status);
       return;
     }
     // SIMT path (b % 128 != 0): single-CTA tile kernels, panel via buffer
@@ -1408,7 +1408,58 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
   };
 
   panel_work(0);
-  for (int64_t j = 0; j < N; ++j) {
+  if (use_oz) {
+    // INT8 path, columns in pairs (j0, j1 = j0 + 1): the trailing update of a
+    // pair runs as ONE K = 2b update, [L_i,j0 L_i,j1] [L_k,j0 L_k,j1]^T, which
+    // halves the epilogue passes over C (the K = b kernel is epilogue-bound:
+    // 61 -> 83 TF/s at K = 2b). Schedule (P: panel stream, U: lookahead
+    // updates, U2: the bulk "rest" update):
+    //   U : tile column j1 by column j0 alone (K = b)    -> P: panel j1,
+    //       joint slices of (j0, j1)
+    //   U : tile column j1+1 by the pair                 -> P: panel j1+1 (next j0)
+    //   U : tile column j1+2 by the pair
+    //   U2: tile columns >= j1+3 by the pair, overlapping the next pair's
+    //       panels and lookahead; the next pair's U work waits for it
+    HS_CUDA(cudaStreamCreateWithPriority(&cs.u2, cudaStreamNonBlocking, lo_pri));
+    HS_CUDA(cudaStreamWaitEvent(cs.u2, start));
+    cudaEvent_t rest_done = nullptr;
+    for (int64_t j0 = 0; j0 < N; j0 += 2) {
+      const int64_t j1 = j0 + 1;
+      if (j1 >= N) break;
+      cudaEvent_t p0 = cs.make();
+      HS_CUDA(cudaEventRecord(p0, cs.p));
+      HS_CUDA(cudaStreamWaitEvent(cs.u, p0));
+      oz.update(c, cs.u, m->d, m->tile_lo, (int64_t)m->local_tiles(), N, j0, true,
+                &flag->status);
+      cudaEvent_t ucol = cs.make();
+      HS_CUDA(cudaEventRecord(ucol, cs.u));
+      HS_CUDA(cudaStreamWaitEvent(cs.p, ucol));
+      panel_work(j1);
+      if (j1 + 1 >= N) break;
+      oz.slice_pair(c, cs.p, m->d, m->tile_lo, N, j0, &flag->status);
+      cudaEvent_t p1 = cs.make();
+      HS_CUDA(cudaEventRecord(p1, cs.p));
+      HS_CUDA(cudaStreamWaitEvent(cs.u, p1));
+      if (rest_done) HS_CUDA(cudaStreamWaitEvent(cs.u, rest_done));
+      oz.update_pair(c, cs.u, m->d, m->tile_lo, N, j0, true, j1 + 1, &flag->status);
+      cudaEvent_t ua = cs.make();
+      HS_CUDA(cudaEventRecord(ua, cs.u));
+      if (j1 + 2 < N) {
+        oz.update_pair(c, cs.u, m->d, m->tile_lo, N, j0, true, j1 + 2, &flag->status);
+        cudaEvent_t ub = cs.make();
+        HS_CUDA(cudaEventRecord(ub, cs.u));
+        if (j1 + 3 < N) {
+          HS_CUDA(cudaStreamWaitEvent(cs.u2, ub));
+          oz.update_pair(c, cs.u2, m->d, m->tile_lo, N, j0, false, j1 + 3, &flag->status);
+          rest_done = cs.make();
+          HS_CUDA(cudaEventRecord(rest_done, cs.u2));
+        }
+      }
+      HS_CUDA(cudaStreamWaitEvent(cs.p, ua));
+      panel_work(j1 + 1);
+    }
+  }
+  for (int64_t j = 0; j < N && !use_oz; ++j) {
     const int64_t t = N - 1 - j;
     cudaEvent_t pdone = cs.make();
     HS_CUDA(cudaEventRecord(pdone, cs.p));
@@ -1420,11 +1471,7 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
     const CUtensorMap* mx = fast ? &mapA : nullptr;
     // lookahead: tile column j+1 first
     gu.mode = G_UPDATE_COL;
-    if (use_oz)
-      oz.update(c, cs.u, m->d, m->tile_lo, (int64_t)m->local_tiles(), N, j, true,
-                &flag->status);
-    else
-      launch_gemm(c, cs.u, gu, t * f * f, mx, mx);
+    launch_gemm(c, cs.u, gu, t * f * f, mx, mx);
     cudaEvent_t ucol = cs.make();
     HS_CUDA(cudaEventRecord(ucol, cs.u));
     HS_CUDA(cudaStreamWaitEvent(cs.p, ucol));
@@ -1432,11 +1479,7 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
     // panel touches only tile column j+1; the update reads column j)
     gu.mode = G_UPDATE_REST;
     const int64_t tr = t - 1;
-    if (use_oz)
-      oz.update(c, cs.u, m->d, m->tile_lo, (int64_t)m->local_tiles(), N, j, false,
-                &flag->status);
-    else
-      launch_gemm(c, cs.u, gu, tr * (tr + 1) / 2 * f * f, mx, mx);
+    launch_gemm(c, cs.u, gu, tr * (tr + 1) / 2 * f * f, mx, mx);
     panel_work(j + 1);
   }
   cudaEvent_t pend = cs.make(), uend = cs.make();
@@ -1444,6 +1487,11 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
   HS_CUDA(cudaEventRecord(uend, cs.u));
   HS_CUDA(cudaStreamWaitEvent(c->stream, pend));
   HS_CUDA(cudaStreamWaitEvent(c->stream, uend));
+  if (cs.u2) {
+    cudaEvent_t u2end = cs.make();
+    HS_CUDA(cudaEventRecord(u2end, cs.u2));
+    HS_CUDA(cudaStreamWaitEvent(c->stream, u2end));
+  }
   check_finite_kernel<<<4 * 148, 256, 0, c->stream>>>(
       m->d, m->tile_lo, nullptr, (int64_t)m->local_tiles(), b, flag);
   HS_CUDA(cudaGetLastError());

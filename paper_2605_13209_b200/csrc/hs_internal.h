@@ -169,20 +169,26 @@ CUtensorMap make_tensor_map(CUtensorMapDataType type, const void* base, int rank
                             const cuuint32_t* box, CUtensorMapSwizzle swizzle);
 
 // Emulated-FP64 (Ozaki, INT8 tensor core) trailing update of the Cholesky
-// factorization (hs_oz.cu): int8 slices of the current panel, double
-// buffered by column parity so column j+1's slicing overlaps column j's
-// update.
+// factorization (hs_oz.cu): int8 slices of a column's panel (single, K = b)
+// or of a column pair's joint panel (K = 2b, one exponent per row), each
+// double buffered so the next slicing overlaps the current update.
 struct OzPanel {
   int b = 0, s = 0;
   int64_t rows = 0;                       // panel rows per buffer ((N-1) b)
-  int8_t* S[2] = {nullptr, nullptr};     // [slice][row][K] planes
+  int8_t* S[2] = {nullptr, nullptr};     // [slice][row][K] planes, single column
   int32_t* E[2] = {nullptr, nullptr};    // row exponents
+  int8_t* SJ[2] = {nullptr, nullptr};    // column pairs: K = 2b, joint exponents
+  int32_t* EJ[2] = {nullptr, nullptr};
   ~OzPanel();
-  void init(int b, int64_t N, int s);
+  void init(int b, int64_t N, int s, bool pairs = false);
   void slice(hs_ctx* c, cudaStream_t st, const double* A, int64_t tile_lo, int64_t N,
              int64_t j, const int32_t* status);
   void update(hs_ctx* c, cudaStream_t st, double* A, int64_t tile_lo, int64_t local_tiles,
               int64_t N, int64_t j, bool col, const int32_t* status);
+  void slice_pair(hs_ctx* c, cudaStream_t st, const double* A, int64_t tile_lo, int64_t N,
+                  int64_t j0, const int32_t* status);
+  void update_pair(hs_ctx* c, cudaStream_t st, double* A, int64_t tile_lo, int64_t N,
+                   int64_t j0, bool col, int64_t kk, const int32_t* status);
   void slice_contig(hs_ctx* c, cudaStream_t st, const double* X, int64_t N, int64_t j,
                     const int32_t* status);
   void update_list(hs_ctx* c, cudaStream_t st, double* A, const int64_t* lpos, int64_t j,

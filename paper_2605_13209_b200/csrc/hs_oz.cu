@@ -83,9 +83,11 @@ struct Args {
   const int32_t* EA;    // row exponents of the A operand rows
   const int32_t* EB;    // row exponents of the B operand rows
   int b, s;
+  int K;                // operand width (K) per slice row: b, or 2b for column pairs
   int lower_only;       // BATCH: SYRK-style lower-triangle update
   int64_t count;        // BATCH: number of (C, P, Q) triples
-  int64_t j, tile_lo;   // CHOL: column, first local packed tile
+  int64_t j, tile_lo;   // CHOL: panel-row origin (rows of tile i at (i-j-1) b), first local tile
+  int64_t kk;           // CHOL_COL: the tile column; CHOL_REST: first tile column
   const int32_t* pairs;  // CHOL_LIST: (i, k) pairs of this launch
   const int64_t* lpos;   // CHOL_LIST: packed tile -> local slot (2D block-cyclic)
   const int32_t* status;  // optional: non-zero -> skip (factorization failed)
@@ -105,24 +107,37 @@ __device__ __forceinline__ void prof_stamp(long long* prof, int64_t lt, int k) {
 // slicing: one warp per operand row; lane handles 4 consecutive elements
 // per step so every int8 slice row is written with 32-bit stores.
 
-// col >= 0: the operand rows are the panel tiles (i, col), i > col, of a
-// packed matrix (tile t of the panel = packed tile tri(col + 1 + t, col) -
-// tile_lo); col < 0: `rows` contiguous rows of X.
+// Operand rows (K = b, or 2b for a column pair) of `rows` rows:
+//   colA < 0: contiguous rows of X (K = b);
+//   colA >= 0: row r of panel tile t is row r of packed tile (jb + 1 + t, colA)
+//   (tile index tri(i, col) - tile_lo), followed, when colB >= 0, by row r of
+//   tile (jb + 1 + t, colB): the concatenated operand of a two-column update.
+// Output: exponent E[row] and S[p][row][K] for p < s (plane = plane_rows K).
 __global__ void __launch_bounds__(256)
     slice_kernel(const double* __restrict__ X, int64_t rows, int b, int s,
                  int8_t* __restrict__ S, int32_t* __restrict__ E, int64_t plane_rows,
-                 int64_t col, int64_t tile_lo, const int32_t* status) {
+                 int64_t colA, int64_t colB, int64_t jb, int64_t tile_lo,
+                 const int32_t* status) {
   if (status && *status) return;
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
   const int64_t t = row / b, r = row % b;
-  const double* x = col < 0 ? X + row * (int64_t)b
-                            : X + ((tri(col + 1 + t, col) - tile_lo) * b + r) * (int64_t)b;
+  const int K = colB >= 0 ? 2 * b : b;
+  const double* seg0;
+  const double* seg1 = nullptr;
+  if (colA < 0) {
+    seg0 = X + row * (int64_t)b;
+  } else {
+    const int64_t i = jb + 1 + t;
+    seg0 = X + ((tri(i, colA) - tile_lo) * b + r) * (int64_t)b;
+    if (colB >= 0) seg1 = X + ((tri(i, colB) - tile_lo) * b + r) * (int64_t)b;
+  }
+  auto at = [&](int c) { return c < b ? seg0[c] : seg1[c - b]; };
   double mx = 0.0;
   bool finite = true;
-  for (int c = lane; c < b; c += 32) {
-    const double v = x[c];
+  for (int c = lane; c < K; c += 32) {
+    const double v = at(c);
     finite &= isfinite(v);
     mx = fmax(mx, fabs(v));
   }
@@ -132,15 +147,13 @@ __global__ void __launch_bounds__(256)
   }
   const int e = (mx > 0.0) ? ilogb(mx) + 1 : 0;
   if (lane == 0) E[row] = finite ? e : NONFINITE;
-  (void)t;
-  (void)r;
-  // plane-major: slice p of this row at S + (p * plane_rows + row) * b
-  int8_t* base = S + row * (int64_t)b;
-  const int64_t pstride = plane_rows * (int64_t)b;
-  for (int c0 = lane * 4; c0 < b; c0 += 128) {
+  // plane-major: slice p of this row at S + (p * plane_rows + row) * K
+  int8_t* base = S + row * (int64_t)K;
+  const int64_t pstride = plane_rows * (int64_t)K;
+  for (int c0 = lane * 4; c0 < K; c0 += 128) {
     double rem[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) rem[u] = finite ? ldexp(x[c0 + u], 6 - e) : 0.0;
+    for (int u = 0; u < 4; ++u) rem[u] = finite ? ldexp(at(c0 + u), 6 - e) : 0.0;
     for (int p = 0; p < s; ++p) {
       uint32_t w = 0;
 #pragma unroll
@@ -285,15 +298,15 @@ __device__ __forceinline__ Item decode_item(const Args& g, int64_t item) {
     // block_kernels.cpp:39-57)
     int64_t i, k;
     if (g.mode == CHOL_COL) {
-      i = g.j + 1 + u;
-      k = g.j + 1;
+      i = g.kk + u;
+      k = g.kk;
     } else if (g.mode == CHOL_LIST) {
       i = g.pairs[2 * u];
       k = g.pairs[2 * u + 1];
     } else {
       const int64_t ii = tile_row(u);
-      i = g.j + 2 + ii;
-      k = g.j + 2 + (u - tri(ii, 0));
+      i = g.kk + ii;
+      k = g.kk + (u - tri(ii, 0));
     }
     it.a_row = (int)((i - g.j - 1) * g.b + mb * M);
     it.b_row = (int)((k - g.j - 1) * g.b + nb * N);
@@ -319,7 +332,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap mapA,
                 const __grid_constant__ CUtensorMap mapB, Args g, int64_t items) {
   if (g.status && *g.status) return;
-  const int nk = g.b / KS;
+  const int nk = g.K / KS;
 
   extern __shared__ __align__(1024) unsigned char raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>(
@@ -549,9 +562,9 @@ static void launch_gemm(hs_ctx* c, cudaStream_t st, const CUtensorMap& ma,
 }
 
 // 3-D map over the slice planes [slice][row][K]: box 64 B x box_rows x s.
-static CUtensorMap slice_map(const int8_t* base, int b, int64_t rows, int box_rows, int s) {
-  cuuint64_t dims[3] = {(cuuint64_t)b, (cuuint64_t)std::max<int64_t>(rows, 1), (cuuint64_t)MAXS};
-  cuuint64_t strides[2] = {(cuuint64_t)b, (cuuint64_t)b * std::max<int64_t>(rows, 1)};
+static CUtensorMap slice_map(const int8_t* base, int K, int64_t rows, int box_rows, int s) {
+  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)std::max<int64_t>(rows, 1), (cuuint64_t)MAXS};
+  cuuint64_t strides[2] = {(cuuint64_t)K, (cuuint64_t)K * std::max<int64_t>(rows, 1)};
   cuuint32_t box[3] = {(cuuint32_t)KS, (cuuint32_t)box_rows, (cuuint32_t)s};
   return make_tensor_map(CU_TENSOR_MAP_DATA_TYPE_UINT8, base, 3, dims, strides, box,
                          CU_TENSOR_MAP_SWIZZLE_64B);
@@ -563,13 +576,13 @@ static CUtensorMap slice_map(const int8_t* base, int b, int64_t rows, int box_ro
 // int8 slice planes ([slice][row][K], plane = plane_rows * b bytes), plus
 // per-row exponents.
 void oz_slice(hs_ctx* c, cudaStream_t st, const double* X, int64_t tiles, int b, int s,
-              int8_t* S, int32_t* E, int64_t plane_rows, int64_t col, int64_t tile_lo,
-              const int32_t* status) {
+              int8_t* S, int32_t* E, int64_t plane_rows, int64_t colA, int64_t colB,
+              int64_t jb, int64_t tile_lo, const int32_t* status) {
   const int64_t rows = tiles * b;
   if (rows <= 0) return;
   oz::slice_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(X, rows, b, s, S, E,
-                                                                 plane_rows, col, tile_lo,
-                                                                 status);
+                                                                 plane_rows, colA, colB, jb,
+                                                                 tile_lo, status);
   HS_CUDA(cudaGetLastError());
   launch_count(c);
 }
@@ -580,16 +593,22 @@ OzPanel::~OzPanel() {
   for (int k = 0; k < 2; ++k) {
     cudaFree(S[k]);
     cudaFree(E[k]);
+    cudaFree(SJ[k]);
+    cudaFree(EJ[k]);
   }
 }
 
-void OzPanel::init(int b_, int64_t N_, int s_) {
+void OzPanel::init(int b_, int64_t N_, int s_, bool pairs) {
   b = b_;
   s = s_;
   rows = std::max<int64_t>(N_ - 1, 1) * b;
   for (int k = 0; k < 2; ++k) {
     HS_CUDA(cudaMalloc(&S[k], (size_t)rows * b * oz::MAXS));
     HS_CUDA(cudaMalloc(&E[k], (size_t)rows * sizeof(int32_t)));
+    if (pairs) {
+      HS_CUDA(cudaMalloc(&SJ[k], (size_t)rows * 2 * b * oz::MAXS));
+      HS_CUDA(cudaMalloc(&EJ[k], (size_t)rows * sizeof(int32_t)));
+    }
   }
 }
 
@@ -597,7 +616,39 @@ void OzPanel::init(int b_, int64_t N_, int s_) {
 void OzPanel::slice(hs_ctx* c, cudaStream_t st, const double* A, int64_t tile_lo, int64_t N,
                     int64_t j, const int32_t* status) {
   const int64_t t = N - 1 - j;
-  oz_slice(c, st, A, t, b, s, S[j & 1], E[j & 1], rows, j, tile_lo, status);
+  oz_slice(c, st, A, t, b, s, S[j & 1], E[j & 1], rows, j, -1, j, tile_lo, status);
+}
+
+// Joint slices of the column pair (j0, j0 + 1): operand rows
+// [L_i,j0 | L_i,j0+1] (K = 2b, one exponent per row) of the tiles
+// i >= j0 + 2, into pair buffer (j0 / 2) & 1.
+void OzPanel::slice_pair(hs_ctx* c, cudaStream_t st, const double* A, int64_t tile_lo,
+                         int64_t N, int64_t j0, const int32_t* status) {
+  const int64_t t = N - 2 - j0;
+  const int k = (int)((j0 / 2) & 1);
+  oz_slice(c, st, A, t, b, s, SJ[k], EJ[k], rows, j0, j0 + 1, j0 + 1, tile_lo, status);
+}
+
+static void launch_update(hs_ctx* c, cudaStream_t st, const int8_t* S, const int32_t* E,
+                          int b, int K, int s, int64_t rows, double* A, int64_t tile_lo,
+                          int64_t jb, int mode, int64_t kk, int64_t tiles,
+                          const int32_t* status) {
+  if (tiles <= 0) return;
+  const int fm = b / oz::M, fn = b / oz::N;
+  const CUtensorMap ma = oz::slice_map(S, K, rows, oz::M, s);
+  const CUtensorMap mb = oz::slice_map(S, K, rows, oz::N, s);
+  oz::Args g{};
+  g.mode = mode;
+  g.C = A;
+  g.EA = g.EB = E;
+  g.b = b;
+  g.K = K;
+  g.s = s;
+  g.j = jb;
+  g.kk = kk;
+  g.tile_lo = tile_lo;
+  g.status = status;
+  oz::launch_gemm(c, st, ma, mb, g, tiles * fm * fn);
 }
 
 // A_ik -= L_ij L_kj^T for the tiles of column j: `col` selects k == j + 1
@@ -605,23 +656,21 @@ void OzPanel::slice(hs_ctx* c, cudaStream_t st, const double* A, int64_t tile_lo
 void OzPanel::update(hs_ctx* c, cudaStream_t st, double* A, int64_t tile_lo,
                      int64_t local_tiles, int64_t N, int64_t j, bool col,
                      const int32_t* status) {
-  const int64_t t = N - 1 - j;
-  const int64_t tiles = col ? t : (t - 1) * t / 2;
-  if (tiles <= 0) return;
-  const int fm = b / oz::M, fn = b / oz::N;
-  const CUtensorMap ma = oz::slice_map(S[j & 1], b, rows, oz::M, s);
-  const CUtensorMap mb = oz::slice_map(S[j & 1], b, rows, oz::N, s);
-  oz::Args g{};
-  g.mode = col ? oz::CHOL_COL : oz::CHOL_REST;
-  g.C = A;
-  g.EA = g.EB = E[j & 1];
-  g.b = b;
-  g.s = s;
-  g.j = j;
-  g.tile_lo = tile_lo;
-  g.status = status;
   (void)local_tiles;
-  oz::launch_gemm(c, st, ma, mb, g, tiles * fm * fn);
+  const int64_t t = N - 1 - j;
+  launch_update(c, st, S[j & 1], E[j & 1], b, b, s, rows, A, tile_lo, j,
+                col ? oz::CHOL_COL : oz::CHOL_REST, col ? j + 1 : j + 2,
+                col ? t : (t - 1) * t / 2, status);
+}
+
+// A_ik -= [L_i,j0 L_i,j0+1] [L_k,j0 L_k,j0+1]^T (K = 2b): `col` = the single
+// tile column k == kk, else every k >= kk.
+void OzPanel::update_pair(hs_ctx* c, cudaStream_t st, double* A, int64_t tile_lo, int64_t N,
+                          int64_t j0, bool col, int64_t kk, const int32_t* status) {
+  const int64_t t = N - kk;  // tile columns kk .. N-1
+  const int k = (int)((j0 / 2) & 1);
+  launch_update(c, st, SJ[k], EJ[k], b, 2 * b, s, rows, A, tile_lo, j0 + 1,
+                col ? oz::CHOL_COL : oz::CHOL_REST, kk, col ? t : t * (t + 1) / 2, status);
 }
 
 // Distributed variant: the panel of column j arrives broadcast into a
@@ -629,7 +678,7 @@ void OzPanel::update(hs_ctx* c, cudaStream_t st, double* A, int64_t tile_lo,
 void OzPanel::slice_contig(hs_ctx* c, cudaStream_t st, const double* X, int64_t N, int64_t j,
                            const int32_t* status) {
   const int64_t t = N - 1 - j;
-  oz_slice(c, st, X, t, b, s, S[j & 1], E[j & 1], rows, -1, 0, status);
+  oz_slice(c, st, X, t, b, s, S[j & 1], E[j & 1], rows, -1, -1, j, 0, status);
 }
 
 // A_ik -= L_ij L_kj^T for `npairs` owned (i, k) of column j (device list),
@@ -646,6 +695,7 @@ void OzPanel::update_list(hs_ctx* c, cudaStream_t st, double* A, const int64_t* 
   g.C = A;
   g.EA = g.EB = E[j & 1];
   g.b = b;
+  g.K = b;
   g.s = s;
   g.j = j;
   g.pairs = pairs;
@@ -704,13 +754,14 @@ hs_status hs_oz_gemm_tiles(hs_ctx* c, double* d_c, const double* d_p, const doub
     HS_CUDA(cudaMalloc(&ep, count * b * sizeof(int32_t)));
     HS_CUDA(cudaMalloc(&eq, count * b * sizeof(int32_t)));
     const int64_t rows = (int64_t)(count * b);
-    oz_slice(c, c->stream, d_p, (int64_t)count, (int)b, s, sp, ep, rows, -1, 0, nullptr);
-    oz_slice(c, c->stream, d_q, (int64_t)count, (int)b, s, sq, eq, rows, -1, 0, nullptr);
+    oz_slice(c, c->stream, d_p, (int64_t)count, (int)b, s, sp, ep, rows, -1, -1, 0, 0, nullptr);
+    oz_slice(c, c->stream, d_q, (int64_t)count, (int)b, s, sq, eq, rows, -1, -1, 0, 0, nullptr);
     const CUtensorMap ma = oz::slice_map(sp, (int)b, rows, oz::M, s);
     const CUtensorMap mb = oz::slice_map(sq, (int)b, rows, oz::N, s);
     oz::Args g{};
     g.mode = oz::BATCH;
     g.prof = g_oz_prof;
+    g.K = (int)b;
     g.C = d_c;
     g.EA = ep;
     g.EB = eq;
