@@ -70,6 +70,23 @@ hs_status hs_ctx_create(int device, void* stream, hs_ctx** out);
 hs_status hs_nccl_unique_id(void* id128);
 hs_status hs_ctx_create_nccl(int device, void* stream, int rank, int world,
                              const void* id128, hs_ctx** out);
+/* Multi-rank context over caller-provided collectives instead of NCCL: the
+ * SAME distributed CG / Cholesky code paths, with every collective handed to
+ * a host callback (device pointers on the context's GPU; the library
+ * synchronizes the issuing stream first, and the callback must complete the
+ * operation -- e.g. D2H, a gloo collective, H2D -- before returning, status 0
+ * on success). Lets several processes share one GPU as separate ranks (NCCL
+ * refuses duplicate GPUs), which is how the world > 1 paths are tested on a
+ * single-GPU box; it is not a performance transport. */
+typedef struct {
+  int (*allgather)(void* user, const double* send, double* recv, size_t count);
+  int (*reduce_scatter)(void* user, const double* send, double* recv, size_t count);
+  int (*broadcast)(void* user, const double* send, double* recv, size_t count, int root);
+  int (*allreduce_max_i64)(void* user, int64_t* buf, size_t count);
+  void* user;
+} hs_comm_ops;
+hs_status hs_ctx_create_custom_comm(int device, void* stream, int rank, int world,
+                                    const hs_comm_ops* ops, hs_ctx** out);
 void hs_ctx_destroy(hs_ctx* ctx);
 int hs_ctx_rank(const hs_ctx* ctx);
 int hs_ctx_world(const hs_ctx* ctx);

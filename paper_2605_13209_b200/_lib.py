@@ -30,6 +30,7 @@ HS_ERR_CUDA = 100
 EXPORTED = [
     "hs_last_error", "hs_last_error_payload", "hs_error_kind_name",
     "hs_ctx_create", "hs_nccl_unique_id", "hs_ctx_create_nccl", "hs_ctx_destroy",
+    "hs_ctx_create_custom_comm",
     "hs_ctx_rank", "hs_ctx_world", "hs_ctx_stream", "hs_ctx_kernel_launches",
     "hs_ctx_set_cholesky_gemm",
     "hs_rng_at", "hs_rng_uniform_pm1", "hs_generate_inputs",
@@ -69,6 +70,18 @@ class CholStats(C.Structure):
                 ("transfer_ms", C.c_double), ("true_residual", C.c_double)]
 
 
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
+REDUCE_SCATTER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
+BROADCAST_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int)
+ALLREDUCE_MAX_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t)
+
+
+class CommOps(C.Structure):  # hs_comm_ops
+    _fields_ = [("allgather", ALLGATHER_FN), ("reduce_scatter", REDUCE_SCATTER_FN),
+                ("broadcast", BROADCAST_FN), ("allreduce_max_i64", ALLREDUCE_MAX_FN),
+                ("user", C.c_void_p)]
+
+
 class LedgerEntry(C.Structure):  # hs_ledger_entry
     _fields_ = [("kind", C.c_uint8), ("direction", C.c_uint8), ("bytes", C.c_uint64),
                 ("step", C.c_int64)]
@@ -98,6 +111,8 @@ def lib():
         "hs_ctx_create": (C.c_int, [C.c_int, vp, pp]),
         "hs_nccl_unique_id": (C.c_int, [vp]),
         "hs_ctx_create_nccl": (C.c_int, [C.c_int, vp, C.c_int, C.c_int, vp, pp]),
+        "hs_ctx_create_custom_comm": (C.c_int, [C.c_int, vp, C.c_int, C.c_int,
+                                                C.POINTER(CommOps), pp]),
         "hs_ctx_destroy": (None, [vp]),
         "hs_ctx_rank": (C.c_int, [vp]),
         "hs_ctx_world": (C.c_int, [vp]),

@@ -709,12 +709,15 @@ void ensure_plan(hs_matrix* m) {
   std::vector<int64_t> row_cnt(hi - lo + 1, 0);
   std::vector<std::vector<int32_t>> extras(hi);
   int64_t nr = 0;
-  for (int64_t c = 0; c <= grid; ++c) cta_slab[c] = S * c / grid;
+  // slab indices are GLOBAL (the kernel derives global tile / block-row
+  // indices from them): this rank's slabs start at tile_lo * spt
+  const int64_t s_lo = m->tile_lo * spt;
+  for (int64_t c = 0; c <= grid; ++c) cta_slab[c] = s_lo + S * c / grid;
   for (int64_t c = 0; c < grid; ++c) {
     cta_rseg[c] = nr;
     const int64_t g0 = cta_slab[c], g1 = cta_slab[c + 1];
     if (g0 >= g1) continue;
-    const int64_t t0 = g0 / spt + m->tile_lo, t1 = (g1 - 1) / spt + m->tile_lo;
+    const int64_t t0 = g0 / spt, t1 = (g1 - 1) / spt;
     const int64_t i0 = tile_row(t0), i1 = tile_row(t1);
     for (int64_t i = i0; i <= i1; ++i) row_cnt[i - lo]++;
     nr += i1 - i0 + 1;
@@ -924,7 +927,7 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   const int world = c->world, rank = c->rank;
   // distributed protocol whenever there is a communicator (also world == 1,
   // which runs the NCCL path on one GPU)
-  const bool dp = c->comm != nullptr;
+  const bool dp = c->distributed();
   const int64_t b = (int64_t)m->b;
   const int64_t N = (int64_t)m->N;
   const int64_t chunk = m->vec_len / world;  // doubles per rank chunk

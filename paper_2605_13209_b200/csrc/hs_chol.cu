@@ -1286,7 +1286,7 @@ static void alloc_inverses(hs_matrix* m) {
 static void potrf_run_dist(hs_ctx* c, hs_matrix* m);
 
 static void potrf_run(hs_ctx* c, hs_matrix* m) {
-  if (c->comm && m->layout == 1) {  // NCCL context: 2D block-cyclic path
+  if (c->distributed() && m->layout == 1) {  // multi-rank: 2D block-cyclic path
     potrf_run_dist(c, m);
     return;
   }

@@ -91,8 +91,18 @@ static void ledger_add(hs_ctx* c, LedgerKind kind, uint64_t bytes) {
                                       bytes, c->step});
 }
 
+static void custom_check(int r, const char* what) {
+  if (r != 0) throw Failure{HS_ERR_CUDA, std::string(what) + ": custom transport failed"};
+}
+
 void comm_allgather(hs_ctx* c, const double* send, double* recv,
                     size_t count, LedgerKind kind) {
+  if (c->custom) {
+    HS_CUDA(cudaStreamSynchronize(c->stream));
+    custom_check(c->ops.allgather(c->ops.user, send, recv, count), "allgather");
+    ledger_add(c, kind, (uint64_t)count * c->world * sizeof(double));
+    return;
+  }
   nccl_check(c->nccl,
              c->nccl->AllGather(send, recv, count, ncclFloat64,
                                 (ncclComm_t)c->comm, c->stream),
@@ -101,6 +111,12 @@ void comm_allgather(hs_ctx* c, const double* send, double* recv,
 }
 void comm_reduce_scatter(hs_ctx* c, const double* send, double* recv,
                          size_t count, LedgerKind kind) {
+  if (c->custom) {
+    HS_CUDA(cudaStreamSynchronize(c->stream));
+    custom_check(c->ops.reduce_scatter(c->ops.user, send, recv, count), "reduce_scatter");
+    ledger_add(c, kind, (uint64_t)count * sizeof(double));
+    return;
+  }
   nccl_check(c->nccl,
              c->nccl->ReduceScatter(send, recv, count, ncclFloat64, ncclSum,
                                     (ncclComm_t)c->comm, c->stream),
@@ -110,6 +126,12 @@ void comm_reduce_scatter(hs_ctx* c, const double* send, double* recv,
 // broadcast from root's `send` into every rank's `recv` on stream s
 void comm_bcast_on(hs_ctx* c, const double* send, double* recv, size_t count,
                    int root, cudaStream_t s, LedgerKind kind) {
+  if (c->custom) {
+    HS_CUDA(cudaStreamSynchronize(s));
+    custom_check(c->ops.broadcast(c->ops.user, send, recv, count, root), "broadcast");
+    ledger_add(c, kind, (uint64_t)count * sizeof(double));
+    return;
+  }
   nccl_check(c->nccl,
              c->nccl->Broadcast(send, recv, count, ncclFloat64, root,
                                 (ncclComm_t)c->comm, s),
@@ -117,12 +139,19 @@ void comm_bcast_on(hs_ctx* c, const double* send, double* recv, size_t count,
   ledger_add(c, kind, (uint64_t)count * sizeof(double));
 }
 void comm_group(hs_ctx* c, bool start) {
+  if (c->custom) return;  // custom collectives complete one by one
   nccl_check(c->nccl, start ? c->nccl->GroupStart() : c->nccl->GroupEnd(),
              "ncclGroupStart/End");
 }
 // element-wise max over ranks of `count` int64 values (in place)
 void comm_allreduce_max_i64(hs_ctx* c, int64_t* buf, size_t count,
                             cudaStream_t s) {
+  if (c->custom) {
+    HS_CUDA(cudaStreamSynchronize(s));
+    custom_check(c->ops.allreduce_max_i64(c->ops.user, buf, count), "allreduce_max");
+    ledger_add(c, LK_SCALAR, (uint64_t)count * sizeof(int64_t));
+    return;
+  }
   nccl_check(c->nccl,
              c->nccl->AllReduce(buf, buf, count, ncclInt64, ncclMax,
                                 (ncclComm_t)c->comm, s),
@@ -537,6 +566,28 @@ hs_status hs_ctx_create_nccl(int device, void* stream, int rank, int world,
     nccl_check(c->nccl, c->nccl->CommInitRank(&comm, world, id, rank),
                "ncclCommInitRank");
     c->comm = comm;
+  } catch (...) {
+    delete c;
+    throw;
+  }
+  *out = c;
+  HS_API_END
+}
+
+hs_status hs_ctx_create_custom_comm(int device, void* stream, int rank, int world,
+                                    const hs_comm_ops* ops, hs_ctx** out) {
+  HS_API_BEGIN
+  HS_REQUIRE(out && ops && ops->allgather && ops->reduce_scatter && ops->broadcast &&
+                 ops->allreduce_max_i64,
+             HS_ERR_CONFIG, "null pointer / missing collective");
+  HS_REQUIRE(world >= 1 && rank >= 0 && rank < world, HS_ERR_CONFIG, "bad rank/world");
+  hs_ctx* c = new hs_ctx;
+  try {
+    ctx_common_init(c, device, stream);
+    c->rank = rank;
+    c->world = world;
+    c->ops = *ops;
+    c->custom = true;
   } catch (...) {
     delete c;
     throw;

@@ -65,6 +65,9 @@ struct hs_ctx {
   int rank = 0, world = 1;
   hs::Nccl* nccl = nullptr;
   void* comm = nullptr;  // ncclComm_t
+  hs_comm_ops ops{};      // custom host transport (hs_ctx_create_custom_comm)
+  bool custom = false;
+  bool distributed() const { return comm != nullptr || custom; }
   uint64_t launches = 0;
   int num_sms = 148;
   // profiling of the SYMV launches

@@ -332,6 +332,39 @@ class Runtime:
                                     C.byref(h)))
         return cls(device=device, _handle=h)
 
+    @classmethod
+    def custom_comm(cls, device: int, rank: int, world: int, transport,
+                    stream: int | None = None) -> "Runtime":
+        """Multi-rank context whose collectives go through ``transport``, an
+        object with ``allgather(send_ptr, recv_ptr, count)``,
+        ``reduce_scatter(send_ptr, recv_ptr, count)``,
+        ``broadcast(send_ptr, recv_ptr, count, root)`` and
+        ``allreduce_max_i64(ptr, count)`` on device pointers (see
+        hs_ctx_create_custom_comm; a test transport, not a fast one)."""
+        L = _lib.lib()
+
+        def wrap(fn):
+            def cb(*args):
+                try:
+                    fn(*args[1:])
+                    return 0
+                except Exception:  # the C side turns non-zero into an error
+                    import traceback
+                    traceback.print_exc()
+                    return 1
+            return cb
+
+        ops = _lib.CommOps(_lib.ALLGATHER_FN(wrap(transport.allgather)),
+                           _lib.REDUCE_SCATTER_FN(wrap(transport.reduce_scatter)),
+                           _lib.BROADCAST_FN(wrap(transport.broadcast)),
+                           _lib.ALLREDUCE_MAX_FN(wrap(transport.allreduce_max_i64)), None)
+        h = C.c_void_p()
+        _check(L.hs_ctx_create_custom_comm(device, C.c_void_p(stream or 0), rank, world,
+                                           C.byref(ops), C.byref(h)))
+        rt = cls(device=device, _handle=h)
+        rt._ops = ops  # keep the callbacks alive with the context
+        return rt
+
     @staticmethod
     def nccl_unique_id() -> bytes:
         buf = C.create_string_buffer(128)
