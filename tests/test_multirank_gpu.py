@@ -122,8 +122,27 @@ def _work(rank, world, port, job, result_q):
             led = [(e.kind, e.step) for e in rt.ledger()]
             out = {"x": d_x.cpu().numpy(), "iters": st.iterations, "conv": st.converged,
                    "res": st.true_residual, "u0": st.u0, "ledger": led}
+        elif kind == "io":
+            # every rank streams its own tiles from the file, then writes them
+            # back into a shared file at their offsets
+            path, out_path = extra["path"], extra["out"] + f"{int(extra['cyclic'])}"
+            m = hs.DeviceMatrix.load_bspd1(rt, path, cyclic=extra["cyclic"])
+            mine = np.zeros_like(a)
+            m.download(mine)
+            t = torch.from_numpy(mine)
+            dist.all_reduce(t)
+            dist.barrier()
+            m.save_bspd1(out_path)
+            dist.barrier()
+            out = {"A": t.numpy()}
         else:
             rt.set_cholesky_gemm(extra.get("slices", 0))
+            if extra.get("break_at"):
+                k = extra["break_at"]  # element (k, k) made negative
+                N = (n + b - 1) // b
+                i = k // b
+                a = a.copy()
+                a[(i * (i + 1) // 2 + i) * b * b + (k % b) * b + (k % b)] = -5.0
             m = hs.DeviceMatrix(rt, n, b, cyclic=True).upload(a)
             err = None
             try:
@@ -215,3 +234,24 @@ def test_block_cyclic_cholesky_multi_rank(oracle, world, n, b, slices):
         assert res[r]["err"] is None
         err = np.abs(res[r]["L"][mask] - L_ref[mask]).max()
         assert err <= 1e-10 * np.abs(a[mask]).max(), (r, err)
+
+
+def test_block_cyclic_not_spd_agreed_by_all_ranks(oracle):
+    n, b = 2048, 256
+    res = run_ranks(4, ("chol", n, b, {"break_at": 2 * b + 8}))
+    for r in range(4):
+        assert res[r]["err"] == (2, 8), res[r]["err"]
+
+
+@pytest.mark.parametrize("cyclic", [False, True])
+def test_multi_rank_bspd1_stream_load_and_save(oracle, tmp_path, cyclic):
+    import paper_2605_13209_b200 as hs
+    n, b = 1500, 128
+    a = oracle.generate_spd(n, b, seed=42)
+    path = str(tmp_path / "a.bspd")
+    hs.save_matrix(hs.BlockedSPDMatrix(n, b, a.copy()), path)
+    out = str(tmp_path / "back")
+    res = run_ranks(3, ("io", n, b, {"path": path, "out": out, "cyclic": cyclic}))
+    for r in range(3):
+        assert res[r]["A"].tobytes() == a.tobytes()
+    assert open(out + f"{int(cyclic)}", "rb").read() == open(path, "rb").read()
