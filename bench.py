@@ -249,7 +249,8 @@ def cholesky_secondary(hs, H, rt, torch, args, peak_tf: float, world: int = 1,
            "ms_per_factor": ms,
            "config": {"workload": "tiled Cholesky + substitutions (configs[2])"
                                   if world == 1 else
-                                  "tiled Cholesky, 2D block-cyclic (configs[4] layout)",
+                                  "tiled Cholesky + substitutions, 2D block-cyclic "
+                                  "(configs[4] layout)",
                       "n": n, "b": b, "flops": "n^3/3", "gpus": world},
            "gpu_launches_per_factor": int(launches),
            "roofline": {"bound": "tensor", "achieved": gflops / 1e3 / world,
@@ -334,18 +335,20 @@ def cholesky_secondary(hs, H, rt, torch, args, peak_tf: float, world: int = 1,
                          "int8_frac_approx": i8 / 4.5}}
         work.copy_from(m)
         H.potrf_device(rt, work)  # DMMA factor again for the solve below
-    if not cyclic:  # substitutions (single GPU), for the record
-        rhs = torch.from_numpy(hs.generate_rhs(n, b, 42).values).cuda()
-        x = torch.empty_like(rhs)
-        torch.cuda.synchronize()
-        t0 = time.time()
-        x.copy_(rhs)
-        H.trsv_device(rt, work, x.data_ptr(), upper=False)
-        H.trsv_device(rt, work, x.data_ptr(), upper=True)
-        torch.cuda.synchronize()
-        out["solve_ms"] = (time.time() - t0) * 1e3
-        res = H.true_residual_device(rt, m, x.data_ptr(), rhs.data_ptr())
-        out["relative_residual"] = res / float(torch.linalg.vector_norm(rhs[:n]))
+    # substitutions (single GPU, or pipelined over the block-cyclic factor)
+    rhs = torch.from_numpy(hs.generate_rhs(n, b, 42).values).cuda()
+    x = torch.empty_like(rhs)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    t0 = time.time()
+    x.copy_(rhs)
+    H.trsv_device(rt, work, x.data_ptr(), upper=False)
+    H.trsv_device(rt, work, x.data_ptr(), upper=True)
+    torch.cuda.synchronize()
+    out["solve_ms"] = (time.time() - t0) * 1e3
+    res = H.true_residual_device(rt, m, x.data_ptr(), rhs.data_ptr())
+    out["relative_residual"] = res / float(torch.linalg.vector_norm(rhs[:n]))
     work.free()
     m.free()
     return out

@@ -191,7 +191,9 @@ hs_status hs_solve_cg_host(hs_ctx* ctx, size_t n, size_t b,
 /* t = A x (symv_range over all rows, block_kernels.hpp:34-38). */
 hs_status hs_symv(hs_ctx* ctx, const hs_matrix* a, const double* d_x,
                   double* d_y);
-/* ||rhs - A x||_2 (the solvers' exit diagnostic). */
+/* ||rhs - A x||_2 (the solvers' exit diagnostic). Multi-rank: the matrix
+ * must be block-cyclic and x / rhs full-length on every rank (owned-tile
+ * partials all-gathered and summed in rank order). */
 hs_status hs_true_residual(hs_ctx* ctx, const hs_matrix* a, const double* d_x,
                            const double* d_rhs, double* out);
 
@@ -210,7 +212,10 @@ typedef struct {
  * HS_ERR_NUMERICAL on a non-finite factor (cholesky_solver.cpp:222-238). */
 hs_status hs_potrf(hs_ctx* ctx, hs_matrix* a, hs_chol_stats* stats);
 /* In-place L y = v (forward_substitute) and L^T x = y (back_substitute) on a
- * device vector; HS_ERR_SINGULAR_BLOCK on a zero / NaN diagonal. */
+ * device vector; HS_ERR_SINGULAR_BLOCK on a zero / NaN diagonal. Multi-rank
+ * (block-cyclic L, b % 128 == 0): every rank passes the same full-length v
+ * and gets the same result; steps pipeline over tile rows with b-double
+ * broadcasts (cholesky_solver.cpp:256-273 semantics). */
 hs_status hs_trsv_lower(hs_ctx* ctx, const hs_matrix* l, double* d_v);
 hs_status hs_trsv_upper(hs_ctx* ctx, const hs_matrix* l, double* d_v);
 /* factorize + substitutions, device resident (a is destroyed, holds L).

@@ -1168,17 +1168,97 @@ hs_status hs_symv(hs_ctx* c, const hs_matrix* m, const double* d_x,
   HS_API_END
 }
 
+// t (full length) = this rank's share of A x over a block-cyclic matrix:
+// block row i (blockIdx.y), 32 rows (blockIdx.x), summed over the owned
+// tiles (i, j <= i) as rows and (j > i, i) transposed; diagonal tiles use
+// their lower triangle only, like the SYMV. Fixed order, no atomics.
+__global__ void __launch_bounds__(256)
+    cyclic_partial_symv_kernel(const double* A, const int64_t* lpos, const double* x,
+                               double* t, int b, int64_t N) {
+  const int64_t i = blockIdx.y;
+  const int o0 = blockIdx.x * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t bb = (int64_t)b * b;
+  double rowacc[4] = {0.0, 0.0, 0.0, 0.0};  // rows o0 + warp + 8q (lanes over cols)
+  double colacc = 0.0;                      // row o0 + lane (warps over tile rows)
+  for (int64_t j = 0; j < N; ++j) {
+    const double* xj = x + j * b;
+    if (j <= i) {
+      const int64_t slot = lpos[i * (i + 1) / 2 + j];
+      if (slot >= 0) {
+        const double* T = A + slot * bb;
+        for (int q = 0; q < 4; ++q) {
+          const int r = o0 + warp + 8 * q;
+          if (r >= b) break;
+          const int cend = j == i ? r + 1 : b;
+          for (int cc = lane; cc < cend; cc += 32) rowacc[q] = fma(T[(int64_t)r * b + cc], xj[cc], rowacc[q]);
+        }
+        if (j == i && o0 + lane < b)  // strictly upper part of the diagonal tile
+          for (int cc = o0 + lane + 1 + warp; cc < b; cc += 8)
+            colacc = fma(T[(int64_t)cc * b + o0 + lane], xj[cc], colacc);
+      }
+    } else {
+      const int64_t slot = lpos[j * (j + 1) / 2 + i];
+      if (slot >= 0 && o0 + lane < b) {
+        const double* T = A + slot * bb;
+        for (int cc = warp; cc < b; cc += 8)
+          colacc = fma(T[(int64_t)cc * b + o0 + lane], xj[cc], colacc);
+      }
+    }
+  }
+  __shared__ double rows[32], cols[8][33];
+  for (int q = 0; q < 4; ++q) {
+    double a = rowacc[q];
+    for (int off = 16; off; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+    if (lane == 0) rows[warp + 8 * q] = a;
+  }
+  cols[warp][lane] = colacc;
+  __syncthreads();
+  if (warp == 0 && o0 + lane < b) {
+    double v = rows[lane];
+    for (int w = 0; w < 8; ++w) v += cols[w][lane];
+    t[i * b + o0 + lane] = v;
+  }
+}
+
+// t = sum over ranks of the gathered partials, rank order
+__global__ void rank_sum_kernel(const double* G, double* t, int64_t len, int world) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < len;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int r = 0; r < world; ++r) v += G[r * len + k];
+    t[k] = v;
+  }
+}
+
 hs_status hs_true_residual(hs_ctx* c, const hs_matrix* m, const double* d_x,
                            const double* d_rhs, double* out) {
   HS_API_BEGIN
   HS_REQUIRE(c && m && d_x && d_rhs && out, HS_ERR_CONFIG, "null pointer");
-  HS_REQUIRE(c->world == 1, HS_ERR_CONFIG, "hs_true_residual is single-rank");
+  HS_REQUIRE(c->world == 1 || m->layout == 1, HS_ERR_CONFIG,
+             "multi-rank hs_true_residual needs a block-cyclic matrix (full-length x)");
   HS_CUDA(cudaSetDevice(c->device));
   const int64_t pn = (int64_t)m->N * (int64_t)m->b;
   double* t = nullptr;
+  double* gath = nullptr;
   HS_CUDA(cudaMalloc(&t, pn * sizeof(double)));
   try {
-    symv_local(c, m, d_x, t);
+    if (c->world > 1) {
+      // every rank: its owned tiles' share of A x; all-gather; rank-order sum
+      const int b = (int)m->b;
+      HS_CUDA(cudaMalloc(&gath, pn * c->world * sizeof(double)));
+      cyclic_partial_symv_kernel<<<dim3((b + 31) / 32, (unsigned)m->N), 256, 0, c->stream>>>(
+          m->d, m->d_lpos, d_x, t, b, (int64_t)m->N);
+      HS_CUDA(cudaGetLastError());
+      launch_count(c);
+      c->step = -1;
+      comm_allgather(c, t, gath, (size_t)pn, LK_RESULT);
+      rank_sum_kernel<<<592, 256, 0, c->stream>>>(gath, t, pn, c->world);
+      HS_CUDA(cudaGetLastError());
+      launch_count(c);
+    } else {
+      symv_local(c, m, d_x, t);
+    }
     ensure_dpart(c, std::max<int64_t>((int64_t)m->N + 1, VGRID));
     HS_CUDA(cudaMemsetAsync(c->d_scalars, 0, sizeof(CgScalars), c->stream));
     VecArgs v{};
@@ -1198,9 +1278,11 @@ hs_status hs_true_residual(hs_ctx* c, const hs_matrix* m, const double* d_x,
     *out = sqrt(dd_value(acc));
   } catch (...) {
     cudaFree(t);
+    cudaFree(gath);
     throw;
   }
   cudaFree(t);
+  cudaFree(gath);
   HS_API_END
 }
 

@@ -1005,16 +1005,23 @@ __global__ void check_finite_kernel(const double* A, int64_t tile_lo,
 constexpr int TRSV_DIAG_THREADS = 1024;
 
 __global__ void __launch_bounds__(TRSV_DIAG_THREADS)
-    trsv_diag_kernel(const double* A, int64_t tile_lo, const double* W, double* v,
-                     int b, int cb, int f, int64_t i, int upper) {
+    trsv_diag_kernel(const double* A, int64_t tile_lo, const int64_t* lpos, const double* W,
+                     double* v, const double* G, int world, int b, int cb, int f, int64_t i,
+                     int upper) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ double sh[];  // vin[b] | sol[b]
   double* vin = sh;
   double* sol = sh + b;
-  const double* D = A + (tri(i, i) - tile_lo) * (int64_t)b * b;
+  const double* D = A + (lpos ? lpos[tri(i, i)] : tri(i, i) - tile_lo) * (int64_t)b * b;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  for (int k = tid; k < b; k += blockDim.x) vin[k] = v[i * b + k];
+  // multi-rank: v_i plus every rank's (negated) partial update, rank order
+  for (int k = tid; k < b; k += blockDim.x) {
+    double t = v[i * b + k];
+    if (G)
+      for (int r = 0; r < world; ++r) t += G[(int64_t)r * b + k];
+    vin[k] = t;
+  }
   __syncthreads();
   for (int step = 0; step < f; ++step) {
     const int sb = upper ? f - 1 - step : step;  // sub-block being solved
@@ -1091,15 +1098,19 @@ __global__ void __launch_bounds__(TRSV_DIAG_THREADS)
   for (int k = tid; k < b; k += blockDim.x) v[i * b + k] = sol[k];
 }
 
-// forward: v_k[rows] -= L_ki[rows, :] y_i for k = i+1 .. N-1 (blockIdx.y),
+// forward: out_k[rows] -= L_ki[rows, :] y_i for k = i+1 .. N-1 (blockIdx.y),
 //          32-row chunks (blockIdx.x)
-// backward: v_k[cols] -= L_ik[:, cols]^T x_i for k = 0 .. i-1, 32-col chunks
+// backward: out_k[cols] -= L_ik[:, cols]^T x_i for k = 0 .. i-1, 32-col chunks
+// (single rank: out = v; multi-rank: k from this rank's owned-tile `list`,
+// out = its partial-update vector)
 __global__ void __launch_bounds__(256)
-    trsv_update_kernel(const double* A, int64_t tile_lo, double* v, int b,
+    trsv_update_kernel(const double* A, int64_t tile_lo, const int64_t* lpos,
+                       const int32_t* list, const double* v, double* out, int b,
                        int64_t i, int upper) {
   pdl_wait();
   pdl_trigger();
-  const int64_t k = upper ? (int64_t)blockIdx.y : i + 1 + blockIdx.y;
+  const int64_t k = list ? (int64_t)list[blockIdx.y]
+                         : upper ? (int64_t)blockIdx.y : i + 1 + blockIdx.y;
   const int o0 = blockIdx.x * 32;
   extern __shared__ double yi[];  // [b]
   __shared__ double red[8][33];
@@ -1107,17 +1118,17 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (!upper) {
-    const double* T = A + (tri(k, i) - tile_lo) * (int64_t)b * b;
+    const double* T = A + (lpos ? lpos[tri(k, i)] : tri(k, i) - tile_lo) * (int64_t)b * b;
     for (int rr = warp; rr < 32; rr += 8) {
       const int r = o0 + rr;
       if (r >= b) break;
       double acc = 0.0;
       for (int c = lane; c < b; c += 32) acc = fma(T[(int64_t)r * b + c], yi[c], acc);
       for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-      if (lane == 0) v[k * b + r] -= acc;
+      if (lane == 0) out[k * b + r] -= acc;
     }
   } else {
-    const double* T = A + (tri(i, k) - tile_lo) * (int64_t)b * b;
+    const double* T = A + (lpos ? lpos[tri(i, k)] : tri(i, k) - tile_lo) * (int64_t)b * b;
     const int c = o0 + lane;
     double acc = 0.0;
     if (c < b)
@@ -1127,7 +1138,7 @@ __global__ void __launch_bounds__(256)
     if (warp == 0 && c < b) {
       double t = 0.0;
       for (int w = 0; w < 8; ++w) t += red[w][lane];
-      v[k * b + c] -= t;
+      out[k * b + c] -= t;
     }
   }
 }
@@ -1751,6 +1762,35 @@ static void ensure_inverses(hs_ctx* c, hs_matrix* m) {
   CholFlag* flag = nullptr;
   HS_CUDA(cudaMalloc(&flag, sizeof(CholFlag)));
   HS_CUDA(cudaMemsetAsync(flag, 0, sizeof(CholFlag), c->stream));
+  if (c->world > 1) {
+    // block-cyclic factor: each rank inverts the diagonal tiles it owns
+    // (the ones its substitution steps use), and all agree on the outcome
+    HS_REQUIRE(dmma_ok(b) && m->layout == 1, HS_ERR_CONFIG,
+               "multi-rank triangular solves need a block-cyclic factor with b % 128 == 0");
+    for (int64_t j = 0; j < N; ++j)
+      if (cyclic_owner(j, j, m->P, m->Q) == c->rank) {
+        diag128_kernel<<<(unsigned)f, 256, kDiagSmem, c->stream>>>(
+            m->d, 0, m->d_lpos, b, f, m->dinv, j * f, 1, flag);
+        HS_CUDA(cudaGetLastError());
+        launch_count(c);
+      }
+    CholFlag h{};
+    HS_CUDA(cudaMemcpyAsync(&h, flag, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    HS_CUDA(cudaStreamSynchronize(c->stream));
+    int64_t st[3] = {h.status, h.status ? h.col : -1, h.status ? h.pivot : -1};
+    HS_CUDA(cudaMemcpy(flag, st, sizeof(st), cudaMemcpyHostToDevice));
+    c->step = -1;
+    comm_allreduce_max_i64(c, (int64_t*)flag, 3, c->stream);
+    HS_CUDA(cudaMemcpyAsync(st, flag, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
+    HS_CUDA(cudaStreamSynchronize(c->stream));
+    cudaFree(flag);
+    h.status = (int32_t)st[0];
+    h.col = st[1];
+    h.pivot = st[2];
+    throw_flag(h);
+    m->has_inv = true;
+    return;
+  }
   if (dmma_ok(b)) {
     diag128_kernel<<<(unsigned)(N * f), 256, kDiagSmem, c->stream>>>(
         m->d, m->tile_lo, m->d_lpos, b, f, m->dinv, 0, 1, flag);
@@ -1768,8 +1808,97 @@ static void ensure_inverses(hs_ctx* c, hs_matrix* m) {
   m->has_inv = true;
 }
 
+// Multi-rank substitution over the 2D block-cyclic factor (SURVEY §8e:
+// pipelined over tile rows, b-double blocks on the wire). Every rank holds
+// the full vector v on entry and exit. Step i (forward i = 0..N-1, backward
+// i = N-1..0):
+//   all-gather the b-double slice i of each rank's partial-update vector w
+//     (w_k accumulates -L_ki y_i over the rank's own tiles);
+//   owner(i, i): v_i = W_i (v_i + sum_r w_i^(r)) with the stored inverse
+//     blocks (rank-order sum: identical on every run);
+//   broadcast v_i from owner(i, i);
+//   every rank: w_k -= L_ki v_i (forward, owned tiles below i) or
+//     w_k -= L_ik^T v_i (backward, owned tiles left of i).
+// The reference runs both substitutions on the one executor holding the
+// factor (cholesky_solver.cpp:287-309); with the factor spread over ranks
+// the steps are pipelined over tile rows instead and only b-double blocks
+// move, never a tile.
+static void trsv_run_dist(hs_ctx* c, hs_matrix* m, double* v, bool upper) {
+  HS_REQUIRE(m->layout == 1, HS_ERR_CONFIG,
+             "multi-rank triangular solves need a block-cyclic factor");
+  ensure_inverses(c, m);
+  const int b = (int)m->b;
+  const int cb = compute_block(b), f = b / cb;
+  const int64_t N = (int64_t)m->N;
+  const int P = m->P, Q = m->Q, me = c->rank, G = c->world;
+  const int chunks = (b + 31) / 32;
+  const size_t dsm = 2 * (size_t)b * sizeof(double), usm = (size_t)b * sizeof(double);
+  if (dsm > 48 * 1024)
+    HS_CUDA(cudaFuncSetAttribute(trsv_diag_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+  // per step, the owned tiles this rank applies v_i through
+  std::vector<int32_t> list;
+  std::vector<int64_t> off(N + 1, 0);
+  for (int64_t s = 0; s < N; ++s) {
+    const int64_t i = upper ? N - 1 - s : s;
+    off[s] = (int64_t)list.size();
+    if (upper) {
+      for (int64_t k = 0; k < i; ++k)
+        if (cyclic_owner(i, k, P, Q) == me) list.push_back((int32_t)k);
+    } else {
+      for (int64_t k = i + 1; k < N; ++k)
+        if (cyclic_owner(k, i, P, Q) == me) list.push_back((int32_t)k);
+    }
+  }
+  off[N] = (int64_t)list.size();
+  double *w = nullptr, *gath = nullptr;
+  int32_t* d_list = nullptr;
+  struct Free {
+    double **w, **g;
+    int32_t** l;
+    ~Free() {
+      cudaFree(*w);
+      cudaFree(*g);
+      cudaFree(*l);
+    }
+  } guard{&w, &gath, &d_list};
+  HS_CUDA(cudaMalloc(&w, (size_t)N * b * sizeof(double)));
+  HS_CUDA(cudaMalloc(&gath, (size_t)G * b * sizeof(double)));
+  HS_CUDA(cudaMalloc(&d_list, std::max<size_t>(list.size(), 1) * sizeof(int32_t)));
+  HS_CUDA(cudaMemcpyAsync(d_list, list.data(), list.size() * sizeof(int32_t),
+                          cudaMemcpyHostToDevice, c->stream));
+  HS_CUDA(cudaMemsetAsync(w, 0, (size_t)N * b * sizeof(double), c->stream));
+  for (int64_t s = 0; s < N; ++s) {
+    const int64_t i = upper ? N - 1 - s : s;
+    const int root = cyclic_owner(i, i, P, Q);
+    c->step = i;
+    // nobody has touched w_i before the first step
+    const bool gather = s > 0;
+    if (gather) comm_allgather(c, w + i * b, gath, (size_t)b, LK_SUBVECTOR);
+    if (root == me) {
+      HS_CUDA(launch_pdl(trsv_diag_kernel, dim3(1), dim3(TRSV_DIAG_THREADS / cb * cb), dsm,
+                         c->stream, (const double*)m->d, (int64_t)0,
+                         (const int64_t*)m->d_lpos, (const double*)m->dinv, v,
+                         gather ? (const double*)gath : nullptr, G, b, cb, f, i,
+                         upper ? 1 : 0));
+      launch_count(c);
+    }
+    comm_bcast_on(c, v + i * b, v + i * b, (size_t)b, root, c->stream, LK_SUBVECTOR);
+    const int64_t nk = off[s + 1] - off[s];
+    if (nk > 0) {
+      HS_CUDA(launch_pdl(trsv_update_kernel, dim3(chunks, (unsigned)nk), dim3(256), usm,
+                         c->stream, (const double*)m->d, (int64_t)0,
+                         (const int64_t*)m->d_lpos, (const int32_t*)(d_list + off[s]),
+                         (const double*)v, w, b, i, upper ? 1 : 0));
+      launch_count(c);
+    }
+  }
+  c->step = -1;
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+}
+
 static void trsv_run(hs_ctx* c, hs_matrix* m, double* v, bool upper) {
-  HS_REQUIRE(c->world == 1, HS_ERR_CONFIG, "triangular solves are single-rank");
+  if (c->world > 1) return trsv_run_dist(c, m, v, upper);
   ensure_inverses(c, m);
   const int b = (int)m->b;
   const int cb = compute_block(b), f = b / cb;
@@ -1783,15 +1912,16 @@ static void trsv_run(hs_ctx* c, hs_matrix* m, double* v, bool upper) {
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
   for (int64_t s = 0; s < N; ++s) {
     const int64_t i = upper ? N - 1 - s : s;
-    HS_CUDA(launch_pdl(trsv_diag_kernel, dim3(1), dim3(TRSV_DIAG_THREADS / cb * cb), dsm, c->stream,
-                       (const double*)m->d, m->tile_lo, (const double*)m->dinv, v, b, cb, f,
-                       i, upper ? 1 : 0));
+    HS_CUDA(launch_pdl(trsv_diag_kernel, dim3(1), dim3(TRSV_DIAG_THREADS / cb * cb), dsm,
+                       c->stream, (const double*)m->d, m->tile_lo, (const int64_t*)nullptr,
+                       (const double*)m->dinv, v, (const double*)nullptr, 1, b, cb, f, i,
+                       upper ? 1 : 0));
     launch_count(c);
     const int64_t nk = upper ? i : N - 1 - i;
     if (nk > 0) {
       HS_CUDA(launch_pdl(trsv_update_kernel, dim3(chunks, (unsigned)nk), dim3(256), usm,
-                         c->stream, (const double*)m->d, m->tile_lo, v, b, i,
-                         upper ? 1 : 0));
+                         c->stream, (const double*)m->d, m->tile_lo, (const int64_t*)nullptr,
+                         (const int32_t*)nullptr, (const double*)v, v, b, i, upper ? 1 : 0));
       launch_count(c);
     }
   }

@@ -790,6 +790,12 @@ hs_status hs_matrix_create_cyclic(hs_ctx* c, size_t n, size_t b, hs_matrix** out
     HS_CUDA(cudaMalloc(&m->d_owned, std::max<size_t>(1, m->owned.size()) * sizeof(int64_t)));
     HS_CUDA(cudaMalloc(&m->d_lpos, T * sizeof(int64_t)));
     HS_CUDA(cudaMemcpy(m->d_lpos, m->lpos.data(), T * sizeof(int64_t), cudaMemcpyHostToDevice));
+    // vectors are full length on every rank: block row i at i * b (the SYMV
+    // of a 1x1 grid, i.e. world 1, reads it)
+    std::vector<int64_t> off(N);
+    for (int64_t i = 0; i < N; ++i) off[i] = i * (int64_t)b;
+    HS_CUDA(cudaMalloc(&m->d_row_off, N * sizeof(int64_t)));
+    HS_CUDA(cudaMemcpy(m->d_row_off, off.data(), N * sizeof(int64_t), cudaMemcpyHostToDevice));
     if (!m->owned.empty())
       HS_CUDA(cudaMemcpy(m->d_owned, m->owned.data(), m->owned.size() * sizeof(int64_t),
                          cudaMemcpyHostToDevice));
@@ -813,6 +819,7 @@ hs_status hs_matrix_create_cyclic(hs_ctx* c, size_t n, size_t b, hs_matrix** out
     cudaFree(m->d);
     cudaFree(m->d_owned);
     cudaFree(m->d_lpos);
+    cudaFree(m->d_row_off);
     delete m;
     throw;
   }

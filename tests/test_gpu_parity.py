@@ -465,6 +465,27 @@ def test_distributed_cholesky_world1_matches_oracle(oracle, n, b):
         rt.close()
 
 
+@pytest.mark.parametrize("n,b", [(1024, 128), (2048, 512), (1500, 256)])
+def test_distributed_solve_world1_matches_oracle(oracle, n, b):
+    """Factor + substitutions + residual on a block-cyclic matrix through a
+    world-1 communicator (the 1x1 grid takes the single-rank kernels)."""
+    rt = hs.Runtime.distributed(0, 0, 1, hs.Runtime.nccl_unique_id())
+    try:
+        a = oracle.generate_spd(n, b, seed=42)
+        rhs = oracle.generate_rhs(n, b, seed=42)
+        ref = oracle.solve_spd(n, b, a, rhs)
+        m = hs.DeviceMatrix(rt, n, b, cyclic=True).upload(a)
+        orig = hs.DeviceMatrix(rt, n, b, cyclic=True).upload(a)
+        d_rhs = dev(rhs)
+        d_x = torch.zeros_like(d_rhs)
+        sp = hs.solve_spd_device(rt, m, d_rhs.data_ptr(), d_x.data_ptr(), a_orig=orig)
+        x = d_x.cpu().numpy()
+        assert np.linalg.norm(x - ref["x"]) <= 1e-9 * np.linalg.norm(ref["x"])
+        assert abs(sp.true_residual - ref["true_residual"]) <= 1e-10 * np.linalg.norm(rhs)
+    finally:
+        rt.close()
+
+
 @pytest.mark.parametrize("n,b", [(2048, 128), (1000, 64)])
 def test_distributed_cg_world1_matches_oracle(oracle, n, b):
     """The row-sharded NCCL protocol (reduce-scatter, all-gather of s,

@@ -135,6 +135,35 @@ def _work(rank, world, port, job, result_q):
             m.save_bspd1(out_path)
             dist.barrier()
             out = {"A": t.numpy()}
+        elif kind == "solve":
+            # factor + distributed substitutions + distributed residual, then
+            # substitutions on an uploaded factor (owned inverses computed)
+            rt.set_cholesky_gemm(extra.get("slices", 0))
+            rhs = o.generate_rhs(n, b, seed=42)
+            m = hs.DeviceMatrix(rt, n, b, cyclic=True).upload(a)
+            orig = hs.DeviceMatrix(rt, n, b, cyclic=True).upload(a)
+            d_rhs = torch.from_numpy(rhs).cuda()
+            d_x = torch.zeros_like(d_rhs)
+            rt.ledger(clear=True)
+            sp = hs.solve_spd_device(rt, m, d_rhs.data_ptr(), d_x.data_ptr(), a_orig=orig)
+            led = [(e.kind, e.step, e.bytes) for e in rt.ledger()]
+            _, L, _, _ = o.factorize(n, b, a)
+            if extra.get("singular_at") is not None:
+                k = extra["singular_at"]
+                i = k // b
+                L[(i * (i + 1) // 2 + i) * b * b + (k % b) * b + (k % b)] = 0.0
+            f = hs.DeviceMatrix(rt, n, b, cyclic=True).upload(L)
+            v = d_rhs.clone()
+            err = None
+            try:
+                H.trsv_device(rt, f, v.data_ptr(), False)
+                y = v.cpu().numpy()
+                H.trsv_device(rt, f, v.data_ptr(), True)
+            except hs.SingularBlockError as e:
+                err = str(e)
+                y = None
+            out = {"x": d_x.cpu().numpy(), "res": sp.true_residual, "y": y,
+                   "x2": v.cpu().numpy(), "err": err, "ledger": led}
         else:
             rt.set_cholesky_gemm(extra.get("slices", 0))
             if extra.get("break_at"):
@@ -255,3 +284,46 @@ def test_multi_rank_bspd1_stream_load_and_save(oracle, tmp_path, cyclic):
     for r in range(3):
         assert res[r]["A"].tobytes() == a.tobytes()
     assert open(out + f"{int(cyclic)}", "rb").read() == open(path, "rb").read()
+
+
+@pytest.mark.parametrize("world,n,b,slices", [(2, 2048, 256, 0), (4, 2048, 128, 0),
+                                              (3, 1500, 128, 8), (4, 4096, 512, 8)])
+def test_block_cyclic_solve_multi_rank(oracle, world, n, b, slices):
+    """Distributed factor + substitutions + residual, every rank
+    returning the same full x; substitutions on an uploaded factor match the
+    oracle's forward/back substitution."""
+    res = run_ranks(world, ("solve", n, b, {"slices": slices}))
+    a = oracle.generate_spd(n, b, seed=42)
+    rhs = oracle.generate_rhs(n, b, seed=42)
+    ref = oracle.solve_spd(n, b, a, rhs)
+    _, y_ref = oracle.forward_substitute(n, b, ref["L"], rhs)
+    _, x_ref = oracle.back_substitute(n, b, ref["L"], y_ref)
+    nb = np.linalg.norm(rhs)
+    N = (n + b - 1) // b
+    for r in range(world):
+        out = res[r]
+        assert np.array_equal(out["x"], res[0]["x"]) and out["res"] == res[0]["res"]
+        assert np.linalg.norm(out["x"] - ref["x"]) <= 1e-9 * np.linalg.norm(ref["x"])
+        # the reference's own acceptance bound (test_cholesky_solver.cpp:255-269)
+        assert out["res"] <= 1e-10 * nb, out["res"] / nb
+        assert abs(out["res"] - ref["true_residual"]) <= 1e-10 * nb
+        assert np.linalg.norm(out["y"] - y_ref) <= 1e-11 * np.linalg.norm(y_ref)
+        assert np.linalg.norm(out["x2"] - x_ref) <= 1e-10 * np.linalg.norm(x_ref)
+        # per substitution step: one b-double broadcast; an all-gather of
+        # b doubles per rank on every step but the first
+        steps = {}
+        for kind, st, nbytes in out["ledger"]:
+            if kind == "subvector" and st >= 0:
+                steps.setdefault(st, []).append(nbytes)
+        assert sorted(steps) == list(range(N))
+        for st, v in steps.items():
+            # forward + backward; the first step of each has no all-gather
+            gathers = 2 - (st == 0) - (st == N - 1)
+            assert sorted(v) == sorted([b * 8] * 2 + [world * b * 8] * gathers), (st, v)
+
+
+def test_block_cyclic_substitution_singular_agreed(oracle):
+    n, b = 1024, 128
+    res = run_ranks(3, ("solve", n, b, {"singular_at": 5 * b + 3}))
+    for r in range(3):
+        assert res[r]["err"] is not None and res[r]["y"] is None
