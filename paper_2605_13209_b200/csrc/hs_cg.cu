@@ -378,6 +378,11 @@ struct StepArgs {
   double eps;
   Dd* dd_slots;        // [world] per-rank partials (multi-GPU) or null
   int world;
+  // multi-GPU: the local (hi, lo) partial goes to dd_slots[g * slot_stride]
+  // for g < slot_count (one copy per rank chunk of a reduce-scattered
+  // buffer); by default to dd_slots[0] only
+  int64_t slot_stride = 0;
+  int slot_count = 1;
 };
 
 // Single-thread scalar step on the combined dot value (cg_solver.cpp lines
@@ -453,7 +458,9 @@ __device__ void dot_epilogue(double part, double* dpart, int slot, int count,
     if (sa.world == 1) {
       scalar_step(step, dd_value(tot), sa);
     } else {
-      sa.dd_slots[0] = tot;  // local slot; all-gathered by the host driver
+      // local partial, carried to the other ranks by the host driver's
+      // collective (all-gather, or inside the reduce-scatter of t)
+      for (int g = 0; g < sa.slot_count; ++g) sa.dd_slots[g * sa.slot_stride] = tot;
     }
   }
 }
@@ -590,7 +597,7 @@ enum VecMode : int {
   V_AXPY_X = 2,     // x += a s (recompute iteration, first half)
   V_RESIDUAL = 3,   // r = rhs - t, dot(r, r) -> BETA (recompute second half)
   V_SDIR = 4,       // s = r + beta s
-  V_DOT_ST = 5,     // dot(s, t) -> ALPHA (multi-rank path)
+  V_DOT_ST = 5,     // dot(s, t) -> ALPHA (after the generic SYMV)
   V_RESNORM = 6,    // dot(rhs - t, rhs - t) -> NONE (true residual)
 };
 
@@ -653,12 +660,12 @@ __global__ void __launch_bounds__(VBLOCK) vec_kernel(VecArgs va) {
 
 // Combine all-gathered per-rank (hi, lo) partials in rank order, then the
 // scalar step (multi-rank path; identical on every rank).
-__global__ void combine_kernel(const Dd* slots, int world, int step,
+__global__ void combine_kernel(const Dd* slots, int64_t stride, int world, int step,
                                StepArgs sa, double* out_value,
                                const int32_t* done) {
   if (step != STEP_INIT && step != STEP_NONE && done && *done) return;
   Dd acc = slots[0];
-  for (int g = 1; g < world; ++g) acc = dd_add(acc, slots[g]);
+  for (int g = 1; g < world; ++g) acc = dd_add(acc, slots[g * stride]);
   const double v = dd_value(acc);
   if (out_value) *out_value = v;
   if (step != STEP_NONE) scalar_step(step, v, sa);
@@ -894,6 +901,7 @@ struct CgBuffers {
   double* s_alt = nullptr;   // second direction buffer (fused s update)
   double* x_full = nullptr;  // padded full layout (recompute / result)
   double* t = nullptr;       // partial (vec_len) or local result (world 1)
+  double* r_full = nullptr;  // multi-rank: all-gathered r chunks (+ slots)
   double* t_loc = nullptr;   // reduced own rows (multi-rank)
   double* r = nullptr;       // local chunk
   double* rhs = nullptr;     // local chunk
@@ -905,6 +913,7 @@ struct CgBuffers {
     cudaFree(x_full);
     cudaFree(t);
     cudaFree(t_loc);
+    cudaFree(r_full);
     cudaFree(r);
     cudaFree(rhs);
     cudaFree(trace);
@@ -932,6 +941,7 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   const int64_t N = (int64_t)m->N;
   const int64_t chunk = m->vec_len / world;  // doubles per rank chunk
   const int64_t full = m->vec_len;
+  const int64_t rows_len = m->slot_off;      // row part of a chunk
   const int64_t lo = (int64_t)m->row_lo, hi = (int64_t)m->row_hi;
   const int64_t own = (hi - lo) * b;  // valid doubles in the chunk
   const size_t trace_n = prm->record_trace ? (size_t)prm->max_iters : 0;
@@ -951,11 +961,13 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   HS_CUDA(cudaMalloc(&B.x_full, full * sizeof(double)));
   HS_CUDA(cudaMalloc(&B.t, full * sizeof(double)));
   HS_CUDA(cudaMalloc(&B.r, chunk * sizeof(double)));
+  if (dp) HS_CUDA(cudaMalloc(&B.r_full, full * sizeof(double)));
   HS_CUDA(cudaMalloc(&B.rhs, chunk * sizeof(double)));
   HS_CUDA(cudaMalloc(&B.slots, std::max(world, 1) * sizeof(Dd)));
   if (dp) HS_CUDA(cudaMalloc(&B.t_loc, chunk * sizeof(double)));
   if (trace_n) HS_CUDA(cudaMalloc(&B.trace, 3 * trace_n * sizeof(double)));
   HS_CUDA(cudaMemsetAsync(B.t, 0, full * sizeof(double), c->stream));
+  HS_CUDA(cudaMemsetAsync(B.r, 0, chunk * sizeof(double), c->stream));
   HS_CUDA(cudaMemsetAsync(B.rhs, 0, chunk * sizeof(double), c->stream));
   HS_CUDA(cudaMemsetAsync(B.x_full, 0, full * sizeof(double), c->stream));
   HS_CUDA(cudaMemsetAsync(c->d_scalars, 0, sizeof(CgScalars), c->stream));
@@ -977,7 +989,7 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
     // all-gather the (hi, lo) partials in place, combine in rank order
     comm_allgather(c, reinterpret_cast<double*>(B.slots) + 2 * rank,
                    reinterpret_cast<double*>(B.slots), 2, LK_SCALAR);
-    combine_kernel<<<1, 1, 0, c->stream>>>(B.slots, world, step, sa, nullptr,
+    combine_kernel<<<1, 1, 0, c->stream>>>(B.slots, 1, world, step, sa, nullptr,
                                            done);
     HS_CUDA(cudaGetLastError());
     launch_count(c);
@@ -986,9 +998,15 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   // relocate it into this rank's slot before the in-place all-gather.
   StepArgs sa_local = sa;
   sa_local.dd_slots = B.slots + rank;
+  // per-iteration dots ride in the chunk slots (see the loop)
+  StepArgs sa_alpha = sa, sa_beta = sa;
+  sa_alpha.dd_slots = reinterpret_cast<Dd*>(B.t + rows_len) + rank;
+  sa_alpha.slot_stride = chunk / 2;
+  sa_alpha.slot_count = world;
+  sa_beta.dd_slots = reinterpret_cast<Dd*>(B.r + rows_len) + rank;
 
   VecArgs v{};
-  v.len = chunk;
+  v.len = rows_len;  // the chunk's rows (its slot region is not vector data)
   v.x = x_loc;
   v.r = B.r;
   v.s = s_loc;
@@ -1003,7 +1021,10 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   launch_vec(c, v);
   c->step = -1;  // ledger: setup
   dot_finish(STEP_INIT);
-  if (dp) comm_allgather(c, s_loc, B.s_full, (size_t)chunk, LK_SUBVECTOR);
+  if (dp) {
+    comm_allgather(c, s_loc, B.s_full, (size_t)chunk, LK_SUBVECTOR);
+    v.sa = sa_beta;  // r^T r partials ride in the r all-gather
+  }
 
   // Convergence is decided on the device (done flag); the host polls a
   // pinned copy of the scalars one chunk behind, so the GPU queue never
@@ -1030,11 +1051,18 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
         symv_to(c, m, B.s_full, B.t, true, &sa, done);
       }
     } else {
-      symv_to(c, m, B.s_full, B.t, false, nullptr, done);
+      // s^T t = sum over ranks of s^T (this rank's partial t): the finalize
+      // forms it on the full-length partial and writes the (hi, lo) into
+      // slot `rank` of every rank chunk of t (other slots stay 0), so the
+      // reduce-scatter that sums t also hands every rank all W partials,
+      // exactly; combined in rank order -> alpha, identical everywhere
+      symv_to(c, m, B.s_full, B.t, true, &sa_alpha, done);
       comm_reduce_scatter(c, B.t, B.t_loc, (size_t)chunk, LK_SUBVECTOR);
-      v.mode = V_DOT_ST;
-      launch_vec(c, v);
-      dot_finish(STEP_ALPHA);
+      combine_kernel<<<1, 1, 0, c->stream>>>(
+          reinterpret_cast<const Dd*>(B.t_loc + rows_len), 1, world, STEP_ALPHA, sa,
+          nullptr, done);
+      HS_CUDA(cudaGetLastError());
+      launch_count(c);
     }
     const bool recompute = rec_on && (it % prm->recompute_interval == 0);
     if (recompute) {
@@ -1050,12 +1078,29 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
       v.mode = V_UPDATE;  // lines 6-7 + u = r^T r + beta
       launch_vec(c, v);
     }
-    dot_finish(STEP_BETA);
-    if (!fuse_sdir) {
-      v.mode = V_SDIR;  // line 11
-      launch_vec(c, v);
+    if (!dp) {
+      if (!fuse_sdir) {
+        v.mode = V_SDIR;  // line 11
+        launch_vec(c, v);
+      }
+    } else {
+      // r chunks (+ each rank's r^T r partial in its slot) to every rank;
+      // beta from the slots in rank order; s = r + beta s on the full
+      // vector by every rank (the arithmetic of the local update + an
+      // all-gather of s, without that second collective)
+      comm_allgather(c, B.r, B.r_full, (size_t)chunk, LK_SUBVECTOR);
+      combine_kernel<<<1, 1, 0, c->stream>>>(
+          reinterpret_cast<const Dd*>(B.r_full + rows_len), (chunk + 2) / 2, world,
+          STEP_BETA, sa, nullptr, done);
+      HS_CUDA(cudaGetLastError());
+      launch_count(c);
+      VecArgs vs = v;
+      vs.len = full;
+      vs.r = B.r_full;
+      vs.s = B.s_full;
+      vs.mode = V_SDIR;
+      launch_vec(c, vs);
     }
-    if (dp) comm_allgather(c, s_loc, B.s_full, (size_t)chunk, LK_SUBVECTOR);
     if (it % check_every == 0) {
       const int slot = (int)((it / check_every) & 1);
       HS_CUDA(cudaMemcpyAsync(pin + slot, c->d_scalars, sizeof(CgScalars),
@@ -1109,12 +1154,13 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   VecArgs vr = v;
   vr.mode = V_RESNORM;
   vr.done = nullptr;
+  if (dp) vr.sa = sa_local;
   launch_vec(c, vr);
   double res2;
   if (dp) {
     comm_allgather(c, reinterpret_cast<double*>(B.slots) + 2 * rank,
                    reinterpret_cast<double*>(B.slots), 2, LK_SCALAR);
-    combine_kernel<<<1, 1, 0, c->stream>>>(B.slots, world, STEP_NONE, sa,
+    combine_kernel<<<1, 1, 0, c->stream>>>(B.slots, 1, world, STEP_NONE, sa,
                                            c->d_dpart + N, nullptr);
     HS_CUDA(cudaGetLastError());
     launch_count(c);

@@ -724,11 +724,13 @@ hs_status hs_matrix_create(hs_ctx* c, size_t n, size_t b, hs_matrix** out) {
   int64_t lmax = 0;
   for (int g = 0; g < c->world; ++g)
     lmax = std::max<int64_t>(lmax, m->bounds[g + 1] - m->bounds[g]);
-  m->vec_len = lmax * (int64_t)b * c->world;
+  m->slot_off = lmax * (int64_t)b;
+  const int64_t stride = m->slot_off + (c->distributed() ? 2 * (int64_t)c->world : 0);
+  m->vec_len = stride * c->world;
   std::vector<int64_t> off(m->N);
   for (int g = 0; g < c->world; ++g)
     for (int64_t i = m->bounds[g]; i < m->bounds[g + 1]; ++i)
-      off[i] = ((int64_t)g * lmax + (i - m->bounds[g])) * (int64_t)b;
+      off[i] = (int64_t)g * stride + (i - m->bounds[g]) * (int64_t)b;
   try {
     const size_t bytes = m->local_tiles() * b * b * sizeof(double);
     if (bytes) HS_CUDA(cudaMalloc(&m->d, bytes));
@@ -784,6 +786,7 @@ hs_status hs_matrix_create_cyclic(hs_ctx* c, size_t n, size_t b, hs_matrix** out
   m->tile_hi = T;
   m->bounds = {0, (int64_t)m->N};
   m->vec_len = (int64_t)(m->N * b);
+  m->slot_off = m->vec_len;
   try {
     const size_t bytes = m->local_tiles() * b * b * sizeof(double);
     if (bytes) HS_CUDA(cudaMalloc(&m->d, bytes));

@@ -116,6 +116,11 @@ struct hs_matrix {
   // Multi-rank vector layout: row i lives at vec_off[i] (padded rank chunks).
   std::vector<int64_t> bounds;    // world+1 block-row bounds
   int64_t vec_len = 0;            // doubles in a full (padded) vector
+  // Multi-rank CG: each rank chunk (vec_len / world doubles) holds its rows
+  // (padded to the largest rank) and, from slot_off on, 2 * world doubles of
+  // dot-product slots that ride along in the chunk's collectives.
+  // slot_off == chunk length when there are no slots.
+  int64_t slot_off = 0;
   int64_t* d_row_off = nullptr;   // [N] element offset of block row i
   size_t local_tiles() const {
     return layout == 1 ? owned.size() : (size_t)(tile_hi - tile_lo);

@@ -4,10 +4,13 @@ The closed-form per-iteration / per-column contracts below play the role of
 the reference's ledger tests (test_cg_solver.cpp:131-187,
 test_cholesky_solver.cpp:125-176) for the G-GPU protocols:
 
-* CG, iteration k: 2 scalar entries (the alpha and beta dot all-gathers) and
-  2 subvector entries (reduce-scatter of t, all-gather of s), plus 2 more
-  subvector entries on each recompute iteration (all-gather of x,
-  reduce-scatter of A x); setup and exit entries carry step -1; the result
+* CG, iteration k: 2 subvector entries and no scalar one: the reduce-scatter
+  of t carries every rank's s^T t partial, the all-gather of r every rank's
+  r^T r partial (2 doubles per rank appended to each rank chunk), so the
+  two dot reductions of the reference's iteration cost no collective of
+  their own; plus 2 more subvector entries on each recompute iteration
+  (all-gather of x, reduce-scatter of A x); setup and exit entries carry
+  step -1 (one scalar all-gather each for u0 and the residual); the result
   all-gather is one `result` entry.
 * Cholesky, column j: 2 + (N - j - 1) block entries (L_jj, its inverse
   blocks, and one broadcast per panel tile), then one scalar status
@@ -56,13 +59,14 @@ def test_cg_ledger_contract(iters, interval, recomputes):
         sc, sv = by_step(led, "scalar"), by_step(led, "subvector")
         rec_steps = {k for k in range(1, iters + 1) if interval and k % interval == 0}
         for k in range(1, iters + 1):
-            assert sc[k] == 2, k
+            assert sc[k] == 0, k
             assert sv[k] == 2 + (2 if k in rec_steps else 0), k
-        assert sum(v for s, v in sc.items() if s >= 1) == 2 * iters
+        assert sum(v for s, v in sc.items() if s >= 1) == 0
         assert sum(v for s, v in sv.items() if s >= 1) == 2 * iters + 2 * recomputes
         assert Counter(e.kind for e in led if e.step == -1) == {
             "scalar": 2, "subvector": 2, "result": 1}
-        vec_bytes = n * 8  # world 1: the padded chunk is the whole vector
+        # world 1: the chunk is the whole vector + one (hi, lo) dot slot
+        vec_bytes = (n + 2) * 8
         for e in led:
             if e.kind in ("subvector", "result"):
                 assert e.bytes == vec_bytes

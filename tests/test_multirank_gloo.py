@@ -2,17 +2,22 @@
 
 The GPU path (hs_cg.cu cg_run, world > 1) shards the packed tiles by block
 rows with the product's own partition (hs_partition_rows), keeps vectors in a
-padded rank-chunk layout, and per iteration does
+padded rank-chunk layout whose chunks end in 2 * world doubles of dot slots,
+and per iteration does
   1. local packed SYMV -> full-length partial t (own rows + transposed
-     contributions to earlier rows),
-  2. reduce-scatter of the partial -> own rows of t,
-  3. local dot partials as double-double, all-gathered and combined in rank
-     order (identical on every rank),
-  4. local x / r / s updates,
-  5. all-gather of s (and of x on recompute iterations).
-This test restates exactly that protocol with torch.distributed over gloo
-(NCCL needs GPUs; gloo has no reduce-scatter, so all-reduce + slice stands in)
-and checks the solution against the single-process oracle CG.
+     contributions to earlier rows), and this rank's s^T t_partial as a
+     double-double written into slot `rank` of every chunk,
+  2. reduce-scatter of the partial -> own rows of t and, in the slots, every
+     rank's s^T t partial (exact: the other ranks' slots are 0); rank-order
+     combine -> alpha, identical on every rank,
+  3. local x / r updates and r^T r partial into slot `rank` of the r chunk,
+  4. all-gather of the r chunks (rows + slots); rank-order combine -> beta;
+     s = r + beta s on the full vector by every rank,
+  5. on recompute iterations, also an all-gather of x.
+Two collectives per iteration. This test restates exactly that protocol with
+torch.distributed over gloo (NCCL needs GPUs; gloo has no reduce-scatter, so
+all-reduce + slice stands in) and checks the solution against the
+single-process oracle CG.
 """
 import os
 import socket
@@ -72,7 +77,8 @@ def worker(rank, world, port, a_packed, rhs, bounds, iters, out):
     b, N = B_, (N_ + B_ - 1) // B_
     lo, hi = bounds[rank], bounds[rank + 1]
     lmax = max(bounds[g + 1] - bounds[g] for g in range(world))
-    chunk = lmax * b
+    rows_len = lmax * b
+    chunk = rows_len + 2 * world  # rows, then one (hi, lo) slot per rank
     tri = lambda i: i * (i + 1) // 2  # noqa: E731
     tiles = a_packed.reshape(-1, b * b)[tri(lo):tri(hi)]
 
@@ -100,41 +106,55 @@ def worker(rank, world, port, a_packed, rhs, bounds, iters, out):
         dist.all_reduce(t)
         return t.numpy()[rank * chunk:(rank + 1) * chunk].copy()
 
-    def dot(u, v):
-        part = dd_sum([u[i * b:(i + 1) * b] @ v[i * b:(i + 1) * b] for i in range(hi - lo)])
+    def dd_dot(u, v, nblk):
+        return dd_sum([u[i * b:(i + 1) * b] @ v[i * b:(i + 1) * b] for i in range(nblk)])
+
+    def combine(slots):
+        acc = tuple(slots[0])
+        for p in slots[1:]:
+            acc = dd_add(acc, tuple(p))
+        return acc[0] + acc[1]
+
+    def setup_dot(u, v):  # u0 (and the exit residual): a scalar all-gather
+        part = dd_dot(u, v, hi - lo)
         parts = [torch.zeros(2, dtype=torch.float64) for _ in range(world)]
         dist.all_gather(parts, torch.tensor(part, dtype=torch.float64))
-        acc = tuple(parts[0].tolist())
-        for p in parts[1:]:
-            acc = dd_add(acc, tuple(p.tolist()))
-        return acc[0] + acc[1]
+        return combine([p.tolist() for p in parts])
 
     own = (hi - lo) * b
     rhs_loc = np.zeros(chunk)
     rhs_loc[:own] = rhs[lo * b:hi * b]
     x = np.zeros(chunk)
     r = rhs_loc.copy()
-    s_loc = rhs_loc.copy()
-    s_full = allgather_chunk(s_loc)
-    u = dot(rhs_loc, rhs_loc)
+    s_full = allgather_chunk(rhs_loc)
+    u = setup_dot(rhs_loc, rhs_loc)
     limit = 1e-12 * u  # eps = 1e-6, as cg_solver.cpp:248
     done = 0
     for it in range(1, iters + 1):
-        t_part = to_padded(local_symv(tiles, lo, hi, b, to_std(s_full), N))
+        t_std = local_symv(tiles, lo, hi, b, to_std(s_full), N)
+        t_part = to_padded(t_std)
+        # s^T t_partial over the full length, into slot `rank` of every chunk
+        part = dd_sum([to_std(s_full)[i * b:(i + 1) * b] @ t_std[i * b:(i + 1) * b]
+                       for i in range(N)])
+        for g in range(world):
+            t_part[g * chunk + rows_len + 2 * rank:g * chunk + rows_len + 2 * rank + 2] = part
         t = reduce_scatter(t_part)
-        alpha = u / dot(s_loc, t)
-        x = x + alpha * s_loc
+        alpha = u / combine([t[rows_len + 2 * g:rows_len + 2 * g + 2] for g in range(world)])
+        s_loc = s_full[rank * chunk:(rank + 1) * chunk]
+        x[:rows_len] = x[:rows_len] + alpha * s_loc[:rows_len]
         if it % 50 == 0:
             x_full = allgather_chunk(x)
             t = reduce_scatter(to_padded(local_symv(tiles, lo, hi, b, to_std(x_full), N)))
-            r = rhs_loc - t
+            r[:rows_len] = rhs_loc[:rows_len] - t[:rows_len]
         else:
-            r = r - alpha * t
-        unew = dot(r, r)
+            r[:rows_len] = r[:rows_len] - alpha * t[:rows_len]
+        r[rows_len + 2 * rank:rows_len + 2 * rank + 2] = dd_dot(r, r, hi - lo)
+        r_full = allgather_chunk(r)
+        unew = combine([r_full[g * chunk + rows_len + 2 * g:g * chunk + rows_len + 2 * g + 2]
+                        for g in range(world)])
         beta = unew / u
         u = unew
-        s_loc = r + beta * s_loc
-        s_full = allgather_chunk(s_loc)
+        s_full = r_full + beta * s_full  # every rank, full length
         done = it
         if u <= limit:
             break
