@@ -1,9 +1,10 @@
 // Blocked conjugate gradient on B200 (reference cg_solver.cpp:223-368).
 //
 // Hot kernel: packed-symmetric SYMV that streams every stored tile of A
-// exactly once per matvec. Persistent CTAs (one per SM) own contiguous
-// ranges of 32-KB "slabs" (row strips of the row-major tiles) in packed
-// order. A producer warp moves slabs + the two s-vector segments they need
+// exactly once per matvec. Persistent CTAs (one per SM) claim work units --
+// contiguous ranges of 32-KB "slabs" (row strips of the row-major tiles) in
+// packed order, guided sizes shrinking towards the end -- from an atomic
+// counter, so CTAs on slower SMs simply take fewer units. A producer warp moves slabs + the two s-vector segments they need
 // into a 5-stage shared-memory ring with the TMA bulk-copy engine
 // (cp.async.bulk + mbarrier complete_tx); 8 consumer warps read each element
 // once from shared memory and use it twice: for the row sum (A_ij s_j -> t_i)
@@ -49,14 +50,14 @@ struct SymvCfg {
   static constexpr int G = TPR <= 32 ? NCW : RPP;
   // 8 consumer warps (16 measured slower: more smem traffic per slab)
   static constexpr int NSTAGE = B == 512 ? 4 : 5;
-  // slab | seg_j (B) | seg_i (RS) | r_j (B) | r_i (RS); the r segments are
-  // filled only when the s update is fused (s = r + beta s_old on the fly)
+  // slab | seg_j (B) | seg_i (RS)
   static constexpr int SEG_BYTES = (B + RS) * 8;
-  static constexpr int STAGE_BYTES = SLAB_BYTES + 2 * SEG_BYTES;
+  static constexpr int STAGE_BYTES = SLAB_BYTES + SEG_BYTES;
   static constexpr int COLRED_BYTES = G * B * 8;
   static constexpr int YROW_BYTES = H * B * 8;
+  // + full/empty mbarriers + per-stage (slab, unit) headers
   static constexpr int SMEM = NSTAGE * STAGE_BYTES + 2 * COLRED_BYTES +
-                              2 * YROW_BYTES + 2 * NSTAGE * 8;
+                              2 * YROW_BYTES + 2 * NSTAGE * 8 + NSTAGE * 12;
   static_assert(RT >= 1 && RT <= 2 && RS == RT * RPP, "row mapping");
   static_assert(STAGE_BYTES % 16 == 0, "bulk copy alignment");
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
@@ -74,14 +75,15 @@ struct SymvArgs {
   double* colextra;       // [grid][B]   a CTA's first tile when it starts
                           //             mid-tile (split tiles)
   const int32_t* done;    // CG early-exit flag (nullable)
-  // fused CG direction update (single rank): the input `s` is s_old and the
-  // kernel multiplies with s = r + beta s_old, which it also stores to s_out
-  // (each entry once, by the slab of its diagonal tile)
-  const double* r;
-  double* s_out;
-  const double* beta;
-  int fuse;
+  uint32_t* unit_ctr;     // next unclaimed work unit
+  int vgrid;              // work units (cta_slab has vgrid + 1 entries)
+  unsigned ts_seq;        // launch sequence (HS_SYMV_TIMING builds only)
 };
+
+#ifdef HS_SYMV_TIMING
+__device__ unsigned long long g_symv_ts[4096][2];
+__device__ int g_symv_ts_print = 0;
+#endif
 
 template <int B, int NCW>
 __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
@@ -99,11 +101,18 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
   double* yrow = colred + 2 * G * B;  // [2][H][B]
   uint64_t* full = reinterpret_cast<uint64_t*>(yrow + 2 * Cfg::H * B);
   uint64_t* empty = full + NS;
+  // per-stage header: the slab staged and its work unit (-1: no more work)
+  int64_t* hdr_g = reinterpret_cast<int64_t*>(empty + NS);
+  int32_t* hdr_u = reinterpret_cast<int32_t*>(hdr_g + NS);
 
   const int tid = threadIdx.x;
-  const int64_t g0 = args.cta_slab[blockIdx.x];
-  const int64_t g1 = args.cta_slab[blockIdx.x + 1];
-  if (g0 >= g1) return;
+#ifdef HS_SYMV_TIMING
+  uint64_t ts_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts_start));
+  unsigned sm_id;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_id));
+  int64_t ts_slabs = 0;
+#endif
 
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -115,46 +124,50 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
   for (int k = tid; k < 2 * Cfg::H * B; k += blockDim.x) yrow[k] = 0.0;
   __syncthreads();
 
-  const int64_t t_first = g0 / SPT;
-  const int64_t i_first = tile_row(t_first);
-
   if (tid >= CT) {
     // ---------------- producer warp ----------------
+    // claims work units in order (one atomic per unit) and streams their
+    // slabs; the header tells the consumers which slab / unit a stage holds
     if (tid == CT) {
-      int64_t t = t_first, i = i_first, j = t_first - tri(i_first, 0);
-      int q = (int)(g0 - t_first * SPT);
-      for (int64_t g = g0; g < g1; ++g) {
-        const int64_t k = g - g0;
-        const int st = (int)(k % NS);
-        if (k >= NS) mbar_wait(&empty[st], (uint32_t)(((k / NS) - 1) & 1));
-        unsigned char* buf = stages + st * Cfg::STAGE_BYTES;
-        // the s_j (and r_j) segment is constant over a tile: consumers keep
-        // it in registers, so it is only staged with a tile's first slab
-        const bool seg_j = (q == 0) || (g == g0);
-        const int nvec = args.fuse ? 2 : 1;
-        mbar_arrive_expect_tx(&full[st],
-                              Cfg::SLAB_BYTES + nvec * (RS * 8 + (seg_j ? B * 8 : 0)));
-        const double* src =
-            args.a + ((t - args.tile_lo) * B + (int64_t)q * RS) * B;
-        const int64_t oi = args.row_off[i] + q * RS;
-        bulk_g2s(buf, src, Cfg::SLAB_BYTES, &full[st]);
-        bulk_g2s(buf + Cfg::SLAB_BYTES + B * 8, args.s + oi, RS * 8, &full[st]);
-        if (args.fuse)
-          bulk_g2s(buf + Cfg::SLAB_BYTES + Cfg::SEG_BYTES + B * 8, args.r + oi,
-                   RS * 8, &full[st]);
-        if (seg_j) {
-          const int64_t oj = args.row_off[j];
-          bulk_g2s(buf + Cfg::SLAB_BYTES, args.s + oj, B * 8, &full[st]);
-          if (args.fuse)
-            bulk_g2s(buf + Cfg::SLAB_BYTES + Cfg::SEG_BYTES, args.r + oj, B * 8,
-                     &full[st]);
+      int64_t k = 0;  // stages filled so far
+      for (;;) {
+        const int u = (int)atomicAdd(args.unit_ctr, 1u);
+        const int st0 = (int)(k % NS);
+        if (u >= args.vgrid) {
+          if (k >= NS) mbar_wait(&empty[st0], (uint32_t)(((k / NS) - 1) & 1));
+          hdr_g[st0] = -1;
+          hdr_u[st0] = -1;
+          mbar_arrive(&full[st0]);  // end of work, no bytes
+          break;
         }
-        if (++q == SPT) {
-          q = 0;
-          ++t;
-          if (++j > i) {
-            ++i;
-            j = 0;
+        const int64_t g0 = args.cta_slab[u], g1 = args.cta_slab[u + 1];
+        const int64_t t0 = g0 / SPT;
+        int64_t t = t0, i = tile_row(t0), j = t0 - tri(tile_row(t0), 0);
+        int q = (int)(g0 - t0 * SPT);
+        for (int64_t g = g0; g < g1; ++g, ++k) {
+          const int st = (int)(k % NS);
+          if (k >= NS) mbar_wait(&empty[st], (uint32_t)(((k / NS) - 1) & 1));
+          hdr_g[st] = g;
+          hdr_u[st] = u;
+          unsigned char* buf = stages + st * Cfg::STAGE_BYTES;
+          // the s_j (and r_j) segment is constant over a tile: consumers keep
+          // it in registers, so it is only staged with a tile's first slab
+          const bool seg_j = (q == 0) || (g == g0);
+          mbar_arrive_expect_tx(&full[st], Cfg::SLAB_BYTES + RS * 8 + (seg_j ? B * 8 : 0));
+          const double* src =
+              args.a + ((t - args.tile_lo) * B + (int64_t)q * RS) * B;
+          const int64_t oi = args.row_off[i] + q * RS;
+          bulk_g2s(buf, src, Cfg::SLAB_BYTES, &full[st]);
+          bulk_g2s(buf + Cfg::SLAB_BYTES + B * 8, args.s + oi, RS * 8, &full[st]);
+          if (seg_j)
+            bulk_g2s(buf + Cfg::SLAB_BYTES, args.s + args.row_off[j], B * 8, &full[st]);
+          if (++q == SPT) {
+            q = 0;
+            ++t;
+            if (++j > i) {
+              ++i;
+              j = 0;
+            }
           }
         }
       }
@@ -168,24 +181,42 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
   const int rl = tid / TPR;  // row lane: slab rows RT*rl + r
   const int h = cl / W;      // row-sharing warp index (B = 512)
   const int grp = TPR <= 32 ? warp : rl;  // colred row after the warp reduce
-  const int64_t rseg0 = args.cta_rseg[blockIdx.x];
-  const bool split_start = (g0 % SPT) != 0;
-  const bool fuse = args.fuse != 0;
-  const double beta = fuse ? *args.beta : 0.0;
 
   double cacc[8];
 #pragma unroll
   for (int m = 0; m < 8; ++m) cacc[m] = 0.0;
   double2 sj[4];  // this thread's 8 columns of s_j, kept for the whole tile
 
-  int64_t t = t_first, i = i_first, j = t_first - tri(i_first, 0);
-  int q = (int)(g0 - t_first * SPT);
+  // state of the current work unit (set when its first slab arrives)
+  int cur_u = -1;
+  int64_t g0 = 0, g1 = 0, t_first = 0, i_first = 0, rseg0 = 0;
+  bool split_start = false;
+  int64_t t = 0, i = 0, j = 0;
+  int q = 0;
   int tpar = 0, rpar = 0;  // parity of tiles / block rows flushed
 
-  for (int64_t g = g0; g < g1; ++g) {
-    const int64_t k = g - g0;
+  for (int64_t k = 0;; ++k) {
     const int st = (int)(k % NS);
     mbar_wait(&full[st], (uint32_t)((k / NS) & 1));
+    const int64_t g = hdr_g[st];
+    if (g < 0) break;
+    const int u = hdr_u[st];
+    if (u != cur_u) {
+      cur_u = u;
+      g0 = args.cta_slab[u];
+      g1 = args.cta_slab[u + 1];
+      t_first = g0 / SPT;
+      i_first = tile_row(t_first);
+      rseg0 = args.cta_rseg[u];
+      split_start = (g0 % SPT) != 0;
+      t = t_first;
+      i = i_first;
+      j = t_first - tri(i_first, 0);
+      q = (int)(g0 - t_first * SPT);
+    }
+#ifdef HS_SYMV_TIMING
+    ++ts_slabs;
+#endif
     const unsigned char* buf = stages + st * Cfg::STAGE_BYTES;
     const double2* A2 = reinterpret_cast<const double2*>(buf);
     const double* si =
@@ -198,31 +229,14 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
 #pragma unroll
       for (int m = 0; m < 4; ++m)
         a[r][m] = A2[(RT * rl + r) * (B / 2) + cl + TPR * m];
-    if (q == 0 || g == g0) {  // tile start: load (and update) s_j once
+    if (q == 0 || g == g0) {  // tile start: load s_j once
       const double2* sj2 =
           reinterpret_cast<const double2*>(buf + Cfg::SLAB_BYTES);
 #pragma unroll
       for (int m = 0; m < 4; ++m) sj[m] = sj2[cl + TPR * m];
-      if (fuse) {
-        const double2* rj2 = reinterpret_cast<const double2*>(
-            buf + Cfg::SLAB_BYTES + Cfg::SEG_BYTES);
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const double2 rv = rj2[cl + TPR * m];
-          sj[m] = make_double2(fma(beta, sj[m].x, rv.x), fma(beta, sj[m].y, rv.y));
-        }
-      }
     }
 #pragma unroll
     for (int r = 0; r < RT; ++r) sir[r] = si[RT * rl + r];
-    if (fuse) {  // s = r + beta s_old  (cg_solver.cpp line 11, xpay_range)
-      const double* ri = reinterpret_cast<const double*>(
-          buf + Cfg::SLAB_BYTES + Cfg::SEG_BYTES + B * 8);
-#pragma unroll
-      for (int r = 0; r < RT; ++r) sir[r] = fma(beta, sir[r], ri[RT * rl + r]);
-      if (i == j && tid < RS)  // the diagonal tile's slab owns these rows
-        args.s_out[args.row_off[i] + q * RS + tid] = fma(beta, si[tid], ri[tid]);
-    }
 
     double rs[RT];
 #pragma unroll
@@ -297,7 +311,7 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
       }
       named_bar_sync(1, CT);
       double* dst = (split_start && t == t_first)
-                        ? args.colextra + (int64_t)blockIdx.x * B
+                        ? args.colextra + (int64_t)u * B
                         : args.colmain + (t - args.tile_lo) * B;
       for (int c = tid; c < B; c += CT) {
         double acc = 0.0;
@@ -334,6 +348,19 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
       }
     }
   }
+#ifdef HS_SYMV_TIMING
+  if (tid == 0) {
+    uint64_t ts_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts_end));
+    if (g_symv_ts_print)
+      printf("symvts %d %u %lld %llu %llu\n", blockIdx.x, sm_id, (long long)ts_slabs,
+             (unsigned long long)ts_start, (unsigned long long)ts_end);
+    // per launch: min start / max end over CTAs (slot = launch sequence)
+    const unsigned slot = args.ts_seq % 4096u;
+    atomicMin(reinterpret_cast<unsigned long long*>(&g_symv_ts[slot][0]), ts_start);
+    atomicMax(reinterpret_cast<unsigned long long*>(&g_symv_ts[slot][1]), ts_end);
+  }
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -440,7 +467,7 @@ __device__ void scalar_step(int step, double val, const StepArgs& sa) {
 __device__ void dot_epilogue(double part, double* dpart, int slot, int count,
                              int step, const StepArgs& sa) {
   __shared__ double red_d[32];
-  __shared__ Dd red_dd[1024];  // up to 1024 threads (finalize)
+  __shared__ Dd red_dd[256];  // up to 256 threads (finalize, vector kernels)
   __shared__ bool last;
   const double p = block_sum(part, red_d);
   if (threadIdx.x == 0) {
@@ -473,18 +500,13 @@ __device__ void dot_epilogue(double part, double* dpart, int slot, int count,
 //           then (optionally) the dot s_j . t_j and, via a global ticket, the
 //           double-double total and the CG alpha step.
 struct FinalizeArgs {
-  const int32_t* unit_row;
-  const int32_t* unit_i0;
-  const int32_t* unit_i1;
-  const int32_t* row_unit;   // [rows+1] unit range of each output row
   const int64_t* row_rseg;   // [own rows+1] row segments
   const int32_t* row_extra;  // [rows+1] range into extra_cta
-  const int32_t* extra_cta;  // CTAs whose first (split) tile is in row j
+  const int32_t* extra_cta;  // units whose first (split) tile is in column j
   const double* rowpart;
   const double* colmain;
   const double* colextra;
-  double* upart;
-  uint32_t* row_ticket;
+  uint32_t* unit_ctr;        // SYMV work-unit counter, reset here
   const int64_t* row_off;
   int64_t row_lo, row_hi, tile_lo;
   int b;
@@ -496,46 +518,62 @@ struct FinalizeArgs {
   const int32_t* done;
 };
 
-// One CTA of FIN_THREADS per output block row j: the FIN_THREADS / b threads
-// of each column split the row's tile slots (i = i0 + p, i0 + p + P, ...),
-// then add in a fixed order (smem), plus row segments and split-tile extras;
-// fused dot s_j . t_j and, via a global ticket, the alpha step.
-constexpr int FIN_THREADS = 1024;
+// Block row j (blockIdx.x), 32 columns (blockIdx.y): out_j[c] is the sum of
+// every partial b-vector that lands on block row j -- the column partials
+// of tiles (i, j), the row segments of the units that covered row j, and the
+// split-tile extras. The FIN_WARPS warps of the CTA take the partials
+// round-robin (one coalesced 256-B load per warp per partial, 8 loads in
+// flight per thread), then warp 0 adds the per-warp sums in a fixed order:
+// deterministic. Small CTAs so the whole grid (N * b / 32 CTAs) is resident
+// in one wave. Optionally fused with the dot s_j . out_j and, via a global
+// ticket, the alpha step.
+constexpr int FIN_WARPS = 8;
+constexpr int FIN_THREADS = FIN_WARPS * 32;
+constexpr int FIN_COLS = 32;
 
 __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(FinalizeArgs fa) {
   pdl_wait();
   pdl_trigger();
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *fa.unit_ctr = 0u;
   if (fa.done && *fa.done) return;
   const int64_t jr = blockIdx.x;  // output block row
   const int b = fa.b;
-  const int P = blockDim.x / b;   // threads per column
-  const int c = threadIdx.x % b, p = threadIdx.x / b;
-  __shared__ double red[FIN_THREADS];
+  const int cl = threadIdx.x & 31, p = threadIdx.x >> 5;
+  const int c = blockIdx.y * FIN_COLS + cl;
+  __shared__ double red[FIN_WARPS][33];
+  // entries: [0, nc) column partials of tiles (i0 + e, jr); [nc, nc + nrs)
+  // row segments; then the split-tile extras
+  const int64_t i0 = jr > fa.row_lo ? jr : fa.row_lo;
+  const int64_t nc = fa.row_hi - i0;
+  const bool own = jr >= fa.row_lo && jr < fa.row_hi;
+  const int64_t rs0 = own ? fa.row_rseg[jr - fa.row_lo] : 0;
+  const int64_t nrs = own ? fa.row_rseg[jr - fa.row_lo + 1] - rs0 : 0;
+  const int e0 = fa.row_extra[jr];
+  const int64_t ne = fa.row_extra[jr + 1] - e0;
+  const int64_t E = nc + nrs + ne;
+  const double* colbase = fa.colmain - fa.tile_lo * b + c;
   double acc = 0.0;
-  if (p < P) {
-    const int64_t i0 = (jr > fa.row_lo ? jr : fa.row_lo) + p;
-    const double* base = fa.colmain - fa.tile_lo * b + c;
+  int64_t e = p;
 #pragma unroll 8
-    for (int64_t i = i0; i < fa.row_hi; i += P) acc += __ldg(base + tri(i, jr) * b);
-  }
-  red[threadIdx.x] = acc;
+  for (; e < nc; e += FIN_WARPS) acc += __ldg(colbase + tri(i0 + e, jr) * b);
+#pragma unroll 4
+  for (; e < nc + nrs; e += FIN_WARPS) acc += __ldg(fa.rowpart + (rs0 + e - nc) * b + c);
+  for (; e < E; e += FIN_WARPS)
+    acc += __ldg(fa.colextra + (int64_t)fa.extra_cta[e0 + (e - nc - nrs)] * b + c);
+  red[p][cl] = acc;
   __syncthreads();
   double dotp = 0.0;
   if (p == 0) {
     double t = 0.0;
-    for (int pp = 0; pp < P; ++pp) t += red[pp * b + c];
-    const bool own = jr >= fa.row_lo && jr < fa.row_hi;
-    if (own) {
-      const int64_t rs0 = fa.row_rseg[jr - fa.row_lo], rs1 = fa.row_rseg[jr - fa.row_lo + 1];
-      for (int64_t sg = rs0; sg < rs1; ++sg) t += fa.rowpart[sg * b + c];
-    }
-    const int e0 = fa.row_extra[jr], e1 = fa.row_extra[jr + 1];
-    for (int e = e0; e < e1; ++e) t += fa.colextra[(int64_t)fa.extra_cta[e] * b + c];
+#pragma unroll
+    for (int pp = 0; pp < FIN_WARPS; ++pp) t += red[pp][cl];
     const int64_t o = fa.row_off[jr] + c;
     fa.out[o] = t;
     if (fa.s) dotp = fa.s[o] * t;
   }
-  if (fa.s) dot_epilogue(dotp, fa.dpart, (int)jr, (int)fa.row_hi, fa.step, fa.sa);
+  if (fa.s)
+    dot_epilogue(dotp, fa.dpart, (int)(jr * gridDim.y + blockIdx.y),
+                 (int)(gridDim.x * gridDim.y), fa.step, fa.sa);
 }
 
 // ---------------------------------------------------------------------------
@@ -677,10 +715,8 @@ __global__ void combine_kernel(const Dd* slots, int64_t stride, int world, int s
 void free_plan(SymvPlan* p) {
   if (!p) return;
   for (void* q : {(void*)p->cta_slab, (void*)p->cta_rseg, (void*)p->row_rseg,
-                  (void*)p->unit_row, (void*)p->unit_i0, (void*)p->unit_i1,
-                  (void*)p->row_unit, (void*)p->row_extra, (void*)p->extra_cta,
-                  (void*)p->row_ticket, (void*)p->rowpart, (void*)p->colmain,
-                  (void*)p->colextra, (void*)p->upart})
+                  (void*)p->row_extra, (void*)p->extra_cta, (void*)p->unit_ctr,
+                  (void*)p->rowpart, (void*)p->colmain, (void*)p->colextra})
     cudaFree(q);
   delete p;
 }
@@ -711,16 +747,38 @@ void ensure_plan(hs_matrix* m) {
   const int64_t T = m->tile_hi - m->tile_lo;
   const int64_t S = T * spt;
   const int64_t lo = (int64_t)m->row_lo, hi = (int64_t)m->row_hi;
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(m->ctx->num_sms, S));
-  std::vector<int64_t> cta_slab(grid + 1), cta_rseg(grid);
-  std::vector<int64_t> row_cnt(hi - lo + 1, 0);
-  std::vector<std::vector<int32_t>> extras(hi);
-  int64_t nr = 0;
+  const int64_t sms = std::max(1, m->ctx->num_sms);
+  // Work units, claimed dynamically by the persistent CTAs in this order.
+  // Measured per-SM streaming rates differ by up to 20 % on a B200 (44-54
+  // GB/s per CTA, fixed by SM position), so a static equal split leaves the
+  // fastest CTAs idle for the last ~15 % of the launch. Guided sizes:
+  // remaining / (2 * SMs), at least kMinUnit slabs, so the final units are
+  // short (a few us) and CTAs finish together. A unit is processed exactly
+  // like a static CTA range (its own row / split-tile partial slots), so the
+  // sums do not depend on which CTA claims it.
+  constexpr int64_t kMinUnit = 8;
+  std::vector<int64_t> cta_slab;
   // slab indices are GLOBAL (the kernel derives global tile / block-row
   // indices from them): this rank's slabs start at tile_lo * spt
   const int64_t s_lo = m->tile_lo * spt;
-  for (int64_t c = 0; c <= grid; ++c) cta_slab[c] = s_lo + S * c / grid;
-  for (int64_t c = 0; c < grid; ++c) {
+  {
+    int64_t g = 0;
+    cta_slab.push_back(s_lo);
+    while (g < S) {
+      const int64_t rem = S - g;
+      const int64_t sz = std::min(rem, std::max(kMinUnit, rem / (2 * sms)));
+      g += sz;
+      cta_slab.push_back(s_lo + g);
+    }
+    if (S == 0) cta_slab.push_back(s_lo);
+  }
+  const int64_t vgrid = (int64_t)cta_slab.size() - 1;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(sms, vgrid));
+  std::vector<int64_t> cta_rseg(vgrid);
+  std::vector<int64_t> row_cnt(hi - lo + 1, 0);
+  std::vector<std::vector<int32_t>> extras(hi);
+  int64_t nr = 0;
+  for (int64_t c = 0; c < vgrid; ++c) {
     cta_rseg[c] = nr;
     const int64_t g0 = cta_slab[c], g1 = cta_slab[c + 1];
     if (g0 >= g1) continue;
@@ -737,55 +795,36 @@ void ensure_plan(hs_matrix* m) {
     for (int32_t c : extras[j]) extra_cta.push_back(c);
     row_extra[j + 1] = (int32_t)extra_cta.size();
   }
-  // finalize units: column j's local tiles i in [max(j, lo), hi), 16 per unit
-  constexpr int64_t kUnit = 16;
-  std::vector<int32_t> unit_row, unit_i0, unit_i1, row_unit(hi + 1, 0);
-  for (int64_t j = 0; j < hi; ++j) {
-    for (int64_t i = std::max(j, lo); i < hi; i += kUnit) {
-      unit_row.push_back((int32_t)j);
-      unit_i0.push_back((int32_t)i);
-      unit_i1.push_back((int32_t)std::min(hi, i + kUnit));
-    }
-    row_unit[j + 1] = (int32_t)unit_row.size();
-  }
   p->grid = (int)grid;
-  p->units = (int)unit_row.size();
+  p->vgrid = (int)vgrid;
   p->slabs_per_tile = spt;
   p->nrseg = nr;
   upload_vec(&p->cta_slab, cta_slab);
   upload_vec(&p->cta_rseg, cta_rseg);
   upload_vec(&p->row_rseg, row_rseg);
-  upload_vec(&p->unit_row, unit_row);
-  upload_vec(&p->unit_i0, unit_i0);
-  upload_vec(&p->unit_i1, unit_i1);
-  upload_vec(&p->row_unit, row_unit);
   upload_vec(&p->row_extra, row_extra);
   upload_vec(&p->extra_cta, extra_cta);
-  upload_vec(&p->row_ticket, std::vector<uint32_t>(hi, 0u));
+  upload_vec(&p->unit_ctr, std::vector<uint32_t>(1, 0u));
   HS_CUDA(cudaMalloc(&p->rowpart, std::max<int64_t>(1, nr) * b * sizeof(double)));
   HS_CUDA(cudaMalloc(&p->colmain, std::max<int64_t>(1, T) * b * sizeof(double)));
-  HS_CUDA(cudaMalloc(&p->colextra, grid * b * sizeof(double)));
-  HS_CUDA(cudaMalloc(&p->upart, std::max<int>(1, p->units) * b * sizeof(double)));
+  HS_CUDA(cudaMalloc(&p->colextra, std::max<int64_t>(1, vgrid) * b * sizeof(double)));
   m->plan = p;
 }
 
-struct SymvFuse {  // fused direction update s_out = r + beta * s
-  const double* r;
-  double* s_out;
-  const double* beta;
-};
-
 template <int B, int NCW>
 static void launch_symv_fast(hs_ctx* c, const hs_matrix* m, const double* s,
-                             const int32_t* done, const SymvFuse* fz) {
+                             const int32_t* done) {
   using Cfg = SymvCfg<B, NCW>;
   static std::atomic<uint64_t> attr{0};
   HS_CUDA(smem_attr_once(symv_slab_kernel<B, NCW>, Cfg::SMEM, attr));
   SymvPlan* p = m->plan;
-  SymvArgs a{m->d,        s,           m->d_row_off, m->tile_lo, p->cta_slab,
-             p->cta_rseg, p->rowpart, p->colmain,   p->colextra, done,
-             fz ? fz->r : nullptr, fz ? fz->s_out : nullptr,
-             fz ? fz->beta : nullptr, fz ? 1 : 0};
+  SymvArgs a{m->d,       s,           m->d_row_off, m->tile_lo,
+             p->cta_slab, p->cta_rseg, p->rowpart,   p->colmain,
+             p->colextra, done,        p->unit_ctr,  p->vgrid, 0u};
+#ifdef HS_SYMV_TIMING
+  static unsigned seq = 0;
+  a.ts_seq = seq++;
+#endif
   HS_CUDA(launch_pdl(symv_slab_kernel<B, NCW>, dim3(p->grid), dim3(Cfg::THREADS),
                      Cfg::SMEM, c->stream, a));
   HS_CUDA(cudaGetLastError());
@@ -800,12 +839,10 @@ static void ensure_dpart(hs_ctx* c, size_t count) {
 }
 
 // SYMV over the rank's tiles into `out` (padded full layout). With fuse_dot,
-// also dot(s, out) over the rows and the ALPHA step (single rank only).
-// With fz, `s` is s_old and the kernel multiplies with s = r + beta s_old
-// (written to fz->s_out); the fused dot then uses fz->s_out.
+// also dot(s, out) in the finalize and the ALPHA step (single rank), or the
+// rank's s^T t partial into the dot slots (multi-rank).
 static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
-                    bool fuse_dot, const StepArgs* sa, const int32_t* done,
-                    const SymvFuse* fz = nullptr) {
+                    bool fuse_dot, const StepArgs* sa, const int32_t* done) {
   const int b = (int)m->b;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   const bool prof = c->prof && (c->prof_counter++ % c->prof_every == 0);
@@ -841,10 +878,10 @@ static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
     return;
   }
   switch (b) {
-    case 64: launch_symv_fast<64, 8>(c, m, s, done, fz); break;
-    case 128: launch_symv_fast<128, 8>(c, m, s, done, fz); break;
-    case 256: launch_symv_fast<256, 8>(c, m, s, done, fz); break;
-    case 512: launch_symv_fast<512, 8>(c, m, s, done, fz); break;
+    case 64: launch_symv_fast<64, 8>(c, m, s, done); break;
+    case 128: launch_symv_fast<128, 8>(c, m, s, done); break;
+    case 256: launch_symv_fast<256, 8>(c, m, s, done); break;
+    case 512: launch_symv_fast<512, 8>(c, m, s, done); break;
   }
   if (prof) {
     HS_CUDA(cudaEventRecord(e1, c->stream));
@@ -853,31 +890,26 @@ static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
   }
   SymvPlan* p = m->plan;
   FinalizeArgs fa{};
-  fa.unit_row = p->unit_row;
-  fa.unit_i0 = p->unit_i0;
-  fa.unit_i1 = p->unit_i1;
-  fa.row_unit = p->row_unit;
   fa.row_rseg = p->row_rseg;
   fa.row_extra = p->row_extra;
   fa.extra_cta = p->extra_cta;
   fa.rowpart = p->rowpart;
   fa.colmain = p->colmain;
   fa.colextra = p->colextra;
-  fa.upart = p->upart;
-  fa.row_ticket = p->row_ticket;
+  fa.unit_ctr = p->unit_ctr;
   fa.row_off = m->d_row_off;
   fa.row_lo = (int64_t)m->row_lo;
   fa.row_hi = (int64_t)m->row_hi;
   fa.tile_lo = m->tile_lo;
   fa.b = b;
   fa.out = out;
-  fa.s = fuse_dot ? (fz ? fz->s_out : s) : nullptr;
+  fa.s = fuse_dot ? s : nullptr;
   fa.dpart = c->d_dpart;
   fa.step = STEP_ALPHA;
   if (sa) fa.sa = *sa;
   fa.done = done;
-  HS_CUDA(launch_pdl(finalize_kernel, dim3((unsigned)m->row_hi), dim3(FIN_THREADS / b * b), 0,
-                     c->stream, fa));
+  HS_CUDA(launch_pdl(finalize_kernel, dim3((unsigned)m->row_hi, (unsigned)(b / FIN_COLS)),
+                     dim3(FIN_THREADS), 0, c->stream, fa));
   HS_CUDA(cudaGetLastError());
   launch_count(c);
 }
@@ -896,9 +928,10 @@ static void launch_vec(hs_ctx* c, VecArgs va) {
 // ---------------------------------------------------------------------------
 // CG driver
 
+// CG vectors, carved from the context's persistent workspace (grown when a
+// call needs more, never freed per call)
 struct CgBuffers {
   double* s_full = nullptr;  // padded full layout (vec_len)
-  double* s_alt = nullptr;   // second direction buffer (fused s update)
   double* x_full = nullptr;  // padded full layout (recompute / result)
   double* t = nullptr;       // partial (vec_len) or local result (world 1)
   double* r_full = nullptr;  // multi-rank: all-gathered r chunks (+ slots)
@@ -907,19 +940,42 @@ struct CgBuffers {
   double* rhs = nullptr;     // local chunk
   double* trace = nullptr;   // device trace
   Dd* slots = nullptr;       // [world] gathered partials
-  void release() {
-    cudaFree(s_full);
-    cudaFree(s_alt);
-    cudaFree(x_full);
-    cudaFree(t);
-    cudaFree(t_loc);
-    cudaFree(r_full);
-    cudaFree(r);
-    cudaFree(rhs);
-    cudaFree(trace);
-    cudaFree(slots);
-  }
 };
+
+static void carve_cg_buffers(hs_ctx* c, CgBuffers& B, int64_t full, int64_t chunk, int world,
+                             size_t trace_n, bool dp) {
+  struct Req {
+    void** p;
+    size_t bytes;
+  };
+  const Req req[] = {
+      {(void**)&B.s_full, full * sizeof(double)},
+      {(void**)&B.x_full, full * sizeof(double)},
+      {(void**)&B.t, full * sizeof(double)},
+      {(void**)&B.r, chunk * sizeof(double)},
+      {(void**)&B.r_full, dp ? full * sizeof(double) : 0},
+      {(void**)&B.rhs, chunk * sizeof(double)},
+      {(void**)&B.slots, std::max(world, 1) * sizeof(Dd)},
+      {(void**)&B.t_loc, dp ? chunk * sizeof(double) : 0},
+      {(void**)&B.trace, 3 * trace_n * sizeof(double)},
+  };
+  auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  size_t total = 0;
+  for (const Req& q : req) total += up(q.bytes);
+  if (total > c->cg_ws_bytes) {
+    HS_CUDA(cudaStreamSynchronize(c->stream));
+    cudaFree(c->cg_ws);
+    c->cg_ws = nullptr;
+    c->cg_ws_bytes = 0;
+    HS_CUDA(cudaMalloc(&c->cg_ws, total));
+    c->cg_ws_bytes = total;
+  }
+  char* base = static_cast<char*>(c->cg_ws);
+  for (const Req& q : req) {
+    *q.p = q.bytes ? base : nullptr;
+    base += up(q.bytes);
+  }
+}
 
 static double ms_since(std::chrono::steady_clock::time_point t0) {
   return std::chrono::duration<double, std::milli>(
@@ -932,6 +988,18 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
                    const hs_cg_params* prm, double* d_x, hs_cg_stats* st,
                    double* h_trace) {
   HS_REQUIRE(prm->eps > 0.0, HS_ERR_CONFIG, "eps must be positive");
+  // HS_CG_HOST_TIMING=1: host-side phase times of this call on stderr
+  static const bool host_timing = getenv("HS_CG_HOST_TIMING") != nullptr;
+  const auto ht0 = std::chrono::steady_clock::now();
+  auto ht = [&](const char* what) {
+    if (host_timing) {
+      const auto now = std::chrono::steady_clock::now();
+      fprintf(stderr, "cg_run %-10s %9.3f ms (monotonic %.3f ms)\n", what,
+              std::chrono::duration<double, std::milli>(now - ht0).count(),
+              std::chrono::duration<double, std::milli>(now.time_since_epoch()).count());
+    }
+  };
+  ht("enter");
   ensure_plan(const_cast<hs_matrix*>(m));
   const int world = c->world, rank = c->rank;
   // distributed protocol whenever there is a communicator (also world == 1,
@@ -947,25 +1015,11 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   const size_t trace_n = prm->record_trace ? (size_t)prm->max_iters : 0;
   const bool rec_on = prm->recompute_interval > 0;
 
-  ensure_dpart(c, std::max<int64_t>(N + 1, VGRID));
+  ensure_dpart(c, std::max<int64_t>({N * b / FIN_COLS + 1, N + 1, VGRID}));
   CgBuffers B;
-  struct Guard {
-    CgBuffers* b;
-    ~Guard() { b->release(); }
-  } guard{&B};
   // single rank + fast SYMV: the direction update rides inside the SYMV
   // (double-buffered s); otherwise a separate vector kernel does it
-  const bool fuse_sdir = !dp && fast_b(m->b);
-  HS_CUDA(cudaMalloc(&B.s_full, full * sizeof(double)));
-  if (fuse_sdir) HS_CUDA(cudaMalloc(&B.s_alt, full * sizeof(double)));
-  HS_CUDA(cudaMalloc(&B.x_full, full * sizeof(double)));
-  HS_CUDA(cudaMalloc(&B.t, full * sizeof(double)));
-  HS_CUDA(cudaMalloc(&B.r, chunk * sizeof(double)));
-  if (dp) HS_CUDA(cudaMalloc(&B.r_full, full * sizeof(double)));
-  HS_CUDA(cudaMalloc(&B.rhs, chunk * sizeof(double)));
-  HS_CUDA(cudaMalloc(&B.slots, std::max(world, 1) * sizeof(Dd)));
-  if (dp) HS_CUDA(cudaMalloc(&B.t_loc, chunk * sizeof(double)));
-  if (trace_n) HS_CUDA(cudaMalloc(&B.trace, 3 * trace_n * sizeof(double)));
+  carve_cg_buffers(c, B, full, chunk, world, trace_n, dp);
   HS_CUDA(cudaMemsetAsync(B.t, 0, full * sizeof(double), c->stream));
   HS_CUDA(cudaMemsetAsync(B.r, 0, chunk * sizeof(double), c->stream));
   HS_CUDA(cudaMemsetAsync(B.rhs, 0, chunk * sizeof(double), c->stream));
@@ -1036,20 +1090,12 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   HS_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
   int pending = -1;
   CgScalars h{};
-  double* sbuf[2] = {B.s_full, B.s_alt};
+  ht("setup");
   for (uint64_t it = 1; it <= prm->max_iters; ++it) {
     c->step = (int64_t)it;
-    // line 4 (+5 fused for a single rank): t = A s, alpha = u / s^T t
+    // lines 4-5: t = A s, alpha = u / s^T t (the dot fused into the finalize)
     if (!dp) {
-      if (fuse_sdir) {
-        // s_it = r + beta s_{it-1} (line 11 of the previous iteration, with
-        // beta_0 = 0 so s_1 = r_0 = rhs), formed inside the SYMV
-        SymvFuse fz{B.r, sbuf[it & 1], &c->d_scalars->beta};
-        symv_to(c, m, sbuf[(it - 1) & 1], B.t, true, &sa, done, &fz);
-        v.s = sbuf[it & 1];
-      } else {
-        symv_to(c, m, B.s_full, B.t, true, &sa, done);
-      }
+      symv_to(c, m, B.s_full, B.t, true, &sa, done);
     } else {
       // s^T t = sum over ranks of s^T (this rank's partial t): the finalize
       // forms it on the full-length partial and writes the (hi, lo) into
@@ -1079,10 +1125,11 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
       launch_vec(c, v);
     }
     if (!dp) {
-      if (!fuse_sdir) {
-        v.mode = V_SDIR;  // line 11
-        launch_vec(c, v);
-      }
+      // line 11 as its own small kernel: forming s = r + beta s inside the
+      // next SYMV (one more staged segment per slab) measured 4 % slower per
+      // iteration under the board's power cap
+      v.mode = V_SDIR;
+      launch_vec(c, v);
     } else {
       // r chunks (+ each rank's r^T r partial in its slot) to every rank;
       // beta from the slots in rank order; s = r + beta s on the full
@@ -1113,11 +1160,13 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
       pending = slot;
     }
   }
+  ht("loop");
   cudaEventDestroy(ev[0]);
   cudaEventDestroy(ev[1]);
   HS_CUDA(cudaMemcpyAsync(&h, c->d_scalars, sizeof(CgScalars),
                           cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
+  ht("drained");
   // recomputation count is a pure function of the iteration count
   st->iterations = (uint64_t)h.iter;
   st->recomputations = rec_on ? (uint64_t)h.iter / prm->recompute_interval : 0;
@@ -1179,6 +1228,7 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   }
   HS_CUDA(cudaStreamSynchronize(c->stream));
   st->true_residual = sqrt(res2);
+  ht("exit");
 }
 
 }  // namespace hs
@@ -1305,7 +1355,8 @@ hs_status hs_true_residual(hs_ctx* c, const hs_matrix* m, const double* d_x,
     } else {
       symv_local(c, m, d_x, t);
     }
-    ensure_dpart(c, std::max<int64_t>((int64_t)m->N + 1, VGRID));
+    ensure_dpart(c, std::max<int64_t>({(int64_t)(m->N * m->b) / FIN_COLS + 1,
+                                       (int64_t)m->N + 1, VGRID}));
     HS_CUDA(cudaMemsetAsync(c->d_scalars, 0, sizeof(CgScalars), c->stream));
     VecArgs v{};
     v.len = pn;
@@ -1357,11 +1408,10 @@ hs_status hs_solve_cg_host(hs_ctx* c, size_t n, size_t b, const double* a,
   std::memset(st, 0, sizeof(*st));
   const auto t0 = std::chrono::steady_clock::now();
   hs_matrix* m = cached_matrix(c, 0, n, b);
-  double *d_rhs = nullptr, *d_x = nullptr;
   const size_t pn = (size_t)ceil_div(n, b) * b;
-  try {
-    HS_CUDA(cudaMalloc(&d_rhs, pn * sizeof(double)));
-    HS_CUDA(cudaMalloc(&d_x, pn * sizeof(double)));
+  double* d_rhs = ctx_vec(c, 0, pn);
+  double* d_x = ctx_vec(c, 1, pn);
+  {
     const auto tt = std::chrono::steady_clock::now();
     hs_status s = hs_matrix_upload(m, a);
     if (s != HS_OK) throw Failure{s, hs_last_error()};
@@ -1378,14 +1428,26 @@ hs_status hs_solve_cg_host(hs_ctx* c, size_t n, size_t b, const double* a,
     st->wall_ms = ms_since(t0);
     st->transfer_ms = xfer;
     st->compute_ms = st->wall_ms - xfer;
-  } catch (...) {
-    cudaFree(d_rhs);
-    cudaFree(d_x);
-    throw;
   }
-  cudaFree(d_rhs);
-  cudaFree(d_x);
   HS_API_END
 }
 
 }  // extern "C"
+
+#ifdef HS_SYMV_TIMING
+// debug builds only: per-launch SYMV (min CTA start, max CTA end) globaltimer
+// stamps; reset clears them and sets the per-CTA printf switch
+extern "C" int hs_debug_symv_ts(unsigned long long* out, int count, int reset, int print) {
+  if (reset) {
+    static unsigned long long init[4096][2];
+    for (int k = 0; k < 4096; ++k) {
+      init[k][0] = ~0ull;
+      init[k][1] = 0;
+    }
+    cudaMemcpyToSymbol(hs::g_symv_ts, init, sizeof(init));
+    cudaMemcpyToSymbol(hs::g_symv_ts_print, &print, sizeof(int));
+    return 0;
+  }
+  return (int)cudaMemcpyFromSymbol(out, hs::g_symv_ts, (size_t)count * 2 * sizeof(unsigned long long));
+}
+#endif

@@ -1311,18 +1311,15 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
   set_tile_kernel_attrs(b);
   alloc_inverses(m);
   m->has_inv = false;
-  CholFlag* flag = nullptr;
+  CholFlag* flag = static_cast<CholFlag*>(ctx_scratch(c));  // slot 0
   double* X[2] = {nullptr, nullptr};
-  HS_CUDA(cudaMalloc(&flag, sizeof(CholFlag)));
   struct Guard {
-    CholFlag* f;
     double** x;
     ~Guard() {
-      cudaFree(f);
       cudaFree(x[0]);
       cudaFree(x[1]);
     }
-  } guard{flag, X};
+  } guard{X};
   const int64_t panel = std::max<int64_t>(N - 1, 1);
   if (!fast) {
     HS_CUDA(cudaMalloc(&X[0], panel * bb * sizeof(double)));
@@ -1347,7 +1344,7 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
   }
   // trailing update on the INT8 tensor cores (emulated FP64) when selected
   const bool use_oz = fast && c->chol_slices > 0 && N > 1;
-  OzPanel oz;
+  OzPanel& oz = ctx_oz_panel(c);  // buffers persist across calls
   if (use_oz) oz.init(b, N, c->chol_slices, /*pairs=*/true);
 
   GemmArgs g{};
@@ -1579,8 +1576,7 @@ static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
     }
   } guard;
   const int64_t panel = std::max<int64_t>(N - 1, 1);
-  HS_CUDA(cudaMalloc(&flag, sizeof(CholFlag)));
-  guard.p.push_back(flag);
+  flag = static_cast<CholFlag*>(ctx_scratch(c));  // slot 0
   HS_CUDA(cudaMalloc(&d_rows, std::max<size_t>(rows.size(), 1) * sizeof(int32_t)));
   guard.p.push_back(d_rows);
   HS_CUDA(cudaMalloc(&d_pairs, std::max<size_t>(pairs.size(), 2) * sizeof(int32_t)));
@@ -1593,8 +1589,7 @@ static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
     HS_CUDA(cudaMalloc(&PB[k], panel * bb * sizeof(double)));
     guard.p.push_back(PB[k]);
   }
-  HS_CUDA(cudaMalloc(&d_status, 3 * sizeof(int64_t)));
-  guard.p.push_back(d_status);
+  d_status = reinterpret_cast<int64_t*>(static_cast<CholFlag*>(ctx_scratch(c)) + 1);
   if (!rows.empty())
     HS_CUDA(cudaMemcpy(d_rows, rows.data(), rows.size() * sizeof(int32_t),
                        cudaMemcpyHostToDevice));
@@ -1618,7 +1613,7 @@ static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
   // trailing update on the INT8 tensor cores when selected (slices of the
   // broadcast panel, double buffered like PB)
   const bool use_oz = c->chol_slices > 0 && N > 1;
-  OzPanel oz;
+  OzPanel& oz = ctx_oz_panel(c);  // buffers persist across calls
   if (use_oz) oz.init(b, N, c->chol_slices);
   const CUtensorMap mapLd = tile_map(Ld, b, 1);
   const CUtensorMap mapWb = tile_map(Wb, cb, f);
@@ -1759,8 +1754,7 @@ static void ensure_inverses(hs_ctx* c, hs_matrix* m) {
   const int64_t N = (int64_t)m->N;
   set_tile_kernel_attrs(b);
   alloc_inverses(m);
-  CholFlag* flag = nullptr;
-  HS_CUDA(cudaMalloc(&flag, sizeof(CholFlag)));
+  CholFlag* flag = static_cast<CholFlag*>(ctx_scratch(c)) + 2;
   HS_CUDA(cudaMemsetAsync(flag, 0, sizeof(CholFlag), c->stream));
   if (c->world > 1) {
     // block-cyclic factor: each rank inverts the diagonal tiles it owns
@@ -1783,7 +1777,6 @@ static void ensure_inverses(hs_ctx* c, hs_matrix* m) {
     comm_allreduce_max_i64(c, (int64_t*)flag, 3, c->stream);
     HS_CUDA(cudaMemcpyAsync(st, flag, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
     HS_CUDA(cudaStreamSynchronize(c->stream));
-    cudaFree(flag);
     h.status = (int32_t)st[0];
     h.col = st[1];
     h.pivot = st[2];
@@ -1803,7 +1796,6 @@ static void ensure_inverses(hs_ctx* c, hs_matrix* m) {
   CholFlag h{};
   HS_CUDA(cudaMemcpyAsync(&h, flag, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
-  cudaFree(flag);
   throw_flag(h);
   m->has_inv = true;
 }
@@ -2041,17 +2033,9 @@ hs_status hs_solve_spd_host(hs_ctx* c, size_t n, size_t b, double* a_packed,
   hs_matrix* m = cached_matrix(c, 0, n, b);
   hs_matrix* orig = cached_matrix(c, 1, n, b);
   hs_status s = HS_OK;
-  double *d_rhs = nullptr, *d_x = nullptr;
-  struct G {
-    double **r, **x;
-    ~G() {
-      cudaFree(*r);
-      cudaFree(*x);
-    }
-  } guard{&d_rhs, &d_x};
   const size_t pn = (size_t)ceil_div(n, b) * b;
-  HS_CUDA(cudaMalloc(&d_rhs, pn * sizeof(double)));
-  HS_CUDA(cudaMalloc(&d_x, pn * sizeof(double)));
+  double* d_rhs = ctx_vec(c, 0, pn);
+  double* d_x = ctx_vec(c, 1, pn);
   const auto t0 = std::chrono::steady_clock::now();
   s = hs_matrix_upload(m, a_packed);
   if (s != HS_OK) throw Failure{s, hs_last_error()};
@@ -2139,8 +2123,7 @@ hs_status hs_potf_tiles(hs_ctx* c, double* d_tiles, size_t b, size_t count,
   HS_REQUIRE(c && d_tiles && b > 0, HS_ERR_CONFIG, "bad arguments");
   HS_CUDA(cudaSetDevice(c->device));
   set_simt_tile_attrs((int)b);
-  CholFlag* flag = nullptr;
-  HS_CUDA(cudaMalloc(&flag, sizeof(CholFlag)));
+  CholFlag* flag = static_cast<CholFlag*>(ctx_scratch(c)) + 3;
   HS_CUDA(cudaMemsetAsync(flag, 0, sizeof(CholFlag), c->stream));
   potrf_tile_kernel<<<(unsigned)count, 256, potrf_smem((int)b), c->stream>>>(
       d_tiles, (int64_t)(b * b), (int)b, flag, -1);
@@ -2149,7 +2132,6 @@ hs_status hs_potf_tiles(hs_ctx* c, double* d_tiles, size_t b, size_t count,
   CholFlag h{};
   HS_CUDA(cudaMemcpyAsync(&h, flag, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
-  cudaFree(flag);
   if (first_bad_pivot) *first_bad_pivot = h.status ? h.pivot : -1;
   if (h.status)
     throw Failure{h.status,

@@ -447,6 +447,26 @@ __global__ void probe_ldg_kernel(const double2* __restrict__ src, int64_t n2, do
   if (acc == 123.456) *sink = acc;
 }
 
+void* ctx_scratch(hs_ctx* c) {
+  if (!c->scratch) {
+    HS_CUDA(cudaMalloc(&c->scratch, 256));
+    HS_CUDA(cudaMemset(c->scratch, 0, 256));
+  }
+  return c->scratch;
+}
+
+double* ctx_vec(hs_ctx* c, int slot, size_t count) {
+  if (c->vec_cap[slot] < count) {
+    HS_CUDA(cudaStreamSynchronize(c->stream));
+    cudaFree(c->vec[slot]);
+    c->vec[slot] = nullptr;
+    c->vec_cap[slot] = 0;
+    HS_CUDA(cudaMalloc(&c->vec[slot], count * sizeof(double)));
+    c->vec_cap[slot] = count;
+  }
+  return c->vec[slot];
+}
+
 hs_matrix* cached_matrix(hs_ctx* c, int slot, size_t n, size_t b) {
   hs_matrix*& m = c->cache[slot];
   if (m && (m->n != n || m->b != b)) {
@@ -608,6 +628,10 @@ void hs_ctx_destroy(hs_ctx* c) {
   for (cudaEvent_t e : c->prof_events) cudaEventDestroy(e);
   cudaFree(c->d_scalars);
   cudaFree(c->d_dpart);
+  cudaFree(c->cg_ws);
+  cudaFree(c->scratch);
+  delete c->oz_panel;
+  for (double* v : c->vec) cudaFree(v);
   cudaFreeHost(c->h_pinned);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;

@@ -35,28 +35,27 @@ struct CgScalars {
 // the packed tiles; partial row / column sums go to fixed segment slots so
 // the reduction order is deterministic.
 struct SymvPlan {
-  int grid = 0;
-  int units = 0;
+  int grid = 0;                  // persistent CTAs launched
+  int vgrid = 0;                 // work units (dynamically claimed)
   int64_t slabs_per_tile = 0;
   int64_t nrseg = 0;
   // device arrays
-  int64_t* cta_slab = nullptr;   // [grid+1] slab range per CTA
-  int64_t* cta_rseg = nullptr;   // [grid] first row segment id
+  int64_t* cta_slab = nullptr;   // [vgrid+1] slab range per work unit
+  int64_t* cta_rseg = nullptr;   // [vgrid] first row segment id
   int64_t* row_rseg = nullptr;   // [own rows+1] row segments of block row i
-  int32_t* unit_row = nullptr;   // [units] finalize stage-1 work units
-  int32_t* unit_i0 = nullptr;
-  int32_t* unit_i1 = nullptr;
-  int32_t* row_unit = nullptr;   // [row_hi+1]
   int32_t* row_extra = nullptr;  // [row_hi+1]
-  int32_t* extra_cta = nullptr;  // [grid]
-  uint32_t* row_ticket = nullptr;  // [row_hi]
+  int32_t* extra_cta = nullptr;  // [vgrid] units whose first tile is split
+  uint32_t* unit_ctr = nullptr;  // next unclaimed unit (reset by finalize)
   double* rowpart = nullptr;     // [nrseg * b]
   double* colmain = nullptr;     // [T_local * b]
-  double* colextra = nullptr;    // [grid * b]
-  double* upart = nullptr;       // [units * b]
+  double* colextra = nullptr;    // [vgrid * b]
 };
 
 }  // namespace hs
+
+namespace hs {
+struct OzPanel;
+}
 
 struct hs_ctx {
   int device = 0;
@@ -80,6 +79,17 @@ struct hs_ctx {
   // scratch
   hs::CgScalars* d_scalars = nullptr;
   double* d_dpart = nullptr;  // per-block-row dot partials
+  // CG workspace, kept across calls (a cudaMalloc / cudaFree per solve
+  // measured 0-80 ms of host stall on a loaded device)
+  void* cg_ws = nullptr;
+  size_t cg_ws_bytes = 0;
+  // small device scratch (status flags), allocated once
+  void* scratch = nullptr;
+  // vectors of the host-buffer entry points, kept across calls
+  double* vec[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t vec_cap[4] = {0, 0, 0, 0};
+  // INT8-emulation panel buffers of the Cholesky, kept across calls
+  hs::OzPanel* oz_panel = nullptr;
   size_t dpart_cap = 0;
   double* h_pinned = nullptr;  // small pinned readback buffer
   // device matrices reused by the host-buffer entry points (slot 0: the
@@ -183,12 +193,13 @@ CUtensorMap make_tensor_map(CUtensorMapDataType type, const void* base, int rank
 struct OzPanel {
   int b = 0, s = 0;
   int64_t rows = 0;                       // panel rows per buffer ((N-1) b)
+  size_t cap_s = 0, cap_sj = 0, cap_e = 0;  // allocated bytes (reused across calls)
   int8_t* S[2] = {nullptr, nullptr};     // [slice][row][K] planes, single column
   int32_t* E[2] = {nullptr, nullptr};    // row exponents
   int8_t* SJ[2] = {nullptr, nullptr};    // column pairs: K = 2b, joint exponents
   int32_t* EJ[2] = {nullptr, nullptr};
   ~OzPanel();
-  void init(int b, int64_t N, int s, bool pairs = false);
+  void init(int b, int64_t N, int s, bool pairs = false);  // reuses big-enough buffers
   void slice(hs_ctx* c, cudaStream_t st, const double* A, int64_t tile_lo, int64_t N,
              int64_t j, const int32_t* status);
   void update(hs_ctx* c, cudaStream_t st, double* A, int64_t tile_lo, int64_t local_tiles,
@@ -202,5 +213,11 @@ struct OzPanel {
   void update_list(hs_ctx* c, cudaStream_t st, double* A, const int64_t* lpos, int64_t j,
                    const int32_t* pairs, int64_t npairs, const int32_t* status);
 };
+
+// the context's persistent OzPanel / device scratch (lazily allocated)
+OzPanel& ctx_oz_panel(hs_ctx* c);
+void* ctx_scratch(hs_ctx* c);
+// device vector `slot` (0..3) of at least `count` doubles, kept across calls
+double* ctx_vec(hs_ctx* c, int slot, size_t count);
 
 }  // namespace hs

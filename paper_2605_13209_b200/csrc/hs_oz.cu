@@ -602,14 +602,38 @@ void OzPanel::init(int b_, int64_t N_, int s_, bool pairs) {
   b = b_;
   s = s_;
   rows = std::max<int64_t>(N_ - 1, 1) * b;
+  // buffers are kept across factorizations (a cudaMalloc / cudaFree of the
+  // ~0.8 GB at n = 32768 per call cost tens of ms): grow only
+  const size_t need_s = (size_t)rows * b * oz::MAXS;
+  const size_t need_e = (size_t)rows * sizeof(int32_t);
+  const size_t need_sj = pairs ? (size_t)rows * 2 * b * oz::MAXS : 0;
   for (int k = 0; k < 2; ++k) {
-    HS_CUDA(cudaMalloc(&S[k], (size_t)rows * b * oz::MAXS));
-    HS_CUDA(cudaMalloc(&E[k], (size_t)rows * sizeof(int32_t)));
-    if (pairs) {
-      HS_CUDA(cudaMalloc(&SJ[k], (size_t)rows * 2 * b * oz::MAXS));
-      HS_CUDA(cudaMalloc(&EJ[k], (size_t)rows * sizeof(int32_t)));
+    if (need_s > cap_s) {
+      cudaFree(S[k]);
+      S[k] = nullptr;
+      HS_CUDA(cudaMalloc(&S[k], need_s));
+    }
+    if (need_e > cap_e) {
+      cudaFree(E[k]);
+      cudaFree(EJ[k]);
+      E[k] = EJ[k] = nullptr;
+      HS_CUDA(cudaMalloc(&E[k], need_e));
+      HS_CUDA(cudaMalloc(&EJ[k], need_e));
+    }
+    if (need_sj > cap_sj) {
+      cudaFree(SJ[k]);
+      SJ[k] = nullptr;
+      HS_CUDA(cudaMalloc(&SJ[k], need_sj));
     }
   }
+  cap_s = std::max(cap_s, need_s);
+  cap_e = std::max(cap_e, need_e);
+  cap_sj = std::max(cap_sj, need_sj);
+}
+
+OzPanel& ctx_oz_panel(hs_ctx* c) {
+  if (!c->oz_panel) c->oz_panel = new OzPanel;
+  return *c->oz_panel;
 }
 
 // Slices the panel tiles (i, j), i > j, of column j into buffer j & 1.

@@ -1,0 +1,70 @@
+"""SYMV launch timeline inside CG (debug build
+tools/libhsolve_cuda_symvtiming.so, -DHS_SYMV_TIMING): per launch the first
+CTA start / last CTA end (globaltimer), so the gaps between SYMVs (finalize,
+vector kernels, launch latency, host stalls) can be seen iteration by
+iteration."""
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2605_13209_b200 import _lib  # noqa: E402
+
+LIB = os.path.join(ROOT, "tools", "libhsolve_cuda_symvtiming.so")
+_lib.lib_path = lambda: LIB
+import torch  # noqa: E402
+
+import paper_2605_13209_b200 as hs  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
+b = int(sys.argv[2]) if len(sys.argv) > 2 else 128
+iters = int(sys.argv[3]) if len(sys.argv) > 3 else 200
+reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
+mode = sys.argv[5] if len(sys.argv) > 5 else ""
+dbg = C.CDLL(LIB)
+dbg.hs_debug_symv_ts.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
+rt = (hs.Runtime(device=0, stream=torch.cuda.current_stream().cuda_stream)
+      if "torchstream" in mode else hs.Runtime())
+m = hs.generate_spd_device(rt, n, b, seed=42)
+rhs = torch.from_numpy(hs.generate_rhs(n, b, 42).values).cuda()
+x = torch.zeros_like(rhs)
+from paper_2605_13209_b200 import hsolve as H  # noqa: E402
+y = torch.zeros_like(rhs)
+dbg.hs_debug_symv_ts(None, 0, 1, 0)
+for _ in range(20):
+    H.symv_device(rt, m, rhs.data_ptr(), y.data_ptr())
+torch.cuda.synchronize()
+buf0 = (C.c_ulonglong * (2 * 4096))()
+dbg.hs_debug_symv_ts(buf0, 4096, 0, 0)
+d0 = sorted((buf0[2 * k + 1] - buf0[2 * k]) / 1e3 for k in range(4096) if buf0[2 * k + 1])
+print(f"standalone hs_symv: {len(d0)} launches, SYMV kernel us median {d0[len(d0) // 2]:.1f} "
+      f"min {d0[0]:.1f} max {d0[-1]:.1f}")
+cfg = hs.SolverConfig(block_size=b, eps=1e-300, max_iters=iters)
+hs.solve_cg_device(rt, m, rhs.data_ptr(), x.data_ptr(), cfg)
+torch.cuda.synchronize()
+for rep in range(reps):
+    dbg.hs_debug_symv_ts(None, 0, 1, 0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    hs.solve_cg_device(rt, m, rhs.data_ptr(), x.data_ptr(), cfg)
+    e1.record()
+    e1.synchronize()
+    buf = (C.c_ulonglong * (2 * 4096))()
+    dbg.hs_debug_symv_ts(buf, 4096, 0, 0)
+    ts = [(buf[2 * k], buf[2 * k + 1]) for k in range(4096) if buf[2 * k + 1] != 0]
+    ts.sort()
+    dur = [(e - s) / 1e3 for s, e in ts]
+    gaps = [(ts[k][0] - ts[k - 1][1]) / 1e3 for k in range(1, len(ts))]
+    sd, sg = sorted(dur), sorted(gaps)
+    print(f"rep {rep}: {e0.elapsed_time(e1) / iters:.3f} ms/iter; {len(ts)} SYMV launches; "
+          f"duration us median {sd[len(sd) // 2]:.1f} max {sd[-1]:.1f}; "
+          f"gap us median {sg[len(sg) // 2]:.1f} p90 {sg[9 * len(sg) // 10]:.1f} "
+          f"max {sg[-1]:.1f}; total gap {sum(gaps) / 1e3:.2f} ms")
+    big = [(k, round(g, 1)) for k, g in enumerate(gaps) if g > 200]
+    if big:
+        print("   gaps > 200 us (launch index, us):", big[:20])
+    slow = [(k, round(d, 1)) for k, d in enumerate(dur) if d > 1.5 * sd[len(sd) // 2]]
+    if slow:
+        print("   slow SYMVs (index, us):", slow[:20])
