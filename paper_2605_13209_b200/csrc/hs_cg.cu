@@ -49,6 +49,7 @@ struct SymvCfg {
   // (TPR <= 32) or per row lane (TPR = 64)
   static constexpr int G = TPR <= 32 ? NCW : RPP;
   // 8 consumer warps (16 measured slower: more smem traffic per slab)
+  // (6 stages at b <= 128 measured no faster)
   static constexpr int NSTAGE = B == 512 ? 4 : 5;
   // slab | seg_j (B) | seg_i (RS)
   static constexpr int SEG_BYTES = (B + RS) * 8;
