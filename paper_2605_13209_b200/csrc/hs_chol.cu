@@ -590,7 +590,8 @@ __global__ void __launch_bounds__(288, 1)
   if (it.op == 0 && !it.lower) {
     // C -= acc through the TMA engine: stage -acc row-major in the (now free)
     // stage buffers, then one bulk reduce-add per 1-KB row. The L2 performs
-    // the read-modify-write; no register-held HBM round trips.
+    // the read-modify-write; no register-held HBM round trips. (Per-element
+    // red.global.add.f64 instead measured 1.4 % slower over a factorization.)
     named_bar_sync(1, 256);  // every MMA warp is done with the stage buffers
     constexpr int RS = GBM * 8 + 16;  // padded smem row stride (bytes)
     unsigned char* tile = gsm;

@@ -10,6 +10,9 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
+if os.environ.get("HS_LIB"):  # A/B against another build of the CUDA library
+    from paper_2605_13209_b200 import _lib  # noqa: E402
+    _lib.lib_path = lambda: os.environ["HS_LIB"]
 import paper_2605_13209_b200 as hs  # noqa: E402
 from paper_2605_13209_b200 import hsolve as H  # noqa: E402
 
