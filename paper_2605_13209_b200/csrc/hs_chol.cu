@@ -517,8 +517,9 @@ __global__ void __launch_bounds__(288, 1)
   const int nks = it.K / GKS;
 
   extern __shared__ __align__(1024) unsigned char gsm_raw[];
-  unsigned char* gsm = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
+  // align by offsetting the shared pointer itself (a round trip through
+  // uintptr_t would turn every operand load into a generic LD)
+  unsigned char* gsm = gsm_raw + ((1024u - (smem_u32(gsm_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(gsm + GSTAGES * G_STAGE_BYTES);
   uint64_t* empty = full + GSTAGES;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -558,6 +559,18 @@ __global__ void __launch_bounds__(288, 1)
 #pragma unroll
     for (int y = 0; y < 8; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
   const int fr = lane >> 2, fk = lane & 3;
+  // Operand addresses, hoisted: element (row, k) of a [128 x 16] 128B-swizzled
+  // box is at row*128 + ((k/2) ^ (row%8))*16 + (k%2)*8 (see swz). This
+  // thread reads rows wm*32 + x*8 + fr (A) / wn*64 + y*8 + fr (B), so
+  // row % 8 == fr, and k = 4 kk + fk. Only the XOR term depends on kk % 4;
+  // x, y and kk / 4 become immediate offsets. (The half-warps' LDS.64 carry
+  // a 2-way bank conflict in this order; a conflict-free row permutation
+  // measured no faster -- the LSU pipe is < 10 % busy.)
+  const uint32_t offA = (uint32_t)(wm * 32 + fr) * 128u + (uint32_t)(fk & 1) * 8u;
+  const uint32_t offB = (uint32_t)(wn * 64 + fr) * 128u + (uint32_t)(fk & 1) * 8u;
+  uint32_t xo[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) xo[q] = (uint32_t)(((q * 2 + (fk >> 1)) ^ fr) << 4);
 
   for (int ks = 0; ks < nks; ++ks) {
     const int st = ks % GSTAGES;
@@ -566,16 +579,14 @@ __global__ void __launch_bounds__(288, 1)
     const unsigned char* sb = sa + G_OPERAND_BYTES;
 #pragma unroll
     for (int kk = 0; kk < GKS / 4; ++kk) {
-      const int k = kk * 4 + fk;  // 0..31
-      const unsigned char* ba = sa + (k >> 4) * (G_OPERAND_BYTES / 2);
-      const unsigned char* bbp = sb + (k >> 4) * (G_OPERAND_BYTES / 2);
+      const uint32_t h = (uint32_t)((kk >> 2) * (G_OPERAND_BYTES / 2)) + xo[kk & 3];
+      const double* pa = reinterpret_cast<const double*>(sa + offA + h);
+      const double* pb = reinterpret_cast<const double*>(sb + offB + h);
       double af[4], bf[8];
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
-        af[x] = *reinterpret_cast<const double*>(ba + swz(wm * 32 + x * 8 + fr, k & 15));
+      for (int x = 0; x < 4; ++x) af[x] = pa[x * 128];  // + x * 1024 bytes
 #pragma unroll
-      for (int y = 0; y < 8; ++y)
-        bf[y] = *reinterpret_cast<const double*>(bbp + swz(wn * 64 + y * 8 + fr, k & 15));
+      for (int y = 0; y < 8; ++y) bf[y] = pb[y * 128];
 #pragma unroll
       for (int x = 0; x < 4; ++x)
 #pragma unroll

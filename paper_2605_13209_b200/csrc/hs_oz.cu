@@ -335,8 +335,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int nk = g.K / KS;
 
   extern __shared__ __align__(1024) unsigned char raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  // align by offsetting the shared pointer (a uintptr_t round trip would
+  // make the epilogue's exponent reads generic loads)
+  unsigned char* sm = raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * STAGE);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
