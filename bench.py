@@ -482,10 +482,11 @@ def run_ours(args) -> None:
         "roofline": roofline,
     }
 
-    # ---- e2e through the host-buffer C-ABI entry (rank 0 / single GPU) ----
-    if not use_dist and not args.no_e2e:
+    # ---- e2e through the host-buffer C-ABI entry (every rank; with N GPUs each
+    # rank uploads its own block rows from its pinned copy of the matrix) ----
+    if not args.no_e2e:
         host = torch.empty(packed_bytes // 8, dtype=torch.float64, pin_memory=True)
-        m.download(host.numpy())
+        m.download(host.numpy())  # this rank's tiles (all of them at N = 1)
         rhs_pin = torch.from_numpy(rhs_np.copy()).pin_memory()
         x_pin = torch.zeros_like(rhs_pin).pin_memory()
         import ctypes as C
@@ -502,23 +503,32 @@ def run_ours(args) -> None:
         # PCIe / pinned-memory bandwidth varies between calls on shared boxes)
         call_s, xfer = [], []
         for _ in range(args.e2e_reps):
+            if use_dist:
+                dist.barrier()
             t0 = time.perf_counter()
             H._check(rt._L.hs_solve_cg_host(rt.ctx, n, b, C.c_void_p(host.data_ptr()),
                                             C.c_void_p(rhs_pin.data_ptr()), C.byref(p),
                                             C.c_void_p(x_pin.data_ptr()), C.byref(ste),
                                             None))
-            call_s.append(time.perf_counter() - t0)
-            xfer.append(ste.transfer_ms)
+            t = time.perf_counter() - t0
+            tx = ste.transfer_ms
+            if use_dist:  # the job's time is the slowest rank's
+                tt = torch.tensor([t, tx], dtype=torch.float64, device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t, tx = float(tt[0]), float(tt[1])
+            call_s.append(t)
+            xfer.append(tx)
         med = statistics.median(call_s)
+        h2d = (local_bytes + rhs_np.nbytes) * world  # all ranks' uploads
         line["e2e"] = {"value": ste.iterations / med, "unit": "iters/s",
-                       "h2d_bytes_per_step": packed_bytes + rhs_np.nbytes,
-                       "d2h_bytes_per_step": rhs_np.nbytes,
+                       "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": rhs_np.nbytes * world,
                        "step": f"one hs_solve_cg_host call ({args.e2e_iters} iterations) "
-                               "from pinned host buffers; host wall clock; median of "
-                               f"{args.e2e_reps} calls",
+                               "from pinned host buffers; host wall clock (max over "
+                               f"ranks); median of {args.e2e_reps} calls",
                        "calls_ms": [round(t * 1e3, 2) for t in call_s],
                        "transfer_ms_per_step": statistics.median(xfer),
-                       "h2d_gbs": (packed_bytes + rhs_np.nbytes) / 1e9 /
+                       "h2d_gbs": (local_bytes + rhs_np.nbytes) / 1e9 /
                                   (statistics.median(xfer) * 1e-3)}
         del host
     else:
