@@ -631,6 +631,7 @@ void hs_ctx_destroy(hs_ctx* c) {
   cudaFree(c->cg_ws);
   cudaFree(c->scratch);
   delete c->oz_panel;
+  free_stager(c);
   for (double* v : c->vec) cudaFree(v);
   cudaFreeHost(c->h_pinned);
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -879,16 +880,19 @@ hs_status hs_matrix_info(const hs_matrix* m, size_t* n, size_t* b,
 }
 
 static void cyclic_copy(hs_matrix* m, double* host, bool to_device) {
+  // owned tiles, merged into runs that are contiguous on both sides
   const size_t bb = m->b * m->b;
+  std::vector<CopySeg> segs;
   for (size_t k = 0; k < m->owned.size(); ++k) {
     double* h = host + (size_t)m->owned[k] * bb;
     double* d = m->d + k * bb;
-    HS_CUDA(cudaMemcpyAsync(to_device ? (void*)d : (void*)h, to_device ? (void*)h : (void*)d,
-                            bb * sizeof(double),
-                            to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
-                            m->ctx->stream));
+    if (!segs.empty() && static_cast<char*>(segs.back().host) + segs.back().bytes == (char*)h &&
+        static_cast<char*>(segs.back().dev) + segs.back().bytes == (char*)d)
+      segs.back().bytes += bb * sizeof(double);
+    else
+      segs.push_back({d, h, bb * sizeof(double)});
   }
-  HS_CUDA(cudaStreamSynchronize(m->ctx->stream));
+  host_copy(m->ctx, segs, to_device);
 }
 
 hs_status hs_matrix_upload(hs_matrix* m, const double* host) {
@@ -900,10 +904,8 @@ hs_status hs_matrix_upload(hs_matrix* m, const double* host) {
     return HS_OK;
   }
   const size_t bytes = m->local_tiles() * m->b * m->b * sizeof(double);
-  if (bytes)
-    HS_CUDA(cudaMemcpyAsync(m->d, host + (size_t)m->tile_lo * m->b * m->b,
-                            bytes, cudaMemcpyHostToDevice, m->ctx->stream));
-  HS_CUDA(cudaStreamSynchronize(m->ctx->stream));
+  host_copy(m->ctx, {{m->d, const_cast<double*>(host) + (size_t)m->tile_lo * m->b * m->b, bytes}},
+            true);
   m->has_inv = false;
   HS_API_END
 }
@@ -916,10 +918,7 @@ hs_status hs_matrix_download(const hs_matrix* m, double* host) {
     return HS_OK;
   }
   const size_t bytes = m->local_tiles() * m->b * m->b * sizeof(double);
-  if (bytes)
-    HS_CUDA(cudaMemcpyAsync(host + (size_t)m->tile_lo * m->b * m->b, m->d,
-                            bytes, cudaMemcpyDeviceToHost, m->ctx->stream));
-  HS_CUDA(cudaStreamSynchronize(m->ctx->stream));
+  host_copy(m->ctx, {{m->d, host + (size_t)m->tile_lo * m->b * m->b, bytes}}, false);
   HS_API_END
 }
 

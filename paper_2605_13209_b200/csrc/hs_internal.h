@@ -55,6 +55,7 @@ struct SymvPlan {
 
 namespace hs {
 struct OzPanel;
+struct HostStager;
 }
 
 struct hs_ctx {
@@ -90,6 +91,8 @@ struct hs_ctx {
   size_t vec_cap[4] = {0, 0, 0, 0};
   // INT8-emulation panel buffers of the Cholesky, kept across calls
   hs::OzPanel* oz_panel = nullptr;
+  // pinned staging for pageable host buffers (hs_xfer.cu)
+  hs::HostStager* stager = nullptr;
   size_t dpart_cap = 0;
   double* h_pinned = nullptr;  // small pinned readback buffer
   // device matrices reused by the host-buffer entry points (slot 0: the
@@ -219,5 +222,15 @@ OzPanel& ctx_oz_panel(hs_ctx* c);
 void* ctx_scratch(hs_ctx* c);
 // device vector `slot` (0..3) of at least `count` doubles, kept across calls
 double* ctx_vec(hs_ctx* c, int slot, size_t count);
+// blocking host <-> device copy of a list of segments: pinned host memory
+// goes straight to the DMA engines, pageable memory through the context's
+// pinned staging threads (hs_xfer.cu)
+struct CopySeg {
+  void* dev;
+  void* host;
+  size_t bytes;
+};
+void host_copy(hs_ctx* c, const std::vector<CopySeg>& segs, bool h2d);
+void free_stager(hs_ctx* c);
 
 }  // namespace hs
