@@ -276,6 +276,24 @@ def test_factor_and_solve_match_oracle(rt, oracle, n, b):
     assert res.stats.true_residual <= 1e-10 * np.linalg.norm(rhs[:n])
 
 
+@pytest.mark.parametrize("n", [256, 512, 1024, 2048])
+def test_factor_reconstruction_acceptance_grid(rt, oracle, n):
+    # acceptance.cpp:84-110: ||A - L L^T||_F / ||A||_F <= 1e-12 over
+    # n x b in {256..2048} x {16, 32, 64, 128}; and the factors of the same
+    # matrix at different block sizes agree (test_cholesky_solver.cpp:94-113)
+    dense = {}
+    for b in (16, 32, 64, 128):
+        a = hs.BlockedSPDMatrix(n, b, oracle.generate_spd(n, b, seed=42))
+        A = a.to_dense()
+        hs.factorize(a, hs.SolverConfig(block_size=b), rt)
+        L = np.tril(a.to_dense())
+        assert np.linalg.norm(A - L @ L.T) <= 1e-12 * np.linalg.norm(A), (n, b)
+        dense[b] = (L, np.abs(A).max())
+    L16, maxa = dense[16]
+    for b in (32, 64, 128):
+        assert np.abs(dense[b][0] - L16).max() <= 1e-10 * maxa, (n, b)
+
+
 def test_factor_closed_form_and_identity(rt):
     # test_cholesky_solver.cpp:35-70
     m = hs.BlockedSPDMatrix(2, 1)
