@@ -88,6 +88,11 @@ typedef struct {
 hs_status hs_ctx_create_custom_comm(int device, void* stream, int rank, int world,
                                     const hs_comm_ops* ops, hs_ctx** out);
 void hs_ctx_destroy(hs_ctx* ctx);
+/* Release what the context keeps between calls: the device matrices cached
+ * by the host-buffer entry points (hs_solve_cg_host etc. keep the uploaded
+ * matrix), the CG workspace, the Cholesky's INT8 panel buffers and the
+ * pinned staging buffers. The next call re-creates what it needs. */
+hs_status hs_ctx_trim(hs_ctx* ctx);
 int hs_ctx_rank(const hs_ctx* ctx);
 int hs_ctx_world(const hs_ctx* ctx);
 void* hs_ctx_stream(const hs_ctx* ctx);

@@ -29,7 +29,7 @@ HS_ERR_CUDA = 100
 # Every symbol include/hs_cuda.h declares (checked by tests/test_abi.py).
 EXPORTED = [
     "hs_last_error", "hs_last_error_payload", "hs_error_kind_name",
-    "hs_ctx_create", "hs_nccl_unique_id", "hs_ctx_create_nccl", "hs_ctx_destroy",
+    "hs_ctx_create", "hs_nccl_unique_id", "hs_ctx_create_nccl", "hs_ctx_destroy", "hs_ctx_trim",
     "hs_ctx_create_custom_comm",
     "hs_ctx_rank", "hs_ctx_world", "hs_ctx_stream", "hs_ctx_kernel_launches",
     "hs_ctx_set_cholesky_gemm",
@@ -114,6 +114,7 @@ def lib():
         "hs_ctx_create_custom_comm": (C.c_int, [C.c_int, vp, C.c_int, C.c_int,
                                                 C.POINTER(CommOps), pp]),
         "hs_ctx_destroy": (None, [vp]),
+        "hs_ctx_trim": (C.c_int, [vp]),
         "hs_ctx_rank": (C.c_int, [vp]),
         "hs_ctx_world": (C.c_int, [vp]),
         "hs_ctx_stream": (vp, [vp]),

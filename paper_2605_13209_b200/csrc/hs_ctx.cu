@@ -616,6 +616,29 @@ hs_status hs_ctx_create_custom_comm(int device, void* stream, int rank, int worl
   HS_API_END
 }
 
+hs_status hs_ctx_trim(hs_ctx* c) {
+  HS_API_BEGIN
+  HS_REQUIRE(c, HS_ERR_CONFIG, "null context");
+  HS_CUDA(cudaSetDevice(c->device));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  for (hs_matrix*& m : c->cache) {
+    hs_matrix_destroy(m);
+    m = nullptr;
+  }
+  cudaFree(c->cg_ws);
+  c->cg_ws = nullptr;
+  c->cg_ws_bytes = 0;
+  delete c->oz_panel;
+  c->oz_panel = nullptr;
+  free_stager(c);
+  for (int k = 0; k < 4; ++k) {
+    cudaFree(c->vec[k]);
+    c->vec[k] = nullptr;
+    c->vec_cap[k] = 0;
+  }
+  HS_API_END
+}
+
 void hs_ctx_destroy(hs_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);

@@ -391,6 +391,10 @@ class Runtime:
         FP64 emulated on the INT8 tensor cores with that many slices."""
         _check(self._L.hs_ctx_set_cholesky_gemm(self.ctx, int(slices)))
 
+    def trim(self) -> None:
+        """Release cached device matrices / workspaces (hs_ctx_trim)."""
+        _check(self._L.hs_ctx_trim(self.ctx))
+
     def close(self) -> None:
         if getattr(self, "ctx", None):
             for m in list(getattr(self, "_matrices", ())):

@@ -446,6 +446,27 @@ def test_gemm_worked_examples(rt):
     assert c.cpu().numpy().ravel().tolist() == [3.0, 42.0, 0.0, 3.0]
 
 
+def test_ctx_trim_releases_and_recovers(oracle):
+    # hs_ctx_trim drops the cached upload, workspaces and staging buffers;
+    # the next host-buffer call rebuilds them and gives the same answer
+    rt = hs.Runtime()
+    try:
+        n, b = 1024, 128
+        a = hs.BlockedSPDMatrix(n, b, oracle.generate_spd(n, b, seed=3))
+        rhs = hs.BlockVector(n, b, oracle.generate_rhs(n, b, seed=3))
+        cfg = hs.SolverConfig(block_size=b)
+        first = hs.solve_cg(a, rhs, cfg, rt)
+        free0 = torch.cuda.mem_get_info()[0]
+        rt.trim()
+        assert torch.cuda.mem_get_info()[0] > free0  # the cached upload is gone
+        again = hs.solve_cg(a, rhs, cfg, rt)
+        assert np.array_equal(first.x.values, again.x.values)
+        rt.trim()
+        rt.trim()  # idempotent
+    finally:
+        rt.close()
+
+
 def test_kernel_launches_are_counted(rt):
     before = rt.kernel_launches()
     hs.generate_spd(256, 128, seed=1, rt=rt)
