@@ -186,6 +186,16 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
   double cacc[8];
 #pragma unroll
   for (int m = 0; m < 8; ++m) cacc[m] = 0.0;
+  // b <= 128: a thread's rows recur every tile of a block row (slab q of
+  // each tile), so it keeps its row partials in registers, racc[q][r], and
+  // the lanes of a row are reduced once per block row instead of per slab
+  constexpr bool RACC = SPT * RT <= 8;
+  constexpr int NQ = RACC ? SPT : 1;
+  double racc[NQ][RT];
+#pragma unroll
+  for (int qq = 0; qq < NQ; ++qq)
+#pragma unroll
+    for (int r = 0; r < RT; ++r) racc[qq][r] = 0.0;
   double2 sj[4];  // this thread's 8 columns of s_j, kept for the whole tile
 
   // state of the current work unit (set when its first slab arrives)
@@ -279,7 +289,14 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
 
     // row sums over the W lanes of a row in this warp; the owning lane adds
     // into yrow[rpar][h][row]
-    if (RT == 2) {
+    if (RACC) {
+#pragma unroll
+      for (int qq = 0; qq < NQ; ++qq)
+        if (qq == q) {
+#pragma unroll
+          for (int r = 0; r < RT; ++r) racc[qq][r] += rs[r];
+        }
+    } else if (RT == 2) {
       const bool hi = (cl & (W / 2)) != 0;
       const double send = hi ? rs[0] : rs[RT - 1];
       double v = (hi ? rs[RT - 1] : rs[0]) + __shfl_xor_sync(0xffffffffu, send, W / 2);
@@ -298,6 +315,21 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
 
     const bool tile_end = (q == SPT - 1) || (g + 1 == g1);
     if (tile_end) {
+      const bool row_end = (j == i && q == SPT - 1) || (g + 1 == g1);
+      if (RACC && row_end) {
+        // lanes of each row -> yrow (H == 1 here); flushed below
+#pragma unroll
+        for (int qq = 0; qq < NQ; ++qq)
+#pragma unroll
+          for (int r = 0; r < RT; ++r) {
+            double v = racc[qq][r];
+#pragma unroll
+            for (int off = W / 2; off >= 1; off >>= 1)
+              v += __shfl_xor_sync(0xffffffffu, v, off);
+            if ((cl & (W - 1)) == 0) yrow[rpar * B + qq * RS + RT * rl + r] = v;
+            racc[qq][r] = 0.0;
+          }
+      }
       // pre-reduce the row lanes that share columns inside the warp
 #pragma unroll
       for (int off = TPR; off < 32; off <<= 1)
@@ -320,7 +352,6 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
         for (int r = 0; r < G; ++r) acc += cr[r * B + c];
         dst[c] = acc;
       }
-      const bool row_end = (j == i && q == SPT - 1) || (g + 1 == g1);
       if (row_end) {
         const int64_t rseg = rseg0 + (i - i_first);
         double* yr = yrow + rpar * Cfg::H * B;
