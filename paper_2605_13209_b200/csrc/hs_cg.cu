@@ -183,19 +183,149 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
   const int h = cl / W;      // row-sharing warp index (B = 512)
   const int grp = TPR <= 32 ? warp : rl;  // colred row after the warp reduce
 
+  if constexpr (SPT <= 4) {
+    // b <= 128: units are whole tiles (ensure_plan), so the loop runs per
+    // tile with the slab index q a compile-time constant. A thread's rows
+    // recur in every tile of a block row: their partial sums stay in
+    // registers (two FMA chains, ra / rb) across the block row and the lanes
+    // of a row are reduced once per block row. Fewer instructions per byte
+    // matter here: a sustained CG loop runs under the board's power cap.
+    static_assert(RT == 2 && Cfg::H == 1 && TPR <= 32, "tiled layout");
+    double ra[SPT][RT], rb[SPT][RT], cac[8];
+#pragma unroll
+    for (int qq = 0; qq < SPT; ++qq)
+#pragma unroll
+      for (int r = 0; r < RT; ++r) ra[qq][r] = rb[qq][r] = 0.0;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) cac[m] = 0.0;
+    double2 sjt[4];
+    int cur = -1;
+    int64_t ug1 = 0, ti = 0, ii = 0, jj = 0, ifirst = 0, rsg0 = 0;
+    int tp = 0, rp = 0;
+    for (int64_t k = 0;; k += SPT) {
+      const int st0 = (int)(k % NS);
+      mbar_wait(&full[st0], (uint32_t)((k / NS) & 1));
+      const int64_t g = hdr_g[st0];
+      if (g < 0) break;
+      const int u = hdr_u[st0];
+      if (u != cur) {
+        cur = u;
+        ug1 = args.cta_slab[u + 1];
+        ti = args.cta_slab[u] / SPT;
+        ii = tile_row(ti);
+        jj = ti - tri(ii, 0);
+        ifirst = ii;
+        rsg0 = args.cta_rseg[u];
+      }
+#ifdef HS_SYMV_TIMING
+      ts_slabs += SPT;
+#endif
+      {
+        const double2* sj2 =
+            reinterpret_cast<const double2*>(stages + st0 * Cfg::STAGE_BYTES + Cfg::SLAB_BYTES);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) sjt[m] = sj2[cl + TPR * m];
+      }
+      const bool diag = ii == jj;
+#pragma unroll
+      for (int q = 0; q < SPT; ++q) {
+        const int64_t kq = k + q;
+        const int st = (int)(kq % NS);
+        if (q > 0) mbar_wait(&full[st], (uint32_t)((kq / NS) & 1));
+        const unsigned char* buf = stages + st * Cfg::STAGE_BYTES;
+        const double2* A2 = reinterpret_cast<const double2*>(buf);
+        const double2 si2 =
+            reinterpret_cast<const double2*>(buf + Cfg::SLAB_BYTES + B * 8)[rl];
+        const double sir[2] = {si2.x, si2.y};
+        double2 a[RT][4];
+#pragma unroll
+        for (int r = 0; r < RT; ++r)
+#pragma unroll
+          for (int m = 0; m < 4; ++m) a[r][m] = A2[(RT * rl + r) * (B / 2) + cl + TPR * m];
+        if (!diag) {
+#pragma unroll
+          for (int r = 0; r < RT; ++r)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+              ra[q][r] = fma(a[r][m].x, sjt[m].x, ra[q][r]);
+              rb[q][r] = fma(a[r][m].y, sjt[m].y, rb[q][r]);
+              cac[2 * m] = fma(a[r][m].x, sir[r], cac[2 * m]);
+              cac[2 * m + 1] = fma(a[r][m].y, sir[r], cac[2 * m + 1]);
+            }
+        } else {
+          // diagonal tile: lower triangle only (c <= r for rows, c < r for cols)
+#pragma unroll
+          for (int r = 0; r < RT; ++r) {
+            const int rr = q * RS + RT * rl + r;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+              const int c0 = 2 * cl + 2 * TPR * m;
+              ra[q][r] = fma(c0 <= rr ? a[r][m].x : 0.0, sjt[m].x, ra[q][r]);
+              rb[q][r] = fma(c0 + 1 <= rr ? a[r][m].y : 0.0, sjt[m].y, rb[q][r]);
+              cac[2 * m] = fma(c0 < rr ? a[r][m].x : 0.0, sir[r], cac[2 * m]);
+              cac[2 * m + 1] = fma(c0 + 1 < rr ? a[r][m].y : 0.0, sir[r], cac[2 * m + 1]);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+      }
+      // tile end: column partial of tile ti; block row end: row partials
+      const bool row_end = diag || (g + SPT == ug1);
+      if (row_end) {
+#pragma unroll
+        for (int qq = 0; qq < SPT; ++qq)
+#pragma unroll
+          for (int r = 0; r < RT; ++r) {
+            double v = ra[qq][r] + rb[qq][r];
+#pragma unroll
+            for (int off = W / 2; off >= 1; off >>= 1)
+              v += __shfl_xor_sync(0xffffffffu, v, off);
+            if ((cl & (W - 1)) == 0) yrow[rp * B + qq * RS + RT * rl + r] = v;
+            ra[qq][r] = rb[qq][r] = 0.0;
+          }
+      }
+#pragma unroll
+      for (int off = TPR; off < 32; off <<= 1)
+#pragma unroll
+        for (int m = 0; m < 8; ++m) cac[m] += __shfl_xor_sync(0xffffffffu, cac[m], off);
+      double* cr = colred + tp * G * B;
+      if (lane < TPR) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          reinterpret_cast<double2*>(cr + grp * B)[cl + TPR * m] =
+              make_double2(cac[2 * m], cac[2 * m + 1]);
+      }
+      named_bar_sync(1, CT);
+      {
+        double* dst = args.colmain + (ti - args.tile_lo) * B;
+        for (int c = tid; c < B; c += CT) {
+          double acc = 0.0;
+#pragma unroll 4
+          for (int r = 0; r < G; ++r) acc += cr[r * B + c];
+          dst[c] = acc;
+        }
+      }
+      if (row_end) {
+        double* yr = yrow + rp * B;
+        double* out = args.rowpart + (rsg0 + (ii - ifirst)) * B;
+        for (int c = tid; c < B; c += CT) out[c] = yr[c];
+        rp ^= 1;
+      }
+      tp ^= 1;
+#pragma unroll
+      for (int m = 0; m < 8; ++m) cac[m] = 0.0;
+      ++ti;
+      if (++jj > ii) {
+        ++ii;
+        jj = 0;
+      }
+    }
+  } else {
+
   double cacc[8];
 #pragma unroll
   for (int m = 0; m < 8; ++m) cacc[m] = 0.0;
-  // b <= 128: a thread's rows recur every tile of a block row (slab q of
-  // each tile), so it keeps its row partials in registers, racc[q][r], and
-  // the lanes of a row are reduced once per block row instead of per slab
-  constexpr bool RACC = SPT * RT <= 8;
-  constexpr int NQ = RACC ? SPT : 1;
-  double racc[NQ][RT];
-#pragma unroll
-  for (int qq = 0; qq < NQ; ++qq)
-#pragma unroll
-    for (int r = 0; r < RT; ++r) racc[qq][r] = 0.0;
   double2 sj[4];  // this thread's 8 columns of s_j, kept for the whole tile
 
   // state of the current work unit (set when its first slab arrives)
@@ -289,14 +419,7 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
 
     // row sums over the W lanes of a row in this warp; the owning lane adds
     // into yrow[rpar][h][row]
-    if (RACC) {
-#pragma unroll
-      for (int qq = 0; qq < NQ; ++qq)
-        if (qq == q) {
-#pragma unroll
-          for (int r = 0; r < RT; ++r) racc[qq][r] += rs[r];
-        }
-    } else if (RT == 2) {
+    if (RT == 2) {
       const bool hi = (cl & (W / 2)) != 0;
       const double send = hi ? rs[0] : rs[RT - 1];
       double v = (hi ? rs[RT - 1] : rs[0]) + __shfl_xor_sync(0xffffffffu, send, W / 2);
@@ -316,20 +439,6 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
     const bool tile_end = (q == SPT - 1) || (g + 1 == g1);
     if (tile_end) {
       const bool row_end = (j == i && q == SPT - 1) || (g + 1 == g1);
-      if (RACC && row_end) {
-        // lanes of each row -> yrow (H == 1 here); flushed below
-#pragma unroll
-        for (int qq = 0; qq < NQ; ++qq)
-#pragma unroll
-          for (int r = 0; r < RT; ++r) {
-            double v = racc[qq][r];
-#pragma unroll
-            for (int off = W / 2; off >= 1; off >>= 1)
-              v += __shfl_xor_sync(0xffffffffu, v, off);
-            if ((cl & (W - 1)) == 0) yrow[rpar * B + qq * RS + RT * rl + r] = v;
-            racc[qq][r] = 0.0;
-          }
-      }
       // pre-reduce the row lanes that share columns inside the warp
 #pragma unroll
       for (int off = TPR; off < 32; off <<= 1)
@@ -380,6 +489,7 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
       }
     }
   }
+  }  // slab-level loop (b >= 256)
 #ifdef HS_SYMV_TIMING
   if (tid == 0) {
     uint64_t ts_end;
@@ -798,7 +908,9 @@ void ensure_plan(hs_matrix* m) {
     cta_slab.push_back(s_lo);
     while (g < S) {
       const int64_t rem = S - g;
-      const int64_t sz = std::min(rem, std::max(kMinUnit, rem / (2 * sms)));
+      int64_t sz = std::min(rem, std::max(kMinUnit, rem / (2 * sms)));
+      // b <= 128: whole tiles per unit (the kernel's tile-level loop)
+      if (spt <= 4) sz = std::min(rem, (sz + spt - 1) / spt * spt);
       g += sz;
       cta_slab.push_back(s_lo + g);
     }
