@@ -130,24 +130,26 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
     // claims work units in order (one atomic per unit) and streams their
     // slabs; the header tells the consumers which slab / unit a stage holds
     if (tid == CT) {
-      int64_t k = 0;  // stages filled so far
+      // ring position (stage, phase) kept incrementally: a 64-bit % / by NS
+      // per slab cost more integer work than the rest of the producer
+      int st = 0;
+      uint32_t ph = 0;
+      bool wrapped = false;  // every stage used once: wait for its release
       for (;;) {
         const int u = (int)atomicAdd(args.unit_ctr, 1u);
-        const int st0 = (int)(k % NS);
         if (u >= args.vgrid) {
-          if (k >= NS) mbar_wait(&empty[st0], (uint32_t)(((k / NS) - 1) & 1));
-          hdr_g[st0] = -1;
-          hdr_u[st0] = -1;
-          mbar_arrive(&full[st0]);  // end of work, no bytes
+          if (wrapped) mbar_wait(&empty[st], ph ^ 1u);
+          hdr_g[st] = -1;
+          hdr_u[st] = -1;
+          mbar_arrive(&full[st]);  // end of work, no bytes
           break;
         }
         const int64_t g0 = args.cta_slab[u], g1 = args.cta_slab[u + 1];
         const int64_t t0 = g0 / SPT;
         int64_t t = t0, i = tile_row(t0), j = t0 - tri(tile_row(t0), 0);
         int q = (int)(g0 - t0 * SPT);
-        for (int64_t g = g0; g < g1; ++g, ++k) {
-          const int st = (int)(k % NS);
-          if (k >= NS) mbar_wait(&empty[st], (uint32_t)(((k / NS) - 1) & 1));
+        for (int64_t g = g0; g < g1; ++g) {
+          if (wrapped) mbar_wait(&empty[st], ph ^ 1u);
           hdr_g[st] = g;
           hdr_u[st] = u;
           unsigned char* buf = stages + st * Cfg::STAGE_BYTES;
@@ -162,6 +164,11 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
           bulk_g2s(buf + Cfg::SLAB_BYTES + B * 8, args.s + oi, RS * 8, &full[st]);
           if (seg_j)
             bulk_g2s(buf + Cfg::SLAB_BYTES, args.s + args.row_off[j], B * 8, &full[st]);
+          if (++st == NS) {
+            st = 0;
+            ph ^= 1u;
+            wrapped = true;
+          }
           if (++q == SPT) {
             q = 0;
             ++t;
@@ -202,9 +209,11 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
     int cur = -1;
     int64_t ug1 = 0, ti = 0, ii = 0, jj = 0, ifirst = 0, rsg0 = 0;
     int tp = 0, rp = 0;
-    for (int64_t k = 0;; k += SPT) {
-      const int st0 = (int)(k % NS);
-      mbar_wait(&full[st0], (uint32_t)((k / NS) & 1));
+    int st = 0;  // ring position of the tile's first slab
+    uint32_t ph = 0;
+    for (;;) {
+      const int st0 = st;
+      mbar_wait(&full[st0], ph);
       const int64_t g = hdr_g[st0];
       if (g < 0) break;
       const int u = hdr_u[st0];
@@ -229,9 +238,7 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
       const bool diag = ii == jj;
 #pragma unroll
       for (int q = 0; q < SPT; ++q) {
-        const int64_t kq = k + q;
-        const int st = (int)(kq % NS);
-        if (q > 0) mbar_wait(&full[st], (uint32_t)((kq / NS) & 1));
+        if (q > 0) mbar_wait(&full[st], ph);
         const unsigned char* buf = stages + st * Cfg::STAGE_BYTES;
         const double2* A2 = reinterpret_cast<const double2*>(buf);
         const double2 si2 =
@@ -268,7 +275,11 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
+        mbar_arrive_if(&empty[st], lane == 0);
+        if (++st == NS) {
+          st = 0;
+          ph ^= 1u;
+        }
       }
       // tile end: column partial of tile ti; block row end: row partials
       const bool row_end = diag || (g + SPT == ug1);
@@ -336,9 +347,10 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
   int q = 0;
   int tpar = 0, rpar = 0;  // parity of tiles / block rows flushed
 
-  for (int64_t k = 0;; ++k) {
-    const int st = (int)(k % NS);
-    mbar_wait(&full[st], (uint32_t)((k / NS) & 1));
+  int st = 0;  // ring position
+  uint32_t ph = 0;
+  for (;; st = (st + 1 == NS) ? 0 : st + 1, ph ^= (st == 0) ? 1u : 0u) {
+    mbar_wait(&full[st], ph);
     const int64_t g = hdr_g[st];
     if (g < 0) break;
     const int u = hdr_u[st];
@@ -415,7 +427,7 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
+    mbar_arrive_if(&empty[st], lane == 0);
 
     // row sums over the W lanes of a row in this warp; the owning lane adds
     // into yrow[rpar][h][row]

@@ -128,6 +128,15 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar,
       : "memory");
 }
 
+// arrive from the threads where `pred` holds, without a divergent branch
+__device__ __forceinline__ void mbar_arrive_if(uint64_t* bar, bool pred) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.u32 p, %1, 0; "
+      "@p mbarrier.arrive.release.cta.shared::cta.b64 _, [%0]; }" ::"r"(smem_u32(bar)),
+      "r"((uint32_t)pred)
+      : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
                    smem_u32(bar))
