@@ -94,6 +94,35 @@ def test_symv_matches_oracle(rt, oracle, n, b):
     assert np.all(y[n:] == x[n:])  # identity padding: padded rows copy x (zeros)
 
 
+@pytest.mark.parametrize("n,b", [(32768, 128), (8192, 512), (3000, 64)])
+def test_symv_bitwise_deterministic_under_dynamic_units(rt, n, b):
+    # the SYMV's work units are claimed dynamically (the CTA that processes
+    # a unit varies run to run), but every partial slot belongs to a unit and
+    # the finalize adds them in a fixed order: repeated products, and whole
+    # CG solves, must be bitwise identical
+    m = hs.generate_spd_device(rt, n, b, seed=7)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    N = (n + b - 1) // b
+    x = torch.randn(N * b, dtype=torch.float64, device="cuda", generator=g)
+    x[n:] = 0
+    ys = []
+    for _ in range(4):
+        y = torch.empty_like(x)
+        H.symv_device(rt, m, x.data_ptr(), y.data_ptr())
+        ys.append(y)
+    for y in ys[1:]:
+        assert torch.equal(y, ys[0])
+    rhs = x.clone()
+    sols = []
+    for _ in range(2):
+        out = torch.zeros_like(rhs)
+        st = hs.solve_cg_device(rt, m, rhs.data_ptr(), out.data_ptr(),
+                                hs.SolverConfig(block_size=b, eps=1e-300, max_iters=60))
+        sols.append((out, st.true_residual))
+    assert torch.equal(sols[0][0], sols[1][0]) and sols[0][1] == sols[1][1]
+    m.free()
+
+
 def test_symv_identity_and_worked_example(rt):
     # test_block_kernels.cpp:197-220
     ident = hs.BlockedSPDMatrix.identity(13, 4)
@@ -444,6 +473,27 @@ def test_gemm_worked_examples(rt):
     pp = dev(np.ones((2, 2)))
     H.gemm_update_tiles_device(rt, c.data_ptr(), pp.data_ptr(), pp.data_ptr(), 2, 1, True)
     assert c.cpu().numpy().ravel().tolist() == [3.0, 42.0, 0.0, 3.0]
+
+
+def test_pageable_staged_upload_and_download(rt, oracle):
+    # > 4 MB from pageable numpy memory takes the pinned staging threads
+    # (hs_xfer.cu) both ways; the bytes must arrive unchanged
+    n, b = 4096, 256
+    a = oracle.generate_spd(n, b, seed=11)
+    assert a.nbytes > (8 << 20)
+    m = hs.DeviceMatrix(rt, n, b).upload(a)
+    back = np.empty_like(a)
+    m.download(back)
+    assert back.tobytes() == a.tobytes()
+    # odd sizes: a piece boundary inside a tile, a short tail
+    n2, b2 = 3001, 200
+    a2 = oracle.generate_spd(n2, b2, seed=12)
+    m2 = hs.DeviceMatrix(rt, n2, b2).upload(a2)
+    back2 = np.empty_like(a2)
+    m2.download(back2)
+    assert back2.tobytes() == a2.tobytes()
+    m.free()
+    m2.free()
 
 
 def test_ctx_trim_releases_and_recovers(oracle):
