@@ -92,9 +92,6 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
   using Cfg = SymvCfg<B, NCW>;
   constexpr int RS = Cfg::RS, SPT = Cfg::SPT, TPR = Cfg::TPR, RT = Cfg::RT;
   constexpr int W = Cfg::W, NS = Cfg::NSTAGE, CT = Cfg::CT, G = Cfg::G;
-  pdl_wait();
-  pdl_trigger();
-  if (args.done && *args.done) return;
 
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* stages = smem;
@@ -124,6 +121,11 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
   }
   for (int k = tid; k < 2 * Cfg::H * B; k += blockDim.x) yrow[k] = 0.0;
   __syncthreads();
+  // the CTA-private setup above overlaps the previous kernel's tail (PDL);
+  // everything below reads its results
+  pdl_wait();
+  pdl_trigger();
+  if (args.done && *args.done) return;
 
   if (tid >= CT) {
     // ---------------- producer warp ----------------
@@ -686,10 +688,6 @@ constexpr int FIN_THREADS = FIN_WARPS * 32;
 constexpr int FIN_COLS = 32;
 
 __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(FinalizeArgs fa) {
-  pdl_wait();
-  pdl_trigger();
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *fa.unit_ctr = 0u;
-  if (fa.done && *fa.done) return;
   const int64_t jr = blockIdx.x;  // output block row
   const int b = fa.b;
   const int cl = threadIdx.x & 31, p = threadIdx.x >> 5;
@@ -706,6 +704,13 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(FinalizeArgs fa) 
   const int64_t ne = fa.row_extra[jr + 1] - e0;
   const int64_t E = nc + nrs + ne;
   const double* colbase = fa.colmain - fa.tile_lo * b + c;
+  const int64_t o = fa.row_off[jr] + c;
+  // the plan lookups above overlap the SYMV's tail (PDL); the partial slots
+  // below are its output
+  pdl_wait();
+  pdl_trigger();
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *fa.unit_ctr = 0u;
+  if (fa.done && *fa.done) return;
   double acc = 0.0;
   int64_t e = p;
 #pragma unroll 8
@@ -721,7 +726,6 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(FinalizeArgs fa) 
     double t = 0.0;
 #pragma unroll
     for (int pp = 0; pp < FIN_WARPS; ++pp) t += red[pp][cl];
-    const int64_t o = fa.row_off[jr] + c;
     fa.out[o] = t;
     if (fa.s) dotp = fa.s[o] * t;
   }
