@@ -78,7 +78,12 @@ def test_assembly_rejects_bad_variance(rt):
 
 
 @pytest.mark.parametrize("n,b", [(45, 8), (1024, 128), (1000, 64), (4096, 256), (2048, 512),
-                                 (333, 7), (96, 32), (8192, 128)])
+                                 (333, 7), (96, 32), (8192, 128),
+                                 # work-unit edge cases: one tile, fewer units
+                                 # than SMs, ragged last block row, many units
+                                 (128, 128), (64, 64), (200, 128), (1300, 128),
+                                 (12345, 128), (700, 64), (20000, 64), (1500, 256),
+                                 (5000, 512)])
 def test_symv_matches_oracle(rt, oracle, n, b):
     a = oracle.generate_spd(n, b, seed=5)
     x = oracle.generate_rhs(n, b, seed=9)
