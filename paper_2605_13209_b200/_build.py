@@ -102,5 +102,28 @@ def build(force: bool = False) -> None:
     build_cli(force)
 
 
+def build_debug_variant(macro: str, out_name: str) -> str:
+    """A diagnostic build of the CUDA library with `-D<macro>` into tools/
+    (HS_SYMV_TIMING: per-launch / per-CTA SYMV timestamps for
+    tools/symv_timing.py and tools/cg_timeline.py; HS_DIAG_TIMING: diag128
+    phase timing for tools/diag_timing.py). Never loaded by the product."""
+    objdir = os.path.join(ROOT, "build", "obj_" + macro.lower())
+    os.makedirs(objdir, exist_ok=True)
+    objs = []
+    for cu in sorted(glob.glob(os.path.join(CSRC, "*.cu"))):
+        obj = os.path.join(objdir, os.path.basename(cu) + ".o")
+        _run([NVCC, *NVCC_FLAGS, "-D" + macro, "-I", INC, "-I", CSRC, "-c", cu, "-o", obj])
+        objs.append(obj)
+    out = os.path.join(ROOT, "tools", out_name)
+    _run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+          "-Xcompiler", "-fPIC", *objs, "-o", out, "-ldl"])
+    return out
+
+
 if __name__ == "__main__":
-    build(force="--force" in sys.argv)
+    if "--symv-timing" in sys.argv:
+        build_debug_variant("HS_SYMV_TIMING", "libhsolve_cuda_symvtiming.so")
+    elif "--diag-timing" in sys.argv:
+        build_debug_variant("HS_DIAG_TIMING", "libhsolve_cuda_diagtiming.so")
+    else:
+        build(force="--force" in sys.argv)

@@ -1,5 +1,6 @@
 """SYMV launch timeline inside CG (debug build
-tools/libhsolve_cuda_symvtiming.so, -DHS_SYMV_TIMING): per launch the first
+tools/libhsolve_cuda_symvtiming.so: `python -m paper_2605_13209_b200._build
+--symv-timing`): per launch the first
 CTA start / last CTA end (globaltimer), so the gaps between SYMVs (finalize,
 vector kernels, launch latency, host stalls) can be seen iteration by
 iteration."""

@@ -1,6 +1,6 @@
 """Per-CTA start / end times of the SYMV (debug build
-tools/libhsolve_cuda_symvtiming.so, compiled with -DHS_SYMV_TIMING; the
-kernel printf's one line per CTA). Run a few CG iterations and summarise
+tools/libhsolve_cuda_symvtiming.so: `python -m paper_2605_13209_b200._build
+--symv-timing`; the kernel printf's one line per CTA). Run a few CG iterations and summarise
 each launch: spread of CTA start and end times, per-CTA bytes/time."""
 import os
 import subprocess
@@ -13,9 +13,13 @@ def run_child(n, b, iters):
     sys.path.insert(0, ROOT)
     from paper_2605_13209_b200 import _lib
     _lib.lib_path = lambda: os.path.join(ROOT, "tools", "libhsolve_cuda_symvtiming.so")
+    import ctypes as C
     import torch
     import paper_2605_13209_b200 as hs
     rt = hs.Runtime()
+    dbg = C.CDLL(_lib.lib_path())
+    dbg.hs_debug_symv_ts.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
+    dbg.hs_debug_symv_ts(None, 0, 1, 1)  # reset, per-CTA printf on
     m = hs.generate_spd_device(rt, n, b, seed=42)
     rhs = torch.from_numpy(hs.generate_rhs(n, b, 42).values).cuda()
     x = torch.zeros_like(rhs)
