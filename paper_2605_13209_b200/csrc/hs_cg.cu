@@ -648,13 +648,6 @@ __device__ void dot_epilogue(double part, double* dpart, int slot, int count,
   }
 }
 
-// Two-stage fixed-order reduction of the SYMV partial slots.
-//  stage 1: unit u = (output block row j, tiles i in [i0, i1) of column j,
-//           <= 16 tiles): sum of the tiles' column partials -> upart[u]
-//  stage 2: the last unit CTA of row j (per-row ticket) adds, in order, its
-//           row's unit partials, row segments and split-tile extras -> t_j,
-//           then (optionally) the dot s_j . t_j and, via a global ticket, the
-//           double-double total and the CG alpha step.
 struct FinalizeArgs {
   const int64_t* row_rseg;   // [own rows+1] row segments
   const int32_t* row_extra;  // [rows+1] range into extra_cta

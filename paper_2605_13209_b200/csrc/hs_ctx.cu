@@ -537,7 +537,8 @@ static void ctx_common_init(hs_ctx* c, int device, void* stream) {
   HS_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount,
                                  device));
   HS_CUDA(cudaMalloc(&c->d_scalars, sizeof(CgScalars)));
-  HS_CUDA(cudaMallocHost(&c->h_pinned, 64 * sizeof(double)));
+  // room for two CgScalars snapshots (the CG poll double-buffers them)
+  HS_CUDA(cudaMallocHost(&c->h_pinned, std::max(64 * sizeof(double), 2 * sizeof(CgScalars))));
 }
 
 hs_status hs_ctx_create(int device, void* stream, hs_ctx** out) {
