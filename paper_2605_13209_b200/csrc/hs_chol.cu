@@ -1325,17 +1325,14 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
   m->has_inv = false;
   CholFlag* flag = static_cast<CholFlag*>(ctx_scratch(c));  // slot 0
   double* X[2] = {nullptr, nullptr};
-  struct Guard {
-    double** x;
-    ~Guard() {
-      cudaFree(x[0]);
-      cudaFree(x[1]);
-    }
-  } guard{X};
   const int64_t panel = std::max<int64_t>(N - 1, 1);
-  if (!fast) {
-    HS_CUDA(cudaMalloc(&X[0], panel * bb * sizeof(double)));
-    HS_CUDA(cudaMalloc(&X[1], panel * bb * sizeof(double)));
+  if (!fast) {  // panel buffers of the SIMT path, persistent across calls
+    const size_t sz[2] = {(size_t)(panel * bb) * sizeof(double),
+                          (size_t)(panel * bb) * sizeof(double)};
+    void* ws[2];
+    ctx_workspace(c, 3, sz, 2, ws);
+    X[0] = static_cast<double*>(ws[0]);
+    X[1] = static_cast<double*>(ws[1]);
   }
   HS_CUDA(cudaMemsetAsync(flag, 0, sizeof(CholFlag), c->stream));
 
@@ -1577,31 +1574,25 @@ static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
   row_off[N] = (int64_t)rows.size();
   col_off[N] = rest_off[N] = (int64_t)pairs.size() / 2;
 
-  CholFlag* flag = nullptr;
-  int32_t *d_rows = nullptr, *d_pairs = nullptr;
-  double *Ld = nullptr, *Wb = nullptr, *PB[2] = {nullptr, nullptr};
-  int64_t* d_status = nullptr;
-  struct Guard {
-    std::vector<void*> p;
-    ~Guard() {
-      for (void* q : p) cudaFree(q);
-    }
-  } guard;
   const int64_t panel = std::max<int64_t>(N - 1, 1);
-  flag = static_cast<CholFlag*>(ctx_scratch(c));  // slot 0
-  HS_CUDA(cudaMalloc(&d_rows, std::max<size_t>(rows.size(), 1) * sizeof(int32_t)));
-  guard.p.push_back(d_rows);
-  HS_CUDA(cudaMalloc(&d_pairs, std::max<size_t>(pairs.size(), 2) * sizeof(int32_t)));
-  guard.p.push_back(d_pairs);
-  HS_CUDA(cudaMalloc(&Ld, bb * sizeof(double)));
-  guard.p.push_back(Ld);
-  HS_CUDA(cudaMalloc(&Wb, (int64_t)f * cb * cb * sizeof(double)));
-  guard.p.push_back(Wb);
-  for (int k = 0; k < 2; ++k) {
-    HS_CUDA(cudaMalloc(&PB[k], panel * bb * sizeof(double)));
-    guard.p.push_back(PB[k]);
-  }
-  d_status = reinterpret_cast<int64_t*>(static_cast<CholFlag*>(ctx_scratch(c)) + 1);
+  CholFlag* flag = static_cast<CholFlag*>(ctx_scratch(c));  // slot 0
+  int64_t* d_status = reinterpret_cast<int64_t*>(flag + 1);
+  // panel broadcast buffers and work lists from the context's persistent
+  // workspace (a per-call cudaMalloc / cudaFree of the ~250 MB at n=32768
+  // stalls the host for tens of ms)
+  const size_t sz[6] = {std::max<size_t>(rows.size(), 1) * sizeof(int32_t),
+                        std::max<size_t>(pairs.size(), 2) * sizeof(int32_t),
+                        (size_t)bb * sizeof(double),
+                        (size_t)f * cb * cb * sizeof(double),
+                        (size_t)(panel * bb) * sizeof(double),
+                        (size_t)(panel * bb) * sizeof(double)};
+  void* ws[6];
+  ctx_workspace(c, 1, sz, 6, ws);
+  int32_t* d_rows = static_cast<int32_t*>(ws[0]);
+  int32_t* d_pairs = static_cast<int32_t*>(ws[1]);
+  double* Ld = static_cast<double*>(ws[2]);
+  double* Wb = static_cast<double*>(ws[3]);
+  double* PB[2] = {static_cast<double*>(ws[4]), static_cast<double*>(ws[5])};
   if (!rows.empty())
     HS_CUDA(cudaMemcpy(d_rows, rows.data(), rows.size() * sizeof(int32_t),
                        cudaMemcpyHostToDevice));
@@ -1855,20 +1846,13 @@ static void trsv_run_dist(hs_ctx* c, hs_matrix* m, double* v, bool upper) {
     }
   }
   off[N] = (int64_t)list.size();
-  double *w = nullptr, *gath = nullptr;
-  int32_t* d_list = nullptr;
-  struct Free {
-    double **w, **g;
-    int32_t** l;
-    ~Free() {
-      cudaFree(*w);
-      cudaFree(*g);
-      cudaFree(*l);
-    }
-  } guard{&w, &gath, &d_list};
-  HS_CUDA(cudaMalloc(&w, (size_t)N * b * sizeof(double)));
-  HS_CUDA(cudaMalloc(&gath, (size_t)G * b * sizeof(double)));
-  HS_CUDA(cudaMalloc(&d_list, std::max<size_t>(list.size(), 1) * sizeof(int32_t)));
+  const size_t sz[3] = {(size_t)N * b * sizeof(double), (size_t)G * b * sizeof(double),
+                        std::max<size_t>(list.size(), 1) * sizeof(int32_t)};
+  void* ws[3];
+  ctx_workspace(c, 2, sz, 3, ws);  // persistent across calls
+  double* w = static_cast<double*>(ws[0]);
+  double* gath = static_cast<double*>(ws[1]);
+  int32_t* d_list = static_cast<int32_t*>(ws[2]);
   HS_CUDA(cudaMemcpyAsync(d_list, list.data(), list.size() * sizeof(int32_t),
                           cudaMemcpyHostToDevice, c->stream));
   HS_CUDA(cudaMemsetAsync(w, 0, (size_t)N * b * sizeof(double), c->stream));

@@ -455,6 +455,25 @@ void* ctx_scratch(hs_ctx* c) {
   return c->scratch;
 }
 
+void ctx_workspace(hs_ctx* c, int slot, const size_t* sizes, int n, void** out) {
+  auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  size_t total = 0;
+  for (int k = 0; k < n; ++k) total += up(sizes[k]);
+  if (total > c->ws_bytes[slot]) {
+    HS_CUDA(cudaDeviceSynchronize());  // the old buffer may be in use on any stream
+    cudaFree(c->ws[slot]);
+    c->ws[slot] = nullptr;
+    c->ws_bytes[slot] = 0;
+    HS_CUDA(cudaMalloc(&c->ws[slot], total));
+    c->ws_bytes[slot] = total;
+  }
+  char* p = static_cast<char*>(c->ws[slot]);
+  for (int k = 0; k < n; ++k) {
+    out[k] = p;
+    p += up(sizes[k]);
+  }
+}
+
 double* ctx_vec(hs_ctx* c, int slot, size_t count) {
   if (c->vec_cap[slot] < count) {
     HS_CUDA(cudaStreamSynchronize(c->stream));
@@ -636,6 +655,9 @@ hs_status hs_ctx_trim(hs_ctx* c) {
     cudaFree(c->vec[k]);
     c->vec[k] = nullptr;
     c->vec_cap[k] = 0;
+    cudaFree(c->ws[k]);
+    c->ws[k] = nullptr;
+    c->ws_bytes[k] = 0;
   }
   HS_API_END
 }
@@ -657,6 +679,7 @@ void hs_ctx_destroy(hs_ctx* c) {
   delete c->oz_panel;
   free_stager(c);
   for (double* v : c->vec) cudaFree(v);
+  for (void* w : c->ws) cudaFree(w);
   cudaFreeHost(c->h_pinned);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;

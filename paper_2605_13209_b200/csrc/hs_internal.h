@@ -86,6 +86,10 @@ struct hs_ctx {
   size_t cg_ws_bytes = 0;
   // small device scratch (status flags), allocated once
   void* scratch = nullptr;
+  // general workspaces kept across calls (slot 0 unused, 1: distributed
+  // Cholesky panel buffers), grown on demand
+  void* ws[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t ws_bytes[4] = {0, 0, 0, 0};
   // vectors of the host-buffer entry points, kept across calls
   double* vec[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t vec_cap[4] = {0, 0, 0, 0};
@@ -222,6 +226,9 @@ OzPanel& ctx_oz_panel(hs_ctx* c);
 void* ctx_scratch(hs_ctx* c);
 // device vector `slot` (0..3) of at least `count` doubles, kept across calls
 double* ctx_vec(hs_ctx* c, int slot, size_t count);
+// carve `n` buffers of sizes[k] bytes (256-B aligned) out of the context's
+// persistent workspace `slot`, growing it when needed
+void ctx_workspace(hs_ctx* c, int slot, const size_t* sizes, int n, void** out);
 // blocking host <-> device copy of a list of segments: pinned host memory
 // goes straight to the DMA engines, pageable memory through the context's
 // pinned staging threads (hs_xfer.cu)
