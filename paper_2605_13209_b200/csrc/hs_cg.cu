@@ -1488,14 +1488,17 @@ hs_status hs_true_residual(hs_ctx* c, const hs_matrix* m, const double* d_x,
              "multi-rank hs_true_residual needs a block-cyclic matrix (full-length x)");
   HS_CUDA(cudaSetDevice(c->device));
   const int64_t pn = (int64_t)m->N * (int64_t)m->b;
-  double* t = nullptr;
-  double* gath = nullptr;
-  HS_CUDA(cudaMalloc(&t, pn * sizeof(double)));
-  try {
+  // scratch from the context's persistent workspace 0
+  const size_t sz[2] = {(size_t)pn * sizeof(double),
+                        c->world > 1 ? (size_t)pn * c->world * sizeof(double) : 0};
+  void* ws[2];
+  ctx_workspace(c, 0, sz, 2, ws);
+  double* t = static_cast<double*>(ws[0]);
+  double* gath = static_cast<double*>(ws[1]);
+  {
     if (c->world > 1) {
       // every rank: its owned tiles' share of A x; all-gather; rank-order sum
       const int b = (int)m->b;
-      HS_CUDA(cudaMalloc(&gath, pn * c->world * sizeof(double)));
       cyclic_partial_symv_kernel<<<dim3((b + 31) / 32, (unsigned)m->N), 256, 0, c->stream>>>(
           m->d, m->d_lpos, d_x, t, b, (int64_t)m->N);
       HS_CUDA(cudaGetLastError());
@@ -1526,13 +1529,7 @@ hs_status hs_true_residual(hs_ctx* c, const hs_matrix* m, const double* d_x,
     Dd acc{0.0, 0.0};
     for (double p : parts) acc = dd_add(acc, p);
     *out = sqrt(dd_value(acc));
-  } catch (...) {
-    cudaFree(t);
-    cudaFree(gath);
-    throw;
   }
-  cudaFree(t);
-  cudaFree(gath);
   HS_API_END
 }
 

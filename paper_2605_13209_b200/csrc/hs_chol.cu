@@ -2063,22 +2063,12 @@ hs_status hs_forward_substitute_host(hs_ctx* c, size_t n, size_t b,
   HS_API_BEGIN
   HS_REQUIRE(c && l && rhs && y, HS_ERR_CONFIG, "null pointer");
   HS_CUDA(cudaSetDevice(c->device));
-  hs_matrix* m = nullptr;
-  hs_status s = hs_matrix_create(c, n, b, &m);
-  if (s != HS_OK) throw Failure{s, hs_last_error()};
-  double* d_v = nullptr;
-  struct G {
-    hs_matrix* m;
-    double** v;
-    ~G() {
-      hs_matrix_destroy(m);
-      cudaFree(*v);
-    }
-  } guard{m, &d_v};
-  s = hs_matrix_upload(m, l);
+  // the context's cached device matrix and vector (kept across calls)
+  hs_matrix* m = cached_matrix(c, 0, n, b);
+  const hs_status s = hs_matrix_upload(m, l);
   if (s != HS_OK) throw Failure{s, hs_last_error()};
   const size_t pn = (size_t)ceil_div(n, b) * b;
-  HS_CUDA(cudaMalloc(&d_v, pn * sizeof(double)));
+  double* d_v = ctx_vec(c, 2, pn);
   HS_CUDA(cudaMemcpy(d_v, rhs, pn * sizeof(double), cudaMemcpyHostToDevice));
   trsv_run(c, m, d_v, false);
   HS_CUDA(cudaMemcpy(y, d_v, pn * sizeof(double), cudaMemcpyDeviceToHost));
@@ -2091,22 +2081,12 @@ hs_status hs_back_substitute_host(hs_ctx* c, size_t n, size_t b,
   HS_API_BEGIN
   HS_REQUIRE(c && l && yv && x, HS_ERR_CONFIG, "null pointer");
   HS_CUDA(cudaSetDevice(c->device));
-  hs_matrix* m = nullptr;
-  hs_status s = hs_matrix_create(c, n, b, &m);
-  if (s != HS_OK) throw Failure{s, hs_last_error()};
-  double* d_v = nullptr;
-  struct G {
-    hs_matrix* m;
-    double** v;
-    ~G() {
-      hs_matrix_destroy(m);
-      cudaFree(*v);
-    }
-  } guard{m, &d_v};
-  s = hs_matrix_upload(m, l);
+  // the context's cached device matrix and vector (kept across calls)
+  hs_matrix* m = cached_matrix(c, 0, n, b);
+  const hs_status s = hs_matrix_upload(m, l);
   if (s != HS_OK) throw Failure{s, hs_last_error()};
   const size_t pn = (size_t)ceil_div(n, b) * b;
-  HS_CUDA(cudaMalloc(&d_v, pn * sizeof(double)));
+  double* d_v = ctx_vec(c, 2, pn);
   HS_CUDA(cudaMemcpy(d_v, yv, pn * sizeof(double), cudaMemcpyHostToDevice));
   trsv_run(c, m, d_v, true);
   HS_CUDA(cudaMemcpy(x, d_v, pn * sizeof(double), cudaMemcpyDeviceToHost));

@@ -86,8 +86,8 @@ struct hs_ctx {
   size_t cg_ws_bytes = 0;
   // small device scratch (status flags), allocated once
   void* scratch = nullptr;
-  // general workspaces kept across calls (slot 0 unused, 1: distributed
-  // Cholesky panel buffers), grown on demand
+  // general workspaces kept across calls, grown on demand: 0 true residual,
+  // 1 distributed Cholesky panels, 2 distributed substitutions, 3 SIMT panels
   void* ws[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t ws_bytes[4] = {0, 0, 0, 0};
   // vectors of the host-buffer entry points, kept across calls
