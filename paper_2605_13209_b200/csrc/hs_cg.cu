@@ -83,6 +83,9 @@ struct SymvArgs {
 
 #ifdef HS_SYMV_TIMING
 __device__ unsigned long long g_symv_ts[4096][2];
+// finalize per launch: [0] min CTA start (after the PDL wait), [1] max end of
+// the partial-slot sums, [2] max CTA end (incl. the dot epilogue)
+__device__ unsigned long long g_fin_ts[4096][5];  // + [3] max start, [4] max sums time
 __device__ int g_symv_ts_print = 0;
 #endif
 
@@ -656,6 +659,7 @@ struct FinalizeArgs {
   const double* colmain;
   const double* colextra;
   uint32_t* unit_ctr;        // SYMV work-unit counter, reset here
+  unsigned ts_seq;           // launch sequence (HS_SYMV_TIMING builds only)
   const int64_t* row_off;
   int64_t row_lo, row_hi, tile_lo;
   int b;
@@ -680,7 +684,8 @@ constexpr int FIN_WARPS = 8;
 constexpr int FIN_THREADS = FIN_WARPS * 32;
 constexpr int FIN_COLS = 32;
 
-__global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(FinalizeArgs fa) {
+// (8 CTAs per SM: the whole N * b / 32 grid must be resident in one wave)
+__global__ void __launch_bounds__(FIN_THREADS, 8) finalize_kernel(FinalizeArgs fa) {
   const int64_t jr = blockIdx.x;  // output block row
   const int b = fa.b;
   const int cl = threadIdx.x & 31, p = threadIdx.x >> 5;
@@ -702,11 +707,25 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(FinalizeArgs fa) 
   // below are its output
   pdl_wait();
   pdl_trigger();
+#ifdef HS_SYMV_TIMING
+  unsigned long long ft0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ft0));
+#endif
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *fa.unit_ctr = 0u;
   if (fa.done && *fa.done) return;
+  // entries e = p, p + FIN_WARPS, ... added in that order. The column
+  // partials (a heavy row has ~N of them) are loaded 8 at a time before the
+  // adds, so the loads overlap instead of forming a serial chain (the plain
+  // `acc += load` loop measured 18 us for the heaviest row)
   double acc = 0.0;
   int64_t e = p;
-#pragma unroll 8
+  for (; e + 7 * FIN_WARPS < nc; e += 8 * FIN_WARPS) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(colbase + tri(i0 + e + u * FIN_WARPS, jr) * b);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u];
+  }
   for (; e < nc; e += FIN_WARPS) acc += __ldg(colbase + tri(i0 + e, jr) * b);
 #pragma unroll 4
   for (; e < nc + nrs; e += FIN_WARPS) acc += __ldg(fa.rowpart + (rs0 + e - nc) * b + c);
@@ -722,9 +741,25 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(FinalizeArgs fa) 
     fa.out[o] = t;
     if (fa.s) dotp = fa.s[o] * t;
   }
+#ifdef HS_SYMV_TIMING
+  unsigned long long ft1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ft1));
+#endif
   if (fa.s)
     dot_epilogue(dotp, fa.dpart, (int)(jr * gridDim.y + blockIdx.y),
                  (int)(gridDim.x * gridDim.y), fa.step, fa.sa);
+#ifdef HS_SYMV_TIMING
+  if (threadIdx.x == 0) {
+    unsigned long long ft2;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ft2));
+    const unsigned sl = fa.ts_seq % 4096u;
+    atomicMin(&g_fin_ts[sl][0], ft0);
+    atomicMax(&g_fin_ts[sl][1], ft1);
+    atomicMax(&g_fin_ts[sl][2], ft2);
+    atomicMax(&g_fin_ts[sl][3], ft0);
+    atomicMax(&g_fin_ts[sl][4], ft1 - ft0);
+  }
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -1050,6 +1085,10 @@ static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
   fa.colmain = p->colmain;
   fa.colextra = p->colextra;
   fa.unit_ctr = p->unit_ctr;
+#ifdef HS_SYMV_TIMING
+  static unsigned fseq = 0;
+  fa.ts_seq = fseq++;
+#endif
   fa.row_off = m->d_row_off;
   fa.row_lo = (int64_t)m->row_lo;
   fa.row_hi = (int64_t)m->row_hi;
@@ -1587,6 +1626,16 @@ hs_status hs_solve_cg_host(hs_ctx* c, size_t n, size_t b, const double* a,
 #ifdef HS_SYMV_TIMING
 // debug builds only: per-launch SYMV (min CTA start, max CTA end) globaltimer
 // stamps; reset clears them and sets the per-CTA printf switch
+extern "C" int hs_debug_fin_ts(unsigned long long* out, int count, int reset) {
+  if (reset) {
+    static unsigned long long init[4096][5];
+    for (int k = 0; k < 4096; ++k)
+      init[k][0] = ~0ull, init[k][1] = init[k][2] = init[k][3] = init[k][4] = 0;
+    return (int)cudaMemcpyToSymbol(hs::g_fin_ts, init, sizeof(init));
+  }
+  return (int)cudaMemcpyFromSymbol(out, hs::g_fin_ts, (size_t)count * 5 * sizeof(unsigned long long));
+}
+
 extern "C" int hs_debug_symv_ts(unsigned long long* out, int count, int reset, int print) {
   if (reset) {
     static unsigned long long init[4096][2];

@@ -25,6 +25,7 @@ reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 mode = sys.argv[5] if len(sys.argv) > 5 else ""
 dbg = C.CDLL(LIB)
 dbg.hs_debug_symv_ts.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
+dbg.hs_debug_fin_ts.argtypes = [C.c_void_p, C.c_int, C.c_int]
 rt = (hs.Runtime(device=0, stream=torch.cuda.current_stream().cuda_stream)
       if "torchstream" in mode else hs.Runtime())
 m = hs.generate_spd_device(rt, n, b, seed=42)
@@ -46,6 +47,7 @@ hs.solve_cg_device(rt, m, rhs.data_ptr(), x.data_ptr(), cfg)
 torch.cuda.synchronize()
 for rep in range(reps):
     dbg.hs_debug_symv_ts(None, 0, 1, 0)
+    dbg.hs_debug_fin_ts(None, 0, 1)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -54,6 +56,10 @@ for rep in range(reps):
     e1.synchronize()
     buf = (C.c_ulonglong * (2 * 4096))()
     dbg.hs_debug_symv_ts(buf, 4096, 0, 0)
+    fb = (C.c_ulonglong * (5 * 4096))()
+    dbg.hs_debug_fin_ts(fb, 4096, 0)
+    fin = sorted(tuple(fb[5 * k + i] for i in range(5)) for k in range(4096)
+                 if fb[5 * k + 2] != 0)
     ts = [(buf[2 * k], buf[2 * k + 1]) for k in range(4096) if buf[2 * k + 1] != 0]
     ts.sort()
     dur = [(e - s) / 1e3 for s, e in ts]
@@ -63,6 +69,21 @@ for rep in range(reps):
           f"duration us median {sd[len(sd) // 2]:.1f} max {sd[-1]:.1f}; "
           f"gap us median {sg[len(sg) // 2]:.1f} p90 {sg[9 * len(sg) // 10]:.1f} "
           f"max {sg[-1]:.1f}; total gap {sum(gaps) / 1e3:.2f} ms")
+    # per iteration: SYMV end -> finalize start, finalize sums, dot epilogue,
+    # finalize end -> next SYMV start (the two vector kernels + launch gaps)
+    br = []
+    for k in range(len(ts) - 1):
+        s_end, nxt = ts[k][1], ts[k + 1][0]
+        f = [x for x in fin if s_end <= x[0] < nxt]
+        if f:
+            f0, f1, f2, f3, f4 = f[0]
+            br.append(((f0 - s_end) / 1e3, (f1 - f0) / 1e3, (f2 - f1) / 1e3, (nxt - f2) / 1e3,
+                       (f3 - f0) / 1e3, f4 / 1e3))
+    if br:
+        med = [sorted(x[i] for x in br)[len(br) // 2] for i in range(6)]
+        print("   gap breakdown us (median): SYMV end->finalize start %.1f, sums %.1f, "
+              "dot epilogue %.1f, finalize end->next SYMV %.1f; CTA start spread %.1f, "
+              "longest CTA sums %.1f" % tuple(med))
     big = [(k, round(g, 1)) for k, g in enumerate(gaps) if g > 200]
     if big:
         print("   gaps > 200 us (launch index, us):", big[:20])
