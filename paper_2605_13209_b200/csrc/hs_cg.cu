@@ -135,6 +135,9 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
     // claims work units in order (one atomic per unit) and streams their
     // slabs; the header tells the consumers which slab / unit a stage holds
     if (tid == CT) {
+      // A is streamed once per launch: evict-first, so the partial slots the
+      // finalize reads next stay in L2
+      const uint64_t stream_pol = l2_policy_evict_first();
       // ring position (stage, phase) kept incrementally: a 64-bit % / by NS
       // per slab cost more integer work than the rest of the producer
       int st = 0;
@@ -165,7 +168,7 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
           const double* src =
               args.a + ((t - args.tile_lo) * B + (int64_t)q * RS) * B;
           const int64_t oi = args.row_off[i] + q * RS;
-          bulk_g2s(buf, src, Cfg::SLAB_BYTES, &full[st]);
+          bulk_g2s_hint(buf, src, Cfg::SLAB_BYTES, &full[st], stream_pol);
           bulk_g2s(buf + Cfg::SLAB_BYTES + B * 8, args.s + oi, RS * 8, &full[st]);
           if (seg_j)
             bulk_g2s(buf + Cfg::SLAB_BYTES, args.s + args.row_off[j], B * 8, &full[st]);
@@ -190,6 +193,8 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
 
   // ---------------- consumer warps ----------------
   const int lane = tid & 31, warp = tid >> 5;
+  // the partial slots are read by the finalize right after: keep them in L2
+  const uint64_t keep_pol = l2_policy_evict_last();
   const int cl = tid % TPR;  // column lane: columns 2cl + 2TPR*m (+1)
   const int rl = tid / TPR;  // row lane: slab rows RT*rl + r
   const int h = cl / W;      // row-sharing warp index (B = 512)
@@ -319,13 +324,13 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
           double acc = 0.0;
 #pragma unroll 4
           for (int r = 0; r < G; ++r) acc += cr[r * B + c];
-          dst[c] = acc;
+          st_hint(dst + c, acc, keep_pol);
         }
       }
       if (row_end) {
         double* yr = yrow + rp * B;
         double* out = args.rowpart + (rsg0 + (ii - ifirst)) * B;
-        for (int c = tid; c < B; c += CT) out[c] = yr[c];
+        for (int c = tid; c < B; c += CT) st_hint(out + c, yr[c], keep_pol);
         rp ^= 1;
       }
       tp ^= 1;
@@ -476,7 +481,7 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
         double acc = 0.0;
 #pragma unroll 4
         for (int r = 0; r < G; ++r) acc += cr[r * B + c];
-        dst[c] = acc;
+        st_hint(dst + c, acc, keep_pol);
       }
       if (row_end) {
         const int64_t rseg = rseg0 + (i - i_first);
@@ -489,7 +494,7 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
             acc += yr[hh * B + c];
             yr[hh * B + c] = 0.0;
           }
-          args.rowpart[rseg * B + c] = acc;
+          st_hint(args.rowpart + rseg * B + c, acc, keep_pol);
         }
         rpar ^= 1;
       }
