@@ -671,6 +671,7 @@ struct FinalizeArgs {
   double* out;         // padded layout
   const double* s;     // for the fused dot (padded layout) or null
   double* dpart;
+  double* apart;       // deferred alpha: per-CTA s.t partials only (see V_UPDATE)
   int step;
   StepArgs sa;
   const int32_t* done;
@@ -750,9 +751,16 @@ __global__ void __launch_bounds__(FIN_THREADS, 8) finalize_kernel(FinalizeArgs f
   unsigned long long ft1;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ft1));
 #endif
-  if (fa.s)
+  if (fa.apart) {
+    // deferred alpha: the per-CTA partial only; the next vector kernel's
+    // CTAs reduce the partials themselves (no ticket, no last-CTA tail)
+    __shared__ double red_d[32];
+    const double pt = block_sum(dotp, red_d);
+    if (threadIdx.x == 0) fa.apart[jr * gridDim.y + blockIdx.y] = pt;
+  } else if (fa.s) {
     dot_epilogue(dotp, fa.dpart, (int)(jr * gridDim.y + blockIdx.y),
                  (int)(gridDim.x * gridDim.y), fa.step, fa.sa);
+  }
 #ifdef HS_SYMV_TIMING
   if (threadIdx.x == 0) {
     unsigned long long ft2;
@@ -818,6 +826,10 @@ struct VecArgs {
   StepArgs sa;
   const int32_t* done;
   int mode;
+  // V_UPDATE with a deferred alpha: the finalize's per-CTA s.t partials
+  // (reduced here by every CTA in the finalize's fixed order)
+  const double* apart = nullptr;
+  int acount = 0;
 };
 
 enum VecMode : int {
@@ -834,8 +846,19 @@ __global__ void __launch_bounds__(VBLOCK) vec_kernel(VecArgs va) {
   pdl_wait();
   pdl_trigger();
   if (va.mode != V_INIT && va.mode != V_RESNORM && va.done && *va.done) return;
-  const double alpha = va.sa.sc->alpha;
+  double alpha = va.sa.sc->alpha;
   const double beta = va.sa.sc->beta;
+  if (va.apart) {
+    // alpha = u / s^T t from the finalize's partials: every CTA computes the
+    // same double-double sum (same order and tree shape as the finalize's
+    // own last-CTA reduction); CTA 0 keeps the books (alpha, non-finite ->
+    // done / status). A non-finite alpha skips the update, as `done` would.
+    __shared__ Dd red_a[VBLOCK];
+    const double st = dd_value(dd_reduce_parts(va.apart, va.acount, red_a));
+    alpha = va.sa.sc->u / st;
+    if (blockIdx.x == 0 && threadIdx.x == 0) scalar_step(STEP_ALPHA, st, va.sa);
+    if (!isfinite(alpha)) return;
+  }
   double part = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < va.len;
@@ -1035,7 +1058,8 @@ static void ensure_dpart(hs_ctx* c, size_t count) {
 // also dot(s, out) in the finalize and the ALPHA step (single rank), or the
 // rank's s^T t partial into the dot slots (multi-rank).
 static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
-                    bool fuse_dot, const StepArgs* sa, const int32_t* done) {
+                    bool fuse_dot, const StepArgs* sa, const int32_t* done,
+                    double* defer_alpha = nullptr) {
   const int b = (int)m->b;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   const bool prof = c->prof && (c->prof_counter++ % c->prof_every == 0);
@@ -1102,6 +1126,7 @@ static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
   fa.out = out;
   fa.s = fuse_dot ? s : nullptr;
   fa.dpart = c->d_dpart;
+  fa.apart = fuse_dot ? defer_alpha : nullptr;
   fa.step = STEP_ALPHA;
   if (sa) fa.sa = *sa;
   fa.done = done;
@@ -1212,7 +1237,11 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   const size_t trace_n = prm->record_trace ? (size_t)prm->max_iters : 0;
   const bool rec_on = prm->recompute_interval > 0;
 
-  ensure_dpart(c, std::max<int64_t>({N * b / FIN_COLS + 1, N + 1, VGRID}));
+  // finalize / vector partials, and (after VGRID + 8) the deferred-alpha
+  // partials of the single-rank iteration
+  ensure_dpart(c, std::max<int64_t>({N * b / FIN_COLS + VGRID + 8, N + 1, VGRID}));
+  double* apart = c->d_dpart + VGRID + 8;
+  const int acount = (int)(N * b / FIN_COLS);
   CgBuffers B;
   // single rank + fast SYMV: the direction update rides inside the SYMV
   // (double-buffered s); otherwise a separate vector kernel does it
@@ -1290,9 +1319,13 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   ht("setup");
   for (uint64_t it = 1; it <= prm->max_iters; ++it) {
     c->step = (int64_t)it;
+    const bool recompute = rec_on && (it % prm->recompute_interval == 0);
+    // single rank, fast b, plain iteration: alpha is reduced by the update
+    // kernel itself from the finalize's partials (no last-CTA tail)
+    const bool defer = !dp && fast_b(m->b) && !recompute;
     // lines 4-5: t = A s, alpha = u / s^T t (the dot fused into the finalize)
     if (!dp) {
-      symv_to(c, m, B.s_full, B.t, true, &sa, done);
+      symv_to(c, m, B.s_full, B.t, true, &sa, done, defer ? apart : nullptr);
     } else {
       // s^T t = sum over ranks of s^T (this rank's partial t): the finalize
       // forms it on the full-length partial and writes the (hi, lo) into
@@ -1307,7 +1340,6 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
       HS_CUDA(cudaGetLastError());
       launch_count(c);
     }
-    const bool recompute = rec_on && (it % prm->recompute_interval == 0);
     if (recompute) {
       // x += alpha s; r = rhs - A x (cg_solver.cpp:277-298)
       v.mode = V_AXPY_X;
@@ -1318,8 +1350,13 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
       v.mode = V_RESIDUAL;
       launch_vec(c, v);
     } else {
-      v.mode = V_UPDATE;  // lines 6-7 + u = r^T r + beta
-      launch_vec(c, v);
+      VecArgs vu = v;
+      vu.mode = V_UPDATE;  // lines 6-7 + u = r^T r + beta
+      if (defer) {
+        vu.apart = apart;
+        vu.acount = acount;
+      }
+      launch_vec(c, vu);
     }
     if (!dp) {
       // line 11 as its own small kernel: forming s = r + beta s inside the
