@@ -675,6 +675,12 @@ struct FinalizeArgs {
   int step;
   StepArgs sa;
   const int32_t* done;
+  // L2 prefetch of the next SYMV's first slabs (see finalize_kernel)
+  const unsigned char* pf_base;  // local tiles (bytes)
+  const int64_t* pf_slab;        // the plan's cta_slab
+  int64_t pf_slab_lo;            // global index of the first local slab
+  int pf_units;                  // units claimed first (one per SYMV CTA)
+  int pf_slabs;                  // slabs prefetched per unit (0: off)
 };
 
 // Block row j (blockIdx.x), 32 columns (blockIdx.y): out_j[c] is the sum of
@@ -719,6 +725,19 @@ __global__ void __launch_bounds__(FIN_THREADS, 8) finalize_kernel(FinalizeArgs f
 #endif
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *fa.unit_ctr = 0u;
   if (fa.done && *fa.done) return;
+  {
+    // HBM is nearly idle from here to the next SYMV (the partial slots below
+    // are L2 hits): prefetch into L2 the first slabs of the units the next
+    // SYMV's CTAs claim first (units 0 .. grid-1; A is constant over the
+    // solve), so its ramp-up reads hit L2 instead of waiting on HBM
+    const int lin = (int)(blockIdx.x * gridDim.y + blockIdx.y);
+    if (lin < fa.pf_units && threadIdx.x == 0) {
+      const int64_t g0 = fa.pf_slab[lin], g1 = fa.pf_slab[lin + 1];
+      const int64_t ns = g1 - g0 < fa.pf_slabs ? g1 - g0 : fa.pf_slabs;
+      if (ns > 0)
+        bulk_prefetch_l2(fa.pf_base + (g0 - fa.pf_slab_lo) * 32768, (uint32_t)(ns * 32768));
+    }
+  }
   // entries e = p, p + FIN_WARPS, ... added in that order. The column
   // partials (a heavy row has ~N of them) are loaded 8 at a time before the
   // adds, so the loads overlap instead of forming a serial chain (the plain
@@ -1130,6 +1149,19 @@ static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
   fa.step = STEP_ALPHA;
   if (sa) fa.sa = *sa;
   fa.done = done;
+  {
+    // slabs of every unit's head prefetched into L2 for the next SYMV
+    // (HS_SYMV_PF_SLABS overrides, 0 disables)
+    static const int pf = [] {
+      const char* e = getenv("HS_SYMV_PF_SLABS");
+      return e ? atoi(e) : 8;
+    }();
+    fa.pf_base = reinterpret_cast<const unsigned char*>(m->d);
+    fa.pf_slab = p->cta_slab;
+    fa.pf_slab_lo = m->tile_lo * p->slabs_per_tile;
+    fa.pf_units = std::min(p->grid, p->vgrid);
+    fa.pf_slabs = pf;
+  }
   HS_CUDA(launch_pdl(finalize_kernel, dim3((unsigned)m->row_hi, (unsigned)(b / FIN_COLS)),
                      dim3(FIN_THREADS), 0, c->stream, fa));
   HS_CUDA(cudaGetLastError());
