@@ -1013,8 +1013,37 @@ __global__ void check_finite_kernel(const double* A, int64_t tile_lo,
 // The diagonal tile solve walks its f = b / cb sub-blocks with the stored
 // cb x cb inverses W (cb = 128 on the DMMA path, b otherwise).
 
-// v_i <- L_ii^-1 v_i (forward) or L_ii^-T v_i (backward), one CTA.
-constexpr int TRSV_DIAG_THREADS = 1024;
+// v_i <- L_ii^-1 v_i (forward) or L_ii^-T v_i (backward) by a cluster of
+// TRSV_CLUSTER CTAs (the diagonal solve is the substitutions' serial critical
+// path: one CTA alone is load-latency bound at ~50 us for a 512 tile). Every
+// CTA keeps full copies of vin / sol in its shared memory; per sub-block each
+// CTA computes its share of the rows (forward) or columns (backward) and
+// stores the new values into every CTA's copy through distributed shared
+// memory, then a cluster barrier publishes them.
+constexpr int TRSV_DIAG_THREADS = 512;
+constexpr int TRSV_CLUSTER = 8;
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+// store v at `p` (a shared-memory address of this CTA's layout) in all CTAs
+__device__ __forceinline__ void st_cluster_all(double* p, double v) {
+  const uint32_t a = smem_u32(p);
+#pragma unroll
+  for (int r = 0; r < TRSV_CLUSTER; ++r) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(r));
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+  }
+}
 
 __global__ void __launch_bounds__(TRSV_DIAG_THREADS)
     trsv_diag_kernel(const double* A, int64_t tile_lo, const int64_t* lpos, const double* W,
@@ -1025,8 +1054,10 @@ __global__ void __launch_bounds__(TRSV_DIAG_THREADS)
   extern __shared__ double sh[];  // vin[b] | sol[b]
   double* vin = sh;
   double* sol = sh + b;
+  __shared__ double red[TRSV_DIAG_THREADS / 16][17];
   const double* D = A + (lpos ? lpos[tri(i, i)] : tri(i, i) - tile_lo) * (int64_t)b * b;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int rank = (int)cluster_rank();
   // multi-rank: v_i plus every rank's (negated) partial update, rank order
   for (int k = tid; k < b; k += blockDim.x) {
     double t = v[i * b + k];
@@ -1034,7 +1065,10 @@ __global__ void __launch_bounds__(TRSV_DIAG_THREADS)
       for (int r = 0; r < world; ++r) t += G[(int64_t)r * b + k];
     vin[k] = t;
   }
-  __syncthreads();
+  // no CTA stores into another's vin before that CTA has initialised it
+  cluster_sync_all();
+  // backward: 16 columns per group, nrl row lanes
+  const int cg = tid & 15, rl = tid >> 4, nrl = blockDim.x >> 4;
   for (int step = 0; step < f; ++step) {
     const int sb = upper ? f - 1 - step : step;  // sub-block being solved
     const int o = sb * cb;
@@ -1042,72 +1076,94 @@ __global__ void __launch_bounds__(TRSV_DIAG_THREADS)
     //   forward:  L[sb][s'] sol_s' for s' < sb  (rows o.., cols < o)
     //   backward: L[s'][sb]^T sol_s' for s' > sb (rows > o+cb, cols o..)
     if (!upper) {
-      for (int r = warp; r < cb; r += nw) {
-        // 4 independent partial sums keep several loads in flight
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        const double* row = D + (int64_t)(o + r) * b;
-        int c = lane;
-        for (; c + 96 < o; c += 128) {
-          a0 = fma(row[c], sol[c], a0);
-          a1 = fma(row[c + 32], sol[c + 32], a1);
-          a2 = fma(row[c + 64], sol[c + 64], a2);
-          a3 = fma(row[c + 96], sol[c + 96], a3);
+      if (o > 0) {
+        for (int r = rank * nw + warp; r < cb; r += TRSV_CLUSTER * nw) {
+          // 8 independent partial sums keep the row's loads in flight
+          double a[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) a[u] = 0.0;
+          const double* row = D + (int64_t)(o + r) * b;
+          int c = lane;
+          for (; c + 224 < o; c += 256)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[u] = fma(row[c + 32 * u], sol[c + 32 * u], a[u]);
+          for (; c < o; c += 32) a[0] = fma(row[c], sol[c], a[0]);
+          double acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+          for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+          const double nv = vin[o + r] - acc;
+          if (lane == 0) st_cluster_all(&vin[o + r], nv);
         }
-        for (; c < o; c += 32) a0 = fma(row[c], sol[c], a0);
-        double acc = (a0 + a1) + (a2 + a3);
-        for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-        if (lane == 0) vin[o + r] -= acc;
+        cluster_sync_all();
       }
     } else {
-      const int c = o + (tid % cb);  // column of L = row of L^T
-      const int stride = blockDim.x / cb;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int r = o + cb + tid / cb;
-      for (; r + 3 * stride < b; r += 4 * stride) {
-        a0 = fma(D[(int64_t)r * b + c], sol[r], a0);
-        a1 = fma(D[(int64_t)(r + stride) * b + c], sol[r + stride], a1);
-        a2 = fma(D[(int64_t)(r + 2 * stride) * b + c], sol[r + 2 * stride], a2);
-        a3 = fma(D[(int64_t)(r + 3 * stride) * b + c], sol[r + 3 * stride], a3);
-      }
-      for (; r < b; r += stride) a0 = fma(D[(int64_t)r * b + c], sol[r], a0);
-      const double acc = (a0 + a1) + (a2 + a3);
-      // reduce the blockDim / cb partials of each column
-      __shared__ double red[TRSV_DIAG_THREADS];
-      red[tid] = acc;
-      __syncthreads();
-      if (tid < cb) {
-        double t = 0.0;
-        for (int p = 0; p < (int)blockDim.x / cb; ++p) t += red[p * cb + tid];
-        vin[o + tid] -= t;
+      if (o + cb < b) {
+        for (int c0 = 16 * rank; c0 < cb; c0 += 16 * TRSV_CLUSTER) {
+          const int cc = c0 + cg;
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          if (cc < cb) {
+            const int c = o + cc;
+            int r = o + cb + rl;
+            for (; r + 3 * nrl < b; r += 4 * nrl) {
+              a0 = fma(D[(int64_t)r * b + c], sol[r], a0);
+              a1 = fma(D[(int64_t)(r + nrl) * b + c], sol[r + nrl], a1);
+              a2 = fma(D[(int64_t)(r + 2 * nrl) * b + c], sol[r + 2 * nrl], a2);
+              a3 = fma(D[(int64_t)(r + 3 * nrl) * b + c], sol[r + 3 * nrl], a3);
+            }
+            for (; r < b; r += nrl) a0 = fma(D[(int64_t)r * b + c], sol[r], a0);
+          }
+          red[rl][cg] = (a0 + a1) + (a2 + a3);
+          __syncthreads();
+          if (rl == 0 && cc < cb) {
+            double t = 0.0;
+            for (int p = 0; p < nrl; ++p) t += red[p][cg];
+            st_cluster_all(&vin[o + cc], vin[o + cc] - t);
+          }
+          __syncthreads();
+        }
+        cluster_sync_all();
       }
     }
-    __syncthreads();
     // sol_sb = W_sb vin_sb (forward) or W_sb^T vin_sb (backward)
     const double* Wb = W + (i * f + sb) * (int64_t)cb * cb;
     if (!upper) {
-      for (int r = warp; r < cb; r += nw) {
-        double acc = 0.0;
-        for (int c = lane; c <= r; c += 32) acc = fma(Wb[(int64_t)r * cb + c], vin[o + c], acc);
+      for (int r = rank * nw + warp; r < cb; r += TRSV_CLUSTER * nw) {
+        double a[4] = {0.0, 0.0, 0.0, 0.0};
+        int c = lane;
+        for (; c + 96 <= r; c += 128)
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            a[u] = fma(Wb[(int64_t)r * cb + c + 32 * u], vin[o + c + 32 * u], a[u]);
+        for (; c <= r; c += 32) a[0] = fma(Wb[(int64_t)r * cb + c], vin[o + c], a[0]);
+        double acc = (a[0] + a[1]) + (a[2] + a[3]);
         for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-        if (lane == 0) sol[o + r] = acc;
+        if (lane == 0) st_cluster_all(&sol[o + r], acc);
       }
     } else {
-      __shared__ double red2[TRSV_DIAG_THREADS];
-      const int c = tid % cb;
-      double acc = 0.0;
-      for (int r = c + tid / cb; r < cb; r += blockDim.x / cb)
-        acc = fma(Wb[(int64_t)r * cb + c], vin[o + r], acc);
-      red2[tid] = acc;
-      __syncthreads();
-      if (tid < cb) {
-        double t = 0.0;
-        for (int p = 0; p < (int)blockDim.x / cb; ++p) t += red2[p * cb + tid];
-        sol[o + tid] = t;
+      for (int c0 = 16 * rank; c0 < cb; c0 += 16 * TRSV_CLUSTER) {
+        const int c = c0 + cg;
+        double a0 = 0.0, a1 = 0.0;
+        if (c < cb) {
+          int r = c + rl;
+          for (; r + nrl < cb; r += 2 * nrl) {
+            a0 = fma(Wb[(int64_t)r * cb + c], vin[o + r], a0);
+            a1 = fma(Wb[(int64_t)(r + nrl) * cb + c], vin[o + r + nrl], a1);
+          }
+          for (; r < cb; r += nrl) a0 = fma(Wb[(int64_t)r * cb + c], vin[o + r], a0);
+        }
+        red[rl][cg] = a0 + a1;
+        __syncthreads();
+        if (rl == 0 && c < cb) {
+          double t = 0.0;
+          for (int p = 0; p < nrl; ++p) t += red[p][cg];
+          st_cluster_all(&sol[o + c], t);
+        }
+        __syncthreads();
       }
     }
-    __syncthreads();
+    cluster_sync_all();
   }
-  for (int k = tid; k < b; k += blockDim.x) v[i * b + k] = sol[k];
+  if (rank == 0)
+    for (int k = tid; k < b; k += blockDim.x) v[i * b + k] = sol[k];
 }
 
 // forward: out_k[rows] -= L_ki[rows, :] y_i for k = i+1 .. N-1 (blockIdx.y),
@@ -1864,7 +1920,8 @@ static void trsv_run_dist(hs_ctx* c, hs_matrix* m, double* v, bool upper) {
     const bool gather = s > 0;
     if (gather) comm_allgather(c, w + i * b, gath, (size_t)b, LK_SUBVECTOR);
     if (root == me) {
-      HS_CUDA(launch_pdl(trsv_diag_kernel, dim3(1), dim3(TRSV_DIAG_THREADS / cb * cb), dsm,
+      HS_CUDA(launch_pdl_cluster(trsv_diag_kernel, dim3(TRSV_CLUSTER), dim3(TRSV_DIAG_THREADS),
+                         TRSV_CLUSTER, dsm,
                          c->stream, (const double*)m->d, (int64_t)0,
                          (const int64_t*)m->d_lpos, (const double*)m->dinv, v,
                          gather ? (const double*)gath : nullptr, G, b, cb, f, i,
@@ -1890,7 +1947,7 @@ static void trsv_run(hs_ctx* c, hs_matrix* m, double* v, bool upper) {
   ensure_inverses(c, m);
   const int b = (int)m->b;
   const int cb = compute_block(b), f = b / cb;
-  HS_REQUIRE(b <= 2048 && cb <= TRSV_DIAG_THREADS, HS_ERR_CONFIG,
+  HS_REQUIRE(b <= 2048, HS_ERR_CONFIG,
              "block size unsupported in the triangular solves");
   const int64_t N = (int64_t)m->N;
   const int chunks = (b + 31) / 32;
@@ -1900,7 +1957,8 @@ static void trsv_run(hs_ctx* c, hs_matrix* m, double* v, bool upper) {
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
   for (int64_t s = 0; s < N; ++s) {
     const int64_t i = upper ? N - 1 - s : s;
-    HS_CUDA(launch_pdl(trsv_diag_kernel, dim3(1), dim3(TRSV_DIAG_THREADS / cb * cb), dsm,
+    HS_CUDA(launch_pdl_cluster(trsv_diag_kernel, dim3(TRSV_CLUSTER), dim3(TRSV_DIAG_THREADS),
+                         TRSV_CLUSTER, dsm,
                        c->stream, (const double*)m->d, m->tile_lo, (const int64_t*)nullptr,
                        (const double*)m->dinv, v, (const double*)nullptr, 1, b, cb, f, i,
                        upper ? 1 : 0));

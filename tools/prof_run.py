@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--iters", type=int, default=6)
     ap.add_argument("--dist", action="store_true",
                     help="world-1 NCCL context, 2D block-cyclic Cholesky path")
+    ap.add_argument("--solve", type=int, default=0,
+                    help="after the factorization: this many timed forward + back substitutions")
     ap.add_argument("--slices", type=int, default=0,
                     help="Cholesky trailing update on the INT8 tensor cores (0: DMMA)")
     a = ap.parse_args()
@@ -40,6 +42,18 @@ def main():
         rt.set_cholesky_gemm(a.slices)
         st = hs.potrf_device(rt, m)
         print("factor ms", st.factor_ms)
+        if a.solve:
+            v = torch.from_numpy(hs.generate_rhs(a.n, a.b, 42).values).cuda()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            for _ in range(a.solve):
+                ev[0].record()
+                hs.trsv_device(rt, m, v.data_ptr(), False)
+                ev[1].record()
+                hs.trsv_device(rt, m, v.data_ptr(), True)
+                ev[2].record()
+                torch.cuda.synchronize()
+                print("trsv lower / upper ms %.3f %.3f" % (ev[0].elapsed_time(ev[1]),
+                                                          ev[1].elapsed_time(ev[2])))
     torch.cuda.synchronize()
     rt.close()
 
