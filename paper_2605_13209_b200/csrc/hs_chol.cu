@@ -1167,14 +1167,26 @@ __global__ void __launch_bounds__(TRSV_DIAG_THREADS)
 }
 
 // forward: out_k[rows] -= L_ki[rows, :] y_i for k = i+1 .. N-1 (blockIdx.y),
-//          32-row chunks (blockIdx.x)
-// backward: out_k[cols] -= L_ik[:, cols]^T x_i for k = 0 .. i-1, 32-col chunks
+//          row chunks (blockIdx.x; trsv_chunks)
+// backward: out_k[cols] -= L_ik[:, cols]^T x_i for k = 0 .. i-1, column chunks
 // (single rank: out = v; multi-rank: k from this rank's owned-tile `list`,
 // out = its partial-update vector)
 __global__ void __launch_bounds__(256)
     trsv_update_kernel(const double* A, int64_t tile_lo, const int64_t* lpos,
                        const int32_t* list, const double* v, double* out, int b,
                        int64_t i, int upper) {
+  const bool cl = upper == 2;  // launched in clusters (launch_trsv_update)
+  if (!list && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    // single rank: the next step's diagonal tile into L2 (the factor is
+    // constant), so the diagonal solve's serial load chain hits L2
+    const int64_t nx = upper ? i - 1 : i + 1;
+    // (forward: launched only when a row below i exists; backward: i >= 1)
+    if (nx >= 0)
+      bulk_prefetch_l2(A + (tri(nx, nx) - tile_lo) * (int64_t)b * b,
+                       (uint32_t)(((int64_t)b * b * 8) & ~(int64_t)15));
+  }
+  // DSMEM stores below only after every CTA of the cluster has started
+  if (cl) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   pdl_wait();
   pdl_trigger();
   const int64_t k = list ? (int64_t)list[blockIdx.y]
@@ -1185,6 +1197,91 @@ __global__ void __launch_bounds__(256)
   for (int c = threadIdx.x; c < b; c += blockDim.x) yi[c] = v[i * b + c];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if ((b & 1) == 0 && upper != 1) {
+    // even b: 16-byte loads (rows of a tile are 16-B aligned)
+    const double2* yi2 = reinterpret_cast<const double2*>(yi);
+    const int b2 = b / 2;
+    if (!upper) {
+      // 8 rows per CTA (blockIdx.x), one per warp: a row's loads all in flight
+      const double* T = A + (lpos ? lpos[tri(k, i)] : tri(k, i) - tile_lo) * (int64_t)b * b;
+      const int r = blockIdx.x * 8 + warp;
+      if (r >= b) return;
+      const double2* R0 = reinterpret_cast<const double2*>(T + (int64_t)r * b);
+      double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0;
+      int c2 = lane;
+#pragma unroll 4
+      for (; c2 + 32 < b2; c2 += 64) {
+        const double2 p = R0[c2], q = R0[c2 + 32], y = yi2[c2], z = yi2[c2 + 32];
+        a0 = fma(p.x, y.x, a0);
+        a1 = fma(p.y, y.y, a1);
+        c0 = fma(q.x, z.x, c0);
+        c1 = fma(q.y, z.y, c1);
+      }
+      if (c2 < b2) {
+        const double2 p = R0[c2], y = yi2[c2];
+        a0 = fma(p.x, y.x, a0);
+        a1 = fma(p.y, y.y, a1);
+      }
+      double u = (a0 + a1) + (c0 + c1);
+      for (int off = 16; off; off >>= 1) u += __shfl_xor_sync(0xffffffffu, u, off);
+      if (lane == 0) out[k * b + r] -= u;
+    } else {
+      // a cluster of TRSV_CLUSTER CTAs per 64-column chunk (32 double2
+      // lanes): CTA `rg` sums its row group, the leader adds the groups'
+      // partials in rank order (deterministic) from its shared memory
+      const int chunk = blockIdx.x / TRSV_CLUSTER, rg = blockIdx.x % TRSV_CLUSTER;
+      const double* T = A + (lpos ? lpos[tri(i, k)] : tri(i, k) - tile_lo) * (int64_t)b * b;
+      const int c2 = chunk * 32 + lane;
+      const int R = (b + TRSV_CLUSTER - 1) / TRSV_CLUSTER;
+      const int rlo = rg * R, rhi = min(b, rlo + R);
+      double2 acc = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+      if (c2 < b2) {
+        const double2* T2 = reinterpret_cast<const double2*>(T) + c2;
+        int r = rlo + warp;
+#pragma unroll 4
+        for (; r + 8 < rhi; r += 16) {
+          const double2 p = T2[(int64_t)r * b2], q = T2[(int64_t)(r + 8) * b2];
+          acc.x = fma(p.x, yi[r], acc.x);
+          acc.y = fma(p.y, yi[r], acc.y);
+          acc1.x = fma(q.x, yi[r + 8], acc1.x);
+          acc1.y = fma(q.y, yi[r + 8], acc1.y);
+        }
+        if (r < rhi) {
+          const double2 p = T2[(int64_t)r * b2];
+          acc.x = fma(p.x, yi[r], acc.x);
+          acc.y = fma(p.y, yi[r], acc.y);
+        }
+      }
+      __shared__ double2 red2[8][32];
+      __shared__ double2 grp[TRSV_CLUSTER][32];  // leader: the groups' partials
+      red2[warp][lane] = make_double2(acc.x + acc1.x, acc.y + acc1.y);
+      __syncthreads();
+      asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+      if (warp == 0) {
+        double2 t = make_double2(0.0, 0.0);
+        for (int w = 0; w < 8; ++w) {
+          t.x += red2[w][lane].x;
+          t.y += red2[w][lane].y;
+        }
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                     : "=r"(ra) : "r"(smem_u32(&grp[rg][lane])), "r"(0));
+        asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(ra), "d"(t.x), "d"(t.y)
+                     : "memory");
+      }
+      cluster_sync_all();
+      if (rg == 0 && warp == 0 && c2 < b2) {
+        double2 t = make_double2(0.0, 0.0);
+        for (int g = 0; g < TRSV_CLUSTER; ++g) {
+          t.x += grp[g][lane].x;
+          t.y += grp[g][lane].y;
+        }
+        out[k * b + 2 * c2] -= t.x;
+        out[k * b + 2 * c2 + 1] -= t.y;
+      }
+    }
+    return;
+  }
   if (!upper) {
     const double* T = A + (lpos ? lpos[tri(k, i)] : tri(k, i) - tile_lo) * (int64_t)b * b;
     for (int rr = warp; rr < 32; rr += 8) {
@@ -1209,6 +1306,32 @@ __global__ void __launch_bounds__(256)
       out[k * b + c] -= t;
     }
   }
+}
+
+// update variant (the kernel's `upper` argument): 0 forward; backward 1
+// (one CTA per 32 columns over the whole tile height) or, at even b when the
+// step has few tiles, 2 (one cluster of TRSV_CLUSTER CTAs per 64 columns,
+// each CTA a row group: more SMs per tile where variant 1 would leave most
+// of the GPU idle and latency-bound)
+static int trsv_mode(int b, bool upper, int64_t nk) {
+  if (!upper) return 0;
+  return ((b & 1) == 0 && nk * ((b + 63) / 64) <= 148) ? 2 : 1;
+}
+
+// CTAs per tile along x: forward 8 rows per CTA at even b (16-byte loads)
+static int trsv_chunks(int b, int mode) {
+  if (mode == 2) return (b + 63) / 64 * TRSV_CLUSTER;
+  if (mode == 0 && (b & 1) == 0) return (b + 7) / 8;
+  return (b + 31) / 32;
+}
+
+template <typename... Args>
+static cudaError_t launch_trsv_update(int mode, dim3 grid, size_t smem,
+                                      cudaStream_t st, Args&&... args) {
+  if (mode == 2)
+    return launch_pdl_cluster(trsv_update_kernel, grid, dim3(256), TRSV_CLUSTER, smem, st,
+                              std::forward<Args>(args)...);
+  return launch_pdl(trsv_update_kernel, grid, dim3(256), smem, st, std::forward<Args>(args)...);
 }
 
 // ---------------------------------------------------------------------------
@@ -1882,7 +2005,6 @@ static void trsv_run_dist(hs_ctx* c, hs_matrix* m, double* v, bool upper) {
   const int cb = compute_block(b), f = b / cb;
   const int64_t N = (int64_t)m->N;
   const int P = m->P, Q = m->Q, me = c->rank, G = c->world;
-  const int chunks = (b + 31) / 32;
   const size_t dsm = 2 * (size_t)b * sizeof(double), usm = (size_t)b * sizeof(double);
   if (dsm > 48 * 1024)
     HS_CUDA(cudaFuncSetAttribute(trsv_diag_kernel,
@@ -1931,10 +2053,11 @@ static void trsv_run_dist(hs_ctx* c, hs_matrix* m, double* v, bool upper) {
     comm_bcast_on(c, v + i * b, v + i * b, (size_t)b, root, c->stream, LK_SUBVECTOR);
     const int64_t nk = off[s + 1] - off[s];
     if (nk > 0) {
-      HS_CUDA(launch_pdl(trsv_update_kernel, dim3(chunks, (unsigned)nk), dim3(256), usm,
+      const int mode = trsv_mode(b, upper, nk);
+      HS_CUDA(launch_trsv_update(mode, dim3(trsv_chunks(b, mode), (unsigned)nk), usm,
                          c->stream, (const double*)m->d, (int64_t)0,
                          (const int64_t*)m->d_lpos, (const int32_t*)(d_list + off[s]),
-                         (const double*)v, w, b, i, upper ? 1 : 0));
+                         (const double*)v, w, b, i, mode));
       launch_count(c);
     }
   }
@@ -1950,7 +2073,6 @@ static void trsv_run(hs_ctx* c, hs_matrix* m, double* v, bool upper) {
   HS_REQUIRE(b <= 2048, HS_ERR_CONFIG,
              "block size unsupported in the triangular solves");
   const int64_t N = (int64_t)m->N;
-  const int chunks = (b + 31) / 32;
   const size_t dsm = 2 * (size_t)b * sizeof(double), usm = (size_t)b * sizeof(double);
   if (dsm > 48 * 1024)
     HS_CUDA(cudaFuncSetAttribute(trsv_diag_kernel,
@@ -1965,9 +2087,10 @@ static void trsv_run(hs_ctx* c, hs_matrix* m, double* v, bool upper) {
     launch_count(c);
     const int64_t nk = upper ? i : N - 1 - i;
     if (nk > 0) {
-      HS_CUDA(launch_pdl(trsv_update_kernel, dim3(chunks, (unsigned)nk), dim3(256), usm,
+      const int mode = trsv_mode(b, upper, nk);
+      HS_CUDA(launch_trsv_update(mode, dim3(trsv_chunks(b, mode), (unsigned)nk), usm,
                          c->stream, (const double*)m->d, m->tile_lo, (const int64_t*)nullptr,
-                         (const int32_t*)nullptr, (const double*)v, v, b, i, upper ? 1 : 0));
+                         (const int32_t*)nullptr, (const double*)v, v, b, i, mode));
       launch_count(c);
     }
   }
