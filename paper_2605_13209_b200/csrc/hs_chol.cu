@@ -1045,19 +1045,75 @@ __device__ __forceinline__ void st_cluster_all(double* p, double v) {
   }
 }
 
+// Staged variant (cb = 128 = TRSV_CLUSTER x 16 warps, f <= 4): each CTA's
+// share of L_ii and of the inverses -- 16 rows (forward) or 16 columns
+// (backward) per sub-block -- is copied into shared memory with cp.async
+// before the PDL wait (the factor is constant), overlapping the previous
+// update kernel; the sub-block steps then read shared memory only.
+__host__ __device__ inline bool trsv_staged(int b, int cb, int f) {
+  return cb == 128 && f <= 4 && b == cb * f;
+}
+// doubles staged per CTA: L_ii part 16 cb f(f-1)/2, inverses 16 cb f
+__host__ __device__ inline int trsv_staged_doubles(int cb, int f) {
+  return 16 * cb * (f * (f - 1) / 2 + f);
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+
 __global__ void __launch_bounds__(TRSV_DIAG_THREADS)
     trsv_diag_kernel(const double* A, int64_t tile_lo, const int64_t* lpos, const double* W,
                      double* v, const double* G, int world, int b, int cb, int f, int64_t i,
                      int upper) {
-  pdl_wait();
-  pdl_trigger();
-  extern __shared__ double sh[];  // vin[b] | sol[b]
+  extern __shared__ double sh[];  // vin[b] | sol[b] | staged L_ii | staged W
   double* vin = sh;
   double* sol = sh + b;
   __shared__ double red[TRSV_DIAG_THREADS / 16][17];
   const double* D = A + (lpos ? lpos[tri(i, i)] : tri(i, i) - tile_lo) * (int64_t)b * b;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int rank = (int)cluster_rank();
+  const bool staged = trsv_staged(b, cb, f) && nw * TRSV_CLUSTER == cb;
+  double* Ds = sh + 2 * b;               // [sb] blocks, see below
+  double* Ws = Ds + 16 * cb * (f * (f - 1) / 2);  // [sb][cb][16] or [sb][16][cb]
+  if (staged) {
+    const double* Wi = W + i * f * (int64_t)cb * cb;
+    int64_t base = 0;
+    for (int sb = 0; sb < f; ++sb) {
+      const int o = sb * cb;
+      if (!upper) {
+        // rows rank*16 + rr of sub-block sb, columns [0, o): Ds[base + rr*o + c]
+        const int h = o / 2;  // 16-B chunks per row
+        for (int q = tid; q < 16 * h; q += blockDim.x) {
+          const int rr = q / h, cc = 2 * (q % h);
+          cp_async16(Ds + base + rr * o + cc, D + (int64_t)(o + rank * 16 + rr) * b + cc);
+        }
+        base += 16 * o;
+        for (int q = tid; q < 16 * cb / 2; q += blockDim.x) {
+          const int rr = q / (cb / 2), cc = 2 * (q % (cb / 2));
+          cp_async16(Ws + (sb * 16 + rr) * cb + cc,
+                     Wi + ((int64_t)sb * cb + rank * 16 + rr) * cb + cc);
+        }
+      } else {
+        // rows [o + cb, b), columns o + rank*16 + [0, 16): Ds[base + rr*16 + c]
+        const int nr = b - o - cb;
+        for (int q = tid; q < nr * 8; q += blockDim.x) {
+          const int rr = q >> 3, cc = 2 * (q & 7);
+          cp_async16(Ds + base + rr * 16 + cc, D + (int64_t)(o + cb + rr) * b + o + rank * 16 + cc);
+        }
+        base += 16 * nr;
+        for (int q = tid; q < cb * 8; q += blockDim.x) {
+          const int r = q >> 3, cc = 2 * (q & 7);
+          cp_async16(Ws + (sb * cb + r) * 16 + cc,
+                     Wi + ((int64_t)sb * cb + r) * cb + rank * 16 + cc);
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  pdl_wait();
+  pdl_trigger();
   // multi-rank: v_i plus every rank's (negated) partial update, rank order
   for (int k = tid; k < b; k += blockDim.x) {
     double t = v[i * b + k];
@@ -1065,6 +1121,8 @@ __global__ void __launch_bounds__(TRSV_DIAG_THREADS)
       for (int r = 0; r < world; ++r) t += G[(int64_t)r * b + k];
     vin[k] = t;
   }
+  if (staged) asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
   // no CTA stores into another's vin before that CTA has initialised it
   cluster_sync_all();
   // backward: 16 columns per group, nrl row lanes
@@ -1075,7 +1133,39 @@ __global__ void __launch_bounds__(TRSV_DIAG_THREADS)
     // residual of sub-block sb: vin_sb - sum over solved sub-blocks
     //   forward:  L[sb][s'] sol_s' for s' < sb  (rows o.., cols < o)
     //   backward: L[s'][sb]^T sol_s' for s' > sb (rows > o+cb, cols o..)
-    if (!upper) {
+    if (staged) {
+      // forward: row warp of this CTA's 16; backward: column cg of its 16.
+      // Sub-block sb's part of L_ii starts at 16 cb * (sum over s < sb of
+      // s (forward) or f - 1 - s (backward) row-blocks)
+      const int64_t dbase = upper ? 16LL * cb * (sb * (f - 1) - sb * (sb - 1) / 2)
+                                  : 16LL * cb * (sb * (sb - 1) / 2);
+      if (!upper && o > 0) {
+        const double* row = Ds + dbase + warp * o;
+        double a[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int c = lane; c < o; c += 128)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) a[u] = fma(row[c + 32 * u], sol[c + 32 * u], a[u]);
+        double acc = (a[0] + a[1]) + (a[2] + a[3]);
+        for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        const int r = rank * 16 + warp;
+        const double nv = vin[o + r] - acc;
+        if (lane == 0) st_cluster_all(&vin[o + r], nv);
+        cluster_sync_all();
+      } else if (upper && o + cb < b) {
+        const int nr = b - o - cb;
+        double a0 = 0.0;
+        for (int rr = rl; rr < nr; rr += nrl) a0 = fma(Ds[dbase + rr * 16 + cg], sol[o + cb + rr], a0);
+        red[rl][cg] = a0;
+        __syncthreads();
+        if (rl == 0) {
+          double t = 0.0;
+          for (int p = 0; p < nrl; ++p) t += red[p][cg];
+          const int c = o + rank * 16 + cg;
+          st_cluster_all(&vin[c], vin[c] - t);
+        }
+        cluster_sync_all();
+      }
+    } else if (!upper) {
       if (o > 0) {
         for (int r = rank * nw + warp; r < cb; r += TRSV_CLUSTER * nw) {
           // 8 independent partial sums keep the row's loads in flight
@@ -1125,7 +1215,33 @@ __global__ void __launch_bounds__(TRSV_DIAG_THREADS)
     }
     // sol_sb = W_sb vin_sb (forward) or W_sb^T vin_sb (backward)
     const double* Wb = W + (i * f + sb) * (int64_t)cb * cb;
-    if (!upper) {
+    if (staged) {
+      if (!upper) {
+        const int r = rank * 16 + warp;
+        const double* wr = Ws + (sb * 16 + warp) * cb;
+        double a[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = lane + 32 * u;
+          if (c <= r) a[u] = wr[c] * vin[o + c];
+        }
+        double acc = (a[0] + a[1]) + (a[2] + a[3]);
+        for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (lane == 0) st_cluster_all(&sol[o + r], acc);
+      } else {
+        const int c = rank * 16 + cg;
+        double a0 = 0.0;
+        for (int r = c + rl; r < cb; r += nrl) a0 = fma(Ws[(sb * cb + r) * 16 + cg], vin[o + r], a0);
+        red[rl][cg] = a0;
+        __syncthreads();
+        if (rl == 0) {
+          double t = 0.0;
+          for (int p = 0; p < nrl; ++p) t += red[p][cg];
+          st_cluster_all(&sol[o + c], t);
+        }
+        __syncthreads();
+      }
+    } else if (!upper) {
       for (int r = rank * nw + warp; r < cb; r += TRSV_CLUSTER * nw) {
         double a[4] = {0.0, 0.0, 0.0, 0.0};
         int c = lane;
@@ -2005,7 +2121,9 @@ static void trsv_run_dist(hs_ctx* c, hs_matrix* m, double* v, bool upper) {
   const int cb = compute_block(b), f = b / cb;
   const int64_t N = (int64_t)m->N;
   const int P = m->P, Q = m->Q, me = c->rank, G = c->world;
-  const size_t dsm = 2 * (size_t)b * sizeof(double), usm = (size_t)b * sizeof(double);
+  const size_t dsm = (2 * (size_t)b + (trsv_staged(b, cb, f) ? trsv_staged_doubles(cb, f) : 0)) *
+                         sizeof(double),
+               usm = (size_t)b * sizeof(double);
   if (dsm > 48 * 1024)
     HS_CUDA(cudaFuncSetAttribute(trsv_diag_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
@@ -2073,7 +2191,9 @@ static void trsv_run(hs_ctx* c, hs_matrix* m, double* v, bool upper) {
   HS_REQUIRE(b <= 2048, HS_ERR_CONFIG,
              "block size unsupported in the triangular solves");
   const int64_t N = (int64_t)m->N;
-  const size_t dsm = 2 * (size_t)b * sizeof(double), usm = (size_t)b * sizeof(double);
+  const size_t dsm = (2 * (size_t)b + (trsv_staged(b, cb, f) ? trsv_staged_doubles(cb, f) : 0)) *
+                         sizeof(double),
+               usm = (size_t)b * sizeof(double);
   if (dsm > 48 * 1024)
     HS_CUDA(cudaFuncSetAttribute(trsv_diag_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
