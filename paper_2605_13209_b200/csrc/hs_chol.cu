@@ -1297,9 +1297,14 @@ __global__ void __launch_bounds__(256)
     // constant), so the diagonal solve's serial load chain hits L2
     const int64_t nx = upper ? i - 1 : i + 1;
     // (forward: launched only when a row below i exists; backward: i >= 1)
-    if (nx >= 0)
-      bulk_prefetch_l2(A + (tri(nx, nx) - tile_lo) * (int64_t)b * b,
-                       (uint32_t)(((int64_t)b * b * 8) & ~(int64_t)15));
+    if (nx >= 0) {
+      // the bulk prefetch needs a 16-B aligned start and size (odd b: tiles
+      // start 8-B aligned)
+      const uintptr_t a0 = (uintptr_t)(A + (tri(nx, nx) - tile_lo) * (int64_t)b * b);
+      const uintptr_t a16 = (a0 + 15) & ~(uintptr_t)15;
+      const int64_t bytes = ((int64_t)b * b * 8 - (int64_t)(a16 - a0)) & ~(int64_t)15;
+      if (bytes > 0) bulk_prefetch_l2(reinterpret_cast<const void*>(a16), (uint32_t)bytes);
+    }
   }
   // DSMEM stores below only after every CTA of the cluster has started
   if (cl) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");

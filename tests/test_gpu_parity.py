@@ -398,8 +398,11 @@ def test_singular_factor_dmma_path(rt):
         hs.forward_substitute(sing, r, rt)
 
 
-@pytest.mark.parametrize("n,b", [(1024, 128), (2048, 512), (200, 16), (1500, 256)])
+@pytest.mark.parametrize("n,b", [(1024, 128), (2048, 512), (200, 16), (1500, 256),
+                                 (1152, 384), (700, 100), (999, 37), (2048, 1024)])
 def test_substitutions_match_oracle(rt, oracle, n, b):
+    # b = 128 f (f <= 4): staged cluster diagonal solve; 1024: unstaged (f = 8);
+    # 100 / 16: cb = b; 37: odd b (scalar update path)
     a = oracle.generate_spd(n, b, seed=8)
     _, L, _, _ = oracle.factorize(n, b, a)
     rhs = oracle.generate_rhs(n, b, seed=8)
@@ -600,3 +603,25 @@ def test_distributed_cg_world1_matches_oracle(oracle, n, b):
         assert st.true_residual <= 2e-6 * np.sqrt(st.u0)
     finally:
         rt.close()
+
+
+@pytest.mark.parametrize("n,b", [(6144, 32), (4096, 128)])
+def test_substitutions_wide_steps(rt, n, b):
+    """Steps with many tiles (backward update without clusters, forward
+    update grids of several waves) against a dense LAPACK-free reference:
+    a diagonally dominant lower-triangular L solved by scipy."""
+    from scipy.linalg import solve_triangular
+    rng = np.random.default_rng(3)
+    N = n // b
+    dense = np.tril(rng.uniform(-1.0, 1.0, (n, n)) / np.sqrt(n))
+    dense[np.diag_indices(n)] = rng.uniform(1.0, 2.0, n)
+    ti, tj = np.tril_indices(N)
+    packed = dense.reshape(N, b, N, b).transpose(0, 2, 1, 3)[ti, tj].ravel()
+    rhs = rng.uniform(-1.0, 1.0, n)
+    lm = hs.BlockedSPDMatrix(n, b, packed)
+    y = hs.forward_substitute(lm, hs.BlockVector(n, b, rhs), rt)
+    x = hs.back_substitute(lm, y, rt)
+    y_ref = solve_triangular(dense, rhs, lower=True)
+    x_ref = solve_triangular(dense.T, y_ref, lower=False)
+    assert np.linalg.norm(y.logical() - y_ref) <= 1e-12 * np.linalg.norm(y_ref)
+    assert np.linalg.norm(x.logical() - x_ref) <= 1e-12 * np.linalg.norm(x_ref)
