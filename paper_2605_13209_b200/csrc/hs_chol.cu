@@ -1006,7 +1006,7 @@ __global__ void check_finite_kernel(const double* A, int64_t tile_lo,
 
 // ---- triangular solves with the stored inverses ----------------------------
 // Right-looking at tile granularity, 2 launches per tile row (PDL-chained):
-//   forward  (L y = v):   y_i = solve(L_ii, v_i)   [trsv_diag_kernel, 1 CTA]
+//   forward  (L y = v):   y_i = solve(L_ii, v_i)   [trsv_diag_kernel, 8-CTA cluster]
 //                         v_k -= L_ki y_i, k > i   [trsv_update_kernel]
 //   backward (L^T x = v): x_i = solve(L_ii^T, v_i)
 //                         v_k -= L_ik^T x_i, k < i
