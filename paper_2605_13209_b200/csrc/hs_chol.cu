@@ -1075,6 +1075,9 @@ __global__ void __launch_bounds__(TRSV_DIAG_THREADS)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int rank = (int)cluster_rank();
   const bool staged = trsv_staged(b, cb, f) && nw * TRSV_CLUSTER == cb;
+  // first half of the cluster barrier that guarantees every CTA of the
+  // cluster is running before any DSMEM store (the wait is below)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   double* Ds = sh + 2 * b;               // [sb] blocks, see below
   double* Ws = Ds + 16 * cb * (f * (f - 1) / 2);  // [sb][cb][16] or [sb][16][cb]
   if (staged) {
@@ -1123,8 +1126,11 @@ __global__ void __launch_bounds__(TRSV_DIAG_THREADS)
   }
   if (staged) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
-  // no CTA stores into another's vin before that CTA has initialised it
-  cluster_sync_all();
+  // every CTA arrived at kernel entry, so this returns at once. Remote
+  // stores before the first full barrier below only target sol (which the
+  // initialisation above does not write); remote vin stores happen after
+  // it, i.e. after every CTA's initialisation.
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   // backward: 16 columns per group, nrl row lanes
   const int cg = tid & 15, rl = tid >> 4, nrl = blockDim.x >> 4;
   for (int step = 0; step < f; ++step) {
