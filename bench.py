@@ -167,21 +167,41 @@ def cpu_reference_cholesky(n: int, b: int) -> dict:
             "kind": kind, "sample": f"factorize n={n}, b={b}, workers_a={threads}"}
 
 
+def workload_config(args, world: int) -> dict:
+    """The `config` dict, identical in both arms (same workload, same keys)."""
+    n, b = args.n, args.b
+    N = (n + b - 1) // b
+    packed = N * (N + 1) // 2 * b * b * 8
+    cfg_idx = "BASELINE.json configs[1]" if n == 32768 and b == 128 else (
+        "BASELINE.json configs[3]" if n == 131072 and b == 128 else "not a BASELINE config")
+    l2 = (f"inputs larger than L2 (packed A = {packed / 1e9:.2f} GB)" if packed > 126e6 else
+          f"inputs fit in L2 (packed A = {packed / 1e6:.1f} MB, not flushed)")
+    return {"workload": f"CG on GP squared-exponential SPD matrix, n={n}, b={b} ({cfg_idx})",
+            "n": n, "b": b, "seed": 42, "recompute_interval": 50,
+            "eps": "1e-300 (fixed iteration count)",
+            "parallelism": (f"row-sharded x{world} (NCCL)" if world > 1 else "single device"),
+            "l2": l2}
+
+
 def run_reference_arm(args) -> None:
+    """The reference's own CPU implementation (oracle/_ref: the unmodified
+    sources compiled by oracle/Makefile) on all host cores, same workload,
+    steps and warm-up as our arm. Under torchrun only rank 0 runs."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    iters = max(1, min(args.steps, args.ref_iters))
-    warm = min(args.warmup, 3)
+    iters, warm = args.steps, args.warmup
     cb = cpu_reference_cg(args.n, args.b, iters, warm)
     line = {
         "impl": "reference", "metric": "cg_iters_per_s", "value": cb["value"],
         "unit": "iters/s", "n_gpus": args.gpus, "steps": iters, "warmup": warm,
-        "ms_per_step": 1e3 / cb["value"], "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "CG on GP squared-exponential SPD matrix (configs[1])",
-                   "n": args.n, "b": args.b, "seed": 42, "recompute_interval": 50,
-                   "device": "host CPU (reference hsolve, homogeneous executor A)"},
+        "ms_per_step": 1e3 / cb["value"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic GP squared-exponential matrix (generate_spd seed 42)",
+        "config": workload_config(args, args.gpus),
+        "device": f"host CPU, {cb['cores']} threads (reference hsolve, homogeneous "
+                  f"executor A, fraction 0); rank 0 of {world}",
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": cb["value"], "unit": "iters/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -361,6 +381,12 @@ def run_ours(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: refusing to "
+                         "measure a different number of GPUs than asked for")
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench.py: rank {rank} needs cuda:{local} but only "
+                         f"{torch.cuda.device_count()} device(s) are visible")
     torch.cuda.set_device(local)
     import paper_2605_13209_b200 as hs
     from paper_2605_13209_b200 import hsolve as H
@@ -472,12 +498,8 @@ def run_ours(args) -> None:
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic GP squared-exponential matrix (generate_spd seed 42, median "
                 "length-scale rule) assembled on the device",
-        "config": {"workload": "CG on GP SE matrix, n=%d, b=%d (BASELINE.json configs[1])"
-                               % (n, b), "n": n, "b": b, "seed": 42,
-                   "recompute_interval": 50, "eps": "1e-300 (fixed iteration count)",
-                   "parallelism": (f"row-sharded x{world} (NCCL)" if use_dist else "single GPU"),
-                   "l2": f"inputs larger than L2 (packed A = {packed_bytes / 1e9:.2f} GB)",
-                   "matrix_assembly_s": round(gen_s, 3)},
+        "config": workload_config(args, world),
+        "matrix_assembly_s": round(gen_s, 3),
         "gpu_launches": int(launches),
         "roofline": roofline,
     }
@@ -551,6 +573,14 @@ def run_ours(args) -> None:
         if rank == 0:
             line["secondary"] = sec
 
+    if world == 1 and not args.no_anchor:
+        # the north-star size on one GPU: CG at n=131072 (configs[3]'s matrix),
+        # so the N>1 lines (which run that size) have a same-workload N=1 point
+        try:
+            line["single_gpu_n131072"] = cg_anchor(hs, rt, torch, args)
+        except Exception as e:
+            line["single_gpu_n131072"] = {"error": repr(e)}
+
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_reference_cg(n, b, args.cpu_iters, 1)
@@ -559,11 +589,56 @@ def run_ours(args) -> None:
                     args.cpu_chol_n, args.chol_b)
         except Exception as e:
             line["cpu_baseline"] = {"error": repr(e)}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
     rt.close()
     if use_dist:
         dist.destroy_process_group()
+    if rank == 0:  # last, after the communicators' teardown logging
+        print(json.dumps(line), flush=True)
+
+
+def cg_anchor(hs, rt, torch, args, n: int = 131072, b: int = 128, iters: int = 20) -> dict:
+    """CG iterations/s at n=131072 (68.8 GB packed) on this one GPU."""
+    m = hs.generate_spd_device(rt, n, b, seed=42)
+    rhs = torch.from_numpy(hs.generate_rhs(n, b, 42).values).cuda()
+    x = torch.zeros_like(rhs)
+    hs.solve_cg_device(rt, m, rhs.data_ptr(), x.data_ptr(),
+                       hs.SolverConfig(block_size=b, eps=1e-300, max_iters=3))
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    st = hs.solve_cg_device(rt, m, rhs.data_ptr(), x.data_ptr(),
+                            hs.SolverConfig(block_size=b, eps=1e-300, max_iters=iters))
+    ev1.record()
+    ev1.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    m.free()
+    del rhs, x
+    torch.cuda.empty_cache()
+    N = n // b
+    bytes_ = N * (N + 1) // 2 * b * b * 8
+    return {"metric": "cg_iters_per_s", "value": st.iterations / (ms * 1e-3), "unit": "iters/s",
+            "n": n, "b": b, "iterations": st.iterations, "warmup": 3,
+            "ms_per_step": ms / st.iterations,
+            "step_gbs": bytes_ / (ms / st.iterations * 1e-3) / 1e9,
+            "note": "the N>1 lines run this workload (configs[3]) row-sharded; "
+                    "this is its one-GPU point"}
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` outside torchrun: launch N ranks on this node (one
+    per GPU) with torch.distributed.run, refusing if fewer GPUs are visible."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        log(f"bench.py: --gpus {args.gpus} asked for but only {have} GPU(s) visible; "
+            "refusing to measure fewer GPUs than asked for")
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1",
+           "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1",
+           "--master-port", str(29500 + os.getpid() % 1000), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    log("+ " + " ".join(cmd))
+    return subprocess.call(cmd)
 
 
 def main():
@@ -572,9 +647,13 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--cg-n", "--n", dest="n", type=int, default=None,
+                    help="CG size (default 32768 = configs[1] at N=1, 131072 = configs[3] "
+                         "at N>1)")
     ap.add_argument("--b", type=int, default=128)
-    ap.add_argument("--chol-n", type=int, default=32768)
+    ap.add_argument("--chol-n", type=int, default=None,
+                    help="Cholesky size (default 32768 = configs[2] at N=1, 131072 = "
+                         "configs[4] block-cyclic at N>1)")
     ap.add_argument("--chol-b", type=int, default=512)
     ap.add_argument("--chol-reps", type=int, default=2)
     ap.add_argument("--chol-slices", type=int, default=8,
@@ -592,10 +671,22 @@ def main():
                     help="use the NCCL (multi-GPU) code paths even on one GPU")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-anchor", action="store_true",
+                    help="skip the one-GPU n=131072 CG point (N=1 only)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: --warmup < 3 violates the timing rules; using 3")
         args.warmup = 3
+    if args.n is None:
+        args.n = 32768 if args.gpus == 1 else 131072
+    if args.chol_n is None:
+        args.chol_n = 32768 if args.gpus == 1 else 131072
+    if args.gpus > 1:
+        # NCCL init lines (nranks per communicator) for the driver's logs
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        if "WORLD_SIZE" not in os.environ and args.impl == "ours":
+            sys.exit(spawn_ranks(args))
     if args.impl == "reference":
         run_reference_arm(args)
     else:
