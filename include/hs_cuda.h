@@ -63,6 +63,7 @@ void hs_last_error_payload(int64_t* a, int64_t* b);
 const char* hs_error_kind_name(hs_status s); /* transfer_ledger.cpp:28-42 */
 
 /* ---- context (replaces hsolve::Runtime, executor.hpp:128-221) ---------- */
+hs_status hs_device_count(int* count); /* visible CUDA devices */
 /* stream: a cudaStream_t to order work on (NULL = the library creates one). */
 hs_status hs_ctx_create(int device, void* stream, hs_ctx** out);
 /* Multi-GPU: one process per GPU; nccl_id = 128 bytes from
@@ -88,6 +89,35 @@ typedef struct {
 hs_status hs_ctx_create_custom_comm(int device, void* stream, int rank, int world,
                                     const hs_comm_ops* ops, hs_ctx** out);
 void hs_ctx_destroy(hs_ctx* ctx);
+
+/* ---- single-process multi-GPU group (hsolve::Runtime with gpus > 1) ----
+ * The reference's Runtime drives its two executors from one orchestrator
+ * (executor.hpp:122-132); a group drives G ranks from one process: one
+ * hs_ctx per rank (rank r on devices[r], or device r % count when NULL) and
+ * one host thread per rank while a solve runs. transport: 0 = auto (NCCL via
+ * ncclCommInitAll when every rank has its own device, else in-process),
+ * 1 = NCCL, 2 = in-process (collectives are event-ordered device copies
+ * between the ranks' buffers: asynchronous like NCCL, never synchronizing a
+ * stream, and ranks may share a device). world == 1 is a plain context. */
+typedef struct hs_group hs_group;
+hs_status hs_group_create(int world, const int* devices, int transport,
+                          hs_group** out);
+void hs_group_destroy(hs_group* g);
+int hs_group_world(const hs_group* g);
+int hs_group_transport(const hs_group* g); /* resolved: 0 none, 1 NCCL, 2 in-process */
+hs_ctx* hs_group_ctx(hs_group* g, int rank);
+/* CG work split of a 2-rank group (SolverConfig::fraction,
+ * solver_config.hpp:8-16): rank 0 owns block rows [0, split), rank 1
+ * [split, N), split = floor(f N + 0.5) (partition.cpp:11-22) clamped to
+ * [1, N-1]; 0 or 1 = the tile-balanced split. Cholesky is 2D block-cyclic. */
+hs_status hs_group_set_row_fraction(hs_group* g, double fraction);
+hs_status hs_group_set_cholesky_gemm(hs_group* g, int slices);
+/* Runs fn(rank, hs_group_ctx(g, rank), arg) on one host thread per rank;
+ * returns the first failing rank's status (its message / payload in
+ * hs_last_error of the calling thread). */
+hs_status hs_group_run(hs_group* g, int (*fn)(int rank, hs_ctx* ctx, void* arg),
+                       void* arg);
+
 /* Release what the context keeps between calls: the device matrices cached
  * by the host-buffer entry points (hs_solve_cg_host etc. keep the uploaded
  * matrix), the CG workspace, the Cholesky's INT8 panel buffers and the
@@ -240,6 +270,21 @@ hs_status hs_forward_substitute_host(hs_ctx* ctx, size_t n, size_t b,
 hs_status hs_back_substitute_host(hs_ctx* ctx, size_t n, size_t b,
                                   const double* l_packed, const double* y,
                                   double* x);
+/* Host-buffer drop-ins over the group (solve_cg / factorize / solve_spd,
+ * cg_solver.hpp:48-49, cholesky_solver.hpp:44-58): CG row-sharded (each rank
+ * uploads its block rows), Cholesky 2D block-cyclic (each rank moves only its
+ * tiles); x is written once. Shapes the distributed kernels do not serve
+ * (CG b not in {64,128,256,512}, Cholesky b % 128 != 0) run on rank 0's GPU.
+ * The group's ledger is rank 0's (every collective once). */
+hs_status hs_group_solve_cg_host(hs_group* g, size_t n, size_t b,
+                                 const double* a_packed, const double* rhs,
+                                 const hs_cg_params* p, double* x,
+                                 hs_cg_stats* stats, double* trace);
+hs_status hs_group_factorize_host(hs_group* g, size_t n, size_t b,
+                                  double* a_packed, hs_chol_stats* stats);
+hs_status hs_group_solve_spd_host(hs_group* g, size_t n, size_t b,
+                                  double* a_packed, const double* rhs,
+                                  double* x, hs_chol_stats* stats);
 
 /* ---- single-tile kernels (block_kernels.hpp:17-31), for parity tests --- */
 /* Batched over `count` independent b x b tiles in device memory. */

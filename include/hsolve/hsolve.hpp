@@ -12,9 +12,10 @@
 // SolverConfig fields and validate(), exception types and ErrorKind names,
 // NotConverged as a status, factorize() in place with stale diagonal-tile
 // upper halves, solve_spd() destroying its matrix. Changed: arithmetic runs
-// on a B200 (Runtime = GPU context), `fraction` / `workers_*` / `slowdown_*`
-// are accepted but only `gpus` partitions work, and the transfer ledger of a
-// single-GPU run is empty (as in the reference's homogeneous modes).
+// on B200s (Runtime = GPU context, or a group of `gpus` GPUs), `fraction`
+// sets the CG row split of a 2-GPU Runtime, `workers_*` / `slowdown_*` are
+// accepted but unused, and the transfer ledger holds the multi-GPU
+// collectives (empty for one GPU, as in the reference's homogeneous modes).
 #pragma once
 
 #include <cstddef>
@@ -24,6 +25,7 @@
 #include <vector>
 
 struct hs_ctx;
+struct hs_group;
 
 namespace hsolve {
 
@@ -184,7 +186,17 @@ struct SolverConfig {
   double slowdown_b = 1.0;
   std::uint64_t seed = 42;
   bool record_trace = false;
-  int device = 0;  // B200 build: GPU ordinal of the Runtime
+  int device = 0;  // B200 build: GPU ordinal of the Runtime (rank 0's)
+  // B200 build: GPUs the work is partitioned over (the reference's two
+  // executors generalised to G devices of one process). CG shards block rows
+  // (with G == 2, `fraction` in (0, 1) gives rank 0 the reference's
+  // partition_for_fraction share, partition.cpp:11-22); Cholesky uses a 2D
+  // block-cyclic tile grid. Rank r runs on device (device + r) % count.
+  int gpus = 1;
+  // B200 build: collectives of a multi-GPU Runtime. 0 = auto (NCCL when every
+  // rank has its own device, else in-process), 1 = NCCL, 2 = in-process
+  // device copies (ranks may share a GPU).
+  int comm = 0;
   // B200 build: Cholesky trailing-update engine. 0 = FP64 DMMA tensor cores
   // (the reference's arithmetic); 1..8 = FP64 emulated on the INT8 tensor
   // cores with that many slices (8: FP64-level error bound).
@@ -270,7 +282,9 @@ class Runtime {
   std::uint64_t observed_transfer_bytes() const { return 0; }
   bool audit() const { return audit_; }
 
-  hs_ctx* native();  // the C-ABI context (created on first use)
+  hs_ctx* native();  // the C-ABI context (rank 0's with gpus > 1)
+  hs_group* group();  // the multi-GPU group (nullptr when gpus == 1)
+  int gpus() const { return gpus_; }
   void add_transfer_ms(double ms) { transfer_seconds_ += ms * 1e-3; }
   // Moves the context's NCCL ledger entries (one per collective) into
   // ledger(); called by the solvers after each native call.
@@ -278,7 +292,10 @@ class Runtime {
 
  private:
   int device_ = 0;
+  int gpus_ = 1;
+  int comm_ = 0;
   hs_ctx* ctx_ = nullptr;
+  hs_group* group_ = nullptr;
   TransferLedger ledger_;
   double transfer_seconds_ = 0.0;
   bool audit_ = true;

@@ -65,6 +65,7 @@ class Oracle:
                                        _sz, C.c_uint64, C.c_int, _dp]
         L.hso_generate_rhs.argtypes = [_sz, _sz, C.c_uint64, _dp]
         L.hso_symv.argtypes = [_sz, _sz, _dp, _dp, _dp, C.c_int]
+        L.hso_set_symv_order.argtypes = [C.c_int]
         L.hso_dot.restype = C.c_double
         L.hso_dot.argtypes = [_sz, _sz, _dp, _dp]
         L.hso_solve_cg.argtypes = [_sz, _sz, _dp, _dp, C.c_double, _sz, _sz, C.c_int,
@@ -110,6 +111,11 @@ class Oracle:
         y = np.zeros(nrows(n, b) * b)
         self.lib.hso_symv(n, b, a, np.ascontiguousarray(x), y, threads or os.cpu_count())
         return y
+
+    def set_symv_order(self, order: int) -> None:
+        """0 = the reference's accumulation order; 1 = per-tile partials
+        (the GPU SYMV's class) — for the iteration-envelope tests only."""
+        self.lib.hso_set_symv_order(int(order))
 
     def dot(self, n, b, u, v):
         return self.lib.hso_dot(n, b, u, v)

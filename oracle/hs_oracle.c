@@ -215,9 +215,20 @@ typedef struct {
   double* y;
 } symv_ctx;
 
+/* Accumulation-order switch, for measuring the CG iteration envelope only
+ * (tests/test_gpu_fullsize.py, tools/cg_envelope.py). 0 = the reference's
+ * order: one running sum per output row over ascending j, c
+ * (block_kernels.cpp:59-95). 1 = "tile partials": each tile's contribution
+ * to a row is summed from 0 over its b columns and then added to the row in
+ * ascending j, which is the accumulation class of the GPU SYMV (per-tile
+ * partial slots added in a fixed order). Same products, different rounding. */
+static int g_symv_order = 0;
+void hso_set_symv_order(int order) { g_symv_order = order; }
+
 static void symv_row(size_t row, void* p) {
   symv_ctx* s = (symv_ctx*)p;
   const size_t b = s->b;
+  const int tiled = g_symv_order == 1;
   double* out = s->y + row * b;
   for (size_t r = 0; r < b; ++r) out[r] = 0.0;
   for (size_t j = 0; j < s->rows; ++j) {
@@ -225,26 +236,26 @@ static void symv_row(size_t row, void* p) {
     if (j < row) {
       const double* blk = s->a + tri(row, j) * b * b;
       for (size_t r = 0; r < b; ++r) {
-        double acc = out[r];
+        double acc = tiled ? 0.0 : out[r];
         for (size_t c = 0; c < b; ++c) acc += blk[r * b + c] * xj[c];
-        out[r] = acc;
+        out[r] = tiled ? out[r] + acc : acc;
       }
     } else if (j == row) {
       const double* blk = s->a + tri(row, row) * b * b;
       for (size_t r = 0; r < b; ++r) {
-        double acc = out[r];
+        double acc = tiled ? 0.0 : out[r];
         for (size_t c = 0; c < b; ++c) {
           const double v = (c <= r) ? blk[r * b + c] : blk[c * b + r];
           acc += v * xj[c];
         }
-        out[r] = acc;
+        out[r] = tiled ? out[r] + acc : acc;
       }
     } else {
       const double* blk = s->a + tri(j, row) * b * b;
       for (size_t r = 0; r < b; ++r) {
-        double acc = out[r];
+        double acc = tiled ? 0.0 : out[r];
         for (size_t c = 0; c < b; ++c) acc += blk[c * b + r] * xj[c];
-        out[r] = acc;
+        out[r] = tiled ? out[r] + acc : acc;
       }
     }
   }

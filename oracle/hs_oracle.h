@@ -43,6 +43,9 @@ int hso_generate_spd(size_t n, size_t b, double sigma_f2, double length_scale,
 void hso_generate_rhs(size_t n, size_t b, uint64_t seed, double* out);
 
 /* block_kernels.cpp:59-100 over all block rows */
+/* envelope measurement only: 0 = reference accumulation order (default),
+ * 1 = per-tile partials added in ascending j (the GPU SYMV's class) */
+void hso_set_symv_order(int order);
 void hso_symv(size_t n, size_t b, const double* a, const double* x, double* y,
               int threads);
 /* block_kernels.cpp:102-121 (+ dd.hpp:18-40): full-range compensated dot */

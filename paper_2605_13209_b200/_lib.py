@@ -32,7 +32,10 @@ EXPORTED = [
     "hs_ctx_create", "hs_nccl_unique_id", "hs_ctx_create_nccl", "hs_ctx_destroy", "hs_ctx_trim",
     "hs_ctx_create_custom_comm",
     "hs_ctx_rank", "hs_ctx_world", "hs_ctx_stream", "hs_ctx_kernel_launches",
-    "hs_ctx_set_cholesky_gemm",
+    "hs_ctx_set_cholesky_gemm", "hs_device_count",
+    "hs_group_create", "hs_group_destroy", "hs_group_world", "hs_group_transport",
+    "hs_group_ctx", "hs_group_set_row_fraction", "hs_group_set_cholesky_gemm", "hs_group_run",
+    "hs_group_solve_cg_host", "hs_group_factorize_host", "hs_group_solve_spd_host",
     "hs_rng_at", "hs_rng_uniform_pm1", "hs_generate_inputs",
     "hs_median_pairwise_distance", "hs_generate_rhs",
     "hs_partition_for_fraction", "hs_cholesky_border", "hs_partition_rows",
@@ -114,6 +117,19 @@ def lib():
         "hs_ctx_create_custom_comm": (C.c_int, [C.c_int, vp, C.c_int, C.c_int,
                                                 C.POINTER(CommOps), pp]),
         "hs_ctx_destroy": (None, [vp]),
+        "hs_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+        "hs_group_create": (C.c_int, [C.c_int, vp, C.c_int, pp]),
+        "hs_group_destroy": (None, [vp]),
+        "hs_group_world": (C.c_int, [vp]),
+        "hs_group_transport": (C.c_int, [vp]),
+        "hs_group_ctx": (vp, [vp, C.c_int]),
+        "hs_group_set_row_fraction": (C.c_int, [vp, C.c_double]),
+        "hs_group_set_cholesky_gemm": (C.c_int, [vp, C.c_int]),
+        "hs_group_run": (C.c_int, [vp, vp, vp]),
+        "hs_group_solve_cg_host": (C.c_int, [vp, sz, sz, dp, dp, C.POINTER(CgParams), dp,
+                                             C.POINTER(CgStats), dp]),
+        "hs_group_factorize_host": (C.c_int, [vp, sz, sz, dp, C.POINTER(CholStats)]),
+        "hs_group_solve_spd_host": (C.c_int, [vp, sz, sz, dp, dp, dp, C.POINTER(CholStats)]),
         "hs_ctx_trim": (C.c_int, [vp]),
         "hs_ctx_rank": (C.c_int, [vp]),
         "hs_ctx_world": (C.c_int, [vp]),

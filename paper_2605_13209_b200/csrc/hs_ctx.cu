@@ -41,6 +41,7 @@ struct Nccl {
   void* h = nullptr;
   ncclResult_t (*GetUniqueId)(ncclUniqueId*);
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*);
   ncclResult_t (*CommDestroy)(ncclComm_t);
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t,
                             ncclComm_t, cudaStream_t);
@@ -68,6 +69,7 @@ static Nccl* load_nccl() {
   HS_REQUIRE(n->field, HS_ERR_CUDA, "NCCL symbol missing: " name);
   HS_SYM(GetUniqueId, "ncclGetUniqueId");
   HS_SYM(CommInitRank, "ncclCommInitRank");
+  HS_SYM(CommInitAll, "ncclCommInitAll");
   HS_SYM(CommDestroy, "ncclCommDestroy");
   HS_SYM(AllGather, "ncclAllGather");
   HS_SYM(ReduceScatter, "ncclReduceScatter");
@@ -97,6 +99,11 @@ static void custom_check(int r, const char* what) {
 
 void comm_allgather(hs_ctx* c, const double* send, double* recv,
                     size_t count, LedgerKind kind) {
+  if (c->local) {
+    local_allgather(c, send, recv, count, c->stream);
+    ledger_add(c, kind, (uint64_t)count * c->world * sizeof(double));
+    return;
+  }
   if (c->custom) {
     HS_CUDA(cudaStreamSynchronize(c->stream));
     custom_check(c->ops.allgather(c->ops.user, send, recv, count), "allgather");
@@ -111,6 +118,11 @@ void comm_allgather(hs_ctx* c, const double* send, double* recv,
 }
 void comm_reduce_scatter(hs_ctx* c, const double* send, double* recv,
                          size_t count, LedgerKind kind) {
+  if (c->local) {
+    local_reduce_scatter(c, send, recv, count, c->stream);
+    ledger_add(c, kind, (uint64_t)count * sizeof(double));
+    return;
+  }
   if (c->custom) {
     HS_CUDA(cudaStreamSynchronize(c->stream));
     custom_check(c->ops.reduce_scatter(c->ops.user, send, recv, count), "reduce_scatter");
@@ -126,6 +138,11 @@ void comm_reduce_scatter(hs_ctx* c, const double* send, double* recv,
 // broadcast from root's `send` into every rank's `recv` on stream s
 void comm_bcast_on(hs_ctx* c, const double* send, double* recv, size_t count,
                    int root, cudaStream_t s, LedgerKind kind) {
+  if (c->local) {
+    local_bcast(c, send, recv, count, root, s);
+    ledger_add(c, kind, (uint64_t)count * sizeof(double));
+    return;
+  }
   if (c->custom) {
     HS_CUDA(cudaStreamSynchronize(s));
     custom_check(c->ops.broadcast(c->ops.user, send, recv, count, root), "broadcast");
@@ -139,13 +156,18 @@ void comm_bcast_on(hs_ctx* c, const double* send, double* recv, size_t count,
   ledger_add(c, kind, (uint64_t)count * sizeof(double));
 }
 void comm_group(hs_ctx* c, bool start) {
-  if (c->custom) return;  // custom collectives complete one by one
+  if (c->custom || c->local) return;  // these collectives complete one by one
   nccl_check(c->nccl, start ? c->nccl->GroupStart() : c->nccl->GroupEnd(),
              "ncclGroupStart/End");
 }
 // element-wise max over ranks of `count` int64 values (in place)
 void comm_allreduce_max_i64(hs_ctx* c, int64_t* buf, size_t count,
                             cudaStream_t s) {
+  if (c->local) {
+    local_allreduce_max_i64(c, buf, count, s);
+    ledger_add(c, LK_SCALAR, (uint64_t)count * sizeof(int64_t));
+    return;
+  }
   if (c->custom) {
     HS_CUDA(cudaStreamSynchronize(s));
     custom_check(c->ops.allreduce_max_i64(c->ops.user, buf, count), "allreduce_max");
@@ -486,6 +508,20 @@ double* ctx_vec(hs_ctx* c, int slot, size_t count) {
   return c->vec[slot];
 }
 
+// One communicator per context of a single-process group over distinct
+// devices (ncclCommInitAll); rank r of the clique is ctxs[r].
+void nccl_init_all(hs_ctx** ctxs, int world) {
+  Nccl* n = load_nccl();
+  std::vector<int> devs(world);
+  for (int r = 0; r < world; ++r) devs[r] = ctxs[r]->device;
+  std::vector<ncclComm_t> comms(world);
+  nccl_check(n, n->CommInitAll(comms.data(), world, devs.data()), "ncclCommInitAll");
+  for (int r = 0; r < world; ++r) {
+    ctxs[r]->nccl = n;
+    ctxs[r]->comm = comms[r];
+  }
+}
+
 hs_matrix* cached_matrix(hs_ctx* c, int slot, size_t n, size_t b) {
   hs_matrix*& m = c->cache[slot];
   if (m && (m->n != n || m->b != b)) {
@@ -493,7 +529,8 @@ hs_matrix* cached_matrix(hs_ctx* c, int slot, size_t n, size_t b) {
     m = nullptr;
   }
   if (!m) {
-    const hs_status s = hs_matrix_create(c, n, b, &m);
+    const hs_status s =
+        slot >= 2 ? hs_matrix_create_cyclic(c, n, b, &m) : hs_matrix_create(c, n, b, &m);
     if (s != HS_OK) throw Failure{s, hs_last_error()};
   }
   m->has_inv = false;
@@ -558,6 +595,14 @@ static void ctx_common_init(hs_ctx* c, int device, void* stream) {
   HS_CUDA(cudaMalloc(&c->d_scalars, sizeof(CgScalars)));
   // room for two CgScalars snapshots (the CG poll double-buffers them)
   HS_CUDA(cudaMallocHost(&c->h_pinned, std::max(64 * sizeof(double), 2 * sizeof(CgScalars))));
+}
+
+hs_status hs_device_count(int* count) {
+  HS_API_BEGIN
+  HS_REQUIRE(count, HS_ERR_CONFIG, "null pointer");
+  *count = 0;
+  HS_CUDA(cudaGetDeviceCount(count));
+  HS_API_END
 }
 
 hs_status hs_ctx_create(int device, void* stream, hs_ctx** out) {
@@ -671,6 +716,7 @@ void hs_ctx_destroy(hs_ctx* c) {
     m = nullptr;
   }
   if (c->comm) c->nccl->CommDestroy((ncclComm_t)c->comm);
+  local_comm_release(c);
   for (cudaEvent_t e : c->prof_events) cudaEventDestroy(e);
   cudaFree(c->d_scalars);
   cudaFree(c->d_dpart);
@@ -788,6 +834,13 @@ hs_status hs_matrix_create(hs_ctx* c, size_t n, size_t b, hs_matrix** out) {
   m->b = b;
   m->N = (size_t)ceil_div(n, b);
   m->bounds = row_bounds((int64_t)m->N, c->world);
+  if (c->world == 2 && c->row_fraction > 0.0 && c->row_fraction < 1.0 && m->N >= 2) {
+    // the reference's executor split (partition.cpp:11-22): rank 0 plays B
+    // (block rows [0, split)), rank 1 plays A ([split, N)); each rank keeps
+    // at least one block row
+    const int64_t split = (int64_t)floor(c->row_fraction * (double)m->N + 0.5);
+    m->bounds[1] = std::min<int64_t>(std::max<int64_t>(split, 1), (int64_t)m->N - 1);
+  }
   m->row_lo = (size_t)m->bounds[c->rank];
   m->row_hi = (size_t)m->bounds[c->rank + 1];
   m->tile_lo = tri((int64_t)m->row_lo, 0);

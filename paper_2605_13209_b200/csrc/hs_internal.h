@@ -56,6 +56,7 @@ struct SymvPlan {
 namespace hs {
 struct OzPanel;
 struct HostStager;
+struct LocalComm;  // in-process device-copy collectives (hs_group.cu)
 }
 
 struct hs_ctx {
@@ -67,7 +68,13 @@ struct hs_ctx {
   void* comm = nullptr;  // ncclComm_t
   hs_comm_ops ops{};      // custom host transport (hs_ctx_create_custom_comm)
   bool custom = false;
-  bool distributed() const { return comm != nullptr || custom; }
+  // rank of a single-process group whose collectives are device copies
+  // between the ranks' buffers, ordered by events (hs_group.cu)
+  hs::LocalComm* local = nullptr;
+  bool distributed() const { return comm != nullptr || custom || local != nullptr; }
+  // CG row split of a 2-rank context: fraction of the block rows on rank 0
+  // (partition_for_fraction, partition.cpp:11-22); 0 = tile-balanced split
+  double row_fraction = 0.0;
   uint64_t launches = 0;
   int num_sms = 148;
   // profiling of the SYMV launches
@@ -101,7 +108,9 @@ struct hs_ctx {
   double* h_pinned = nullptr;  // small pinned readback buffer
   // device matrices reused by the host-buffer entry points (slot 0: the
   // solve matrix, slot 1: the unfactored copy kept for the residual)
-  hs_matrix* cache[2] = {nullptr, nullptr};
+  // (slots 2, 3: the same for the 2D block-cyclic layout of a multi-rank
+  // Cholesky)
+  hs_matrix* cache[4] = {nullptr, nullptr, nullptr, nullptr};
   // communication ledger: one entry per NCCL collective (multi-rank only);
   // `step` is the CG iteration / Cholesky column the drivers are in
   std::vector<hs_ledger_entry> ledger;
@@ -187,6 +196,19 @@ void launch_fill(hs_ctx* c, double* p, double v, int64_t count);
 // Scratch matrix of the context for host-buffer calls (created on first use
 // or when the shape changes; contents are overwritten by the caller).
 hs_matrix* cached_matrix(hs_ctx* c, int slot, size_t n, size_t b);
+// In-process group collectives (hs_group.cu): the same contract as the NCCL
+// calls they replace, enqueued on stream `s` without blocking the host on
+// the GPU (an issue-time rendezvous of the rank threads, then event-ordered
+// device copies; peers' buffers are read only after their producers ran).
+void local_allgather(hs_ctx* c, const double* send, double* recv, size_t count,
+                     cudaStream_t s);
+void local_reduce_scatter(hs_ctx* c, const double* send, double* recv, size_t count,
+                          cudaStream_t s);
+void local_bcast(hs_ctx* c, const double* send, double* recv, size_t count, int root,
+                 cudaStream_t s);
+void local_allreduce_max_i64(hs_ctx* c, int64_t* buf, size_t count, cudaStream_t s);
+void local_comm_release(hs_ctx* c);
+void nccl_init_all(hs_ctx** ctxs, int world);
 // cuTensorMapEncodeTiled through the runtime's driver entry point (hs_chol.cu):
 // `rank`-D map, dims / box in elements, strides (rank-1 of them) in bytes.
 CUtensorMap make_tensor_map(CUtensorMapDataType type, const void* base, int rank,

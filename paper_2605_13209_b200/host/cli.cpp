@@ -59,6 +59,8 @@ const std::vector<Opt>& options() {
       {"no-warmup", Kind::flag, S | W},
       {"device", Kind::size, G | S | W},
       {"fp64-emulation-slices", Kind::size, S | W},
+      {"gpus", Kind::size, S | W},
+      {"comm", Kind::size, S | W},
       {"fractions", Kind::text, W},
       {"sizes", Kind::text, W},
       {"block-sizes", Kind::text, W},
@@ -206,7 +208,9 @@ void usage(std::ostream& os) {
         "solver options: --block-size --fraction --eps --max-iters --recompute-interval\n"
         "  --workers-a --workers-b --slowdown-a --slowdown-b --reps --seed --no-warmup\n"
         "  --device --fp64-emulation-slices S (Cholesky update on the INT8 tensor\n"
-        "  cores, 1..8; 0 = FP64 DMMA); kernel options: --sigma-f2 --sigma-n2\n"
+        "  cores, 1..8; 0 = FP64 DMMA) --gpus G (one process, G GPUs; --fraction\n"
+        "  sets rank 0's CG row share at G = 2) --comm 0|1|2 (auto / NCCL /\n"
+        "  in-process); kernel options: --sigma-f2 --sigma-n2\n"
         "  --length-scale --dim;\n"
         "  --config FILE (key=value, [command] sections; flags override)\n";
 }
@@ -299,6 +303,8 @@ Common apply(const Values& v) {
   if (auto s = get("slowdown-a")) c.cfg.slowdown_a = as_real("slowdown-a", *s);
   if (auto s = get("slowdown-b")) c.cfg.slowdown_b = as_real("slowdown-b", *s);
   if (auto s = get("device")) c.cfg.device = (int)as_size("device", *s);
+  if (auto s = get("gpus")) c.cfg.gpus = (int)as_size("gpus", *s);
+  if (auto s = get("comm")) c.cfg.comm = (int)as_size("comm", *s);
   if (auto s = get("fp64-emulation-slices"))
     c.cfg.emulated_fp64_slices = (int)as_size("fp64-emulation-slices", *s);
   if (auto s = get("reps")) c.reps = as_size("reps", *s);

@@ -54,9 +54,10 @@ hs_ctx* default_ctx() {
   return ctx;
 }
 
-CholeskyPlan plan_for(const SolverConfig& cfg, std::size_t rows) {
-  if (cfg.fraction > 0.0 && cfg.fraction < 1.0)
-    return CholeskyPlan::for_fraction(cfg.fraction, rows);
+// The plan a factorization reports: the GPU paths never run the reference's
+// moving-border CPU/GPU split (one GPU, or a static 2D block-cyclic grid),
+// so no borders and no shift events -- only the requested fraction.
+CholeskyPlan plan_for(const SolverConfig& cfg, std::size_t) {
   CholeskyPlan p;
   p.fraction = cfg.fraction;
   return p;
@@ -168,6 +169,8 @@ void SolverConfig::validate() const {
     throw ConfigError("slowdown factors must be >= 1.0");
   if (emulated_fp64_slices < 0 || emulated_fp64_slices > 8)
     throw ConfigError("emulated_fp64_slices must be in [0, 8]");
+  if (gpus < 1) throw ConfigError("gpus must be >= 1");
+  if (comm < 0 || comm > 2) throw ConfigError("comm must be 0 (auto), 1 (NCCL) or 2 (in-process)");
 }
 
 Partition partition_for_fraction(double f, std::size_t rows) {
@@ -246,13 +249,31 @@ Runtime::Runtime(std::size_t wa, std::size_t wb, double sa, double sb, bool audi
   if (!(sa >= 1.0) || !(sb >= 1.0)) throw ConfigError("slowdown factors must be >= 1.0");
 }
 
-Runtime::Runtime(const SolverConfig& cfg) : device_(cfg.device) { cfg.validate(); }
+Runtime::Runtime(const SolverConfig& cfg)
+    : device_(cfg.device), gpus_(cfg.gpus), comm_(cfg.comm) {
+  cfg.validate();
+}
 
 Runtime::~Runtime() {
-  if (ctx_) hs_ctx_destroy(ctx_);
+  if (group_) hs_group_destroy(group_);
+  else if (ctx_) hs_ctx_destroy(ctx_);
+}
+
+hs_group* Runtime::group() {
+  if (gpus_ <= 1) return nullptr;
+  if (!group_) {
+    int count = 0;
+    check(hs_device_count(&count));
+    std::vector<int> dev(gpus_);
+    for (int r = 0; r < gpus_; ++r) dev[r] = (device_ + r) % std::max(count, 1);
+    check(hs_group_create(gpus_, dev.data(), comm_, &group_));
+    ctx_ = hs_group_ctx(group_, 0);
+  }
+  return group_;
 }
 
 hs_ctx* Runtime::native() {
+  if (gpus_ > 1) return (group(), ctx_);
   if (!ctx_) check(hs_ctx_create(device_, nullptr, &ctx_));
   return ctx_;
 }
@@ -325,8 +346,14 @@ CgResult solve_cg(const BlockedSPDMatrix& a, const BlockVector& rhs,
                  cfg.record_trace ? 1 : 0};
   hs_cg_stats st{};
   std::vector<double> trace(cfg.record_trace ? 3 * std::max<std::size_t>(cfg.max_iters, 1) : 0);
-  check(hs_solve_cg_host(rt.native(), a.n(), a.block_size(), a.data(), rhs.data(), &p,
-                         res.x.data(), &st, cfg.record_trace ? trace.data() : nullptr));
+  if (hs_group* g = rt.group()) {
+    check(hs_group_set_row_fraction(g, cfg.fraction));
+    check(hs_group_solve_cg_host(g, a.n(), a.block_size(), a.data(), rhs.data(), &p,
+                                 res.x.data(), &st, cfg.record_trace ? trace.data() : nullptr));
+  } else {
+    check(hs_solve_cg_host(rt.native(), a.n(), a.block_size(), a.data(), rhs.data(), &p,
+                           res.x.data(), &st, cfg.record_trace ? trace.data() : nullptr));
+  }
   rt.add_transfer_ms(st.transfer_ms);
   rt.sync_ledger();
   res.stats.iterations = st.iterations;
@@ -336,9 +363,13 @@ CgResult solve_cg(const BlockedSPDMatrix& a, const BlockVector& rhs,
   res.stats.true_residual = st.true_residual;
   res.stats.wall_ms = st.wall_ms;
   res.stats.compute_ms = st.compute_ms;
-  res.stats.partition =
-      cfg.fraction > 0.0 ? partition_for_fraction(cfg.fraction, a.block_rows())
-                         : Partition{0, cfg.fraction};
+  // the split that ran: rank 0's block rows with 2 GPUs (partition.hpp:8-18
+  // semantics for B = rank 0), none on one GPU
+  res.stats.partition = Partition{0, cfg.fraction};
+  if (rt.gpus() == 2 && cfg.fraction > 0.0 && cfg.fraction < 1.0 && a.block_rows() >= 2)
+    res.stats.partition.split_row =
+        std::min(std::max<std::size_t>(partition_for_fraction(cfg.fraction, a.block_rows()).split_row, 1),
+                 a.block_rows() - 1);
   for (std::size_t k = 0; cfg.record_trace && k < st.iterations; ++k)
     res.stats.trace.push_back({trace[3 * k], trace[3 * k + 1], trace[3 * k + 2]});
   return res;
@@ -347,8 +378,13 @@ CgResult solve_cg(const BlockedSPDMatrix& a, const BlockVector& rhs,
 FactorizeStats factorize(BlockedSPDMatrix& a, const SolverConfig& cfg, Runtime& rt) {
   cfg.validate();
   hs_chol_stats st{};
-  check(hs_ctx_set_cholesky_gemm(rt.native(), cfg.emulated_fp64_slices));
-  check(hs_factorize_host(rt.native(), a.n(), a.block_size(), a.data(), &st));
+  if (hs_group* g = rt.group()) {
+    check(hs_group_set_cholesky_gemm(g, cfg.emulated_fp64_slices));
+    check(hs_group_factorize_host(g, a.n(), a.block_size(), a.data(), &st));
+  } else {
+    check(hs_ctx_set_cholesky_gemm(rt.native(), cfg.emulated_fp64_slices));
+    check(hs_factorize_host(rt.native(), a.n(), a.block_size(), a.data(), &st));
+  }
   rt.add_transfer_ms(st.transfer_ms);
   rt.sync_ledger();
   FactorizeStats out;
@@ -383,9 +419,15 @@ SpdSolveResult solve_spd(BlockedSPDMatrix& a, const BlockVector& rhs,
     throw ConfigError("matrix and right-hand side shapes do not match");
   SpdSolveResult res{BlockVector(a.n(), a.block_size()), SpdSolveStats{}};
   hs_chol_stats st{};
-  check(hs_ctx_set_cholesky_gemm(rt.native(), cfg.emulated_fp64_slices));
-  check(hs_solve_spd_host(rt.native(), a.n(), a.block_size(), a.data(), rhs.data(),
-                          res.x.data(), &st));
+  if (hs_group* g = rt.group()) {
+    check(hs_group_set_cholesky_gemm(g, cfg.emulated_fp64_slices));
+    check(hs_group_solve_spd_host(g, a.n(), a.block_size(), a.data(), rhs.data(),
+                                  res.x.data(), &st));
+  } else {
+    check(hs_ctx_set_cholesky_gemm(rt.native(), cfg.emulated_fp64_slices));
+    check(hs_solve_spd_host(rt.native(), a.n(), a.block_size(), a.data(), rhs.data(),
+                            res.x.data(), &st));
+  }
   rt.add_transfer_ms(st.transfer_ms);
   rt.sync_ledger();
   res.stats.plan = plan_for(cfg, a.block_rows());

@@ -140,6 +140,7 @@ class SolverConfig:
     seed: int = 42
     record_trace: bool = False
     gpus: int = 1  # B200 build: number of GPUs the work is partitioned over
+    comm: int = 0  # multi-GPU collectives: 0 auto, 1 NCCL, 2 in-process copies
 
     def validate(self) -> None:  # solver_config.cpp:9-26
         if not (self.eps > 0.0):
@@ -154,6 +155,8 @@ class SolverConfig:
             raise ConfigError("slowdown factors must be >= 1.0")
         if self.gpus < 1:
             raise ConfigError("gpus must be >= 1")
+        if self.comm not in (0, 1, 2):
+            raise ConfigError("comm must be 0 (auto), 1 (NCCL) or 2 (in-process)")
 
 
 @dataclass
@@ -312,6 +315,17 @@ class Runtime:
         if cfg is not None:
             cfg.validate()
         self._L = _lib.lib()
+        self.group = None
+        gpus = cfg.gpus if cfg is not None else 1
+        if _handle is None and gpus > 1:
+            # one process, G GPUs (hs_group): rank r on device (device + r) % count
+            cnt = C.c_int(0)
+            _check(self._L.hs_device_count(C.byref(cnt)))
+            devs = (C.c_int * gpus)(*[(device + r) % max(cnt.value, 1) for r in range(gpus)])
+            g = C.c_void_p()
+            _check(self._L.hs_group_create(gpus, devs, cfg.comm, C.byref(g)))
+            self.group = g
+            _handle = C.c_void_p(self._L.hs_group_ctx(g, 0))
         if _handle is not None:
             self.ctx = _handle
         else:
@@ -389,7 +403,10 @@ class Runtime:
     def set_cholesky_gemm(self, slices: int) -> None:
         """Cholesky trailing-update engine: 0 = FP64 DMMA (default), 1..8 =
         FP64 emulated on the INT8 tensor cores with that many slices."""
-        _check(self._L.hs_ctx_set_cholesky_gemm(self.ctx, int(slices)))
+        if self.group:
+            _check(self._L.hs_group_set_cholesky_gemm(self.group, int(slices)))
+        else:
+            _check(self._L.hs_ctx_set_cholesky_gemm(self.ctx, int(slices)))
 
     def trim(self) -> None:
         """Release cached device matrices / workspaces (hs_ctx_trim)."""
@@ -399,8 +416,23 @@ class Runtime:
         if getattr(self, "ctx", None):
             for m in list(getattr(self, "_matrices", ())):
                 m.free()
-            self._L.hs_ctx_destroy(self.ctx)
+            if getattr(self, "group", None):
+                self._L.hs_group_destroy(self.group)
+                self.group = None
+            else:
+                self._L.hs_ctx_destroy(self.ctx)
             self.ctx = None
+
+    @property
+    def gpus(self) -> int:
+        return self._L.hs_group_world(self.group) if self.group else 1
+
+    @property
+    def transport(self) -> str:
+        """Collectives of a multi-GPU Runtime: "nccl", "in-process" or "none"."""
+        if not self.group:
+            return "none"
+        return {0: "none", 1: "nccl", 2: "in-process"}[self._L.hs_group_transport(self.group)]
 
     def __del__(self):
         try:
@@ -649,12 +681,16 @@ def _cg_params(cfg: SolverConfig) -> CgParams:
                     1 if cfg.record_trace else 0)
 
 
-def _cg_stats(st: CgStats, tr: np.ndarray | None, cfg: SolverConfig, rows: int) -> CgStatsPy:
+def _cg_stats(st: CgStats, tr: np.ndarray | None, cfg: SolverConfig, rows: int,
+              gpus: int = 1) -> CgStatsPy:
     out = CgStatsPy(int(st.iterations), int(st.recomputations), bool(st.converged),
                     st.u0, st.true_residual, st.wall_ms, st.compute_ms, st.transfer_ms)
-    out.partition = Partition(0 if cfg.fraction == 0.0 else
-                              partition_for_fraction(cfg.fraction, rows).split_row,
-                              cfg.fraction)
+    # the split that ran: rank 0's block rows of a 2-GPU Runtime (clamped to
+    # [1, N-1]); none on one GPU
+    split = 0
+    if gpus == 2 and 0.0 < cfg.fraction < 1.0 and rows >= 2:
+        split = min(max(partition_for_fraction(cfg.fraction, rows).split_row, 1), rows - 1)
+    out.partition = Partition(split, cfg.fraction)
     if tr is not None:
         k = out.iterations
         out.trace = [CgIteration(*tr[3 * i:3 * i + 3]) for i in range(k)]
@@ -678,10 +714,17 @@ def solve_cg(a: BlockedSPDMatrix, rhs: BlockVector, cfg: SolverConfig,
     st = CgStats()
     tr = np.zeros(3 * max(cfg.max_iters, 1)) if cfg.record_trace else None
     p = _cg_params(cfg)
-    _check(rt._L.hs_solve_cg_host(rt.ctx, a.n, a.b, a.values.ctypes.data,
-                                  rhs.values.ctypes.data, C.byref(p), x.values.ctypes.data,
-                                  C.byref(st), tr.ctypes.data if tr is not None else None))
-    return CgResult(x, _cg_stats(st, tr, cfg, a.rows))
+    if rt.group:
+        _check(rt._L.hs_group_set_row_fraction(rt.group, cfg.fraction))
+        _check(rt._L.hs_group_solve_cg_host(rt.group, a.n, a.b, a.values.ctypes.data,
+                                            rhs.values.ctypes.data, C.byref(p),
+                                            x.values.ctypes.data, C.byref(st),
+                                            tr.ctypes.data if tr is not None else None))
+    else:
+        _check(rt._L.hs_solve_cg_host(rt.ctx, a.n, a.b, a.values.ctypes.data,
+                                      rhs.values.ctypes.data, C.byref(p), x.values.ctypes.data,
+                                      C.byref(st), tr.ctypes.data if tr is not None else None))
+    return CgResult(x, _cg_stats(st, tr, cfg, a.rows, rt.gpus))
 
 
 def solve_cg_device(rt: Runtime, a: DeviceMatrix, d_rhs: int, d_x: int,
@@ -740,7 +783,11 @@ def factorize(a: BlockedSPDMatrix, cfg: SolverConfig, rt: Runtime | None = None
     cfg.validate()
     rt = rt or default_runtime()
     st = CholStats()
-    _check(rt._L.hs_factorize_host(rt.ctx, a.n, a.b, a.values.ctypes.data, C.byref(st)))
+    if rt.group:
+        _check(rt._L.hs_group_factorize_host(rt.group, a.n, a.b, a.values.ctypes.data,
+                                             C.byref(st)))
+    else:
+        _check(rt._L.hs_factorize_host(rt.ctx, a.n, a.b, a.values.ctypes.data, C.byref(st)))
     return FactorizeStats(st.factor_ms, st.compute_ms, st.transfer_ms)
 
 
@@ -772,9 +819,10 @@ def solve_spd(a: BlockedSPDMatrix, rhs: BlockVector, cfg: SolverConfig,
     rt = rt or default_runtime()
     x = BlockVector(a.n, a.b)
     st = CholStats()
-    _check(rt._L.hs_solve_spd_host(rt.ctx, a.n, a.b, a.values.ctypes.data,
-                                   rhs.values.ctypes.data, x.values.ctypes.data,
-                                   C.byref(st)))
+    f = (lambda *a_: rt._L.hs_group_solve_spd_host(rt.group, *a_)) if rt.group else (
+        lambda *a_: rt._L.hs_solve_spd_host(rt.ctx, *a_))
+    _check(f(a.n, a.b, a.values.ctypes.data, rhs.values.ctypes.data, x.values.ctypes.data,
+             C.byref(st)))
     return SpdSolveResult(x, SpdSolveStats(st.factor_ms, st.solve_ms, st.wall_ms,
                                            st.compute_ms, st.transfer_ms, st.true_residual))
 

@@ -55,3 +55,17 @@ def test_cpp_matrix_io_and_cli_gpu_part(tmp_path):
     out = subprocess.run([_build_io(tmp_path), "--gpu"], capture_output=True, text=True,
                          timeout=600)
     assert out.returncode == 0 and "ALL PASSED" in out.stdout, out.stdout + out.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_multigpu_runtime(tmp_path):
+    """SolverConfig::gpus = 2 through the reference API (in-process transport
+    on a one-GPU box, NCCL with two GPUs)."""
+    exe = str(tmp_path / "test_hsolve_multigpu")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "test_hsolve_multigpu.cpp"), "-o", exe,
+                    "-L", PKG, "-lhsolve_b200", "-lhsolve_cuda", f"-Wl,-rpath,{PKG}"],
+                   check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(out.stdout)
+    assert out.returncode == 0 and "ALL PASSED" in out.stdout, out.stdout + out.stderr

@@ -1,16 +1,19 @@
 """Full BASELINE.json sizes on one B200, checked through size-independent
-properties (no CPU oracle finishes at these sizes):
+properties. Parity with the reference itself at configs[1] / configs[2]
+(golden outputs of the compiled reference, and a live reference CG run on
+the host cores) lives in tests/test_gpu_reference_fullsize.py; this file
+adds:
 
 * cfg2 CG n=32768, b=128: converges to eps = 1e-6 with the true residual
   within the reference bound 2 eps sqrt(u0) (test_cg_solver.cpp:76-91),
-  in a comparable iteration count (45 on the CPU, 39 here), and
-  agrees with the Cholesky solution of the same system;
+  and agrees with the Cholesky solution of the same system;
 * SYMV symmetry s^T (A t) = t^T (A s) and linearity A(s + t) = As + At;
 * cfg3 Cholesky n=32768, b=512: relative residual <= 1e-10 (reference
   test_cholesky_solver.cpp:255-269), DMMA and INT8-emulated, factors
   within 1e-11 of each other;
-* n=131072 (cfg4/5 sizes, 68.8 GB): CG converges with the reference bound;
-  the INT8-emulated Cholesky solves to 1e-10.
+* n=131072 (cfg4/5 sizes, 68.8 GB): the reference needs more host memory
+  and hours of CPU here, so CG is checked by convergence with the reference
+  bound and the INT8-emulated Cholesky by a 1e-10 residual.
 """
 import numpy as np
 import pytest
@@ -39,9 +42,9 @@ def test_cfg2_cg_full_size(rt):
     m = hs.generate_spd_device(rt, n, b, seed=42)
     st, x, rhs = cg_solve(rt, m, n, b)
     assert st.converged
-    # the reference CPU run takes 45; the count is rounding-order sensitive
-    # (the trace is chaotic), measured 39 here (FMA SYMV)
-    assert 30 <= st.iterations <= 60, st.iterations
+    # measured envelope of summation-order variants at this size: 39..46
+    # (profiles/r02_cg_envelope.json; test_gpu_reference_fullsize.py)
+    assert 37 <= st.iterations <= 48, st.iterations
     assert st.true_residual <= 2e-6 * np.sqrt(st.u0)
     # SYMV symmetry and linearity (fixed-order, deterministic kernels)
     g = torch.Generator(device="cuda").manual_seed(5)

@@ -1,0 +1,129 @@
+"""Single-process multi-GPU Runtime (hs_group) through the Python mirror of
+the reference API, on one GPU: G ranks share the device and talk through the
+in-process transport, whose collectives are event-ordered device copies that
+never synchronize a stream (unlike the blocking host-callback transport of
+tests/test_multirank_gpu.py). So the distributed CG and the 2D block-cyclic
+Cholesky -- with its lookahead streams and panel broadcasts overlapping the
+trailing updates -- run with real asynchronous stream ordering, checked
+against the oracle (cholesky_solver.cpp:177-198, cg_solver.cpp:141-146,
+209-215, 333-335).
+"""
+import numpy as np
+import pytest
+
+import paper_2605_13209_b200 as hs
+
+pytestmark = pytest.mark.gpu
+
+
+def _rt(world, **kw):
+    return hs.Runtime(hs.SolverConfig(gpus=world, comm=2, **kw))
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("n,b", [(1024, 64), (2000, 128), (4096, 256), (3072, 512)])
+def test_group_cg_matches_oracle(oracle, world, n, b):
+    a = oracle.generate_spd(n, b, seed=7)
+    rhs = oracle.generate_rhs(n, b, seed=7)
+    ref = oracle.solve_cg(n, b, a, rhs, eps=1e-6)
+    rt = _rt(world)
+    try:
+        assert rt.gpus == world and rt.transport == "in-process"
+        cfg = hs.SolverConfig(block_size=b, eps=1e-6, record_trace=True, gpus=world, comm=2)
+        res = hs.solve_cg(hs.BlockedSPDMatrix(n, b, a), hs.BlockVector(n, b, rhs), cfg, rt)
+    finally:
+        rt.close()
+    st = res.stats
+    assert st.converged and abs(st.iterations - ref["iterations"]) <= 2
+    assert st.true_residual <= 2e-6 * np.sqrt(st.u0)
+    x = res.x.values[:n]
+    assert np.linalg.norm(x - ref["x"][:n]) <= 1e-6 * np.linalg.norm(ref["x"][:n])
+    tr = np.array([[t.u, t.alpha, t.beta] for t in st.trace[:5]])
+    np.testing.assert_allclose(tr, ref["trace"][:5], rtol=1e-10)
+
+
+@pytest.mark.parametrize("f", [0.25, 0.5, 0.85])
+def test_group_cg_fraction_split(oracle, f):
+    n, b = 2048, 64
+    a = oracle.generate_spd(n, b, seed=21)
+    rhs = oracle.generate_rhs(n, b, seed=21)
+    ref = oracle.solve_cg(n, b, a, rhs, eps=1e-6)
+    cfg = hs.SolverConfig(block_size=b, fraction=f, gpus=2, comm=2)
+    rt = hs.Runtime(cfg)
+    try:
+        res = hs.solve_cg(hs.BlockedSPDMatrix(n, b, a), hs.BlockVector(n, b, rhs), cfg, rt)
+    finally:
+        rt.close()
+    assert res.stats.partition.split_row == oracle.partition_for_fraction(f, n // b)
+    assert res.stats.converged
+    assert np.linalg.norm(res.x.values[:n] - ref["x"][:n]) <= 1e-6 * np.linalg.norm(ref["x"][:n])
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("slices", [0, 8], ids=["dmma", "int8_emulated"])
+@pytest.mark.parametrize("n,b", [(1536, 128), (2048, 512)])
+def test_group_cholesky_matches_oracle(oracle, world, slices, n, b):
+    a = oracle.generate_spd(n, b, seed=9)
+    rhs = oracle.generate_rhs(n, b, seed=9)
+    st, L_ref, _, _ = oracle.factorize(n, b, a)
+    assert st == 0
+    sref = oracle.solve_spd(n, b, a, rhs)
+    cfg = hs.SolverConfig(block_size=b, gpus=world, comm=2)
+    rt = hs.Runtime(cfg)
+    try:
+        rt.set_cholesky_gemm(slices)
+        L = hs.BlockedSPDMatrix(n, b, a.copy())
+        hs.factorize(L, cfg, rt)
+        sp = hs.solve_spd(hs.BlockedSPDMatrix(n, b, a.copy()), hs.BlockVector(n, b, rhs), cfg, rt)
+    finally:
+        rt.close()
+    amax = np.abs(a).max()
+    N = n // b
+    for i in range(N):  # lower triangles only (diagonal-tile upper halves are stale)
+        for j in range(i + 1):
+            k = (i * (i + 1) // 2 + j) * b * b
+            got = L.values[k:k + b * b].reshape(b, b)
+            want = L_ref[k:k + b * b].reshape(b, b)
+            if i == j:
+                got, want = np.tril(got), np.tril(want)
+            assert np.abs(got - want).max() <= 1e-10 * amax, (i, j)
+    x = sp.x.values[:n]
+    assert np.linalg.norm(x - sref["x"][:n]) <= 1e-10 * np.linalg.norm(sref["x"][:n])
+    assert sp.stats.true_residual <= 1e-10 * np.linalg.norm(rhs[:n])
+
+
+def test_group_not_spd_and_ledger(oracle):
+    n, b = 1024, 128
+    a = hs.BlockedSPDMatrix(n, b, oracle.generate_spd(n, b, seed=2))
+    a.set(700, 700, -5.0)
+    cfg = hs.SolverConfig(block_size=b, gpus=2, comm=2)
+    rt = hs.Runtime(cfg)
+    try:
+        with pytest.raises(hs.NotSpdError) as ei:
+            hs.factorize(a, cfg, rt)
+        assert ei.value.block_row == 700 // b and ei.value.pivot_index == 700 % b
+        # the runtime stays usable after an agreed failure
+        ok = hs.BlockedSPDMatrix(n, b, oracle.generate_spd(n, b, seed=2))
+        rt.ledger(clear=True)
+        hs.factorize(ok, cfg, rt)
+        blk = [e for e in rt.ledger() if e.kind == "block"]
+        N = n // b
+        assert len(blk) == 2 * N + N * (N - 1) // 2
+    finally:
+        rt.close()
+
+
+def test_group_repeated_solves_stay_consistent(oracle):
+    """Many back-to-back solves on one group (collective parity, event reuse)."""
+    n, b = 1024, 128
+    a = oracle.generate_spd(n, b, seed=3)
+    rhs = oracle.generate_rhs(n, b, seed=3)
+    cfg = hs.SolverConfig(block_size=b, gpus=3, comm=2)
+    rt = hs.Runtime(cfg)
+    try:
+        xs = [hs.solve_cg(hs.BlockedSPDMatrix(n, b, a), hs.BlockVector(n, b, rhs), cfg,
+                          rt).x.values.copy() for _ in range(4)]
+    finally:
+        rt.close()
+    for x in xs[1:]:
+        assert np.array_equal(x, xs[0])  # deterministic run to run
