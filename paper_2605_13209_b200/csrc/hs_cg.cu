@@ -1343,7 +1343,14 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   // drains while the host checks.
   const uint64_t check_every = 4;
   CgScalars* pin = reinterpret_cast<CgScalars*>(c->h_pinned);
-  cudaEvent_t ev[2];
+  struct PollEvents {  // destroyed on every exit path, including throws
+    cudaEvent_t e[2] = {nullptr, nullptr};
+    ~PollEvents() {
+      for (cudaEvent_t x : e)
+        if (x) cudaEventDestroy(x);
+    }
+  } pe;
+  cudaEvent_t* ev = pe.e;
   HS_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
   HS_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
   int pending = -1;
@@ -1427,8 +1434,6 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
     }
   }
   ht("loop");
-  cudaEventDestroy(ev[0]);
-  cudaEventDestroy(ev[1]);
   HS_CUDA(cudaMemcpyAsync(&h, c->d_scalars, sizeof(CgScalars),
                           cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
@@ -1463,6 +1468,10 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
                               (ghi - glo) * b * sizeof(double),
                               cudaMemcpyDeviceToDevice, c->stream));
   }
+  // the solve ends here; the exit diagnostic below is untimed, as in the
+  // reference (cg_solver.cpp:354-365)
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  st->compute_ms = ms_since(ht0);
   // exit diagnostic: ||rhs - A x|| (cg_solver.cpp:360-365)
   symv_to(c, m, B.x_full, B.t, false, nullptr, nullptr);
   if (dp) comm_reduce_scatter(c, B.t, B.t_loc, (size_t)chunk, LK_SUBVECTOR);
@@ -1654,10 +1663,8 @@ hs_status hs_cg_solve(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   HS_REQUIRE(m->ctx == c, HS_ERR_CONFIG, "matrix belongs to another context");
   HS_CUDA(cudaSetDevice(c->device));
   std::memset(st, 0, sizeof(*st));
-  const auto t0 = std::chrono::steady_clock::now();
-  cg_run(c, m, d_rhs, p, d_x, st, trace);
-  st->wall_ms = ms_since(t0);
-  st->compute_ms = st->wall_ms;
+  cg_run(c, m, d_rhs, p, d_x, st, trace);  // sets compute_ms (exit diagnostic excluded)
+  st->wall_ms = st->compute_ms;
   HS_API_END
 }
 
@@ -1669,12 +1676,15 @@ hs_status hs_solve_cg_host(hs_ctx* c, size_t n, size_t b, const double* a,
   HS_REQUIRE(p->eps > 0.0, HS_ERR_CONFIG, "eps must be positive");
   HS_CUDA(cudaSetDevice(c->device));
   std::memset(st, 0, sizeof(*st));
-  const auto t0 = std::chrono::steady_clock::now();
+  // device storage cached by the context across calls (allocated once)
   hs_matrix* m = cached_matrix(c, 0, n, b);
   const size_t pn = (size_t)ceil_div(n, b) * b;
   double* d_rhs = ctx_vec(c, 0, pn);
   double* d_x = ctx_vec(c, 1, pn);
   {
+    // wall = initial transfer + solve + result download; compute = the
+    // solve; the exit residual diagnostic is outside both
+    // (cg_solver.cpp:232-234, 354-356)
     const auto tt = std::chrono::steady_clock::now();
     hs_status s = hs_matrix_upload(m, a);
     if (s != HS_OK) throw Failure{s, hs_last_error()};
@@ -1688,9 +1698,8 @@ hs_status hs_solve_cg_host(hs_ctx* c, size_t n, size_t b, const double* a,
                             c->stream));
     HS_CUDA(cudaStreamSynchronize(c->stream));
     xfer += ms_since(t2);
-    st->wall_ms = ms_since(t0);
     st->transfer_ms = xfer;
-    st->compute_ms = st->wall_ms - xfer;
+    st->wall_ms = xfer + st->compute_ms;
   }
   HS_API_END
 }

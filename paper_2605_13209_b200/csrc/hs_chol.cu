@@ -775,10 +775,14 @@ __global__ void __launch_bounds__(256)
             failed = k;
             break;
           }
+          // akk = +Inf passes the pivot test as in potf_block
+          // (block_kernels.cpp:9-21): L_kk = sqrt(Inf) = Inf and the column
+          // below is finite / Inf = 0 (rsqrt(Inf) = 0); akk * rinv would be
+          // NaN there, so the diagonal takes akk itself
           const double rinv = rsqrt(akk);
           const double lrk = lane > k ? Dp[lane * DLD + k] * rinv : 0.0;
           __syncwarp();
-          if (lane == k) Dp[k * DLD + k] = akk * rinv;
+          if (lane == k) Dp[k * DLD + k] = isinf(akk) ? akk : akk * rinv;
           if (lane > k) Dp[lane * DLD + k] = lrk;
           __syncwarp();
 // column k of L comes from the owning lanes by shuffle; only this lane's
@@ -2124,9 +2128,19 @@ static void ensure_inverses(hs_ctx* c, hs_matrix* m) {
 // factor (cholesky_solver.cpp:287-309); with the factor spread over ranks
 // the steps are pipelined over tile rows instead and only b-double blocks
 // move, never a tile.
+// The substitution kernels stage 2b doubles (+ the diagonal tile's share)
+// in shared memory: b <= 2048. Checked before any factorization that is
+// followed by a solve, so an unsupported b fails before A is overwritten.
+static void require_trsv_block(size_t b) {
+  HS_REQUIRE(b <= 2048, HS_ERR_CONFIG,
+             "block size " + std::to_string(b) +
+                 " unsupported in the triangular solves (b <= 2048)");
+}
+
 static void trsv_run_dist(hs_ctx* c, hs_matrix* m, double* v, bool upper) {
   HS_REQUIRE(m->layout == 1, HS_ERR_CONFIG,
              "multi-rank triangular solves need a block-cyclic factor");
+  require_trsv_block(m->b);
   ensure_inverses(c, m);
   const int b = (int)m->b;
   const int cb = compute_block(b), f = b / cb;
@@ -2199,8 +2213,7 @@ static void trsv_run(hs_ctx* c, hs_matrix* m, double* v, bool upper) {
   ensure_inverses(c, m);
   const int b = (int)m->b;
   const int cb = compute_block(b), f = b / cb;
-  HS_REQUIRE(b <= 2048, HS_ERR_CONFIG,
-             "block size unsupported in the triangular solves");
+  require_trsv_block(m->b);
   const int64_t N = (int64_t)m->N;
   const size_t dsm = (2 * (size_t)b + (trsv_staged(b, cb, f) ? trsv_staged_doubles(cb, f) : 0)) *
                          sizeof(double),
@@ -2284,6 +2297,7 @@ hs_status hs_solve_spd(hs_ctx* c, hs_matrix* a, const double* d_rhs,
                        hs_chol_stats* st) {
   HS_API_BEGIN
   HS_REQUIRE(c && a && d_rhs && d_x, HS_ERR_CONFIG, "null pointer");
+  require_trsv_block(a->b);  // before the factorization overwrites A
   HS_CUDA(cudaSetDevice(c->device));
   hs_chol_stats s{};
   const auto t0 = std::chrono::steady_clock::now();
@@ -2337,6 +2351,7 @@ hs_status hs_solve_spd_host(hs_ctx* c, size_t n, size_t b, double* a_packed,
                             const double* rhs, double* x, hs_chol_stats* st) {
   HS_API_BEGIN
   HS_REQUIRE(c && a_packed && rhs && x, HS_ERR_CONFIG, "null pointer");
+  require_trsv_block(b);
   HS_CUDA(cudaSetDevice(c->device));
   hs_matrix* m = cached_matrix(c, 0, n, b);
   hs_matrix* orig = cached_matrix(c, 1, n, b);

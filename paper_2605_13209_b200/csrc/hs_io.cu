@@ -124,8 +124,19 @@ Header read_header(int fd, uint64_t file_size, const char* path) {
     throw Failure{HS_ERR_FORMAT, "implausible header (n = " + std::to_string(r.n) +
                                      ", b = " + std::to_string(r.b) + ") in " + path};
   r.N = (r.n + r.b - 1) / r.b;
-  r.values = r.N * (r.N + 1) / 2 * r.b * r.b;
-  const uint64_t expected = kHeader + r.values * 8;
+  // N (N + 1) / 2 * b^2 * 8 + header, every step overflow-checked: a header
+  // whose size wraps 64 bits would otherwise pass the truncation check
+  uint64_t tiles = 0, bb = 0, expected = 0;
+  const bool wraps = __builtin_mul_overflow(r.N, r.N + 1, &tiles) ||
+                     __builtin_mul_overflow(tiles / 2, 1, &tiles) ||
+                     __builtin_mul_overflow(r.b, r.b, &bb) ||
+                     __builtin_mul_overflow(tiles, bb, &r.values) ||
+                     __builtin_mul_overflow(r.values, (uint64_t)8, &expected) ||
+                     __builtin_add_overflow(expected, (uint64_t)kHeader, &expected);
+  if (wraps)
+    throw Failure{HS_ERR_FORMAT, "implausible header (n = " + std::to_string(r.n) +
+                                     ", b = " + std::to_string(r.b) +
+                                     ": size overflows 64 bits) in " + path};
   if (file_size < expected)
     throw Failure{HS_ERR_TRUNCATED_FILE,
                   "file truncated: expected " + std::to_string(expected) +

