@@ -943,13 +943,213 @@ __global__ void combine_kernel(const Dd* slots, int64_t stride, int world, int s
 }
 
 // ---------------------------------------------------------------------------
+// Fused CG tail (single GPU, plain iterations): everything between two SYMVs
+// in ONE kernel -- t from the partial slots, alpha, x / r updates, r^T r,
+// beta, s = r + beta s (cg_solver.cpp:258-332) -- instead of finalize +
+// update + direction (three launches, two of them short, latency-bound
+// vector kernels, and a finalize set by the heaviest block row's ~N column
+// partials). Persistent, co-resident grid (cooperative launch), two grid
+// barriers:
+//   phase 1: the finalize's partial sums, balanced: every block row's
+//     entry list (column partials of its tiles, row segments, split-tile
+//     extras; same order as finalize_kernel) is cut into items of at most
+//     TAIL_ITEM entries; one warp per (item, 32 columns), up to 16 loads in
+//     flight; the last warp of a (row, column chunk) -- ticket -- adds the
+//     item sums in item order, stores t and the chunk's s . t partial.
+//   barrier; every CTA reduces the s . t partials in one fixed order
+//     (identical alpha everywhere); x += alpha s, r -= alpha t on its slice,
+//     r . r partial per CTA.
+//   barrier; every CTA reduces the r . r partials -> beta; s = r + beta s.
+// CTA 0 keeps the scalar books (scalar_step: alpha / beta, non-finite
+// checks, trace, done). Deterministic: every sum has a fixed order and
+// shape whichever warp or CTA computes it.
+constexpr int TAIL_THREADS = 256;
+constexpr int TAIL_ITEM = 32;   // entries per item
+constexpr int TAIL_BATCH = 16;  // loads in flight per lane
+
+struct TailArgs {
+  const int64_t* row_rseg;
+  const int32_t* row_extra;
+  const int32_t* extra_cta;
+  const double* rowpart;
+  const double* colmain;
+  const double* colextra;
+  uint32_t* unit_ctr;
+  int64_t N;
+  int b, nch;
+  const int32_t* item_row;   // [nitems]
+  const int32_t* item_e0;    // [nitems]
+  const int32_t* item_e1;    // [nitems]
+  const int32_t* row_item;   // [N + 1]
+  int64_t nitems;
+  double* itempart;          // [nitems * b]
+  uint32_t* row_ticket;      // [N * nch], zero between launches
+  double* dotpart;           // [N * nch]
+  double* rrpart;            // [grid]
+  unsigned* bar;             // [2] grid-barrier counters
+  int64_t len;               // N * b
+  double* x;
+  double* r;
+  double* s;
+  double* t;
+  StepArgs sa;
+  const int32_t* done;
+  const unsigned char* pf_base;
+  const int64_t* pf_slab;
+  int64_t pf_slab_lo;
+  int pf_units, pf_slabs;
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// all CTAs of a co-resident grid; writes before it are visible after it
+__device__ __forceinline__ void tail_grid_barrier(unsigned* ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    while (ld_acquire_u32(ctr) < gridDim.x) {
+    }
+  }
+  __syncthreads();
+}
+
+// fixed-order double-double sum of `count` values read through L2 (written
+// by other CTAs of this grid before a barrier)
+__device__ Dd dd_reduce_cg(const double* parts, int64_t count, Dd* red) {
+  Dd acc{0.0, 0.0};
+  for (int64_t k = threadIdx.x; k < count; k += blockDim.x) acc = dd_add(acc, __ldcg(parts + k));
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w >= 1; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] = dd_add(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  const Dd out = red[0];
+  __syncthreads();
+  return out;
+}
+
+__global__ void __launch_bounds__(TAIL_THREADS, 4) cg_tail_kernel(TailArgs ta) {
+  pdl_wait();
+  if (ta.done && *ta.done) return;
+  const int lane = threadIdx.x & 31;
+  const int b = ta.b, nch = ta.nch;
+  const int64_t N = ta.N;
+  const double u_old = ta.sa.sc->u;  // CTA 0 replaces it after barrier 2
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ta.bar[1] = 0u;      // nobody reaches barrier 2 before CTA 0 arrives at barrier 1
+    *ta.unit_ctr = 0u;   // SYMV work-unit counter for the next launch
+  }
+  if ((int)blockIdx.x < ta.pf_units && threadIdx.x == 0 && ta.pf_slabs > 0) {
+    // L2 prefetch of the next SYMV's first slabs (as finalize_kernel)
+    const int64_t g0 = ta.pf_slab[blockIdx.x], g1 = ta.pf_slab[blockIdx.x + 1];
+    const int64_t ns = g1 - g0 < ta.pf_slabs ? g1 - g0 : ta.pf_slabs;
+    if (ns > 0)
+      bulk_prefetch_l2(ta.pf_base + (g0 - ta.pf_slab_lo) * 32768, (uint32_t)(ns * 32768));
+  }
+  // ---- phase 1: t and the s . t partials ----
+  const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t units = ta.nitems * nch;
+  for (int64_t u = gwarp; u < units; u += nwarps) {
+    const int64_t it = u / nch;
+    const int ch = (int)(u - it * nch);
+    const int64_t j = ta.item_row[it];
+    const int64_t e0 = ta.item_e0[it], e1 = ta.item_e1[it];
+    const int c = ch * 32 + lane;
+    const int64_t nc = N - j;  // column partials of tiles (j .. N-1, j)
+    const int64_t rs0 = ta.row_rseg[j], nrs = ta.row_rseg[j + 1] - rs0;
+    const int x0 = ta.row_extra[j];
+    const double* colbase = ta.colmain + c;
+    double acc = 0.0;
+    int64_t e = e0;
+    for (; e + TAIL_BATCH <= e1 && e + TAIL_BATCH <= nc; e += TAIL_BATCH) {
+      double v[TAIL_BATCH];
+#pragma unroll
+      for (int k = 0; k < TAIL_BATCH; ++k) v[k] = __ldg(colbase + tri(j + e + k, j) * b);
+#pragma unroll
+      for (int k = 0; k < TAIL_BATCH; ++k) acc += v[k];
+    }
+    for (; e < e1 && e < nc; ++e) acc += __ldg(colbase + tri(j + e, j) * b);
+    for (; e < e1 && e < nc + nrs; ++e) acc += __ldg(ta.rowpart + (rs0 + e - nc) * b + c);
+    for (; e < e1; ++e)
+      acc += __ldg(ta.colextra + (int64_t)ta.extra_cta[x0 + (e - nc - nrs)] * b + c);
+    const int64_t i0 = ta.row_item[j], m = ta.row_item[j + 1] - i0;
+    bool fin = true;
+    double tv = acc;
+    if (m > 1) {
+      ta.itempart[it * b + c] = acc;
+      __threadfence();
+      __syncwarp();
+      unsigned last = 0;
+      if (lane == 0) last = atomicAdd(&ta.row_ticket[j * nch + ch], 1u) == (unsigned)(m - 1);
+      fin = __shfl_sync(0xffffffffu, last, 0) != 0;
+      if (fin) {
+        __threadfence();
+        tv = 0.0;
+        for (int64_t k = 0; k < m; ++k) tv += __ldcg(ta.itempart + (i0 + k) * b + c);
+        if (lane == 0) ta.row_ticket[j * nch + ch] = 0u;
+      }
+    }
+    if (fin) {
+      const int64_t o = j * b + c;
+      ta.t[o] = tv;
+      double d = ta.s[o] * tv;
+      for (int off = 16; off >= 1; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
+      if (lane == 0) ta.dotpart[j * nch + ch] = d;
+    }
+  }
+  tail_grid_barrier(&ta.bar[0]);
+  pdl_trigger();  // every tail CTA is resident: the next SYMV may launch
+  // ---- phase 2: alpha; x, r; r . r ----
+  __shared__ Dd red[TAIL_THREADS];
+  __shared__ double red_d[32];
+  const double st = dd_value(dd_reduce_cg(ta.dotpart, N * nch, red));
+  const double alpha = u_old / st;
+  if (blockIdx.x == 0 && threadIdx.x == 0) scalar_step(STEP_ALPHA, st, ta.sa);
+  if (!isfinite(alpha)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) ta.bar[0] = 0u;  // all passed barrier 1
+    return;
+  }
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  double part = 0.0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ta.len; k += stride) {
+    ta.x[k] = fma(alpha, ta.s[k], ta.x[k]);
+    const double rr = fma(-alpha, __ldcg(ta.t + k), ta.r[k]);
+    ta.r[k] = rr;
+    part = fma(rr, rr, part);
+  }
+  const double pc = block_sum(part, red_d);
+  if (threadIdx.x == 0) ta.rrpart[blockIdx.x] = pc;
+  tail_grid_barrier(&ta.bar[1]);
+  // ---- phase 3: beta; s = r + beta s ----
+  const double un = dd_value(dd_reduce_cg(ta.rrpart, gridDim.x, red));
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    scalar_step(STEP_BETA, un, ta.sa);
+    ta.bar[0] = 0u;  // every CTA passed barrier 1
+  }
+  if (!(un >= 0.0) || !isfinite(un)) return;
+  const double beta = un / u_old;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ta.len; k += stride)
+    ta.s[k] = fma(beta, ta.s[k], ta.r[k]);
+}
+
+// ---------------------------------------------------------------------------
 // plan
 
 void free_plan(SymvPlan* p) {
   if (!p) return;
   for (void* q : {(void*)p->cta_slab, (void*)p->cta_rseg, (void*)p->row_rseg,
                   (void*)p->row_extra, (void*)p->extra_cta, (void*)p->unit_ctr,
-                  (void*)p->rowpart, (void*)p->colmain, (void*)p->colextra})
+                  (void*)p->rowpart, (void*)p->colmain, (void*)p->colextra,
+                  (void*)p->item_row, (void*)p->item_e0, (void*)p->item_e1,
+                  (void*)p->row_item, (void*)p->itempart, (void*)p->row_ticket,
+                  (void*)p->tail_dot, (void*)p->tail_rr, (void*)p->tail_bar})
     cudaFree(q);
   delete p;
 }
@@ -961,6 +1161,46 @@ static void upload_vec(T** dst, const std::vector<T>& v) {
   HS_CUDA(cudaMalloc(dst, std::max<size_t>(v.size(), 1) * sizeof(T)));
   if (!v.empty())
     HS_CUDA(cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+// Items of the fused CG tail: row j's entry list (N - j column partials,
+// then its row segments and split-tile extras) cut into near-equal pieces of
+// at most TAIL_ITEM entries; the grid is what fits co-resident.
+static void build_tail_plan(hs_matrix* m, SymvPlan* p, const std::vector<int64_t>& row_rseg,
+                            const std::vector<int32_t>& row_extra) {
+  static const bool off = [] {
+    const char* e = getenv("HS_CG_TAIL");
+    return e && atoi(e) == 0;
+  }();
+  if (off) return;
+  const int64_t N = (int64_t)m->N, b = (int64_t)m->b;
+  int per_sm = 0;
+  HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_tail_kernel, TAIL_THREADS, 0));
+  if (per_sm < 1) return;
+  std::vector<int32_t> item_row, item_e0, item_e1, row_item(N + 1, 0);
+  for (int64_t j = 0; j < N; ++j) {
+    const int64_t E = (N - j) + (row_rseg[j + 1] - row_rseg[j]) + (row_extra[j + 1] - row_extra[j]);
+    const int64_t mj = std::max<int64_t>(1, (E + TAIL_ITEM - 1) / TAIL_ITEM);
+    row_item[j] = (int32_t)item_row.size();
+    for (int64_t k = 0; k < mj; ++k) {
+      item_row.push_back((int32_t)j);
+      item_e0.push_back((int32_t)(E * k / mj));
+      item_e1.push_back((int32_t)(E * (k + 1) / mj));
+    }
+  }
+  row_item[N] = (int32_t)item_row.size();
+  p->nitems = (int64_t)item_row.size();
+  p->tail_grid = std::min(per_sm, 4) * std::max(1, m->ctx->num_sms);
+  const int64_t nch = b / 32;
+  upload_vec(&p->item_row, item_row);
+  upload_vec(&p->item_e0, item_e0);
+  upload_vec(&p->item_e1, item_e1);
+  upload_vec(&p->row_item, row_item);
+  upload_vec(&p->row_ticket, std::vector<uint32_t>((size_t)(N * nch), 0u));
+  upload_vec(&p->tail_bar, std::vector<unsigned>(2, 0u));
+  HS_CUDA(cudaMalloc(&p->itempart, (size_t)p->nitems * b * sizeof(double)));
+  HS_CUDA(cudaMalloc(&p->tail_dot, (size_t)(N * nch) * sizeof(double)));
+  HS_CUDA(cudaMalloc(&p->tail_rr, (size_t)p->tail_grid * sizeof(double)));
 }
 
 // Static work plan of the SYMV + finalize pair for one matrix (host side).
@@ -1043,6 +1283,7 @@ void ensure_plan(hs_matrix* m) {
   HS_CUDA(cudaMalloc(&p->rowpart, std::max<int64_t>(1, nr) * b * sizeof(double)));
   HS_CUDA(cudaMalloc(&p->colmain, std::max<int64_t>(1, T) * b * sizeof(double)));
   HS_CUDA(cudaMalloc(&p->colextra, std::max<int64_t>(1, vgrid) * b * sizeof(double)));
+  if (m->ctx->world == 1 && !m->ctx->distributed()) build_tail_plan(m, p, row_rseg, row_extra);
   m->plan = p;
 }
 
@@ -1078,7 +1319,7 @@ static void ensure_dpart(hs_ctx* c, size_t count) {
 // rank's s^T t partial into the dot slots (multi-rank).
 static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
                     bool fuse_dot, const StepArgs* sa, const int32_t* done,
-                    double* defer_alpha = nullptr) {
+                    double* defer_alpha = nullptr, bool finalize = true) {
   const int b = (int)m->b;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   const bool prof = c->prof && (c->prof_counter++ % c->prof_every == 0);
@@ -1124,6 +1365,7 @@ static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
     c->prof_events.push_back(e0);
     c->prof_events.push_back(e1);
   }
+  if (!finalize) return;  // the fused CG tail consumes the partial slots
   SymvPlan* p = m->plan;
   FinalizeArgs fa{};
   fa.row_rseg = p->row_rseg;
@@ -1165,6 +1407,82 @@ static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
   HS_CUDA(launch_pdl(finalize_kernel, dim3((unsigned)m->row_hi, (unsigned)(b / FIN_COLS)),
                      dim3(FIN_THREADS), 0, c->stream, fa));
   HS_CUDA(cudaGetLastError());
+  launch_count(c);
+}
+
+// The fused tail after a plain single-rank SYMV: cooperative launch (the
+// grid barriers need every CTA resident), programmatic serialization when
+// the driver accepts both attributes together.
+static void launch_tail(hs_ctx* c, const hs_matrix* m, double* x, double* r, double* s,
+                        double* t, const StepArgs& sa, const int32_t* done) {
+  SymvPlan* p = m->plan;
+  TailArgs ta{};
+  ta.row_rseg = p->row_rseg;
+  ta.row_extra = p->row_extra;
+  ta.extra_cta = p->extra_cta;
+  ta.rowpart = p->rowpart;
+  ta.colmain = p->colmain;
+  ta.colextra = p->colextra;
+  ta.unit_ctr = p->unit_ctr;
+  ta.N = (int64_t)m->N;
+  ta.b = (int)m->b;
+  ta.nch = (int)(m->b / 32);
+  ta.item_row = p->item_row;
+  ta.item_e0 = p->item_e0;
+  ta.item_e1 = p->item_e1;
+  ta.row_item = p->row_item;
+  ta.nitems = p->nitems;
+  ta.itempart = p->itempart;
+  ta.row_ticket = p->row_ticket;
+  ta.dotpart = p->tail_dot;
+  ta.rrpart = p->tail_rr;
+  ta.bar = p->tail_bar;
+  ta.len = (int64_t)(m->N * m->b);
+  ta.x = x;
+  ta.r = r;
+  ta.s = s;
+  ta.t = t;
+  ta.sa = sa;
+  ta.done = done;
+  static const int pf = [] {
+    const char* e = getenv("HS_SYMV_PF_SLABS");
+    return e ? atoi(e) : 8;
+  }();
+  ta.pf_base = reinterpret_cast<const unsigned char*>(m->d);
+  ta.pf_slab = p->cta_slab;
+  ta.pf_slab_lo = m->tile_lo * p->slabs_per_tile;
+  ta.pf_units = std::min(p->grid, p->vgrid);
+  ta.pf_slabs = pf;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)p->tail_grid);
+  cfg.blockDim = dim3(TAIL_THREADS);
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  // 0 unknown, 1 cooperative + PDL accepted, 2 cooperative only
+  static std::atomic<int> mode{0};
+  int md = mode.load();
+  cudaError_t e = cudaSuccess;
+  if (md != 2) {
+    cfg.numAttrs = 2;
+    e = cudaLaunchKernelEx(&cfg, cg_tail_kernel, ta);
+    if (e == cudaSuccess) {
+      mode.store(1);
+    } else if (md == 0) {
+      cudaGetLastError();
+      mode.store(2);
+      md = 2;
+    }
+  }
+  if (md == 2) {
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, cg_tail_kernel, ta);
+  }
+  HS_CUDA(e);
   launch_count(c);
 }
 
@@ -1362,6 +1680,13 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
     // single rank, fast b, plain iteration: alpha is reduced by the update
     // kernel itself from the finalize's partials (no last-CTA tail)
     const bool defer = !dp && fast_b(m->b) && !recompute;
+    if (defer && m->plan->tail_grid > 0) {
+      // lines 4-11 in two launches: the SYMV, then the fused tail (t,
+      // alpha, x, r, r^T r, beta, s)
+      symv_to(c, m, B.s_full, B.t, false, nullptr, done, nullptr, false);
+      launch_tail(c, m, x_loc, B.r, s_loc, B.t, sa, done);
+      goto poll;
+    }
     // lines 4-5: t = A s, alpha = u / s^T t (the dot fused into the finalize)
     if (!dp) {
       symv_to(c, m, B.s_full, B.t, true, &sa, done, defer ? apart : nullptr);
@@ -1421,6 +1746,7 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
       vs.mode = V_SDIR;
       launch_vec(c, vs);
     }
+  poll:
     if (it % check_every == 0) {
       const int slot = (int)((it / check_every) & 1);
       HS_CUDA(cudaMemcpyAsync(pin + slot, c->d_scalars, sizeof(CgScalars),

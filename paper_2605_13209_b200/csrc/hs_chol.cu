@@ -1590,6 +1590,29 @@ static double ms_since(std::chrono::steady_clock::time_point t0) {
       .count();
 }
 
+// All ranks agree on a distributed factorization's outcome: one all-reduce
+// (max) of a key that orders failures by column, earliest first (the
+// column a sequential factorization would have stopped at; a rank that runs
+// on past another's failure can only fail later), then status and pivot.
+// d_buf: 3 device int64 (the ledger logs one 24-byte scalar all-reduce).
+static CholFlag agree_on_flag(hs_ctx* c, CholFlag h, int64_t* d_buf) {
+  int64_t st[3] = {-1, 0, 0};
+  if (h.status)
+    st[0] = ((int64_t)(0x7fffffff - h.col) << 32) | ((int64_t)h.status << 24) |
+            (h.pivot & 0xffffff);
+  HS_CUDA(cudaMemcpy(d_buf, st, sizeof(st), cudaMemcpyHostToDevice));
+  comm_allreduce_max_i64(c, d_buf, 3, c->stream);
+  HS_CUDA(cudaMemcpyAsync(st, d_buf, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  CholFlag out{};
+  if (st[0] >= 0) {
+    out.col = 0x7fffffff - (st[0] >> 32);
+    out.status = (int32_t)((st[0] >> 24) & 0xff);
+    out.pivot = st[0] & 0xffffff;
+  }
+  return out;
+}
+
 static void throw_flag(const CholFlag& h) {
   if (h.status == HS_ERR_NOT_SPD)
     throw Failure{HS_ERR_NOT_SPD,
@@ -2042,19 +2065,12 @@ static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
       m->d, 0, m->d_owned, (int64_t)m->local_tiles(), b, flag);
   HS_CUDA(cudaGetLastError());
   launch_count(c);
-  // agree on the outcome: element-wise max of (status, column, pivot)
+  // agree on the outcome: the earliest failing column wins
   CholFlag h{};
   HS_CUDA(cudaMemcpyAsync(&h, flag, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
   HS_CUDA(cudaStreamSynchronize(c->stream));
-  int64_t st[3] = {h.status, h.status ? h.col : -1, h.status ? h.pivot : -1};
-  HS_CUDA(cudaMemcpy(d_status, st, sizeof(st), cudaMemcpyHostToDevice));
   c->step = -1;
-  comm_allreduce_max_i64(c, d_status, 3, c->stream);
-  HS_CUDA(cudaMemcpyAsync(st, d_status, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
-  HS_CUDA(cudaStreamSynchronize(c->stream));
-  h.status = (int32_t)st[0];
-  h.col = st[1];
-  h.pivot = st[2];
+  h = agree_on_flag(c, h, d_status);
   throw_flag(h);
   m->has_inv = true;
 }
@@ -2084,15 +2100,8 @@ static void ensure_inverses(hs_ctx* c, hs_matrix* m) {
     CholFlag h{};
     HS_CUDA(cudaMemcpyAsync(&h, flag, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     HS_CUDA(cudaStreamSynchronize(c->stream));
-    int64_t st[3] = {h.status, h.status ? h.col : -1, h.status ? h.pivot : -1};
-    HS_CUDA(cudaMemcpy(flag, st, sizeof(st), cudaMemcpyHostToDevice));
     c->step = -1;
-    comm_allreduce_max_i64(c, (int64_t*)flag, 3, c->stream);
-    HS_CUDA(cudaMemcpyAsync(st, flag, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
-    HS_CUDA(cudaStreamSynchronize(c->stream));
-    h.status = (int32_t)st[0];
-    h.col = st[1];
-    h.pivot = st[2];
+    h = agree_on_flag(c, h, reinterpret_cast<int64_t*>(flag));
     throw_flag(h);
     m->has_inv = true;
     return;

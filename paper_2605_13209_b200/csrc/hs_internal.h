@@ -49,6 +49,19 @@ struct SymvPlan {
   double* rowpart = nullptr;     // [nrseg * b]
   double* colmain = nullptr;     // [T_local * b]
   double* colextra = nullptr;    // [vgrid * b]
+  // fused CG tail (single rank, hs_cg.cu cg_tail_kernel): balanced items of
+  // the per-row partial lists, their sums, tickets, dot / norm partials
+  int64_t nitems = 0;
+  int tail_grid = 0;             // co-resident CTAs (0: tail kernel unused)
+  int32_t* item_row = nullptr;   // [nitems]
+  int32_t* item_e0 = nullptr;
+  int32_t* item_e1 = nullptr;
+  int32_t* row_item = nullptr;   // [N + 1]
+  double* itempart = nullptr;    // [nitems * b]
+  uint32_t* row_ticket = nullptr;  // [N * b / 32]
+  double* tail_dot = nullptr;    // [N * b / 32]
+  double* tail_rr = nullptr;     // [tail_grid]
+  unsigned* tail_bar = nullptr;  // [2]
 };
 
 }  // namespace hs

@@ -26,6 +26,12 @@ def test_group_cg_matches_oracle(oracle, world, n, b):
     a = oracle.generate_spd(n, b, seed=7)
     rhs = oracle.generate_rhs(n, b, seed=7)
     ref = oracle.solve_cg(n, b, a, rhs, eps=1e-6)
+    one = hs.Runtime()
+    try:  # the single-GPU solve: same accumulation class as the ranks
+        single = hs.solve_cg(hs.BlockedSPDMatrix(n, b, a), hs.BlockVector(n, b, rhs),
+                             hs.SolverConfig(block_size=b, eps=1e-6), one).stats.iterations
+    finally:
+        one.close()
     rt = _rt(world)
     try:
         assert rt.gpus == world and rt.transport == "in-process"
@@ -34,7 +40,11 @@ def test_group_cg_matches_oracle(oracle, world, n, b):
     finally:
         rt.close()
     st = res.stats
-    assert st.converged and abs(st.iterations - ref["iterations"]) <= 2
+    # iteration count: +-2 of the single-GPU solve; against the reference
+    # order the measured rounding-order envelope (39..46 at n=32768,
+    # profiles/r02_cg_envelope.json) -> within 20 %
+    assert st.converged and abs(st.iterations - single) <= 2
+    assert abs(st.iterations - ref["iterations"]) <= max(2, 0.2 * ref["iterations"])
     assert st.true_residual <= 2e-6 * np.sqrt(st.u0)
     x = res.x.values[:n]
     assert np.linalg.norm(x - ref["x"][:n]) <= 1e-6 * np.linalg.norm(ref["x"][:n])
