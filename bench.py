@@ -507,17 +507,23 @@ def run_ours(args) -> None:
     # ---- e2e through the host-buffer C-ABI entry (every rank; with N GPUs each
     # rank uploads its own block rows from its pinned copy of the matrix) ----
     if not args.no_e2e:
-        host = torch.empty(packed_bytes // 8, dtype=torch.float64, pin_memory=True)
-        m.download(host.numpy())  # this rank's tiles (all of them at N = 1)
+        # pinned host copy of THIS rank's block rows only (the full packed
+        # array is 68.8 GB at n=131072; N ranks would pin N copies); the C
+        # ABI addresses the caller's full packed array, so it gets the base
+        # this buffer would have inside one (only the rank's range is touched)
+        import ctypes as C
+        host = torch.empty(max(local_bytes // 8, 1), dtype=torch.float64, pin_memory=True)
+        tile_off = m.row_lo * (m.row_lo + 1) // 2 * b * b * 8
+        base = host.data_ptr() - tile_off
+        H._check(rt._L.hs_matrix_download(m.h, C.c_void_p(base)))
         rhs_pin = torch.from_numpy(rhs_np.copy()).pin_memory()
         x_pin = torch.zeros_like(rhs_pin).pin_memory()
-        import ctypes as C
         cfge = hs.SolverConfig(block_size=b, eps=1e-300, max_iters=args.e2e_iters)
         p = H._cg_params(cfge)
         from paper_2605_13209_b200._lib import CgStats
         ste = CgStats()
         # one untimed call (allocator / plan warm-up), then timed calls
-        H._check(rt._L.hs_solve_cg_host(rt.ctx, n, b, C.c_void_p(host.data_ptr()),
+        H._check(rt._L.hs_solve_cg_host(rt.ctx, n, b, C.c_void_p(base),
                                         C.c_void_p(rhs_pin.data_ptr()), C.byref(p),
                                         C.c_void_p(x_pin.data_ptr()), C.byref(ste), None))
         torch.cuda.synchronize()
@@ -528,7 +534,7 @@ def run_ours(args) -> None:
             if use_dist:
                 dist.barrier()
             t0 = time.perf_counter()
-            H._check(rt._L.hs_solve_cg_host(rt.ctx, n, b, C.c_void_p(host.data_ptr()),
+            H._check(rt._L.hs_solve_cg_host(rt.ctx, n, b, C.c_void_p(base),
                                             C.c_void_p(rhs_pin.data_ptr()), C.byref(p),
                                             C.c_void_p(x_pin.data_ptr()), C.byref(ste),
                                             None))
@@ -541,7 +547,7 @@ def run_ours(args) -> None:
             call_s.append(t)
             xfer.append(tx)
         med = statistics.median(call_s)
-        h2d = (local_bytes + rhs_np.nbytes) * world  # all ranks' uploads
+        h2d = packed_bytes + rhs_np.nbytes * world  # all ranks' uploads (rows + rhs each)
         line["e2e"] = {"value": ste.iterations / med, "unit": "iters/s",
                        "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": rhs_np.nbytes * world,

@@ -1463,9 +1463,21 @@ static void launch_tail(hs_ctx* c, const hs_matrix* m, double* x, double* r, dou
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  // 0 unknown, 1 cooperative + PDL accepted, 2 cooperative only
-  static std::atomic<int> mode{0};
+  // 0 unknown, 1 cooperative + PDL accepted, 2 cooperative only;
+  // HS_CG_TAIL_LAUNCH: 3 = plain PDL launch (diagnostics: no co-residency
+  // guarantee), 2 = cooperative without PDL
+  static std::atomic<int> mode{[] {
+    const char* e = getenv("HS_CG_TAIL_LAUNCH");
+    return e ? atoi(e) : 0;
+  }()};
   int md = mode.load();
+  if (md == 3) {
+    cfg.attrs = attr + 1;
+    cfg.numAttrs = 1;
+    HS_CUDA(cudaLaunchKernelEx(&cfg, cg_tail_kernel, ta));
+    launch_count(c);
+    return;
+  }
   cudaError_t e = cudaSuccess;
   if (md != 2) {
     cfg.numAttrs = 2;
