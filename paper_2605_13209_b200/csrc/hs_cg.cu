@@ -86,6 +86,9 @@ __device__ unsigned long long g_symv_ts[4096][2];
 // finalize per launch: [0] min CTA start (after the PDL wait), [1] max end of
 // the partial-slot sums, [2] max CTA end (incl. the dot epilogue)
 __device__ unsigned long long g_fin_ts[4096][5];  // + [3] max start, [4] max sums time
+// fused tail: [0] min start, [1] max phase-1 end, [2] max barrier-1 exit,
+// [3] max phase-2 end, [4] max barrier-2 exit, [5] max end, [6] min barrier-1 exit
+__device__ unsigned long long g_tail_ts[4096][7];
 __device__ int g_symv_ts_print = 0;
 #endif
 
@@ -946,59 +949,68 @@ __global__ void combine_kernel(const Dd* slots, int64_t stride, int world, int s
 // Fused CG tail (single GPU, plain iterations): everything between two SYMVs
 // in ONE kernel -- t from the partial slots, alpha, x / r updates, r^T r,
 // beta, s = r + beta s (cg_solver.cpp:258-332) -- instead of finalize +
-// update + direction (three launches, two of them short, latency-bound
-// vector kernels, and a finalize set by the heaviest block row's ~N column
-// partials). Persistent, co-resident grid (cooperative launch), two grid
-// barriers:
-//   phase 1: the finalize's partial sums, balanced: every block row's
-//     entry list (column partials of its tiles, row segments, split-tile
-//     extras; same order as finalize_kernel) is cut into items of at most
-//     TAIL_ITEM entries; one warp per (item, 32 columns), up to 16 loads in
-//     flight; the last warp of a (row, column chunk) -- ticket -- adds the
-//     item sums in item order, stores t and the chunk's s . t partial.
+// update + direction (three launches, two of them short latency-bound vector
+// kernels, and a finalize set by the heaviest block row's ~N column
+// partials). Persistent co-resident grid (cooperative launch), two grid
+// barriers, no other inter-CTA waits:
+//   phase 1: the finalize's partial sums, balanced: block row j's entry list
+//     (column partials of tiles (j..N-1, j), its row segments, split-tile
+//     extras; the finalize's order) is cut into items of at most TAIL_ITEM
+//     entries; one warp per (item, 32 columns) sums its entries (16 loads in
+//     flight) into an item partial, and accumulates s_j . (item partial) --
+//     s . t is linear in the partials, so no combine is needed for alpha.
+//     Per-CTA s . t partial (fixed order over the CTA's warps and units).
 //   barrier; every CTA reduces the s . t partials in one fixed order
-//     (identical alpha everywhere); x += alpha s, r -= alpha t on its slice,
-//     r . r partial per CTA.
+//     (identical alpha everywhere); per element, t = the row's item partials
+//     added in item order; x += alpha s, r -= alpha t; r . r partial per CTA.
 //   barrier; every CTA reduces the r . r partials -> beta; s = r + beta s.
 // CTA 0 keeps the scalar books (scalar_step: alpha / beta, non-finite
-// checks, trace, done). Deterministic: every sum has a fixed order and
-// shape whichever warp or CTA computes it.
+// checks, trace, done). Deterministic: every sum has a fixed order and shape
+// for a given grid (the grid is fixed per device).
 constexpr int TAIL_THREADS = 256;
 constexpr int TAIL_ITEM = 32;   // entries per item
 constexpr int TAIL_BATCH = 16;  // loads in flight per lane
 
 struct TailArgs {
-  const int64_t* row_rseg;
-  const int32_t* row_extra;
-  const int32_t* extra_cta;
   const double* rowpart;
   const double* colmain;
   const double* colextra;
+  const int32_t* extra_cta;
   uint32_t* unit_ctr;
   int64_t N;
-  int b, nch;
-  const int32_t* item_row;   // [nitems]
-  const int32_t* item_e0;    // [nitems]
-  const int32_t* item_e1;    // [nitems]
-  const int32_t* row_item;   // [N + 1]
+  int b, nch, lgb;             // b = 1 << lgb
+  const int4* item;            // [nitems] (row j, e0, e1, first row segment)
+  const int2* item_aux;        // [nitems] (row segments of j, first extra of j)
+  const int32_t* row_item;     // [N + 1]
   int64_t nitems;
-  double* itempart;          // [nitems * b]
-  uint32_t* row_ticket;      // [N * nch], zero between launches
-  double* dotpart;           // [N * nch]
-  double* rrpart;            // [grid]
-  unsigned* bar;             // [2] grid-barrier counters
-  int64_t len;               // N * b
+  double* itempart;            // [nitems * b]
+  double* dotpart;             // [grid]
+  double* rrpart;              // [grid]
+  unsigned* bar;               // [2] grid-barrier counters
+  int64_t len;                 // N * b
   double* x;
   double* r;
   double* s;
-  double* t;
   StepArgs sa;
   const int32_t* done;
   const unsigned char* pf_base;
   const int64_t* pf_slab;
   int64_t pf_slab_lo;
   int pf_units, pf_slabs;
+  unsigned ts_seq;  // launch sequence (HS_SYMV_TIMING builds only)
 };
+
+#ifdef HS_SYMV_TIMING
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TAIL_TS(k, op)                                                        \
+  if (threadIdx.x == 0) atomic##op(&g_tail_ts[ta.ts_seq % 4096u][k], gtime());
+#else
+#define TAIL_TS(k, op)
+#endif
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -1037,10 +1049,12 @@ __device__ Dd dd_reduce_cg(const double* parts, int64_t count, Dd* red) {
 __global__ void __launch_bounds__(TAIL_THREADS, 4) cg_tail_kernel(TailArgs ta) {
   pdl_wait();
   if (ta.done && *ta.done) return;
-  const int lane = threadIdx.x & 31;
+  TAIL_TS(0, Min)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = ta.b, nch = ta.nch;
   const int64_t N = ta.N;
   const double u_old = ta.sa.sc->u;  // CTA 0 replaces it after barrier 2
+  __shared__ double red_w[TAIL_THREADS / 32];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     ta.bar[1] = 0u;      // nobody reaches barrier 2 before CTA 0 arrives at barrier 1
     *ta.unit_ctr = 0u;   // SYMV work-unit counter for the next launch
@@ -1052,64 +1066,57 @@ __global__ void __launch_bounds__(TAIL_THREADS, 4) cg_tail_kernel(TailArgs ta) {
     if (ns > 0)
       bulk_prefetch_l2(ta.pf_base + (g0 - ta.pf_slab_lo) * 32768, (uint32_t)(ns * 32768));
   }
-  // ---- phase 1: t and the s . t partials ----
+  // ---- phase 1: item partials and s . t ----
   const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t units = ta.nitems * nch;
+  double dacc = 0.0;
   for (int64_t u = gwarp; u < units; u += nwarps) {
     const int64_t it = u / nch;
     const int ch = (int)(u - it * nch);
-    const int64_t j = ta.item_row[it];
-    const int64_t e0 = ta.item_e0[it], e1 = ta.item_e1[it];
+    const int4 d = __ldg(ta.item + it);
+    const int64_t j = d.x, e1 = d.z;
     const int c = ch * 32 + lane;
+    const double sj = ta.s[(j << ta.lgb) + c];
     const int64_t nc = N - j;  // column partials of tiles (j .. N-1, j)
-    const int64_t rs0 = ta.row_rseg[j], nrs = ta.row_rseg[j + 1] - rs0;
-    const int x0 = ta.row_extra[j];
     const double* colbase = ta.colmain + c;
     double acc = 0.0;
-    int64_t e = e0;
+    int64_t e = d.y;
     for (; e + TAIL_BATCH <= e1 && e + TAIL_BATCH <= nc; e += TAIL_BATCH) {
       double v[TAIL_BATCH];
 #pragma unroll
-      for (int k = 0; k < TAIL_BATCH; ++k) v[k] = __ldg(colbase + tri(j + e + k, j) * b);
+      for (int k = 0; k < TAIL_BATCH; ++k) v[k] = __ldg(colbase + (tri(j + e + k, j) << ta.lgb));
 #pragma unroll
       for (int k = 0; k < TAIL_BATCH; ++k) acc += v[k];
     }
-    for (; e < e1 && e < nc; ++e) acc += __ldg(colbase + tri(j + e, j) * b);
-    for (; e < e1 && e < nc + nrs; ++e) acc += __ldg(ta.rowpart + (rs0 + e - nc) * b + c);
-    for (; e < e1; ++e)
-      acc += __ldg(ta.colextra + (int64_t)ta.extra_cta[x0 + (e - nc - nrs)] * b + c);
-    const int64_t i0 = ta.row_item[j], m = ta.row_item[j + 1] - i0;
-    bool fin = true;
-    double tv = acc;
-    if (m > 1) {
-      ta.itempart[it * b + c] = acc;
-      __threadfence();
-      __syncwarp();
-      unsigned last = 0;
-      if (lane == 0) last = atomicAdd(&ta.row_ticket[j * nch + ch], 1u) == (unsigned)(m - 1);
-      fin = __shfl_sync(0xffffffffu, last, 0) != 0;
-      if (fin) {
-        __threadfence();
-        tv = 0.0;
-        for (int64_t k = 0; k < m; ++k) tv += __ldcg(ta.itempart + (i0 + k) * b + c);
-        if (lane == 0) ta.row_ticket[j * nch + ch] = 0u;
-      }
+    for (; e < e1 && e < nc; ++e) acc += __ldg(colbase + (tri(j + e, j) << ta.lgb));
+    if (e < e1) {  // row segments, then split-tile extras
+      const int2 a = __ldg(ta.item_aux + it);
+      for (; e < e1 && e < nc + a.x; ++e) acc += __ldg(ta.rowpart + ((d.w + e - nc) << ta.lgb) + c);
+      for (; e < e1; ++e)
+        acc += __ldg(ta.colextra + ((int64_t)ta.extra_cta[a.y + (e - nc - a.x)] << ta.lgb) + c);
     }
-    if (fin) {
-      const int64_t o = j * b + c;
-      ta.t[o] = tv;
-      double d = ta.s[o] * tv;
-      for (int off = 16; off >= 1; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
-      if (lane == 0) ta.dotpart[j * nch + ch] = d;
-    }
+    ta.itempart[(it << ta.lgb) + c] = acc;
+    dacc = fma(sj, acc, dacc);
   }
+  for (int off = 16; off >= 1; off >>= 1) dacc += __shfl_xor_sync(0xffffffffu, dacc, off);
+  if (lane == 0) red_w[warp] = dacc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < TAIL_THREADS / 32; ++w) t += red_w[w];
+    ta.dotpart[blockIdx.x] = t;
+  }
+  TAIL_TS(1, Max)
   tail_grid_barrier(&ta.bar[0]);
+  TAIL_TS(2, Max)
+  TAIL_TS(6, Min)
   pdl_trigger();  // every tail CTA is resident: the next SYMV may launch
-  // ---- phase 2: alpha; x, r; r . r ----
+  // ---- phase 2: alpha; t; x, r; r . r ----
   __shared__ Dd red[TAIL_THREADS];
   __shared__ double red_d[32];
-  const double st = dd_value(dd_reduce_cg(ta.dotpart, N * nch, red));
+  const double st = dd_value(dd_reduce_cg(ta.dotpart, gridDim.x, red));
   const double alpha = u_old / st;
   if (blockIdx.x == 0 && threadIdx.x == 0) scalar_step(STEP_ALPHA, st, ta.sa);
   if (!isfinite(alpha)) {
@@ -1119,14 +1126,21 @@ __global__ void __launch_bounds__(TAIL_THREADS, 4) cg_tail_kernel(TailArgs ta) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   double part = 0.0;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ta.len; k += stride) {
+    const int64_t j = k >> ta.lgb;
+    const int c = (int)(k & (b - 1));
+    const int i0 = __ldg(ta.row_item + j), m = __ldg(ta.row_item + j + 1) - i0;
+    double t = 0.0;
+    for (int q = 0; q < m; ++q) t += __ldcg(ta.itempart + ((int64_t)(i0 + q) << ta.lgb) + c);
     ta.x[k] = fma(alpha, ta.s[k], ta.x[k]);
-    const double rr = fma(-alpha, __ldcg(ta.t + k), ta.r[k]);
+    const double rr = fma(-alpha, t, ta.r[k]);
     ta.r[k] = rr;
     part = fma(rr, rr, part);
   }
   const double pc = block_sum(part, red_d);
   if (threadIdx.x == 0) ta.rrpart[blockIdx.x] = pc;
+  TAIL_TS(3, Max)
   tail_grid_barrier(&ta.bar[1]);
+  TAIL_TS(4, Max)
   // ---- phase 3: beta; s = r + beta s ----
   const double un = dd_value(dd_reduce_cg(ta.rrpart, gridDim.x, red));
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1137,6 +1151,8 @@ __global__ void __launch_bounds__(TAIL_THREADS, 4) cg_tail_kernel(TailArgs ta) {
   const double beta = un / u_old;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ta.len; k += stride)
     ta.s[k] = fma(beta, ta.s[k], ta.r[k]);
+  __syncthreads();
+  TAIL_TS(5, Max)
 }
 
 // ---------------------------------------------------------------------------
@@ -1147,9 +1163,9 @@ void free_plan(SymvPlan* p) {
   for (void* q : {(void*)p->cta_slab, (void*)p->cta_rseg, (void*)p->row_rseg,
                   (void*)p->row_extra, (void*)p->extra_cta, (void*)p->unit_ctr,
                   (void*)p->rowpart, (void*)p->colmain, (void*)p->colextra,
-                  (void*)p->item_row, (void*)p->item_e0, (void*)p->item_e1,
-                  (void*)p->row_item, (void*)p->itempart, (void*)p->row_ticket,
-                  (void*)p->tail_dot, (void*)p->tail_rr, (void*)p->tail_bar})
+                  (void*)p->item, (void*)p->item_aux, (void*)p->row_item,
+                  (void*)p->itempart, (void*)p->tail_dot, (void*)p->tail_rr,
+                  (void*)p->tail_bar})
     cudaFree(q);
   delete p;
 }
@@ -1177,29 +1193,29 @@ static void build_tail_plan(hs_matrix* m, SymvPlan* p, const std::vector<int64_t
   int per_sm = 0;
   HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_tail_kernel, TAIL_THREADS, 0));
   if (per_sm < 1) return;
-  std::vector<int32_t> item_row, item_e0, item_e1, row_item(N + 1, 0);
+  std::vector<int4> item;
+  std::vector<int2> aux;
+  std::vector<int32_t> row_item(N + 1, 0);
   for (int64_t j = 0; j < N; ++j) {
-    const int64_t E = (N - j) + (row_rseg[j + 1] - row_rseg[j]) + (row_extra[j + 1] - row_extra[j]);
+    const int64_t nrs = row_rseg[j + 1] - row_rseg[j];
+    const int64_t E = (N - j) + nrs + (row_extra[j + 1] - row_extra[j]);
     const int64_t mj = std::max<int64_t>(1, (E + TAIL_ITEM - 1) / TAIL_ITEM);
-    row_item[j] = (int32_t)item_row.size();
+    row_item[j] = (int32_t)item.size();
     for (int64_t k = 0; k < mj; ++k) {
-      item_row.push_back((int32_t)j);
-      item_e0.push_back((int32_t)(E * k / mj));
-      item_e1.push_back((int32_t)(E * (k + 1) / mj));
+      item.push_back(make_int4((int)j, (int)(E * k / mj), (int)(E * (k + 1) / mj),
+                               (int)row_rseg[j]));
+      aux.push_back(make_int2((int)nrs, (int)row_extra[j]));
     }
   }
-  row_item[N] = (int32_t)item_row.size();
-  p->nitems = (int64_t)item_row.size();
+  row_item[N] = (int32_t)item.size();
+  p->nitems = (int64_t)item.size();
   p->tail_grid = std::min(per_sm, 4) * std::max(1, m->ctx->num_sms);
-  const int64_t nch = b / 32;
-  upload_vec(&p->item_row, item_row);
-  upload_vec(&p->item_e0, item_e0);
-  upload_vec(&p->item_e1, item_e1);
+  upload_vec(&p->item, item);
+  upload_vec(&p->item_aux, aux);
   upload_vec(&p->row_item, row_item);
-  upload_vec(&p->row_ticket, std::vector<uint32_t>((size_t)(N * nch), 0u));
   upload_vec(&p->tail_bar, std::vector<unsigned>(2, 0u));
   HS_CUDA(cudaMalloc(&p->itempart, (size_t)p->nitems * b * sizeof(double)));
-  HS_CUDA(cudaMalloc(&p->tail_dot, (size_t)(N * nch) * sizeof(double)));
+  HS_CUDA(cudaMalloc(&p->tail_dot, (size_t)p->tail_grid * sizeof(double)));
   HS_CUDA(cudaMalloc(&p->tail_rr, (size_t)p->tail_grid * sizeof(double)));
 }
 
@@ -1414,26 +1430,24 @@ static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
 // grid barriers need every CTA resident), programmatic serialization when
 // the driver accepts both attributes together.
 static void launch_tail(hs_ctx* c, const hs_matrix* m, double* x, double* r, double* s,
-                        double* t, const StepArgs& sa, const int32_t* done) {
+                        const StepArgs& sa, const int32_t* done) {
   SymvPlan* p = m->plan;
   TailArgs ta{};
-  ta.row_rseg = p->row_rseg;
-  ta.row_extra = p->row_extra;
-  ta.extra_cta = p->extra_cta;
   ta.rowpart = p->rowpart;
   ta.colmain = p->colmain;
   ta.colextra = p->colextra;
+  ta.extra_cta = p->extra_cta;
   ta.unit_ctr = p->unit_ctr;
   ta.N = (int64_t)m->N;
   ta.b = (int)m->b;
   ta.nch = (int)(m->b / 32);
-  ta.item_row = p->item_row;
-  ta.item_e0 = p->item_e0;
-  ta.item_e1 = p->item_e1;
+  ta.lgb = 0;
+  while ((1 << ta.lgb) < ta.b) ++ta.lgb;
+  ta.item = p->item;
+  ta.item_aux = p->item_aux;
   ta.row_item = p->row_item;
   ta.nitems = p->nitems;
   ta.itempart = p->itempart;
-  ta.row_ticket = p->row_ticket;
   ta.dotpart = p->tail_dot;
   ta.rrpart = p->tail_rr;
   ta.bar = p->tail_bar;
@@ -1441,9 +1455,12 @@ static void launch_tail(hs_ctx* c, const hs_matrix* m, double* x, double* r, dou
   ta.x = x;
   ta.r = r;
   ta.s = s;
-  ta.t = t;
   ta.sa = sa;
   ta.done = done;
+#ifdef HS_SYMV_TIMING
+  static unsigned tseq = 0;
+  ta.ts_seq = tseq++;
+#endif
   static const int pf = [] {
     const char* e = getenv("HS_SYMV_PF_SLABS");
     return e ? atoi(e) : 8;
@@ -1696,7 +1713,7 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
       // lines 4-11 in two launches: the SYMV, then the fused tail (t,
       // alpha, x, r, r^T r, beta, s)
       symv_to(c, m, B.s_full, B.t, false, nullptr, done, nullptr, false);
-      launch_tail(c, m, x_loc, B.r, s_loc, B.t, sa, done);
+      launch_tail(c, m, x_loc, B.r, s_loc, sa, done);
       goto poll;
     }
     // lines 4-5: t = A s, alpha = u / s^T t (the dot fused into the finalize)
@@ -2055,6 +2072,16 @@ extern "C" int hs_debug_fin_ts(unsigned long long* out, int count, int reset) {
     return (int)cudaMemcpyToSymbol(hs::g_fin_ts, init, sizeof(init));
   }
   return (int)cudaMemcpyFromSymbol(out, hs::g_fin_ts, (size_t)count * 5 * sizeof(unsigned long long));
+}
+
+extern "C" int hs_debug_tail_ts(unsigned long long* out, int count, int reset) {
+  if (reset) {
+    static unsigned long long init[4096][7];
+    for (int k = 0; k < 4096; ++k)
+      for (int i = 0; i < 7; ++i) init[k][i] = (i == 0 || i == 6) ? ~0ull : 0ull;
+    return (int)cudaMemcpyToSymbol(hs::g_tail_ts, init, sizeof(init));
+  }
+  return (int)cudaMemcpyFromSymbol(out, hs::g_tail_ts, (size_t)count * 7 * sizeof(unsigned long long));
 }
 
 extern "C" int hs_debug_symv_ts(unsigned long long* out, int count, int reset, int print) {

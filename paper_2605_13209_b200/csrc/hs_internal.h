@@ -53,13 +53,11 @@ struct SymvPlan {
   // the per-row partial lists, their sums, tickets, dot / norm partials
   int64_t nitems = 0;
   int tail_grid = 0;             // co-resident CTAs (0: tail kernel unused)
-  int32_t* item_row = nullptr;   // [nitems]
-  int32_t* item_e0 = nullptr;
-  int32_t* item_e1 = nullptr;
+  int4* item = nullptr;          // [nitems] (row, e0, e1, first row segment)
+  int2* item_aux = nullptr;      // [nitems] (row segments, first extra)
   int32_t* row_item = nullptr;   // [N + 1]
   double* itempart = nullptr;    // [nitems * b]
-  uint32_t* row_ticket = nullptr;  // [N * b / 32]
-  double* tail_dot = nullptr;    // [N * b / 32]
+  double* tail_dot = nullptr;    // [tail_grid]
   double* tail_rr = nullptr;     // [tail_grid]
   unsigned* tail_bar = nullptr;  // [2]
 };

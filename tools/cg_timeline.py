@@ -26,6 +26,7 @@ mode = sys.argv[5] if len(sys.argv) > 5 else ""
 dbg = C.CDLL(LIB)
 dbg.hs_debug_symv_ts.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
 dbg.hs_debug_fin_ts.argtypes = [C.c_void_p, C.c_int, C.c_int]
+dbg.hs_debug_tail_ts.argtypes = [C.c_void_p, C.c_int, C.c_int]
 rt = (hs.Runtime(device=0, stream=torch.cuda.current_stream().cuda_stream)
       if "torchstream" in mode else hs.Runtime())
 m = hs.generate_spd_device(rt, n, b, seed=42)
@@ -48,6 +49,7 @@ torch.cuda.synchronize()
 for rep in range(reps):
     dbg.hs_debug_symv_ts(None, 0, 1, 0)
     dbg.hs_debug_fin_ts(None, 0, 1)
+    dbg.hs_debug_tail_ts(None, 0, 1)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -84,6 +86,23 @@ for rep in range(reps):
         print("   gap breakdown us (median): SYMV end->finalize start %.1f, sums %.1f, "
               "dot epilogue %.1f, finalize end->next SYMV %.1f; CTA start spread %.1f, "
               "longest CTA sums %.1f" % tuple(med))
+    tb = (C.c_ulonglong * (7 * 4096))()
+    dbg.hs_debug_tail_ts(tb, 4096, 0)
+    tail = sorted(tuple(tb[7 * k + i] for i in range(7)) for k in range(4096)
+                  if tb[7 * k + 5] != 0)
+    tr = []
+    for k in range(len(ts) - 1):
+        s_end, nxt = ts[k][1], ts[k + 1][0]
+        f = [x for x in tail if s_end <= x[0] < nxt]
+        if f:
+            t0, t1, t2, t3, t4, t5, t6 = f[0]
+            tr.append(((t0 - s_end) / 1e3, (t1 - t0) / 1e3, (t2 - t1) / 1e3, (t6 - t1) / 1e3,
+                       (t3 - t2) / 1e3, (t4 - t3) / 1e3, (t5 - t4) / 1e3, (nxt - t5) / 1e3))
+    if tr:
+        med = [sorted(x[i] for x in tr)[len(tr) // 2] for i in range(8)]
+        print("   fused tail us (median): SYMV end->tail start %.1f, phase 1 %.1f, "
+              "barrier 1 (last arrival->last exit %.1f, ->first exit %.1f), phase 2 %.1f, "
+              "barrier 2 %.1f, phase 3 %.1f, tail end->next SYMV %.1f" % tuple(med))
     big = [(k, round(g, 1)) for k, g in enumerate(gaps) if g > 200]
     if big:
         print("   gaps > 200 us (launch index, us):", big[:20])
