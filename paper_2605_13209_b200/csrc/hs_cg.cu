@@ -89,6 +89,10 @@ __device__ unsigned long long g_fin_ts[4096][5];  // + [3] max start, [4] max su
 // fused tail: [0] min start, [1] max phase-1 end, [2] max barrier-1 exit,
 // [3] max phase-2 end, [4] max barrier-2 exit, [5] max end, [6] min barrier-1 exit
 __device__ unsigned long long g_tail_ts[4096][7];
+// per-CTA stamps of one tail launch (seq == g_tail_cta_seq): start, phase-1
+// end, barrier-1 exit, phase-2 end, end
+__device__ unsigned long long g_tail_cta[1024][5];
+__device__ unsigned g_tail_cta_seq = 100;
 __device__ int g_symv_ts_print = 0;
 #endif
 
@@ -1008,8 +1012,12 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 #define TAIL_TS(k, op)                                                        \
   if (threadIdx.x == 0) atomic##op(&g_tail_ts[ta.ts_seq % 4096u][k], gtime());
+#define TAIL_CTA(k)                                                           \
+  if (threadIdx.x == 0 && ta.ts_seq == g_tail_cta_seq && blockIdx.x < 1024)    \
+    g_tail_cta[blockIdx.x][k] = gtime();
 #else
 #define TAIL_TS(k, op)
+#define TAIL_CTA(k)
 #endif
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
@@ -1050,6 +1058,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 4) cg_tail_kernel(TailArgs ta) {
   pdl_wait();
   if (ta.done && *ta.done) return;
   TAIL_TS(0, Min)
+  TAIL_CTA(0)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = ta.b, nch = ta.nch;
   const int64_t N = ta.N;
@@ -1058,13 +1067,6 @@ __global__ void __launch_bounds__(TAIL_THREADS, 4) cg_tail_kernel(TailArgs ta) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     ta.bar[1] = 0u;      // nobody reaches barrier 2 before CTA 0 arrives at barrier 1
     *ta.unit_ctr = 0u;   // SYMV work-unit counter for the next launch
-  }
-  if ((int)blockIdx.x < ta.pf_units && threadIdx.x == 0 && ta.pf_slabs > 0) {
-    // L2 prefetch of the next SYMV's first slabs (as finalize_kernel)
-    const int64_t g0 = ta.pf_slab[blockIdx.x], g1 = ta.pf_slab[blockIdx.x + 1];
-    const int64_t ns = g1 - g0 < ta.pf_slabs ? g1 - g0 : ta.pf_slabs;
-    if (ns > 0)
-      bulk_prefetch_l2(ta.pf_base + (g0 - ta.pf_slab_lo) * 32768, (uint32_t)(ns * 32768));
   }
   // ---- phase 1: item partials and s . t ----
   const int64_t gwarp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -1082,14 +1084,21 @@ __global__ void __launch_bounds__(TAIL_THREADS, 4) cg_tail_kernel(TailArgs ta) {
     const double* colbase = ta.colmain + c;
     double acc = 0.0;
     int64_t e = d.y;
-    for (; e + TAIL_BATCH <= e1 && e + TAIL_BATCH <= nc; e += TAIL_BATCH) {
-      double v[TAIL_BATCH];
+    // column partials in predicated batches: every load of a batch is in
+    // flight at once (a scalar remainder loop is one L2 round trip per
+    // entry); the absent entries add exact zeros
+    const int64_t ce = e1 < nc ? e1 : nc;
+    if (e < ce) {
+      for (; e < ce; e += TAIL_BATCH) {
+        double v[TAIL_BATCH];
 #pragma unroll
-      for (int k = 0; k < TAIL_BATCH; ++k) v[k] = __ldg(colbase + (tri(j + e + k, j) << ta.lgb));
+        for (int k = 0; k < TAIL_BATCH; ++k)
+          v[k] = e + k < ce ? __ldg(colbase + (tri(j + e + k, j) << ta.lgb)) : 0.0;
 #pragma unroll
-      for (int k = 0; k < TAIL_BATCH; ++k) acc += v[k];
+        for (int k = 0; k < TAIL_BATCH; ++k) acc += v[k];
+      }
+      e = ce;
     }
-    for (; e < e1 && e < nc; ++e) acc += __ldg(colbase + (tri(j + e, j) << ta.lgb));
     if (e < e1) {  // row segments, then split-tile extras
       const int2 a = __ldg(ta.item_aux + it);
       for (; e < e1 && e < nc + a.x; ++e) acc += __ldg(ta.rowpart + ((d.w + e - nc) << ta.lgb) + c);
@@ -1109,10 +1118,20 @@ __global__ void __launch_bounds__(TAIL_THREADS, 4) cg_tail_kernel(TailArgs ta) {
     ta.dotpart[blockIdx.x] = t;
   }
   TAIL_TS(1, Max)
+  TAIL_CTA(1)
   tail_grid_barrier(&ta.bar[0]);
   TAIL_TS(2, Max)
+  TAIL_CTA(2)
   TAIL_TS(6, Min)
   pdl_trigger();  // every tail CTA is resident: the next SYMV may launch
+  if ((int)blockIdx.x < ta.pf_units && threadIdx.x == 0 && ta.pf_slabs > 0) {
+    // L2 prefetch of the next SYMV's first slabs (as finalize_kernel), after
+    // phase 1 so the fills do not compete with the partial-slot reads
+    const int64_t g0 = ta.pf_slab[blockIdx.x], g1 = ta.pf_slab[blockIdx.x + 1];
+    const int64_t ns = g1 - g0 < ta.pf_slabs ? g1 - g0 : ta.pf_slabs;
+    if (ns > 0)
+      bulk_prefetch_l2(ta.pf_base + (g0 - ta.pf_slab_lo) * 32768, (uint32_t)(ns * 32768));
+  }
   // ---- phase 2: alpha; t; x, r; r . r ----
   __shared__ Dd red[TAIL_THREADS];
   __shared__ double red_d[32];
@@ -1130,7 +1149,14 @@ __global__ void __launch_bounds__(TAIL_THREADS, 4) cg_tail_kernel(TailArgs ta) {
     const int c = (int)(k & (b - 1));
     const int i0 = __ldg(ta.row_item + j), m = __ldg(ta.row_item + j + 1) - i0;
     double t = 0.0;
-    for (int q = 0; q < m; ++q) t += __ldcg(ta.itempart + ((int64_t)(i0 + q) << ta.lgb) + c);
+    for (int q0 = 0; q0 < m; q0 += 8) {  // predicated batches, as in phase 1
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        v[q] = q0 + q < m ? __ldcg(ta.itempart + ((int64_t)(i0 + q0 + q) << ta.lgb) + c) : 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) t += v[q];
+    }
     ta.x[k] = fma(alpha, ta.s[k], ta.x[k]);
     const double rr = fma(-alpha, t, ta.r[k]);
     ta.r[k] = rr;
@@ -1139,6 +1165,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 4) cg_tail_kernel(TailArgs ta) {
   const double pc = block_sum(part, red_d);
   if (threadIdx.x == 0) ta.rrpart[blockIdx.x] = pc;
   TAIL_TS(3, Max)
+  TAIL_CTA(3)
   tail_grid_barrier(&ta.bar[1]);
   TAIL_TS(4, Max)
   // ---- phase 3: beta; s = r + beta s ----
@@ -1153,6 +1180,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 4) cg_tail_kernel(TailArgs ta) {
     ta.s[k] = fma(beta, ta.s[k], ta.r[k]);
   __syncthreads();
   TAIL_TS(5, Max)
+  TAIL_CTA(4)
 }
 
 // ---------------------------------------------------------------------------
@@ -1184,11 +1212,14 @@ static void upload_vec(T** dst, const std::vector<T>& v) {
 // at most TAIL_ITEM entries; the grid is what fits co-resident.
 static void build_tail_plan(hs_matrix* m, SymvPlan* p, const std::vector<int64_t>& row_rseg,
                             const std::vector<int32_t>& row_extra) {
-  static const bool off = [] {
+  // opt-in (HS_CG_TAIL=1): measured no faster than finalize + two vector
+  // kernels on B200 -- its phase 1 re-reads the same 34 MB of
+  // partial slots and the per-CTA round trips, not launches, set the time
+  static const bool on = [] {
     const char* e = getenv("HS_CG_TAIL");
-    return e && atoi(e) == 0;
+    return e && atoi(e) == 1;
   }();
-  if (off) return;
+  if (!on) return;
   const int64_t N = (int64_t)m->N, b = (int64_t)m->b;
   int per_sm = 0;
   HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_tail_kernel, TAIL_THREADS, 0));
@@ -2082,6 +2113,10 @@ extern "C" int hs_debug_tail_ts(unsigned long long* out, int count, int reset) {
     return (int)cudaMemcpyToSymbol(hs::g_tail_ts, init, sizeof(init));
   }
   return (int)cudaMemcpyFromSymbol(out, hs::g_tail_ts, (size_t)count * 7 * sizeof(unsigned long long));
+}
+
+extern "C" int hs_debug_tail_cta(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, hs::g_tail_cta, sizeof(hs::g_tail_cta));
 }
 
 extern "C" int hs_debug_symv_ts(unsigned long long* out, int count, int reset, int print) {

@@ -27,6 +27,7 @@ dbg = C.CDLL(LIB)
 dbg.hs_debug_symv_ts.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
 dbg.hs_debug_fin_ts.argtypes = [C.c_void_p, C.c_int, C.c_int]
 dbg.hs_debug_tail_ts.argtypes = [C.c_void_p, C.c_int, C.c_int]
+dbg.hs_debug_tail_cta.argtypes = [C.c_void_p]
 rt = (hs.Runtime(device=0, stream=torch.cuda.current_stream().cuda_stream)
       if "torchstream" in mode else hs.Runtime())
 m = hs.generate_spd_device(rt, n, b, seed=42)
@@ -103,6 +104,20 @@ for rep in range(reps):
         print("   fused tail us (median): SYMV end->tail start %.1f, phase 1 %.1f, "
               "barrier 1 (last arrival->last exit %.1f, ->first exit %.1f), phase 2 %.1f, "
               "barrier 2 %.1f, phase 3 %.1f, tail end->next SYMV %.1f" % tuple(med))
+    if tr and rep == 0:
+        cb = (C.c_ulonglong * (5 * 1024))()
+        dbg.hs_debug_tail_cta(cb)
+        rows = [[cb[5 * k + i] for i in range(5)] for k in range(1024) if cb[5 * k + 4]]
+        if rows:
+            t0 = min(r[0] for r in rows)
+            def q(v):
+                v = sorted(v)
+                return "min %.1f med %.1f p90 %.1f max %.1f" % (v[0], v[len(v) // 2],
+                                                               v[9 * len(v) // 10], v[-1])
+            print("   per-CTA (us) start offset:", q([(r[0] - t0) / 1e3 for r in rows]))
+            print("   per-CTA phase 1 (own start->own end):", q([(r[1] - r[0]) / 1e3 for r in rows]))
+            print("   per-CTA phase 1 end offset:", q([(r[1] - t0) / 1e3 for r in rows]))
+            print("   per-CTA phase 2:", q([(r[3] - r[2]) / 1e3 for r in rows]))
     big = [(k, round(g, 1)) for k, g in enumerate(gaps) if g > 200]
     if big:
         print("   gaps > 200 us (launch index, us):", big[:20])
