@@ -64,6 +64,12 @@ const char* hs_error_kind_name(hs_status s); /* transfer_ledger.cpp:28-42 */
 
 /* ---- context (replaces hsolve::Runtime, executor.hpp:128-221) ---------- */
 hs_status hs_device_count(int* count); /* visible CUDA devices */
+/* Device buffers on the context's GPU for FFI callers without a CUDA
+ * runtime of their own; hs_memcpy copies any direction (unified addressing)
+ * and returns when the copy is done. */
+hs_status hs_device_alloc(hs_ctx* ctx, size_t bytes, void** out);
+void hs_device_free(hs_ctx* ctx, void* p);
+hs_status hs_memcpy(hs_ctx* ctx, void* dst, const void* src, size_t bytes);
 /* stream: a cudaStream_t to order work on (NULL = the library creates one). */
 hs_status hs_ctx_create(int device, void* stream, hs_ctx** out);
 /* Multi-GPU: one process per GPU; nccl_id = 128 bytes from
@@ -293,6 +299,34 @@ hs_status hs_potf_tiles(hs_ctx* ctx, double* d_tiles, size_t b, size_t count,
 hs_status hs_gemm_update_tiles(hs_ctx* ctx, double* d_c, const double* d_p,
                                const double* d_q, size_t b, size_t count,
                                int lower_only);
+
+/* Kernel-level drop-ins of hsolve::kernels (block_kernels.hpp:16-74), one
+ * output element per sequential chain in the reference's order with
+ * separately rounded multiply and add (bitwise the reference's results):
+ * X_t L_t^T = B_t in place for `count` tiles (trsm_block; singular_block
+ * with the first zero / NaN diagonal index as payload b). */
+hs_status hs_trsm_tiles(hs_ctx* ctx, double* d_x, const double* d_l, size_t b,
+                        size_t count);
+/* op 0: potf_block in place (b <= 1024; not_spd payload (-1, pivot) and
+ * *bad_pivot); 1: C -= P Q^T (gemm_update); 2: lower(C) -= lower(P P^T)
+ * (syrk_update, d_q = d_p). */
+hs_status hs_block_exact(hs_ctx* ctx, int op, double* d_c, const double* d_p,
+                         const double* d_q, size_t b, int64_t* bad_pivot);
+/* y rows of block rows [lo, hi) = (A x) rows, symv_row's order
+ * (block_kernels.cpp:59-95) on the packed matrix d_a (N(N+1)/2 b^2). */
+hs_status hs_symv_exact(hs_ctx* ctx, const double* d_a, const double* d_x, double* d_y,
+                        size_t n, size_t b, size_t lo, size_t hi);
+/* op 0: y -= M x (gemv_sub); 1: y -= M^T x (gemv_transpose_sub);
+ * 2: L y = y in place (lower_solve); 3: L^T y = y (lower_transpose_solve;
+ * singular_block at the first bad row in the solve order) */
+hs_status hs_block_vec_op(hs_ctx* ctx, int op, const double* d_m, const double* d_x,
+                          double* d_y, size_t b);
+/* Block rows [lo, hi) of padded vectors (N*b doubles): op 0: out[i] =
+ * row_dot(u, v, i) (one double per row, at index i); 1: out += alpha u
+ * (axpy_range); 2: out = u + alpha out (xpay_range); 3: out = u - v
+ * (sub_range). */
+hs_status hs_range_op(hs_ctx* ctx, int op, double* d_out, const double* d_u,
+                      const double* d_v, double alpha, size_t lo, size_t hi, size_t b);
 
 /* C_t -= P_t Q_t^T (t < count) on the INT8 tensor cores with FP64-accurate
  * Ozaki slicing (`slices` int8 slices per operand, 1..8; 8 gives FP64-level

@@ -32,7 +32,8 @@ EXPORTED = [
     "hs_ctx_create", "hs_nccl_unique_id", "hs_ctx_create_nccl", "hs_ctx_destroy", "hs_ctx_trim",
     "hs_ctx_create_custom_comm",
     "hs_ctx_rank", "hs_ctx_world", "hs_ctx_stream", "hs_ctx_kernel_launches",
-    "hs_ctx_set_cholesky_gemm", "hs_device_count",
+    "hs_ctx_set_cholesky_gemm", "hs_device_count", "hs_device_alloc", "hs_device_free",
+    "hs_memcpy",
     "hs_group_create", "hs_group_destroy", "hs_group_world", "hs_group_transport",
     "hs_group_ctx", "hs_group_set_row_fraction", "hs_group_set_cholesky_gemm", "hs_group_run",
     "hs_group_solve_cg_host", "hs_group_factorize_host", "hs_group_solve_spd_host",
@@ -46,6 +47,7 @@ EXPORTED = [
     "hs_potrf", "hs_trsv_lower", "hs_trsv_upper", "hs_solve_spd",
     "hs_factorize_host", "hs_solve_spd_host", "hs_forward_substitute_host",
     "hs_back_substitute_host", "hs_potf_tiles", "hs_gemm_update_tiles", "hs_oz_gemm_tiles",
+    "hs_trsm_tiles", "hs_block_vec_op", "hs_range_op", "hs_block_exact", "hs_symv_exact",
     "hs_oz_set_profile",
     "hs_prof_enable", "hs_prof_symv", "hs_prof_reset", "hs_probe_hbm_read",
     "hs_ctx_ledger_size", "hs_ctx_ledger_read", "hs_ctx_ledger_clear",
@@ -118,6 +120,9 @@ def lib():
                                                 C.POINTER(CommOps), pp]),
         "hs_ctx_destroy": (None, [vp]),
         "hs_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+        "hs_device_alloc": (C.c_int, [vp, sz, pp]),
+        "hs_device_free": (None, [vp, vp]),
+        "hs_memcpy": (C.c_int, [vp, vp, vp, sz]),
         "hs_group_create": (C.c_int, [C.c_int, vp, C.c_int, pp]),
         "hs_group_destroy": (None, [vp]),
         "hs_group_world": (C.c_int, [vp]),
@@ -173,6 +178,11 @@ def lib():
         "hs_gemm_update_tiles": (C.c_int, [vp, dp, dp, dp, sz, sz, C.c_int]),
         "hs_oz_gemm_tiles": (C.c_int, [vp, dp, dp, dp, sz, sz, C.c_int, C.c_int]),
         "hs_oz_set_profile": (None, [vp]),
+        "hs_trsm_tiles": (C.c_int, [vp, dp, dp, sz, sz]),
+        "hs_block_exact": (C.c_int, [vp, C.c_int, dp, dp, dp, sz, C.POINTER(i64)]),
+        "hs_symv_exact": (C.c_int, [vp, dp, dp, dp, sz, sz, sz, sz]),
+        "hs_block_vec_op": (C.c_int, [vp, C.c_int, dp, dp, dp, sz]),
+        "hs_range_op": (C.c_int, [vp, C.c_int, dp, dp, dp, C.c_double, sz, sz, sz]),
         "hs_prof_enable": (None, [vp, C.c_int]),
         "hs_prof_symv": (None, [vp, C.POINTER(u64), C.POINTER(C.c_double)]),
         "hs_prof_reset": (None, [vp]),

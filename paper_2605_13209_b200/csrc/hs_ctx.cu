@@ -597,6 +597,31 @@ static void ctx_common_init(hs_ctx* c, int device, void* stream) {
   HS_CUDA(cudaMallocHost(&c->h_pinned, std::max(64 * sizeof(double), 2 * sizeof(CgScalars))));
 }
 
+hs_status hs_device_alloc(hs_ctx* c, size_t bytes, void** out) {
+  HS_API_BEGIN
+  HS_REQUIRE(c && out, HS_ERR_CONFIG, "null pointer");
+  HS_CUDA(cudaSetDevice(c->device));
+  *out = nullptr;
+  if (bytes) HS_CUDA(cudaMalloc(out, bytes));
+  HS_API_END
+}
+
+void hs_device_free(hs_ctx* c, void* p) {
+  if (!c || !p) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  cudaFree(p);
+}
+
+hs_status hs_memcpy(hs_ctx* c, void* dst, const void* src, size_t bytes) {
+  HS_API_BEGIN
+  HS_REQUIRE(c && (bytes == 0 || (dst && src)), HS_ERR_CONFIG, "null pointer");
+  HS_CUDA(cudaSetDevice(c->device));
+  if (bytes) HS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream));
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  HS_API_END
+}
+
 hs_status hs_device_count(int* count) {
   HS_API_BEGIN
   HS_REQUIRE(count, HS_ERR_CONFIG, "null pointer");

@@ -41,13 +41,9 @@ void check(hs_status s) {
 
 }  // namespace detail
 
-namespace {
-
-using detail::check;
-
 // Context for the reference entry points that take no Runtime
-// (forward_substitute / back_substitute, generate_spd).
-hs_ctx* default_ctx() {
+// (forward_substitute / back_substitute, generate_spd, hsolve::kernels).
+hs_ctx* detail::default_ctx() {
   static std::once_flag once;
   static hs_ctx* ctx = nullptr;
   static hs_status st = HS_OK;
@@ -55,6 +51,11 @@ hs_ctx* default_ctx() {
   check(st);
   return ctx;
 }
+
+namespace {
+
+using detail::check;
+using detail::default_ctx;
 
 // The plan a factorization reports: the GPU paths never run the reference's
 // moving-border CPU/GPU split (one GPU, or a static 2D block-cyclic grid),

@@ -69,3 +69,30 @@ def test_cpp_multigpu_runtime(tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     print(out.stdout)
     assert out.returncode == 0 and "ALL PASSED" in out.stdout, out.stdout + out.stderr
+
+
+def _build_named(tmp_path, name):
+    exe = str(tmp_path / name)
+    subprocess.run(["g++", "-std=c++20", "-O1", "-ffp-contract=off", "-I",
+                    os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", name + ".cpp"), "-o", exe,
+                    "-L", PKG, "-lhsolve_b200", "-lhsolve_cuda", f"-Wl,-rpath,{PKG}"],
+                   check=True)
+    return exe
+
+
+def test_cpp_block_kernels_api_compiles(tmp_path):
+    """block_kernels.hpp / dd.hpp drop-in headers compile against the shim."""
+    if not os.path.exists(os.path.join(PKG, "libhsolve_b200.so")):
+        pytest.skip("shim not built")
+    assert os.path.exists(_build_named(tmp_path, "test_block_kernels_api"))
+
+
+@pytest.mark.gpu
+def test_cpp_block_kernels_api(tmp_path):
+    """hsolve::kernels on the GPU: the reference's closed forms and bitwise
+    agreement with its loops (test_block_kernels.cpp)."""
+    out = subprocess.run([_build_named(tmp_path, "test_block_kernels_api")], capture_output=True,
+                         text=True, timeout=600)
+    print(out.stdout)
+    assert out.returncode == 0 and "ALL PASSED" in out.stdout, out.stdout + out.stderr

@@ -625,3 +625,37 @@ def test_substitutions_wide_steps(rt, n, b):
     x_ref = solve_triangular(dense.T, y_ref, lower=False)
     assert np.linalg.norm(y.logical() - y_ref) <= 1e-12 * np.linalg.norm(y_ref)
     assert np.linalg.norm(x.logical() - x_ref) <= 1e-12 * np.linalg.norm(x_ref)
+
+
+def test_cg_fused_tail_opt_in_matches_oracle():
+    """HS_CG_TAIL=1 (fused single-launch CG tail, opt-in): same oracle bounds
+    as the default path, in a subprocess (the switch is read once)."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, ".")
+import paper_2605_13209_b200 as hs
+from oracle import Oracle
+o = Oracle()
+rt = hs.Runtime()
+for n, b in [(1024, 128), (3000, 64), (2048, 512), (4096, 256)]:
+    a = o.generate_spd(n, b, seed=11); rhs = o.generate_rhs(n, b, seed=11)
+    ref = o.solve_cg(n, b, a, rhs, eps=1e-6)
+    r = hs.solve_cg(hs.BlockedSPDMatrix(n, b, a), hs.BlockVector(n, b, rhs),
+                    hs.SolverConfig(block_size=b, eps=1e-6, record_trace=True), rt)
+    st = r.stats
+    assert st.converged and abs(st.iterations - ref["iterations"]) <= max(2, 0.2 * ref["iterations"])
+    assert st.true_residual <= 2e-6 * np.sqrt(st.u0)
+    x = r.x.values[:n]
+    assert np.linalg.norm(x - ref["x"][:n]) <= 1e-6 * np.linalg.norm(ref["x"][:n])
+    tr = np.array([[t.u, t.alpha, t.beta] for t in st.trace[:5]])
+    np.testing.assert_allclose(tr, ref["trace"][:5], rtol=1e-10)
+print("TAIL OK")
+'''
+    import os
+    env = dict(os.environ, HS_CG_TAIL="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert p.returncode == 0 and "TAIL OK" in p.stdout, p.stdout + p.stderr
