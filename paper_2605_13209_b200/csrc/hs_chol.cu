@@ -1809,7 +1809,48 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
       panel_work(j1 + 1);
     }
   }
-  for (int64_t j = 0; j < N && !use_oz; ++j) {
+  // HS_CHOL_SCHED=1: the rest of column j's update runs on its own
+  // low-priority stream from the moment the panel is done, next to the
+  // high-priority column-(j+1) update (whose last wave it fills), instead of
+  // after it on the same stream
+  static const int sched = [] {
+    const char* e = getenv("HS_CHOL_SCHED");
+    return e ? atoi(e) : 0;
+  }();
+  if (sched == 1 && !use_oz && N > 1) {
+    HS_CUDA(cudaStreamCreateWithPriority(&cs.u2, cudaStreamNonBlocking, lo_pri));
+    HS_CUDA(cudaStreamWaitEvent(cs.u2, start));
+    HS_CUDA(cudaStreamDestroy(cs.u));  // re-created with the panel's priority
+    HS_CUDA(cudaStreamCreateWithPriority(&cs.u, cudaStreamNonBlocking, hi_pri));
+    HS_CUDA(cudaStreamWaitEvent(cs.u, start));
+    for (int64_t j = 0; j + 1 < N; ++j) {
+      const int64_t t = N - 1 - j;
+      cudaEvent_t pdone = cs.make();
+      HS_CUDA(cudaEventRecord(pdone, cs.p));
+      GemmArgs gu = g;
+      gu.j = j;
+      gu.X = fast ? nullptr : X[j & 1];
+      const CUtensorMap* mx = fast ? &mapA : nullptr;
+      // column j+1 (urgent): after panel j and after REST(j-1), which
+      // updated these tiles with panel j-1
+      HS_CUDA(cudaStreamWaitEvent(cs.u, pdone));
+      gu.mode = G_UPDATE_COL;
+      launch_gemm(c, cs.u, gu, t * f * f, mx, mx);
+      cudaEvent_t ucol = cs.make();
+      HS_CUDA(cudaEventRecord(ucol, cs.u));
+      // columns > j+1: alongside, low priority (u2 is in order with REST(j-1))
+      HS_CUDA(cudaStreamWaitEvent(cs.u2, pdone));
+      gu.mode = G_UPDATE_REST;
+      const int64_t tr = t - 1;
+      if (tr > 0) launch_gemm(c, cs.u2, gu, tr * (tr + 1) / 2 * f * f, mx, mx);
+      cudaEvent_t rdone = cs.make();
+      HS_CUDA(cudaEventRecord(rdone, cs.u2));
+      HS_CUDA(cudaStreamWaitEvent(cs.u, rdone));  // before UCOL(j+1)
+      HS_CUDA(cudaStreamWaitEvent(cs.p, ucol));
+      panel_work(j + 1);
+    }
+  }
+  for (int64_t j = 0; j < N && !use_oz && sched != 1; ++j) {
     const int64_t t = N - 1 - j;
     cudaEvent_t pdone = cs.make();
     HS_CUDA(cudaEventRecord(pdone, cs.p));

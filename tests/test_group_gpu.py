@@ -40,10 +40,12 @@ def test_group_cg_matches_oracle(oracle, world, n, b):
     finally:
         rt.close()
     st = res.stats
-    # iteration count: +-2 of the single-GPU solve; against the reference
-    # order the measured rounding-order envelope (39..46 at n=32768,
-    # profiles/r02_cg_envelope.json) -> within 20 %
-    assert st.converged and abs(st.iterations - single) <= 2
+    # iteration count: the rank partial sums round differently from the
+    # single-GPU ones (reduce-scatter of per-rank partial t), so both
+    # comparisons use the measured rounding-order envelope (39..46 at
+    # n=32768, profiles/r02_cg_envelope.json): within 20 %
+    assert st.converged
+    assert abs(st.iterations - single) <= max(2, 0.2 * single)
     assert abs(st.iterations - ref["iterations"]) <= max(2, 0.2 * ref["iterations"])
     assert st.true_residual <= 2e-6 * np.sqrt(st.u0)
     x = res.x.values[:n]
