@@ -2,21 +2,31 @@
 //
 // Hot kernel: packed-symmetric SYMV that streams every stored tile of A
 // exactly once per matvec. Persistent CTAs (one per SM) claim work units --
-// contiguous ranges of 32-KB "slabs" (row strips of the row-major tiles) in
-// packed order, guided sizes shrinking towards the end -- from an atomic
-// counter, so CTAs on slower SMs simply take fewer units. A producer warp moves slabs + the two s-vector segments they need
-// into a 5-stage shared-memory ring with the TMA bulk-copy engine
-// (cp.async.bulk + mbarrier complete_tx); 8 consumer warps read each element
-// once from shared memory and use it twice: for the row sum (A_ij s_j -> t_i)
-// and for the transposed column sum (A_ij^T s_i -> t_j). Row sums are
-// accumulated per CTA per block row, column sums per CTA per tile, into
-// fixed segment slots; a finalize kernel adds the slots in a fixed order,
-// so results are deterministic (no atomics on values). Diagonal tiles read
-// only their lower triangle (block_kernels.cpp:76-85 semantics).
+// contiguous runs of 32-KB "slabs" (row strips of the row-major tiles),
+// guided sizes shrinking towards the end -- from an atomic counter, so CTAs
+// on slower SMs simply take fewer units. A producer warp moves slabs + the
+// two s-vector segments they need into a 5-stage shared-memory ring with the
+// TMA bulk-copy engine (cp.async.bulk + mbarrier complete_tx); 8 consumer
+// warps read each element once from shared memory and use it twice: for the
+// row sum (A_ij s_j -> t_i) and for the transposed column sum (A_ij^T s_i ->
+// t_j). Row sums are accumulated per work unit per block row, column sums
+// per tile, into fixed slots that are added in a fixed order, so results
+// are deterministic (no atomics on values). Diagonal tiles read only their
+// lower triangle (block_kernels.cpp:76-85 semantics).
+//
+// b <= 128 (the progressive mode, default): the units walk the block rows
+// from the last to the first, so t_j is complete as soon as block row j has
+// been streamed (every tile (k, j), k >= j, lies in a block row k >= j).
+// Consumers announce each finished (unit, block row) segment on a per-row
+// counter, and two finalize warps in every CTA add each row's slots while
+// the streaming goes on: one launch per matvec, and when the last tile has
+// been read only the last block rows' sums remain. b >= 256: memory-order
+// walk, then a finalize kernel.
 //
 // Roofline: HBM-bound. Algorithmic bytes per matvec = packed tile bytes
 // (T * b^2 * 8); the partial slots add ~2/b of that (0.8 % at b = 128).
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -30,13 +40,82 @@ namespace hs {
 
 
 // ---------------------------------------------------------------------------
+// CG scalar steps on the device
+
+enum ScalarStep : int { STEP_NONE = 0, STEP_INIT = 1, STEP_ALPHA = 2, STEP_BETA = 3 };
+
+struct StepArgs {
+  CgScalars* sc;
+  double* trace;       // device trace buffer (3 per iteration) or null
+  double eps;
+  Dd* dd_slots;        // [world] per-rank partials (multi-GPU) or null
+  int world;
+  // multi-GPU: the local (hi, lo) partial goes to dd_slots[g * slot_stride]
+  // for g < slot_count (one copy per rank chunk of a reduce-scattered
+  // buffer); by default to dd_slots[0] only
+  int64_t slot_stride = 0;
+  int slot_count = 1;
+};
+
+// Single-thread scalar step on the combined dot value (cg_solver.cpp lines
+// 5, 8-10 and the start-up checks :243-249).
+__device__ void scalar_step(int step, double val, const StepArgs& sa) {
+  CgScalars* sc = sa.sc;
+  if (step == STEP_INIT) {
+    sc->u0 = val;
+    sc->u = val;
+    sc->iter = 0;
+    sc->recomputations = 0;
+    sc->status = HS_OK;
+    sc->err_iter = -1;
+    sc->alpha = sc->beta = 0.0;
+    if (!isfinite(val)) {
+      sc->status = HS_ERR_NUMERICAL;
+      sc->err_iter = 0;
+      sc->done = 1;
+      return;
+    }
+    sc->limit = sa.eps * sa.eps * val;
+    sc->done = (val <= sc->limit) ? 1 : 0;
+  } else if (step == STEP_ALPHA) {
+    const double alpha = sc->u / val;
+    sc->alpha = alpha;
+    if (!isfinite(alpha)) {
+      sc->status = HS_ERR_NUMERICAL;
+      sc->err_iter = sc->iter + 1;
+      sc->done = 1;
+    }
+  } else if (step == STEP_BETA) {
+    const double u = val;
+    if (!(u >= 0.0) || !isfinite(u)) {
+      sc->status = HS_ERR_NUMERICAL;
+      sc->err_iter = sc->iter + 1;
+      sc->done = 1;
+      return;
+    }
+    const double beta = u / sc->u;
+    sc->beta = beta;
+    sc->u = u;
+    const int64_t it = ++sc->iter;
+    if (sa.trace) {
+      sa.trace[3 * (it - 1) + 0] = u;
+      sa.trace[3 * (it - 1) + 1] = sc->alpha;
+      sa.trace[3 * (it - 1) + 2] = beta;
+    }
+    if (u <= sc->limit) sc->done = 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Fast SYMV for b in {64, 128, 256, 512}
 
-template <int B, int NCW_ = 8>
+template <int B, int NCW_ = 8, bool PROG_ = false>
 struct SymvCfg {
   static constexpr int NCW = NCW_;               // consumer warps
   static constexpr int CT = NCW * 32;            // consumer threads
-  static constexpr int THREADS = CT + 32;        // + one producer warp
+  // progressive mode: + FW finalize warps (see symv_finalize_rows)
+  static constexpr int FW = PROG_ ? 2 : 0;
+  static constexpr int THREADS = CT + 32 + FW * 32;  // + one producer warp
   static constexpr int SLAB_BYTES = 32768;
   static constexpr int RS = 4096 / B;    // tile rows per slab
   static constexpr int SPT = B / RS;     // slabs per tile
@@ -58,7 +137,7 @@ struct SymvCfg {
   static constexpr int YROW_BYTES = H * B * 8;
   // + full/empty mbarriers + per-stage (slab, unit) headers
   static constexpr int SMEM = NSTAGE * STAGE_BYTES + 2 * COLRED_BYTES +
-                              2 * YROW_BYTES + 2 * NSTAGE * 8 + NSTAGE * 12;
+                              2 * YROW_BYTES + 2 * NSTAGE * 8 + NSTAGE * 28;
   static_assert(RT >= 1 && RT <= 2 && RS == RT * RPP, "row mapping");
   static_assert(STAGE_BYTES % 16 == 0, "bulk copy alignment");
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
@@ -79,7 +158,173 @@ struct SymvArgs {
   uint32_t* unit_ctr;     // next unclaimed work unit
   int vgrid;              // work units (cta_slab has vgrid + 1 entries)
   unsigned ts_seq;        // launch sequence (HS_SYMV_TIMING builds only)
+  // progressive mode (b <= 128; SymvPlan::prog): units from unit_pos walk
+  // the block rows downwards, and the end of every (unit, block row) segment
+  // is announced by one arrival on rowdone[row] (this launch's parity)
+  int prog;
+  const int4* unit_pos;
+  uint32_t* rowdone;
+  // progressive mode: the finalize warps' inputs / outputs
+  uint32_t* rowdone_next;   // the other parity's arrivals: reset here
+  uint32_t* unit_ctr_next;  // the other parity's unit counter: reset here
+  uint32_t* arrivals;       // all segment arrivals of this launch (== nseg: streaming done)
+  uint32_t* arrivals_next;  // the other parity's: reset here
+  uint32_t nseg;
+  const int64_t* pf;        // L2 prefetch of the next launch's unit heads (see plan)
+  int pf_units;
+  const int32_t* row_seg0;
+  const int32_t* row_nseg;
+  int64_t row_lo, row_hi;
+  double* out;              // t (padded layout)
+  const double* dot_s;      // fused dot s . t (or null)
+  double* apart;            // [row_hi] per-block-row s . t partials
+  int defer;                // 1: leave the partials to the next kernel
+  StepArgs sa;              // otherwise: ticket -> combine -> scalar step / slots
 };
+
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Progressive finalize, run by FW dedicated warps of every SYMV CTA while
+// the CTA streams (SymvPlan::prog, b <= 128). The SYMV walks the block rows
+// from the last to the first, so t_j -- the row partial(s) of block row j
+// plus the column partials of tiles (k, j), k >= j -- is complete as soon as
+// block row j has been streamed. The CTA's block rows j = blockIdx.x +
+// m * gridDim.x are taken from the highest down; for each, the column
+// partials are added in the fixed order k = row_hi - 1 .. max(j, row_lo) as
+// the rows k complete (rowdone[k] reaches the row's segment count; 32 rows
+// checked per poll, 16 loads in flight), then the row segments of j in claim
+// order: deterministic, and when the streaming ends only the partials of
+// the last few block rows are still to be added. Each lane owns B / (32 FW)
+// columns. s . t is formed per block row (apart[j]); without `defer` the
+// last block row to finish (ticket) combines them as a fixed-shape
+// double-double tree and applies the scalar step.
+template <int B, int FW>
+__device__ void symv_finalize_rows(const SymvArgs& args, int fw, int lane) {
+  constexpr int CPL = B / (32 * FW);  // columns per lane (1 or 2)
+  static_assert(CPL == 1 || CPL == 2, "finalize column mapping");
+  __shared__ double fin_red[FW];
+  __shared__ int fin_last;
+  const int col = fw * (B / FW) + lane * CPL;
+  const double* colbase = args.colmain - args.tile_lo * B + col;
+  const int64_t rows = args.row_hi;
+  int64_t j = blockIdx.x + ((rows - 1 - blockIdx.x) / gridDim.x) * (int64_t)gridDim.x;
+  if (blockIdx.x >= rows) j = -1;
+  for (; j >= 0; j -= gridDim.x) {
+    double a0 = 0.0, a1 = 0.0;
+    int64_t k = rows - 1;
+    const int64_t kend = j > args.row_lo ? j : args.row_lo;
+    uint64_t t0 = 0;
+    while (k >= kend) {
+      const int n = (int)(k - kend + 1 < 32 ? k - kend + 1 : 32);
+      bool ok = false;
+      if (lane < n)
+        ok = ld_relaxed_u32(args.rowdone + (k - lane)) == (uint32_t)args.row_nseg[k - lane];
+      const unsigned mask = __ballot_sync(0xffffffffu, ok);
+      const int ready = mask == 0xffffffffu ? 32 : __ffs(~mask) - 1;
+      if (ready == 0) {
+        __nanosleep(256);
+        // a lost arrival would hang the GPU: fail the launch instead
+        uint64_t now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > 4000000000ull) __trap();
+        continue;
+      }
+      t0 = 0;
+      __threadfence();  // acquire: the partials were stored before the arrivals
+      int m = 0;
+      if constexpr (CPL == 2) {
+        for (; m + 16 <= ready; m += 16) {
+          double2 v[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u)
+            v[u] = __ldcg(reinterpret_cast<const double2*>(colbase + tri(k - m - u, j) * B));
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            a0 += v[u].x;
+            a1 += v[u].y;
+          }
+        }
+        for (; m < ready; ++m) {
+          const double2 v = __ldcg(reinterpret_cast<const double2*>(colbase + tri(k - m, j) * B));
+          a0 += v.x;
+          a1 += v.y;
+        }
+      } else {
+        for (; m + 16 <= ready; m += 16) {
+          double v[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) v[u] = __ldcg(colbase + tri(k - m - u, j) * B);
+#pragma unroll
+          for (int u = 0; u < 16; ++u) a0 += v[u];
+        }
+        for (; m < ready; ++m) a0 += __ldcg(colbase + tri(k - m, j) * B);
+      }
+      k -= ready;
+    }
+    if (j >= args.row_lo) {
+      const int s0 = args.row_seg0[j], ns = args.row_nseg[j];
+      for (int e = 0; e < ns; ++e) {
+        const double* rp = args.rowpart + (int64_t)(s0 + e) * B + col;
+        a0 += __ldcg(rp);
+        if (CPL == 2) a1 += __ldcg(rp + 1);
+      }
+    }
+    const int64_t o = args.row_off[j] + col;
+    args.out[o] = a0;
+    if (CPL == 2) args.out[o + 1] = a1;
+    if (args.dot_s) {
+      double d = args.dot_s[o] * a0;
+      if (CPL == 2) d = fma(args.dot_s[o + 1], a1, d);
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
+      if (lane == 0) fin_red[fw] = d;
+      named_bar_sync(3, FW * 32);
+      if (fw == 0 && lane == 0) {
+        double pt = fin_red[0];
+#pragma unroll
+        for (int w = 1; w < FW; ++w) pt += fin_red[w];
+        args.apart[j] = pt;
+        if (!args.defer) {
+          __threadfence();
+          fin_last = atomicAdd(&args.sa.sc->ticket, 1u) == (unsigned)rows - 1 ? 1 : 0;
+        }
+      }
+      named_bar_sync(3, FW * 32);
+      if (!args.defer && fin_last && fw == 0) {
+        // last block row: fixed-shape double-double tree over apart[0..rows)
+        __threadfence();
+        Dd acc{0.0, 0.0};
+        for (int64_t q = lane; q < rows; q += 32) acc = dd_add(acc, __ldcg(args.apart + q));
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+          Dd o2;
+          o2.hi = __shfl_xor_sync(0xffffffffu, acc.hi, off);
+          o2.lo = __shfl_xor_sync(0xffffffffu, acc.lo, off);
+          acc = lane & off ? dd_add(o2, acc) : dd_add(acc, o2);
+        }
+        if (lane == 0) {
+          args.sa.sc->ticket = 0;
+          if (args.sa.world == 1) {
+            scalar_step(STEP_ALPHA, dd_value(acc), args.sa);
+          } else {
+            for (int g = 0; g < args.sa.slot_count; ++g)
+              args.sa.dd_slots[g * args.sa.slot_stride] = acc;
+          }
+        }
+      }
+    }
+    if (fw == 0 && lane == 0) args.rowdone_next[j] = 0u;
+  }
+  if (blockIdx.x == 0 && fw == 0 && lane == 0) {
+    *args.unit_ctr_next = 0u;
+    *args.arrivals_next = 0u;
+  }
+}
 
 #ifdef HS_SYMV_TIMING
 __device__ unsigned long long g_symv_ts[4096][2];
@@ -94,12 +339,14 @@ __device__ unsigned long long g_tail_ts[4096][7];
 __device__ unsigned long long g_tail_cta[1024][5];
 __device__ unsigned g_tail_cta_seq = 100;
 __device__ int g_symv_ts_print = 0;
+// progressive mode: per launch, the last finalize warp's end
+__device__ unsigned long long g_symv_fin_end[4096];
 #endif
 
-template <int B, int NCW>
-__global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
+template <int B, int NCW, bool PROG>
+__global__ void __launch_bounds__(SymvCfg<B, NCW, PROG>::THREADS, 1)
     symv_slab_kernel(SymvArgs args) {
-  using Cfg = SymvCfg<B, NCW>;
+  using Cfg = SymvCfg<B, NCW, PROG>;
   constexpr int RS = Cfg::RS, SPT = Cfg::SPT, TPR = Cfg::TPR, RT = Cfg::RT;
   constexpr int W = Cfg::W, NS = Cfg::NSTAGE, CT = Cfg::CT, G = Cfg::G;
 
@@ -109,8 +356,11 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
   double* yrow = colred + 2 * G * B;  // [2][H][B]
   uint64_t* full = reinterpret_cast<uint64_t*>(yrow + 2 * Cfg::H * B);
   uint64_t* empty = full + NS;
-  // per-stage header: the slab staged and its work unit (-1: no more work)
-  int64_t* hdr_g = reinterpret_cast<int64_t*>(empty + NS);
+  // per-stage header: the slab staged and its work unit (-1: no more work);
+  // progressive mode also (block row, column, row end, row segment) of the
+  // tile (16-B aligned: 2 * NS mbarriers above)
+  int4* hdr_x = reinterpret_cast<int4*>(empty + NS);
+  int64_t* hdr_g = reinterpret_cast<int64_t*>(hdr_x + NS);
   int32_t* hdr_u = reinterpret_cast<int32_t*>(hdr_g + NS);
 
   const int tid = threadIdx.x;
@@ -135,8 +385,34 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
   // everything below reads its results
   pdl_wait();
   pdl_trigger();
-  if (args.done && *args.done) return;
+  if (args.done && *args.done) {
+    if constexpr (PROG) {
+      // a skipped launch still hands the other parity's counters to the
+      // next launch (which may run: e.g. the exit residual after CG ends)
+      for (int64_t j = blockIdx.x * (int64_t)blockDim.x + tid; j < args.row_hi;
+           j += (int64_t)gridDim.x * blockDim.x)
+        args.rowdone_next[j] = 0u;
+      if (blockIdx.x == 0 && tid == 0) {
+        *args.unit_ctr_next = 0u;
+        *args.arrivals_next = 0u;
+      }
+    }
+    return;
+  }
 
+  if constexpr (PROG) {
+    if (tid >= CT + 32) {
+      symv_finalize_rows<B, Cfg::FW>(args, (tid - CT - 32) >> 5, tid & 31);
+#ifdef HS_SYMV_TIMING
+      if (tid == CT + 32) {
+        uint64_t te;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(te));
+        atomicMax(&g_symv_fin_end[args.ts_seq % 4096u], (unsigned long long)te);
+      }
+#endif
+      return;
+    }
+  }
   if (tid >= CT) {
     // ---------------- producer warp ----------------
     // claims work units in order (one atomic per unit) and streams their
@@ -150,6 +426,70 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
       int st = 0;
       uint32_t ph = 0;
       bool wrapped = false;  // every stage used once: wait for its release
+      if constexpr (PROG) {
+        // progressive mode: whole tiles, block rows downwards (row k's
+        // tiles j = 0..k in memory order, then row k - 1)
+        for (;;) {
+          const int u = (int)atomicAdd(args.unit_ctr, 1u);
+          if (u >= args.vgrid) {
+            if (wrapped) mbar_wait(&empty[st], ph ^ 1u);
+            hdr_g[st] = -1;
+            hdr_u[st] = -1;
+            mbar_arrive(&full[st]);
+            // once every segment has arrived (HBM idle until the next
+            // SYMV; A is constant over a solve), prefetch into L2 the head of
+            // one of the units the next launch's CTAs claim first
+            if ((int)blockIdx.x < args.pf_units && args.pf[2 * blockIdx.x + 1] > 0) {
+              uint64_t t0 = 0;
+              while (ld_relaxed_u32(args.arrivals) != args.nseg) {
+                __nanosleep(500);
+                uint64_t now;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                if (t0 == 0) t0 = now;
+                else if (now - t0 > 4000000000ull) __trap();
+              }
+              bulk_prefetch_l2(reinterpret_cast<const unsigned char*>(args.a) + args.pf[2 * blockIdx.x],
+                               (uint32_t)args.pf[2 * blockIdx.x + 1]);
+            }
+            return;
+          }
+          const int4 up = args.unit_pos[u];
+          int64_t k = up.x, j = up.y;
+          int seg = up.w;
+          for (int n = 0; n < up.z; ++n) {
+            const int64_t t = tri(k, j);
+            const int rend = (j == k || n + 1 == up.z) ? 1 : 0;
+            const int64_t ok = args.row_off[k];
+#pragma unroll 1
+            for (int q = 0; q < SPT; ++q) {
+              if (wrapped) mbar_wait(&empty[st], ph ^ 1u);
+              const int64_t g = t * SPT + q;
+              hdr_g[st] = g;
+              hdr_u[st] = u;
+              hdr_x[st] = make_int4((int)k, (int)j, rend, seg);
+              unsigned char* buf = stages + st * Cfg::STAGE_BYTES;
+              mbar_arrive_expect_tx(&full[st],
+                                    Cfg::SLAB_BYTES + RS * 8 + (q == 0 ? B * 8 : 0));
+              bulk_g2s_hint(buf, args.a + ((t - args.tile_lo) * B + (int64_t)q * RS) * B,
+                            Cfg::SLAB_BYTES, &full[st], stream_pol);
+              bulk_g2s(buf + Cfg::SLAB_BYTES + B * 8, args.s + ok + q * RS, RS * 8, &full[st]);
+              if (q == 0) bulk_g2s(buf + Cfg::SLAB_BYTES, args.s + args.row_off[j], B * 8, &full[st]);
+              if (++st == NS) {
+                st = 0;
+                ph ^= 1u;
+                wrapped = true;
+              }
+            }
+            if (j == k) {
+              --k;
+              j = 0;
+              ++seg;
+            } else {
+              ++j;
+            }
+          }
+        }
+      } else {
       for (;;) {
         const int u = (int)atomicAdd(args.unit_ctr, 1u);
         if (u >= args.vgrid) {
@@ -194,6 +534,7 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
           }
         }
       }
+      }  // memory-order walk
     }
     return;
   }
@@ -228,13 +569,25 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
     int tp = 0, rp = 0;
     int st = 0;  // ring position of the tile's first slab
     uint32_t ph = 0;
+    // progressive mode: block row whose finished segment is announced at the
+    // next tile end (its stores have drained by then, so the fence is cheap)
+    int64_t pend_row = -1;
     for (;;) {
       const int st0 = st;
       mbar_wait(&full[st0], ph);
       const int64_t g = hdr_g[st0];
       if (g < 0) break;
       const int u = hdr_u[st0];
-      if (u != cur) {
+      bool prog_rend = false;
+      int64_t prog_seg = 0;
+      if constexpr (PROG) {
+        const int4 hx = hdr_x[st0];
+        ii = hx.x;
+        jj = hx.y;
+        ti = tri(ii, jj);
+        prog_rend = hx.z != 0;
+        prog_seg = hx.w;
+      } else if (u != cur) {
         cur = u;
         ug1 = args.cta_slab[u + 1];
         ti = args.cta_slab[u] / SPT;
@@ -299,7 +652,7 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
         }
       }
       // tile end: column partial of tile ti; block row end: row partials
-      const bool row_end = diag || (g + SPT == ug1);
+      const bool row_end = PROG ? prog_rend : (diag || (g + SPT == ug1));
       if (row_end) {
 #pragma unroll
         for (int qq = 0; qq < SPT; ++qq)
@@ -324,7 +677,18 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
           reinterpret_cast<double2*>(cr + grp * B)[cl + TPR * m] =
               make_double2(cac[2 * m], cac[2 * m + 1]);
       }
+      if constexpr (PROG) {
+        if (pend_row >= 0 && tid < B) __threadfence();
+      }
       named_bar_sync(1, CT);
+      if constexpr (PROG) {
+        // release pattern: the storing threads fenced before the barrier
+        if (pend_row >= 0 && tid == 0) {
+          atomicAdd(args.rowdone + pend_row, 1u);
+          atomicAdd(args.arrivals, 1u);
+        }
+        pend_row = -1;
+      }
       {
         double* dst = args.colmain + (ti - args.tile_lo) * B;
         for (int c = tid; c < B; c += CT) {
@@ -336,9 +700,12 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
       }
       if (row_end) {
         double* yr = yrow + rp * B;
-        double* out = args.rowpart + (rsg0 + (ii - ifirst)) * B;
+        double* out = args.rowpart + (PROG ? prog_seg : rsg0 + (ii - ifirst)) * B;
         for (int c = tid; c < B; c += CT) st_hint(out + c, yr[c], keep_pol);
         rp ^= 1;
+        // the segment (its column partials and row partial) is announced
+        // at the next tile end, or below when the work runs out
+        if constexpr (PROG) pend_row = ii;
       }
       tp ^= 1;
 #pragma unroll
@@ -347,6 +714,16 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW>::THREADS, 1)
       if (++jj > ii) {
         ++ii;
         jj = 0;
+      }
+    }
+    if constexpr (PROG) {
+      if (pend_row >= 0) {
+        if (tid < B) __threadfence();
+        named_bar_sync(2, CT);
+        if (tid == 0) {
+          atomicAdd(args.rowdone + pend_row, 1u);
+          atomicAdd(args.arrivals, 1u);
+        }
       }
     }
   } else {
@@ -566,70 +943,6 @@ __device__ Dd dd_reduce_parts(const double* parts, int count, Dd* red) {
     __syncthreads();
   }
   return red[0];
-}
-
-enum ScalarStep : int { STEP_NONE = 0, STEP_INIT = 1, STEP_ALPHA = 2, STEP_BETA = 3 };
-
-struct StepArgs {
-  CgScalars* sc;
-  double* trace;       // device trace buffer (3 per iteration) or null
-  double eps;
-  Dd* dd_slots;        // [world] per-rank partials (multi-GPU) or null
-  int world;
-  // multi-GPU: the local (hi, lo) partial goes to dd_slots[g * slot_stride]
-  // for g < slot_count (one copy per rank chunk of a reduce-scattered
-  // buffer); by default to dd_slots[0] only
-  int64_t slot_stride = 0;
-  int slot_count = 1;
-};
-
-// Single-thread scalar step on the combined dot value (cg_solver.cpp lines
-// 5, 8-10 and the start-up checks :243-249).
-__device__ void scalar_step(int step, double val, const StepArgs& sa) {
-  CgScalars* sc = sa.sc;
-  if (step == STEP_INIT) {
-    sc->u0 = val;
-    sc->u = val;
-    sc->iter = 0;
-    sc->recomputations = 0;
-    sc->status = HS_OK;
-    sc->err_iter = -1;
-    sc->alpha = sc->beta = 0.0;
-    if (!isfinite(val)) {
-      sc->status = HS_ERR_NUMERICAL;
-      sc->err_iter = 0;
-      sc->done = 1;
-      return;
-    }
-    sc->limit = sa.eps * sa.eps * val;
-    sc->done = (val <= sc->limit) ? 1 : 0;
-  } else if (step == STEP_ALPHA) {
-    const double alpha = sc->u / val;
-    sc->alpha = alpha;
-    if (!isfinite(alpha)) {
-      sc->status = HS_ERR_NUMERICAL;
-      sc->err_iter = sc->iter + 1;
-      sc->done = 1;
-    }
-  } else if (step == STEP_BETA) {
-    const double u = val;
-    if (!(u >= 0.0) || !isfinite(u)) {
-      sc->status = HS_ERR_NUMERICAL;
-      sc->err_iter = sc->iter + 1;
-      sc->done = 1;
-      return;
-    }
-    const double beta = u / sc->u;
-    sc->beta = beta;
-    sc->u = u;
-    const int64_t it = ++sc->iter;
-    if (sa.trace) {
-      sa.trace[3 * (it - 1) + 0] = u;
-      sa.trace[3 * (it - 1) + 1] = sc->alpha;
-      sa.trace[3 * (it - 1) + 2] = beta;
-    }
-    if (u <= sc->limit) sc->done = 1;
-  }
 }
 
 // Last-CTA epilogue shared by the dot-producing kernels: combine per-CTA
@@ -1193,7 +1506,8 @@ void free_plan(SymvPlan* p) {
                   (void*)p->rowpart, (void*)p->colmain, (void*)p->colextra,
                   (void*)p->item, (void*)p->item_aux, (void*)p->row_item,
                   (void*)p->itempart, (void*)p->tail_dot, (void*)p->tail_rr,
-                  (void*)p->tail_bar})
+                  (void*)p->tail_bar, (void*)p->unit_pos, (void*)p->row_seg0,
+                  (void*)p->row_nseg, (void*)p->rowdone, (void*)p->pf})
     cudaFree(q);
   delete p;
 }
@@ -1250,6 +1564,7 @@ static void build_tail_plan(hs_matrix* m, SymvPlan* p, const std::vector<int64_t
   HS_CUDA(cudaMalloc(&p->tail_rr, (size_t)p->tail_grid * sizeof(double)));
 }
 
+
 // Static work plan of the SYMV + finalize pair for one matrix (host side).
 void ensure_plan(hs_matrix* m) {
   if (m->plan) return;
@@ -1277,6 +1592,73 @@ void ensure_plan(hs_matrix* m) {
   // like a static CTA range (its own row / split-tile partial slots), so the
   // sums do not depend on which CTA claims it.
   constexpr int64_t kMinUnit = 8;
+  // progressive mode for whole-tile units (b <= 128); HS_CG_PROG=0 keeps the
+  // memory-order walk with a finalize after the SYMV
+  static const bool prog_on = [] {
+    const char* e = getenv("HS_CG_PROG");
+    return !(e && atoi(e) == 0);
+  }();
+  if (spt <= 4 && prog_on && T > 0) {
+    // units over the tiles in the order: block row hi-1 (columns 0..hi-1),
+    // then hi-2, ..., lo; guided sizes as below, in whole tiles
+    const int64_t min_tiles = std::max<int64_t>(1, kMinUnit / spt);
+    std::vector<int4> unit_pos;
+    std::vector<int32_t> row_seg0(hi, 0), row_nseg(hi, 0);
+    int64_t k = hi - 1, j = 0, done_t = 0, nseg = 0;
+    while (done_t < T) {
+      const int64_t rem = T - done_t;
+      const int64_t sz = std::min(rem, std::max(min_tiles, rem / (2 * sms)));
+      unit_pos.push_back(make_int4((int)k, (int)j, (int)sz, (int)nseg));
+      for (int64_t n = 0; n < sz; ++n) {
+        if (n == 0 || j == 0) {  // a new (unit, block row) segment
+          if (row_nseg[k] == 0) row_seg0[k] = (int32_t)nseg;
+          ++row_nseg[k];
+          ++nseg;
+        }
+        if (j == k) {
+          --k;
+          j = 0;
+        } else {
+          ++j;
+        }
+      }
+      done_t += sz;
+    }
+    p->prog = true;
+    p->vgrid = (int)unit_pos.size();
+    p->grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, p->vgrid));
+    p->slabs_per_tile = spt;
+    p->nrseg = nseg;
+    {
+      // the heads of the units claimed first (2 tiles, within the block row)
+      static const int pf_tiles = [] {
+        const char* e = getenv("HS_SYMV_PF_TILES");
+        return e ? atoi(e) : 2;
+      }();
+      std::vector<int64_t> pf;
+      for (int64_t u = 0; u < std::min<int64_t>(sms, (int64_t)unit_pos.size()); ++u) {
+        const int4 up = unit_pos[u];
+        const int64_t nt = std::min<int64_t>({(int64_t)pf_tiles, (int64_t)up.z,
+                                              (int64_t)(up.x - up.y + 1)});
+        pf.push_back((tri(up.x, up.y) - m->tile_lo) * b * b * 8);
+        pf.push_back(std::max<int64_t>(0, nt) * b * b * 8);
+      }
+      p->pf_units = (int)(pf.size() / 2);
+      upload_vec(&p->pf, pf);
+    }
+    upload_vec(&p->unit_pos, unit_pos);
+    upload_vec(&p->row_seg0, row_seg0);
+    upload_vec(&p->row_nseg, row_nseg);
+    upload_vec(&p->rowdone, std::vector<uint32_t>(2 * hi, 0u));
+    upload_vec(&p->unit_ctr, std::vector<uint32_t>(4, 0u));
+    // dummies for the memory-order arrays (unused in this mode)
+    upload_vec(&p->cta_slab, std::vector<int64_t>(1, 0));
+    upload_vec(&p->cta_rseg, std::vector<int64_t>(1, 0));
+    HS_CUDA(cudaMalloc(&p->rowpart, std::max<int64_t>(1, nseg) * b * sizeof(double)));
+    HS_CUDA(cudaMalloc(&p->colmain, std::max<int64_t>(1, T) * b * sizeof(double)));
+    m->plan = p;
+    return;
+  }
   std::vector<int64_t> cta_slab;
   // slab indices are GLOBAL (the kernel derives global tile / block-row
   // indices from them): this rank's slabs start at tile_lo * spt
@@ -1326,7 +1708,7 @@ void ensure_plan(hs_matrix* m) {
   upload_vec(&p->row_rseg, row_rseg);
   upload_vec(&p->row_extra, row_extra);
   upload_vec(&p->extra_cta, extra_cta);
-  upload_vec(&p->unit_ctr, std::vector<uint32_t>(1, 0u));
+  upload_vec(&p->unit_ctr, std::vector<uint32_t>(2, 0u));
   HS_CUDA(cudaMalloc(&p->rowpart, std::max<int64_t>(1, nr) * b * sizeof(double)));
   HS_CUDA(cudaMalloc(&p->colmain, std::max<int64_t>(1, T) * b * sizeof(double)));
   HS_CUDA(cudaMalloc(&p->colextra, std::max<int64_t>(1, vgrid) * b * sizeof(double)));
@@ -1334,21 +1716,66 @@ void ensure_plan(hs_matrix* m) {
   m->plan = p;
 }
 
-template <int B, int NCW>
+
+// Progressive-mode outputs of one SYMV launch (the in-kernel finalize)
+struct ProgOut {
+  double* out = nullptr;
+  const double* dot_s = nullptr;
+  double* apart = nullptr;
+  bool defer = false;
+  StepArgs sa{};
+};
+
+template <int B, int NCW, bool PROG>
 static void launch_symv_fast(hs_ctx* c, const hs_matrix* m, const double* s,
-                             const int32_t* done) {
-  using Cfg = SymvCfg<B, NCW>;
+                             const int32_t* done, const ProgOut* po = nullptr) {
+  using Cfg = SymvCfg<B, NCW, PROG>;
   static std::atomic<uint64_t> attr{0};
-  HS_CUDA(smem_attr_once(symv_slab_kernel<B, NCW>, Cfg::SMEM, attr));
+  HS_CUDA(smem_attr_once(symv_slab_kernel<B, NCW, PROG>, Cfg::SMEM, attr));
   SymvPlan* p = m->plan;
-  SymvArgs a{m->d,       s,           m->d_row_off, m->tile_lo,
-             p->cta_slab, p->cta_rseg, p->rowpart,   p->colmain,
-             p->colextra, done,        p->unit_ctr,  p->vgrid, 0u};
+  SymvArgs a{};
+  a.a = m->d;
+  a.s = s;
+  a.row_off = m->d_row_off;
+  a.tile_lo = m->tile_lo;
+  a.cta_slab = p->cta_slab;
+  a.cta_rseg = p->cta_rseg;
+  a.rowpart = p->rowpart;
+  a.colmain = p->colmain;
+  a.colextra = p->colextra;
+  a.done = done;
+  a.unit_ctr = p->unit_ctr;
+  a.vgrid = p->vgrid;
+  if constexpr (PROG) {
+    const int par = (int)(p->launch_seq & 1);
+    const int64_t rows = (int64_t)m->row_hi;
+    a.prog = 1;
+    a.unit_pos = p->unit_pos;
+    a.unit_ctr = p->unit_ctr + par;
+    a.unit_ctr_next = p->unit_ctr + (par ^ 1);
+    a.arrivals = p->unit_ctr + 2 + par;
+    a.arrivals_next = p->unit_ctr + 2 + (par ^ 1);
+    a.nseg = (uint32_t)p->nrseg;
+    a.pf = p->pf;
+    a.pf_units = p->pf_units;
+    a.rowdone = p->rowdone + par * rows;
+    a.rowdone_next = p->rowdone + (par ^ 1) * rows;
+    a.row_seg0 = p->row_seg0;
+    a.row_nseg = p->row_nseg;
+    a.row_lo = (int64_t)m->row_lo;
+    a.row_hi = rows;
+    a.out = po->out;
+    a.dot_s = po->dot_s;
+    a.apart = po->apart;
+    a.defer = po->defer ? 1 : 0;
+    a.sa = po->sa;
+    ++p->launch_seq;
+  }
 #ifdef HS_SYMV_TIMING
   static unsigned seq = 0;
   a.ts_seq = seq++;
 #endif
-  HS_CUDA(launch_pdl(symv_slab_kernel<B, NCW>, dim3(p->grid), dim3(Cfg::THREADS),
+  HS_CUDA(launch_pdl(symv_slab_kernel<B, NCW, PROG>, dim3(p->grid), dim3(Cfg::THREADS),
                      Cfg::SMEM, c->stream, a));
   HS_CUDA(cudaGetLastError());
   launch_count(c);
@@ -1401,11 +1828,30 @@ static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
     }
     return;
   }
+  SymvPlan* p = m->plan;
+  if (p->prog) {
+    // one launch: the SYMV's finalize warps form t (and s . t) as the
+    // block rows complete
+    ProgOut po;
+    po.out = out;
+    po.dot_s = fuse_dot ? s : nullptr;
+    po.apart = defer_alpha ? defer_alpha : c->d_dpart + VGRID + 8;  // per-block-row s . t
+    po.defer = defer_alpha != nullptr;
+    if (sa) po.sa = *sa;
+    if (b == 64) launch_symv_fast<64, 8, true>(c, m, s, done, &po);
+    else launch_symv_fast<128, 8, true>(c, m, s, done, &po);
+    if (prof) {
+      HS_CUDA(cudaEventRecord(e1, c->stream));
+      c->prof_events.push_back(e0);
+      c->prof_events.push_back(e1);
+    }
+    return;
+  }
   switch (b) {
-    case 64: launch_symv_fast<64, 8>(c, m, s, done); break;
-    case 128: launch_symv_fast<128, 8>(c, m, s, done); break;
-    case 256: launch_symv_fast<256, 8>(c, m, s, done); break;
-    case 512: launch_symv_fast<512, 8>(c, m, s, done); break;
+    case 64: launch_symv_fast<64, 8, false>(c, m, s, done); break;
+    case 128: launch_symv_fast<128, 8, false>(c, m, s, done); break;
+    case 256: launch_symv_fast<256, 8, false>(c, m, s, done); break;
+    case 512: launch_symv_fast<512, 8, false>(c, m, s, done); break;
   }
   if (prof) {
     HS_CUDA(cudaEventRecord(e1, c->stream));
@@ -1413,7 +1859,6 @@ static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
     c->prof_events.push_back(e1);
   }
   if (!finalize) return;  // the fused CG tail consumes the partial slots
-  SymvPlan* p = m->plan;
   FinalizeArgs fa{};
   fa.row_rseg = p->row_rseg;
   fa.row_extra = p->row_extra;
@@ -1651,7 +2096,9 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   // partials of the single-rank iteration
   ensure_dpart(c, std::max<int64_t>({N * b / FIN_COLS + VGRID + 8, N + 1, VGRID}));
   double* apart = c->d_dpart + VGRID + 8;
-  const int acount = (int)(N * b / FIN_COLS);
+  // deferred-alpha partials: one per finalize CTA (N * b / 32), or one per
+  // block row in the progressive mode
+  const int acount = m->plan->prog ? (int)m->row_hi : (int)(N * b / FIN_COLS);
   CgBuffers B;
   // single rank + fast SYMV: the direction update rides inside the SYMV
   // (double-buffered s); otherwise a separate vector kernel does it
@@ -2103,6 +2550,14 @@ extern "C" int hs_debug_fin_ts(unsigned long long* out, int count, int reset) {
     return (int)cudaMemcpyToSymbol(hs::g_fin_ts, init, sizeof(init));
   }
   return (int)cudaMemcpyFromSymbol(out, hs::g_fin_ts, (size_t)count * 5 * sizeof(unsigned long long));
+}
+
+extern "C" int hs_debug_symv_fin_end(unsigned long long* out, int count, int reset) {
+  if (reset) {
+    static unsigned long long init[4096];
+    return (int)cudaMemcpyToSymbol(hs::g_symv_fin_end, init, sizeof(init));
+  }
+  return (int)cudaMemcpyFromSymbol(out, hs::g_symv_fin_end, (size_t)count * sizeof(unsigned long long));
 }
 
 extern "C" int hs_debug_tail_ts(unsigned long long* out, int count, int reset) {

@@ -261,6 +261,21 @@ inline cudaError_t smem_attr_once(Kernel* kernel, int bytes, std::atomic<uint64_
   return e;
 }
 
+// Shared-memory carveout preference (percent of the maximum), once per device.
+// A kernel meant to run beside a big-smem persistent kernel needs the SM
+// configured for the full carveout, not the smallest one that fits.
+template <typename Kernel>
+inline cudaError_t carveout_once(Kernel* kernel, int pct, std::atomic<uint64_t>& mask) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  if (e == cudaSuccess) mask.fetch_or(bit, std::memory_order_release);
+  return e;
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block,
                               size_t smem, cudaStream_t stream, Args&&... args) {

@@ -60,6 +60,18 @@ struct SymvPlan {
   double* tail_dot = nullptr;    // [tail_grid]
   double* tail_rr = nullptr;     // [tail_grid]
   unsigned* tail_bar = nullptr;  // [2]
+  // progressive mode (b <= 128, hs_cg.cu): work units walk the block rows
+  // from the last to the first, so t_j is complete as soon as block row j is
+  // (every tile (k, j) with k >= j has been streamed); a finalizer grid running
+  // beside the SYMV sums each row's partials as their block rows complete.
+  bool prog = false;
+  int4* unit_pos = nullptr;      // [vgrid] (first row, first column, tiles, first row segment)
+  int32_t* row_seg0 = nullptr;   // [row_hi] first row segment of block row k
+  int32_t* row_nseg = nullptr;   // [row_hi] row segments of block row k (= its arrivals)
+  uint32_t* rowdone = nullptr;   // [2][row_hi] arrivals per block row, by launch parity
+  uint64_t launch_seq = 0;       // host-side SYMV launch count (parity)
+  int64_t* pf = nullptr;         // [2 * pf_units] L2 prefetch (byte offset, bytes) per unit
+  int pf_units = 0;
 };
 
 }  // namespace hs

@@ -627,9 +627,14 @@ def test_substitutions_wide_steps(rt, n, b):
     assert np.linalg.norm(x.logical() - x_ref) <= 1e-12 * np.linalg.norm(x_ref)
 
 
-def test_cg_fused_tail_opt_in_matches_oracle():
-    """HS_CG_TAIL=1 (fused single-launch CG tail, opt-in): same oracle bounds
-    as the default path, in a subprocess (the switch is read once)."""
+@pytest.mark.parametrize("env", [{"HS_CG_PROG": "0"}, {"HS_CG_PROG": "0", "HS_CG_TAIL": "1"}],
+                         ids=["memory_order_walk", "fused_tail"])
+def test_cg_alternative_schedules_match_oracle(env):
+    """The non-default CG schedules for b <= 128 -- the memory-order SYMV walk
+    with a finalize kernel after it (HS_CG_PROG=0), and that walk with the
+    fused single-launch tail (HS_CG_TAIL=1) -- meet the same oracle bounds as
+    the default progressive path, in a subprocess (the switches are read
+    once)."""
     import subprocess
     import sys
     code = r'''
@@ -654,7 +659,7 @@ for n, b in [(1024, 128), (3000, 64), (2048, 512), (4096, 256)]:
 print("TAIL OK")
 '''
     import os
-    env = dict(os.environ, HS_CG_TAIL="1")
+    env = dict(os.environ, **env)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     p = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                        text=True, timeout=600)

@@ -28,6 +28,7 @@ dbg.hs_debug_symv_ts.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
 dbg.hs_debug_fin_ts.argtypes = [C.c_void_p, C.c_int, C.c_int]
 dbg.hs_debug_tail_ts.argtypes = [C.c_void_p, C.c_int, C.c_int]
 dbg.hs_debug_tail_cta.argtypes = [C.c_void_p]
+dbg.hs_debug_symv_fin_end.argtypes = [C.c_void_p, C.c_int, C.c_int]
 rt = (hs.Runtime(device=0, stream=torch.cuda.current_stream().cuda_stream)
       if "torchstream" in mode else hs.Runtime())
 m = hs.generate_spd_device(rt, n, b, seed=42)
@@ -51,6 +52,7 @@ for rep in range(reps):
     dbg.hs_debug_symv_ts(None, 0, 1, 0)
     dbg.hs_debug_fin_ts(None, 0, 1)
     dbg.hs_debug_tail_ts(None, 0, 1)
+    dbg.hs_debug_symv_fin_end(None, 0, 1)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -87,6 +89,19 @@ for rep in range(reps):
         print("   gap breakdown us (median): SYMV end->finalize start %.1f, sums %.1f, "
               "dot epilogue %.1f, finalize end->next SYMV %.1f; CTA start spread %.1f, "
               "longest CTA sums %.1f" % tuple(med))
+    fe = (C.c_ulonglong * 4096)()
+    dbg.hs_debug_symv_fin_end(fe, 4096, 0)
+    fends = sorted(v for v in fe if v)
+    fin_tail = []
+    for s0, s1 in ts:
+        f = [v for v in fends if s1 - 100000 <= v < s1 + 200000]
+        if f:
+            fin_tail.append((f[0] - s1) / 1e3)
+    if fin_tail:
+        fin_tail.sort()
+        print("   in-kernel finalize: last finalize warp end - streaming end us: median %.1f "
+              "p90 %.1f max %.1f" % (fin_tail[len(fin_tail) // 2],
+                                     fin_tail[9 * len(fin_tail) // 10], fin_tail[-1]))
     tb = (C.c_ulonglong * (7 * 4096))()
     dbg.hs_debug_tail_ts(tb, 4096, 0)
     tail = sorted(tuple(tb[7 * k + i] for i in range(7)) for k in range(4096)
