@@ -737,6 +737,7 @@ __global__ void __launch_bounds__(256)
   extern __shared__ double S[];       // [128][129]
   double* Tm = S + DCB * DLD;         // [96][33] scratch
   __shared__ double Rv[DPB];          // reciprocal diagonal of the panel
+  __shared__ __align__(16) double Ck[2 * DPB];  // warp 0's broadcast column / row
   __shared__ int bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #pragma unroll 8
@@ -765,39 +766,50 @@ __global__ void __launch_bounds__(256)
     for (int p = 0; p < DCB / DPB; ++p) {
       const int o = p * DPB;
       if (warp == 0) {
-        // right-looking 32x32 factor in smem, lane r owns row r; fixed-bound
-        // predicated inner loop (no register arrays -> no local memory)
+        // right-looking 32x32 factor in registers: lane r owns row r of the
+        // block (fully unrolled, so a[] stays in registers); the pivot comes
+        // from lane k and column k of L from the owning lanes by shuffle
         double* Dp = S + o * DLD + o;
-        int failed = -1;
-        for (int k = 0; k < DPB; ++k) {
-          const double akk = Dp[k * DLD + k];
-          if (!(akk > 0.0)) {
-            failed = k;
-            break;
-          }
-          // akk = +Inf passes the pivot test as in potf_block
-          // (block_kernels.cpp:9-21): L_kk = sqrt(Inf) = Inf and the column
-          // below is finite / Inf = 0 (rsqrt(Inf) = 0); akk * rinv would be
-          // NaN there, so the diagonal takes akk itself
-          const double rinv = rsqrt(akk);
-          const double lrk = lane > k ? Dp[lane * DLD + k] * rinv : 0.0;
-          __syncwarp();
-          if (lane == k) Dp[k * DLD + k] = isinf(akk) ? akk : akk * rinv;
-          if (lane > k) Dp[lane * DLD + k] = lrk;
-          __syncwarp();
-// column k of L comes from the owning lanes by shuffle; only this lane's
-          // own row is touched in smem, so loads / stores pipeline
-          double* myrow = Dp + lane * DLD;
+        double a[DPB];
 #pragma unroll
-          for (int c = 1; c < DPB; ++c) {
-            const double lck = __shfl_sync(0xffffffffu, lrk, c);
-            if (c > k && c <= lane) myrow[c] = fma(-lrk, lck, myrow[c]);
+        for (int c = 0; c < DPB; ++c) a[c] = c <= lane ? Dp[lane * DLD + c] : 0.0;
+        int failed = -1;
+#pragma unroll
+        for (int k = 0; k < DPB; ++k) {
+          const double akk = __shfl_sync(0xffffffffu, a[k], k);
+          // warp-uniform (broadcast pivot); no `break`, which would put a[]
+          // in local memory
+          if (failed < 0 && !(akk > 0.0)) failed = k;
+          if (failed < 0) {
+            // akk = +Inf passes the pivot test as in potf_block
+            // (block_kernels.cpp:9-21): L_kk = sqrt(Inf) = Inf and the column
+            // below is finite / Inf = 0 (rsqrt(Inf) = 0); akk * rinv would be
+            // NaN there, so the diagonal takes akk itself
+            const double rinv = rsqrt(akk);
+            const double lrk = lane > k ? a[k] * rinv : 0.0;
+            if (lane == k) a[k] = isinf(akk) ? akk : akk * rinv;
+            if (lane > k) a[k] = lrk;
+            // column k of L to every lane through a shared-memory broadcast
+            // (double-buffered by step parity; 16-B loads), then the rank-1
+            // update of this lane's row. Entries right of the diagonal
+            // (c > lane) take garbage that is never read or stored; lanes
+            // <= k have lrk = 0 and keep their rows
+            double* colk = Ck + (k & 1) * DPB;
+            colk[lane] = lrk;
+            __syncwarp();
+#pragma unroll
+            for (int c = k + 1; c < DPB; ++c) a[c] = fma(-lrk, colk[c], a[c]);
           }
-          __syncwarp();
         }
         if (failed >= 0) {
+          // the rows as far as the factorization got (the failing column's
+          // pivot is reported; the tile is not used further)
           if (lane == 0) bad = o + failed;
         } else {
+#pragma unroll
+          for (int c = 0; c < DPB; ++c)
+            if (c <= lane) Dp[lane * DLD + c] = a[c];
+          __syncwarp();
           Rv[lane] = 1.0 / Dp[lane * DLD + lane];  // reciprocal diagonal
         }
       }
@@ -900,21 +912,41 @@ __global__ void __launch_bounds__(256)
     HS_PHASE("inv_T");
     // (2) lane c inverts column c of the 32x32 diagonal block (registers)
     if (warp == 0) {
-      Rv[lane] = 1.0 / S[(o + lane) * DLD + o + lane];
-      __syncwarp();
-      double w[DPB];
+      // W_pp = L_pp^-1 by rows in registers: lane r holds row r of L (a[])
+      // and of W (w[]). Step k: lane k's row is final once scaled by
+      // 1 / L_kk; every lane r > k then subtracts L_rk W_k,c (W_k,c by
+      // shuffle) -- the column-by-column recurrence
+      // W_rc = (delta_rc - sum_{c<=k<r} L_rk W_kc) / L_rr with the same
+      // k-ascending order, as independent chains across c
+      double a[DPB], w[DPB];
 #pragma unroll
-      for (int r = 0; r < DPB; ++r) {
-        double acc = (r == lane) ? 1.0 : 0.0;
+      for (int c = 0; c < DPB; ++c) {
+        a[c] = c <= lane ? S[(o + lane) * DLD + o + c] : 0.0;
+        w[c] = c == lane ? 1.0 : 0.0;
+      }
 #pragma unroll
-        for (int k = 0; k < r; ++k)
-          if (k >= lane) acc = fma(-S[(o + r) * DLD + o + k], w[k], acc);
-        w[r] = r >= lane ? acc * Rv[r] : 0.0;
+      for (int k = 0; k < DPB; ++k) {
+        // lane k's row is final once scaled; it reaches the other lanes
+        // through shared memory (double-buffered by step parity)
+        double* rowk = Ck + (k & 1) * DPB;
+        if (lane == k) {
+          const double rk = 1.0 / a[k];
+#pragma unroll
+          for (int c = 0; c <= k; ++c) {
+            w[c] *= rk;
+            rowk[c] = w[c];
+          }
+        }
+        __syncwarp();
+        // lanes > k subtract L_rk W_k,c; the others multiply by -0 (exact)
+        const double lrk = lane > k ? a[k] : 0.0;
+#pragma unroll
+        for (int c = 0; c <= k; ++c) w[c] = fma(-lrk, rowk[c], w[c]);
       }
       __syncwarp();
 #pragma unroll
-      for (int r = 0; r < DPB; ++r)
-        if (r >= lane) S[(o + r) * DLD + o + lane] = w[r];
+      for (int c = 0; c < DPB; ++c)
+        if (c <= lane) S[(o + lane) * DLD + o + c] = w[c];
     }
     __syncthreads();
     HS_PHASE("inv_diag");
@@ -1850,6 +1882,18 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
       panel_work(j + 1);
     }
   }
+  // HS_CHOL_TIMING=1: per-column event times of the default schedule on
+  // stderr (panel chain on P, column-(j+1) update and rest on U)
+  static const bool col_timing = getenv("HS_CHOL_TIMING") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  auto tmark = [&](cudaStream_t st) {
+    if (!col_timing) return;
+    cudaEvent_t e;
+    HS_CUDA(cudaEventCreate(&e));
+    HS_CUDA(cudaEventRecord(e, st));
+    tev.push_back(e);
+  };
+  tmark(cs.p);
   for (int64_t j = 0; j < N && !use_oz && sched != 1; ++j) {
     const int64_t t = N - 1 - j;
     cudaEvent_t pdone = cs.make();
@@ -1861,17 +1905,35 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
     gu.X = fast ? nullptr : X[j & 1];
     const CUtensorMap* mx = fast ? &mapA : nullptr;
     // lookahead: tile column j+1 first
+    tmark(cs.u);
     gu.mode = G_UPDATE_COL;
     launch_gemm(c, cs.u, gu, t * f * f, mx, mx);
     cudaEvent_t ucol = cs.make();
     HS_CUDA(cudaEventRecord(ucol, cs.u));
+    tmark(cs.u);
     HS_CUDA(cudaStreamWaitEvent(cs.p, ucol));
     // the rest of column j's update overlaps column j+1's panel work (the
     // panel touches only tile column j+1; the update reads column j)
     gu.mode = G_UPDATE_REST;
     const int64_t tr = t - 1;
     launch_gemm(c, cs.u, gu, tr * (tr + 1) / 2 * f * f, mx, mx);
+    tmark(cs.u);
+    tmark(cs.p);
     panel_work(j + 1);
+    tmark(cs.p);
+  }
+  if (col_timing && !tev.empty()) {
+    HS_CUDA(cudaDeviceSynchronize());
+    auto ms = [&](size_t k) {
+      float v = 0.f;
+      cudaEventElapsedTime(&v, tev[0], tev[k]);
+      return v;
+    };
+    fprintf(stderr, "chol timing: j ucol_start ucol_end rest_end panel_start panel_end (ms)\n");
+    for (size_t k = 1, j = 0; k + 4 < tev.size() + 1 && k + 4 <= tev.size(); k += 5, ++j)
+      fprintf(stderr, "chol %3zu %9.3f %9.3f %9.3f %9.3f %9.3f\n", j, ms(k), ms(k + 1),
+              ms(k + 2), ms(k + 3), ms(k + 4));
+    for (cudaEvent_t e : tev) cudaEventDestroy(e);
   }
   cudaEvent_t pend = cs.make(), uend = cs.make();
   HS_CUDA(cudaEventRecord(pend, cs.p));
