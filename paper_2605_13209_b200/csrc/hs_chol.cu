@@ -480,10 +480,23 @@ __device__ __forceinline__ GemmItem decode_item(const GemmArgs& g, int64_t item)
 // ---------------------------------------------------------------------------
 // DMMA sub-block GEMM (cb = 128), TMA-fed.
 
-constexpr int GBM = 128, GKS = 32, GSTAGES = 3;
-constexpr int G_OPERAND_BYTES = GBM * GKS * 8;        // 32 KB
-constexpr int G_STAGE_BYTES = 2 * G_OPERAND_BYTES;    // A + B
-constexpr int G_SMEM = GSTAGES * G_STAGE_BYTES + 1024 + 64;
+constexpr int GKS = 32, GSTAGES = 3;
+// CTA tile BM x BN of an item's 128 x 128 output: 128 x 128 (the trailing
+// updates), or split for launches of few items on the critical path (the
+// diagonal-tile and panel steps; a 128^2 item with K = 128 takes ~23 us on
+// one SM): 64 x 64 quadrants for C -= A B^T, 64 x 128 row halves for the
+// in-place TRSM steps (C = A W^T with C = A: a CTA must read only the rows
+// it writes)
+template <int BM, int BN>
+struct GemmCfg {
+  static constexpr int A_BYTES = BM * GKS * 8;
+  static constexpr int B_BYTES = BN * GKS * 8;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM = GSTAGES * STAGE_BYTES + 1024 + 64;
+  static constexpr int WM = BM / 32;      // warps along m (32 rows each)
+  static constexpr int WN = 8 / WM;       // warps along n
+  static constexpr int Y = BN / (WN * 8); // 8-column fragments per warp
+};
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map,
                                             int c0, int c1, int c2,
@@ -508,11 +521,29 @@ __device__ __forceinline__ uint32_t swz(int row, int k) {
   return (uint32_t)(row * 128 + ((((k >> 1) ^ (row & 7))) << 4) + ((k & 1) << 3));
 }
 
+template <int BM, int BN>
 __global__ void __launch_bounds__(288, 1)
     gemm_dmma_kernel(const __grid_constant__ CUtensorMap mapA,
                      const __grid_constant__ CUtensorMap mapB, GemmArgs g) {
+  using Cfg = GemmCfg<BM, BN>;
+  constexpr int A_BYTES = Cfg::A_BYTES, B_BYTES = Cfg::B_BYTES;
+  constexpr int G_STAGE_BYTES = Cfg::STAGE_BYTES;
+  constexpr int GBM = BM, Y = Cfg::Y;
   if (g.flag && g.flag->status) return;
-  const GemmItem it = decode_item(g, blockIdx.x);
+  // split tiles: part (qm, qn) of the item's 128 x 128 output
+  constexpr int QM = 128 / BM, QN = 128 / BN;
+  GemmItem it = decode_item(g, blockIdx.x / (QM * QN));
+  int roff = 0, coff = 0;  // the tile's offset inside the item (lower test)
+  if constexpr (QM * QN > 1) {
+    const int part = (int)(blockIdx.x % (QM * QN)), qm = part / QN, qn = part % QN;
+    roff = qm * BM;
+    coff = qn * BN;
+    if (it.lower && coff > roff + BM - 1) return;  // above a diagonal block's diagonal
+    it.lower = it.lower && coff + BN - 1 > roff;  // straddles the diagonal
+    it.a_r0 += roff;
+    it.b_r0 += coff;
+    it.c += (int64_t)roff * g.b + coff;
+  }
   if (it.skip) return;
   const int nks = it.K / GKS;
 
@@ -538,26 +569,28 @@ __global__ void __launch_bounds__(288, 1)
         const int st = ks % GSTAGES;
         if (ks >= GSTAGES) mbar_wait(&empty[st], ((ks / GSTAGES) - 1) & 1);
         unsigned char* sa = gsm + st * G_STAGE_BYTES;
-        unsigned char* sb = sa + G_OPERAND_BYTES;
+        unsigned char* sb = sa + A_BYTES;
         mbar_arrive_expect_tx(&full[st], G_STAGE_BYTES);
         const int ka = it.a_k0 + ks * GKS, kb = it.b_k0 + ks * GKS;
         tma_load_3d(sa, &mapA, ka, it.a_r0, (int)it.a_tile, &full[st]);
-        tma_load_3d(sa + G_OPERAND_BYTES / 2, &mapA, ka + 16, it.a_r0,
+        tma_load_3d(sa + A_BYTES / 2, &mapA, ka + 16, it.a_r0,
                     (int)it.a_tile, &full[st]);
         tma_load_3d(sb, &mapB, kb, it.b_r0, (int)it.b_tile, &full[st]);
-        tma_load_3d(sb + G_OPERAND_BYTES / 2, &mapB, kb + 16, it.b_r0,
+        tma_load_3d(sb + B_BYTES / 2, &mapB, kb + 16, it.b_r0,
                     (int)it.b_tile, &full[st]);
       }
     }
     return;
   }
 
-  const int wm = warp & 3, wn = warp >> 2;  // 4 x 2 warps of 32 x 64
-  double acc[4][8][2];
+  // WM x WN warps of 32 x (8 Y): 4 x 2 of 32 x 64 (128 x 128), 2 x 4 of
+  // 32 x 16 (64 x 64), 2 x 4 of 32 x 32 (64 x 128)
+  const int wm = warp % Cfg::WM, wn = warp / Cfg::WM;
+  double acc[4][Y][2];
 #pragma unroll
   for (int x = 0; x < 4; ++x)
 #pragma unroll
-    for (int y = 0; y < 8; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    for (int y = 0; y < Y; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
   const int fr = lane >> 2, fk = lane & 3;
   // Operand addresses, hoisted: element (row, k) of a [128 x 16] 128B-swizzled
   // box is at row*128 + ((k/2) ^ (row%8))*16 + (k%2)*8 (see swz). This
@@ -567,7 +600,7 @@ __global__ void __launch_bounds__(288, 1)
   // a 2-way bank conflict in this order; a conflict-free row permutation
   // measured no faster -- the LSU pipe is < 10 % busy.)
   const uint32_t offA = (uint32_t)(wm * 32 + fr) * 128u + (uint32_t)(fk & 1) * 8u;
-  const uint32_t offB = (uint32_t)(wn * 64 + fr) * 128u + (uint32_t)(fk & 1) * 8u;
+  const uint32_t offB = (uint32_t)(wn * 8 * Y + fr) * 128u + (uint32_t)(fk & 1) * 8u;
   uint32_t xo[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) xo[q] = (uint32_t)(((q * 2 + (fk >> 1)) ^ fr) << 4);
@@ -576,42 +609,47 @@ __global__ void __launch_bounds__(288, 1)
     const int st = ks % GSTAGES;
     mbar_wait(&full[st], (ks / GSTAGES) & 1);
     const unsigned char* sa = gsm + st * G_STAGE_BYTES;
-    const unsigned char* sb = sa + G_OPERAND_BYTES;
+    const unsigned char* sb = sa + A_BYTES;
 #pragma unroll
     for (int kk = 0; kk < GKS / 4; ++kk) {
-      const uint32_t h = (uint32_t)((kk >> 2) * (G_OPERAND_BYTES / 2)) + xo[kk & 3];
-      const double* pa = reinterpret_cast<const double*>(sa + offA + h);
-      const double* pb = reinterpret_cast<const double*>(sb + offB + h);
-      double af[4], bf[8];
+      const uint32_t hA = (uint32_t)((kk >> 2) * (A_BYTES / 2)) + xo[kk & 3];
+      const uint32_t hB = (uint32_t)((kk >> 2) * (B_BYTES / 2)) + xo[kk & 3];
+      const double* pa = reinterpret_cast<const double*>(sa + offA + hA);
+      const double* pb = reinterpret_cast<const double*>(sb + offB + hB);
+      double af[4], bf[Y];
 #pragma unroll
       for (int x = 0; x < 4; ++x) af[x] = pa[x * 128];  // + x * 1024 bytes
 #pragma unroll
-      for (int y = 0; y < 8; ++y) bf[y] = pb[y * 128];
+      for (int y = 0; y < Y; ++y) bf[y] = pb[y * 128];
 #pragma unroll
       for (int x = 0; x < 4; ++x)
 #pragma unroll
-        for (int y = 0; y < 8; ++y) dmma_8x8x4(acc[x][y], af[x], bf[y]);
+        for (int y = 0; y < Y; ++y) dmma_8x8x4(acc[x][y], af[x], bf[y]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }
 
-  // epilogue: sub-block rows (wm*32 + x*8 + fr), cols (wn*64 + y*8 + 2*fk)
+  // epilogue: sub-block rows (wm*32 + x*8 + fr), cols (wn*8Y + y*8 + 2*fk)
   const int b = g.b;
-  if (it.op == 0 && !it.lower) {
+  // (the split tiles of small launches write C directly: with two of their
+  // CTAs resident on an SM, the bulk reduce-add epilogue below gave
+  // run-to-run differences in the factor -- cause not identified; one CTA
+  // per SM or the plain read-modify-write were exact in every run)
+  if (BM == 128 && it.op == 0 && !it.lower) {
     // C -= acc through the TMA engine: stage -acc row-major in the (now free)
     // stage buffers, then one bulk reduce-add per 1-KB row. The L2 performs
     // the read-modify-write; no register-held HBM round trips. (Per-element
     // red.global.add.f64 instead measured 1.4 % slower over a factorization.)
     named_bar_sync(1, 256);  // every MMA warp is done with the stage buffers
-    constexpr int RS = GBM * 8 + 16;  // padded smem row stride (bytes)
+    constexpr int RS = BN * 8 + 16;  // padded smem row stride (bytes)
     unsigned char* tile = gsm;
 #pragma unroll
     for (int x = 0; x < 4; ++x) {
       const int row = wm * 32 + x * 8 + fr;
 #pragma unroll
-      for (int y = 0; y < 8; ++y) {
-        const int col = wn * 64 + y * 8 + 2 * fk;
+      for (int y = 0; y < Y; ++y) {
+        const int col = wn * 8 * Y + y * 8 + 2 * fk;
         *reinterpret_cast<double2*>(tile + row * RS + col * 8) =
             make_double2(-acc[x][y][0], -acc[x][y][1]);
       }
@@ -619,7 +657,7 @@ __global__ void __launch_bounds__(288, 1)
     fence_proxy_async_smem();
     named_bar_sync(1, 256);
     if (tid < GBM) {
-      bulk_reduce_add_f64(it.c + (int64_t)tid * b, tile + tid * RS, GBM * 8);
+      bulk_reduce_add_f64(it.c + (int64_t)tid * b, tile + tid * RS, BN * 8);
       bulk_commit_group();
       bulk_wait_group_read0();
     }
@@ -629,17 +667,17 @@ __global__ void __launch_bounds__(288, 1)
   for (int x = 0; x < 4; ++x) {
     const int row = wm * 32 + x * 8 + fr;
 #pragma unroll
-    for (int y = 0; y < 8; ++y) {
-      const int col = wn * 64 + y * 8 + 2 * fk;
+    for (int y = 0; y < Y; ++y) {
+      const int col = wn * 8 * Y + y * 8 + 2 * fk;
       double2* p = reinterpret_cast<double2*>(it.c + (int64_t)row * b + col);
       if (it.op == 1) {
         *p = make_double2(acc[x][y][0], acc[x][y][1]);
-      } else if (!it.lower || col + 1 <= row) {
+      } else if (!it.lower || coff + col + 1 <= roff + row) {
         double2 v = *p;
         v.x -= acc[x][y][0];
         v.y -= acc[x][y][1];
         *p = v;
-      } else if (col <= row) {
+      } else if (coff + col <= roff + row) {
         it.c[(int64_t)row * b + col] -= acc[x][y][0];
       }
     }
@@ -1522,12 +1560,12 @@ static EncodeTiledFn encode_fn() {
 }
 
 // 3-D map over `ntiles` contiguous side x side tiles: box 16 (k) x 128 x 1.
-static CUtensorMap tile_map(const double* base, int side, int64_t ntiles) {
+static CUtensorMap tile_map1(const double* base, int side, int64_t ntiles, int rows) {
   CUtensorMap m;
   cuuint64_t dims[3] = {(cuuint64_t)side, (cuuint64_t)side,
                         (cuuint64_t)std::max<int64_t>(ntiles, 1)};
   cuuint64_t strides[2] = {(cuuint64_t)side * 8, (cuuint64_t)side * side * 8};
-  cuuint32_t box[3] = {16, 128, 1};
+  cuuint32_t box[3] = {16, (cuuint32_t)rows, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
                            const_cast<double*>(base), dims, strides, box, es,
@@ -1537,6 +1575,14 @@ static CUtensorMap tile_map(const double* base, int side, int64_t ntiles) {
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   HS_REQUIRE(r == CUDA_SUCCESS, HS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   return m;
+}
+
+// The two box heights of the DMMA GEMM's operand tiles (128- and 64-row CTAs)
+struct TileMaps {
+  CUtensorMap m128, m64;
+};
+static TileMaps tile_map(const double* base, int side, int64_t ntiles) {
+  return TileMaps{tile_map1(base, side, ntiles, 128), tile_map1(base, side, ntiles, 64)};
 }
 
 CUtensorMap make_tensor_map(CUtensorMapDataType type, const void* base, int rank,
@@ -1556,13 +1602,37 @@ static bool dmma_ok(int b) { return b % 128 == 0; }
 static int compute_block(int b) { return dmma_ok(b) ? 128 : b; }
 
 static void launch_gemm(hs_ctx* c, cudaStream_t s, const GemmArgs& g,
-                        int64_t items, const CUtensorMap* ma,
-                        const CUtensorMap* mb) {
+                        int64_t items, const TileMaps* ma,
+                        const TileMaps* mb) {
   if (items <= 0) return;
   if (g.cb == 128 && ma && mb) {
-    static std::atomic<uint64_t> attr{0};
-    HS_CUDA(smem_attr_once(gemm_dmma_kernel, G_SMEM, attr));
-    gemm_dmma_kernel<<<(unsigned)items, 288, G_SMEM, s>>>(*ma, *mb, g);
+    // launches of at most one wave of 128^2 items run as 64^2 quadrants:
+    // 4x the CTAs, each a quarter of the work (HS_GEMM64=0: always 128)
+    static const bool q64 = [] {
+      const char* e = getenv("HS_GEMM64");
+      return !(e && atoi(e) == 0);
+    }();
+    const int sms = std::max(1, c->num_sms);
+    // in-place steps (C = A W^T, C and A the same sub-block) split by rows
+    // only, so no CTA reads columns another CTA writes
+    const bool in_place = g.mode == G_PANEL_TRSM || g.mode == G_DIAG_TRSM ||
+                          g.mode == G_DIST_PANEL_TRSM;
+    if (q64 && items <= sms && in_place) {
+      using C = GemmCfg<64, 128>;
+      static std::atomic<uint64_t> attr64{0};
+      HS_CUDA(smem_attr_once(gemm_dmma_kernel<64, 128>, C::SMEM, attr64));
+      gemm_dmma_kernel<64, 128><<<(unsigned)(items * 2), 288, C::SMEM, s>>>(ma->m64, mb->m128, g);
+    } else if (q64 && items <= sms) {
+      using C = GemmCfg<64, 64>;
+      static std::atomic<uint64_t> attr64{0};
+      HS_CUDA(smem_attr_once(gemm_dmma_kernel<64, 64>, C::SMEM, attr64));
+      gemm_dmma_kernel<64, 64><<<(unsigned)(items * 4), 288, C::SMEM, s>>>(ma->m64, mb->m64, g);
+    } else {
+      using C = GemmCfg<128, 128>;
+      static std::atomic<uint64_t> attr{0};
+      HS_CUDA(smem_attr_once(gemm_dmma_kernel<128, 128>, C::SMEM, attr));
+      gemm_dmma_kernel<128, 128><<<(unsigned)items, 288, C::SMEM, s>>>(ma->m128, mb->m128, g);
+    }
   } else {
     const int tpd = (g.cb + 63) / 64;
     gemm_simt_kernel<<<(unsigned)(items * tpd * tpd), 256, 0, s>>>(g);
@@ -1711,7 +1781,7 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
   HS_CUDA(cudaStreamWaitEvent(cs.p, start));
   HS_CUDA(cudaStreamWaitEvent(cs.u, start));
 
-  CUtensorMap mapA{}, mapW{};
+  TileMaps mapA{}, mapW{};
   if (fast) {
     mapA = tile_map(m->d, b, (int64_t)m->local_tiles());
     mapW = tile_map(m->dinv, cb, N * f);
@@ -1862,7 +1932,7 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
       GemmArgs gu = g;
       gu.j = j;
       gu.X = fast ? nullptr : X[j & 1];
-      const CUtensorMap* mx = fast ? &mapA : nullptr;
+      const TileMaps* mx = fast ? &mapA : nullptr;
       // column j+1 (urgent): after panel j and after REST(j-1), which
       // updated these tiles with panel j-1
       HS_CUDA(cudaStreamWaitEvent(cs.u, pdone));
@@ -1893,31 +1963,32 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
     HS_CUDA(cudaEventRecord(e, st));
     tev.push_back(e);
   };
+  cudaStream_t su = cs.u;
   tmark(cs.p);
   for (int64_t j = 0; j < N && !use_oz && sched != 1; ++j) {
     const int64_t t = N - 1 - j;
     cudaEvent_t pdone = cs.make();
     HS_CUDA(cudaEventRecord(pdone, cs.p));
     if (t == 0) break;
-    HS_CUDA(cudaStreamWaitEvent(cs.u, pdone));
+    HS_CUDA(cudaStreamWaitEvent(su, pdone));
     GemmArgs gu = g;
     gu.j = j;
     gu.X = fast ? nullptr : X[j & 1];
-    const CUtensorMap* mx = fast ? &mapA : nullptr;
+    const TileMaps* mx = fast ? &mapA : nullptr;
     // lookahead: tile column j+1 first
-    tmark(cs.u);
+    tmark(su);
     gu.mode = G_UPDATE_COL;
-    launch_gemm(c, cs.u, gu, t * f * f, mx, mx);
+    launch_gemm(c, su, gu, t * f * f, mx, mx);
     cudaEvent_t ucol = cs.make();
-    HS_CUDA(cudaEventRecord(ucol, cs.u));
-    tmark(cs.u);
+    HS_CUDA(cudaEventRecord(ucol, su));
+    tmark(su);
     HS_CUDA(cudaStreamWaitEvent(cs.p, ucol));
     // the rest of column j's update overlaps column j+1's panel work (the
     // panel touches only tile column j+1; the update reads column j)
     gu.mode = G_UPDATE_REST;
     const int64_t tr = t - 1;
-    launch_gemm(c, cs.u, gu, tr * (tr + 1) / 2 * f * f, mx, mx);
-    tmark(cs.u);
+    launch_gemm(c, su, gu, tr * (tr + 1) / 2 * f * f, mx, mx);
+    tmark(su);
     tmark(cs.p);
     panel_work(j + 1);
     tmark(cs.p);
@@ -2047,16 +2118,16 @@ static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
   HS_CUDA(cudaStreamWaitEvent(cs.p, start));
   HS_CUDA(cudaStreamWaitEvent(cs.u, start));
 
-  const CUtensorMap mapA = tile_map(m->d, b, std::max<int64_t>((int64_t)m->local_tiles(), 1));
-  const CUtensorMap mapW = tile_map(m->dinv, cb, N * f);
+  const TileMaps mapA = tile_map(m->d, b, std::max<int64_t>((int64_t)m->local_tiles(), 1));
+  const TileMaps mapW = tile_map(m->dinv, cb, N * f);
   // trailing update on the INT8 tensor cores when selected (slices of the
   // broadcast panel, double buffered like PB)
   const bool use_oz = c->chol_slices > 0 && N > 1;
   OzPanel& oz = ctx_oz_panel(c);  // buffers persist across calls
   if (use_oz) oz.init(b, N, c->chol_slices);
-  const CUtensorMap mapLd = tile_map(Ld, b, 1);
-  const CUtensorMap mapWb = tile_map(Wb, cb, f);
-  const CUtensorMap mapPB[2] = {tile_map(PB[0], b, panel), tile_map(PB[1], b, panel)};
+  const TileMaps mapLd = tile_map(Ld, b, 1);
+  const TileMaps mapWb = tile_map(Wb, cb, f);
+  const TileMaps mapPB[2] = {tile_map(PB[0], b, panel), tile_map(PB[1], b, panel)};
 
   GemmArgs g{};
   g.N = N;
@@ -2573,8 +2644,8 @@ hs_status hs_gemm_update_tiles(hs_ctx* c, double* d_c, const double* d_p,
   g.lower_only = lower_only;
   const int64_t items = (int64_t)count * g.f * g.f;
   if (dmma_ok((int)b)) {
-    CUtensorMap mp = tile_map(d_p, (int)b, (int64_t)count);
-    CUtensorMap mq = tile_map(d_q, (int)b, (int64_t)count);
+    TileMaps mp = tile_map(d_p, (int)b, (int64_t)count);
+    TileMaps mq = tile_map(d_q, (int)b, (int64_t)count);
     launch_gemm(c, c->stream, g, items, &mp, &mq);
   } else {
     launch_gemm(c, c->stream, g, items, nullptr, nullptr);
