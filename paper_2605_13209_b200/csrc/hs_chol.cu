@@ -273,6 +273,9 @@ enum GemmMode : int {
   G_DIST_UPDATE = 9,      // owned (i, k): A_ik -= PB_i PB_k^T
   G_DIST_PANEL_UPD = 10,  // owned panel rows i: A_ij[:,c] -= A_ij[:,<c] Ld[c,<c]^T
   G_DIST_PANEL_TRSM = 11, // owned panel rows i: A_ij[:,c] = A_ij[:,c] Wb_c^T
+  // column pairs (j, j1 = j + 1), K = 2b: A_ik -= [A_ij A_ij1] [A_kj A_kj1]^T
+  // for tile column k = step only (k1 == step + 1) or every k >= step
+  G_UPDATE_PAIR = 12,
 };
 
 struct GemmArgs {
@@ -293,6 +296,7 @@ struct GemmArgs {
   const CholFlag* flag;
   const int64_t* lpos;    // cyclic layout: global tile -> local slot
   const int32_t* list;    // dist modes: (i, k) pairs or panel rows i
+  int64_t k1;             // G_UPDATE_PAIR: step + 1 (one tile column) or N
 };
 
 struct GemmItem {
@@ -301,6 +305,8 @@ struct GemmItem {
   int lda, ldb;
   int64_t a_tile, b_tile;  // TMA coordinates: tile index, row, k offset
   int a_r0, a_k0, b_r0, b_k0;
+  // K = 2b column pairs: k-slices from k = b on come from these tiles
+  int64_t a_tile2 = -1, b_tile2 = -1;
   double* c;        // output sub-block (ld = b)
   int K;
   int op;           // 0 SUB, 1 SET
@@ -349,6 +355,31 @@ __device__ __forceinline__ GemmItem decode_item(const GemmArgs& g, int64_t item)
         it.a_tile = tile(i, g.j);
         it.b_tile = tile(k, g.j);
       }
+      it.a_r0 = mb * cb;
+      it.b_r0 = nb * cb;
+      it.c = sub(tile(i, k), mb, nb);
+      return it;
+    }
+    case G_UPDATE_PAIR: {
+      const int64_t u = item / (f * f);
+      const int sb = (int)(item % (f * f));
+      const int mb = sb / f, nb = sb % f;
+      int64_t i, k;
+      if (g.k1 == g.step + 1) {
+        k = g.step;
+        i = k + u;
+      } else {
+        const int64_t ii = tile_row(u);
+        i = g.step + ii;
+        k = g.step + (u - tri(ii, 0));
+      }
+      it.lower = (i == k) && mb == nb;
+      it.skip = (i == k) && nb > mb;
+      it.K = 2 * b;
+      it.a_tile = tile(i, g.j);
+      it.b_tile = tile(k, g.j);
+      it.a_tile2 = tile(i, g.j + 1);
+      it.b_tile2 = tile(k, g.j + 1);
       it.a_r0 = mb * cb;
       it.b_r0 = nb * cb;
       it.c = sub(tile(i, k), mb, nb);
@@ -571,13 +602,18 @@ __global__ void __launch_bounds__(288, 1)
         unsigned char* sa = gsm + st * G_STAGE_BYTES;
         unsigned char* sb = sa + A_BYTES;
         mbar_arrive_expect_tx(&full[st], G_STAGE_BYTES);
-        const int ka = it.a_k0 + ks * GKS, kb = it.b_k0 + ks * GKS;
-        tma_load_3d(sa, &mapA, ka, it.a_r0, (int)it.a_tile, &full[st]);
-        tma_load_3d(sa + A_BYTES / 2, &mapA, ka + 16, it.a_r0,
-                    (int)it.a_tile, &full[st]);
-        tma_load_3d(sb, &mapB, kb, it.b_r0, (int)it.b_tile, &full[st]);
-        tma_load_3d(sb + B_BYTES / 2, &mapB, kb + 16, it.b_r0,
-                    (int)it.b_tile, &full[st]);
+        int ka = it.a_k0 + ks * GKS, kb = it.b_k0 + ks * GKS;
+        int at = (int)it.a_tile, bt = (int)it.b_tile;
+        if (it.a_tile2 >= 0 && ks * GKS >= g.b) {  // second column of a pair
+          ka -= g.b;
+          kb -= g.b;
+          at = (int)it.a_tile2;
+          bt = (int)it.b_tile2;
+        }
+        tma_load_3d(sa, &mapA, ka, it.a_r0, at, &full[st]);
+        tma_load_3d(sa + A_BYTES / 2, &mapA, ka + 16, it.a_r0, at, &full[st]);
+        tma_load_3d(sb, &mapB, kb, it.b_r0, bt, &full[st]);
+        tma_load_3d(sb + B_BYTES / 2, &mapB, kb + 16, it.b_r0, bt, &full[st]);
       }
     }
     return;
@@ -1874,6 +1910,15 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
     //       panels and lookahead; the next pair's U work waits for it
     HS_CUDA(cudaStreamCreateWithPriority(&cs.u2, cudaStreamNonBlocking, lo_pri));
     HS_CUDA(cudaStreamWaitEvent(cs.u2, start));
+    static const bool oz_hi = [] {
+      const char* e = getenv("HS_OZ_U_HIPRI");
+      return !(e && atoi(e) == 0);
+    }();
+    if (oz_hi) {  // the lookahead updates ahead of the bulk (as the DMMA pairs)
+      HS_CUDA(cudaStreamDestroy(cs.u));
+      HS_CUDA(cudaStreamCreateWithPriority(&cs.u, cudaStreamNonBlocking, hi_pri));
+      HS_CUDA(cudaStreamWaitEvent(cs.u, start));
+    }
     cudaEvent_t rest_done = nullptr;
     for (int64_t j0 = 0; j0 < N; j0 += 2) {
       const int64_t j1 = j0 + 1;
@@ -1911,6 +1956,78 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
       panel_work(j1 + 1);
     }
   }
+  // DMMA in column pairs (the INT8 path's schedule above): the bulk of the
+  // trailing update runs with K = 2b per CTA, halving the per-CTA start-up and
+  // epilogue share of each 128^2 item (HS_CHOL_PAIRS=0: one column at a time)
+  static const bool pairs_env = [] {
+    const char* e = getenv("HS_CHOL_PAIRS");
+    return !(e && atoi(e) == 0);
+  }();
+  const bool pairs = pairs_env && fast && !use_oz && N >= 4;
+  if (pairs) {
+    HS_CUDA(cudaStreamCreateWithPriority(&cs.u2, cudaStreamNonBlocking, lo_pri));
+    HS_CUDA(cudaStreamWaitEvent(cs.u2, start));
+    // the lookahead updates feed the panel chain: the panel's priority, so
+    // they take SMs ahead of the bulk update on U2
+    HS_CUDA(cudaStreamDestroy(cs.u));
+    HS_CUDA(cudaStreamCreateWithPriority(&cs.u, cudaStreamNonBlocking, hi_pri));
+    HS_CUDA(cudaStreamWaitEvent(cs.u, start));
+    cudaEvent_t rest_done = nullptr;
+    int64_t j0 = 0;
+    for (; j0 + 1 < N; j0 += 2) {
+      const int64_t j1 = j0 + 1;
+      // tile column j1 by panel j0 alone, then panel j1
+      // (tile column j1 is not in the previous pair's bulk, which covers
+      // columns >= j1 + 2: that bulk keeps running beside this update and
+      // both of this pair's panels)
+      cudaEvent_t p0 = cs.make();
+      HS_CUDA(cudaEventRecord(p0, cs.p));
+      HS_CUDA(cudaStreamWaitEvent(cs.u, p0));
+      GemmArgs gu = g;
+      gu.j = j0;
+      gu.mode = G_UPDATE_COL;
+      launch_gemm(c, cs.u, gu, (N - 1 - j0) * f * f, &mapA, &mapA);
+      cudaEvent_t ucol = cs.make();
+      HS_CUDA(cudaEventRecord(ucol, cs.u));
+      HS_CUDA(cudaStreamWaitEvent(cs.p, ucol));
+      panel_work(j1);
+      if (j1 + 1 >= N) break;
+      // columns > j1 by the pair (K = 2b): j1+1 first (the next panel needs
+      // it), j1+2, then the bulk on U2 beside the next pair's panels
+      cudaEvent_t p1 = cs.make();
+      HS_CUDA(cudaEventRecord(p1, cs.p));
+      HS_CUDA(cudaStreamWaitEvent(cs.u, p1));
+      if (rest_done) HS_CUDA(cudaStreamWaitEvent(cs.u, rest_done));  // previous bulk
+      GemmArgs gp = g;
+      gp.j = j0;
+      gp.mode = G_UPDATE_PAIR;
+      gp.step = (int)(j1 + 1);
+      gp.k1 = j1 + 2;
+      launch_gemm(c, cs.u, gp, (N - 1 - j1) * f * f, &mapA, &mapA);
+      cudaEvent_t ua = cs.make();
+      HS_CUDA(cudaEventRecord(ua, cs.u));
+      rest_done = nullptr;
+      if (j1 + 2 < N) {
+        gp.step = (int)(j1 + 2);
+        gp.k1 = j1 + 3;
+        launch_gemm(c, cs.u, gp, (N - 2 - j1) * f * f, &mapA, &mapA);
+        cudaEvent_t ub = cs.make();
+        HS_CUDA(cudaEventRecord(ub, cs.u));
+        if (j1 + 3 < N) {
+          HS_CUDA(cudaStreamWaitEvent(cs.u2, ub));
+          gp.step = (int)(j1 + 3);
+          gp.k1 = N;
+          const int64_t tr = N - 3 - j1;
+          launch_gemm(c, cs.u2, gp, tr * (tr + 1) / 2 * f * f, &mapA, &mapA);
+          rest_done = cs.make();
+          HS_CUDA(cudaEventRecord(rest_done, cs.u2));
+        }
+      }
+      HS_CUDA(cudaStreamWaitEvent(cs.p, ua));
+      panel_work(j1 + 1);
+    }
+    // an odd trailing column: its panel j0 = N - 1 is the last one
+  }
   // HS_CHOL_SCHED=1: the rest of column j's update runs on its own
   // low-priority stream from the moment the panel is done, next to the
   // high-priority column-(j+1) update (whose last wave it fills), instead of
@@ -1919,7 +2036,7 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
     const char* e = getenv("HS_CHOL_SCHED");
     return e ? atoi(e) : 0;
   }();
-  if (sched == 1 && !use_oz && N > 1) {
+  if (sched == 1 && !use_oz && !pairs && N > 1) {
     HS_CUDA(cudaStreamCreateWithPriority(&cs.u2, cudaStreamNonBlocking, lo_pri));
     HS_CUDA(cudaStreamWaitEvent(cs.u2, start));
     HS_CUDA(cudaStreamDestroy(cs.u));  // re-created with the panel's priority
@@ -1965,7 +2082,7 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
   };
   cudaStream_t su = cs.u;
   tmark(cs.p);
-  for (int64_t j = 0; j < N && !use_oz && sched != 1; ++j) {
+  for (int64_t j = 0; j < N && !use_oz && !pairs && sched != 1; ++j) {
     const int64_t t = N - 1 - j;
     cudaEvent_t pdone = cs.make();
     HS_CUDA(cudaEventRecord(pdone, cs.p));
