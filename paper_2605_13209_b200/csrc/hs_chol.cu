@@ -797,7 +797,50 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
 // diagonal) goes to W + J*128^2.
 
 constexpr int DCB = 128, DLD = 129, DPB = 32;
-constexpr size_t kDiagSmemBytes = (size_t)(DCB * DLD + (DCB - DPB) * (DPB + 1)) * 8;
+// S [128][129] | T scratch [96][33] | the four 32 x 32 diagonal-block inverses
+// [4][32][33] (mode 0: formed while the other warps update, see below)
+constexpr size_t kDiagSmemBytes =
+    (size_t)(DCB * DLD + (DCB - DPB) * (DPB + 1) + (DCB / DPB) * DPB * (DPB + 1)) * 8;
+
+// W = L^-1 of a 32 x 32 lower-triangular block by one warp, by rows in
+// registers: lane r holds row r of L (a[]) and of W (w[]). Step k: lane k's
+// row is final once scaled by 1 / L_kk and reaches the other lanes through
+// shared memory (ck, double-buffered by step parity); every lane r > k then
+// subtracts L_rk W_k,c -- the column recurrence
+// W_rc = (delta_rc - sum_{c<=k<r} L_rk W_kc) / L_rr in the same k-ascending
+// order, as independent chains across c. L at Lb (leading dimension ldl);
+// the lower triangle of W goes to Wb (leading dimension ldw; may alias Lb).
+__device__ __forceinline__ void diag_block_inverse(const double* Lb, int ldl, double* Wb, int ldw,
+                                                   int lane, double* ck) {
+  constexpr int NB = 32;
+  double a[NB], w[NB];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) {
+    a[c] = c <= lane ? Lb[lane * ldl + c] : 0.0;
+    w[c] = c == lane ? 1.0 : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < NB; ++k) {
+    double* rowk = ck + (k & 1) * NB;
+    if (lane == k) {
+      const double rk = 1.0 / a[k];
+#pragma unroll
+      for (int c = 0; c <= k; ++c) {
+        w[c] *= rk;
+        rowk[c] = w[c];
+      }
+    }
+    __syncwarp();
+    // lanes > k subtract L_rk W_k,c; the others multiply by -0 (exact)
+    const double lrk = lane > k ? a[k] : 0.0;
+#pragma unroll
+    for (int c = 0; c <= k; ++c) w[c] = fma(-lrk, rowk[c], w[c]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < NB; ++c)
+    if (c <= lane) Wb[lane * ldw + c] = w[c];
+}
 
 __global__ void __launch_bounds__(256)
     diag128_kernel(double* A, int64_t tile_lo, const int64_t* lpos, int b, int f,
@@ -810,6 +853,7 @@ __global__ void __launch_bounds__(256)
   double* D = A + slot * (int64_t)b * b + (int64_t)sblk * DCB * b + sblk * DCB;
   extern __shared__ double S[];       // [128][129]
   double* Tm = S + DCB * DLD;         // [96][33] scratch
+  double* Wd = Tm + (DCB - DPB) * (DPB + 1);  // [4][32][33] W_pp = L_pp^-1
   __shared__ double Rv[DPB];          // reciprocal diagonal of the panel
   __shared__ __align__(16) double Ck[2 * DPB];  // warp 0's broadcast column / row
   __shared__ int bad;
@@ -894,8 +938,14 @@ __global__ void __launch_bounds__(256)
         return;
       }
       const int q0 = o + DPB, m = DCB - q0;
+      if (warp == 0) {
+        // W_pp = L_pp^-1 now, beside the other warps' panel solve and
+        // update (the inverse pass below only copies it)
+        diag_block_inverse(S + o * DLD + o, DLD, Wd + p * DPB * (DPB + 1), DPB + 1, lane, Ck);
+      } else {
+      const int t0 = tid - 32, nt = (int)blockDim.x - 32;
       // panel rows below: x L_pp^T = a
-      for (int r = tid; r < m; r += blockDim.x) {
+      for (int r = t0; r < m; r += nt) {
         double* row = S + (q0 + r) * DLD + o;
         double x[DPB];
 #pragma unroll
@@ -910,11 +960,11 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int c = 0; c < DPB; ++c) row[c] = x[c];
       }
-      __syncthreads();
+      named_bar_sync(2, nt);
       HS_PHASE("paneltrsm");
       // trailing rank-32 update of the lower triangle, 4x4 register tiles
       const int mt = m / 4, ntile = mt * (mt + 1) / 2;
-      for (int u = tid; u < ntile; u += blockDim.x) {
+      for (int u = t0; u < ntile; u += nt) {
         const int ti = (int)tile_row(u), tj = u - (int)tri(ti, 0);
         const int r0 = q0 + ti * 4, c0 = q0 + tj * 4;
         double acc[4][4] = {};
@@ -937,6 +987,7 @@ __global__ void __launch_bounds__(256)
           for (int y = 0; y < 4; ++y)
             if (c0 + y <= r0 + x) S[(r0 + x) * DLD + c0 + y] -= acc[x][y];
       }
+      }  // warps 1..7
       __syncthreads();
       HS_PHASE("update");
     }
@@ -985,42 +1036,14 @@ __global__ void __launch_bounds__(256)
     }
     HS_PHASE("inv_T");
     // (2) lane c inverts column c of the 32x32 diagonal block (registers)
-    if (warp == 0) {
-      // W_pp = L_pp^-1 by rows in registers: lane r holds row r of L (a[])
-      // and of W (w[]). Step k: lane k's row is final once scaled by
-      // 1 / L_kk; every lane r > k then subtracts L_rk W_k,c (W_k,c by
-      // shuffle) -- the column-by-column recurrence
-      // W_rc = (delta_rc - sum_{c<=k<r} L_rk W_kc) / L_rr with the same
-      // k-ascending order, as independent chains across c
-      double a[DPB], w[DPB];
-#pragma unroll
-      for (int c = 0; c < DPB; ++c) {
-        a[c] = c <= lane ? S[(o + lane) * DLD + o + c] : 0.0;
-        w[c] = c == lane ? 1.0 : 0.0;
+    if (mode == 0) {
+      // formed during the factorization (Wd)
+      for (int idx = tid; idx < DPB * DPB; idx += blockDim.x) {
+        const int r = idx >> 5, c = idx & 31;
+        if (c <= r) S[(o + r) * DLD + o + c] = Wd[p * DPB * (DPB + 1) + r * (DPB + 1) + c];
       }
-#pragma unroll
-      for (int k = 0; k < DPB; ++k) {
-        // lane k's row is final once scaled; it reaches the other lanes
-        // through shared memory (double-buffered by step parity)
-        double* rowk = Ck + (k & 1) * DPB;
-        if (lane == k) {
-          const double rk = 1.0 / a[k];
-#pragma unroll
-          for (int c = 0; c <= k; ++c) {
-            w[c] *= rk;
-            rowk[c] = w[c];
-          }
-        }
-        __syncwarp();
-        // lanes > k subtract L_rk W_k,c; the others multiply by -0 (exact)
-        const double lrk = lane > k ? a[k] : 0.0;
-#pragma unroll
-        for (int c = 0; c <= k; ++c) w[c] = fma(-lrk, rowk[c], w[c]);
-      }
-      __syncwarp();
-#pragma unroll
-      for (int c = 0; c < DPB; ++c)
-        if (c <= lane) S[(o + lane) * DLD + o + c] = w[c];
+    } else if (warp == 0) {
+      diag_block_inverse(S + o * DLD + o, DLD, S + o * DLD + o, DLD, lane, Ck);
     }
     __syncthreads();
     HS_PHASE("inv_diag");
@@ -1956,6 +1979,17 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
       panel_work(j1 + 1);
     }
   }
+  // HS_CHOL_TIMING=1: per-column event times of the default schedule on
+  // stderr (panel chain on P, column-(j+1) update and rest on U)
+  static const bool col_timing = getenv("HS_CHOL_TIMING") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  auto tmark = [&](cudaStream_t st) {
+    if (!col_timing) return;
+    cudaEvent_t e;
+    HS_CUDA(cudaEventCreate(&e));
+    HS_CUDA(cudaEventRecord(e, st));
+    tev.push_back(e);
+  };
   // DMMA in column pairs (the INT8 path's schedule above): the bulk of the
   // trailing update runs with K = 2b per CTA, halving the per-CTA start-up and
   // epilogue share of each 128^2 item (HS_CHOL_PAIRS=0: one column at a time)
@@ -1982,6 +2016,7 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
       // both of this pair's panels)
       cudaEvent_t p0 = cs.make();
       HS_CUDA(cudaEventRecord(p0, cs.p));
+      tmark(cs.p);
       HS_CUDA(cudaStreamWaitEvent(cs.u, p0));
       GemmArgs gu = g;
       gu.j = j0;
@@ -1989,8 +2024,10 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
       launch_gemm(c, cs.u, gu, (N - 1 - j0) * f * f, &mapA, &mapA);
       cudaEvent_t ucol = cs.make();
       HS_CUDA(cudaEventRecord(ucol, cs.u));
+      tmark(cs.u);
       HS_CUDA(cudaStreamWaitEvent(cs.p, ucol));
       panel_work(j1);
+      tmark(cs.p);
       if (j1 + 1 >= N) break;
       // columns > j1 by the pair (K = 2b): j1+1 first (the next panel needs
       // it), j1+2, then the bulk on U2 beside the next pair's panels
@@ -2006,6 +2043,7 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
       launch_gemm(c, cs.u, gp, (N - 1 - j1) * f * f, &mapA, &mapA);
       cudaEvent_t ua = cs.make();
       HS_CUDA(cudaEventRecord(ua, cs.u));
+      tmark(cs.u);
       rest_done = nullptr;
       if (j1 + 2 < N) {
         gp.step = (int)(j1 + 2);
@@ -2023,8 +2061,25 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
           HS_CUDA(cudaEventRecord(rest_done, cs.u2));
         }
       }
+      tmark(cs.u2);
       HS_CUDA(cudaStreamWaitEvent(cs.p, ua));
       panel_work(j1 + 1);
+      tmark(cs.p);
+    }
+    if (col_timing && !tev.empty()) {
+      HS_CUDA(cudaDeviceSynchronize());
+      auto ms = [&](size_t k) {
+        float v = 0.f;
+        cudaEventElapsedTime(&v, tev[0], tev[k]);
+        return v;
+      };
+      fprintf(stderr, "chol pairs: j0 panel_j0_end ucol_end panel_j1_end ua_end bulk_end "
+                      "panel_j1+1_end (ms)\n");
+      for (size_t k = 0, j = 0; k + 6 <= tev.size(); k += 6, j += 2)
+        fprintf(stderr, "pair %3zu %9.3f %9.3f %9.3f %9.3f %9.3f %9.3f\n", j, ms(k), ms(k + 1),
+                ms(k + 2), ms(k + 3), ms(k + 4), ms(k + 5));
+      for (cudaEvent_t e : tev) cudaEventDestroy(e);
+      tev.clear();
     }
     // an odd trailing column: its panel j0 = N - 1 is the last one
   }
@@ -2069,19 +2124,8 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
       panel_work(j + 1);
     }
   }
-  // HS_CHOL_TIMING=1: per-column event times of the default schedule on
-  // stderr (panel chain on P, column-(j+1) update and rest on U)
-  static const bool col_timing = getenv("HS_CHOL_TIMING") != nullptr;
-  std::vector<cudaEvent_t> tev;
-  auto tmark = [&](cudaStream_t st) {
-    if (!col_timing) return;
-    cudaEvent_t e;
-    HS_CUDA(cudaEventCreate(&e));
-    HS_CUDA(cudaEventRecord(e, st));
-    tev.push_back(e);
-  };
   cudaStream_t su = cs.u;
-  tmark(cs.p);
+  if (!pairs) tmark(cs.p);
   for (int64_t j = 0; j < N && !use_oz && !pairs && sched != 1; ++j) {
     const int64_t t = N - 1 - j;
     cudaEvent_t pdone = cs.make();
