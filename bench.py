@@ -206,7 +206,7 @@ def run_reference_arm(args) -> None:
         "e2e": {"value": cb["value"], "unit": "iters/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit_json(line)
 
 
 # ---------------------------------------------------------------------------
@@ -599,7 +599,7 @@ def run_ours(args) -> None:
     if use_dist:
         dist.destroy_process_group()
     if rank == 0:  # last, after the communicators' teardown logging
-        print(json.dumps(line), flush=True)
+        emit_json(line)
 
 
 def cg_anchor(hs, rt, torch, args, n: int = 131072, b: int = 128, iters: int = 20) -> dict:
@@ -644,10 +644,29 @@ def spawn_ranks(args) -> int:
            "--master-port", str(29500 + os.getpid() % 1000), os.path.abspath(__file__),
            *sys.argv[1:]]
     log("+ " + " ".join(cmd))
-    return subprocess.call(cmd)
+    # the ranks' fd 1 is the original stdout (this process points its own fd
+    # 1 at stderr; see emit_json)
+    return subprocess.call(cmd, stdout=_JSON_OUT if _JSON_OUT is not None else None)
+
+
+# stdout carries only the JSON line: native libraries (NCCL prints its version
+# line and, with NCCL_DEBUG=INFO, its INIT lines to stdout) write to fd 1,
+# which main() points at stderr; the JSON goes to a saved copy of the
+# original stdout
+_JSON_OUT = None
+
+
+def emit_json(line):
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 
 def main():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1000)
