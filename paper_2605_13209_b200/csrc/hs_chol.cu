@@ -1665,23 +1665,26 @@ static void launch_gemm(hs_ctx* c, cudaStream_t s, const GemmArgs& g,
                         const TileMaps* mb) {
   if (items <= 0) return;
   if (g.cb == 128 && ma && mb) {
-    // launches of at most one wave of 128^2 items run as 64^2 quadrants:
-    // 4x the CTAs, each a quarter of the work (HS_GEMM64=0: always 128)
-    static const bool q64 = [] {
+    // CTA tiles: 64 x 64 quadrants of the 128^2 items (two CTAs per SM, so one
+    // CTA's start-up and epilogue overlap the other's DMMA work, and the
+    // panel chain's small launches find SMs sooner than behind 128^2 CTAs),
+    // 64 x 128 row halves for the in-place TRSM steps; HS_GEMM64=0: 128 x 128
+    // throughout, HS_GEMM64=2: split tiles only for launches of at most one
+    // wave (and in-place always within that rule)
+    static const int q64 = [] {
       const char* e = getenv("HS_GEMM64");
-      return !(e && atoi(e) == 0);
+      return e ? atoi(e) : 1;
     }();
     const int sms = std::max(1, c->num_sms);
-    // in-place steps (C = A W^T, C and A the same sub-block) split by rows
-    // only, so no CTA reads columns another CTA writes
     const bool in_place = g.mode == G_PANEL_TRSM || g.mode == G_DIAG_TRSM ||
                           g.mode == G_DIST_PANEL_TRSM;
-    if (q64 && items <= sms && in_place) {
+    const bool split = q64 == 1 || (q64 == 2 && items <= sms);
+    if (split && in_place) {
       using C = GemmCfg<64, 128>;
       static std::atomic<uint64_t> attr64{0};
       HS_CUDA(smem_attr_once(gemm_dmma_kernel<64, 128>, C::SMEM, attr64));
       gemm_dmma_kernel<64, 128><<<(unsigned)(items * 2), 288, C::SMEM, s>>>(ma->m64, mb->m128, g);
-    } else if (q64 && items <= sms) {
+    } else if (split) {
       using C = GemmCfg<64, 64>;
       static std::atomic<uint64_t> attr64{0};
       HS_CUDA(smem_attr_once(gemm_dmma_kernel<64, 64>, C::SMEM, attr64));
