@@ -518,12 +518,13 @@ constexpr int GKS = 32, GSTAGES = 3;
 // one SM): 64 x 64 quadrants for C -= A B^T, 64 x 128 row halves for the
 // in-place TRSM steps (C = A W^T with C = A: a CTA must read only the rows
 // it writes)
-template <int BM, int BN>
+template <int BM, int BN, int NST = GSTAGES>
 struct GemmCfg {
+  static constexpr int STAGES = NST;
   static constexpr int A_BYTES = BM * GKS * 8;
   static constexpr int B_BYTES = BN * GKS * 8;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM = GSTAGES * STAGE_BYTES + 1024 + 64;
+  static constexpr int SMEM = NST * STAGE_BYTES + 1024 + 64;
   static constexpr int WM = BM / 32;      // warps along m (32 rows each)
   static constexpr int WN = 8 / WM;       // warps along n
   static constexpr int Y = BN / (WN * 8); // 8-column fragments per warp
@@ -552,11 +553,12 @@ __device__ __forceinline__ uint32_t swz(int row, int k) {
   return (uint32_t)(row * 128 + ((((k >> 1) ^ (row & 7))) << 4) + ((k & 1) << 3));
 }
 
-template <int BM, int BN>
+template <int BM, int BN, int NST = GSTAGES>
 __global__ void __launch_bounds__(288, 1)
     gemm_dmma_kernel(const __grid_constant__ CUtensorMap mapA,
                      const __grid_constant__ CUtensorMap mapB, GemmArgs g) {
-  using Cfg = GemmCfg<BM, BN>;
+  using Cfg = GemmCfg<BM, BN, NST>;
+  constexpr int GSTAGES = NST;  // (shadows the default)
   constexpr int A_BYTES = Cfg::A_BYTES, B_BYTES = Cfg::B_BYTES;
   constexpr int G_STAGE_BYTES = Cfg::STAGE_BYTES;
   constexpr int GBM = BM, Y = Cfg::Y;
