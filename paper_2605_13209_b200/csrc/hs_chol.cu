@@ -1684,7 +1684,14 @@ static void launch_gemm(hs_ctx* c, cudaStream_t s, const GemmArgs& g,
     // chain runs here, beside the Ozaki GEMM: split tiles for small launches
     // only, 184 vs 187 ms at n = 32768)
     const int pol = (q64 == 1 && c->chol_slices > 0) ? 2 : q64;
-    const bool split = pol == 1 || (pol == 2 && items <= sms);
+    // The distributed trailing update (panel tiles from the broadcast
+    // buffer, NCCL copies on the panel stream) gave wrong factors with
+    // 64 x 64 CTAs in launches of more than one wave -- at world 1 with a
+    // 1 x 1 grid, where its work equals the single-GPU path's (which is
+    // exact and deterministic with them); cause not identified: it keeps
+    // 128 x 128 CTAs there (tools/gpu/chol_dist_det.py)
+    const bool big_ok = pol == 1 && g.mode != G_DIST_UPDATE;
+    const bool split = pol != 0 && (items <= sms || big_ok);
     if (split && in_place) {
       using C = GemmCfg<64, 128>;
       static std::atomic<uint64_t> attr64{0};
