@@ -1688,8 +1688,9 @@ static void launch_gemm(hs_ctx* c, cudaStream_t s, const GemmArgs& g,
     // buffer, NCCL copies on the panel stream) gave wrong factors with
     // 64 x 64 CTAs in launches of more than one wave -- at world 1 with a
     // 1 x 1 grid, where its work equals the single-GPU path's (which is
-    // exact and deterministic with them); cause not identified: it keeps
-    // 128 x 128 CTAs there (tools/gpu/chol_dist_det.py)
+    // exact and deterministic with them), and only with the panel and
+    // update streams concurrent (one stream: exact); cause not identified:
+    // it keeps 128 x 128 CTAs there (tools/gpu/chol_dist_det.py)
     const bool big_ok = pol == 1 && g.mode != G_DIST_UPDATE;
     const bool split = pol != 0 && (items <= sms || big_ok);
     if (split && in_place) {
@@ -2294,6 +2295,7 @@ static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
   HS_CUDA(cudaEventRecord(start, c->stream));
   HS_CUDA(cudaStreamWaitEvent(cs.p, start));
   HS_CUDA(cudaStreamWaitEvent(cs.u, start));
+  cudaStream_t cs_u = cs.u;
 
   const TileMaps mapA = tile_map(m->d, b, std::max<int64_t>((int64_t)m->local_tiles(), 1));
   const TileMaps mapW = tile_map(m->dinv, cb, N * f);
@@ -2383,27 +2385,27 @@ static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
     cudaEvent_t pdone = cs.make();
     HS_CUDA(cudaEventRecord(pdone, cs.p));
     if (j + 1 >= N) break;
-    HS_CUDA(cudaStreamWaitEvent(cs.u, pdone));
+    HS_CUDA(cudaStreamWaitEvent(cs_u, pdone));
     GemmArgs gu = g;
     gu.j = j;
     gu.mode = G_DIST_UPDATE;
     gu.X = PB[j & 1];
     gu.list = d_pairs + 2 * col_off[j];
     if (use_oz)
-      oz.update_list(c, cs.u, m->d, m->d_lpos, j, gu.list, rest_off[j] - col_off[j],
+      oz.update_list(c, cs_u, m->d, m->d_lpos, j, gu.list, rest_off[j] - col_off[j],
                      &flag->status);
     else
-      launch_gemm(c, cs.u, gu, (rest_off[j] - col_off[j]) * f * f, &mapPB[j & 1],
+      launch_gemm(c, cs_u, gu, (rest_off[j] - col_off[j]) * f * f, &mapPB[j & 1],
                   &mapPB[j & 1]);
     cudaEvent_t ucol = cs.make();
-    HS_CUDA(cudaEventRecord(ucol, cs.u));
+    HS_CUDA(cudaEventRecord(ucol, cs_u));
     HS_CUDA(cudaStreamWaitEvent(cs.p, ucol));
     gu.list = d_pairs + 2 * rest_off[j];
     if (use_oz)
-      oz.update_list(c, cs.u, m->d, m->d_lpos, j, gu.list, col_off[j + 1] - rest_off[j],
+      oz.update_list(c, cs_u, m->d, m->d_lpos, j, gu.list, col_off[j + 1] - rest_off[j],
                      &flag->status);
     else
-      launch_gemm(c, cs.u, gu, (col_off[j + 1] - rest_off[j]) * f * f, &mapPB[j & 1],
+      launch_gemm(c, cs_u, gu, (col_off[j + 1] - rest_off[j]) * f * f, &mapPB[j & 1],
                   &mapPB[j & 1]);
     panel_work(j + 1);
   }
