@@ -664,3 +664,43 @@ print("TAIL OK")
     p = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                        text=True, timeout=600)
     assert p.returncode == 0 and "TAIL OK" in p.stdout, p.stdout + p.stderr
+
+
+def test_split_tile_gemm_factor_bitwise_equals_128x128():
+    """The default DMMA GEMM tiles (64x64 quadrants for C -= A B^T, 64x128 row
+    halves for the in-place TRSM steps) give the same factor as 128x128 CTAs
+    bit for bit -- every element sees the same K order and C - acc either way
+    -- run after run (HS_GEMM64 is read once per process: subprocesses)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, os, numpy as np
+sys.path.insert(0, ".")
+import paper_2605_13209_b200 as hs
+from paper_2605_13209_b200 import hsolve as H
+rt = hs.Runtime()
+out = []
+for n, b in [(8192, 512), (4096, 256)]:
+    m = hs.generate_spd_device(rt, n, b, seed=7)
+    H.potrf_device(rt, m)
+    L = m.download()
+    N = n // b
+    for i in range(N):
+        t = i * (i + 1) // 2 + i
+        T = L[t * b * b:(t + 1) * b * b].reshape(b, b)
+        T[np.triu_indices(b, 1)] = 0.0  # the stale upper half is not part of L
+    out.append(L)
+np.save(sys.argv[1], np.concatenate(out))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for i, v in enumerate(["0", "1", "1"]):
+        path = os.path.join("/tmp", f"hs_tiles_{os.getpid()}_{i}.npy")
+        p = subprocess.run([sys.executable, "-c", code, path], cwd=root,
+                           env=dict(os.environ, HS_GEMM64=v), capture_output=True,
+                           text=True, timeout=600)
+        assert p.returncode == 0, p.stdout + p.stderr
+        res.append(np.load(path))
+        os.remove(path)
+    assert np.array_equal(res[0], res[1]) and np.array_equal(res[0], res[2])
