@@ -109,8 +109,11 @@ __device__ void scalar_step(int step, double val, const StepArgs& sa) {
 // ---------------------------------------------------------------------------
 // Fast SYMV for b in {64, 128, 256, 512}
 
-template <int B, int NCW_ = 8, bool PROG_ = false>
+template <int B, int NCW_ = 8, bool PROG_ = false, bool TWO_ = false>
 struct SymvCfg {
+  // TWO_: two input vectors in one pass over A (t = A s and t2 = A s2; the
+  // CG recompute iteration), progressive mode, b <= 128 only
+  static constexpr bool TWO = TWO_;
   static constexpr int NCW = NCW_;               // consumer warps
   static constexpr int CT = NCW * 32;            // consumer threads
   // progressive mode: + FW finalize warps (see symv_finalize_rows)
@@ -129,14 +132,16 @@ struct SymvCfg {
   static constexpr int G = TPR <= 32 ? NCW : RPP;
   // 8 consumer warps (16 measured slower: more smem traffic per slab)
   // (6 stages at b <= 128 measured no faster)
-  static constexpr int NSTAGE = B == 512 ? 4 : 5;
+  static constexpr int NSTAGE = (B == 512 || TWO_) ? 4 : 5;
   // slab | seg_j (B) | seg_i (RS)
-  static constexpr int SEG_BYTES = (B + RS) * 8;
+  // (TWO_: a second copy of both segments, staged with every slab)
+  static constexpr int SEG_BYTES = (B + RS) * 8 * (TWO_ ? 2 : 1);
   static constexpr int STAGE_BYTES = SLAB_BYTES + SEG_BYTES;
   static constexpr int COLRED_BYTES = G * B * 8;
   static constexpr int YROW_BYTES = H * B * 8;
   // + full/empty mbarriers + per-stage (slab, unit) headers
-  static constexpr int SMEM = NSTAGE * STAGE_BYTES + 2 * COLRED_BYTES +
+  static constexpr int SMEM = NSTAGE * STAGE_BYTES + (TWO_ ? 2 : 1) * 2 * COLRED_BYTES +
+                              (TWO_ ? 2 * YROW_BYTES : 0) +
                               2 * YROW_BYTES + 2 * NSTAGE * 8 + NSTAGE * 28;
   static_assert(RT >= 1 && RT <= 2 && RS == RT * RPP, "row mapping");
   static_assert(STAGE_BYTES % 16 == 0, "bulk copy alignment");
@@ -179,6 +184,11 @@ struct SymvArgs {
   const double* dot_s;      // fused dot s . t (or null)
   double* apart;            // [row_hi] per-block-row s . t partials
   int defer;                // 1: leave the partials to the next kernel
+  // two-vector mode: the second input, its output and partial slots
+  const double* s2;
+  double* out2;
+  double* rowpart2;
+  double* colmain2;
   StepArgs sa;              // otherwise: ticket -> combine -> scalar step / slots
 };
 
@@ -202,7 +212,7 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
 // columns. s . t is formed per block row (apart[j]); without `defer` the
 // last block row to finish (ticket) combines them as a fixed-shape
 // double-double tree and applies the scalar step.
-template <int B, int FW>
+template <int B, int FW, bool TWO = false>
 __device__ void symv_finalize_rows(const SymvArgs& args, int fw, int lane) {
   constexpr int CPL = B / (32 * FW);  // columns per lane (1 or 2)
   static_assert(CPL == 1 || CPL == 2, "finalize column mapping");
@@ -210,11 +220,13 @@ __device__ void symv_finalize_rows(const SymvArgs& args, int fw, int lane) {
   __shared__ int fin_last;
   const int col = fw * (B / FW) + lane * CPL;
   const double* colbase = args.colmain - args.tile_lo * B + col;
+  // two-vector mode: the second vector's slots, same positions
+  const double* colbase2 = TWO ? args.colmain2 - args.tile_lo * B + col : nullptr;
   const int64_t rows = args.row_hi;
   int64_t j = blockIdx.x + ((rows - 1 - blockIdx.x) / gridDim.x) * (int64_t)gridDim.x;
   if (blockIdx.x >= rows) j = -1;
   for (; j >= 0; j -= gridDim.x) {
-    double a0 = 0.0, a1 = 0.0;
+    double a0 = 0.0, a1 = 0.0, e0 = 0.0, e1 = 0.0;
     int64_t k = rows - 1;
     const int64_t kend = j > args.row_lo ? j : args.row_lo;
     uint64_t t0 = 0;
@@ -237,7 +249,23 @@ __device__ void symv_finalize_rows(const SymvArgs& args, int fw, int lane) {
       t0 = 0;
       __threadfence();  // acquire: the partials were stored before the arrivals
       int m = 0;
-      if constexpr (CPL == 2) {
+      if constexpr (TWO) {
+        // (b = 128 and 64, both vectors; fewer loads in flight per batch)
+        for (; m < ready; ++m) {
+          const int64_t off = tri(k - m, j) * B;
+          if constexpr (CPL == 2) {
+            const double2 v = __ldcg(reinterpret_cast<const double2*>(colbase + off));
+            const double2 w = __ldcg(reinterpret_cast<const double2*>(colbase2 + off));
+            a0 += v.x;
+            a1 += v.y;
+            e0 += w.x;
+            e1 += w.y;
+          } else {
+            a0 += __ldcg(colbase + off);
+            e0 += __ldcg(colbase2 + off);
+          }
+        }
+      } else if constexpr (CPL == 2) {
         for (; m + 16 <= ready; m += 16) {
           double2 v[16];
 #pragma unroll
@@ -272,11 +300,20 @@ __device__ void symv_finalize_rows(const SymvArgs& args, int fw, int lane) {
         const double* rp = args.rowpart + (int64_t)(s0 + e) * B + col;
         a0 += __ldcg(rp);
         if (CPL == 2) a1 += __ldcg(rp + 1);
+        if constexpr (TWO) {
+          const double* rp2 = args.rowpart2 + (int64_t)(s0 + e) * B + col;
+          e0 += __ldcg(rp2);
+          if (CPL == 2) e1 += __ldcg(rp2 + 1);
+        }
       }
     }
     const int64_t o = args.row_off[j] + col;
     args.out[o] = a0;
     if (CPL == 2) args.out[o + 1] = a1;
+    if constexpr (TWO) {
+      args.out2[o] = e0;
+      if (CPL == 2) args.out2[o + 1] = e1;
+    }
     if (args.dot_s) {
       double d = args.dot_s[o] * a0;
       if (CPL == 2) d = fma(args.dot_s[o + 1], a1, d);
@@ -343,10 +380,11 @@ __device__ int g_symv_ts_print = 0;
 __device__ unsigned long long g_symv_fin_end[4096];
 #endif
 
-template <int B, int NCW, bool PROG>
-__global__ void __launch_bounds__(SymvCfg<B, NCW, PROG>::THREADS, 1)
+template <int B, int NCW, bool PROG, bool TWO = false>
+__global__ void __launch_bounds__(SymvCfg<B, NCW, PROG, TWO>::THREADS, 1)
     symv_slab_kernel(SymvArgs args) {
-  using Cfg = SymvCfg<B, NCW, PROG>;
+  using Cfg = SymvCfg<B, NCW, PROG, TWO>;
+  static_assert(!TWO || (PROG && Cfg::SPT <= 4), "two-vector mode: progressive, b <= 128");
   constexpr int RS = Cfg::RS, SPT = Cfg::SPT, TPR = Cfg::TPR, RT = Cfg::RT;
   constexpr int W = Cfg::W, NS = Cfg::NSTAGE, CT = Cfg::CT, G = Cfg::G;
 
@@ -354,7 +392,10 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW, PROG>::THREADS, 1)
   unsigned char* stages = smem;
   double* colred = reinterpret_cast<double*>(smem + NS * Cfg::STAGE_BYTES);
   double* yrow = colred + 2 * G * B;  // [2][H][B]
-  uint64_t* full = reinterpret_cast<uint64_t*>(yrow + 2 * Cfg::H * B);
+  // two-vector mode: the second vector's column / row reduction buffers
+  double* colred2 = yrow + 2 * Cfg::H * B;
+  double* yrow2 = colred2 + (TWO ? 2 * G * B : 0);
+  uint64_t* full = reinterpret_cast<uint64_t*>(yrow2 + (TWO ? 2 * Cfg::H * B : 0));
   uint64_t* empty = full + NS;
   // per-stage header: the slab staged and its work unit (-1: no more work);
   // progressive mode also (block row, column, row end, row segment) of the
@@ -380,6 +421,8 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW, PROG>::THREADS, 1)
     fence_mbar_init();
   }
   for (int k = tid; k < 2 * Cfg::H * B; k += blockDim.x) yrow[k] = 0.0;
+  if constexpr (TWO)
+    for (int k = tid; k < 2 * Cfg::H * B; k += blockDim.x) yrow2[k] = 0.0;
   __syncthreads();
   // the CTA-private setup above overlaps the previous kernel's tail (PDL);
   // everything below reads its results
@@ -402,7 +445,7 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW, PROG>::THREADS, 1)
 
   if constexpr (PROG) {
     if (tid >= CT + 32) {
-      symv_finalize_rows<B, Cfg::FW>(args, (tid - CT - 32) >> 5, tid & 31);
+      symv_finalize_rows<B, Cfg::FW, TWO>(args, (tid - CT - 32) >> 5, tid & 31);
 #ifdef HS_SYMV_TIMING
       if (tid == CT + 32) {
         uint64_t te;
@@ -468,12 +511,24 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW, PROG>::THREADS, 1)
               hdr_u[st] = u;
               hdr_x[st] = make_int4((int)k, (int)j, rend, seg);
               unsigned char* buf = stages + st * Cfg::STAGE_BYTES;
-              mbar_arrive_expect_tx(&full[st],
-                                    Cfg::SLAB_BYTES + RS * 8 + (q == 0 ? B * 8 : 0));
+              if constexpr (TWO) {
+                // both vectors' segments with every slab: slab | s_j | s_i |
+                // s2_j | s2_i (the consumers reload s_j per slab)
+                mbar_arrive_expect_tx(&full[st], Cfg::SLAB_BYTES + 2 * (B + RS) * 8);
+              } else {
+                mbar_arrive_expect_tx(&full[st],
+                                      Cfg::SLAB_BYTES + RS * 8 + (q == 0 ? B * 8 : 0));
+              }
               bulk_g2s_hint(buf, args.a + ((t - args.tile_lo) * B + (int64_t)q * RS) * B,
                             Cfg::SLAB_BYTES, &full[st], stream_pol);
               bulk_g2s(buf + Cfg::SLAB_BYTES + B * 8, args.s + ok + q * RS, RS * 8, &full[st]);
-              if (q == 0) bulk_g2s(buf + Cfg::SLAB_BYTES, args.s + args.row_off[j], B * 8, &full[st]);
+              if (TWO || q == 0)
+                bulk_g2s(buf + Cfg::SLAB_BYTES, args.s + args.row_off[j], B * 8, &full[st]);
+              if constexpr (TWO) {
+                unsigned char* b2 = buf + Cfg::SLAB_BYTES + (B + RS) * 8;
+                bulk_g2s(b2, args.s2 + args.row_off[j], B * 8, &full[st]);
+                bulk_g2s(b2 + B * 8, args.s2 + ok + q * RS, RS * 8, &full[st]);
+              }
               if (++st == NS) {
                 st = 0;
                 ph ^= 1u;
@@ -557,12 +612,15 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW, PROG>::THREADS, 1)
     // matter here: a sustained CG loop runs under the board's power cap.
     static_assert(RT == 2 && Cfg::H == 1 && TPR <= 32, "tiled layout");
     double ra[SPT][RT], rb[SPT][RT], cac[8];
+    // two-vector mode: the second vector's row sums (one FMA chain) and
+    // column sums
+    double r2[SPT][RT], cac2[8];
 #pragma unroll
     for (int qq = 0; qq < SPT; ++qq)
 #pragma unroll
-      for (int r = 0; r < RT; ++r) ra[qq][r] = rb[qq][r] = 0.0;
+      for (int r = 0; r < RT; ++r) ra[qq][r] = rb[qq][r] = r2[qq][r] = 0.0;
 #pragma unroll
-    for (int m = 0; m < 8; ++m) cac[m] = 0.0;
+    for (int m = 0; m < 8; ++m) cac[m] = cac2[m] = 0.0;
     double2 sjt[4];
     int cur = -1;
     int64_t ug1 = 0, ti = 0, ii = 0, jj = 0, ifirst = 0, rsg0 = 0;
@@ -599,7 +657,7 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW, PROG>::THREADS, 1)
 #ifdef HS_SYMV_TIMING
       ts_slabs += SPT;
 #endif
-      {
+      if constexpr (!TWO) {
         const double2* sj2 =
             reinterpret_cast<const double2*>(stages + st0 * Cfg::STAGE_BYTES + Cfg::SLAB_BYTES);
 #pragma unroll
@@ -619,7 +677,39 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW, PROG>::THREADS, 1)
         for (int r = 0; r < RT; ++r)
 #pragma unroll
           for (int m = 0; m < 4; ++m) a[r][m] = A2[(RT * rl + r) * (B / 2) + cl + TPR * m];
-        if (!diag) {
+        if constexpr (TWO) {
+          // both s_j segments come with every slab; the second vector's
+          // row and column sums use the same A values
+          const double2* sjs = reinterpret_cast<const double2*>(buf + Cfg::SLAB_BYTES);
+          const unsigned char* b2 = buf + Cfg::SLAB_BYTES + (B + RS) * 8;
+          const double2* sjs2 = reinterpret_cast<const double2*>(b2);
+          const double2 si22 = reinterpret_cast<const double2*>(b2 + B * 8)[rl];
+          const double sir2[2] = {si22.x, si22.y};
+#pragma unroll
+          for (int m = 0; m < 4; ++m) sjt[m] = sjs[cl + TPR * m];
+#pragma unroll
+          for (int r = 0; r < RT; ++r) {
+            const int rr = q * RS + RT * rl + r;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+              const double2 sj2 = sjs2[cl + TPR * m];
+              const int c0 = 2 * cl + 2 * TPR * m;
+              const double ax = a[r][m].x, ay = a[r][m].y;
+              // (the diagonal tile: lower triangle only, as below)
+              const double rx = !diag || c0 <= rr ? ax : 0.0;
+              const double ry = !diag || c0 + 1 <= rr ? ay : 0.0;
+              const double cx = !diag || c0 < rr ? ax : 0.0;
+              const double cy = !diag || c0 + 1 < rr ? ay : 0.0;
+              ra[q][r] = fma(rx, sjt[m].x, ra[q][r]);
+              rb[q][r] = fma(ry, sjt[m].y, rb[q][r]);
+              cac[2 * m] = fma(cx, sir[r], cac[2 * m]);
+              cac[2 * m + 1] = fma(cy, sir[r], cac[2 * m + 1]);
+              r2[q][r] = fma(ry, sj2.y, fma(rx, sj2.x, r2[q][r]));
+              cac2[2 * m] = fma(cx, sir2[r], cac2[2 * m]);
+              cac2[2 * m + 1] = fma(cy, sir2[r], cac2[2 * m + 1]);
+            }
+          }
+        } else if (!diag) {
 #pragma unroll
           for (int r = 0; r < RT; ++r)
 #pragma unroll
@@ -664,6 +754,14 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW, PROG>::THREADS, 1)
               v += __shfl_xor_sync(0xffffffffu, v, off);
             if ((cl & (W - 1)) == 0) yrow[rp * B + qq * RS + RT * rl + r] = v;
             ra[qq][r] = rb[qq][r] = 0.0;
+            if constexpr (TWO) {
+              double v2 = r2[qq][r];
+#pragma unroll
+              for (int off = W / 2; off >= 1; off >>= 1)
+                v2 += __shfl_xor_sync(0xffffffffu, v2, off);
+              if ((cl & (W - 1)) == 0) yrow2[rp * B + qq * RS + RT * rl + r] = v2;
+              r2[qq][r] = 0.0;
+            }
           }
       }
 #pragma unroll
@@ -676,6 +774,19 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW, PROG>::THREADS, 1)
         for (int m = 0; m < 4; ++m)
           reinterpret_cast<double2*>(cr + grp * B)[cl + TPR * m] =
               make_double2(cac[2 * m], cac[2 * m + 1]);
+      }
+      double* cr2 = colred2 + tp * G * B;
+      if constexpr (TWO) {
+#pragma unroll
+        for (int off = TPR; off < 32; off <<= 1)
+#pragma unroll
+          for (int m = 0; m < 8; ++m) cac2[m] += __shfl_xor_sync(0xffffffffu, cac2[m], off);
+        if (lane < TPR) {
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+            reinterpret_cast<double2*>(cr2 + grp * B)[cl + TPR * m] =
+                make_double2(cac2[2 * m], cac2[2 * m + 1]);
+        }
       }
       if constexpr (PROG) {
         if (pend_row >= 0 && tid < B) __threadfence();
@@ -697,11 +808,25 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW, PROG>::THREADS, 1)
           for (int r = 0; r < G; ++r) acc += cr[r * B + c];
           st_hint(dst + c, acc, keep_pol);
         }
+        if constexpr (TWO) {
+          double* dst2 = args.colmain2 + (ti - args.tile_lo) * B;
+          for (int c = tid; c < B; c += CT) {
+            double acc = 0.0;
+#pragma unroll 4
+            for (int r = 0; r < G; ++r) acc += cr2[r * B + c];
+            st_hint(dst2 + c, acc, keep_pol);
+          }
+        }
       }
       if (row_end) {
         double* yr = yrow + rp * B;
         double* out = args.rowpart + (PROG ? prog_seg : rsg0 + (ii - ifirst)) * B;
         for (int c = tid; c < B; c += CT) st_hint(out + c, yr[c], keep_pol);
+        if constexpr (TWO) {
+          double* yr2 = yrow2 + rp * B;
+          double* o2 = args.rowpart2 + prog_seg * B;
+          for (int c = tid; c < B; c += CT) st_hint(o2 + c, yr2[c], keep_pol);
+        }
         rp ^= 1;
         // the segment (its column partials and row partial) is announced
         // at the next tile end, or below when the work runs out
@@ -709,7 +834,7 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW, PROG>::THREADS, 1)
       }
       tp ^= 1;
 #pragma unroll
-      for (int m = 0; m < 8; ++m) cac[m] = 0.0;
+      for (int m = 0; m < 8; ++m) cac[m] = cac2[m] = 0.0;
       ++ti;
       if (++jj > ii) {
         ++ii;
@@ -1169,6 +1294,7 @@ struct VecArgs {
   // (reduced here by every CTA in the finalize's fixed order)
   const double* apart = nullptr;
   int acount = 0;
+  const double* t2 = nullptr;  // V_RECOMP: A x_old
 };
 
 enum VecMode : int {
@@ -1179,6 +1305,9 @@ enum VecMode : int {
   V_SDIR = 4,       // s = r + beta s
   V_DOT_ST = 5,     // dot(s, t) -> ALPHA (after the generic SYMV)
   V_RESNORM = 6,    // dot(rhs - t, rhs - t) -> NONE (true residual)
+  // recompute iteration from one two-vector pass (t = A s, t2 = A x_old):
+  // x += a s, r = rhs - (t2 + a t) = rhs - A x_new, dot(r, r) -> BETA
+  V_RECOMP = 7,
 };
 
 __global__ void __launch_bounds__(VBLOCK) vec_kernel(VecArgs va) {
@@ -1238,11 +1367,18 @@ __global__ void __launch_bounds__(VBLOCK) vec_kernel(VecArgs va) {
         part = fma(rr, rr, part);
         break;
       }
+      case V_RECOMP: {
+        va.x[k] = fma(alpha, va.s[k], va.x[k]);
+        const double rr = va.rhs[k] - fma(alpha, va.t[k], va.t2[k]);
+        va.r[k] = rr;
+        part = fma(rr, rr, part);
+        break;
+      }
     }
   }
   int step = STEP_NONE;
   if (va.mode == V_INIT) step = STEP_INIT;
-  else if (va.mode == V_UPDATE || va.mode == V_RESIDUAL) step = STEP_BETA;
+  else if (va.mode == V_UPDATE || va.mode == V_RESIDUAL || va.mode == V_RECOMP) step = STEP_BETA;
   else if (va.mode == V_DOT_ST) step = STEP_ALPHA;
   else if (va.mode == V_RESNORM) step = STEP_NONE;
   else return;
@@ -1507,7 +1643,8 @@ void free_plan(SymvPlan* p) {
                   (void*)p->item, (void*)p->item_aux, (void*)p->row_item,
                   (void*)p->itempart, (void*)p->tail_dot, (void*)p->tail_rr,
                   (void*)p->tail_bar, (void*)p->unit_pos, (void*)p->row_seg0,
-                  (void*)p->row_nseg, (void*)p->rowdone, (void*)p->pf})
+                  (void*)p->row_nseg, (void*)p->rowdone, (void*)p->pf,
+                  (void*)p->rowpart2, (void*)p->colmain2})
     cudaFree(q);
   delete p;
 }
@@ -1724,14 +1861,17 @@ struct ProgOut {
   double* apart = nullptr;
   bool defer = false;
   StepArgs sa{};
+  // two-vector mode: out2 = A s2 in the same pass
+  const double* s2 = nullptr;
+  double* out2 = nullptr;
 };
 
-template <int B, int NCW, bool PROG>
+template <int B, int NCW, bool PROG, bool TWO = false>
 static void launch_symv_fast(hs_ctx* c, const hs_matrix* m, const double* s,
                              const int32_t* done, const ProgOut* po = nullptr) {
-  using Cfg = SymvCfg<B, NCW, PROG>;
+  using Cfg = SymvCfg<B, NCW, PROG, TWO>;
   static std::atomic<uint64_t> attr{0};
-  HS_CUDA(smem_attr_once(symv_slab_kernel<B, NCW, PROG>, Cfg::SMEM, attr));
+  HS_CUDA(smem_attr_once(symv_slab_kernel<B, NCW, PROG, TWO>, Cfg::SMEM, attr));
   SymvPlan* p = m->plan;
   SymvArgs a{};
   a.a = m->d;
@@ -1775,7 +1915,13 @@ static void launch_symv_fast(hs_ctx* c, const hs_matrix* m, const double* s,
   static unsigned seq = 0;
   a.ts_seq = seq++;
 #endif
-  HS_CUDA(launch_pdl(symv_slab_kernel<B, NCW, PROG>, dim3(p->grid), dim3(Cfg::THREADS),
+  if constexpr (TWO) {
+    a.s2 = po->s2;
+    a.out2 = po->out2;
+    a.rowpart2 = p->rowpart2;
+    a.colmain2 = p->colmain2;
+  }
+  HS_CUDA(launch_pdl(symv_slab_kernel<B, NCW, PROG, TWO>, dim3(p->grid), dim3(Cfg::THREADS),
                      Cfg::SMEM, c->stream, a));
   HS_CUDA(cudaGetLastError());
   launch_count(c);
@@ -1902,6 +2048,32 @@ static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
   launch_count(c);
 }
 
+// Two matvecs in one pass over A (progressive mode, b <= 128): out = A s
+// (with s . out deferred into apart, as the plain CG iteration) and
+// out2 = A s2. The CG recompute iteration uses it for A s and A x.
+static void symv2_to(hs_ctx* c, const hs_matrix* m, const double* s, const double* s2,
+                     double* out, double* out2, const StepArgs& sa, const int32_t* done,
+                     double* apart) {
+  SymvPlan* p = m->plan;
+  const int64_t b = (int64_t)m->b;
+  if (!p->colmain2) {
+    HS_CUDA(cudaStreamSynchronize(c->stream));
+    const int64_t T = m->tile_hi - m->tile_lo;
+    HS_CUDA(cudaMalloc(&p->rowpart2, std::max<int64_t>(1, p->nrseg) * b * sizeof(double)));
+    HS_CUDA(cudaMalloc(&p->colmain2, std::max<int64_t>(1, T) * b * sizeof(double)));
+  }
+  ProgOut po;
+  po.out = out;
+  po.dot_s = s;
+  po.apart = apart;
+  po.defer = true;
+  po.sa = sa;
+  po.s2 = s2;
+  po.out2 = out2;
+  if (b == 64) launch_symv_fast<64, 8, true, true>(c, m, s, done, &po);
+  else launch_symv_fast<128, 8, true, true>(c, m, s, done, &po);
+}
+
 // The fused tail after a plain single-rank SYMV: cooperative launch (the
 // grid barriers need every CTA resident), programmatic serialization when
 // the driver accepts both attributes together.
@@ -2011,6 +2183,7 @@ struct CgBuffers {
   double* s_full = nullptr;  // padded full layout (vec_len)
   double* x_full = nullptr;  // padded full layout (recompute / result)
   double* t = nullptr;       // partial (vec_len) or local result (world 1)
+  double* t2 = nullptr;      // A x_old of the two-vector recompute (world 1)
   double* r_full = nullptr;  // multi-rank: all-gathered r chunks (+ slots)
   double* t_loc = nullptr;   // reduced own rows (multi-rank)
   double* r = nullptr;       // local chunk
@@ -2029,6 +2202,7 @@ static void carve_cg_buffers(hs_ctx* c, CgBuffers& B, int64_t full, int64_t chun
       {(void**)&B.s_full, full * sizeof(double)},
       {(void**)&B.x_full, full * sizeof(double)},
       {(void**)&B.t, full * sizeof(double)},
+      {(void**)&B.t2, full * sizeof(double)},
       {(void**)&B.r, chunk * sizeof(double)},
       {(void**)&B.r_full, dp ? full * sizeof(double) : 0},
       {(void**)&B.rhs, chunk * sizeof(double)},
@@ -2142,6 +2316,11 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   sa_alpha.slot_count = world;
   sa_beta.dd_slots = reinterpret_cast<Dd*>(B.r + rows_len) + rank;
 
+  static const bool recomp2_env = [] {
+    const char* e = getenv("HS_CG_RECOMP2");
+    return !(e && atoi(e) == 0);
+  }();
+  const bool two_pass_ok = recomp2_env && !dp && m->plan->prog;
   VecArgs v{};
   v.len = rows_len;  // the chunk's rows (its slot region is not vector data)
   v.x = x_loc;
@@ -2192,6 +2371,22 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
       // alpha, x, r, r^T r, beta, s)
       symv_to(c, m, B.s_full, B.t, false, nullptr, done, nullptr, false);
       launch_tail(c, m, x_loc, B.r, s_loc, sa, done);
+      goto poll;
+    }
+    // recompute iteration, single rank, progressive SYMV: A s and A x_old in
+    // one pass over A, then x += alpha s and r = rhs - (A x_old + alpha A s)
+    // (= rhs - A x_new, cg_solver.cpp:277-298) in one vector kernel
+    // (HS_CG_RECOMP2=0: two passes as below)
+    if (recompute && two_pass_ok) {
+      symv2_to(c, m, B.s_full, B.x_full, B.t, B.t2, sa, done, apart);
+      VecArgs vr = v;
+      vr.mode = V_RECOMP;
+      vr.apart = apart;
+      vr.acount = acount;
+      vr.t2 = B.t2;
+      launch_vec(c, vr);
+      v.mode = V_SDIR;
+      launch_vec(c, v);
       goto poll;
     }
     // lines 4-5: t = A s, alpha = u / s^T t (the dot fused into the finalize)

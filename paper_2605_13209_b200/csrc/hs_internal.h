@@ -72,6 +72,10 @@ struct SymvPlan {
   uint64_t launch_seq = 0;       // host-side SYMV launch count (parity)
   int64_t* pf = nullptr;         // [2 * pf_units] L2 prefetch (byte offset, bytes) per unit
   int pf_units = 0;
+  // two-vector SYMV (CG recompute iterations): the second vector's slots,
+  // allocated on first use
+  double* rowpart2 = nullptr;    // [nrseg * b]
+  double* colmain2 = nullptr;    // [T_local * b]
 };
 
 }  // namespace hs
