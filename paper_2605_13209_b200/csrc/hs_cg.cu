@@ -2053,7 +2053,7 @@ static void symv_to(hs_ctx* c, const hs_matrix* m, const double* s, double* out,
 // out2 = A s2. The CG recompute iteration uses it for A s and A x.
 static void symv2_to(hs_ctx* c, const hs_matrix* m, const double* s, const double* s2,
                      double* out, double* out2, const StepArgs& sa, const int32_t* done,
-                     double* apart) {
+                     double* apart, bool defer) {
   SymvPlan* p = m->plan;
   const int64_t b = (int64_t)m->b;
   if (!p->colmain2) {
@@ -2066,7 +2066,7 @@ static void symv2_to(hs_ctx* c, const hs_matrix* m, const double* s, const doubl
   po.out = out;
   po.dot_s = s;
   po.apart = apart;
-  po.defer = true;
+  po.defer = defer;
   po.sa = sa;
   po.s2 = s2;
   po.out2 = out2;
@@ -2183,7 +2183,8 @@ struct CgBuffers {
   double* s_full = nullptr;  // padded full layout (vec_len)
   double* x_full = nullptr;  // padded full layout (recompute / result)
   double* t = nullptr;       // partial (vec_len) or local result (world 1)
-  double* t2 = nullptr;      // A x_old of the two-vector recompute (world 1)
+  double* t2 = nullptr;      // A x_old of the two-vector recompute (partial if multi-rank)
+  double* t2_loc = nullptr;  // its reduced own rows (multi-rank)
   double* r_full = nullptr;  // multi-rank: all-gathered r chunks (+ slots)
   double* t_loc = nullptr;   // reduced own rows (multi-rank)
   double* r = nullptr;       // local chunk
@@ -2208,6 +2209,7 @@ static void carve_cg_buffers(hs_ctx* c, CgBuffers& B, int64_t full, int64_t chun
       {(void**)&B.rhs, chunk * sizeof(double)},
       {(void**)&B.slots, std::max(world, 1) * sizeof(Dd)},
       {(void**)&B.t_loc, dp ? chunk * sizeof(double) : 0},
+      {(void**)&B.t2_loc, dp ? chunk * sizeof(double) : 0},
       {(void**)&B.trace, 3 * trace_n * sizeof(double)},
   };
   auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
@@ -2278,6 +2280,9 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   // (double-buffered s); otherwise a separate vector kernel does it
   carve_cg_buffers(c, B, full, chunk, world, trace_n, dp);
   HS_CUDA(cudaMemsetAsync(B.t, 0, full * sizeof(double), c->stream));
+  // (rows a rank's SYMV never writes -- padding, rows past its last block
+  // row -- stay zero for the reduce-scatters)
+  HS_CUDA(cudaMemsetAsync(B.t2, 0, full * sizeof(double), c->stream));
   HS_CUDA(cudaMemsetAsync(B.r, 0, chunk * sizeof(double), c->stream));
   HS_CUDA(cudaMemsetAsync(B.rhs, 0, chunk * sizeof(double), c->stream));
   HS_CUDA(cudaMemsetAsync(B.x_full, 0, full * sizeof(double), c->stream));
@@ -2320,7 +2325,7 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
     const char* e = getenv("HS_CG_RECOMP2");
     return !(e && atoi(e) == 0);
   }();
-  const bool two_pass_ok = recomp2_env && !dp && m->plan->prog;
+  const bool two_pass_ok = recomp2_env && m->plan->prog;
   VecArgs v{};
   v.len = rows_len;  // the chunk's rows (its slot region is not vector data)
   v.x = x_loc;
@@ -2377,8 +2382,8 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
     // one pass over A, then x += alpha s and r = rhs - (A x_old + alpha A s)
     // (= rhs - A x_new, cg_solver.cpp:277-298) in one vector kernel
     // (HS_CG_RECOMP2=0: two passes as below)
-    if (recompute && two_pass_ok) {
-      symv2_to(c, m, B.s_full, B.x_full, B.t, B.t2, sa, done, apart);
+    if (recompute && two_pass_ok && !dp) {
+      symv2_to(c, m, B.s_full, B.x_full, B.t, B.t2, sa, done, apart, true);
       VecArgs vr = v;
       vr.mode = V_RECOMP;
       vr.apart = apart;
@@ -2388,6 +2393,25 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
       v.mode = V_SDIR;
       launch_vec(c, v);
       goto poll;
+    }
+    if (recompute && two_pass_ok && dp) {
+      // the same collectives as the two-pass recompute (one all-gather of
+      // x, two reduce-scatters), one pass over the local tiles: x_old to
+      // every rank first, then A s and A x_old together
+      comm_allgather(c, x_loc, B.x_full, (size_t)chunk, LK_SUBVECTOR);
+      symv2_to(c, m, B.s_full, B.x_full, B.t, B.t2, sa_alpha, done, apart, false);
+      comm_reduce_scatter(c, B.t, B.t_loc, (size_t)chunk, LK_SUBVECTOR);
+      combine_kernel<<<1, 1, 0, c->stream>>>(
+          reinterpret_cast<const Dd*>(B.t_loc + rows_len), 1, world, STEP_ALPHA, sa,
+          nullptr, done);
+      HS_CUDA(cudaGetLastError());
+      launch_count(c);
+      comm_reduce_scatter(c, B.t2, B.t2_loc, (size_t)chunk, LK_SUBVECTOR);
+      VecArgs vr = v;
+      vr.mode = V_RECOMP;
+      vr.t2 = B.t2_loc;
+      launch_vec(c, vr);
+      goto dp_tail;
     }
     // lines 4-5: t = A s, alpha = u / s^T t (the dot fused into the finalize)
     if (!dp) {
@@ -2424,6 +2448,7 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
       }
       launch_vec(c, vu);
     }
+  dp_tail:
     if (!dp) {
       // line 11 as its own small kernel: forming s = r + beta s inside the
       // next SYMV (one more staged segment per slab) measured 4 % slower per
