@@ -1878,14 +1878,51 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
   g.flag = flag;
 
   // P-stream work for column j: diagonal tile, then the panel below it.
+  // panel steps of column block s on their own high-priority stream (P2),
+  // each as soon as diag128(s) is done, beside the diagonal chain's later
+  // sub-blocks: step s needs W_js and L_jj[s, <s] (final once diag128(s)
+  // ran), and the diagonal chain only touches blocks right of column s
+  // (HS_CHOL_PANEL_OVERLAP=0: after the whole diagonal tile, on P)
+  static const bool panel_overlap = [] {
+    const char* e = getenv("HS_CHOL_PANEL_OVERLAP");
+    return !(e && atoi(e) == 0);
+  }();
+  cudaStream_t p2 = nullptr;
+  if (fast && panel_overlap && !c->distributed()) {
+    HS_CUDA(cudaStreamCreateWithPriority(&p2, cudaStreamNonBlocking, hi_pri));
+    HS_CUDA(cudaStreamWaitEvent(p2, start));
+  }
+  struct P2Guard {
+    cudaStream_t s;
+    ~P2Guard() {
+      if (s) cudaStreamDestroy(s);
+    }
+  } p2_guard{p2};
   auto panel_work = [&](int64_t j) {
     const int64_t t = N - 1 - j;
     if (fast) {
+      auto panel_step = [&](int cc, cudaStream_t st) {
+        GemmArgs gp = g;
+        gp.j = j;
+        gp.step = cc;
+        if (cc > 0) {
+          gp.mode = G_PANEL_UPD;
+          launch_gemm(c, st, gp, t * f, &mapA, &mapA);
+        }
+        gp.mode = G_PANEL_TRSM;
+        launch_gemm(c, st, gp, t * f, &mapA, &mapW);
+      };
       for (int s = 0; s < f; ++s) {
         diag128_kernel<<<1, 256, kDiagSmem, cs.p>>>(m->d, m->tile_lo, nullptr, b, f,
                                                     m->dinv, j * f + s, 0, flag);
         HS_CUDA(cudaGetLastError());
         launch_count(c);
+        if (p2 && t > 0) {
+          cudaEvent_t ds = cs.make();
+          HS_CUDA(cudaEventRecord(ds, cs.p));
+          HS_CUDA(cudaStreamWaitEvent(p2, ds));
+          panel_step(s, p2);
+        }
         if (s + 1 < f) {
           GemmArgs gd = g;
           gd.j = j;
@@ -1897,16 +1934,12 @@ static void potrf_run(hs_ctx* c, hs_matrix* m) {
           launch_gemm(c, cs.p, gd, tt * (tt + 1) / 2, &mapA, &mapA);
         }
       }
-      for (int cc = 0; cc < f && t > 0; ++cc) {
-        GemmArgs gp = g;
-        gp.j = j;
-        gp.step = cc;
-        if (cc > 0) {
-          gp.mode = G_PANEL_UPD;
-          launch_gemm(c, cs.p, gp, t * f, &mapA, &mapA);
-        }
-        gp.mode = G_PANEL_TRSM;
-        launch_gemm(c, cs.p, gp, t * f, &mapA, &mapW);
+      if (p2 && t > 0) {
+        cudaEvent_t pe = cs.make();
+        HS_CUDA(cudaEventRecord(pe, p2));
+        HS_CUDA(cudaStreamWaitEvent(cs.p, pe));
+      } else {
+        for (int cc = 0; cc < f && t > 0; ++cc) panel_step(cc, cs.p);
       }
       // single-column slices feed the even column's lookahead update
       if (use_oz && t > 0 && j % 2 == 0)
