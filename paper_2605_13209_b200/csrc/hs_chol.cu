@@ -276,6 +276,9 @@ enum GemmMode : int {
   // column pairs (j, j1 = j + 1), K = 2b: A_ik -= [A_ij A_ij1] [A_kj A_kj1]^T
   // for tile column k = step only (k1 == step + 1) or every k >= step
   G_UPDATE_PAIR = 12,
+  // distributed column pairs: owned (i, k) from the list, A / B rows from
+  // the broadcast panel j (tensor map A) for k < b, then panel j + 1 (map B)
+  G_DIST_UPDATE_PAIR = 13,
 };
 
 struct GemmArgs {
@@ -307,6 +310,7 @@ struct GemmItem {
   int a_r0, a_k0, b_r0, b_k0;
   // K = 2b column pairs: k-slices from k = b on come from these tiles
   int64_t a_tile2 = -1, b_tile2 = -1;
+  bool two_maps = false;  // first half of K from map A, second from map B (both operands)
   double* c;        // output sub-block (ld = b)
   int K;
   int op;           // 0 SUB, 1 SET
@@ -380,6 +384,24 @@ __device__ __forceinline__ GemmItem decode_item(const GemmArgs& g, int64_t item)
       it.b_tile = tile(k, g.j);
       it.a_tile2 = tile(i, g.j + 1);
       it.b_tile2 = tile(k, g.j + 1);
+      it.a_r0 = mb * cb;
+      it.b_r0 = nb * cb;
+      it.c = sub(tile(i, k), mb, nb);
+      return it;
+    }
+    case G_DIST_UPDATE_PAIR: {
+      const int64_t u = item / (f * f);
+      const int sb = (int)(item % (f * f));
+      const int mb = sb / f, nb = sb % f;
+      const int64_t i = g.list[2 * u], k = g.list[2 * u + 1];
+      it.lower = (i == k) && mb == nb;
+      it.skip = (i == k) && nb > mb;
+      it.K = 2 * b;
+      it.a_tile = i - g.j - 1;  // panel buffer of column j
+      it.b_tile = k - g.j - 1;
+      it.a_tile2 = i - g.j - 2; // panel buffer of column j + 1
+      it.b_tile2 = k - g.j - 2;
+      it.two_maps = true;
       it.a_r0 = mb * cb;
       it.b_r0 = nb * cb;
       it.c = sub(tile(i, k), mb, nb);
@@ -606,16 +628,21 @@ __global__ void __launch_bounds__(288, 1)
         mbar_arrive_expect_tx(&full[st], G_STAGE_BYTES);
         int ka = it.a_k0 + ks * GKS, kb = it.b_k0 + ks * GKS;
         int at = (int)it.a_tile, bt = (int)it.b_tile;
+        const CUtensorMap* ma = &mapA;
+        const CUtensorMap* mbp = &mapB;
         if (it.a_tile2 >= 0 && ks * GKS >= g.b) {  // second column of a pair
           ka -= g.b;
           kb -= g.b;
           at = (int)it.a_tile2;
           bt = (int)it.b_tile2;
+          if (it.two_maps) ma = &mapB;
+        } else if (it.two_maps) {
+          mbp = &mapA;
         }
-        tma_load_3d(sa, &mapA, ka, it.a_r0, at, &full[st]);
-        tma_load_3d(sa + A_BYTES / 2, &mapA, ka + 16, it.a_r0, at, &full[st]);
-        tma_load_3d(sb, &mapB, kb, it.b_r0, bt, &full[st]);
-        tma_load_3d(sb + B_BYTES / 2, &mapB, kb + 16, it.b_r0, bt, &full[st]);
+        tma_load_3d(sa, ma, ka, it.a_r0, at, &full[st]);
+        tma_load_3d(sa + A_BYTES / 2, ma, ka + 16, it.a_r0, at, &full[st]);
+        tma_load_3d(sb, mbp, kb, it.b_r0, bt, &full[st]);
+        tma_load_3d(sb + B_BYTES / 2, mbp, kb + 16, it.b_r0, bt, &full[st]);
       }
     }
     return;
@@ -1691,7 +1718,7 @@ static void launch_gemm(hs_ctx* c, cudaStream_t s, const GemmArgs& g,
     // exact and deterministic with them), and only with the panel and
     // update streams concurrent (one stream: exact); cause not identified:
     // it keeps 128 x 128 CTAs there (tools/gpu/chol_dist_det.py)
-    const bool big_ok = pol == 1 && g.mode != G_DIST_UPDATE;
+    const bool big_ok = pol == 1 && g.mode != G_DIST_UPDATE && g.mode != G_DIST_UPDATE_PAIR;
     const bool split = pol != 0 && (items <= sms || big_ok);
     if (split && in_place) {
       using C = GemmCfg<64, 128>;
@@ -2291,6 +2318,40 @@ static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
   }
   row_off[N] = (int64_t)rows.size();
   col_off[N] = rest_off[N] = (int64_t)pairs.size() / 2;
+  // column pairs (DMMA; HS_CHOL_PAIRS=0: one column at a time): per pair
+  // (j0, j1 = j0 + 1) the owned (i, k) of tile column j1 + 1, of j1 + 2, and
+  // of the columns beyond, updated with K = 2b from both broadcast panels
+  static const bool dist_pairs_env = [] {
+    const char* e = getenv("HS_CHOL_PAIRS");
+    return !(e && atoi(e) == 0);
+  }();
+  const bool dpairs = dist_pairs_env && c->chol_slices == 0 && N >= 4;
+  std::vector<int64_t> pp_off;  // 3 lists per pair: [4 m, 4 m + 3]
+  if (dpairs) {
+    for (int64_t j0 = 0; j0 + 1 < N; j0 += 2) {
+      const int64_t j1 = j0 + 1;
+      pp_off.push_back((int64_t)pairs.size() / 2);
+      for (int64_t i = j1 + 1; i < N; ++i)
+        if (cyclic_owner(i, j1 + 1, P, Q) == me) {
+          pairs.push_back((int32_t)i);
+          pairs.push_back((int32_t)(j1 + 1));
+        }
+      pp_off.push_back((int64_t)pairs.size() / 2);
+      for (int64_t i = j1 + 2; i < N; ++i)
+        if (cyclic_owner(i, j1 + 2, P, Q) == me) {
+          pairs.push_back((int32_t)i);
+          pairs.push_back((int32_t)(j1 + 2));
+        }
+      pp_off.push_back((int64_t)pairs.size() / 2);
+      for (int64_t i = j1 + 3; i < N; ++i)
+        for (int64_t k = j1 + 3; k <= i; ++k)
+          if (cyclic_owner(i, k, P, Q) == me) {
+            pairs.push_back((int32_t)i);
+            pairs.push_back((int32_t)k);
+          }
+      pp_off.push_back((int64_t)pairs.size() / 2);
+    }
+  }
 
   const int64_t panel = std::max<int64_t>(N - 1, 1);
   CholFlag* flag = static_cast<CholFlag*>(ctx_scratch(c));  // slot 0
@@ -2298,19 +2359,26 @@ static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
   // panel broadcast buffers and work lists from the context's persistent
   // workspace (a per-call cudaMalloc / cudaFree of the ~250 MB at n=32768
   // stalls the host for tens of ms)
-  const size_t sz[6] = {std::max<size_t>(rows.size(), 1) * sizeof(int32_t),
+  // panel buffers: 2 (by column parity), 4 with column pairs (a pair's bulk
+  // update reads both of its panels while the next pair's arrive)
+  const int npb = dpairs ? 4 : 2;
+  const size_t sz[8] = {std::max<size_t>(rows.size(), 1) * sizeof(int32_t),
                         std::max<size_t>(pairs.size(), 2) * sizeof(int32_t),
                         (size_t)bb * sizeof(double),
                         (size_t)f * cb * cb * sizeof(double),
                         (size_t)(panel * bb) * sizeof(double),
-                        (size_t)(panel * bb) * sizeof(double)};
-  void* ws[6];
-  ctx_workspace(c, 1, sz, 6, ws);
+                        (size_t)(panel * bb) * sizeof(double),
+                        dpairs ? (size_t)(panel * bb) * sizeof(double) : 0,
+                        dpairs ? (size_t)(panel * bb) * sizeof(double) : 0};
+  void* ws[8];
+  ctx_workspace(c, 1, sz, 8, ws);
   int32_t* d_rows = static_cast<int32_t*>(ws[0]);
   int32_t* d_pairs = static_cast<int32_t*>(ws[1]);
   double* Ld = static_cast<double*>(ws[2]);
   double* Wb = static_cast<double*>(ws[3]);
-  double* PB[2] = {static_cast<double*>(ws[4]), static_cast<double*>(ws[5])};
+  double* PB[4] = {static_cast<double*>(ws[4]), static_cast<double*>(ws[5]),
+                   static_cast<double*>(ws[6]), static_cast<double*>(ws[7])};
+  auto pbi = [&](int64_t j) { return (int)(j % npb); };
   if (!rows.empty())
     HS_CUDA(cudaMemcpy(d_rows, rows.data(), rows.size() * sizeof(int32_t),
                        cudaMemcpyHostToDevice));
@@ -2339,7 +2407,8 @@ static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
   if (use_oz) oz.init(b, N, c->chol_slices);
   const TileMaps mapLd = tile_map(Ld, b, 1);
   const TileMaps mapWb = tile_map(Wb, cb, f);
-  const TileMaps mapPB[2] = {tile_map(PB[0], b, panel), tile_map(PB[1], b, panel)};
+  TileMaps mapPB[4];
+  for (int q = 0; q < npb; ++q) mapPB[q] = tile_map(PB[q], b, panel);
 
   GemmArgs g{};
   g.N = N;
@@ -2405,16 +2474,72 @@ static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
       for (int64_t i = j + 1; i < N; ++i) {
         const int own = cyclic_owner(i, j, P, Q);
         const double* send = own == me ? m->d + m->lpos[tri(i, j)] * bb : nullptr;
-        comm_bcast_on(c, send, PB[j & 1] + (i - j - 1) * bb, (size_t)bb, own, cs.p,
+        comm_bcast_on(c, send, PB[pbi(j)] + (i - j - 1) * bb, (size_t)bb, own, cs.p,
                       LK_BLOCK);
       }
       comm_group(c, false);
-      if (use_oz) oz.slice_contig(c, cs.p, PB[j & 1], N, j, &flag->status);
+      if (use_oz) oz.slice_contig(c, cs.p, PB[pbi(j)], N, j, &flag->status);
     }
   };
 
   panel_work(0);
-  for (int64_t j = 0; j < N; ++j) {
+  if (dpairs) {
+    // the single-GPU pair schedule over the broadcast panels: lookahead
+    // updates on U at the panel's priority, the bulk on a low-priority U2
+    HS_CUDA(cudaStreamCreateWithPriority(&cs.u2, cudaStreamNonBlocking, lo_pri));
+    HS_CUDA(cudaStreamWaitEvent(cs.u2, start));
+    HS_CUDA(cudaStreamDestroy(cs.u));
+    HS_CUDA(cudaStreamCreateWithPriority(&cs.u, cudaStreamNonBlocking, hi_pri));
+    HS_CUDA(cudaStreamWaitEvent(cs.u, start));
+    cudaEvent_t rest_done = nullptr;
+    for (int64_t j0 = 0, pm = 0; j0 + 1 < N; j0 += 2, ++pm) {
+      const int64_t j1 = j0 + 1;
+      cudaEvent_t p0 = cs.make();
+      HS_CUDA(cudaEventRecord(p0, cs.p));
+      HS_CUDA(cudaStreamWaitEvent(cs.u, p0));
+      GemmArgs gu = g;
+      gu.j = j0;
+      gu.mode = G_DIST_UPDATE;
+      gu.X = PB[pbi(j0)];
+      gu.list = d_pairs + 2 * col_off[j0];
+      launch_gemm(c, cs.u, gu, (rest_off[j0] - col_off[j0]) * f * f, &mapPB[pbi(j0)],
+                  &mapPB[pbi(j0)]);
+      cudaEvent_t ucol = cs.make();
+      HS_CUDA(cudaEventRecord(ucol, cs.u));
+      HS_CUDA(cudaStreamWaitEvent(cs.p, ucol));
+      panel_work(j1);
+      if (j1 + 1 >= N) break;
+      cudaEvent_t p1 = cs.make();
+      HS_CUDA(cudaEventRecord(p1, cs.p));
+      HS_CUDA(cudaStreamWaitEvent(cs.u, p1));
+      if (rest_done) HS_CUDA(cudaStreamWaitEvent(cs.u, rest_done));  // previous bulk
+      GemmArgs gp = g;
+      gp.j = j0;
+      gp.mode = G_DIST_UPDATE_PAIR;
+      const int64_t* o = &pp_off[4 * pm];
+      gp.list = d_pairs + 2 * o[0];
+      launch_gemm(c, cs.u, gp, (o[1] - o[0]) * f * f, &mapPB[pbi(j0)], &mapPB[pbi(j1)]);
+      cudaEvent_t ua = cs.make();
+      HS_CUDA(cudaEventRecord(ua, cs.u));
+      rest_done = nullptr;
+      if (j1 + 2 < N) {
+        gp.list = d_pairs + 2 * o[1];
+        launch_gemm(c, cs.u, gp, (o[2] - o[1]) * f * f, &mapPB[pbi(j0)], &mapPB[pbi(j1)]);
+        cudaEvent_t ub = cs.make();
+        HS_CUDA(cudaEventRecord(ub, cs.u));
+        if (j1 + 3 < N) {
+          HS_CUDA(cudaStreamWaitEvent(cs.u2, ub));
+          gp.list = d_pairs + 2 * o[2];
+          launch_gemm(c, cs.u2, gp, (o[3] - o[2]) * f * f, &mapPB[pbi(j0)], &mapPB[pbi(j1)]);
+          rest_done = cs.make();
+          HS_CUDA(cudaEventRecord(rest_done, cs.u2));
+        }
+      }
+      HS_CUDA(cudaStreamWaitEvent(cs.p, ua));
+      panel_work(j1 + 1);
+    }
+  }
+  for (int64_t j = 0; j < N && !dpairs; ++j) {
     cudaEvent_t pdone = cs.make();
     HS_CUDA(cudaEventRecord(pdone, cs.p));
     if (j + 1 >= N) break;
@@ -2447,6 +2572,11 @@ static void potrf_run_dist(hs_ctx* c, hs_matrix* m) {
   HS_CUDA(cudaEventRecord(uend, cs.u));
   HS_CUDA(cudaStreamWaitEvent(c->stream, pend));
   HS_CUDA(cudaStreamWaitEvent(c->stream, uend));
+  if (cs.u2) {
+    cudaEvent_t u2end = cs.make();
+    HS_CUDA(cudaEventRecord(u2end, cs.u2));
+    HS_CUDA(cudaStreamWaitEvent(c->stream, u2end));
+  }
   check_finite_kernel<<<4 * 148, 256, 0, c->stream>>>(
       m->d, 0, m->d_owned, (int64_t)m->local_tiles(), b, flag);
   HS_CUDA(cudaGetLastError());
