@@ -2350,7 +2350,11 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
   // Convergence is decided on the device (done flag); the host polls a
   // pinned copy of the scalars one chunk behind, so the GPU queue never
   // drains while the host checks.
-  const uint64_t check_every = 4;
+  // poll points every 4 iterations at first (a converging solve stops at
+  // most two chunks late), then every 16 / 32: long runs keep 20-40 ms of
+  // work queued, so a host thread delayed by the OS does not drain the GPU
+  uint64_t next_poll = 4, polls = 0;
+  auto poll_gap = [](uint64_t it) -> uint64_t { return it < 64 ? 4 : it < 256 ? 16 : 32; };
   CgScalars* pin = reinterpret_cast<CgScalars*>(c->h_pinned);
   struct PollEvents {  // destroyed on every exit path, including throws
     cudaEvent_t e[2] = {nullptr, nullptr};
@@ -2474,8 +2478,9 @@ static void cg_run(hs_ctx* c, const hs_matrix* m, const double* d_rhs,
       launch_vec(c, vs);
     }
   poll:
-    if (it % check_every == 0) {
-      const int slot = (int)((it / check_every) & 1);
+    if (it == next_poll) {
+      next_poll += poll_gap(it);
+      const int slot = (int)(polls++ & 1);
       HS_CUDA(cudaMemcpyAsync(pin + slot, c->d_scalars, sizeof(CgScalars),
                               cudaMemcpyDeviceToHost, c->stream));
       HS_CUDA(cudaEventRecord(ev[slot], c->stream));
