@@ -1,12 +1,11 @@
+# CG timeline (debug build tools/libhsolve_cuda_symvtiming.so): progressive
+# SYMV vs the memory-order walk, then interleaved iteration timings
 cd $GRAFT_REPO_ROOT
-for v in "1 1" "1 0" "0 0"; do
-  set -- $v
-  echo "== HS_CG_PROG=$1 HS_CG_FUSED_UPDATE=$2"
-  HS_CG_PROG=$1 HS_CG_FUSED_UPDATE=$2 timeout 300 python tools/cg_timeline.py 32768 128 200 1 2>&1 | grep -v "per-CTA\|fused\|progressive"
+for v in 1 0; do
+  echo "== HS_CG_PROG=$v"
+  HS_CG_PROG=$v timeout 300 python tools/cg_timeline.py 32768 128 200 1 2>&1 | grep -v "per-CTA\|fused"
 done
-for v in "1 1" "1 0" "0 0" "1 1" "1 0" "0 0"; do
-  set -- $v
-  echo "== HS_CG_PROG=$1 HS_CG_FUSED_UPDATE=$2"
-  HS_CG_PROG=$1 HS_CG_FUSED_UPDATE=$2 timeout 300 python tools/cg_iter_bench.py 32768 128 400 2>/dev/null | grep -E "events|converging"
-done
-timeout 900 python -m pytest tests -m gpu -x -q -k "symv or cg or ledger or multirank or group" 2>&1 | tail -4
+for k in 1 2; do for v in 1 0; do
+  echo "== HS_CG_PROG=$v"
+  HS_CG_PROG=$v timeout 300 python tools/cg_iter_bench.py 32768 128 400 2>/dev/null | grep -E "events|converging"
+done; done
