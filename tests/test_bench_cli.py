@@ -59,3 +59,16 @@ def test_reference_arm_two_ranks_one_line_same_config():
     want = bench.workload_config(argparse.Namespace(n=1024, b=128), 2)
     assert d["config"] == want
     assert d["cpu_baseline"]["kind"] in ("reference", "port")
+
+
+def test_stdout_is_exactly_one_json_line():
+    """stdout carries the JSON line only: native writes to fd 1 (NCCL's
+    version / INIT lines) are pointed at stderr by bench.py."""
+    p = subprocess.run([sys.executable, BENCH, "--impl", "reference", "--cg-n", "1024",
+                        "--steps", "2", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=600, env=_env())
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, p.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["steps"] == 2
