@@ -734,6 +734,10 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW, PROG, TWO>::THREADS, 1)
             }
           }
         }
+        // reads of the stage complete before the TMA refill (hs_chol.cu,
+        // gemm_dmma_kernel: ptxas may put the arrive ahead of the last LDS's
+        // consumers)
+        fence_proxy_async_smem();
         __syncwarp();
         mbar_arrive_if(&empty[st], lane == 0);
         if (++st == NS) {
@@ -945,6 +949,7 @@ __global__ void __launch_bounds__(SymvCfg<B, NCW, PROG, TWO>::THREADS, 1)
         rs[r] = p0 + p1;
       }
     }
+    fence_proxy_async_smem();  // (see the release in the progressive loop)
     __syncwarp();
     mbar_arrive_if(&empty[st], lane == 0);
 

@@ -691,16 +691,24 @@ __global__ void __launch_bounds__(288, 1)
 #pragma unroll
         for (int y = 0; y < Y; ++y) dmma_8x8x4(acc[x][y], af[x], bf[y]);
     }
+    // the stage's operand reads (generic proxy) must be complete before the
+    // TMA (async proxy) refills it. ptxas places the arrive right after the
+    // last LDS, ahead of the DMMAs that consume them, so without this fence
+    // (MEMBAR.CTA + FENCE.VIEW.ASYNC.S) the refill can overwrite data a
+    // pending LDS has not read yet: wrong 64 x 64 tiles, two CTAs per SM,
+    // when other work (copies, NCCL) loads the memory system
+    // (tools/gpu/pollute_check.py; tools/sass_release_check.py checks the
+    // SASS of every kernel for the pattern)
+    fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }
 
   // epilogue: sub-block rows (wm*32 + x*8 + fr), cols (wn*8Y + y*8 + 2*fk)
   const int b = g.b;
-  // (the split tiles of small launches write C directly: with two of their
-  // CTAs resident on an SM, the bulk reduce-add epilogue below gave
-  // run-to-run differences in the factor -- cause not identified; one CTA
-  // per SM or the plain read-modify-write were exact in every run)
+  // (the split tiles write C directly. Their bulk reduce-add variant once
+  // gave run-to-run differences, before the stage-release fence above
+  // existed -- the same stale-stage race)
   if (BM == 128 && it.op == 0 && !it.lower) {
     // C -= acc through the TMA engine: stage -acc row-major in the (now free)
     // stage buffers, then one bulk reduce-add per 1-KB row. The L2 performs
@@ -1711,15 +1719,7 @@ static void launch_gemm(hs_ctx* c, cudaStream_t s, const GemmArgs& g,
     // chain runs here, beside the Ozaki GEMM: split tiles for small launches
     // only, 184 vs 187 ms at n = 32768)
     const int pol = (q64 == 1 && c->chol_slices > 0) ? 2 : q64;
-    // The distributed trailing update (panel tiles from the broadcast
-    // buffer, NCCL copies on the panel stream) gave wrong factors with
-    // 64 x 64 CTAs in launches of more than one wave -- at world 1 with a
-    // 1 x 1 grid, where its work equals the single-GPU path's (which is
-    // exact and deterministic with them), and only with the panel and
-    // update streams concurrent (one stream: exact); cause not identified:
-    // it keeps 128 x 128 CTAs there (tools/gpu/chol_dist_det.py)
-    const bool big_ok = pol == 1 && g.mode != G_DIST_UPDATE && g.mode != G_DIST_UPDATE_PAIR;
-    const bool split = pol != 0 && (items <= sms || big_ok);
+    const bool split = pol != 0 && (items <= sms || pol == 1);
     if (split && in_place) {
       using C = GemmCfg<64, 128>;
       static std::atomic<uint64_t> attr64{0};

@@ -453,6 +453,7 @@ __global__ void __launch_bounds__(288, 1)
       const double2 v = p[tid + 256 * m];
       acc += v.x + v.y;
     }
+    fence_proxy_async_smem();  // reads done before the refill
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(&empty[st]);
   }

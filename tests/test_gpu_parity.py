@@ -706,6 +706,39 @@ np.save(sys.argv[1], np.concatenate(out))
     assert np.array_equal(res[0], res[1]) and np.array_equal(res[0], res[2])
 
 
+@pytest.mark.parametrize("dist", [False, True])
+def test_factor_bitwise_stable_under_outside_copy_traffic(dist):
+    """Unrelated copies on an independent stream beside the factorization
+    (another library's work, an overlapped upload) leave the factor bitwise
+    unchanged. Without the stage-release fence in the TMA-fed kernels
+    (hs_chol.cu gemm_dmma_kernel) this reproduced wrong 64 x 64 tiles and
+    NotSpd failures in most runs at this size, single-GPU and world-1
+    distributed alike."""
+    import numpy as np
+    rt = (hs.Runtime.distributed(0, 0, 1, hs.Runtime.nccl_unique_id()) if dist
+          else hs.Runtime())
+    n, b = 16384, 512
+
+    def factor():
+        m = hs.generate_spd_device(rt, n, b, seed=42, cyclic=dist)
+        H.potrf_device(rt, m)
+        L = m.download()
+        m.free()
+        return L
+
+    ref = factor()
+    a = torch.empty(32 << 20, dtype=torch.float64, device="cuda")  # 256 MB
+    o = torch.empty_like(a)
+    side = torch.cuda.Stream()
+    for rep in range(3):
+        with torch.cuda.stream(side):
+            for _ in range(200):
+                o.copy_(a)
+        L = factor()
+        torch.cuda.synchronize()
+        assert np.array_equal(L, ref), f"rep {rep}: max diff {np.abs(L - ref).max()}"
+
+
 @pytest.mark.parametrize("n,b", [(2048, 128), (1000, 64), (4096, 128)])
 def test_cg_two_vector_recompute_matches_oracle(rt, oracle, n, b):
     """Recompute iterations on the progressive path (b <= 128) run A s and
