@@ -1233,74 +1233,13 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
                : "memory");
 }
 
-__global__ void __launch_bounds__(TRSV_DIAG_THREADS)
-    trsv_diag_kernel(const double* A, int64_t tile_lo, const int64_t* lpos, const double* W,
-                     double* v, const double* G, int world, int b, int cb, int f, int64_t i,
-                     int upper) {
-  extern __shared__ double sh[];  // vin[b] | sol[b] | staged L_ii | staged W
-  double* vin = sh;
-  double* sol = sh + b;
-  __shared__ double red[TRSV_DIAG_THREADS / 16][17];
-  const double* D = A + (lpos ? lpos[tri(i, i)] : tri(i, i) - tile_lo) * (int64_t)b * b;
+// The sub-block steps of a diagonal-tile solve (vin holds the right-hand
+// side in every CTA of the cluster; sol receives the solution in every CTA).
+__device__ __forceinline__ void trsv_diag_steps(const double* D, const double* W, double* vin,
+                                                double* sol, const double* Ds, const double* Ws,
+                                                double (*red)[17], int b, int cb, int f,
+                                                int64_t i, int upper, bool staged, int rank) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int rank = (int)cluster_rank();
-  const bool staged = trsv_staged(b, cb, f) && nw * TRSV_CLUSTER == cb;
-  // first half of the cluster barrier that guarantees every CTA of the
-  // cluster is running before any DSMEM store (the wait is below)
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-  double* Ds = sh + 2 * b;               // [sb] blocks, see below
-  double* Ws = Ds + 16 * cb * (f * (f - 1) / 2);  // [sb][cb][16] or [sb][16][cb]
-  if (staged) {
-    const double* Wi = W + i * f * (int64_t)cb * cb;
-    int64_t base = 0;
-    for (int sb = 0; sb < f; ++sb) {
-      const int o = sb * cb;
-      if (!upper) {
-        // rows rank*16 + rr of sub-block sb, columns [0, o): Ds[base + rr*o + c]
-        const int h = o / 2;  // 16-B chunks per row
-        for (int q = tid; q < 16 * h; q += blockDim.x) {
-          const int rr = q / h, cc = 2 * (q % h);
-          cp_async16(Ds + base + rr * o + cc, D + (int64_t)(o + rank * 16 + rr) * b + cc);
-        }
-        base += 16 * o;
-        for (int q = tid; q < 16 * cb / 2; q += blockDim.x) {
-          const int rr = q / (cb / 2), cc = 2 * (q % (cb / 2));
-          cp_async16(Ws + (sb * 16 + rr) * cb + cc,
-                     Wi + ((int64_t)sb * cb + rank * 16 + rr) * cb + cc);
-        }
-      } else {
-        // rows [o + cb, b), columns o + rank*16 + [0, 16): Ds[base + rr*16 + c]
-        const int nr = b - o - cb;
-        for (int q = tid; q < nr * 8; q += blockDim.x) {
-          const int rr = q >> 3, cc = 2 * (q & 7);
-          cp_async16(Ds + base + rr * 16 + cc, D + (int64_t)(o + cb + rr) * b + o + rank * 16 + cc);
-        }
-        base += 16 * nr;
-        for (int q = tid; q < cb * 8; q += blockDim.x) {
-          const int r = q >> 3, cc = 2 * (q & 7);
-          cp_async16(Ws + (sb * cb + r) * 16 + cc,
-                     Wi + ((int64_t)sb * cb + r) * cb + rank * 16 + cc);
-        }
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-  pdl_wait();
-  pdl_trigger();
-  // multi-rank: v_i plus every rank's (negated) partial update, rank order
-  for (int k = tid; k < b; k += blockDim.x) {
-    double t = v[i * b + k];
-    if (G)
-      for (int r = 0; r < world; ++r) t += G[(int64_t)r * b + k];
-    vin[k] = t;
-  }
-  if (staged) asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncthreads();
-  // every CTA arrived at kernel entry, so this returns at once. Remote
-  // stores before the first full barrier below only target sol (which the
-  // initialisation above does not write); remote vin stores happen after
-  // it, i.e. after every CTA's initialisation.
-  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   // backward: 16 columns per group, nrl row lanes
   const int cg = tid & 15, rl = tid >> 4, nrl = blockDim.x >> 4;
   for (int step = 0; step < f; ++step) {
@@ -1454,6 +1393,77 @@ __global__ void __launch_bounds__(TRSV_DIAG_THREADS)
     }
     cluster_sync_all();
   }
+}
+
+__global__ void __launch_bounds__(TRSV_DIAG_THREADS)
+    trsv_diag_kernel(const double* A, int64_t tile_lo, const int64_t* lpos, const double* W,
+                     double* v, const double* G, int world, int b, int cb, int f, int64_t i,
+                     int upper) {
+  extern __shared__ double sh[];  // vin[b] | sol[b] | staged L_ii | staged W
+  double* vin = sh;
+  double* sol = sh + b;
+  __shared__ double red[TRSV_DIAG_THREADS / 16][17];
+  const double* D = A + (lpos ? lpos[tri(i, i)] : tri(i, i) - tile_lo) * (int64_t)b * b;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int rank = (int)cluster_rank();
+  const bool staged = trsv_staged(b, cb, f) && nw * TRSV_CLUSTER == cb;
+  // first half of the cluster barrier that guarantees every CTA of the
+  // cluster is running before any DSMEM store (the wait is below)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  double* Ds = sh + 2 * b;               // [sb] blocks, see below
+  double* Ws = Ds + 16 * cb * (f * (f - 1) / 2);  // [sb][cb][16] or [sb][16][cb]
+  if (staged) {
+    const double* Wi = W + i * f * (int64_t)cb * cb;
+    int64_t base = 0;
+    for (int sb = 0; sb < f; ++sb) {
+      const int o = sb * cb;
+      if (!upper) {
+        // rows rank*16 + rr of sub-block sb, columns [0, o): Ds[base + rr*o + c]
+        const int h = o / 2;  // 16-B chunks per row
+        for (int q = tid; q < 16 * h; q += blockDim.x) {
+          const int rr = q / h, cc = 2 * (q % h);
+          cp_async16(Ds + base + rr * o + cc, D + (int64_t)(o + rank * 16 + rr) * b + cc);
+        }
+        base += 16 * o;
+        for (int q = tid; q < 16 * cb / 2; q += blockDim.x) {
+          const int rr = q / (cb / 2), cc = 2 * (q % (cb / 2));
+          cp_async16(Ws + (sb * 16 + rr) * cb + cc,
+                     Wi + ((int64_t)sb * cb + rank * 16 + rr) * cb + cc);
+        }
+      } else {
+        // rows [o + cb, b), columns o + rank*16 + [0, 16): Ds[base + rr*16 + c]
+        const int nr = b - o - cb;
+        for (int q = tid; q < nr * 8; q += blockDim.x) {
+          const int rr = q >> 3, cc = 2 * (q & 7);
+          cp_async16(Ds + base + rr * 16 + cc, D + (int64_t)(o + cb + rr) * b + o + rank * 16 + cc);
+        }
+        base += 16 * nr;
+        for (int q = tid; q < cb * 8; q += blockDim.x) {
+          const int r = q >> 3, cc = 2 * (q & 7);
+          cp_async16(Ws + (sb * cb + r) * 16 + cc,
+                     Wi + ((int64_t)sb * cb + r) * cb + rank * 16 + cc);
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  pdl_wait();
+  pdl_trigger();
+  // multi-rank: v_i plus every rank's (negated) partial update, rank order
+  for (int k = tid; k < b; k += blockDim.x) {
+    double t = v[i * b + k];
+    if (G)
+      for (int r = 0; r < world; ++r) t += G[(int64_t)r * b + k];
+    vin[k] = t;
+  }
+  if (staged) asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  // every CTA arrived at kernel entry, so this returns at once. Remote
+  // stores before the first full barrier below only target sol (which the
+  // initialisation above does not write); remote vin stores happen after
+  // it, i.e. after every CTA's initialisation.
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  trsv_diag_steps(D, W, vin, sol, Ds, Ws, red, b, cb, f, i, upper, staged, rank);
   if (rank == 0)
     for (int k = tid; k < b; k += blockDim.x) v[i * b + k] = sol[k];
 }
