@@ -706,10 +706,10 @@ __global__ void __launch_bounds__(288, 1)
 
   // epilogue: sub-block rows (wm*32 + x*8 + fr), cols (wn*8Y + y*8 + 2*fk)
   const int b = g.b;
-  // (the split tiles write C directly. Their bulk reduce-add variant once
-  // gave run-to-run differences, before the stage-release fence above
-  // existed -- the same stale-stage race)
-  if (BM == 128 && it.op == 0 && !it.lower) {
+  // (64 x 64 tiles too: 341.4 -> 340.3 ms at n = 32768, same bits -- C + (-acc)
+  // == C - acc. Before the stage-release fence above existed they used a
+  // plain read-modify-write, which made the stale-stage race rarer.)
+  if ((BM == 128 || BN == 64) && it.op == 0 && !it.lower) {
     // C -= acc through the TMA engine: stage -acc row-major in the (now free)
     // stage buffers, then one bulk reduce-add per 1-KB row. The L2 performs
     // the read-modify-write; no register-held HBM round trips. (Per-element
