@@ -706,6 +706,33 @@ np.save(sys.argv[1], np.concatenate(out))
     assert np.array_equal(res[0], res[1]) and np.array_equal(res[0], res[2])
 
 
+def test_distributed_world1_factor_bitwise_equals_single_gpu():
+    """At world 1 (1 x 1 grid) the block-cyclic factorization does the
+    single-GPU path's work in the same order -- column pairs, K = 2b bulk
+    updates over the broadcast panels, 64 x 64 CTA tiles beyond one wave --
+    so the two factors agree bit for bit (n = 16384: the early bulk
+    launches span many waves)."""
+    import numpy as np
+    n, b = 16384, 512
+    rt1 = hs.Runtime()
+    m = hs.generate_spd_device(rt1, n, b, seed=42)
+    H.potrf_device(rt1, m)
+    L1 = m.download()
+    m.free()
+    rtd = hs.Runtime.distributed(0, 0, 1, hs.Runtime.nccl_unique_id())
+    md = hs.generate_spd_device(rtd, n, b, seed=42, cyclic=True)
+    H.potrf_device(rtd, md)
+    Ld = md.download()
+    md.free()
+    N = n // b
+    for i in range(N):  # the diagonal tiles' upper halves are not part of L
+        t = i * (i + 1) // 2 + i
+        for L in (L1, Ld):
+            T = L[t * b * b:(t + 1) * b * b].reshape(b, b)
+            T[np.triu_indices(b, 1)] = 0.0
+    assert np.array_equal(L1, Ld), float(np.abs(L1 - Ld).max())
+
+
 @pytest.mark.parametrize("dist", [False, True])
 def test_factor_bitwise_stable_under_outside_copy_traffic(dist):
     """Unrelated copies on an independent stream beside the factorization
