@@ -264,6 +264,27 @@ hs_status hs_trsv_upper(hs_ctx* ctx, const hs_matrix* l, double* d_v);
 hs_status hs_solve_spd(hs_ctx* ctx, hs_matrix* a, const double* d_rhs,
                        double* d_x, const hs_matrix* a_orig,
                        hs_chol_stats* stats);
+/* Mixed-precision SPD solve with FP64 iterative refinement (the paper's
+ * future-work direction; beyond the reference API). The factor
+ * of A goes into `work` (same n, b; A stays intact). Its trailing update runs
+ * on the INT8 tensor cores with `slices` Ozaki slices (0 = FP64 DMMA).
+ * Fewer than 8 slices give a cheaper, less accurate L. Then, in FP64:
+ * x = L^-T L^-1 rhs, and per step r = rhs - A x (SYMV over the unmodified
+ * A), x += L^-T L^-1 r, until ||r|| <= tol ||rhs||, max_iters steps, or a
+ * step that does not halve ||r|| (the FP64 floor of rhs - A x: tol = 0 runs
+ * to it). Single rank. HS_ERR_NOT_SPD / HS_ERR_NUMERICAL as hs_potrf; a run
+ * that ends above tol returns HS_OK with stats->rel_residual > tol. */
+typedef struct {
+  double factor_ms;
+  double solve_ms;  /* first solve + refinement */
+  double wall_ms;
+  double rel_residual; /* ||rhs - A x|| / ||rhs|| at exit */
+  int iterations;      /* refinement steps taken */
+  int slices;
+} hs_refine_stats;
+hs_status hs_solve_spd_refine(hs_ctx* ctx, const hs_matrix* a, hs_matrix* work,
+                              const double* d_rhs, double* d_x, int slices,
+                              int max_iters, double tol, hs_refine_stats* stats);
 /* Drop-ins with HOST buffers (factorize / solve_spd / substitutions). */
 hs_status hs_factorize_host(hs_ctx* ctx, size_t n, size_t b, double* a_packed,
                             hs_chol_stats* stats);

@@ -44,7 +44,7 @@ EXPORTED = [
     "hs_matrix_download", "hs_matrix_copy", "hs_matrix_device_data",
     "hs_assemble_se", "hs_generate_spd",
     "hs_cg_solve", "hs_solve_cg_host", "hs_symv", "hs_true_residual",
-    "hs_potrf", "hs_trsv_lower", "hs_trsv_upper", "hs_solve_spd",
+    "hs_potrf", "hs_trsv_lower", "hs_trsv_upper", "hs_solve_spd", "hs_solve_spd_refine",
     "hs_factorize_host", "hs_solve_spd_host", "hs_forward_substitute_host",
     "hs_back_substitute_host", "hs_potf_tiles", "hs_gemm_update_tiles", "hs_oz_gemm_tiles",
     "hs_trsm_tiles", "hs_block_vec_op", "hs_range_op", "hs_block_exact", "hs_symv_exact",
@@ -73,6 +73,12 @@ class CholStats(C.Structure):
     _fields_ = [("factor_ms", C.c_double), ("solve_ms", C.c_double),
                 ("wall_ms", C.c_double), ("compute_ms", C.c_double),
                 ("transfer_ms", C.c_double), ("true_residual", C.c_double)]
+
+
+class RefineStats(C.Structure):
+    _fields_ = [("factor_ms", C.c_double), ("solve_ms", C.c_double),
+                ("wall_ms", C.c_double), ("rel_residual", C.c_double),
+                ("iterations", C.c_int), ("slices", C.c_int)]
 
 
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
@@ -170,6 +176,8 @@ def lib():
         "hs_trsv_lower": (C.c_int, [vp, vp, dp]),
         "hs_trsv_upper": (C.c_int, [vp, vp, dp]),
         "hs_solve_spd": (C.c_int, [vp, vp, dp, dp, vp, C.POINTER(CholStats)]),
+        "hs_solve_spd_refine": (C.c_int, [vp, vp, vp, dp, dp, C.c_int, C.c_int, C.c_double,
+                                          C.POINTER(RefineStats)]),
         "hs_factorize_host": (C.c_int, [vp, sz, sz, dp, C.POINTER(CholStats)]),
         "hs_solve_spd_host": (C.c_int, [vp, sz, sz, dp, dp, dp, C.POINTER(CholStats)]),
         "hs_forward_substitute_host": (C.c_int, [vp, sz, sz, dp, dp, dp]),

@@ -2776,6 +2776,30 @@ static void trsv_run(hs_ctx* c, hs_matrix* m, double* v, bool upper) {
   HS_CUDA(cudaStreamSynchronize(c->stream));
 }
 
+// ---- iterative refinement helpers (hs_solve_spd_refine) -------------------
+// y = a + alpha z (element-wise; y may alias a or z)
+__global__ void refine_axpy_kernel(double* y, const double* a, double alpha, const double* z,
+                                   int64_t n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    y[k] = fma(alpha, z[k], a[k]);
+}
+// *out = ||v||_2, one CTA in a fixed order (deterministic)
+__global__ void __launch_bounds__(1024) refine_norm2_kernel(const double* v, int64_t n,
+                                                            double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) s = fma(v[k], v[k], s);
+  for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (threadIdx.x == 0) *out = sqrt(s);
+  }
+}
+
 }  // namespace hs
 
 using namespace hs;
@@ -2851,6 +2875,81 @@ hs_status hs_solve_spd(hs_ctx* c, hs_matrix* a, const double* d_rhs,
     hs_status r = hs_true_residual(c, a_orig, d_x, d_rhs, &s.true_residual);
     if (r != HS_OK) throw Failure{r, hs_last_error()};
   }
+  if (st) *st = s;
+  HS_API_END
+}
+
+hs_status hs_solve_spd_refine(hs_ctx* c, const hs_matrix* a, hs_matrix* w,
+                              const double* d_rhs, double* d_x, int slices, int max_iters,
+                              double tol, hs_refine_stats* st) {
+  HS_API_BEGIN
+  HS_REQUIRE(c && a && w && d_rhs && d_x, HS_ERR_CONFIG, "null pointer");
+  HS_REQUIRE(c->world == 1 && a->layout == 0 && w->layout == 0, HS_ERR_CONFIG,
+             "hs_solve_spd_refine is single-rank");
+  HS_REQUIRE(a->n == w->n && a->b == w->b, HS_ERR_CONFIG, "work matrix shape differs from a");
+  HS_REQUIRE(slices >= 0 && slices <= 8 && max_iters >= 0 && tol >= 0.0, HS_ERR_CONFIG,
+             "slices in [0, 8], max_iters >= 0, tol >= 0");
+  require_trsv_block(a->b);
+  HS_CUDA(cudaSetDevice(c->device));
+  hs_refine_stats s{};
+  s.slices = slices;
+  const auto t0 = std::chrono::steady_clock::now();
+  hs_status r = hs_matrix_copy(w, a);
+  if (r != HS_OK) throw Failure{r, hs_last_error()};
+  {
+    const int saved = c->chol_slices;
+    c->chol_slices = slices;
+    try {
+      potrf_run(c, w);
+    } catch (...) {
+      c->chol_slices = saved;
+      throw;
+    }
+    c->chol_slices = saved;
+  }
+  s.factor_ms = ms_since(t0);
+  const auto t1 = std::chrono::steady_clock::now();
+  const int64_t pn = (int64_t)a->N * (int64_t)a->b;
+  double* res = ctx_vec(c, 3, (size_t)pn + 1);  // residual / correction, then a norm slot
+  double* nrm = res + pn;
+  auto norm2 = [&](const double* v) {
+    refine_norm2_kernel<<<1, 1024, 0, c->stream>>>(v, pn, nrm);
+    HS_CUDA(cudaGetLastError());
+    launch_count(c);
+    double h = 0.0;
+    HS_CUDA(cudaMemcpyAsync(&h, nrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    HS_CUDA(cudaStreamSynchronize(c->stream));
+    return h;
+  };
+  const unsigned vg = (unsigned)std::min<int64_t>(4 * 148, ceil_div(pn, 256));
+  HS_CUDA(cudaMemcpyAsync(d_x, d_rhs, pn * sizeof(double), cudaMemcpyDeviceToDevice,
+                          c->stream));
+  trsv_run(c, w, d_x, false);
+  trsv_run(c, w, d_x, true);
+  const double rhs_norm = norm2(d_rhs);
+  double prev = -1.0;
+  for (int it = 0;; ++it) {
+    r = hs_symv(c, a, d_x, res);  // res = A x (FP64, the unmodified matrix)
+    if (r != HS_OK) throw Failure{r, hs_last_error()};
+    refine_axpy_kernel<<<vg, 256, 0, c->stream>>>(res, d_rhs, -1.0, res, pn);  // rhs - A x
+    HS_CUDA(cudaGetLastError());
+    launch_count(c);
+    const double rn = norm2(res);
+    s.rel_residual = rhs_norm > 0.0 ? rn / rhs_norm : rn;
+    // done: below tol, out of steps, or stagnated -- the last step did not
+    // halve the residual (FP64 rounding floor of rhs - A x reached)
+    if (!(s.rel_residual > tol) || it == max_iters || (prev >= 0.0 && rn > 0.5 * prev)) break;
+    prev = rn;
+    trsv_run(c, w, res, false);
+    trsv_run(c, w, res, true);
+    refine_axpy_kernel<<<vg, 256, 0, c->stream>>>(d_x, d_x, 1.0, res, pn);  // x += d
+    HS_CUDA(cudaGetLastError());
+    launch_count(c);
+    s.iterations = it + 1;
+  }
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  s.solve_ms = ms_since(t1);
+  s.wall_ms = ms_since(t0);
   if (st) *st = s;
   HS_API_END
 }

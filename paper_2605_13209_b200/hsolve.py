@@ -30,7 +30,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from ._lib import CgParams, CgStats, CholStats
+from ._lib import CgParams, CgStats, CholStats, RefineStats
 
 # ---------------------------------------------------------------------------
 # errors (errors.hpp:10-127; names from transfer_ledger.cpp:28-42)
@@ -845,6 +845,32 @@ def solve_spd_device(rt: Runtime, a: DeviceMatrix, d_rhs: int, d_x: int,
                               a_orig.h if a_orig is not None else None, C.byref(st)))
     return SpdSolveStats(st.factor_ms, st.solve_ms, st.wall_ms, st.compute_ms, 0.0,
                          st.true_residual)
+
+
+@dataclass
+class RefineSolveStats:
+    factor_ms: float = 0.0
+    solve_ms: float = 0.0
+    wall_ms: float = 0.0
+    rel_residual: float = 0.0
+    iterations: int = 0
+    slices: int = 0
+
+
+def solve_spd_refine_device(rt: Runtime, a: DeviceMatrix, work: DeviceMatrix, d_rhs: int,
+                            d_x: int, slices: int = 5, max_iters: int = 10,
+                            tol: float = 0.0) -> RefineSolveStats:
+    """Mixed-precision SPD solve (hs_solve_spd_refine): factor a copy of A into
+    `work` with `slices` Ozaki slices on the INT8 tensor cores (0 = FP64 DMMA),
+    then FP64 iterative refinement against the unmodified A until
+    ||rhs - A x|| <= tol ||rhs||, max_iters steps, or a step that does not
+    halve the residual (tol = 0: refine to the FP64 floor). Beyond the
+    reference API (the paper's future-work direction)."""
+    st = RefineStats()
+    _check(rt._L.hs_solve_spd_refine(rt.ctx, a.h, work.h, C.c_void_p(d_rhs), C.c_void_p(d_x),
+                                     int(slices), int(max_iters), float(tol), C.byref(st)))
+    return RefineSolveStats(st.factor_ms, st.solve_ms, st.wall_ms, st.rel_residual,
+                            st.iterations, st.slices)
 
 
 # single-tile kernels (block_kernels.hpp:17-31), batched on the device

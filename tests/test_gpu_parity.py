@@ -792,3 +792,49 @@ def test_cg_two_vector_recompute_matches_oracle(rt, oracle, n, b):
     assert np.linalg.norm(x - ref["x"][:n]) <= 1e-6 * np.linalg.norm(ref["x"][:n])
     tr = np.array([[t.u, t.alpha, t.beta] for t in st.trace[:6]])
     np.testing.assert_allclose(tr, ref["trace"][:6], rtol=1e-10)
+
+
+@pytest.mark.parametrize("n,b,slices", [(4096, 512, 0), (4096, 512, 4), (4096, 512, 5),
+                                        (2048, 128, 4), (3000, 128, 6)])
+def test_mixed_precision_refined_solve_matches_oracle(oracle, n, b, slices):
+    """hs_solve_spd_refine: a factor with few INT8 Ozaki slices, refined in
+    FP64 against the unmodified A, reaches the requested residual and the
+    oracle's solution; A is left intact; the DMMA factor needs no refinement
+    step (tol above its first-solve residual)."""
+    rt = hs.Runtime()
+    a = oracle.generate_spd(n, b, seed=42)
+    rhs = oracle.generate_rhs(n, b, seed=42)
+    ref = oracle.solve_spd(n, b, a, rhs)
+    m = hs.DeviceMatrix(rt, n, b).upload(a)
+    work = hs.DeviceMatrix(rt, n, b)
+    d_rhs = dev(rhs)
+    d_x = torch.zeros_like(d_rhs)
+    # refine to the FP64 floor (tol = 0: stop when a step no longer halves
+    # the residual); the module's Cholesky tolerance ||b - Ax|| <= 1e-10 ||b||
+    # and at least the direct FP64 solve's residual
+    st = H.solve_spd_refine_device(rt, m, work, d_rhs.data_ptr(), d_x.data_ptr(),
+                                   slices=slices, max_iters=20, tol=0.0)
+    x = d_x.cpu().numpy()
+    assert st.rel_residual <= 1e-10, st
+    assert st.rel_residual <= 1.5 * ref["true_residual"] / np.linalg.norm(rhs), st
+    assert np.linalg.norm(x - ref["x"]) <= 1e-8 * np.linalg.norm(ref["x"]), st
+    assert st.iterations < 20, st  # stopped on the floor, not the cap
+    if slices == 0:
+        assert st.iterations <= 2, st  # the FP64 factor: at most a halving step or two
+    elif slices <= 5:
+        assert st.iterations >= 2, st
+    # A is unmodified: the FP64 residual through it matches the reported one
+    res = H.true_residual_device(rt, m, d_x.data_ptr(), d_rhs.data_ptr())
+    assert abs(res / np.linalg.norm(rhs) - st.rel_residual) <= 1e-3 * st.rel_residual + 1e-16
+
+
+def test_mixed_precision_refine_rejects_bad_arguments():
+    rt = hs.Runtime()
+    m = hs.DeviceMatrix(rt, 1024, 128)
+    w = hs.DeviceMatrix(rt, 1024, 256)
+    d = torch.zeros(1024, dtype=torch.float64, device="cuda")
+    with pytest.raises(hs.ConfigError):
+        H.solve_spd_refine_device(rt, m, w, d.data_ptr(), d.data_ptr(), slices=5)
+    w2 = hs.DeviceMatrix(rt, 1024, 128)
+    with pytest.raises(hs.ConfigError):
+        H.solve_spd_refine_device(rt, m, w2, d.data_ptr(), d.data_ptr(), slices=9)
