@@ -114,3 +114,12 @@ def test_no_gpu_means_loud_failure():
         pytest.skip("GPU present")
     with pytest.raises(hs.DeviceError):
         hs.Runtime()
+
+
+def test_refine_solve_rejects_null_arguments_without_a_gpu():
+    # hs_solve_spd_refine validates its arguments before touching a device
+    L = _lib.lib()
+    st = _lib.RefineStats()
+    r = L.hs_solve_spd_refine(None, None, None, None, None, 4, 10, 0.0, C.byref(st))
+    assert r == 1  # HS_ERR_CONFIG
+    assert b"null pointer" in L.hs_last_error()
