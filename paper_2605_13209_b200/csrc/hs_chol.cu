@@ -1032,6 +1032,10 @@ __global__ void __launch_bounds__(256)
       const int r = idx >> 7, c = idx & 127;
       if (c <= r) D[(int64_t)r * b + c] = S[r * DLD + c];
     }
+    // every thread has read the factor out of S before the inverse pass
+    // overwrites it (its first step copies W_33 from Wd into S; compute-
+    // sanitizer racecheck flagged the missing barrier)
+    __syncthreads();
   } else {
     for (int r = tid; r < DCB; r += blockDim.x) {
       const double d = S[r * DLD + r];
