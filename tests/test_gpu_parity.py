@@ -733,8 +733,8 @@ def test_distributed_world1_factor_bitwise_equals_single_gpu():
     assert np.array_equal(L1, Ld), float(np.abs(L1 - Ld).max())
 
 
-@pytest.mark.parametrize("dist", [False, True])
-def test_factor_bitwise_stable_under_outside_copy_traffic(dist):
+@pytest.mark.parametrize("dist,slices", [(False, 0), (True, 0), (False, 8)])
+def test_factor_bitwise_stable_under_outside_copy_traffic(dist, slices):
     """Unrelated copies on an independent stream beside the factorization
     (another library's work, an overlapped upload) leave the factor bitwise
     unchanged. Without the stage-release fence in the TMA-fed kernels
@@ -744,6 +744,7 @@ def test_factor_bitwise_stable_under_outside_copy_traffic(dist):
     import numpy as np
     rt = (hs.Runtime.distributed(0, 0, 1, hs.Runtime.nccl_unique_id()) if dist
           else hs.Runtime())
+    rt.set_cholesky_gemm(slices)  # 8: the INT8 tensor-core (Ozaki) trailing update
     n, b = 16384, 512
 
     def factor():
