@@ -272,7 +272,9 @@ hs_status hs_solve_spd(hs_ctx* ctx, hs_matrix* a, const double* d_rhs,
  * x = L^-T L^-1 rhs, and per step r = rhs - A x (SYMV over the unmodified
  * A), x += L^-T L^-1 r, until ||r|| <= tol ||rhs||, max_iters steps, or a
  * step that does not halve ||r|| (the FP64 floor of rhs - A x: tol = 0 runs
- * to it). Single rank. HS_ERR_NOT_SPD / HS_ERR_NUMERICAL as hs_potrf; a run
+ * to it). Multi-rank: block-cyclic a and work, full-length vectors on every
+ * rank (identical results on every rank, as hs_solve_spd).
+ * HS_ERR_NOT_SPD / HS_ERR_NUMERICAL as hs_potrf; a run
  * that ends above tol returns HS_OK with stats->rel_residual > tol. */
 typedef struct {
   double factor_ms;

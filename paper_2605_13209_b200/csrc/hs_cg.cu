@@ -2769,6 +2769,34 @@ hs_status hs_solve_cg_host(hs_ctx* c, size_t n, size_t b, const double* a,
 
 }  // extern "C"
 
+namespace hs {
+// y = A x, full length on every rank: the single-rank SYMV, or (world > 1,
+// block-cyclic) each rank's owned-tile partial, all-gathered and summed in
+// rank order (identical on every rank; hs_solve_spd_refine)
+void symv_full(hs_ctx* c, const hs_matrix* m, const double* x, double* y) {
+  if (c->world == 1) {
+    symv_local(c, m, x, y);
+    return;
+  }
+  HS_REQUIRE(m->layout == 1, HS_ERR_CONFIG, "multi-rank SYMV needs a block-cyclic matrix");
+  const int64_t pn = (int64_t)m->N * (int64_t)m->b;
+  const size_t sz[1] = {(size_t)pn * c->world * sizeof(double)};
+  void* ws[1];
+  ctx_workspace(c, 0, sz, 1, ws);
+  double* gath = static_cast<double*>(ws[0]);
+  const int b = (int)m->b;
+  cyclic_partial_symv_kernel<<<dim3((b + 31) / 32, (unsigned)m->N), 256, 0, c->stream>>>(
+      m->d, m->d_lpos, x, y, b, (int64_t)m->N);
+  HS_CUDA(cudaGetLastError());
+  launch_count(c);
+  c->step = -1;
+  comm_allgather(c, y, gath, (size_t)pn, LK_RESULT);
+  rank_sum_kernel<<<592, 256, 0, c->stream>>>(gath, y, pn, c->world);
+  HS_CUDA(cudaGetLastError());
+  launch_count(c);
+}
+}  // namespace hs
+
 #ifdef HS_SYMV_TIMING
 // debug builds only: per-launch SYMV (min CTA start, max CTA end) globaltimer
 // stamps; reset clears them and sets the per-CTA printf switch

@@ -2888,8 +2888,8 @@ hs_status hs_solve_spd_refine(hs_ctx* c, const hs_matrix* a, hs_matrix* w,
                               double tol, hs_refine_stats* st) {
   HS_API_BEGIN
   HS_REQUIRE(c && a && w && d_rhs && d_x, HS_ERR_CONFIG, "null pointer");
-  HS_REQUIRE(c->world == 1 && a->layout == 0 && w->layout == 0, HS_ERR_CONFIG,
-             "hs_solve_spd_refine is single-rank");
+  HS_REQUIRE(a->layout == w->layout && (c->world == 1 || a->layout == 1), HS_ERR_CONFIG,
+             "multi-rank hs_solve_spd_refine needs block-cyclic matrices");
   HS_REQUIRE(a->n == w->n && a->b == w->b, HS_ERR_CONFIG, "work matrix shape differs from a");
   HS_REQUIRE(slices >= 0 && slices <= 8 && max_iters >= 0 && tol >= 0.0, HS_ERR_CONFIG,
              "slices in [0, 8], max_iters >= 0, tol >= 0");
@@ -2933,8 +2933,7 @@ hs_status hs_solve_spd_refine(hs_ctx* c, const hs_matrix* a, hs_matrix* w,
   const double rhs_norm = norm2(d_rhs);
   double prev = -1.0;
   for (int it = 0;; ++it) {
-    r = hs_symv(c, a, d_x, res);  // res = A x (FP64, the unmodified matrix)
-    if (r != HS_OK) throw Failure{r, hs_last_error()};
+    symv_full(c, a, d_x, res);  // res = A x (FP64, the unmodified matrix; every rank)
     refine_axpy_kernel<<<vg, 256, 0, c->stream>>>(res, d_rhs, -1.0, res, pn);  // rhs - A x
     HS_CUDA(cudaGetLastError());
     launch_count(c);

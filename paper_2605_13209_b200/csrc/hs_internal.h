@@ -219,6 +219,8 @@ void free_plan(SymvPlan* p);
 // y (padded layout, full length) = A x over this rank's tiles (partials of
 // other ranks' rows included); dot_out (optional, device) gets per-row dots.
 void symv_local(hs_ctx* c, const hs_matrix* m, const double* x, double* y);
+// y = A x full-length on every rank (single rank, or block-cyclic over the group)
+void symv_full(hs_ctx* c, const hs_matrix* m, const double* x, double* y);
 void launch_fill(hs_ctx* c, double* p, double v, int64_t count);
 // Scratch matrix of the context for host-buffer calls (created on first use
 // or when the shape changes; contents are overwritten by the caller).

@@ -839,3 +839,25 @@ def test_mixed_precision_refine_rejects_bad_arguments():
     w2 = hs.DeviceMatrix(rt, 1024, 128)
     with pytest.raises(hs.ConfigError):
         H.solve_spd_refine_device(rt, m, w2, d.data_ptr(), d.data_ptr(), slices=9)
+
+
+def test_mixed_precision_refine_world1_block_cyclic(oracle):
+    """The refined solve through a world-1 NCCL communicator on a block-cyclic
+    matrix (distributed factorization path, 1 x 1 grid)."""
+    n, b = 4096, 512
+    rt = hs.Runtime.distributed(0, 0, 1, hs.Runtime.nccl_unique_id())
+    try:
+        a = oracle.generate_spd(n, b, seed=42)
+        rhs = oracle.generate_rhs(n, b, seed=42)
+        ref = oracle.solve_spd(n, b, a, rhs)
+        m = hs.DeviceMatrix(rt, n, b, cyclic=True).upload(a)
+        work = hs.DeviceMatrix(rt, n, b, cyclic=True)
+        d_rhs = dev(rhs)
+        d_x = torch.zeros_like(d_rhs)
+        st = H.solve_spd_refine_device(rt, m, work, d_rhs.data_ptr(), d_x.data_ptr(),
+                                       slices=4, max_iters=20)
+        x = d_x.cpu().numpy()
+        assert st.rel_residual <= 1e-10 and st.iterations >= 2, st
+        assert np.linalg.norm(x - ref["x"]) <= 1e-8 * np.linalg.norm(ref["x"]), st
+    finally:
+        rt.close()

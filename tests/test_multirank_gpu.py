@@ -135,6 +135,17 @@ def _work(rank, world, port, job, result_q):
             m.save_bspd1(out_path)
             dist.barrier()
             out = {"A": t.numpy()}
+        elif kind == "refine":
+            # mixed-precision solve over the block-cyclic factor: every rank
+            # passes full-length vectors and gets the same x
+            rhs = o.generate_rhs(n, b, seed=42)
+            m = hs.DeviceMatrix(rt, n, b, cyclic=True).upload(a)
+            work = hs.DeviceMatrix(rt, n, b, cyclic=True)
+            d_rhs = torch.from_numpy(rhs).cuda()
+            d_x = torch.zeros_like(d_rhs)
+            st = H.solve_spd_refine_device(rt, m, work, d_rhs.data_ptr(), d_x.data_ptr(),
+                                           slices=extra.get("slices", 4), max_iters=20)
+            out = {"x": d_x.cpu().numpy(), "rel": st.rel_residual, "steps": st.iterations}
         elif kind == "solve":
             # factor + distributed substitutions + distributed residual, then
             # substitutions on an uploaded factor (owned inverses computed)
@@ -328,3 +339,21 @@ def test_block_cyclic_substitution_singular_agreed(oracle):
     res = run_ranks(3, ("solve", n, b, {"singular_at": 5 * b + 3}))
     for r in range(3):
         assert res[r]["err"] is not None and res[r]["y"] is None
+
+
+@pytest.mark.parametrize("world,n,b,slices", [(2, 2048, 256, 4), (4, 2048, 512, 5),
+                                              (2, 1536, 128, 0)])
+def test_block_cyclic_mixed_precision_refine_multi_rank(oracle, world, n, b, slices):
+    """hs_solve_spd_refine over the 2D block-cyclic factor: distributed INT8 /
+    DMMA factorization, pipelined substitutions and the all-gathered SYMV in
+    each refinement step; every rank ends with the same x, at the FP64
+    floor of the residual."""
+    res = run_ranks(world, ("refine", n, b, {"slices": slices}))
+    a = oracle.generate_spd(n, b, seed=42)
+    rhs = oracle.generate_rhs(n, b, seed=42)
+    ref = oracle.solve_spd(n, b, a, rhs)
+    for r in range(world):
+        out = res[r]
+        assert out["rel"] <= 1e-10, (r, out["rel"])
+        assert np.linalg.norm(out["x"] - ref["x"]) <= 1e-8 * np.linalg.norm(ref["x"])
+        assert np.array_equal(out["x"], res[0]["x"]) and out["steps"] == res[0]["steps"]
