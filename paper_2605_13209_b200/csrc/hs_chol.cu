@@ -2788,6 +2788,21 @@ __global__ void refine_axpy_kernel(double* y, const double* a, double alpha, con
        k += (int64_t)gridDim.x * blockDim.x)
     y[k] = fma(alpha, z[k], a[k]);
 }
+// *out = u . v, one CTA in a fixed order (deterministic)
+__global__ void __launch_bounds__(1024) refine_dot_kernel(const double* u, const double* v,
+                                                          int64_t n, double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) s = fma(u[k], v[k], s);
+  for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (threadIdx.x == 0) *out = s;
+  }
+}
 // *out = ||v||_2, one CTA in a fixed order (deterministic)
 __global__ void __launch_bounds__(1024) refine_norm2_kernel(const double* v, int64_t n,
                                                             double* out) {
@@ -2914,8 +2929,12 @@ hs_status hs_solve_spd_refine(hs_ctx* c, const hs_matrix* a, hs_matrix* w,
   s.factor_ms = ms_since(t0);
   const auto t1 = std::chrono::steady_clock::now();
   const int64_t pn = (int64_t)a->N * (int64_t)a->b;
-  double* res = ctx_vec(c, 3, (size_t)pn + 1);  // residual / correction, then a norm slot
-  double* nrm = res + pn;
+  // residual / correction; PCG: z, p, q; then a scalar slot
+  double* res = ctx_vec(c, 3, 4 * (size_t)pn + 1);
+  double* zv = res + pn;
+  double* pv = zv + pn;
+  double* qv = pv + pn;
+  double* nrm = qv + pn;
   auto norm2 = [&](const double* v) {
     refine_norm2_kernel<<<1, 1024, 0, c->stream>>>(v, pn, nrm);
     HS_CUDA(cudaGetLastError());
@@ -2932,6 +2951,59 @@ hs_status hs_solve_spd_refine(hs_ctx* c, const hs_matrix* a, hs_matrix* w,
   trsv_run(c, w, d_x, true);
   const double rhs_norm = norm2(d_rhs);
   double prev = -1.0;
+  // HS_REFINE_PCG=1: conjugate gradients preconditioned with the factor
+  // (x0 = M^-1 rhs; each step one more SYMV for q = A p, and the true
+  // residual rhs - A x in place of the recursive one)
+  static const bool pcg = [] {
+    const char* e = getenv("HS_REFINE_PCG");
+    return e && atoi(e) != 0;
+  }();
+  auto dot = [&](const double* u, const double* v) {
+    refine_dot_kernel<<<1, 1024, 0, c->stream>>>(u, v, pn, nrm);
+    HS_CUDA(cudaGetLastError());
+    launch_count(c);
+    double h = 0.0;
+    HS_CUDA(cudaMemcpyAsync(&h, nrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    HS_CUDA(cudaStreamSynchronize(c->stream));
+    return h;
+  };
+  auto launch_axpy = [&](double* y, const double* a0, double alpha, const double* z) {
+    refine_axpy_kernel<<<vg, 256, 0, c->stream>>>(y, a0, alpha, z, pn);
+    HS_CUDA(cudaGetLastError());
+    launch_count(c);
+  };
+  if (pcg) {
+    double rz = 0.0;
+    for (int it = 0;; ++it) {
+      symv_full(c, a, d_x, res);
+      launch_axpy(res, d_rhs, -1.0, res);  // r = rhs - A x
+      const double rn = norm2(res);
+      s.rel_residual = rhs_norm > 0.0 ? rn / rhs_norm : rn;
+      if (!(s.rel_residual > tol) || it == max_iters || (prev >= 0.0 && rn > 0.5 * prev)) break;
+      prev = rn;
+      HS_CUDA(cudaMemcpyAsync(zv, res, pn * sizeof(double), cudaMemcpyDeviceToDevice,
+                              c->stream));
+      trsv_run(c, w, zv, false);
+      trsv_run(c, w, zv, true);  // z = M^-1 r
+      const double rz_new = dot(res, zv);
+      if (it == 0)
+        HS_CUDA(cudaMemcpyAsync(pv, zv, pn * sizeof(double), cudaMemcpyDeviceToDevice,
+                                c->stream));
+      else
+        launch_axpy(pv, zv, rz_new / rz, pv);  // p = z + beta p
+      rz = rz_new;
+      symv_full(c, a, pv, qv);  // q = A p
+      const double pq = dot(pv, qv);
+      if (!(pq > 0.0)) break;
+      launch_axpy(d_x, d_x, rz / pq, pv);  // x += alpha p
+      s.iterations = it + 1;
+    }
+    HS_CUDA(cudaStreamSynchronize(c->stream));
+    s.solve_ms = ms_since(t1);
+    s.wall_ms = ms_since(t0);
+    if (st) *st = s;
+    return HS_OK;
+  }
   for (int it = 0;; ++it) {
     symv_full(c, a, d_x, res);  // res = A x (FP64, the unmodified matrix; every rank)
     refine_axpy_kernel<<<vg, 256, 0, c->stream>>>(res, d_rhs, -1.0, res, pn);  // rhs - A x
